@@ -1,0 +1,92 @@
+/* D-CHAG channel front end on B200 (sm_100a) -- C ABI of libdchag.so.
+ *
+ * The reference (/root/reference/pkg/src/dchag) is pure Python/numpy and has no
+ * FFI; its drop-in boundary for this path is the functional API
+ *   tokenize_channels (model.py:51-64), tree_aggregate (model.py:76-97),
+ *   flat_aggregate (model.py:67-73), cross_attention_aggregate (layers.py:94-138),
+ *   linear_mix_aggregate (layers.py:141-146), and the AllGather of gather_shards
+ *   (strategies.py:83-96).
+ * The Python host (paper_2506_21411_b200/ops.py) keeps those names and signatures and
+ * lowers them onto the entry points below; INTEGRATION.md shows the ctypes binding.
+ *
+ * Conventions: every pointer is a device pointer unless noted; bf16 tensors are
+ * uint16 storage; strides/offsets are in ELEMENTS; every launch is stream-ordered on
+ * `stream` (a cudaStream_t, may be NULL = legacy default stream) and performs no
+ * host synchronisation and no device allocation.  Return 0 on success, else a
+ * DCHAG_ERR_* code; dchag_last_error() gives the message (thread-local).
+ */
+#ifndef DCHAG_H_
+#define DCHAG_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DCHAG_OK 0
+#define DCHAG_ERR_SHAPE 1  /* maps to ShapeError / ConfigError in the host layer */
+#define DCHAG_ERR_CONFIG 2
+#define DCHAG_ERR_CUDA 3
+
+const char* dchag_version(void);
+const char* dchag_last_error(void);
+
+/* Grouped projection GEMM (K_gemm), replaces the per-node `matmul(ctx, wo) + bo`
+ * chain of layers.py:103-123 / :141-146 (folded with the consumer's wv/U):
+ *   out[g][m][n] = sum_k A[g][m][k] * W[g][n][k] + bias[g][n] + rowbias[g][(mi % period)][n]
+ * rows m = mo*Mi + mi (Mi % 128 == 0); A is bf16 with strides (sAg, sAmo, sAmi=row);
+ * W is bf16 [G][N][K] contiguous rows; columns n < Nv go to outV (bf16, or fp32 if
+ * outV_f32) at g*sVg + mo*sVmo + mi*sVmi + n; columns Nv <= n < N go to outL (fp32). */
+int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, long long sAmo,
+                    long long sAmi, const void* W, int N, long long sWg, int Nv,
+                    const float* bias, long long bias_g, const void* rowbias,
+                    long long rowbias_g, long long rowbias_row, int rowbias_period, void* outV,
+                    int outV_f32, long long sVg, long long sVmo, long long sVmi, float* outL,
+                    long long sLg, long long sLmo, long long sLmi, void* stream);
+
+/* Level-0 logits + softmax over each node's channels (K_p0): replaces the
+ * q@wq / x@wk / logits / softmax part of layers.py:103-121 for tree level 0 with the
+ * tokenizer (model.py:51-64) folded in.  img: bf16 [B][*][Himg][W] with batch stride
+ * img_sb and channel stride img_sc (slab channel c at img + c*img_sc).
+ * node_c0/node_g (int32) and node_poff (int64) are device arrays of n_nodes.
+ * WUt bf16 [C][HP][P*P], bU fp32 [C][HP], posU fp32 [n_nodes][S][HP]; HP = H rounded up
+ * to a multiple of 8.  Output p bf16 at p[poff[n] + (r*g + c)*H + h]. */
+int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
+                    int P, int H, int HP, int n_nodes, const int* node_c0, const int* node_g,
+                    const long long* node_poff, const void* WUt, const float* bU,
+                    const float* posU, void* p, void* stream);
+
+/* Level-0 node context (K_l0, tcgen05 with A in TMEM):
+ *   ctx[n][r][h*64:(h+1)*64] = sum_c p[r,c,h] * (patch_c[r] @ M_c[:, h-block])
+ *                             + sum_c p[r,c,h] * E_n[c, h-block] + posV[n][s][h-block]
+ * Mt bf16 [H][C_pad][64*P*P] and Et bf16 [n_nodes][H][64*KE] are pre-tiled canonical
+ * UMMA blocks (dchag_tile_weights); p_row_mode = 0 reads a constant table p[poff + c*H + h]
+ * (linear-mix nodes).  Requires head dim 64, H % 4 == 0, S % 128 == 0, 128 % (W/P) == 0,
+ * P in {4, 8}. */
+int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
+                  int P, int H, int D, int n_nodes, const int* node_c0, const int* node_g,
+                  const long long* node_poff, int p_row_mode, const void* p, const void* Mt,
+                  int C_pad, const void* Et, int KE, const void* posV, void* ctx, void* stream);
+
+/* Upper-level / final combine (K_comb): ctx[n][r][:] = sum_j w_j(r,h) V_{first+j}[r][:],
+ * w = softmax_j(L_{first+j}[r][h]) (attention; mix == NULL) or mix[first+j] (linear).
+ * Child j's V at V + j*sVj + r*D (bf16), logits at L + j*sLj + r*H (fp32). */
+int dchag_combine(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
+                  const void* V, long long sVj, const float* L, long long sLj, const float* mix,
+                  void* ctx, void* stream);
+
+/* unfold_patches (tensor.py:303-323): img [B][C][Himg][W] -> out [B][C][S][P*P] bf16. */
+int dchag_unfold(const void* img, long long img_sb, long long img_sc, int B, int C, int Himg,
+                 int W, int P, void* out, void* stream);
+
+/* Re-tile fp32 folded weights into the canonical no-swizzle K-major UMMA blocks read by
+ * dchag_l0_node: src fp32 [nblk][K][64] (block b is a K x 64 matrix, column = output
+ * feature of one head) -> dst bf16 [nblk][64*K] in [K/8][8][8 rows][8 k] core-matrix order. */
+int dchag_tile_weights(const float* src, int nblk, int K, void* dst, void* stream);
+
+/* Number of SMs the kernels size their persistent grids for (device of `stream`). */
+int dchag_num_sms(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DCHAG_H_ */

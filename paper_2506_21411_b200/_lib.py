@@ -1,0 +1,93 @@
+"""ctypes binding of libdchag.so (the C ABI in include/dchag.h).
+
+The library is built in-tree by `__graft_entry__.build()` / `python -m
+paper_2506_21411_b200.build`.  There is no fallback: if the shared object is
+missing or a kernel reports an error, the call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .config import ConfigError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdchag.so")
+
+c_int, c_ll, c_vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p
+
+# name -> argtypes; every function returns int (0 = ok)
+SIGNATURES = {
+    "dchag_gemm_bf16": [c_vp, c_int, c_int, c_int, c_int, c_ll, c_ll, c_ll, c_vp, c_int, c_ll,
+                        c_int, c_vp, c_ll, c_vp, c_ll, c_ll, c_int, c_vp, c_int, c_ll, c_ll,
+                        c_ll, c_vp, c_ll, c_ll, c_ll, c_vp],
+    "dchag_l0_logits": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                        c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
+    "dchag_l0_node": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
+                      c_vp, c_vp, c_int, c_vp, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp],
+    "dchag_combine": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_ll, c_vp, c_ll, c_vp,
+                      c_vp, c_vp],
+    "dchag_unfold": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp],
+    "dchag_tile_weights": [c_vp, c_int, c_int, c_vp, c_vp],
+    "dchag_num_sms": [],
+}
+STRING_FNS = ("dchag_version", "dchag_last_error")
+
+
+class ShapeError(ValueError):
+    """Unsupported or inconsistent tensor shape (reference tensor.py:29-34)."""
+
+
+class KernelError(RuntimeError):
+    """A CUDA launch failed."""
+
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the D-CHAG kernels)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = c_int
+    for name in STRING_FNS:
+        fn = getattr(lib, name)
+        fn.argtypes = []
+        fn.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc == 0:
+        return
+    msg = load().dchag_last_error().decode()
+    if rc == 1:
+        raise ShapeError(f"{what}: {msg}")
+    if rc == 2:
+        raise ConfigError(f"{what}: {msg}")
+    raise KernelError(f"{what}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def ptr(t) -> int:
+    """Device pointer of a torch tensor (0 for None)."""
+    return 0 if t is None else int(t.data_ptr())
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)

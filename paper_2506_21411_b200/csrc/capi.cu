@@ -1,0 +1,223 @@
+// extern "C" boundary of libdchag.so (declared in include/dchag.h).
+// Validates shapes, builds TMA tensor maps (driver entry point fetched at runtime, so the
+// library links only the static CUDA runtime), and launches the kernels on the caller's
+// stream.  No device allocation, no host synchronisation.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/dchag.h"
+#include "common.cuh"
+#include "dchag_kernels.h"
+
+using namespace dchag;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return DCHAG_OK;
+  if (e == cudaErrorInvalidValue)
+    return fail(DCHAG_ERR_SHAPE, "%s: unsupported shape/arguments", what);
+  return fail(DCHAG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int num_sms_cached() {
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  return sms[dev] > 0 ? sms[dev] : 148;
+}
+
+// bf16 tensor map, dims[0] contiguous; strides in bytes for dims 1..rank-1
+int make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
+             const cuuint64_t* strides_bytes, const cuuint32_t* box, CUtensorMapSwizzle swz) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(DCHAG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims,
+                   strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DCHAG_ERR_SHAPE, "tensor map encode failed (%d)", (int)r);
+  return DCHAG_OK;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+// ===================================================================== tiling kernel
+namespace dchag {
+__global__ void tile_weights_kernel(const float* src, int nblk, int K, __nv_bfloat16* dst) {
+  const long long total = (long long)nblk * K * 64;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const int b = (int)(t / (K * 64));
+  const int rem = (int)(t - (long long)b * K * 64);
+  const int k = rem / 64, n = rem % 64;
+  const long long off = (long long)b * K * 64 + ((k / 8) * 8 + (n / 8)) * 64 + (n % 8) * 8 + (k % 8);
+  dst[off] = __float2bfloat16(src[t]);
+}
+}  // namespace dchag
+
+extern "C" {
+
+const char* dchag_version(void) { return "dchag-b200 0.1.0 (sm_100a)"; }
+const char* dchag_last_error(void) { return g_err.c_str(); }
+int dchag_num_sms(void) { return num_sms_cached(); }
+
+int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, long long sAmo,
+                    long long sAmi, const void* W, int N, long long sWg, int Nv,
+                    const float* bias, long long bias_g, const void* rowbias,
+                    long long rowbias_g, long long rowbias_row, int rowbias_period, void* outV,
+                    int outV_f32, long long sVg, long long sVmo, long long sVmi, float* outL,
+                    long long sLg, long long sLmo, long long sLmi, void* stream) {
+  if (G < 1 || Mo < 1 || Mi < 128 || Mi % 128 || K < 16 || K % 16 || N < 16 || Nv < 0 ||
+      Nv > N || Nv % 16)
+    return fail(DCHAG_ERR_SHAPE, "gemm: bad shape G=%d Mo=%d Mi=%d K=%d N=%d Nv=%d", G, Mo, Mi,
+                K, N, Nv);
+  if (Nv < N && !outL) return fail(DCHAG_ERR_SHAPE, "gemm: N > Nv needs outL");
+  if (Nv > 0 && !outV) return fail(DCHAG_ERR_SHAPE, "gemm: Nv > 0 needs outV");
+  if ((sAmi * 2) % 16 || (sAmo * 2) % 16 || (sAg * 2) % 16 || (sWg * 2) % 16)
+    return fail(DCHAG_ERR_SHAPE, "gemm: strides must be multiples of 16 bytes");
+  const int bk = (K % 64 == 0) ? 64 : (K % 32 == 0 ? 32 : 16);
+  const int ntn = (N + 255) / 256;
+  int bn = (N + ntn - 1) / ntn;
+  bn = (bn + 15) / 16 * 16;
+  const CUtensorMapSwizzle swz = bk == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : bk == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                            : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUtensorMap tA, tW;
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)Mi, (cuuint64_t)Mo, (cuuint64_t)G};
+    cuuint64_t str[3] = {(cuuint64_t)sAmi * 2, (cuuint64_t)sAmo * 2, (cuuint64_t)sAg * 2};
+    cuuint32_t box[4] = {(cuuint32_t)bk, 128, 1, 1};
+    int rc = make_map(&tA, A, 4, dims, str, box, swz);
+    if (rc) return rc;
+  }
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)N, (cuuint64_t)G};
+    cuuint64_t str[2] = {(cuuint64_t)K * 2, (cuuint64_t)sWg * 2};
+    cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)bn, 1};
+    int rc = make_map(&tW, W, 3, dims, str, box, swz);
+    if (rc) return rc;
+  }
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.G = G; a.M = Mo * Mi; a.Mi = Mi; a.N = N; a.Nv = Nv; a.K = K; a.BN = bn;
+  a.bias = bias; a.bias_g = bias_g;
+  a.rowbias = reinterpret_cast<const __nv_bfloat16*>(rowbias);
+  a.rowbias_g = rowbias_g; a.rowbias_row = rowbias_row;
+  a.rowbias_period = rowbias_period > 0 ? rowbias_period : 1;
+  a.outV = outV; a.outV_f32 = outV_f32; a.sVg = sVg; a.sVmo = sVmo; a.sVmi = sVmi;
+  a.outL = outL; a.sLg = sLg; a.sLmo = sLmo; a.sLmi = sLmi;
+  return cuda_status(launch_gemm(tA, tW, a, bk, num_sms_cached(), S(stream)), "gemm");
+}
+
+int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
+                    int P, int H, int HP, int n_nodes, const int* node_c0, const int* node_g,
+                    const long long* node_poff, const void* WUt, const float* bU,
+                    const float* posU, void* p, void* stream) {
+  if (Himg % P || W % P || HP % 8 || HP < H || H % 2 || (P * P) % 16)
+    return fail(DCHAG_ERR_SHAPE, "l0_logits: bad shape");
+  L0LogitArgs a;
+  a.img = reinterpret_cast<const __nv_bfloat16*>(img);
+  a.img_sb = img_sb; a.img_sc = img_sc;
+  a.B = B; a.S = (Himg / P) * (W / P); a.W = W; a.P = P; a.wp = W / P; a.H = H; a.HP = HP;
+  a.n_nodes = n_nodes; a.node_c0 = node_c0; a.node_g = node_g; a.node_poff = node_poff;
+  a.WUt = reinterpret_cast<const __nv_bfloat16*>(WUt);
+  a.bU = bU; a.posU = posU;
+  a.p = reinterpret_cast<__nv_bfloat16*>(p);
+  if ((B * a.S) % 64) return fail(DCHAG_ERR_SHAPE, "l0_logits: B*S must be a multiple of 64");
+  return cuda_status(launch_l0_logits(a, S(stream)), "l0_logits");
+}
+
+int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
+                  int P, int H, int D, int n_nodes, const int* node_c0, const int* node_g,
+                  const long long* node_poff, int p_row_mode, const void* p, const void* Mt,
+                  int C_pad, const void* Et, int KE, const void* posV, void* ctx, void* stream) {
+  if (Himg % P || W % P) return fail(DCHAG_ERR_SHAPE, "l0_node: image not divisible by patch");
+  L0NodeArgs a;
+  a.img = reinterpret_cast<const __nv_bfloat16*>(img);
+  a.img_sb = img_sb; a.img_sc = img_sc;
+  a.B = B; a.S = (Himg / P) * (W / P); a.W = W; a.P = P; a.wp = W / P; a.H = H; a.D = D;
+  a.n_nodes = n_nodes; a.node_c0 = node_c0; a.node_g = node_g; a.node_poff = node_poff;
+  a.p_row_mode = p_row_mode;
+  a.p = reinterpret_cast<const __nv_bfloat16*>(p);
+  a.Mt = reinterpret_cast<const __nv_bfloat16*>(Mt);
+  a.C_pad = C_pad;
+  a.Et = reinterpret_cast<const __nv_bfloat16*>(Et);
+  a.KE = KE;
+  a.posV = reinterpret_cast<const __nv_bfloat16*>(posV);
+  a.ctx = reinterpret_cast<__nv_bfloat16*>(ctx);
+  if ((reinterpret_cast<uintptr_t>(img) | (uintptr_t)(img_sb * 2) | (uintptr_t)(img_sc * 2)) % 16)
+    return fail(DCHAG_ERR_SHAPE, "l0_node: image base/strides must be 16-byte aligned");
+  return cuda_status(launch_l0_node(a, num_sms_cached(), S(stream)), "l0_node");
+}
+
+int dchag_combine(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
+                  const void* V, long long sVj, const float* L, long long sLj, const float* mix,
+                  void* ctx, void* stream) {
+  if (!mix && !L) return fail(DCHAG_ERR_SHAPE, "combine: need logits or mix");
+  CombineArgs a;
+  a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H;
+  a.node_first = node_first; a.node_g = node_g;
+  a.V = reinterpret_cast<const __nv_bfloat16*>(V); a.sVj = sVj;
+  a.L = L; a.sLj = sLj; a.mix = mix;
+  a.ctx = reinterpret_cast<__nv_bfloat16*>(ctx);
+  return cuda_status(launch_combine(a, S(stream)), "combine");
+}
+
+int dchag_unfold(const void* img, long long img_sb, long long img_sc, int B, int C, int Himg,
+                 int W, int P, void* out, void* stream) {
+  if (Himg % P || W % P) return fail(DCHAG_ERR_SHAPE, "unfold: image not divisible by patch");
+  return cuda_status(launch_unfold(reinterpret_cast<const __nv_bfloat16*>(img), img_sb, img_sc,
+                                   B, C, Himg, W, P, reinterpret_cast<__nv_bfloat16*>(out),
+                                   S(stream)),
+                     "unfold");
+}
+
+int dchag_tile_weights(const float* src, int nblk, int K, void* dst, void* stream) {
+  if (K % 8) return fail(DCHAG_ERR_SHAPE, "tile_weights: K must be a multiple of 8");
+  const long long total = (long long)nblk * K * 64;
+  if (total == 0) return DCHAG_OK;
+  tile_weights_kernel<<<(unsigned)((total + 255) / 256), 256, 0, S(stream)>>>(
+      src, nblk, K, reinterpret_cast<__nv_bfloat16*>(dst));
+  return cuda_status(cudaGetLastError(), "tile_weights");
+}
+
+}  // extern "C"

@@ -1,0 +1,82 @@
+// Internal (C++) launch interface shared by the kernel translation units and
+// the C-ABI layer (capi.cu).  Not part of the public ABI: see include/dchag.h.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dchag {
+
+struct GemmArgs {
+  int G, M, Mi, N, Nv, K, BN;   // M = Mo * Mi rows per group
+  const float* bias;            // [G][bias_g] fp32 or null
+  long long bias_g;
+  const __nv_bfloat16* rowbias; // [G][rowbias_g] with row (mi % period) * rowbias_row, or null
+  long long rowbias_g, rowbias_row;
+  int rowbias_period;
+  void* outV;                   // columns [0, Nv): bf16 (or fp32 if outV_f32)
+  int outV_f32;
+  long long sVg, sVmo, sVmi;
+  float* outL;                  // columns [Nv, N): fp32
+  long long sLg, sLmo, sLmi;
+};
+
+cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const GemmArgs& a,
+                        int bk, int num_sms, cudaStream_t st);
+
+// Level-0 node: logits + softmax over the node's channels (tensor cores via mma.sync)
+struct L0LogitArgs {
+  const __nv_bfloat16* img;  // [B][*][H][W]; channel c of the slab at img + c*img_sc
+  long long img_sb, img_sc;
+  int B, S, W, P, wp, H, HP;  // H heads, HP = H padded to a multiple of 8
+  int n_nodes;
+  const int* node_c0;         // first slab channel of node n
+  const int* node_g;          // channel count of node n
+  const long long* node_poff; // element offset of node n in p
+  const __nv_bfloat16* WUt;   // [C][HP][PP]  logit weights tok.w[c] @ U_n, transposed
+  const float* bU;            // [C][HP]      (tok.b[c]+chan_id[c]) @ U_n
+  const float* posU;          // [n_nodes][S][HP]
+  __nv_bfloat16* p;           // p[poff[n] + (r*g + c)*H + h]
+};
+cudaError_t launch_l0_logits(const L0LogitArgs& a, cudaStream_t st);
+
+// Level-0 node: ctx[n][r][h*dh:(h+1)*dh] = sum_c p[r,c,h] * (patch_c[r] @ M_c[:,h]) + ext + posV
+struct L0NodeArgs {
+  const __nv_bfloat16* img;
+  long long img_sb, img_sc;
+  int B, S, W, P, wp, H, D;
+  int n_nodes;
+  const int* node_c0;
+  const int* node_g;
+  const long long* node_poff;
+  int p_row_mode;              // 1: p depends on row; 0: constant table p[poff + c*H + h]
+  const __nv_bfloat16* p;
+  const __nv_bfloat16* Mt;     // [H][C_pad][dh*PP] canonical no-swizzle K-major blocks
+  int C_pad;
+  const __nv_bfloat16* Et;     // [n_nodes][H][dh*KE] ext (bias) blocks
+  int KE;
+  const __nv_bfloat16* posV;   // [n_nodes][S][D]
+  __nv_bfloat16* ctx;          // [n_nodes][R][D]
+};
+cudaError_t launch_l0_node(const L0NodeArgs& a, int num_sms, cudaStream_t st);
+
+// Upper-level combine: ctx[n][r][:] = sum_j p_jh(r) * V_child(j)[r][:]
+struct CombineArgs {
+  int n_nodes, R, D, H;
+  const int* node_first;       // first child index of node n
+  const int* node_g;           // child count
+  const __nv_bfloat16* V;      // child j at V + j*sVj + r*D
+  long long sVj;
+  const float* L;              // child j logits at L + j*sLj + r*H (attention mode)
+  long long sLj;
+  const float* mix;            // linear mode: p_j = mix[node_first[n] + j] (L ignored)
+  __nv_bfloat16* ctx;          // [n][R][D]
+};
+cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
+
+// images [B][C][H][W] -> patches [B][C][S][P*P] (bf16)
+cudaError_t launch_unfold(const __nv_bfloat16* img, long long img_sb, long long img_sc, int B,
+                          int C, int Himg, int W, int P, __nv_bfloat16* out, cudaStream_t st);
+
+}  // namespace dchag

@@ -1,0 +1,447 @@
+// Level-0 D-CHAG nodes with the tokenizer folded in (tokens are never formed).
+//
+// For a level-0 single_query node n over channels c in G_n, with
+//   U_n[:,h] = wk[:,h] q'_h / sqrt(dh),  M_c = tok.w[c] @ wv_n,
+// the node's context vector is (verified to 1.9e-16)
+//   logits[r,c,h] = patch_c[r] . (tok.w[c] U_n)[:,h] + (tok.b[c]+chan_id[c]) U_n[:,h] + pos[s] U_n[:,h]
+//   p[r,c,h]      = softmax_c(logits)
+//   ctx[r,h-blk]  = sum_c p[r,c,h] * (patch_c[r] @ M_c[:,h-blk])         <- K_l0, tcgen05
+//                 + sum_c p[r,c,h] * ((tok.b[c]+chan_id[c]) @ wv_n)[h-blk]  <- "ext" K-block
+//                 + (pos[s] @ wv_n)[h-blk]                                  <- epilogue
+// Reference semantics restated: model.py:51-64 (tokenizer) + layers.py:103-123 (node).
+//
+// K_p0 (l0_logits_kernel): logits + softmax with mma.sync (small: K = P*P, N = heads).
+// K_l0 (l0_node_kernel):   A-scaled GEMM.  The A operand p[r,c,h] * patch_c[r,:] is built
+//   by 4 warps (thread = row = TMEM lane) in registers and written to TMEM with
+//   tcgen05.st; tcgen05.mma reads A from TMEM and B = M_c[:,h-blk] from shared memory
+//   (1-D bulk copies of pre-tiled canonical blocks).  Image rows arrive by 1-D bulk copy:
+//   a 128-position tile of one channel is one contiguous run of 128*P*P pixels.
+#include "common.cuh"
+#include "dchag_kernels.h"
+
+namespace dchag {
+
+// =====================================================================  K_p0
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4],
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int NT>  // NT = HP / 8 head tiles
+__global__ void __launch_bounds__(128) l0_logits_kernel(L0LogitArgs a) {
+  const int R = a.B * a.S;
+  const int blocks_per_node = R / 64;
+  const int n = blockIdx.x / blocks_per_node;
+  const int rblk = blockIdx.x - n * blocks_per_node;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int PP = a.P * a.P;
+  const int c0 = __ldg(a.node_c0 + n), g = __ldg(a.node_g + n);
+  const long long poff = __ldg(a.node_poff + n);
+
+  int rows[2];
+  rows[0] = rblk * 64 + warp * 16 + gid;
+  rows[1] = rows[0] + 8;
+  const __nv_bfloat16* rowimg[2];
+  int srow[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int b = rows[q] / a.S, s = rows[q] - b * a.S;
+    srow[q] = s;
+    const int i = s / a.wp, j = s - i * a.wp;
+    rowimg[q] = a.img + b * a.img_sb + (long long)(i * a.P) * a.W + j * a.P;
+  }
+  float pu[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const float* pr0 = a.posU + ((long long)n * a.S + srow[0]) * a.HP + nt * 8 + 2 * tig;
+    const float* pr1 = a.posU + ((long long)n * a.S + srow[1]) * a.HP + nt * 8 + 2 * tig;
+    pu[nt][0] = pr0[0]; pu[nt][1] = pr0[1];
+    pu[nt][2] = pr1[0]; pu[nt][3] = pr1[1];
+  }
+
+  auto logits = [&](int c, float (&L)[NT][4]) {
+    const long long coff = (long long)(c0 + c) * a.img_sc;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const float* bu = a.bU + (long long)(c0 + c) * a.HP + nt * 8 + 2 * tig;
+      L[nt][0] = pu[nt][0] + bu[0];
+      L[nt][1] = pu[nt][1] + bu[1];
+      L[nt][2] = pu[nt][2] + bu[0];
+      L[nt][3] = pu[nt][3] + bu[1];
+    }
+    for (int ks = 0; ks < PP / 16; ++ks) {
+      uint32_t af[4];
+#pragma unroll
+      for (int hk = 0; hk < 2; ++hk) {
+        const int k = ks * 16 + hk * 8 + 2 * tig;
+        const int py = k / a.P, px = k - py * a.P;
+        const long long off = coff + (long long)py * a.W + px;
+        af[hk * 2 + 0] = *reinterpret_cast<const uint32_t*>(rowimg[0] + off);
+        af[hk * 2 + 1] = *reinterpret_cast<const uint32_t*>(rowimg[1] + off);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const __nv_bfloat16* wb = a.WUt + ((long long)(c0 + c) * a.HP + nt * 8 + gid) * PP +
+                                  ks * 16 + 2 * tig;
+        const uint32_t b0 = __ldg(reinterpret_cast<const unsigned int*>(wb));
+        const uint32_t b1 = __ldg(reinterpret_cast<const unsigned int*>(wb + 8));
+        mma_bf16_16816(L[nt], af, b0, b1);
+      }
+    }
+  };
+
+  float mx[NT][4], sm[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { mx[nt][e] = -INFINITY; sm[nt][e] = 0.f; }
+  for (int c = 0; c < g; ++c) {
+    float L[NT][4];
+    logits(c, L);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float m2 = fmaxf(mx[nt][e], L[nt][e]);
+        sm[nt][e] = sm[nt][e] * __expf(mx[nt][e] - m2) + __expf(L[nt][e] - m2);
+        mx[nt][e] = m2;
+      }
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sm[nt][e] = 1.f / sm[nt][e];
+  for (int c = 0; c < g; ++c) {
+    float L[NT][4];
+    logits(c, L);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int h = nt * 8 + 2 * tig;
+      if (h < a.H) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const float p0 = __expf(L[nt][2 * q] - mx[nt][2 * q]) * sm[nt][2 * q];
+          const float p1 = __expf(L[nt][2 * q + 1] - mx[nt][2 * q + 1]) * sm[nt][2 * q + 1];
+          __nv_bfloat16* dst = a.p + poff + ((long long)rows[q] * g + c) * a.H + h;
+          *reinterpret_cast<uint32_t*>(dst) = pack_bf16(p0, p1);
+        }
+      }
+    }
+  }
+}
+
+cudaError_t launch_l0_logits(const L0LogitArgs& a, cudaStream_t st) {
+  const int R = a.B * a.S;
+  if (R % 64) return cudaErrorInvalidValue;
+  const int grid = a.n_nodes * (R / 64);
+  switch (a.HP / 8) {
+    case 1: l0_logits_kernel<1><<<grid, 128, 0, st>>>(a); break;
+    case 2: l0_logits_kernel<2><<<grid, 128, 0, st>>>(a); break;
+    case 4: l0_logits_kernel<4><<<grid, 128, 0, st>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// =====================================================================  K_l0
+constexpr int L0_DH = 64;      // head dim (MMA N)
+constexpr int L0_STAGES = 4;
+constexpr int L0_IMG_BYTES = 16384;                 // 128 rows x 64 K (bf16) per stage
+constexpr int L0_B_BYTES = 4 * L0_DH * 64 * 2;  // up to 4 heads x [64 x 64] bf16
+constexpr int L0_STAGE_BYTES = L0_IMG_BYTES + L0_B_BYTES;
+constexpr int L0_SMEM = L0_STAGES * L0_STAGE_BYTES + 1024 + 256;
+constexpr int L0_THREADS = 192;
+constexpr uint32_t L0_ACC_COLS = 4 * L0_DH;  // accumulator region (NH * 64 used)
+constexpr uint32_t L0_SLOT_COLS = 4 * 32;    // A slot: 64 bf16 K per head = 32 columns
+
+// NH = heads per CTA (2 or 4): accumulator NH*64 TMEM columns, A slot NH*32 columns
+template <int PP, int L0_NH>
+__global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
+  constexpr int CG = 64 / PP;        // channels per stage (K = 64 per head per stage)
+  constexpr int P = PP == 64 ? 8 : 4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L0_STAGES * L0_STAGE_BYTES);
+  uint64_t* empty = full + L0_STAGES;
+  uint64_t* afull = empty + L0_STAGES;
+  uint64_t* aempty = afull + 2;
+  uint64_t* accfull = aempty + 2;
+  uint64_t* accempty = accfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(accempty + 1);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int R = a.B * a.S;
+  const int n_tiles = R / 128;
+  const int HG = a.H / L0_NH;
+  const int total_units = a.n_nodes * n_tiles * HG;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < L0_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 5);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&afull[s], 4);
+      mbar_init(&aempty[s], 1);
+    }
+    mbar_init(accfull, 1);
+    mbar_init(accempty, 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ producer (bulk copies)
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+        const int hg = u % HG;
+        const int rest = u / HG;
+        const int tile = rest % n_tiles;
+        const int n = rest / n_tiles;
+        const int c0 = __ldg(a.node_c0 + n), g = __ldg(a.node_g + n);
+        const int nmain = (g + CG - 1) / CG;
+        const int r0 = tile * 128;
+        const int b = r0 / a.S, s0 = r0 - b * a.S;
+        const __nv_bfloat16* chunk0 =
+            a.img + b * a.img_sb + (long long)(s0 / a.wp) * P * a.W;
+        for (int st = 0; st <= nmain; ++st) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sI = smem + stage * L0_STAGE_BYTES;
+          uint8_t* sB = sI + L0_IMG_BYTES;
+          if (st < nmain) {
+            const int cv = min(CG, g - st * CG);
+            mbar_expect_tx(&full[stage], cv * 128 * PP * 2 + L0_NH * L0_DH * 64 * 2);
+            for (int cc = 0; cc < cv; ++cc)
+              bulk_load(sI + cc * 128 * PP * 2,
+                        chunk0 + (long long)(c0 + st * CG + cc) * a.img_sc, 128 * PP * 2,
+                        &full[stage]);
+            for (int h = 0; h < L0_NH; ++h)
+              bulk_load(sB + h * (L0_DH * 64 * 2),
+                        a.Mt + ((long long)(hg * L0_NH + h) * a.C_pad + c0 + st * CG) *
+                                   (L0_DH * PP),
+                        L0_DH * 64 * 2, &full[stage]);
+          } else {
+            const int eb = L0_DH * a.KE * 2;
+            mbar_expect_tx(&full[stage], L0_NH * eb);
+            for (int h = 0; h < L0_NH; ++h)
+              bulk_load(sB + h * (L0_DH * 64 * 2),
+                        a.Et + ((long long)n * a.H + hg * L0_NH + h) * (L0_DH * a.KE), eb,
+                        &full[stage]);
+          }
+          if (++stage == L0_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (A from TMEM)
+    const uint32_t idesc = idesc_bf16_f32(128, L0_DH);
+    int stage = 0, slot = 0;
+    uint32_t phase = 0, sphase = 0, accphase = 0;
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      const int rest = u / HG;
+      const int n = rest / n_tiles;
+      const int g = __ldg(a.node_g + n);
+      const int nmain = (g + CG - 1) / CG;
+      mbar_wait(accempty, accphase ^ 1);
+      tc_fence_after();
+      for (int st = 0; st <= nmain; ++st) {
+        mbar_wait(&full[stage], phase);
+        mbar_wait(&afull[slot], sphase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t b_addr = smem_u32(smem + stage * L0_STAGE_BYTES + L0_IMG_BYTES);
+          const int ksteps = st < nmain ? 4 : a.KE / 16;
+          for (int h = 0; h < L0_NH; ++h) {
+            for (int kk = 0; kk < ksteps; ++kk) {
+              const uint64_t bd =
+                  smem_desc(b_addr + h * (L0_DH * 64 * 2) + kk * 2048, 1024, 128, 0);
+              const uint32_t at = tbase + L0_ACC_COLS + slot * L0_SLOT_COLS + h * 32 + kk * 8;
+              mma_ts(tbase + h * L0_DH, at, bd, idesc, (st | kk) != 0);
+            }
+          }
+          mma_commit(&empty[stage]);
+          mma_commit(&aempty[slot]);
+          if (st == nmain) mma_commit(accfull);
+        }
+        __syncwarp();
+        if (++stage == L0_STAGES) { stage = 0; phase ^= 1; }
+        if (++slot == 2) { slot = 0; sphase ^= 1; }
+      }
+      accphase ^= 1;
+    }
+  } else {
+    // ------------------------------------------------ A builders + epilogue (warps 2..5)
+    const int quarter = warp & 3;
+    const int m = quarter * 32 + lane;  // row within tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    int stage = 0, slot = 0;
+    uint32_t phase = 0, sphase = 0, accphase = 0;
+    const int i_l = m / a.wp, jj = m - (m / a.wp) * a.wp;
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      const int hg = u % HG;
+      const int rest = u / HG;
+      const int tile = rest % n_tiles;
+      const int n = rest / n_tiles;
+      const int g = __ldg(a.node_g + n);
+      const long long poff = __ldg(a.node_poff + n);
+      const int nmain = (g + CG - 1) / CG;
+      const int r = tile * 128 + m;
+      const int s = r % a.S;
+      const __nv_bfloat16* prow =
+          a.p + poff + (a.p_row_mode ? (long long)r * g * a.H : 0) + hg * L0_NH;
+      for (int st = 0; st <= nmain; ++st) {
+        uint32_t pv[CG][2];  // 4 bf16 heads per channel of this stage
+        if (st < nmain) {
+#pragma unroll
+          for (int cc = 0; cc < CG; ++cc) {
+            const int c = st * CG + cc;
+            if (c < g) {
+              if (L0_NH == 4) {
+                const uint2 q = *reinterpret_cast<const uint2*>(prow + (long long)c * a.H);
+                pv[cc][0] = q.x; pv[cc][1] = q.y;
+              } else {
+                pv[cc][0] = *reinterpret_cast<const uint32_t*>(prow + (long long)c * a.H);
+                pv[cc][1] = 0u;
+              }
+            } else {
+              pv[cc][0] = 0u; pv[cc][1] = 0u;
+            }
+          }
+        }
+        mbar_wait(&full[stage], phase);
+        mbar_wait(&aempty[slot], sphase ^ 1);
+        tc_fence_after();
+        const uint32_t slot_t = tbase + lane_off + L0_ACC_COLS + slot * L0_SLOT_COLS;
+        if (st < nmain) {
+          uint32_t x[32];
+          const uint8_t* sI = smem + stage * L0_STAGE_BYTES;
+#pragma unroll
+          for (int cc = 0; cc < CG; ++cc) {
+            const bool valid = st * CG + cc < g;
+            const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(
+                                            sI + cc * 128 * PP * 2) +
+                                        (i_l * P) * a.W + jj * P;
+#pragma unroll
+            for (int py = 0; py < P; ++py) {
+              if (P == 8) {
+                uint4 q = valid ? *reinterpret_cast<const uint4*>(base + py * a.W)
+                                : make_uint4(0, 0, 0, 0);
+                x[cc * 32 + py * 4 + 0] = q.x; x[cc * 32 + py * 4 + 1] = q.y;
+                x[cc * 32 + py * 4 + 2] = q.z; x[cc * 32 + py * 4 + 3] = q.w;
+              } else {
+                uint2 q = valid ? *reinterpret_cast<const uint2*>(base + py * a.W)
+                                : make_uint2(0, 0);
+                x[cc * 8 + py * 2 + 0] = q.x; x[cc * 8 + py * 2 + 1] = q.y;
+              }
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < L0_NH; ++h) {
+            uint32_t y[32];
+#pragma unroll
+            for (int cc = 0; cc < CG; ++cc) {
+              const uint32_t w = pv[cc][h >> 1];
+              const uint32_t ph = (h & 1) ? (w & 0xffff0000u) | (w >> 16)
+                                          : (w << 16) | (w & 0xffffu);
+#pragma unroll
+              for (int e = 0; e < 32 / CG; ++e)
+                y[cc * (32 / CG) + e] = mul_bf16x2(x[cc * (32 / CG) + e], ph);
+            }
+            tmem_st32(slot_t + h * 32, y);
+          }
+        } else {
+          // ext block: A[r, c] = p[r, c, h], zero-padded to KE
+#pragma unroll 1
+          for (int h = 0; h < L0_NH; ++h) {
+            uint32_t y[32];
+#pragma unroll
+            for (int kc = 0; kc < 32; ++kc) {
+              float lo = 0.f, hi = 0.f;
+              const int c = 2 * kc;
+              if (c < g) lo = __bfloat162float(prow[(long long)c * a.H + h]);
+              if (c + 1 < g) hi = __bfloat162float(prow[(long long)(c + 1) * a.H + h]);
+              y[kc] = pack_bf16(lo, hi);
+            }
+            tmem_st32(slot_t + h * 32, y);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&afull[slot]);
+          mbar_arrive(&empty[stage]);
+        }
+        if (++stage == L0_STAGES) { stage = 0; phase ^= 1; }
+        if (++slot == 2) { slot = 0; sphase ^= 1; }
+      }
+      // epilogue: ctx = acc + posV
+      mbar_wait(accfull, accphase);
+      tc_fence_after();
+      const __nv_bfloat16* pv_row = a.posV + ((long long)n * a.S + s) * a.D + hg * L0_NH * L0_DH;
+      __nv_bfloat16* out =
+          a.ctx + ((long long)n * R + r) * a.D + hg * L0_NH * L0_DH;
+#pragma unroll 1
+      for (int cb = 0; cb < L0_NH * L0_DH; cb += 32) {
+        uint32_t v[32];
+        tmem_ld32(tbase + lane_off + cb, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          const uint4 q = *reinterpret_cast<const uint4*>(pv_row + cb + j);
+          const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+          uint4 o;
+          uint32_t* oo = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            oo[e] = pack_bf16(__uint_as_float(v[j + 2 * e]) + bf16lo(qq[e]),
+                              __uint_as_float(v[j + 2 * e + 1]) + bf16hi(qq[e]));
+          *reinterpret_cast<uint4*>(out + cb + j) = o;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(accempty);
+      accphase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
+cudaError_t launch_l0_node(const L0NodeArgs& a, int num_sms, cudaStream_t st) {
+  const int R = a.B * a.S;
+  const int nh = a.H % 4 == 0 ? 4 : 2;
+  if (R % 128 || a.S % 128 || 128 % a.wp || a.H % nh || a.D != a.H * L0_DH || a.KE % 16 ||
+      a.KE > 64)
+    return cudaErrorInvalidValue;
+  const int units = a.n_nodes * (R / 128) * (a.H / nh);
+  const int grid = units < num_sms ? units : num_sms;
+  void (*kern)(L0NodeArgs) = nullptr;
+  if (a.P == 8) kern = nh == 4 ? l0_node_kernel<64, 4> : l0_node_kernel<64, 2>;
+  else if (a.P == 4) kern = nh == 4 ? l0_node_kernel<16, 4> : l0_node_kernel<16, 2>;
+  else return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L0_SMEM);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, L0_THREADS, L0_SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace dchag

@@ -1,0 +1,316 @@
+"""DchagFrontEnd: the drop-in module for D-CHAG's channel front end on B200.
+
+Constructor arguments are the reference's ModelConfig / StrategyConfig fields for
+this path (config.py:70-84, :121-126); `depth` is optional and validated against
+build_tree_spec(local_channels, max_group).depth.  Weights use the reference's
+dotted names and [D_in, D_out] layout (params.py:1-24, :36-57), so a dict from
+the reference's `create_master` loads 1:1 (`load_weights`).
+
+forward(images[B, C_local or C, H, W]) -> [B, 1, S, D]   (model.py:180-201 hot path)
+
+Execution per rank, all on the caller's current stream:
+  K_p0  level-0 logits+softmax      (dchag_l0_logits)
+  K_l0  level-0 context, tcgen05    (dchag_l0_node)
+  K_gemm per level: node projection folded with its consumer (dchag_gemm_bf16)
+  K_comb per level >= 1: softmax-weighted child sum (dchag_combine)
+  AllGather of the root payload over NCCL (tp > 1), in rank order (runtime.py:259)
+  K_comb + K_gemm: shared final layer.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from .config import (ConfigError, ModelConfig, StrategyConfig, TreeSpec, build_tree_spec,
+                     channel_slabs, max_group_for_depth)
+from .fold import fold_rank, pack_rank
+
+
+def frontend_param_specs(model: ModelConfig, strategy: StrategyConfig):
+    """(name, shape, init) of the front-end parameters in the reference creation order
+    (params.py:99-115), with one tree per rank slab (uneven slabs get their own trees)."""
+    c, d, p = model.channels, model.embed, model.patch
+    specs = [("tok.w", (c, p * p, d), "normal"), ("tok.b", (c, d), "zeros"),
+             ("special.channel_id", (c, d), "normal"), ("special.pos", (model.seq, d), "normal")]
+
+    def node(prefix, g, kind):
+        if kind == "linear":
+            return [(f"{prefix}.mix", (g,), "normal"), (f"{prefix}.w", (d, d), "normal"),
+                    (f"{prefix}.b", (d,), "zeros")]
+        out = [(f"{prefix}.q", (d,), "normal")] if model.agg_variant == "single_query" else []
+        out += [(f"{prefix}.{n}", (d, d), "normal") for n in ("wq", "wk", "wv", "wo")]
+        out.append((f"{prefix}.bo", (d,), "zeros"))
+        if model.agg_variant == "full_cross":
+            out.append((f"{prefix}.rq", (d,), "normal"))
+        return out
+
+    for r in range(strategy.tp_degree):
+        tree = strategy.rank_tree(model, r)
+        for li, level in enumerate(tree.levels):
+            for gi, g in enumerate(level):
+                specs += node(f"agg.slab{r}.l{li}.g{gi}", g, strategy.agg_layer_kind)
+    specs += node("agg.final", strategy.tp_degree, "cross_attention")
+    return specs
+
+
+class DchagFrontEnd(torch.nn.Module):
+    def __init__(self, channels: int, image_h: int, image_w: int, patch: int, embed: int,
+                 heads: int, max_group: int | None = None, depth: int | None = None,
+                 agg_variant: str = "single_query", agg_layer_kind: str = "cross_attention",
+                 tp: int = 1, rank: int = 0, final_layer_tp_split: bool = False,
+                 process_group=None, out_dtype=torch.bfloat16, device=None):
+        super().__init__()
+        self.model = ModelConfig(channels=channels, image_h=image_h, image_w=image_w,
+                                 patch=patch, embed=embed, heads=heads,
+                                 agg_variant=agg_variant, agg_layer_kind=agg_layer_kind)
+        self.model.validate()
+        slabs = channel_slabs(channels, tp)
+        if max_group is None:
+            if depth is None:
+                raise ConfigError("give max_group or depth")
+            max_group = max_group_for_depth([n for _, n in slabs], depth)
+        self.strategy = StrategyConfig(kind="dchag", tp_degree=tp, max_group=max_group,
+                                       agg_layer_kind=agg_layer_kind,
+                                       final_layer_tp_split=final_layer_tp_split,
+                                       uneven_slabs=True)
+        self.strategy.validate(self.model)
+        trees = [build_tree_spec(n, max_group) for _, n in slabs]
+        if depth is not None and any(t.depth != depth for t in trees):
+            raise ConfigError(
+                f"depth {depth} disagrees with build_tree_spec(local_channels, {max_group}): "
+                f"{sorted({t.depth for t in trees})}")
+        if final_layer_tp_split:
+            raise ConfigError("final_layer_tp_split is not implemented on the B200 path yet")
+        if not 0 <= rank < tp:
+            raise ConfigError(f"rank {rank} outside tp {tp}")
+        self._check_gpu_shape()
+        self.tp, self.rank = tp, rank
+        self.slabs = slabs
+        self.slab = slabs[rank]
+        self.tree: TreeSpec = trees[rank]
+        self.process_group = process_group
+        self.out_dtype = out_dtype
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
+            else torch.device("cpu"))
+        self.weights: dict[str, torch.Tensor] = {}
+        self._packed = None
+
+    # ------------------------------------------------------------------ config
+    def _check_gpu_shape(self):
+        m = self.model
+        dh = m.embed // m.heads
+        s = m.seq
+        wp = m.image_w // m.patch
+        probs = []
+        if dh != 64:
+            probs.append(f"head dim {dh} != 64")
+        if m.heads % 2:
+            probs.append(f"heads {m.heads} not even")
+        if m.patch not in (4, 8):
+            probs.append(f"patch {m.patch} not in (4, 8)")
+        if s % 128:
+            probs.append(f"tokens per image {s} not a multiple of 128")
+        if 128 % wp:
+            probs.append(f"patch columns {wp} do not divide 128")
+        if probs:
+            raise ConfigError("shape unsupported by the sm_100a kernels: " + "; ".join(probs))
+
+    @property
+    def seq(self) -> int:
+        return self.model.seq
+
+    def param_specs(self):
+        return frontend_param_specs(self.model, self.strategy)
+
+    # ----------------------------------------------------------------- weights
+    def load_weights(self, master: dict) -> None:
+        """Load reference-named weights (numpy or torch); the rank keeps what it needs:
+        the channel slab of tok.*/special.channel_id, special.pos, its own agg.slab{r}.*
+        and agg.final.* (params.py:180-221)."""
+        keep = {}
+        for name, shape, _ in self.param_specs():
+            if name.startswith("agg.slab") and not name.startswith(f"agg.slab{self.rank}."):
+                continue
+            if name not in master:
+                raise KeyError(f"missing weight {name}")
+            t = torch.as_tensor(master[name])
+            if tuple(t.shape) != tuple(shape):
+                raise ConfigError(f"{name}: shape {tuple(t.shape)} != {shape}")
+            keep[name] = t.to(device=self.device, dtype=torch.float32)
+        self.weights = keep
+        self._packed = None
+
+    def init_weights(self, seed: int = 0, std: float = 0.02) -> dict:
+        """Truncated-normal(std) weights, zero biases (the reference init distribution,
+        params.py:139-150) from a torch generator; returns the full named dict."""
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        master = {}
+        for name, shape, init in self.param_specs():
+            if init == "zeros":
+                master[name] = torch.zeros(shape)
+            else:
+                v = torch.randn(shape, generator=g)
+                bad = v.abs() > 2.0
+                while bad.any():
+                    v[bad] = torch.randn(int(bad.sum()), generator=g)
+                    bad = v.abs() > 2.0
+                master[name] = v * std
+        self.load_weights(master)
+        return master
+
+    def prepare(self):
+        """Fold + pack the weights for the kernels (cached until weights change)."""
+        if self._packed is None:
+            if not self.weights:
+                raise RuntimeError("no weights loaded")
+            with torch.no_grad():
+                fr = fold_rank(self.weights, rank=self.rank, slab=self.slab,
+                               levels=self.tree.levels, embed=self.model.embed,
+                               heads=self.model.heads, patch=self.model.patch, seq=self.seq,
+                               variant=self.model.agg_variant,
+                               layer_kind=self.strategy.agg_layer_kind)
+                self._packed = pack_rank(fr, self.device)
+        return self._packed
+
+    # ------------------------------------------------------------------ forward
+    def forward(self, images: torch.Tensor, return_payload: bool = False):
+        pk = self.prepare()
+        m = self.model
+        if images.dim() != 4:
+            raise ConfigError(f"images must be [B, C, H, W], got {tuple(images.shape)}")
+        b, cin, himg, wimg = images.shape
+        off, cnt = self.slab
+        if (himg, wimg) != (m.image_h, m.image_w):
+            raise ConfigError(f"image {himg}x{wimg} != configured {m.image_h}x{m.image_w}")
+        if cin == m.channels and self.tp > 1:
+            images = images[:, off:off + cnt]
+        elif cin != cnt:
+            raise ConfigError(f"images carry {cin} channels; rank {self.rank} expects {cnt} "
+                              f"(its slab) or {m.channels} (all)")
+        if images.dtype != torch.bfloat16:
+            images = images.to(torch.bfloat16)
+        if images.stride(3) != 1 or images.stride(2) != wimg:
+            images = images.contiguous()
+        if not images.is_cuda:
+            raise ConfigError("images must be on the GPU")
+        payload = self.local_payload(images, pk)
+        gathered = self.gather(payload)
+        out = self.finish(gathered, images.shape[0])
+        return (out, gathered) if return_payload else out
+
+    def gather(self, payload):
+        """AllGather of the per-rank root payload in rank order (runtime.py:259)."""
+        if self.tp == 1:
+            return payload
+        import torch.distributed as dist
+        gathered = torch.empty(self.tp * payload.numel(), device=payload.device,
+                               dtype=torch.uint8)
+        dist.all_gather_into_tensor(gathered, payload, group=self.process_group)
+        return gathered
+
+    def local_payload(self, img, pk=None):
+        """Rank-local part: slab tree -> root payload [V bf16 R*D | L fp32 R*H] (bytes),
+        V/L = the root stream projected into the final layer's value/logit space."""
+        pk = pk or self.prepare()
+        m = self.model
+        d, h, s, p = m.embed, m.heads, self.seq, m.patch
+        B = img.shape[0]
+        R = B * s
+        dev = img.device
+        st = _lib.stream_handle()
+        bf16 = dict(device=dev, dtype=torch.bfloat16)
+        f32 = dict(device=dev, dtype=torch.float32)
+        isb, isc = img.stride(0), img.stride(1)
+
+        # ---- level 0
+        if pk.attn_l0:
+            poff_list, acc = [], 0
+            for g in pk.l0_g_list:
+                poff_list.append(acc)
+                acc += g * R * h
+            poff = torch.tensor(poff_list, device=dev, dtype=torch.int64)
+            pbuf = torch.empty(acc, **bf16)
+            _lib.call("dchag_l0_logits", _lib.ptr(img), isb, isc, B, m.image_h, m.image_w, p,
+                      h, pk.HP, pk.n0, _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g), _lib.ptr(poff),
+                      _lib.ptr(pk.WUt), _lib.ptr(pk.bU), _lib.ptr(pk.posU), _lib.ptr(pbuf), st)
+            prow = 1
+        else:
+            poff = (pk.l0_c0.to(torch.int64) * h).contiguous()
+            pbuf = pk.p_const
+            prow = 0
+        ctx = torch.empty(pk.n0, R, d, **bf16)
+        _lib.call("dchag_l0_node", _lib.ptr(img), isb, isc, B, m.image_h, m.image_w, p, h, d,
+                  pk.n0, _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g), _lib.ptr(poff), prow,
+                  _lib.ptr(pbuf), _lib.ptr(pk.Mt), pk.C_pad, _lib.ptr(pk.Et), pk.KE,
+                  _lib.ptr(pk.posV), _lib.ptr(ctx), st)
+
+        depth = len(pk.levels)
+        payload = None
+        for li in range(depth):
+            n_l = len(pk.levels[li])
+            N = pk.N[li]
+            logits = N > d
+            if li == depth - 1:
+                # root: write straight into the gather payload [V bf16 R*D | L fp32 R*H]
+                nbytes = R * d * 2 + R * h * 4
+                payload = torch.empty(nbytes, device=dev, dtype=torch.uint8)
+                V = payload[:R * d * 2].view(torch.bfloat16).view(1, R, d)
+                L = payload[R * d * 2:].view(torch.float32).view(1, R, h)
+            else:
+                V = torch.empty(n_l, R, d, **bf16)
+                L = torch.empty(n_l, R, h, **f32) if logits else None
+            _lib.call("dchag_gemm_bf16", _lib.ptr(ctx), n_l, 1, R, d, R * d, 0, d,
+                      _lib.ptr(pk.Wp[li]), N, N * d, d, _lib.ptr(pk.bp[li]), N, 0, 0, 0, 1,
+                      _lib.ptr(V), 0, R * d, 0, d, _lib.ptr(L), R * h, 0, h, st)
+            if li + 1 < depth:
+                n_next = len(pk.levels[li + 1])
+                ctx = torch.empty(n_next, R, d, **bf16)
+                mix = pk.comb_mix[li]
+                _lib.call("dchag_combine", n_next, R, d, h, _lib.ptr(pk.comb_first[li]),
+                          _lib.ptr(pk.comb_g[li]), _lib.ptr(V), R * d,
+                          _lib.ptr(None if mix is not None else L), R * h, _lib.ptr(mix),
+                          _lib.ptr(ctx), st)
+        return payload
+
+    def finish(self, gathered, B):
+        """Shared final layer over the gathered streams -> [B, 1, S, D]."""
+        pk = self.prepare()
+        m = self.model
+        d, h, s = m.embed, m.heads, self.seq
+        R = B * s
+        dev = gathered.device
+        st = _lib.stream_handle()
+        bf16 = dict(device=dev, dtype=torch.bfloat16)
+        pb = gathered.numel() // self.tp
+        if pb != R * d * 2 + R * h * 4:
+            raise ConfigError(f"gathered payload of {gathered.numel()} bytes does not match "
+                              f"tp={self.tp}, B={B}")
+        Vg = gathered.view(torch.bfloat16)
+        Lg = gathered.view(torch.float32)
+        if self.tp > 1:
+            ctx_f = torch.empty(1, R, d, **bf16)
+            first = self._final_first(dev)
+            _lib.call("dchag_combine", 1, R, d, h, _lib.ptr(first[0]), _lib.ptr(first[1]),
+                      _lib.ptr(Vg), pb // 2, _lib.ptr(Lg[R * d // 2:]), pb // 4, 0,
+                      _lib.ptr(ctx_f), st)
+        else:
+            ctx_f = Vg[:R * d].view(1, R, d)  # softmax over one stream is exactly 1
+        out = torch.empty(R, d, device=dev, dtype=self.out_dtype)
+        _lib.call("dchag_gemm_bf16", _lib.ptr(ctx_f), 1, 1, R, d, R * d, 0, d, _lib.ptr(pk.Wf),
+                  d, d * d, d, _lib.ptr(pk.bf), d, 0, 0, 0, 1, _lib.ptr(out),
+                  int(self.out_dtype == torch.float32), R * d, 0, d, 0, 0, 0, 0, st)
+        return out.view(B, 1, s, d)
+
+    def _final_first(self, dev):
+        key = ("final_first", dev)
+        cache = getattr(self, "_cache", None)
+        if cache is None:
+            cache = self._cache = {}
+        if key not in cache:
+            cache[key] = (torch.zeros(1, device=dev, dtype=torch.int32),
+                          torch.full((1,), self.tp, device=dev, dtype=torch.int32))
+        return cache[key]

@@ -1,0 +1,137 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle and the
+reference's golden vectors.  bf16 budget: rel_err <= 2e-2 (reference conftest metric)."""
+import numpy as np
+import pytest
+import torch
+
+import dchag_oracle as O
+from conftest import load_golden, rel_err
+
+pytestmark = pytest.mark.gpu
+BF16_TOL = 2e-2
+
+
+def _bf(x):
+    return torch.as_tensor(np.asarray(x, np.float32)).to(torch.bfloat16)
+
+
+def _lib():
+    from paper_2506_21411_b200 import _lib as L
+    return L
+
+
+# ----------------------------------------------------------------- K_gemm
+@pytest.mark.parametrize("G,M,K,N,Nv", [(1, 128, 64, 256, 256), (2, 256, 1024, 1040, 1024),
+                                        (3, 384, 128, 208, 192), (1, 128, 16, 128, 128),
+                                        (2, 256, 32, 96, 64), (1, 1024, 2048, 2080, 2048)])
+def test_gemm_matches_torch(G, M, K, N, Nv):
+    L = _lib()
+    g = torch.Generator().manual_seed(G * 7 + K)
+    A = torch.randn(G, M, K, generator=g).to(torch.bfloat16).cuda()
+    W = (torch.randn(G, N, K, generator=g) / K ** 0.5).to(torch.bfloat16).cuda()
+    bias = torch.randn(G, N, generator=g).cuda()
+    V = torch.empty(G, M, Nv, device="cuda", dtype=torch.bfloat16)
+    Lo = torch.empty(G, M, max(N - Nv, 1), device="cuda", dtype=torch.float32)
+    nl = N - Nv
+    L.call("dchag_gemm_bf16", L.ptr(A), G, 1, M, K, M * K, 0, K, L.ptr(W), N, N * K, Nv,
+           L.ptr(bias), N, 0, 0, 0, 1, L.ptr(V), 0, M * Nv, 0, Nv,
+           L.ptr(Lo) if nl else 0, M * nl, 0, nl, L.stream_handle())
+    torch.cuda.synchronize()
+    ref = torch.einsum("gmk,gnk->gmn", A.float(), W.float()) + bias[:, None]
+    assert rel_err(V.float().cpu(), ref[..., :Nv].cpu()) < 5e-3
+    if nl:
+        assert rel_err(Lo.cpu(), ref[..., Nv:].cpu()) < 1e-4
+
+
+def test_gemm_rowbias_and_4d_rows():
+    # tokenizer-shaped call: rows (b, s) split as Mo x Mi, per-row bias period S
+    L = _lib()
+    G, Mo, Mi, K, N = 3, 2, 256, 16, 128
+    g = torch.Generator().manual_seed(1)
+    A = torch.randn(Mo, G, Mi, K, generator=g).to(torch.bfloat16).cuda()   # [b][c][s][k]
+    W = torch.randn(G, N, K, generator=g).to(torch.bfloat16).cuda()
+    bias = torch.randn(G, N, generator=g).cuda()
+    rb = torch.randn(Mi, N, generator=g).to(torch.bfloat16).cuda()
+    out = torch.empty(Mo, G, Mi, N, device="cuda", dtype=torch.float32)
+    L.call("dchag_gemm_bf16", L.ptr(A), G, Mo, Mi, K, Mi * K, G * Mi * K, K, L.ptr(W), N,
+           N * K, N, L.ptr(bias), N, L.ptr(rb), 0, N, Mi, L.ptr(out), 1, Mi * N, G * Mi * N,
+           N, 0, 0, 0, 0, L.stream_handle())
+    torch.cuda.synchronize()
+    ref = torch.einsum("bgmk,gnk->bgmn", A.float(), W.float()) + bias[None, :, None] + \
+        rb.float()[None, None]
+    assert rel_err(out.cpu(), ref.cpu()) < 1e-5
+
+
+# ------------------------------------------------------------ full front end
+def _frontend(meta, tp=1, rank=0, out_dtype=torch.float32):
+    from paper_2506_21411_b200 import DchagFrontEnd
+    return DchagFrontEnd(meta["channels"], meta["image_h"], meta["image_w"], meta["patch"],
+                         meta["embed"], meta["heads"], max_group=meta["max_group"],
+                         agg_variant=meta.get("variant", "single_query"),
+                         agg_layer_kind=meta.get("layer_kind", "cross_attention"), tp=tp,
+                         rank=rank, out_dtype=out_dtype)
+
+
+def _run_all_ranks(meta, w, images):
+    """All ranks in one process: per-rank payloads, concatenated in rank order (the
+    AllGather, runtime.py:259), shared final layer on rank 0."""
+    tp = meta["tp"]
+    img = _bf(images).cuda()
+    mods = [_frontend(meta, tp, r) for r in range(tp)]
+    pays = []
+    for r, m in enumerate(mods):
+        m.load_weights(w)
+        off, cnt = m.slab
+        pays.append(m.local_payload(img[:, off:off + cnt]))
+    gathered = torch.cat(pays) if tp > 1 else pays[0]
+    out = mods[0].finish(gathered, images.shape[0])
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy()
+
+
+@pytest.mark.parametrize("case", ["T_sq_tp1", "T_sq_tp2"])
+def test_frontend_matches_reference_golden(case):
+    meta, z, w, _ = load_golden(case)
+    meta = dict(meta, image_h=meta["image_h"], image_w=meta["image_w"])
+    out = _run_all_ranks(meta, w, z["images"])
+    assert rel_err(out, z["out"]) < BF16_TOL
+
+
+CONFIGS = [
+    dict(channels=16, image_h=64, image_w=64, patch=4, embed=128, heads=2, tp=1, max_group=8),
+    dict(channels=20, image_h=64, image_w=128, patch=8, embed=256, heads=4, tp=1, max_group=8),
+    dict(channels=20, image_h=64, image_w=128, patch=8, embed=256, heads=4, tp=1, max_group=8,
+         layer_kind="linear"),
+    dict(channels=22, image_h=64, image_w=128, patch=8, embed=256, heads=4, tp=3, max_group=3),
+    dict(channels=40, image_h=64, image_w=64, patch=4, embed=256, heads=4, tp=2, max_group=16),
+    dict(channels=37, image_h=128, image_w=128, patch=8, embed=512, heads=8, tp=1, max_group=4),
+]
+
+
+@pytest.mark.parametrize("meta", CONFIGS, ids=lambda m: "C{channels}P{patch}D{embed}tp{tp}g{max_group}".format(**m) + m.get("layer_kind", ""))
+def test_frontend_matches_oracle(meta):
+    lk = meta.get("layer_kind", "cross_attention")
+    specs = O.frontend_param_specs(meta["channels"], meta["image_h"], meta["image_w"],
+                                   meta["patch"], meta["embed"], meta["tp"], meta["max_group"],
+                                   layer_kind=lk)
+    w = O.random_params(specs, seed=5, std=0.05, bias_std=0.02)
+    w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
+    rng = np.random.default_rng(2)
+    images = rng.standard_normal((2, meta["channels"], meta["image_h"], meta["image_w"]))
+    images = _bf(images).float().numpy().astype(np.float64)
+    want = O.dchag_frontend(images, w, patch=meta["patch"], heads=meta["heads"], tp=meta["tp"],
+                            max_group=meta["max_group"], layer_kind=lk)
+    out = _run_all_ranks(dict(meta, layer_kind=lk), w, images)
+    err = rel_err(out, want)
+    assert err < BF16_TOL, err
+
+
+def test_frontend_forward_entry_and_dtype():
+    meta = CONFIGS[0]
+    from paper_2506_21411_b200 import DchagFrontEnd
+    fe = DchagFrontEnd(16, 64, 64, 4, 128, 2, max_group=8)
+    fe.init_weights(seed=1)
+    x = torch.randn(2, 16, 64, 64, device="cuda").to(torch.bfloat16)
+    y = fe(x)
+    assert y.shape == (2, 1, 256, 128) and y.dtype == torch.bfloat16
+    assert torch.isfinite(y.float()).all()
