@@ -78,8 +78,27 @@ def check(rc: int, what: str) -> None:
     raise KernelError(f"{what}: {msg}")
 
 
+# kernel-launch accounting (bench.py reports `gpu_launches`; an optional hook lets the
+# bench bracket individual kernels with CUDA events on the launching stream)
+LAUNCH_COUNT = {"n": 0}
+_HOOK = {"fn": None}
+_NON_LAUNCH = ("dchag_num_sms",)
+
+
+def set_launch_hook(fn) -> None:
+    """fn(name, phase) with phase in {"pre", "post"} around every kernel launch."""
+    _HOOK["fn"] = fn
+
+
 def call(name: str, *args) -> None:
+    hook = _HOOK["fn"]
+    if hook is not None:
+        hook(name, "pre")
     check(getattr(load(), name)(*args), name)
+    if name not in _NON_LAUNCH:
+        LAUNCH_COUNT["n"] += 1
+    if hook is not None:
+        hook(name, "post")
 
 
 def ptr(t) -> int:

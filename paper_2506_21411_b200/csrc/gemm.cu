@@ -159,10 +159,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
         if (bias) {
+          if (n0 + 16 <= args.N && (args.bias_g & 3) == 0) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            const float4 b4 = *reinterpret_cast<const float4*>(bias + n0 + j);
-            v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+            for (int j = 0; j < 16; j += 4) {
+              const float4 b4 = *reinterpret_cast<const float4*>(bias + n0 + j);
+              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (n0 + j < args.N) v[j] += __ldg(bias + n0 + j);
           }
         }
         if (rb) {
@@ -199,9 +205,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         } else {
           float* o = args.outL + (size_t)g * args.sLg + (size_t)mo * args.sLmo +
                      (size_t)mi * args.sLmi + (n0 - args.Nv);
+          if (n0 + 16 <= args.N && (args.sLmi & 3) == 0 && (args.sLg & 3) == 0 &&
+              (args.sLmo & 3) == 0 && ((n0 - args.Nv) & 3) == 0) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            for (int j = 0; j < 16; j += 4)
+              *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (n0 + j < args.N) o[j] = v[j];
+          }
         }
       }
       tc_fence_before();

@@ -23,7 +23,8 @@ def _lib():
 # ----------------------------------------------------------------- K_gemm
 @pytest.mark.parametrize("G,M,K,N,Nv", [(1, 128, 64, 256, 256), (2, 256, 1024, 1040, 1024),
                                         (3, 384, 128, 208, 192), (1, 128, 16, 128, 128),
-                                        (2, 256, 32, 96, 64), (1, 1024, 2048, 2080, 2048)])
+                                        (2, 256, 32, 96, 64), (1, 1024, 2048, 2080, 2048),
+                                        (3, 256, 128, 130, 128)])
 def test_gemm_matches_torch(G, M, K, N, Nv):
     L = _lib()
     g = torch.Generator().manual_seed(G * 7 + K)
