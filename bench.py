@@ -1,0 +1,391 @@
+"""D-CHAG tokenize+aggregate throughput on B200 (one JSON line on rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload hyperspectral|weather|tiny]
+  python bench.py --impl reference ...      # the reference CPU path on the host cores
+
+A step is one forward of the channel front end (per-channel tokenizer + hierarchical
+cross-channel aggregation + partial-aggregate AllGather + final layer) over one batch
+of synthetic images of the named shape.  With N GPUs the channels are sharded over N
+ranks exactly as D-CHAG's distributed tokenization does (tp = N architecture, balanced
+slabs for 500 / 8); the batch is global, so the scaling is strong.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # SURVEY.md section 8(d) canonical instantiations (heads at dh = 64, max_group derived)
+    "hyperspectral": dict(channels=500, image_h=128, image_w=128, patch=8, embed=1024,
+                          heads=16, depth=3, batch=32),
+    "weather": dict(channels=128, image_h=128, image_w=256, patch=4, embed=1024, heads=16,
+                    depth=2, batch=16),
+    "tiny": dict(channels=16, image_h=64, image_w=64, patch=4, embed=128, heads=2, depth=2,
+                 batch=2),
+}
+METRIC = "D-CHAG tokenize+aggregate images/sec"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="hyperspectral", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=None,
+                    help="tokens per CPU sample (default: 1/8 of an image)")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p["bf16_tflops_sustained"], p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- CPU reference leg
+
+
+def cpu_sample(wl, tp, max_group, tokens, seed=0):
+    """Time the reference algorithm (oracle/dchag_oracle.py: float64 numpy restatement of
+    model.py:180-201, all BLAS threads) on one image restricted to the first `tokens`
+    positions (whole patch rows).  Every position is independent on this path, so
+    images/s = (tokens / S) / seconds."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import dchag_oracle as O
+    p = wl["patch"]
+    wp = wl["image_w"] // p
+    rows = max(1, tokens // wp)
+    tokens = rows * wp
+    specs = O.frontend_param_specs(wl["channels"], rows * p, wl["image_w"], p, wl["embed"], tp,
+                                   max_group)
+    w = O.random_params(specs, seed=seed)
+    img = np.random.default_rng(seed).standard_normal((1, wl["channels"], rows * p,
+                                                         wl["image_w"]))
+    t0 = time.perf_counter()
+    O.dchag_frontend(img, w, patch=p, heads=wl["heads"], tp=tp, max_group=max_group)
+    dt = time.perf_counter() - t0
+    S = (wl["image_h"] // p) * wp
+    return tokens / S / dt, tokens, dt
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max((i.get("num_threads", 1) for i in info), default=1), \
+            ",".join(sorted({f"{i.get('internal_api')} {i.get('version')}" for i in info}))
+    except Exception:
+        return os.cpu_count(), "unknown"
+
+
+def reference_arm(args, wl, tp, max_group):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    S = (wl["image_h"] // wl["patch"]) * (wl["image_w"] // wl["patch"])
+    tokens = args.cpu_tokens or max(S // 8, wl["image_w"] // wl["patch"])
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, tok, dt = cpu_sample(wl, tp, max_group, tokens, seed=i)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    threads, blas = blas_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * (tok / S) / value, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, wl, tp, max_group),
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "port",
+                         "sample": f"1 image x {tok}/{S} tokens per step (float64 numpy "
+                                   f"restatement of the reference, {blas})"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, wl, tp, max_group):
+    return {"workload": args.workload, "channels": wl["channels"],
+            "image": [wl["image_h"], wl["image_w"]], "patch": wl["patch"],
+            "embed": wl["embed"], "heads": wl["heads"], "depth": wl["depth"],
+            "max_group": max_group, "tp": tp, "global_batch": args.batch or wl["batch"],
+            "parallelism": f"dchag-tp{tp}",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# ----------------------------------------------------------------- B200 arm
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"dchag_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(", ") for r in open(self.path).read().strip().splitlines()]
+        except Exception:
+            return None
+        rows = [r for r in rows if len(r) >= 7]
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows]
+        load = [float(r[0]) for r in rows if float(r[2]) > 300] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def b200_arm(args, wl, tp, max_group):
+    import torch
+    import torch.distributed as dist
+    from paper_2506_21411_b200 import DchagFrontEnd, _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B = args.batch or wl["batch"]
+    fe = DchagFrontEnd(wl["channels"], wl["image_h"], wl["image_w"], wl["patch"], wl["embed"],
+                       wl["heads"], max_group=max_group, tp=tp, rank=rank)
+    fe.init_weights(seed=0, all_ranks=False)
+    fe.prepare()
+    off, cnt = fe.slab
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    images = torch.randn(B, cnt, wl["image_h"], wl["image_w"], device="cuda",
+                         generator=gen).to(torch.bfloat16)
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(step_fn, k, per_step_hook=None):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(k)]
+        barrier()
+        for i in range(k):
+            flush.zero_()
+            if per_step_hook:
+                per_step_hook(i)
+            ev[i][0].record()
+            step_fn()
+            ev[i][1].record()
+        barrier()
+        return sum(a.elapsed_time(b) for a, b in ev)
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    step = lambda: fe(images)  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    # ---- pass A: headline (inputs resident in HBM)
+    n0 = _lib.LAUNCH_COUNT["n"]
+    with ClockSampler(local) as clk:
+        ms = timed(step, args.steps)
+    launches = _lib.LAUNCH_COUNT["n"] - n0
+    ms = max_over_ranks(ms)
+    value = B * args.steps / (ms / 1e3)
+
+    # ---- pass B: per-kernel CUDA events on the launching stream
+    plan = fe.launch_plan(B)
+    site_ms = {s: 0.0 for _, s, _, _ in plan}
+    events = []
+    idx = {"i": 0}
+
+    def hook(name, phase):
+        if phase == "pre":
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            events.append([plan[idx["i"]][1], e, None])
+        else:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            events[-1][2] = e
+            idx["i"] += 1
+
+    def reset(_):
+        idx["i"] = 0
+
+    _lib.set_launch_hook(hook)
+    try:
+        timed(step, args.steps, per_step_hook=reset)
+    finally:
+        _lib.set_launch_hook(None)
+    for site, a, b in events:
+        site_ms[site] += a.elapsed_time(b) / args.steps
+    kernels = []
+    peak_burst, peak_sus, hbm, peak_src = load_peaks()
+    for name, site, flops, nbytes in plan:
+        t = site_ms[site] / 1e3
+        kernels.append({"site": site, "kernel": name, "ms": site_ms[site],
+                        "tflops": flops / t / 1e12 if t else None,
+                        "gbs": nbytes / t / 1e9 if t else None})
+    dom = max(kernels, key=lambda k: k["ms"])
+    dom_plan = next(p for p in plan if p[1] == dom["site"])
+    tensor_bound = dom["kernel"] in ("dchag_l0_node", "dchag_gemm_bf16", "dchag_l0_logits")
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(f"{args.workload}:tp{tp}:{dom['site']}")
+    except Exception:
+        pass
+    if tensor_bound:
+        roof = {"bound": "tensor", "achieved": dom["tflops"], "peak": peak_sus,
+                "unit": "TFLOP/s", "frac": dom["tflops"] / peak_sus, "traffic": traffic,
+                "kernel": f"{dom['kernel']}[{dom['site']}]",
+                "flops_per_launch": dom_plan[2], "launch_ms": dom["ms"],
+                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside the step)"}
+    else:
+        roof = {"bound": "hbm", "achieved": dom["gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": dom["gbs"] / hbm, "traffic": traffic,
+                "kernel": f"{dom['kernel']}[{dom['site']}]", "bytes_per_launch": dom_plan[3],
+                "launch_ms": dom["ms"], "peak_source": f"{peak_src} hbm_gbs"}
+
+    # ---- pass C: end to end through the public API from pinned host memory
+    host_img = images.cpu().pin_memory()
+    out_host = torch.empty(B, 1, fe.seq, wl["embed"], dtype=fe.out_dtype).pin_memory()
+    dev_img = torch.empty_like(images)
+
+    def e2e_step():
+        dev_img.copy_(host_img, non_blocking=True)
+        y = fe(dev_img)
+        if rank == 0:
+            out_host.copy_(y, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    e2e_ms = max_over_ranks(timed(e2e_step, args.steps))
+    h2d = images.numel() * 2
+    d2h = out_host.numel() * 2 if rank == 0 else 0
+
+    # ---- whole-job algorithmic work
+    exec_flops = sum(p[2] for p in plan)  # this rank's folded-plan flops per step
+    if world > 1:
+        t = torch.tensor([float(exec_flops - [p for p in plan if p[1] == "gemm_final"][0][2])],
+                         device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        tot_exec = float(t.item()) + [p for p in plan if p[1] == "gemm_final"][0][2]
+    else:
+        tot_exec = exec_flops
+    b_flops = bflops_per_image(wl, fe.slabs, max_group) * B
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        S = fe.seq
+        tokens = args.cpu_tokens or max(S // 2, wl["image_w"] // wl["patch"])
+        v, tok, dt = cpu_sample(wl, tp, max_group, tokens)
+        threads, blas = blas_threads()
+        cpu = {"value": v, "unit": "images/s", "cores": threads, "kind": "port",
+               "sample": f"1 image x {tok}/{S} tokens, {dt:.1f} s (float64 numpy restatement "
+                         f"of the reference hot path, {blas})"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (N(0,1) bf16 images, truncated-normal(0.02) "
+                                     "random-init weights)",
+            "config": workload_config(args, wl, tp, max_group),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": B * args.steps / (e2e_ms / 1e3), "unit": "images/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "work": {"folded_plan_tflop_per_step": tot_exec / 1e12,
+                     "folded_plan_tflops": tot_exec / (ms / args.steps / 1e3) / 1e12,
+                     "reference_graph_B_tflop_per_step": b_flops / 1e12,
+                     "B_flops_effective_tflops": b_flops / (ms / args.steps / 1e3) / 1e12,
+                     "B_flops_roofline_frac": b_flops / (ms / args.steps / 1e3) / 1e12
+                     / (world * peak_sus)},
+            "kernels": kernels,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def bflops_per_image(wl, slabs, max_group):
+    """SURVEY.md section 8(d) 'B' flops: collapsed single_query count, final layer once."""
+    from paper_2506_21411_b200.config import build_tree_spec
+    S = (wl["image_h"] // wl["patch"]) * (wl["image_w"] // wl["patch"])
+    D, H, pp = wl["embed"], wl["heads"], wl["patch"] ** 2
+    tot = 0
+    for _, c in slabs:
+        tot += 2 * c * S * pp * D
+        for level in build_tree_spec(c, max_group).levels:
+            for g in level:
+                tot += S * (4 * g * D * H + 4 * D * D)
+    tot += S * (4 * len(slabs) * D * H + 4 * D * D)
+    return tot
+
+
+def main():
+    args = parse()
+    wl = WORKLOADS[args.workload]
+    tp = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if args.impl == "reference":
+        tp = args.gpus
+    from paper_2506_21411_b200.config import channel_slabs, max_group_for_depth
+    max_group = max_group_for_depth([n for _, n in channel_slabs(wl["channels"], tp)],
+                                    wl["depth"])
+    if args.impl == "reference":
+        reference_arm(args, wl, tp, max_group)
+    else:
+        b200_arm(args, wl, tp, max_group)
+
+
+if __name__ == "__main__":
+    main()

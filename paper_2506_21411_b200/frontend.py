@@ -144,21 +144,32 @@ class DchagFrontEnd(torch.nn.Module):
         self.weights = keep
         self._packed = None
 
-    def init_weights(self, seed: int = 0, std: float = 0.02) -> dict:
+    def needed_names(self):
+        return [n for n, _, _ in self.param_specs()
+                if not n.startswith("agg.slab") or n.startswith(f"agg.slab{self.rank}.")]
+
+    def init_weights(self, seed: int = 0, std: float = 0.02, all_ranks: bool = True) -> dict:
         """Truncated-normal(std) weights, zero biases (the reference init distribution,
-        params.py:139-150) from a torch generator; returns the full named dict."""
-        g = torch.Generator(device="cpu").manual_seed(seed)
+        params.py:139-150).  Every tensor has its own generator seeded from (seed, name), so
+        ranks that build only their own slab's weights (all_ranks=False) agree on the
+        shared ones.  Returns the named dict that was generated."""
+        import zlib
+        names = None if all_ranks else set(self.needed_names())
         master = {}
         for name, shape, init in self.param_specs():
+            if names is not None and name not in names:
+                continue
             if init == "zeros":
-                master[name] = torch.zeros(shape)
-            else:
-                v = torch.randn(shape, generator=g)
+                master[name] = torch.zeros(shape, device=self.device)
+                continue
+            g = torch.Generator(device=self.device)
+            g.manual_seed((seed * 1000003 + zlib.crc32(name.encode())) & 0x7FFFFFFFFFFF)
+            v = torch.randn(shape, generator=g, device=self.device)
+            bad = v.abs() > 2.0
+            while bool(bad.any()):
+                v[bad] = torch.randn(int(bad.sum()), generator=g, device=self.device)
                 bad = v.abs() > 2.0
-                while bad.any():
-                    v[bad] = torch.randn(int(bad.sum()), generator=g)
-                    bad = v.abs() > 2.0
-                master[name] = v * std
+            master[name] = v * std
         self.load_weights(master)
         return master
 
@@ -201,6 +212,38 @@ class DchagFrontEnd(torch.nn.Module):
         gathered = self.gather(payload)
         out = self.finish(gathered, images.shape[0])
         return (out, gathered) if return_payload else out
+
+    def launch_plan(self, B: int):
+        """Kernel launches of one forward in launch order, with the algorithmic work each
+        does: (name, site, flops, bytes).  flops are the MMA flops of the folded plan
+        (DESIGN.md section 5); bytes the compulsory HBM traffic."""
+        pk = self.prepare()
+        m = self.model
+        d, h, s, pp = m.embed, m.heads, self.seq, m.patch * m.patch
+        R = B * s
+        G = sum(pk.l0_g_list)
+        img_bytes = B * G * m.image_h * m.image_w * 2
+        plan = []
+        if pk.attn_l0:
+            plan.append(("dchag_l0_logits", "l0_logits", 2 * 2 * R * G * pp * h,
+                         img_bytes + R * G * h * 2))
+        plan.append(("dchag_l0_node", "l0_node", 2 * R * d * G * (pp + 1),
+                     img_bytes + R * G * h * 2 + pk.n0 * R * d * 2))
+        depth = len(pk.levels)
+        for li in range(depth):
+            n_l, N = len(pk.levels[li]), pk.N[li]
+            plan.append(("dchag_gemm_bf16", f"gemm_l{li}", 2 * R * n_l * d * N,
+                         n_l * R * d * 2 + n_l * R * (d * 2 + (N - d) * 4) + n_l * N * d * 2))
+            if li + 1 < depth:
+                n_next = len(pk.levels[li + 1])
+                plan.append(("dchag_combine", f"combine_l{li + 1}", 2 * R * n_l * d,
+                             n_l * R * (d * 2 + h * 4) + n_next * R * d * 2))
+        if self.tp > 1:
+            plan.append(("dchag_combine", "combine_final", 2 * R * self.tp * d,
+                         self.tp * R * (d * 2 + h * 4) + R * d * 2))
+        plan.append(("dchag_gemm_bf16", "gemm_final", 2 * R * d * d,
+                     R * d * 2 + R * d * (4 if self.out_dtype == torch.float32 else 2)))
+        return plan
 
     def gather(self, payload):
         """AllGather of the per-rank root payload in rank order (runtime.py:259)."""
