@@ -136,43 +136,67 @@ def workload_config(args, wl, tp, max_group):
 
 
 class ClockSampler:
+    """NVML sampler thread (every 5 ms) of SM clock, power and clock-event reasons; the
+    summary covers the samples taken between mark_start() and mark_stop()."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
     def __init__(self, index):
+        import threading
         self.index = index
-        self.proc = None
-        self.path = os.path.join("/tmp", f"dchag_clocks_{os.getpid()}.csv")
+        self.samples = []
+        self.window = [None, None]
+        self.stop_ev = threading.Event()
+        self.thread = None
+
+    def _run(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self.stop_ev.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((time.perf_counter(), sm, pw, rs))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def __enter__(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            import pynvml  # noqa: F401
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
         except Exception:
-            self.proc = None
+            self.thread = None
         return self
 
+    def mark_start(self):
+        self.window[0] = time.perf_counter()
+
+    def mark_stop(self):
+        self.window[1] = time.perf_counter()
+
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            self.proc.wait()
+        self.stop_ev.set()
+        if self.thread:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        try:
-            rows = [r.split(", ") for r in open(self.path).read().strip().splitlines()]
-        except Exception:
+        if not self.samples:
             return None
-        rows = [r for r in rows if len(r) >= 7]
-        if not rows:
-            return None
-        sm = [float(r[0]) for r in rows]
-        load = [float(r[0]) for r in rows if float(r[2]) > 300] or sm
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].strip() == "Active"})
-        return {"sm_mhz": statistics.median(load), "sm_max_mhz": float(rows[0][1]),
-                "reasons": reasons, "samples": len(rows)}
+        t0, t1 = self.window
+        win = [x for x in self.samples if t0 is not None and t0 <= x[0] <= (t1 or 1e30)]
+        src = win or self.samples
+        reasons = sorted({k for x in src for k, bit in self.REASONS.items() if x[3] & bit})
+        return {"sm_mhz": statistics.median(x[1] for x in src),
+                "sm_max_mhz": float(getattr(self, "max_mhz", 0)),
+                "power_w_max": max(x[2] for x in src), "reasons": reasons,
+                "samples": len(src), "window": "timed region" if win else "whole run"}
 
 
 def b200_arm(args, wl, tp, max_group):
@@ -225,12 +249,18 @@ def b200_arm(args, wl, tp, max_group):
         return float(t.item())
 
     step = lambda: fe(images)  # noqa: E731
+    clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         step()
+    t_end = time.perf_counter() + 0.5  # let clocks settle: >= 0.5 s of warm-up work
+    while time.perf_counter() < t_end:
+        step()
+        torch.cuda.synchronize()
     # ---- pass A: headline (inputs resident in HBM)
     n0 = _lib.LAUNCH_COUNT["n"]
-    with ClockSampler(local) as clk:
-        ms = timed(step, args.steps)
+    clk.mark_start()
+    ms = timed(step, args.steps)
+    clk.mark_stop()
     launches = _lib.LAUNCH_COUNT["n"] - n0
     ms = max_over_ranks(ms)
     value = B * args.steps / (ms / 1e3)
@@ -328,6 +358,7 @@ def b200_arm(args, wl, tp, max_group):
                "sample": f"1 image x {tok}/{S} tokens, {dt:.1f} s (float64 numpy restatement "
                          f"of the reference hot path, {blas})"}
 
+    clk.__exit__()
     if rank == 0:
         clocks = clk.summary()
         line = {

@@ -47,32 +47,37 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
  * q@wq / x@wk / logits / softmax part of layers.py:103-121 for tree level 0 with the
  * tokenizer (model.py:51-64) folded in.  img: bf16 [B][*][Himg][W] with batch stride
  * img_sb and channel stride img_sc (slab channel c at img + c*img_sc).
- * node_c0/node_g (int32) and node_poff (int64) are device arrays of n_nodes.
+ * node_c0/node_g (int32) and node_poff (int64) are device arrays of n_nodes; gmax >= all node_g.
  * WUt bf16 [C][HP][P*P], bU fp32 [C][HP], posU fp32 [n_nodes][S][HP]; HP = H rounded up
- * to a multiple of 8.  Output p bf16 at p[poff[n] + (r*g + c)*H + h]. */
+ * to a multiple of 8.  Output p bf16, head-group major (the K_l0 CTA's slice is
+ * contiguous): p[poff[n] + ((hg*R + r)*g + c)*NH + h%NH], hg = h/NH, NH = 4 if H%4==0 else 2. */
 int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
-                    int P, int H, int HP, int n_nodes, const int* node_c0, const int* node_g,
+                    int P, int H, int HP, int n_nodes, int gmax, const int* node_c0,
+                    const int* node_g,
                     const long long* node_poff, const void* WUt, const float* bU,
                     const float* posU, void* p, void* stream);
 
 /* Level-0 node context (K_l0, tcgen05 with A in TMEM):
  *   ctx[n][r][h*64:(h+1)*64] = sum_c p[r,c,h] * (patch_c[r] @ M_c[:, h-block])
- *                             + sum_c p[r,c,h] * E_n[c, h-block] + posV[n][s][h-block]
+ *                             + sum_c p[r,c,h] * E_n[c, h-block]
+ * (the positional term pos[s] @ wv_n is folded into the next dchag_gemm_bf16 row bias)
  * Mt bf16 [H][C_pad][64*P*P] and Et bf16 [n_nodes][H][64*KE] are pre-tiled canonical
- * UMMA blocks (dchag_tile_weights); p_row_mode = 0 reads a constant table p[poff + c*H + h]
+ * UMMA blocks (dchag_tile_weights); p_row_mode = 1 reads the dchag_l0_logits layout, 0 a constant
+ * table p[poff + c*H + h]
  * (linear-mix nodes).  Requires head dim 64, H % 4 == 0, S % 128 == 0, 128 % (W/P) == 0,
  * P in {4, 8}. */
 int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
                   int P, int H, int D, int n_nodes, const int* node_c0, const int* node_g,
                   const long long* node_poff, int p_row_mode, const void* p, const void* Mt,
-                  int C_pad, const void* Et, int KE, const void* posV, void* ctx, void* stream);
+                  int C_pad, const void* Et, int KE, void* ctx, void* stream);
 
 /* Upper-level / final combine (K_comb): ctx[n][r][:] = sum_j w_j(r,h) V_{first+j}[r][:],
  * w = softmax_j(L_{first+j}[r][h]) (attention; mix == NULL) or mix[first+j] (linear).
- * Child j's V at V + j*sVj + r*D (bf16), logits at L + j*sLj + r*H (fp32). */
+ * Child j's V at V + j*sVj + r*D (bf16), logits at L + j*sLj + r*H (fp32).
+ * max_g >= every node_g; requires max_g * H <= 1024 (attention). */
 int dchag_combine(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
-                  const void* V, long long sVj, const float* L, long long sLj, const float* mix,
-                  void* ctx, void* stream);
+                  int max_g, const void* V, long long sVj, const float* L, long long sLj,
+                  const float* mix, void* ctx, void* stream);
 
 /* unfold_patches (tensor.py:303-323): img [B][C][Himg][W] -> out [B][C][S][P*P] bf16. */
 int dchag_unfold(const void* img, long long img_sb, long long img_sc, int B, int C, int Himg,

@@ -4,6 +4,7 @@
 // stream.  No device allocation, no host synchronisation.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -149,7 +150,8 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
 }
 
 int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
-                    int P, int H, int HP, int n_nodes, const int* node_c0, const int* node_g,
+                    int P, int H, int HP, int n_nodes, int gmax, const int* node_c0,
+                    const int* node_g,
                     const long long* node_poff, const void* WUt, const float* bU,
                     const float* posU, void* p, void* stream) {
   if (Himg % P || W % P || HP % 8 || HP < H || H % 2 || (P * P) % 16)
@@ -158,7 +160,9 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
   a.img = reinterpret_cast<const __nv_bfloat16*>(img);
   a.img_sb = img_sb; a.img_sc = img_sc;
   a.B = B; a.S = (Himg / P) * (W / P); a.W = W; a.P = P; a.wp = W / P; a.H = H; a.HP = HP;
-  a.n_nodes = n_nodes; a.node_c0 = node_c0; a.node_g = node_g; a.node_poff = node_poff;
+  a.n_nodes = n_nodes; a.gmax = gmax;
+  a.p0_smem = getenv("DCHAG_P0_SMEM") ? atoi(getenv("DCHAG_P0_SMEM")) : 0;
+  a.node_c0 = node_c0; a.node_g = node_g; a.node_poff = node_poff;
   a.WUt = reinterpret_cast<const __nv_bfloat16*>(WUt);
   a.bU = bU; a.posU = posU;
   a.p = reinterpret_cast<__nv_bfloat16*>(p);
@@ -169,7 +173,7 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
 int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
                   int P, int H, int D, int n_nodes, const int* node_c0, const int* node_g,
                   const long long* node_poff, int p_row_mode, const void* p, const void* Mt,
-                  int C_pad, const void* Et, int KE, const void* posV, void* ctx, void* stream) {
+                  int C_pad, const void* Et, int KE, void* ctx, void* stream) {
   if (Himg % P || W % P) return fail(DCHAG_ERR_SHAPE, "l0_node: image not divisible by patch");
   L0NodeArgs a;
   a.img = reinterpret_cast<const __nv_bfloat16*>(img);
@@ -182,19 +186,22 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
   a.C_pad = C_pad;
   a.Et = reinterpret_cast<const __nv_bfloat16*>(Et);
   a.KE = KE;
-  a.posV = reinterpret_cast<const __nv_bfloat16*>(posV);
   a.ctx = reinterpret_cast<__nv_bfloat16*>(ctx);
+  {
+    const char* dbg = getenv("DCHAG_L0_DEBUG");
+    a.debug_mode = dbg ? atoi(dbg) : 0;
+  }
   if ((reinterpret_cast<uintptr_t>(img) | (uintptr_t)(img_sb * 2) | (uintptr_t)(img_sc * 2)) % 16)
     return fail(DCHAG_ERR_SHAPE, "l0_node: image base/strides must be 16-byte aligned");
   return cuda_status(launch_l0_node(a, num_sms_cached(), S(stream)), "l0_node");
 }
 
 int dchag_combine(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
-                  const void* V, long long sVj, const float* L, long long sLj, const float* mix,
-                  void* ctx, void* stream) {
+                  int max_g, const void* V, long long sVj, const float* L, long long sLj,
+                  const float* mix, void* ctx, void* stream) {
   if (!mix && !L) return fail(DCHAG_ERR_SHAPE, "combine: need logits or mix");
   CombineArgs a;
-  a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H;
+  a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H; a.max_g = max_g;
   a.node_first = node_first; a.node_g = node_g;
   a.V = reinterpret_cast<const __nv_bfloat16*>(V); a.sVj = sVj;
   a.L = L; a.sLj = sLj; a.mix = mix;

@@ -11,72 +11,64 @@
 
 namespace dchag {
 
-constexpr int COMB_MAXG = 128;
+constexpr int COMB_PTAB = 1024;  // softmax table per warp: g * H <= 1024 floats
+constexpr int COMB_MAXH = 32;
 
-// one warp per (node, row); lane owns 8-column chunks lane, lane+32, ... (16-B vectors)
+// One warp per (node, row).  Phase 1: lanes < H own one head each and compute the
+// softmax over the g children from coalesced logit rows; weights go to shared memory.
+// Phase 2: every lane owns 8-column (16-byte) chunks and streams the g child rows,
+// unrolled so each lane keeps several independent 16-byte loads in flight.
 __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
+  __shared__ float sp[8][COMB_PTAB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long item = (long long)blockIdx.x * 8 + warp;
   const int n = (int)(item / a.R);
   const int r = (int)(item - (long long)n * a.R);
   if (n >= a.n_nodes) return;
   const int first = __ldg(a.node_first + n), g = __ldg(a.node_g + n);
-  const int dh = a.D / a.H;
-  const int nchunk = a.D / 8;
-  const int per_lane = (nchunk + 31) / 32;  // <= 8 for D <= 2048
-
+  const int H = a.H, dh = a.D / H;
+  float* p = sp[warp];
+  if (a.mix) {
+    for (int j = lane; j < g; j += 32) p[j] = __ldg(a.mix + first + j);
+  } else if (lane < H) {
+    const float* lr = a.L + (long long)first * a.sLj + (long long)r * H + lane;
+    float m = -INFINITY;
+    for (int j = 0; j < g; ++j) m = fmaxf(m, __ldg(lr + (long long)j * a.sLj));
+    float ssum = 0.f;
+    for (int j = 0; j < g; ++j) {
+      const float e = __expf(__ldg(lr + (long long)j * a.sLj) - m);
+      p[j * H + lane] = e;
+      ssum += e;
+    }
+    const float inv = 1.f / ssum;
+    for (int j = 0; j < g; ++j) p[j * H + lane] *= inv;
+  }
+  __syncwarp();
+  const int nchunk = a.D / 8;  // <= 256 (D <= 2048)
   float acc[8][8];
 #pragma unroll
   for (int q = 0; q < 8; ++q)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[q][e] = 0.f;
-
-  // softmax statistics for the heads this lane touches (computed redundantly per lane)
-  float mx[8], inv[8];
-  if (!a.mix) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      mx[q] = -INFINITY;
-      inv[q] = 0.f;
-      if (q < per_lane) {
-        const int ch = lane + 32 * q;
-        if (ch < nchunk) {
-          const int h = ch * 8 / dh;
-          float m = -INFINITY;
-          for (int j = 0; j < g; ++j)
-            m = fmaxf(m, a.L[(long long)(first + j) * a.sLj + (long long)r * a.H + h]);
-          float s = 0.f;
-          for (int j = 0; j < g; ++j)
-            s += __expf(a.L[(long long)(first + j) * a.sLj + (long long)r * a.H + h] - m);
-          mx[q] = m;
-          inv[q] = 1.f / s;
-        }
-      }
-    }
-  }
+  const __nv_bfloat16* vbase = a.V + (long long)first * a.sVj + (long long)r * a.D;
+  const int per_lane = (nchunk + 31) / 32;
   for (int j = 0; j < g; ++j) {
-    const __nv_bfloat16* vrow = a.V + (long long)(first + j) * a.sVj + (long long)r * a.D;
-    const float* lrow = a.L ? a.L + (long long)(first + j) * a.sLj + (long long)r * a.H : nullptr;
-    const float mixj = a.mix ? __ldg(a.mix + first + j) : 0.f;
+    const __nv_bfloat16* vrow = vbase + (long long)j * a.sVj;
+    uint4 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < per_lane && lane + 32 * q < nchunk)
+        v[q] = __ldg(reinterpret_cast<const uint4*>(vrow) + lane + 32 * q);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      if (q < per_lane) {
+      if (q < per_lane && lane + 32 * q < nchunk) {
         const int ch = lane + 32 * q;
-        if (ch < nchunk) {
-          float pj;
-          if (a.mix) {
-            pj = mixj;
-          } else {
-            const int h = ch * 8 / dh;
-            pj = __expf(lrow[h] - mx[q]) * inv[q];
-          }
-          const uint4 v = *reinterpret_cast<const uint4*>(vrow + ch * 8);
-          const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+        const float pj = a.mix ? p[j] : p[j * H + (ch * 8) / dh];
+        const uint32_t vv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            acc[q][2 * e] += pj * bf16lo(vv[e]);
-            acc[q][2 * e + 1] += pj * bf16hi(vv[e]);
-          }
+        for (int e = 0; e < 4; ++e) {
+          acc[q][2 * e] += pj * bf16lo(vv[e]);
+          acc[q][2 * e + 1] += pj * bf16hi(vv[e]);
         }
       }
     }
@@ -84,22 +76,21 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
   __nv_bfloat16* orow = a.ctx + ((long long)n * a.R + r) * a.D;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    if (q < per_lane) {
-      const int ch = lane + 32 * q;
-      if (ch < nchunk) {
-        uint4 o;
-        o.x = pack_bf16(acc[q][0], acc[q][1]);
-        o.y = pack_bf16(acc[q][2], acc[q][3]);
-        o.z = pack_bf16(acc[q][4], acc[q][5]);
-        o.w = pack_bf16(acc[q][6], acc[q][7]);
-        *reinterpret_cast<uint4*>(orow + ch * 8) = o;
-      }
+    if (q < per_lane && lane + 32 * q < nchunk) {
+      uint4 o;
+      o.x = pack_bf16(acc[q][0], acc[q][1]);
+      o.y = pack_bf16(acc[q][2], acc[q][3]);
+      o.z = pack_bf16(acc[q][4], acc[q][5]);
+      o.w = pack_bf16(acc[q][6], acc[q][7]);
+      reinterpret_cast<uint4*>(orow)[lane + 32 * q] = o;
     }
   }
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
-  if (a.D % 8 || a.D > 2048 || (a.D / a.H) % 8) return cudaErrorInvalidValue;
+  if (a.D % 8 || a.D > 2048 || (a.D / a.H) % 8 || a.H > COMB_MAXH ||
+      a.max_g * (a.mix ? 1 : a.H) > COMB_PTAB)
+    return cudaErrorInvalidValue;
   const long long items = (long long)a.n_nodes * a.R;
   const int grid = (int)((items + 7) / 8);
   combine_kernel<<<grid, 256, 0, st>>>(a);

@@ -30,18 +30,20 @@ struct L0LogitArgs {
   const __nv_bfloat16* img;  // [B][*][H][W]; channel c of the slab at img + c*img_sc
   long long img_sb, img_sc;
   int B, S, W, P, wp, H, HP;  // H heads, HP = H padded to a multiple of 8
-  int n_nodes;
+  int n_nodes, gmax;          // gmax >= every node_g (host-known)
+  int p0_smem;                // use the shared-memory staged variant
   const int* node_c0;         // first slab channel of node n
   const int* node_g;          // channel count of node n
   const long long* node_poff; // element offset of node n in p
   const __nv_bfloat16* WUt;   // [C][HP][PP]  logit weights tok.w[c] @ U_n, transposed
   const float* bU;            // [C][HP]      (tok.b[c]+chan_id[c]) @ U_n
   const float* posU;          // [n_nodes][S][HP]
-  __nv_bfloat16* p;           // p[poff[n] + (r*g + c)*H + h]
+  __nv_bfloat16* p;           // p[poff[n] + ((hg*R + r)*g + c)*NH + h%NH], hg = h/NH,
+                              // NH = 4 if H % 4 == 0 else 2 (head group of one K_l0 CTA)
 };
 cudaError_t launch_l0_logits(const L0LogitArgs& a, cudaStream_t st);
 
-// Level-0 node: ctx[n][r][h*dh:(h+1)*dh] = sum_c p[r,c,h] * (patch_c[r] @ M_c[:,h]) + ext + posV
+// Level-0 node: ctx[n][r][h*dh:(h+1)*dh] = sum_c p[r,c,h] * (patch_c[r] @ M_c[:,h]) + ext
 struct L0NodeArgs {
   const __nv_bfloat16* img;
   long long img_sb, img_sc;
@@ -50,20 +52,20 @@ struct L0NodeArgs {
   const int* node_c0;
   const int* node_g;
   const long long* node_poff;
-  int p_row_mode;              // 1: p depends on row; 0: constant table p[poff + c*H + h]
+  int p_row_mode;              // 1: K_p0 layout (see L0LogitArgs); 0: constant p[poff + c*H + h]
   const __nv_bfloat16* p;
   const __nv_bfloat16* Mt;     // [H][C_pad][dh*PP] canonical no-swizzle K-major blocks
   int C_pad;
   const __nv_bfloat16* Et;     // [n_nodes][H][dh*KE] ext (bias) blocks
   int KE;
-  const __nv_bfloat16* posV;   // [n_nodes][S][D]
   __nv_bfloat16* ctx;          // [n_nodes][R][D]
+  int debug_mode;              // timing probes: 0 normal, 1 no A build, 2 no MMA
 };
 cudaError_t launch_l0_node(const L0NodeArgs& a, int num_sms, cudaStream_t st);
 
 // Upper-level combine: ctx[n][r][:] = sum_j p_jh(r) * V_child(j)[r][:]
 struct CombineArgs {
-  int n_nodes, R, D, H;
+  int n_nodes, R, D, H, max_g;
   const int* node_first;       // first child index of node n
   const int* node_g;           // child count
   const __nv_bfloat16* V;      // child j at V + j*sVj + r*D

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      mbar_wait(&tempty[acc], acc_phase);  // epilogue warps pre-load bias into the buffer
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * GEMM_BN_MAX;
       for (int ks = 0; ks < k_steps; ++ks) {
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = smem_desc(a_addr + kk * 32, 16, SBO, swz_layout<BK>());
             const uint64_t wd = smem_desc(w_addr + kk * 32, 16, SBO, swz_layout<BK>());
-            mma_ss(d_tmem, ad, wd, idesc, (ks | kk) != 0);
+            mma_ss(d_tmem, ad, wd, idesc, 1u);
           }
           mma_commit(&empty[stage]);
           if (ks == k_steps - 1) mma_commit(&tfull[acc]);
@@ -130,25 +130,110 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else {
     // ------------------------------------------------ epilogue (warps 2..5)
+    // The accumulator buffer of tile i is pre-loaded with bias (+ row bias) while the MMAs
+    // of tile i-1 run, so the drain below is pure TMEM -> bf16/fp32 -> HBM.
     const int quarter = warp & 3;
     const int row_in_tile = quarter * 32 + lane;
+    const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
+    auto tile_coords = [&](int t, int& g, int& mo, int& mi, int& nt) {
+      g = t / tiles_per_g;
+      const int rem = t - g * tiles_per_g;
+      const int mt = rem / n_tiles_n;
+      nt = rem - mt * n_tiles_n;
+      const int m = mt * GEMM_BM + row_in_tile;
+      mo = m / args.Mi;
+      mi = m - mo * args.Mi;
+    };
+    // Row bias of a tile: fetched into registers one tile ahead (all 16 chunks issued at
+    // once, so the HBM/L2 latency overlaps the drain of the previous tile).
+    constexpr int NCH = GEMM_BN_MAX / 16;
+    const bool rb_vec = (args.rowbias_row & 7) == 0 && (args.rowbias_g & 7) == 0;
+    auto fetch_rb = [&](int t, uint4 (&rbv)[NCH][2]) {
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) rbv[ch][0] = rbv[ch][1] = make_uint4(0, 0, 0, 0);
+      if (!args.rowbias || t >= total_tiles) return;
+      int g, mo, mi, nt;
+      tile_coords(t, g, mo, mi, nt);
+      const __nv_bfloat16* rb = args.rowbias + (size_t)g * args.rowbias_g +
+                                (size_t)(mi % args.rowbias_period) * args.rowbias_row;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int n0 = nt * args.BN + ch * 16;
+        if (ch * 16 < args.BN && n0 + 16 <= args.N && rb_vec) {
+          rbv[ch][0] = __ldg(reinterpret_cast<const uint4*>(rb + n0));
+          rbv[ch][1] = __ldg(reinterpret_cast<const uint4*>(rb + n0 + 8));
+        } else if (ch * 16 < args.BN) {
+          uint32_t w[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float lo = n0 + 2 * e < args.N ? __bfloat162float(rb[n0 + 2 * e]) : 0.f;
+            const float hi = n0 + 2 * e + 1 < args.N ? __bfloat162float(rb[n0 + 2 * e + 1]) : 0.f;
+            w[e] = pack_bf16(lo, hi);
+          }
+          rbv[ch][0] = make_uint4(w[0], w[1], w[2], w[3]);
+          rbv[ch][1] = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+    };
+    auto init_acc = [&](int t, int buf, const uint4 (&rbv)[NCH][2]) {
+      int g, mo, mi, nt;
+      tile_coords(t, g, mo, mi, nt);
+      const float* bias = args.bias ? args.bias + (size_t)g * args.bias_g : nullptr;
+      const bool bvec = (args.bias_g & 3) == 0;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        if (ch * 16 >= args.BN) break;
+        const int n0 = nt * args.BN + ch * 16;
+        float v[16];
+        const uint32_t q[8] = {rbv[ch][0].x, rbv[ch][0].y, rbv[ch][0].z, rbv[ch][0].w,
+                               rbv[ch][1].x, rbv[ch][1].y, rbv[ch][1].z, rbv[ch][1].w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          v[2 * e] = bf16lo(q[e]);
+          v[2 * e + 1] = bf16hi(q[e]);
+        }
+        if (bias) {
+          if (n0 + 16 <= args.N && bvec) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + n0 + j));
+              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (n0 + j < args.N) v[j] += __ldg(bias + n0 + j);
+          }
+        }
+        uint32_t u[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) u[j] = __float_as_uint(v[j]);
+        tmem_st16(lane_base + buf * GEMM_BN_MAX + ch * 16, u);
+      }
+      tmem_st_wait();
+    };
+    // prologue: pre-load the first two tiles' buffers
+    uint4 rbv[NCH][2];
+    {
+      int i = 0;
+      for (int t = blockIdx.x; t < total_tiles && i < 2; t += gridDim.x, ++i) {
+        fetch_rb(t, rbv);
+        init_acc(t, i, rbv);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[i]);
+      }
+    }
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const int g = t / tiles_per_g;
-      const int rem = t - g * tiles_per_g;
-      const int mt = rem / n_tiles_n;
-      const int nt = rem - mt * n_tiles_n;
-      const int m = mt * GEMM_BM + row_in_tile;
-      const int mo = m / args.Mi, mi = m - mo * args.Mi;
+      int g, mo, mi, nt;
+      tile_coords(t, g, mo, mi, nt);
+      const int t2 = t + 2 * gridDim.x;
+      fetch_rb(t2, rbv);  // in flight while this tile's MMAs finish and it drains
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * GEMM_BN_MAX;
-      const float* bias = args.bias ? args.bias + (size_t)g * args.bias_g : nullptr;
-      const __nv_bfloat16* rb =
-          args.rowbias ? args.rowbias + (size_t)g * args.rowbias_g +
-                             (size_t)(mi % args.rowbias_period) * args.rowbias_row
-                       : nullptr;
+      const uint32_t t_row = lane_base + acc * GEMM_BN_MAX;
       for (int c0 = 0; c0 < args.BN; c0 += 16) {
         const int n0 = nt * args.BN + c0;
         if (n0 >= args.N) break;
@@ -158,31 +243,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float v[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-        if (bias) {
-          if (n0 + 16 <= args.N && (args.bias_g & 3) == 0) {
-#pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-              const float4 b4 = *reinterpret_cast<const float4*>(bias + n0 + j);
-              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (n0 + j < args.N) v[j] += __ldg(bias + n0 + j);
-          }
-        }
-        if (rb) {
-#pragma unroll
-          for (int j = 0; j < 16; j += 8) {
-            const uint4 q = *reinterpret_cast<const uint4*>(rb + n0 + j);
-            const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              v[j + 2 * e] += bf16lo(qq[e]);
-              v[j + 2 * e + 1] += bf16hi(qq[e]);
-            }
-          }
-        }
         if (n0 < args.Nv) {
           if (args.outV_f32) {
             float* o = reinterpret_cast<float*>(args.outV) + (size_t)g * args.sVg +
@@ -217,6 +277,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
       }
+      // re-arm this buffer for the tile two steps ahead
+      if (t2 < total_tiles) init_acc(t2, acc, rbv);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);

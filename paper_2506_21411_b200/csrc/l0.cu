@@ -31,7 +31,7 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-template <int NT>  // NT = HP / 8 head tiles
+template <int NT, int P>  // NT = HP / 8 head tiles; P compile-time so every load unrolls
 __global__ void __launch_bounds__(128) l0_logits_kernel(L0LogitArgs a) {
   const int R = a.B * a.S;
   const int blocks_per_node = R / 64;
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(128) l0_logits_kernel(L0LogitArgs a) {
   const int rblk = blockIdx.x - n * blocks_per_node;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const int PP = a.P * a.P;
+  constexpr int PP = P * P;
   const int c0 = __ldg(a.node_c0 + n), g = __ldg(a.node_g + n);
   const long long poff = __ldg(a.node_poff + n);
 
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(128) l0_logits_kernel(L0LogitArgs a) {
     const int b = rows[q] / a.S, s = rows[q] - b * a.S;
     srow[q] = s;
     const int i = s / a.wp, j = s - i * a.wp;
-    rowimg[q] = a.img + b * a.img_sb + (long long)(i * a.P) * a.W + j * a.P;
+    rowimg[q] = a.img + b * a.img_sb + (long long)(i * P) * a.W + j * P;
   }
   float pu[NT][4];
 #pragma unroll
@@ -74,15 +74,150 @@ __global__ void __launch_bounds__(128) l0_logits_kernel(L0LogitArgs a) {
       L[nt][2] = pu[nt][2] + bu[0];
       L[nt][3] = pu[nt][3] + bu[1];
     }
+    uint32_t afs[PP / 16][4];
+#pragma unroll
+    for (int ks = 0; ks < PP / 16; ++ks) {
+#pragma unroll
+      for (int hk = 0; hk < 2; ++hk) {
+        const int k = ks * 16 + hk * 8 + 2 * tig;
+        const int py = k / P, px = k - py * P;
+        const long long off = coff + (long long)py * a.W + px;
+        afs[ks][hk * 2 + 0] = __ldg(reinterpret_cast<const unsigned int*>(rowimg[0] + off));
+        afs[ks][hk * 2 + 1] = __ldg(reinterpret_cast<const unsigned int*>(rowimg[1] + off));
+      }
+    }
+#pragma unroll
+    for (int ks = 0; ks < PP / 16; ++ks) {
+      const uint32_t (&af)[4] = afs[ks];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const __nv_bfloat16* wb = a.WUt + ((long long)(c0 + c) * a.HP + nt * 8 + gid) * PP +
+                                  ks * 16 + 2 * tig;
+        const uint32_t b0 = __ldg(reinterpret_cast<const unsigned int*>(wb));
+        const uint32_t b1 = __ldg(reinterpret_cast<const unsigned int*>(wb + 8));
+        mma_bf16_16816(L[nt], af, b0, b1);
+      }
+    }
+  };
+
+  float mx[NT][4], sm[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { mx[nt][e] = -INFINITY; sm[nt][e] = 0.f; }
+#pragma unroll 2
+  for (int c = 0; c < g; ++c) {
+    float L[NT][4];
+    logits(c, L);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float m2 = fmaxf(mx[nt][e], L[nt][e]);
+        sm[nt][e] = sm[nt][e] * __expf(mx[nt][e] - m2) + __expf(L[nt][e] - m2);
+        mx[nt][e] = m2;
+      }
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sm[nt][e] = 1.f / sm[nt][e];
+  for (int c = 0; c < g; ++c) {
+    float L[NT][4];
+    logits(c, L);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int h = nt * 8 + 2 * tig;
+      if (h < a.H) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const float p0 = __expf(L[nt][2 * q] - mx[nt][2 * q]) * sm[nt][2 * q];
+          const float p1 = __expf(L[nt][2 * q + 1] - mx[nt][2 * q + 1]) * sm[nt][2 * q + 1];
+          const int nh = (a.H % 4 == 0) ? 4 : 2;
+          const int hg = h / nh, hl = h - hg * nh;
+          __nv_bfloat16* dst = a.p + poff + (((long long)hg * R + rows[q]) * g + c) * nh + hl;
+          *reinterpret_cast<uint32_t*>(dst) = pack_bf16(p0, p1);
+        }
+      }
+    }
+  }
+}
+
+// K_p0 v2: the CTA stages every image row it needs (TR positions x g channels) in shared
+// memory with 1-D bulk copies, recomputes the logits from shared memory in a second pass
+// (mma.sync is cheap next to the HBM read), and writes p through a shared staging tile so
+// the global stores are contiguous 16-byte vectors.
+template <int NT, int TR>
+__global__ void __launch_bounds__(TR * 2) l0_logits_smem_kernel(L0LogitArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                             ~uintptr_t(127));
+  const int R = a.B * a.S;
+  const int blocks_per_node = R / TR;
+  const int n = blockIdx.x / blocks_per_node;
+  const int rblk = blockIdx.x - n * blocks_per_node;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int PP = a.P * a.P;
+  const int c0 = __ldg(a.node_c0 + n), g = __ldg(a.node_g + n);
+  const long long poff = __ldg(a.node_poff + n);
+  const int nh = (a.H % 4 == 0) ? 4 : 2;
+  const int r0 = rblk * TR;
+  const int b = r0 / a.S, s0 = r0 - b * a.S;
+  const int chunk = TR * PP;  // elements per channel
+  __nv_bfloat16* simg = reinterpret_cast<__nv_bfloat16*>(smem);
+  __nv_bfloat16* sp = simg + (size_t)g * chunk;                 // [hg][TR][g][nh]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sp + (size_t)TR * g * a.H + 64);
+  bar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bar) + 7) & ~uintptr_t(7));
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(bar, (uint32_t)(g * chunk * 2));
+    const __nv_bfloat16* src = a.img + b * a.img_sb + (long long)(s0 / a.wp) * a.P * a.W;
+    for (int c = 0; c < g; ++c)
+      bulk_load(simg + (size_t)c * chunk, src + (long long)(c0 + c) * a.img_sc, chunk * 2, bar);
+  }
+  const int rl[2] = {warp * 16 + gid, warp * 16 + gid + 8};  // rows within the tile
+  int rowoff[2];
+  float pu[NT][4];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int m = rl[q];
+    const int i = m / a.wp, j = m - i * a.wp;
+    rowoff[q] = i * a.P * a.W + j * a.P;
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const float* pr0 = a.posU + ((long long)n * a.S + s0 + rl[0]) * a.HP + nt * 8 + 2 * tig;
+    const float* pr1 = a.posU + ((long long)n * a.S + s0 + rl[1]) * a.HP + nt * 8 + 2 * tig;
+    pu[nt][0] = pr0[0]; pu[nt][1] = pr0[1];
+    pu[nt][2] = pr1[0]; pu[nt][3] = pr1[1];
+  }
+  mbar_wait(bar, 0);
+
+  auto logits = [&](int c, float (&L)[NT][4]) {
+    const __nv_bfloat16* cimg = simg + (size_t)c * chunk;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const float* bu = a.bU + (long long)(c0 + c) * a.HP + nt * 8 + 2 * tig;
+      const float b0 = __ldg(bu), b1 = __ldg(bu + 1);
+      L[nt][0] = pu[nt][0] + b0;
+      L[nt][1] = pu[nt][1] + b1;
+      L[nt][2] = pu[nt][2] + b0;
+      L[nt][3] = pu[nt][3] + b1;
+    }
     for (int ks = 0; ks < PP / 16; ++ks) {
       uint32_t af[4];
 #pragma unroll
       for (int hk = 0; hk < 2; ++hk) {
         const int k = ks * 16 + hk * 8 + 2 * tig;
         const int py = k / a.P, px = k - py * a.P;
-        const long long off = coff + (long long)py * a.W + px;
-        af[hk * 2 + 0] = *reinterpret_cast<const uint32_t*>(rowimg[0] + off);
-        af[hk * 2 + 1] = *reinterpret_cast<const uint32_t*>(rowimg[1] + off);
+        const int off = py * a.W + px;
+        af[hk * 2 + 0] = *reinterpret_cast<const uint32_t*>(cimg + rowoff[0] + off);
+        af[hk * 2 + 1] = *reinterpret_cast<const uint32_t*>(cimg + rowoff[1] + off);
       }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
@@ -123,28 +258,61 @@ __global__ void __launch_bounds__(128) l0_logits_kernel(L0LogitArgs a) {
     for (int nt = 0; nt < NT; ++nt) {
       const int h = nt * 8 + 2 * tig;
       if (h < a.H) {
+        const int hg = h / nh, hl = h - hg * nh;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const float p0 = __expf(L[nt][2 * q] - mx[nt][2 * q]) * sm[nt][2 * q];
           const float p1 = __expf(L[nt][2 * q + 1] - mx[nt][2 * q + 1]) * sm[nt][2 * q + 1];
-          __nv_bfloat16* dst = a.p + poff + ((long long)rows[q] * g + c) * a.H + h;
-          *reinterpret_cast<uint32_t*>(dst) = pack_bf16(p0, p1);
+          *reinterpret_cast<uint32_t*>(sp + (((size_t)hg * TR + rl[q]) * g + c) * nh + hl) =
+              pack_bf16(p0, p1);
         }
       }
     }
+  }
+  __syncthreads();
+  // copy out: per head group a contiguous run of TR*g*nh bf16
+  const int run = TR * g * nh;  // elements, multiple of 8
+  for (int hg = 0; hg < a.H / nh; ++hg) {
+    const uint4* src = reinterpret_cast<const uint4*>(sp + (size_t)hg * run);
+    uint4* dst = reinterpret_cast<uint4*>(a.p + poff + ((long long)hg * R + r0) * g * nh);
+    for (int i = threadIdx.x; i < run / 8; i += blockDim.x) dst[i] = src[i];
   }
 }
 
 cudaError_t launch_l0_logits(const L0LogitArgs& a, cudaStream_t st) {
   const int R = a.B * a.S;
+  const int PP = a.P * a.P;
+  // fast path: shared-memory staged (needs whole patch rows per tile and g*PP*TR*2 <= 128 KB;
+  // the node sizes are not known here, so the caller passes them bounded via H*?: use gmax)
+  const int TR = (32 % a.wp == 0) ? 32 : ((64 % a.wp == 0) ? 64 : 0);
+  if (a.p0_smem && TR && a.S % TR == 0 && a.gmax > 0 &&
+      (long long)a.gmax * PP * TR * 2 + (long long)TR * a.gmax * a.H * 2 <= 200000 &&
+      (TR * a.gmax * (a.H % 4 == 0 ? 4 : 2)) % 8 == 0) {
+    const int smem = a.gmax * PP * TR * 2 + TR * a.gmax * a.H * 2 + 64 * 2 + 256;
+    const int grid = a.n_nodes * (R / TR);
+    void (*k)(L0LogitArgs) = nullptr;
+    const int nt = a.HP / 8;
+    if (TR == 32) k = nt == 1 ? l0_logits_smem_kernel<1, 32> : nt == 2 ? l0_logits_smem_kernel<2, 32>
+                                                              : nt == 4 ? l0_logits_smem_kernel<4, 32> : nullptr;
+    else k = nt == 1 ? l0_logits_smem_kernel<1, 64> : nt == 2 ? l0_logits_smem_kernel<2, 64>
+                                                     : nt == 4 ? l0_logits_smem_kernel<4, 64> : nullptr;
+    if (k) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      k<<<grid, TR * 2, smem, st>>>(a);
+      return cudaGetLastError();
+    }
+  }
   if (R % 64) return cudaErrorInvalidValue;
   const int grid = a.n_nodes * (R / 64);
-  switch (a.HP / 8) {
-    case 1: l0_logits_kernel<1><<<grid, 128, 0, st>>>(a); break;
-    case 2: l0_logits_kernel<2><<<grid, 128, 0, st>>>(a); break;
-    case 4: l0_logits_kernel<4><<<grid, 128, 0, st>>>(a); break;
-    default: return cudaErrorInvalidValue;
-  }
+  void (*k)(L0LogitArgs) = nullptr;
+  const int nt = a.HP / 8;
+  if (a.P == 8) k = nt == 1 ? l0_logits_kernel<1, 8> : nt == 2 ? l0_logits_kernel<2, 8>
+                                                      : nt == 4 ? l0_logits_kernel<4, 8> : nullptr;
+  else if (a.P == 4) k = nt == 1 ? l0_logits_kernel<1, 4> : nt == 2 ? l0_logits_kernel<2, 4>
+                                                           : nt == 4 ? l0_logits_kernel<4, 4> : nullptr;
+  if (!k) return cudaErrorInvalidValue;
+  k<<<grid, 128, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -220,7 +388,9 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sI = smem + stage * L0_STAGE_BYTES;
           uint8_t* sB = sI + L0_IMG_BYTES;
-          if (st < nmain) {
+          if (a.debug_mode & 4) {
+            mbar_arrive(&full[stage]);
+          } else if (st < nmain) {
             const int cv = min(CG, g - st * CG);
             mbar_expect_tx(&full[stage], cv * 128 * PP * 2 + L0_NH * L0_DH * 64 * 2);
             for (int cc = 0; cc < cv; ++cc)
@@ -262,7 +432,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
         tc_fence_after();
         if (elect_one()) {
           const uint32_t b_addr = smem_u32(smem + stage * L0_STAGE_BYTES + L0_IMG_BYTES);
-          const int ksteps = st < nmain ? 4 : a.KE / 16;
+          const int ksteps = (a.debug_mode & 2) ? 0 : (st < nmain ? 4 : a.KE / 16);
           for (int h = 0; h < L0_NH; ++h) {
             for (int kk = 0; kk < ksteps; ++kk) {
               const uint64_t bd =
@@ -298,33 +468,40 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
       const long long poff = __ldg(a.node_poff + n);
       const int nmain = (g + CG - 1) / CG;
       const int r = tile * 128 + m;
-      const int s = r % a.S;
+      // p of this (row, head group): channel c at prow + c * pstride, NH heads contiguous
       const __nv_bfloat16* prow =
-          a.p + poff + (a.p_row_mode ? (long long)r * g * a.H : 0) + hg * L0_NH;
-      for (int st = 0; st <= nmain; ++st) {
-        uint32_t pv[CG][2];  // 4 bf16 heads per channel of this stage
-        if (st < nmain) {
+          a.p_row_mode ? a.p + poff + ((long long)(hg * R + r) * g) * L0_NH
+                       : a.p + poff + hg * L0_NH;
+      const int pstride = a.p_row_mode ? L0_NH : a.H;
+      // p prefetch ring: stage st+2 is requested while stage st is built
+      uint32_t pc[CG][2], pn[CG][2], pn2[CG][2];
+      auto load_p = [&](int st, uint32_t (&d)[CG][2]) {
 #pragma unroll
-          for (int cc = 0; cc < CG; ++cc) {
-            const int c = st * CG + cc;
-            if (c < g) {
-              if (L0_NH == 4) {
-                const uint2 q = *reinterpret_cast<const uint2*>(prow + (long long)c * a.H);
-                pv[cc][0] = q.x; pv[cc][1] = q.y;
-              } else {
-                pv[cc][0] = *reinterpret_cast<const uint32_t*>(prow + (long long)c * a.H);
-                pv[cc][1] = 0u;
-              }
+        for (int cc = 0; cc < CG; ++cc) {
+          const int c = st * CG + cc;
+          d[cc][0] = 0u;
+          d[cc][1] = 0u;
+          if (st < nmain && c < g && !(a.debug_mode & 16)) {
+            if (L0_NH == 4) {
+              const uint2 q = __ldg(reinterpret_cast<const uint2*>(prow + (long long)c * pstride));
+              d[cc][0] = q.x; d[cc][1] = q.y;
             } else {
-              pv[cc][0] = 0u; pv[cc][1] = 0u;
+              d[cc][0] = __ldg(reinterpret_cast<const unsigned int*>(prow + (long long)c * pstride));
             }
           }
         }
+      };
+      load_p(0, pc);
+      load_p(1, pn);
+      for (int st = 0; st <= nmain; ++st) {
+        load_p(st + 2, pn2);
         mbar_wait(&full[stage], phase);
         mbar_wait(&aempty[slot], sphase ^ 1);
         tc_fence_after();
         const uint32_t slot_t = tbase + lane_off + L0_ACC_COLS + slot * L0_SLOT_COLS;
-        if (st < nmain) {
+        if (a.debug_mode & 1) {
+          // timing probe: no A construction
+        } else if (st < nmain) {
           uint32_t x[32];
           const uint8_t* sI = smem + stage * L0_STAGE_BYTES;
 #pragma unroll
@@ -352,7 +529,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
             uint32_t y[32];
 #pragma unroll
             for (int cc = 0; cc < CG; ++cc) {
-              const uint32_t w = pv[cc][h >> 1];
+              const uint32_t w = pc[cc][h >> 1];
               const uint32_t ph = (h & 1) ? (w & 0xffff0000u) | (w >> 16)
                                           : (w << 16) | (w & 0xffffu);
 #pragma unroll
@@ -362,7 +539,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
             tmem_st32(slot_t + h * 32, y);
           }
         } else {
-          // ext block: A[r, c] = p[r, c, h], zero-padded to KE
+          // ext block: A[r, c] = p[r, c, h], zero-padded to 64 (MMA reads KE)
 #pragma unroll 1
           for (int h = 0; h < L0_NH; ++h) {
             uint32_t y[32];
@@ -370,8 +547,8 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
             for (int kc = 0; kc < 32; ++kc) {
               float lo = 0.f, hi = 0.f;
               const int c = 2 * kc;
-              if (c < g) lo = __bfloat162float(prow[(long long)c * a.H + h]);
-              if (c + 1 < g) hi = __bfloat162float(prow[(long long)(c + 1) * a.H + h]);
+              if (c < g) lo = __bfloat162float(prow[(long long)c * pstride + h]);
+              if (c + 1 < g) hi = __bfloat162float(prow[(long long)(c + 1) * pstride + h]);
               y[kc] = pack_bf16(lo, hi);
             }
             tmem_st32(slot_t + h * 32, y);
@@ -386,28 +563,32 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
         }
         if (++stage == L0_STAGES) { stage = 0; phase ^= 1; }
         if (++slot == 2) { slot = 0; sphase ^= 1; }
+#pragma unroll
+        for (int cc = 0; cc < CG; ++cc) {
+          pc[cc][0] = pn[cc][0]; pc[cc][1] = pn[cc][1];
+          pn[cc][0] = pn2[cc][0]; pn[cc][1] = pn2[cc][1];
+        }
       }
-      // epilogue: ctx = acc + posV
+      // epilogue: ctx (fp32 TMEM) -> bf16 HBM  (pos term folded into the next K_gemm)
       mbar_wait(accfull, accphase);
       tc_fence_after();
-      const __nv_bfloat16* pv_row = a.posV + ((long long)n * a.S + s) * a.D + hg * L0_NH * L0_DH;
-      __nv_bfloat16* out =
-          a.ctx + ((long long)n * R + r) * a.D + hg * L0_NH * L0_DH;
+      __nv_bfloat16* out = a.ctx + ((long long)n * R + r) * a.D + hg * L0_NH * L0_DH;
 #pragma unroll 1
-      for (int cb = 0; cb < L0_NH * L0_DH; cb += 32) {
+      for (int cb = 0; cb < ((a.debug_mode & 32) ? 0 : L0_NH * L0_DH); cb += 32) {
         uint32_t v[32];
         tmem_ld32(tbase + lane_off + cb, v);
         tmem_ld_wait();
+        if (a.debug_mode & 8) {
+          if (v[0] == 0x7fffffffu && v[31] == 0x7fffffffu) out[cb] = __float2bfloat16(1.f);
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 32; j += 8) {
-          const uint4 q = *reinterpret_cast<const uint4*>(pv_row + cb + j);
-          const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
           uint4 o;
-          uint32_t* oo = reinterpret_cast<uint32_t*>(&o);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            oo[e] = pack_bf16(__uint_as_float(v[j + 2 * e]) + bf16lo(qq[e]),
-                              __uint_as_float(v[j + 2 * e + 1]) + bf16hi(qq[e]));
+          o.x = pack_bf16(__uint_as_float(v[j + 0]), __uint_as_float(v[j + 1]));
+          o.y = pack_bf16(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+          o.z = pack_bf16(__uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
+          o.w = pack_bf16(__uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
           *reinterpret_cast<uint4*>(out + cb + j) = o;
         }
       }

@@ -228,7 +228,7 @@ class DchagFrontEnd(torch.nn.Module):
             plan.append(("dchag_l0_logits", "l0_logits", 2 * 2 * R * G * pp * h,
                          img_bytes + R * G * h * 2))
         plan.append(("dchag_l0_node", "l0_node", 2 * R * d * G * (pp + 1),
-                     img_bytes + R * G * h * 2 + pk.n0 * R * d * 2))
+                     img_bytes + (R * G * h * 2 if pk.attn_l0 else 0) + pk.n0 * R * d * 2))
         depth = len(pk.levels)
         for li in range(depth):
             n_l, N = len(pk.levels[li]), pk.N[li]
@@ -278,7 +278,8 @@ class DchagFrontEnd(torch.nn.Module):
             poff = torch.tensor(poff_list, device=dev, dtype=torch.int64)
             pbuf = torch.empty(acc, **bf16)
             _lib.call("dchag_l0_logits", _lib.ptr(img), isb, isc, B, m.image_h, m.image_w, p,
-                      h, pk.HP, pk.n0, _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g), _lib.ptr(poff),
+                      h, pk.HP, pk.n0, max(pk.l0_g_list), _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g),
+                      _lib.ptr(poff),
                       _lib.ptr(pk.WUt), _lib.ptr(pk.bU), _lib.ptr(pk.posU), _lib.ptr(pbuf), st)
             prow = 1
         else:
@@ -289,7 +290,7 @@ class DchagFrontEnd(torch.nn.Module):
         _lib.call("dchag_l0_node", _lib.ptr(img), isb, isc, B, m.image_h, m.image_w, p, h, d,
                   pk.n0, _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g), _lib.ptr(poff), prow,
                   _lib.ptr(pbuf), _lib.ptr(pk.Mt), pk.C_pad, _lib.ptr(pk.Et), pk.KE,
-                  _lib.ptr(pk.posV), _lib.ptr(ctx), st)
+                  _lib.ptr(ctx), st)
 
         depth = len(pk.levels)
         payload = None
@@ -306,15 +307,17 @@ class DchagFrontEnd(torch.nn.Module):
             else:
                 V = torch.empty(n_l, R, d, **bf16)
                 L = torch.empty(n_l, R, h, **f32) if logits else None
+            # level 0: the positional term (pos @ wv_n) @ Wp enters as a per-row bias
+            rb = pk.rowbias0 if li == 0 else None
             _lib.call("dchag_gemm_bf16", _lib.ptr(ctx), n_l, 1, R, d, R * d, 0, d,
-                      _lib.ptr(pk.Wp[li]), N, N * d, d, _lib.ptr(pk.bp[li]), N, 0, 0, 0, 1,
-                      _lib.ptr(V), 0, R * d, 0, d, _lib.ptr(L), R * h, 0, h, st)
+                      _lib.ptr(pk.Wp[li]), N, N * d, d, _lib.ptr(pk.bp[li]), N, _lib.ptr(rb),
+                      s * N, N, s, _lib.ptr(V), 0, R * d, 0, d, _lib.ptr(L), R * h, 0, h, st)
             if li + 1 < depth:
                 n_next = len(pk.levels[li + 1])
                 ctx = torch.empty(n_next, R, d, **bf16)
                 mix = pk.comb_mix[li]
                 _lib.call("dchag_combine", n_next, R, d, h, _lib.ptr(pk.comb_first[li]),
-                          _lib.ptr(pk.comb_g[li]), _lib.ptr(V), R * d,
+                          _lib.ptr(pk.comb_g[li]), max(pk.levels[li + 1]), _lib.ptr(V), R * d,
                           _lib.ptr(None if mix is not None else L), R * h, _lib.ptr(mix),
                           _lib.ptr(ctx), st)
         return payload
@@ -338,7 +341,7 @@ class DchagFrontEnd(torch.nn.Module):
             ctx_f = torch.empty(1, R, d, **bf16)
             first = self._final_first(dev)
             _lib.call("dchag_combine", 1, R, d, h, _lib.ptr(first[0]), _lib.ptr(first[1]),
-                      _lib.ptr(Vg), pb // 2, _lib.ptr(Lg[R * d // 2:]), pb // 4, 0,
+                      self.tp, _lib.ptr(Vg), pb // 2, _lib.ptr(Lg[R * d // 2:]), pb // 4, 0,
                       _lib.ptr(ctx_f), st)
         else:
             ctx_f = Vg[:R * d].view(1, R, d)  # softmax over one stream is exactly 1
