@@ -323,25 +323,36 @@ constexpr int L0_IMG_BYTES = 16384;                 // 128 rows x 64 K (bf16) pe
 constexpr int L0_B_BYTES = 4 * L0_DH * 64 * 2;  // up to 4 heads x [64 x 64] bf16
 constexpr int L0_STAGE_BYTES = L0_IMG_BYTES + L0_B_BYTES;
 constexpr int L0_SMEM = L0_STAGES * L0_STAGE_BYTES + 1024 + 256;
-constexpr int L0_THREADS = 192;
+constexpr int L0_THREADS = 224;  // producer, gate, 4 builders, image gate
 constexpr uint32_t L0_ACC_COLS = 4 * L0_DH;  // accumulator region (NH * 64 used)
 constexpr uint32_t L0_SLOT_COLS = 4 * 32;    // A slot: 64 bf16 K per head = 32 columns
 
-// NH = heads per CTA (2 or 4): accumulator NH*64 TMEM columns, A slot NH*32 columns
+// NH = heads per CTA (2 or 4): accumulator NH*64 TMEM columns, A slot NH*32 columns.
+//
+// Warp roles (one persistent CTA per SM, a "unit" = (node, 128-row tile, head group)):
+//   warp 0      producer: 1-D bulk copies of the image rows and the pre-tiled B blocks of
+//               every stage (one stage = K 64 per head) into a 4-deep shared-memory ring.
+//   warp 1      control: the only warp that waits on mbarriers (full / A-slot free);
+//               releases the builders with a named barrier (GO), collects them (READY) and
+//               issues the stage's tcgen05.mma (A from TMEM, B from shared memory).
+//   warps 2..5  builders (thread = row = TMEM lane): A = p[r,c,h] * patch_c[r] written to
+//               one of two TMEM slots with tcgen05.st; then the unit's epilogue.
+// Builders never wait on an mbarrier inside the stage loop: an already-completed
+// mbarrier try_wait costs ~157 cycles on B200 against ~20 for bar.sync (tools/sync_probe),
+// and two of them per stage made the first version handshake-bound.
 template <int PP, int L0_NH>
 __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
   constexpr int CG = 64 / PP;        // channels per stage (K = 64 per head per stage)
   constexpr int P = PP == 64 ? 8 : 4;
+  constexpr int NBAR = 160;          // control warp + 4 builder warps
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L0_STAGES * L0_STAGE_BYTES);
   uint64_t* empty = full + L0_STAGES;
-  uint64_t* afull = empty + L0_STAGES;
-  uint64_t* aempty = afull + 2;
+  uint64_t* aempty = empty + L0_STAGES;
   uint64_t* accfull = aempty + 2;
-  uint64_t* accempty = accfull + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(accempty + 1);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(accfull + 1);
 
   const int warp = warp_id(), lane = lane_id();
   const int R = a.B * a.S;
@@ -352,14 +363,11 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < L0_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 5);
+      mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&afull[s], 4);
-      mbar_init(&aempty[s], 1);
-    }
+    mbar_init(&aempty[0], 1);
+    mbar_init(&aempty[1], 1);
     mbar_init(accfull, 1);
-    mbar_init(accempty, 4);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tslot, 512);
@@ -385,7 +393,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
         const __nv_bfloat16* chunk0 =
             a.img + b * a.img_sb + (long long)(s0 / a.wp) * P * a.W;
         for (int st = 0; st <= nmain; ++st) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait(&empty[stage], phase ^ 1);  // MMAs of the stage 4 back are done
           uint8_t* sI = smem + stage * L0_STAGE_BYTES;
           uint8_t* sB = sI + L0_IMG_BYTES;
           if (a.debug_mode & 4) {
@@ -415,49 +423,83 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (A from TMEM)
+    // ------------------------------------------------ control ("gate"): waits + MMA issue
+    // Named barriers (160 threads = this warp + 4 builder warps):
+    //   IMG[k%4]   (ids 1..4) stage k's image/B landed   -> builders precompute A in registers
+    //   SLOT[k%2]  (ids 5..6) stage k's TMEM A slot free  -> builders store A (4 x tcgen05.st)
+    //   READY[k%2] (ids 7..8) stage k's A is in TMEM      -> this warp issues the MMAs
+    // Order per stage k: READY(k) -> issue(k) -> wait slot of k+1 (MMAs of k-1 done) -> SLOT(k+1)
+    // -> wait full(k+2) -> IMG(k+2).  The MMAs of k+1 are then issued while those of k run.
     const uint32_t idesc = idesc_bf16_f32(128, L0_DH);
-    int stage = 0, slot = 0;
-    uint32_t phase = 0, sphase = 0, accphase = 0;
+    // global stage counter q: smem stage q % 4, A slot q % 2 (phase bits derived from q)
+    long long q_total = 0;
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-      const int rest = u / HG;
-      const int n = rest / n_tiles;
+      const int n = (u / HG) / n_tiles;
+      q_total += (__ldg(a.node_g + n) + CG - 1) / CG + 1;
+    }
+    auto slot_free = [&](long long q) {
+      if (q < q_total) {
+        mbar_wait(&aempty[q & 1], (uint32_t)(((q >> 1) & 1) ^ 1));
+        tc_fence_after();
+        asm volatile("bar.arrive %0, %1;" ::"r"(5 + (int)(q & 1)), "r"(NBAR) : "memory");
+      }
+    };
+    slot_free(0);
+    long long q = 0;
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      const int n = (u / HG) / n_tiles;
       const int g = __ldg(a.node_g + n);
       const int nmain = (g + CG - 1) / CG;
-      mbar_wait(accempty, accphase ^ 1);
-      tc_fence_after();
-      for (int st = 0; st <= nmain; ++st) {
-        mbar_wait(&full[stage], phase);
-        mbar_wait(&afull[slot], sphase);
+      for (int st = 0; st <= nmain; ++st, ++q) {
+        const int cs = (int)(q % L0_STAGES), cl = (int)(q & 1);
+        asm volatile("bar.sync %0, %1;" ::"r"(7 + cl), "r"(NBAR) : "memory");  // READY(q)
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t b_addr = smem_u32(smem + stage * L0_STAGE_BYTES + L0_IMG_BYTES);
           const int ksteps = (a.debug_mode & 2) ? 0 : (st < nmain ? 4 : a.KE / 16);
-          for (int h = 0; h < L0_NH; ++h) {
-            for (int kk = 0; kk < ksteps; ++kk) {
-              const uint64_t bd =
-                  smem_desc(b_addr + h * (L0_DH * 64 * 2) + kk * 2048, 1024, 128, 0);
-              const uint32_t at = tbase + L0_ACC_COLS + slot * L0_SLOT_COLS + h * 32 + kk * 8;
-              mma_ts(tbase + h * L0_DH, at, bd, idesc, (st | kk) != 0);
-            }
+          const uint64_t bd0 =
+              smem_desc(smem_u32(smem + cs * L0_STAGE_BYTES + L0_IMG_BYTES), 1024, 128, 0);
+          const uint32_t at0 = tbase + L0_ACC_COLS + cl * L0_SLOT_COLS;
+          if (ksteps == 4) {
+#pragma unroll
+            for (int h = 0; h < L0_NH; ++h)
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_ts(tbase + h * L0_DH, at0 + h * 32 + kk * 8,
+                       bd0 + (uint64_t)((h * (L0_DH * 64 * 2) + kk * 2048) >> 4), idesc,
+                       (st | kk) != 0);
+          } else {
+            for (int h = 0; h < L0_NH; ++h)
+              for (int kk = 0; kk < ksteps; ++kk)
+                mma_ts(tbase + h * L0_DH, at0 + h * 32 + kk * 8,
+                       bd0 + (uint64_t)((h * (L0_DH * 64 * 2) + kk * 2048) >> 4), idesc,
+                       (st | kk) != 0);
           }
-          mma_commit(&empty[stage]);
-          mma_commit(&aempty[slot]);
+          mma_commit(&empty[cs]);
+          mma_commit(&aempty[cl]);
           if (st == nmain) mma_commit(accfull);
         }
         __syncwarp();
-        if (++stage == L0_STAGES) { stage = 0; phase ^= 1; }
-        if (++slot == 2) { slot = 0; sphase ^= 1; }
+        slot_free(q + 1);
       }
-      accphase ^= 1;
+    }
+  } else if (warp == 6) {
+    // ------------------------------------------------ image gate: full(q) -> IMG(q)
+    long long q_total = 0;
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      const int n = (u / HG) / n_tiles;
+      q_total += (__ldg(a.node_g + n) + CG - 1) / CG + 1;
+    }
+    for (long long q = 0; q < q_total; ++q) {
+      mbar_wait(&full[q % L0_STAGES], (uint32_t)((q / L0_STAGES) & 1));
+      asm volatile("bar.arrive %0, %1;" ::"r"(1 + (int)(q & 3)), "r"(NBAR) : "memory");
     }
   } else {
-    // ------------------------------------------------ A builders + epilogue (warps 2..5)
+    // ------------------------------------------------ builders + epilogue (warps 2..5)
     const int quarter = warp & 3;
     const int m = quarter * 32 + lane;  // row within tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    int stage = 0, slot = 0;
-    uint32_t phase = 0, sphase = 0, accphase = 0;
+    uint32_t accphase = 0;
+    long long q = 0;
     const int i_l = m / a.wp, jj = m - (m / a.wp) * a.wp;
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
       const int hg = u % HG;
@@ -473,8 +515,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
           a.p_row_mode ? a.p + poff + ((long long)(hg * R + r) * g) * L0_NH
                        : a.p + poff + hg * L0_NH;
       const int pstride = a.p_row_mode ? L0_NH : a.H;
-      // p prefetch ring: stage st+2 is requested while stage st is built
-      uint32_t pc[CG][2], pn[CG][2], pn2[CG][2];
+      uint32_t pc[CG][2], pn[CG][2];
       auto load_p = [&](int st, uint32_t (&d)[CG][2]) {
 #pragma unroll
         for (int cc = 0; cc < CG; ++cc) {
@@ -483,8 +524,8 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
           d[cc][1] = 0u;
           if (st < nmain && c < g && !(a.debug_mode & 16)) {
             if (L0_NH == 4) {
-              const uint2 q = __ldg(reinterpret_cast<const uint2*>(prow + (long long)c * pstride));
-              d[cc][0] = q.x; d[cc][1] = q.y;
+              const uint2 v = __ldg(reinterpret_cast<const uint2*>(prow + (long long)c * pstride));
+              d[cc][0] = v.x; d[cc][1] = v.y;
             } else {
               d[cc][0] = __ldg(reinterpret_cast<const unsigned int*>(prow + (long long)c * pstride));
             }
@@ -492,18 +533,19 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
         }
       };
       load_p(0, pc);
-      load_p(1, pn);
-      for (int st = 0; st <= nmain; ++st) {
-        load_p(st + 2, pn2);
-        mbar_wait(&full[stage], phase);
-        mbar_wait(&aempty[slot], sphase ^ 1);
-        tc_fence_after();
-        const uint32_t slot_t = tbase + lane_off + L0_ACC_COLS + slot * L0_SLOT_COLS;
+      for (int st = 0; st <= nmain; ++st, ++q) {
+        load_p(st + 1, pn);
+        const int cs = (int)(q % L0_STAGES), cl = (int)(q & 1);
+        uint32_t y[L0_NH][32];
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(q & 3)), "r"(NBAR) : "memory");  // IMG
         if (a.debug_mode & 1) {
-          // timing probe: no A construction
+#pragma unroll
+          for (int h = 0; h < L0_NH; ++h)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) y[h][e] = 0u;
         } else if (st < nmain) {
           uint32_t x[32];
-          const uint8_t* sI = smem + stage * L0_STAGE_BYTES;
+          const uint8_t* sI = smem + cs * L0_STAGE_BYTES;
 #pragma unroll
           for (int cc = 0; cc < CG; ++cc) {
             const bool valid = st * CG + cc < g;
@@ -513,20 +555,19 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
 #pragma unroll
             for (int py = 0; py < P; ++py) {
               if (P == 8) {
-                uint4 q = valid ? *reinterpret_cast<const uint4*>(base + py * a.W)
+                uint4 v = valid ? *reinterpret_cast<const uint4*>(base + py * a.W)
                                 : make_uint4(0, 0, 0, 0);
-                x[cc * 32 + py * 4 + 0] = q.x; x[cc * 32 + py * 4 + 1] = q.y;
-                x[cc * 32 + py * 4 + 2] = q.z; x[cc * 32 + py * 4 + 3] = q.w;
+                x[cc * 32 + py * 4 + 0] = v.x; x[cc * 32 + py * 4 + 1] = v.y;
+                x[cc * 32 + py * 4 + 2] = v.z; x[cc * 32 + py * 4 + 3] = v.w;
               } else {
-                uint2 q = valid ? *reinterpret_cast<const uint2*>(base + py * a.W)
+                uint2 v = valid ? *reinterpret_cast<const uint2*>(base + py * a.W)
                                 : make_uint2(0, 0);
-                x[cc * 8 + py * 2 + 0] = q.x; x[cc * 8 + py * 2 + 1] = q.y;
+                x[cc * 8 + py * 2 + 0] = v.x; x[cc * 8 + py * 2 + 1] = v.y;
               }
             }
           }
 #pragma unroll
           for (int h = 0; h < L0_NH; ++h) {
-            uint32_t y[32];
 #pragma unroll
             for (int cc = 0; cc < CG; ++cc) {
               const uint32_t w = pc[cc][h >> 1];
@@ -534,40 +575,48 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
                                           : (w << 16) | (w & 0xffffu);
 #pragma unroll
               for (int e = 0; e < 32 / CG; ++e)
-                y[cc * (32 / CG) + e] = mul_bf16x2(x[cc * (32 / CG) + e], ph);
+                y[h][cc * (32 / CG) + e] = mul_bf16x2(x[cc * (32 / CG) + e], ph);
             }
-            tmem_st32(slot_t + h * 32, y);
           }
         } else {
-          // ext block: A[r, c] = p[r, c, h], zero-padded to 64 (MMA reads KE)
-#pragma unroll 1
-          for (int h = 0; h < L0_NH; ++h) {
-            uint32_t y[32];
-#pragma unroll
-            for (int kc = 0; kc < 32; ++kc) {
-              float lo = 0.f, hi = 0.f;
-              const int c = 2 * kc;
-              if (c < g) lo = __bfloat162float(prow[(long long)c * pstride + h]);
-              if (c + 1 < g) hi = __bfloat162float(prow[(long long)(c + 1) * pstride + h]);
-              y[kc] = pack_bf16(lo, hi);
+          // ext block: A[r, c] = p[r, c, h], zero-padded to 64 (the MMA reads KE)
+          for (int kc = 0; kc < 32; ++kc) {
+            const int c = 2 * kc;
+            uint32_t lo[2] = {0u, 0u}, hi[2] = {0u, 0u};
+            if (c < g) {
+              if (L0_NH == 4) {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(prow + (long long)c * pstride));
+                lo[0] = v.x; lo[1] = v.y;
+              } else {
+                lo[0] = __ldg(reinterpret_cast<const unsigned int*>(prow + (long long)c * pstride));
+              }
             }
-            tmem_st32(slot_t + h * 32, y);
+            if (c + 1 < g) {
+              if (L0_NH == 4) {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(prow + (long long)(c + 1) * pstride));
+                hi[0] = v.x; hi[1] = v.y;
+              } else {
+                hi[0] = __ldg(reinterpret_cast<const unsigned int*>(prow + (long long)(c + 1) * pstride));
+              }
+            }
+#pragma unroll
+            for (int h = 0; h < L0_NH; ++h) {
+              const uint32_t a16 = (h & 1) ? (lo[h >> 1] >> 16) : (lo[h >> 1] & 0xffffu);
+              const uint32_t b16 = (h & 1) ? (hi[h >> 1] >> 16) : (hi[h >> 1] & 0xffffu);
+              y[h][kc] = a16 | (b16 << 16);
+            }
           }
         }
+        asm volatile("bar.sync %0, %1;" ::"r"(5 + cl), "r"(NBAR) : "memory");  // SLOT free
+        tc_fence_after();
+        const uint32_t slot_t = tbase + lane_off + L0_ACC_COLS + cl * L0_SLOT_COLS;
+#pragma unroll
+        for (int h = 0; h < L0_NH; ++h) tmem_st32(slot_t + h * 32, y[h]);
         tmem_st_wait();
         tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&afull[slot]);
-          mbar_arrive(&empty[stage]);
-        }
-        if (++stage == L0_STAGES) { stage = 0; phase ^= 1; }
-        if (++slot == 2) { slot = 0; sphase ^= 1; }
+        asm volatile("bar.arrive %0, %1;" ::"r"(7 + cl), "r"(NBAR) : "memory");  // READY
 #pragma unroll
-        for (int cc = 0; cc < CG; ++cc) {
-          pc[cc][0] = pn[cc][0]; pc[cc][1] = pn[cc][1];
-          pn[cc][0] = pn2[cc][0]; pn[cc][1] = pn2[cc][1];
-        }
+        for (int cc = 0; cc < CG; ++cc) { pc[cc][0] = pn[cc][0]; pc[cc][1] = pn[cc][1]; }
       }
       // epilogue: ctx (fp32 TMEM) -> bf16 HBM  (pos term folded into the next K_gemm)
       mbar_wait(accfull, accphase);
@@ -592,9 +641,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
           *reinterpret_cast<uint4*>(out + cb + j) = o;
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(accempty);
+      tc_fence_before();  // acc reads precede the next unit's first MMA (via READY)
       accphase ^= 1;
     }
   }
