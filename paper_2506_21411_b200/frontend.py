@@ -27,6 +27,7 @@ from . import _lib
 from .config import (ConfigError, ModelConfig, StrategyConfig, TreeSpec, build_tree_spec,
                      channel_slabs, max_group_for_depth)
 from .fold import fold_rank, pack_rank
+from .payload import payload_nbytes, views
 
 
 def frontend_param_specs(model: ModelConfig, strategy: StrategyConfig):
@@ -299,11 +300,10 @@ class DchagFrontEnd(torch.nn.Module):
             N = pk.N[li]
             logits = N > d
             if li == depth - 1:
-                # root: write straight into the gather payload [V bf16 R*D | L fp32 R*H]
-                nbytes = R * d * 2 + R * h * 4
-                payload = torch.empty(nbytes, device=dev, dtype=torch.uint8)
-                V = payload[:R * d * 2].view(torch.bfloat16).view(1, R, d)
-                L = payload[R * d * 2:].view(torch.float32).view(1, R, h)
+                # root: write straight into the gather payload (payload.py layout)
+                payload = torch.empty(payload_nbytes(R, d, h), device=dev, dtype=torch.uint8)
+                V, L = views(payload, R, d, h)
+                V, L = V.view(1, R, d), L.view(1, R, h)
             else:
                 V = torch.empty(n_l, R, d, **bf16)
                 L = torch.empty(n_l, R, h, **f32) if logits else None
@@ -332,7 +332,7 @@ class DchagFrontEnd(torch.nn.Module):
         st = _lib.stream_handle()
         bf16 = dict(device=dev, dtype=torch.bfloat16)
         pb = gathered.numel() // self.tp
-        if pb != R * d * 2 + R * h * 4:
+        if pb != payload_nbytes(R, d, h):
             raise ConfigError(f"gathered payload of {gathered.numel()} bytes does not match "
                               f"tp={self.tp}, B={B}")
         Vg = gathered.view(torch.bfloat16)

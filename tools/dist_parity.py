@@ -1,0 +1,64 @@
+"""Multi-GPU parity: torchrun --nproc-per-node N tools/dist_parity.py
+Every rank runs its channel slab (tp = N, balanced slabs), the root payloads are
+all-gathered over NCCL in rank order, the shared final layer runs on every rank, and
+each rank's output is compared with the CPU oracle (oracle/ is the checker only)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import dchag_oracle as O  # noqa: E402
+from paper_2506_21411_b200 import DchagFrontEnd  # noqa: E402
+
+CASES = [
+    dict(channels=22, image_h=64, image_w=128, patch=8, embed=256, heads=4, max_group=3),
+    dict(channels=37, image_h=64, image_w=64, patch=4, embed=128, heads=2, max_group=4),
+    dict(channels=40, image_h=64, image_w=128, patch=8, embed=256, heads=4, max_group=4,
+         layer_kind="linear"),
+]
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    tp, rank = dist.get_world_size(), dist.get_rank()
+    worst = 0.0
+    for meta in CASES:
+        lk = meta.get("layer_kind", "cross_attention")
+        specs = O.frontend_param_specs(meta["channels"], meta["image_h"], meta["image_w"],
+                                       meta["patch"], meta["embed"], tp, meta["max_group"],
+                                       layer_kind=lk)
+        w = O.random_params(specs, seed=7, std=0.05, bias_std=0.02)
+        w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
+        img = np.random.default_rng(3).standard_normal(
+            (2, meta["channels"], meta["image_h"], meta["image_w"]))
+        img_bf = torch.from_numpy(img.astype(np.float32)).to(torch.bfloat16)
+        fe = DchagFrontEnd(meta["channels"], meta["image_h"], meta["image_w"], meta["patch"],
+                           meta["embed"], meta["heads"], max_group=meta["max_group"],
+                           agg_layer_kind=lk, tp=tp, rank=rank, out_dtype=torch.float32)
+        fe.load_weights(w)
+        out = fe(img_bf.cuda()).cpu().numpy()  # full images: the rank slices its own slab
+        want = O.dchag_frontend(img_bf.float().numpy().astype(np.float64), w,
+                                patch=meta["patch"], heads=meta["heads"], tp=tp,
+                                max_group=meta["max_group"], layer_kind=lk)
+        err = O.rel_err(out, want)
+        worst = max(worst, err)
+        print(f"rank {rank}/{tp} C={meta['channels']} slab={fe.slab} {lk}: rel_err={err:.3e}",
+              flush=True)
+    t = torch.tensor([worst], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(f"DIST_PARITY tp={tp} worst rel_err={float(t):.3e} -> "
+              f"{'PASS' if float(t) < 2e-2 else 'FAIL'}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if float(t) < 2e-2 else 1)
+
+
+if __name__ == "__main__":
+    main()
