@@ -49,8 +49,9 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
  * img_sb and channel stride img_sc (slab channel c at img + c*img_sc).
  * node_c0/node_g (int32) and node_poff (int64) are device arrays of n_nodes; gmax >= all node_g.
  * WUt bf16 [C][HP][P*P], bU fp32 [C][HP], posU fp32 [n_nodes][S][HP]; HP = H rounded up
- * to a multiple of 8.  Output p bf16, head-group major (the K_l0 CTA's slice is
- * contiguous): p[poff[n] + ((hg*R + r)*g + c)*NH + h%NH], hg = h/NH, NH = 4 if H%4==0 else 2. */
+ * to a multiple of 8.  Output p bf16, head-group then channel major (a 128-row tile's
+ * slice for one (head group, channel) is contiguous, so K_l0 stages it with one bulk copy):
+ * p[poff[n] + ((hg*g + c)*R + r)*NH + h%NH], hg = h/NH, NH = 4 if H%4==0 else 2. */
 int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
                     int P, int H, int HP, int n_nodes, int gmax, const int* node_c0,
                     const int* node_g,
@@ -78,6 +79,14 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
 int dchag_combine(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
                   int max_g, const void* V, long long sVj, const float* L, long long sLj,
                   const float* mix, void* ctx, void* stream);
+
+/* Same, with child rows interleaved: row r = rb*rows_inner + rs lives at
+ * V + j*sVj + rb*sVb + rs*D (L: L + j*sLj + rb*sLb + rs*H) -- e.g. tokens [B][C][S][D]
+ * (tree_aggregate on tokens, model.py:76-97). */
+int dchag_combine_strided(int n_nodes, int R, int D, int H, const int* node_first,
+                          const int* node_g, int max_g, const void* V, long long sVj,
+                          long long sVb, const float* L, long long sLj, long long sLb,
+                          int rows_inner, const float* mix, void* ctx, void* stream);
 
 /* unfold_patches (tensor.py:303-323): img [B][C][Himg][W] -> out [B][C][S][P*P] bf16. */
 int dchag_unfold(const void* img, long long img_sb, long long img_sc, int B, int C, int Himg,

@@ -116,9 +116,20 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
   if ((sAmi * 2) % 16 || (sAmo * 2) % 16 || (sAg * 2) % 16 || (sWg * 2) % 16)
     return fail(DCHAG_ERR_SHAPE, "gemm: strides must be multiples of 16 bytes");
   const int bk = (K % 64 == 0) ? 64 : (K % 32 == 0 ? 32 : 16);
-  const int ntn = (N + 255) / 256;
-  int bn = (N + ntn - 1) / ntn;
-  bn = (bn + 15) / 16 * 16;
+  // N tiling: <= 256 columns per tile; prefer an even tile count (enables the N-pair cluster)
+  int ntn = (N + 255) / 256;
+  int bn = ((N + ntn - 1) / ntn + 15) / 16 * 16;
+  if (ntn > 1 && ntn % 2) {
+    const int bn2 = ((N + ntn) / (ntn + 1) + 15) / 16 * 16;
+    if ((long long)bn2 * (ntn + 1) <= (long long)N * 105 / 100) { ++ntn; bn = bn2; }
+  }
+  const int ntm = Mo * Mi / 128;
+  // clusters (TMA multicast) only on the K-64 path and when the tile grid divides evenly
+  int cm = 1, cn = 1;  // clusters measured no faster on B200; opt-in for probes
+  if (const char* f = getenv("DCHAG_GEMM_CLUSTER")) {  // experiment override, e.g. "21"
+    if (f[0] == '2' && bk == 64 && ntm % 2 == 0 && (bn / 2) % 8 == 0) cm = 2;
+    if (f[0] && f[1] == '2' && bk == 64 && ((N + bn - 1) / bn) % 2 == 0) cn = 2;
+  }
   const CUtensorMapSwizzle swz = bk == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
                                  : bk == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
                                             : CU_TENSOR_MAP_SWIZZLE_32B;
@@ -126,20 +137,22 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
   {
     cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)Mi, (cuuint64_t)Mo, (cuuint64_t)G};
     cuuint64_t str[3] = {(cuuint64_t)sAmi * 2, (cuuint64_t)sAmo * 2, (cuuint64_t)sAg * 2};
-    cuuint32_t box[4] = {(cuuint32_t)bk, 128, 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)bk, (cuuint32_t)(128 / cn), 1, 1};
     int rc = make_map(&tA, A, 4, dims, str, box, swz);
     if (rc) return rc;
   }
   {
     cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)N, (cuuint64_t)G};
     cuuint64_t str[2] = {(cuuint64_t)K * 2, (cuuint64_t)sWg * 2};
-    cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)bn, 1};
+    cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)(bn / cm), 1};
     int rc = make_map(&tW, W, 3, dims, str, box, swz);
     if (rc) return rc;
   }
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.G = G; a.M = Mo * Mi; a.Mi = Mi; a.N = N; a.Nv = Nv; a.K = K; a.BN = bn;
+  a.cm = cm; a.cn = cn;
+  a.debug = getenv("DCHAG_GEMM_DEBUG") ? atoi(getenv("DCHAG_GEMM_DEBUG")) : 0;
   a.bias = bias; a.bias_g = bias_g;
   a.rowbias = reinterpret_cast<const __nv_bfloat16*>(rowbias);
   a.rowbias_g = rowbias_g; a.rowbias_row = rowbias_row;
@@ -161,7 +174,6 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
   a.img_sb = img_sb; a.img_sc = img_sc;
   a.B = B; a.S = (Himg / P) * (W / P); a.W = W; a.P = P; a.wp = W / P; a.H = H; a.HP = HP;
   a.n_nodes = n_nodes; a.gmax = gmax;
-  a.p0_smem = getenv("DCHAG_P0_SMEM") ? atoi(getenv("DCHAG_P0_SMEM")) : 0;
   a.node_c0 = node_c0; a.node_g = node_g; a.node_poff = node_poff;
   a.WUt = reinterpret_cast<const __nv_bfloat16*>(WUt);
   a.bU = bU; a.posU = posU;
@@ -190,6 +202,8 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
   {
     const char* dbg = getenv("DCHAG_L0_DEBUG");
     a.debug_mode = dbg ? atoi(dbg) : 0;
+    const char* tr = getenv("DCHAG_L0_TRACE_PTR");
+    a.trace = tr ? reinterpret_cast<long long*>(strtoull(tr, nullptr, 0)) : nullptr;
   }
   if ((reinterpret_cast<uintptr_t>(img) | (uintptr_t)(img_sb * 2) | (uintptr_t)(img_sc * 2)) % 16)
     return fail(DCHAG_ERR_SHAPE, "l0_node: image base/strides must be 16-byte aligned");
@@ -199,9 +213,19 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
 int dchag_combine(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
                   int max_g, const void* V, long long sVj, const float* L, long long sLj,
                   const float* mix, void* ctx, void* stream) {
+  return dchag_combine_strided(n_nodes, R, D, H, node_first, node_g, max_g, V, sVj, 0, L, sLj,
+                               0, R, mix, ctx, stream);
+}
+
+int dchag_combine_strided(int n_nodes, int R, int D, int H, const int* node_first,
+                          const int* node_g, int max_g, const void* V, long long sVj,
+                          long long sVb, const float* L, long long sLj, long long sLb,
+                          int rows_inner, const float* mix, void* ctx, void* stream) {
   if (!mix && !L) return fail(DCHAG_ERR_SHAPE, "combine: need logits or mix");
+  if (rows_inner < 1) return fail(DCHAG_ERR_SHAPE, "combine: rows_inner must be >= 1");
   CombineArgs a;
   a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H; a.max_g = max_g;
+  a.rows_inner = rows_inner; a.sVb = sVb; a.sLb = sLb;
   a.node_first = node_first; a.node_g = node_g;
   a.V = reinterpret_cast<const __nv_bfloat16*>(V); a.sVj = sVj;
   a.L = L; a.sLj = sLj; a.mix = mix;

@@ -27,11 +27,14 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
   if (n >= a.n_nodes) return;
   const int first = __ldg(a.node_first + n), g = __ldg(a.node_g + n);
   const int H = a.H, dh = a.D / H;
+  // row r = (rb, rs) with rs < rows_inner: child rows may be interleaved with other channels
+  const int rb = r / a.rows_inner, rs = r - rb * a.rows_inner;
   float* p = sp[warp];
   if (a.mix) {
     for (int j = lane; j < g; j += 32) p[j] = __ldg(a.mix + first + j);
   } else if (lane < H) {
-    const float* lr = a.L + (long long)first * a.sLj + (long long)r * H + lane;
+    const float* lr = a.L + (long long)first * a.sLj + (long long)rb * a.sLb +
+                      (long long)rs * H + lane;
     float m = -INFINITY;
     for (int j = 0; j < g; ++j) m = fmaxf(m, __ldg(lr + (long long)j * a.sLj));
     float ssum = 0.f;
@@ -50,7 +53,8 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
   for (int q = 0; q < 8; ++q)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[q][e] = 0.f;
-  const __nv_bfloat16* vbase = a.V + (long long)first * a.sVj + (long long)r * a.D;
+  const __nv_bfloat16* vbase =
+      a.V + (long long)first * a.sVj + (long long)rb * a.sVb + (long long)rs * a.D;
   const int per_lane = (nchunk + 31) / 32;
   for (int j = 0; j < g; ++j) {
     const __nv_bfloat16* vrow = vbase + (long long)j * a.sVj;

@@ -10,6 +10,8 @@ namespace dchag {
 
 struct GemmArgs {
   int G, M, Mi, N, Nv, K, BN;   // M = Mo * Mi rows per group
+  int debug;                    // timing probes (DCHAG_GEMM_DEBUG)
+  int cm, cn;                   // cluster shape (TMA boxes are built with 128/cn, BN/cm rows)
   const float* bias;            // [G][bias_g] fp32 or null
   long long bias_g;
   const __nv_bfloat16* rowbias; // [G][rowbias_g] with row (mi % period) * rowbias_row, or null
@@ -31,15 +33,15 @@ struct L0LogitArgs {
   long long img_sb, img_sc;
   int B, S, W, P, wp, H, HP;  // H heads, HP = H padded to a multiple of 8
   int n_nodes, gmax;          // gmax >= every node_g (host-known)
-  int p0_smem;                // use the shared-memory staged variant
   const int* node_c0;         // first slab channel of node n
   const int* node_g;          // channel count of node n
   const long long* node_poff; // element offset of node n in p
   const __nv_bfloat16* WUt;   // [C][HP][PP]  logit weights tok.w[c] @ U_n, transposed
   const float* bU;            // [C][HP]      (tok.b[c]+chan_id[c]) @ U_n
   const float* posU;          // [n_nodes][S][HP]
-  __nv_bfloat16* p;           // p[poff[n] + ((hg*R + r)*g + c)*NH + h%NH], hg = h/NH,
-                              // NH = 4 if H % 4 == 0 else 2 (head group of one K_l0 CTA)
+  __nv_bfloat16* p;           // p[poff[n] + ((hg*g + c)*R + r)*NH + h%NH], hg = h/NH,
+                              // NH = 4 if H % 4 == 0 else 2 (head group of one K_l0 CTA);
+                              // a 128-row tile's slice of (hg, c) is one contiguous 1 KB run
 };
 cudaError_t launch_l0_logits(const L0LogitArgs& a, cudaStream_t st);
 
@@ -60,6 +62,7 @@ struct L0NodeArgs {
   int KE;
   __nv_bfloat16* ctx;          // [n_nodes][R][D]
   int debug_mode;              // timing probes: 0 normal, 1 no A build, 2 no MMA
+  long long* trace;            // optional [8][256] clock64 timeline of CTA 0 (debug)
 };
 cudaError_t launch_l0_node(const L0NodeArgs& a, int num_sms, cudaStream_t st);
 
@@ -73,6 +76,8 @@ struct CombineArgs {
   const float* L;              // child j logits at L + j*sLj + r*H (attention mode)
   long long sLj;
   const float* mix;            // linear mode: p_j = mix[node_first[n] + j] (L ignored)
+  int rows_inner;              // row r = rb * rows_inner + rs; child row offset
+  long long sVb, sLb;          //   = j*sVj + rb*sVb + rs*D   (L: j*sLj + rb*sLb + rs*H)
   __nv_bfloat16* ctx;          // [n][R][D]
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(128) l0_logits_kernel(L0LogitArgs a) {
           const float p1 = __expf(L[nt][2 * q + 1] - mx[nt][2 * q + 1]) * sm[nt][2 * q + 1];
           const int nh = (a.H % 4 == 0) ? 4 : 2;
           const int hg = h / nh, hl = h - hg * nh;
-          __nv_bfloat16* dst = a.p + poff + (((long long)hg * R + rows[q]) * g + c) * nh + hl;
+          __nv_bfloat16* dst = a.p + poff + (((long long)hg * g + c) * R + rows[q]) * nh + hl;
           *reinterpret_cast<uint32_t*>(dst) = pack_bf16(p0, p1);
         }
       }
@@ -143,166 +143,8 @@ __global__ void __launch_bounds__(128) l0_logits_kernel(L0LogitArgs a) {
   }
 }
 
-// K_p0 v2: the CTA stages every image row it needs (TR positions x g channels) in shared
-// memory with 1-D bulk copies, recomputes the logits from shared memory in a second pass
-// (mma.sync is cheap next to the HBM read), and writes p through a shared staging tile so
-// the global stores are contiguous 16-byte vectors.
-template <int NT, int TR>
-__global__ void __launch_bounds__(TR * 2) l0_logits_smem_kernel(L0LogitArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
-                                             ~uintptr_t(127));
-  const int R = a.B * a.S;
-  const int blocks_per_node = R / TR;
-  const int n = blockIdx.x / blocks_per_node;
-  const int rblk = blockIdx.x - n * blocks_per_node;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int PP = a.P * a.P;
-  const int c0 = __ldg(a.node_c0 + n), g = __ldg(a.node_g + n);
-  const long long poff = __ldg(a.node_poff + n);
-  const int nh = (a.H % 4 == 0) ? 4 : 2;
-  const int r0 = rblk * TR;
-  const int b = r0 / a.S, s0 = r0 - b * a.S;
-  const int chunk = TR * PP;  // elements per channel
-  __nv_bfloat16* simg = reinterpret_cast<__nv_bfloat16*>(smem);
-  __nv_bfloat16* sp = simg + (size_t)g * chunk;                 // [hg][TR][g][nh]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sp + (size_t)TR * g * a.H + 64);
-  bar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bar) + 7) & ~uintptr_t(7));
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(bar, (uint32_t)(g * chunk * 2));
-    const __nv_bfloat16* src = a.img + b * a.img_sb + (long long)(s0 / a.wp) * a.P * a.W;
-    for (int c = 0; c < g; ++c)
-      bulk_load(simg + (size_t)c * chunk, src + (long long)(c0 + c) * a.img_sc, chunk * 2, bar);
-  }
-  const int rl[2] = {warp * 16 + gid, warp * 16 + gid + 8};  // rows within the tile
-  int rowoff[2];
-  float pu[NT][4];
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int m = rl[q];
-    const int i = m / a.wp, j = m - i * a.wp;
-    rowoff[q] = i * a.P * a.W + j * a.P;
-  }
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const float* pr0 = a.posU + ((long long)n * a.S + s0 + rl[0]) * a.HP + nt * 8 + 2 * tig;
-    const float* pr1 = a.posU + ((long long)n * a.S + s0 + rl[1]) * a.HP + nt * 8 + 2 * tig;
-    pu[nt][0] = pr0[0]; pu[nt][1] = pr0[1];
-    pu[nt][2] = pr1[0]; pu[nt][3] = pr1[1];
-  }
-  mbar_wait(bar, 0);
-
-  auto logits = [&](int c, float (&L)[NT][4]) {
-    const __nv_bfloat16* cimg = simg + (size_t)c * chunk;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const float* bu = a.bU + (long long)(c0 + c) * a.HP + nt * 8 + 2 * tig;
-      const float b0 = __ldg(bu), b1 = __ldg(bu + 1);
-      L[nt][0] = pu[nt][0] + b0;
-      L[nt][1] = pu[nt][1] + b1;
-      L[nt][2] = pu[nt][2] + b0;
-      L[nt][3] = pu[nt][3] + b1;
-    }
-    for (int ks = 0; ks < PP / 16; ++ks) {
-      uint32_t af[4];
-#pragma unroll
-      for (int hk = 0; hk < 2; ++hk) {
-        const int k = ks * 16 + hk * 8 + 2 * tig;
-        const int py = k / a.P, px = k - py * a.P;
-        const int off = py * a.W + px;
-        af[hk * 2 + 0] = *reinterpret_cast<const uint32_t*>(cimg + rowoff[0] + off);
-        af[hk * 2 + 1] = *reinterpret_cast<const uint32_t*>(cimg + rowoff[1] + off);
-      }
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const __nv_bfloat16* wb = a.WUt + ((long long)(c0 + c) * a.HP + nt * 8 + gid) * PP +
-                                  ks * 16 + 2 * tig;
-        const uint32_t b0 = __ldg(reinterpret_cast<const unsigned int*>(wb));
-        const uint32_t b1 = __ldg(reinterpret_cast<const unsigned int*>(wb + 8));
-        mma_bf16_16816(L[nt], af, b0, b1);
-      }
-    }
-  };
-
-  float mx[NT][4], sm[NT][4];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) { mx[nt][e] = -INFINITY; sm[nt][e] = 0.f; }
-  for (int c = 0; c < g; ++c) {
-    float L[NT][4];
-    logits(c, L);
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float m2 = fmaxf(mx[nt][e], L[nt][e]);
-        sm[nt][e] = sm[nt][e] * __expf(mx[nt][e] - m2) + __expf(L[nt][e] - m2);
-        mx[nt][e] = m2;
-      }
-  }
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) sm[nt][e] = 1.f / sm[nt][e];
-  for (int c = 0; c < g; ++c) {
-    float L[NT][4];
-    logits(c, L);
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int h = nt * 8 + 2 * tig;
-      if (h < a.H) {
-        const int hg = h / nh, hl = h - hg * nh;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const float p0 = __expf(L[nt][2 * q] - mx[nt][2 * q]) * sm[nt][2 * q];
-          const float p1 = __expf(L[nt][2 * q + 1] - mx[nt][2 * q + 1]) * sm[nt][2 * q + 1];
-          *reinterpret_cast<uint32_t*>(sp + (((size_t)hg * TR + rl[q]) * g + c) * nh + hl) =
-              pack_bf16(p0, p1);
-        }
-      }
-    }
-  }
-  __syncthreads();
-  // copy out: per head group a contiguous run of TR*g*nh bf16
-  const int run = TR * g * nh;  // elements, multiple of 8
-  for (int hg = 0; hg < a.H / nh; ++hg) {
-    const uint4* src = reinterpret_cast<const uint4*>(sp + (size_t)hg * run);
-    uint4* dst = reinterpret_cast<uint4*>(a.p + poff + ((long long)hg * R + r0) * g * nh);
-    for (int i = threadIdx.x; i < run / 8; i += blockDim.x) dst[i] = src[i];
-  }
-}
-
 cudaError_t launch_l0_logits(const L0LogitArgs& a, cudaStream_t st) {
   const int R = a.B * a.S;
-  const int PP = a.P * a.P;
-  // fast path: shared-memory staged (needs whole patch rows per tile and g*PP*TR*2 <= 128 KB;
-  // the node sizes are not known here, so the caller passes them bounded via H*?: use gmax)
-  const int TR = (32 % a.wp == 0) ? 32 : ((64 % a.wp == 0) ? 64 : 0);
-  if (a.p0_smem && TR && a.S % TR == 0 && a.gmax > 0 &&
-      (long long)a.gmax * PP * TR * 2 + (long long)TR * a.gmax * a.H * 2 <= 200000 &&
-      (TR * a.gmax * (a.H % 4 == 0 ? 4 : 2)) % 8 == 0) {
-    const int smem = a.gmax * PP * TR * 2 + TR * a.gmax * a.H * 2 + 64 * 2 + 256;
-    const int grid = a.n_nodes * (R / TR);
-    void (*k)(L0LogitArgs) = nullptr;
-    const int nt = a.HP / 8;
-    if (TR == 32) k = nt == 1 ? l0_logits_smem_kernel<1, 32> : nt == 2 ? l0_logits_smem_kernel<2, 32>
-                                                              : nt == 4 ? l0_logits_smem_kernel<4, 32> : nullptr;
-    else k = nt == 1 ? l0_logits_smem_kernel<1, 64> : nt == 2 ? l0_logits_smem_kernel<2, 64>
-                                                     : nt == 4 ? l0_logits_smem_kernel<4, 64> : nullptr;
-    if (k) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      k<<<grid, TR * 2, smem, st>>>(a);
-      return cudaGetLastError();
-    }
-  }
   if (R % 64) return cudaErrorInvalidValue;
   const int grid = a.n_nodes * (R / 64);
   void (*k)(L0LogitArgs) = nullptr;
@@ -317,38 +159,48 @@ cudaError_t launch_l0_logits(const L0LogitArgs& a, cudaStream_t st) {
 }
 
 // =====================================================================  K_l0
-constexpr int L0_DH = 64;      // head dim (MMA N)
+constexpr int L0_DH = 64;                          // head dim (MMA N)
 constexpr int L0_STAGES = 4;
-constexpr int L0_IMG_BYTES = 16384;                 // 128 rows x 64 K (bf16) per stage
-constexpr int L0_B_BYTES = 4 * L0_DH * 64 * 2;  // up to 4 heads x [64 x 64] bf16
-constexpr int L0_STAGE_BYTES = L0_IMG_BYTES + L0_B_BYTES;
-constexpr int L0_SMEM = L0_STAGES * L0_STAGE_BYTES + 1024 + 256;
-constexpr int L0_THREADS = 224;  // producer, gate, 4 builders, image gate
-constexpr uint32_t L0_ACC_COLS = 4 * L0_DH;  // accumulator region (NH * 64 used)
-constexpr uint32_t L0_SLOT_COLS = 4 * 32;    // A slot: 64 bf16 K per head = 32 columns
+constexpr int L0_IMG_BYTES = 16384;                // 128 rows x 64 K bf16 (or ext: 16 ch of p)
+constexpr int L0_P_BYTES = 4096;                   // p of the stage: CG ch x 128 rows x NH bf16
+constexpr int L0_B_BYTES = 4 * L0_DH * 64 * 2;     // up to 4 heads x [64 x 64] bf16
+constexpr int L0_STAGE_BYTES = L0_IMG_BYTES + L0_P_BYTES + L0_B_BYTES;
+constexpr int L0_STAGE_OUT = 8 * 32 * 64;          // epilogue staging: 8 warps x 32 rows x 64 B
+constexpr int L0_SMEM = L0_STAGES * L0_STAGE_BYTES + L0_STAGE_OUT + 1024 + 256;
+constexpr int L0_THREADS = 352;                    // producer, gate, image gate, 8 builders
+constexpr uint32_t L0_ACC_COLS = 4 * L0_DH;        // accumulator region (NH * 64 used)
+constexpr uint32_t L0_SLOT_COLS = 4 * 32;          // A slot: 64 bf16 K per head = 32 columns
 
-// NH = heads per CTA (2 or 4): accumulator NH*64 TMEM columns, A slot NH*32 columns.
-//
-// Warp roles (one persistent CTA per SM, a "unit" = (node, 128-row tile, head group)):
-//   warp 0      producer: 1-D bulk copies of the image rows and the pre-tiled B blocks of
-//               every stage (one stage = K 64 per head) into a 4-deep shared-memory ring.
-//   warp 1      control: the only warp that waits on mbarriers (full / A-slot free);
-//               releases the builders with a named barrier (GO), collects them (READY) and
-//               issues the stage's tcgen05.mma (A from TMEM, B from shared memory).
-//   warps 2..5  builders (thread = row = TMEM lane): A = p[r,c,h] * patch_c[r] written to
-//               one of two TMEM slots with tcgen05.st; then the unit's epilogue.
-// Builders never wait on an mbarrier inside the stage loop: an already-completed
-// mbarrier try_wait costs ~157 cycles on B200 against ~20 for bar.sync (tools/sync_probe),
-// and two of them per stage made the first version handshake-bound.
+#define L0_TRACE(ev, idx)                                                                   \
+  do {                                                                                      \
+    if (a.trace && blockIdx.x == 0 && (idx) < 256) a.trace[(ev) * 256 + (idx)] = clock64(); \
+  } while (0)
+
+// Stages of one unit (node n, 128-row tile, head group hg of NH heads):
+//   main stage st < nmain: CG channels (K = 64 per head): image rows, p slices, B = M_c blocks
+//   ext stage e < next:    16 channels of the bias K-block: p slices (A = p) and Et K-block
+// Warp roles (one persistent CTA per SM):
+//   warp 0      producer: 1-D bulk copies of every stage into a 4-deep shared-memory ring.
+//   warp 1      gate: waits "A slot free" (mbarrier), releases builders (named barrier SLOT),
+//               collects READY, issues the stage's tcgen05.mma (A from TMEM, B from smem).
+//   warp 2      image gate: waits "stage landed" (mbarrier) -> named barrier IMG.
+//   warps 3..10 builders, two per TMEM lane quarter (thread = row), HW = NH/2 heads each:
+//               A = p[r,c,h] * patch_c[r] (or p itself for ext) -> registers -> tcgen05.st.
+// Builders never touch an mbarrier or global memory inside the stage loop (p arrives with
+// the stage): an already-completed mbarrier try_wait costs ~157 cycles on B200 against ~20
+// for bar.sync, and a global load consumed one stage later still exposed ~800 cycles of L2
+// latency per stage (tools/sync_probe.cu, tools/l0_trace.py).
 template <int PP, int L0_NH>
 __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
-  constexpr int CG = 64 / PP;        // channels per stage (K = 64 per head per stage)
+  constexpr int CG = 64 / PP;        // channels per main stage (K = 64 per head per stage)
   constexpr int P = PP == 64 ? 8 : 4;
-  constexpr int NBAR = 160;          // control warp + 4 builder warps
+  constexpr int NBAR = 288;          // gate (or image gate) warp + 8 builder warps
+  constexpr int PROW = 128 * L0_NH * 2;  // bytes of one channel's p slice for the tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L0_STAGES * L0_STAGE_BYTES);
+  uint8_t* stage_out = smem + L0_STAGES * L0_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + L0_STAGE_OUT);
   uint64_t* empty = full + L0_STAGES;
   uint64_t* aempty = empty + L0_STAGES;
   uint64_t* accfull = aempty + 2;
@@ -359,6 +211,13 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
   const int n_tiles = R / 128;
   const int HG = a.H / L0_NH;
   const int total_units = a.n_nodes * n_tiles * HG;
+  const bool rowp = a.p_row_mode != 0;
+  auto unit_stages = [&](int u, int& g, int& nmain, int& next) {
+    const int n = (u / HG) / n_tiles;
+    g = __ldg(a.node_g + n);
+    nmain = (g + CG - 1) / CG;
+    next = (g + 15) / 16;
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < L0_STAGES; ++s) {
@@ -386,60 +245,72 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
         const int rest = u / HG;
         const int tile = rest % n_tiles;
         const int n = rest / n_tiles;
-        const int c0 = __ldg(a.node_c0 + n), g = __ldg(a.node_g + n);
-        const int nmain = (g + CG - 1) / CG;
+        const int c0 = __ldg(a.node_c0 + n);
+        int g, nmain, next;
+        unit_stages(u, g, nmain, next);
+        const long long poff = __ldg(a.node_poff + n);
         const int r0 = tile * 128;
         const int b = r0 / a.S, s0 = r0 - b * a.S;
         const __nv_bfloat16* chunk0 =
             a.img + b * a.img_sb + (long long)(s0 / a.wp) * P * a.W;
-        for (int st = 0; st <= nmain; ++st) {
+        // p slice of (hg, channel c) for this tile
+        auto pslice = [&](int c) {
+          return a.p + poff + (((long long)hg * g + c) * R + r0) * L0_NH;
+        };
+        for (int st = 0; st < nmain + next; ++st) {
           mbar_wait(&empty[stage], phase ^ 1);  // MMAs of the stage 4 back are done
           uint8_t* sI = smem + stage * L0_STAGE_BYTES;
-          uint8_t* sB = sI + L0_IMG_BYTES;
+          uint8_t* sP = sI + L0_IMG_BYTES;
+          uint8_t* sB = sP + L0_P_BYTES;
           if (a.debug_mode & 4) {
             mbar_arrive(&full[stage]);
           } else if (st < nmain) {
             const int cv = min(CG, g - st * CG);
-            mbar_expect_tx(&full[stage], cv * 128 * PP * 2 + L0_NH * L0_DH * 64 * 2);
-            for (int cc = 0; cc < cv; ++cc)
-              bulk_load(sI + cc * 128 * PP * 2,
-                        chunk0 + (long long)(c0 + st * CG + cc) * a.img_sc, 128 * PP * 2,
-                        &full[stage]);
+            mbar_expect_tx(&full[stage], cv * 128 * PP * 2 + (rowp ? cv * PROW : 0) +
+                                             L0_NH * L0_DH * 64 * 2);
+            for (int cc = 0; cc < cv; ++cc) {
+              const int c = st * CG + cc;
+              bulk_load(sI + cc * 128 * PP * 2, chunk0 + (long long)(c0 + c) * a.img_sc,
+                        128 * PP * 2, &full[stage]);
+              if (rowp) bulk_load(sP + cc * PROW, pslice(c), PROW, &full[stage]);
+            }
             for (int h = 0; h < L0_NH; ++h)
               bulk_load(sB + h * (L0_DH * 64 * 2),
                         a.Mt + ((long long)(hg * L0_NH + h) * a.C_pad + c0 + st * CG) *
                                    (L0_DH * PP),
                         L0_DH * 64 * 2, &full[stage]);
           } else {
-            const int eb = L0_DH * a.KE * 2;
-            mbar_expect_tx(&full[stage], L0_NH * eb);
+            const int e = st - nmain;
+            const int ce = min(16, g - 16 * e);
+            mbar_expect_tx(&full[stage], (rowp ? ce * PROW : 0) + L0_NH * L0_DH * 16 * 2);
+            if (rowp)
+              for (int cc = 0; cc < ce; ++cc)
+                bulk_load(sI + cc * PROW, pslice(16 * e + cc), PROW, &full[stage]);
             for (int h = 0; h < L0_NH; ++h)
               bulk_load(sB + h * (L0_DH * 64 * 2),
-                        a.Et + ((long long)n * a.H + hg * L0_NH + h) * (L0_DH * a.KE), eb,
-                        &full[stage]);
+                        a.Et + ((long long)n * a.H + hg * L0_NH + h) * (L0_DH * a.KE) +
+                            e * 16 * L0_DH,
+                        L0_DH * 16 * 2, &full[stage]);
           }
           if (++stage == L0_STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ control ("gate"): waits + MMA issue
-    // Named barriers (160 threads = this warp + 4 builder warps):
-    //   IMG[k%4]   (ids 1..4) stage k's image/B landed   -> builders precompute A in registers
-    //   SLOT[k%2]  (ids 5..6) stage k's TMEM A slot free  -> builders store A (4 x tcgen05.st)
-    //   READY[k%2] (ids 7..8) stage k's A is in TMEM      -> this warp issues the MMAs
-    // Order per stage k: READY(k) -> issue(k) -> wait slot of k+1 (MMAs of k-1 done) -> SLOT(k+1)
-    // -> wait full(k+2) -> IMG(k+2).  The MMAs of k+1 are then issued while those of k run.
+    // ------------------------------------------------ gate: slot waits + MMA issue
+    // Order per stage q: READY(q) -> issue(q) -> wait A slot of q+1 (MMAs of q-1 done) ->
+    // SLOT(q+1).  The MMAs of q+1 are thus queued while those of q run.
     const uint32_t idesc = idesc_bf16_f32(128, L0_DH);
-    // global stage counter q: smem stage q % 4, A slot q % 2 (phase bits derived from q)
     long long q_total = 0;
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-      const int n = (u / HG) / n_tiles;
-      q_total += (__ldg(a.node_g + n) + CG - 1) / CG + 1;
+      int g, nmain, next;
+      unit_stages(u, g, nmain, next);
+      q_total += nmain + next;
     }
     auto slot_free = [&](long long q) {
       if (q < q_total) {
         mbar_wait(&aempty[q & 1], (uint32_t)(((q >> 1) & 1) ^ 1));
+        if (lane == 0) L0_TRACE(1, q);
         tc_fence_after();
         asm volatile("bar.arrive %0, %1;" ::"r"(5 + (int)(q & 1)), "r"(NBAR) : "memory");
       }
@@ -447,19 +318,19 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
     slot_free(0);
     long long q = 0;
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-      const int n = (u / HG) / n_tiles;
-      const int g = __ldg(a.node_g + n);
-      const int nmain = (g + CG - 1) / CG;
-      for (int st = 0; st <= nmain; ++st, ++q) {
+      int g, nmain, next;
+      unit_stages(u, g, nmain, next);
+      for (int st = 0; st < nmain + next; ++st, ++q) {
         const int cs = (int)(q % L0_STAGES), cl = (int)(q & 1);
         asm volatile("bar.sync %0, %1;" ::"r"(7 + cl), "r"(NBAR) : "memory");  // READY(q)
+        if (lane == 0) L0_TRACE(2, q);
         tc_fence_after();
         if (elect_one()) {
-          const int ksteps = (a.debug_mode & 2) ? 0 : (st < nmain ? 4 : a.KE / 16);
-          const uint64_t bd0 =
-              smem_desc(smem_u32(smem + cs * L0_STAGE_BYTES + L0_IMG_BYTES), 1024, 128, 0);
+          const uint64_t bd0 = smem_desc(
+              smem_u32(smem + cs * L0_STAGE_BYTES + L0_IMG_BYTES + L0_P_BYTES), 1024, 128, 0);
           const uint32_t at0 = tbase + L0_ACC_COLS + cl * L0_SLOT_COLS;
-          if (ksteps == 4) {
+          if (a.debug_mode & 2) {
+          } else if (st < nmain) {
 #pragma unroll
             for (int h = 0; h < L0_NH; ++h)
 #pragma unroll
@@ -468,87 +339,83 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
                        bd0 + (uint64_t)((h * (L0_DH * 64 * 2) + kk * 2048) >> 4), idesc,
                        (st | kk) != 0);
           } else {
+#pragma unroll
             for (int h = 0; h < L0_NH; ++h)
-              for (int kk = 0; kk < ksteps; ++kk)
-                mma_ts(tbase + h * L0_DH, at0 + h * 32 + kk * 8,
-                       bd0 + (uint64_t)((h * (L0_DH * 64 * 2) + kk * 2048) >> 4), idesc,
-                       (st | kk) != 0);
+              mma_ts(tbase + h * L0_DH, at0 + h * 32,
+                     bd0 + (uint64_t)((h * (L0_DH * 64 * 2)) >> 4), idesc, 1u);
           }
           mma_commit(&empty[cs]);
           mma_commit(&aempty[cl]);
-          if (st == nmain) mma_commit(accfull);
+          if (st == nmain + next - 1) mma_commit(accfull);
         }
         __syncwarp();
         slot_free(q + 1);
       }
     }
-  } else if (warp == 6) {
+  } else if (warp == 2) {
     // ------------------------------------------------ image gate: full(q) -> IMG(q)
     long long q_total = 0;
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-      const int n = (u / HG) / n_tiles;
-      q_total += (__ldg(a.node_g + n) + CG - 1) / CG + 1;
+      int g, nmain, next;
+      unit_stages(u, g, nmain, next);
+      q_total += nmain + next;
     }
     for (long long q = 0; q < q_total; ++q) {
       mbar_wait(&full[q % L0_STAGES], (uint32_t)((q / L0_STAGES) & 1));
+      if (lane == 0) L0_TRACE(0, q);
       asm volatile("bar.arrive %0, %1;" ::"r"(1 + (int)(q & 3)), "r"(NBAR) : "memory");
     }
   } else {
-    // ------------------------------------------------ builders + epilogue (warps 2..5)
+    // ------------------------------------------------ builders + epilogue (warps 3..10)
+    constexpr int HW = L0_NH / 2;       // heads per builder warp
     const int quarter = warp & 3;
+    const int hh = (warp - 3) >> 2;
     const int m = quarter * 32 + lane;  // row within tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    uint8_t* my_out = stage_out + (warp - 3) * (32 * 64);
     uint32_t accphase = 0;
     long long q = 0;
     const int i_l = m / a.wp, jj = m - (m / a.wp) * a.wp;
+    // this warp's HW heads of one channel, packed bf16 (HW == 1: low half)
+    auto p_smem = [&](const uint8_t* base, int cc) -> uint32_t {
+      const uint8_t* src = base + cc * PROW + (m * L0_NH + hh * HW) * 2;
+      return HW == 2 ? *reinterpret_cast<const uint32_t*>(src)
+                     : (uint32_t)*reinterpret_cast<const uint16_t*>(src);
+    };
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
       const int hg = u % HG;
       const int rest = u / HG;
       const int tile = rest % n_tiles;
       const int n = rest / n_tiles;
-      const int g = __ldg(a.node_g + n);
+      int g, nmain, next;
+      unit_stages(u, g, nmain, next);
       const long long poff = __ldg(a.node_poff + n);
-      const int nmain = (g + CG - 1) / CG;
-      const int r = tile * 128 + m;
-      // p of this (row, head group): channel c at prow + c * pstride, NH heads contiguous
-      const __nv_bfloat16* prow =
-          a.p_row_mode ? a.p + poff + ((long long)(hg * R + r) * g) * L0_NH
-                       : a.p + poff + hg * L0_NH;
-      const int pstride = a.p_row_mode ? L0_NH : a.H;
-      uint32_t pc[CG][2], pn[CG][2];
-      auto load_p = [&](int st, uint32_t (&d)[CG][2]) {
-#pragma unroll
-        for (int cc = 0; cc < CG; ++cc) {
-          const int c = st * CG + cc;
-          d[cc][0] = 0u;
-          d[cc][1] = 0u;
-          if (st < nmain && c < g && !(a.debug_mode & 16)) {
-            if (L0_NH == 4) {
-              const uint2 v = __ldg(reinterpret_cast<const uint2*>(prow + (long long)c * pstride));
-              d[cc][0] = v.x; d[cc][1] = v.y;
-            } else {
-              d[cc][0] = __ldg(reinterpret_cast<const unsigned int*>(prow + (long long)c * pstride));
-            }
-          }
-        }
+      // constant p table (linear-mix nodes): p[poff + c*H + h]
+      auto p_const = [&](int c) -> uint32_t {
+        const __nv_bfloat16* src = a.p + poff + (long long)c * a.H + hg * L0_NH + hh * HW;
+        return HW == 2 ? __ldg(reinterpret_cast<const unsigned int*>(src))
+                       : (uint32_t)__bfloat16_as_ushort(src[0]);
       };
-      load_p(0, pc);
-      for (int st = 0; st <= nmain; ++st, ++q) {
-        load_p(st + 1, pn);
+      for (int st = 0; st < nmain + next; ++st, ++q) {
         const int cs = (int)(q % L0_STAGES), cl = (int)(q & 1);
-        uint32_t y[L0_NH][32];
+        const uint8_t* sI = smem + cs * L0_STAGE_BYTES;
+        const uint8_t* sP = sI + L0_IMG_BYTES;
+        uint32_t y[HW][32];
         asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(q & 3)), "r"(NBAR) : "memory");  // IMG
+        if (warp == 3 && lane == 0) L0_TRACE(3, q);
+        int ncols = 32;
         if (a.debug_mode & 1) {
 #pragma unroll
-          for (int h = 0; h < L0_NH; ++h)
+          for (int h = 0; h < HW; ++h)
 #pragma unroll
             for (int e = 0; e < 32; ++e) y[h][e] = 0u;
         } else if (st < nmain) {
-          uint32_t x[32];
-          const uint8_t* sI = smem + cs * L0_STAGE_BYTES;
+          uint32_t x[32], pv[CG];
 #pragma unroll
           for (int cc = 0; cc < CG; ++cc) {
-            const bool valid = st * CG + cc < g;
+            const int c = st * CG + cc;
+            const bool valid = c < g;
+            pv[cc] = !valid ? 0u : (rowp ? p_smem(sP, cc) : p_const(c));
             const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(
                                             sI + cc * 128 * PP * 2) +
                                         (i_l * P) * a.W + jj * P;
@@ -567,10 +434,10 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
             }
           }
 #pragma unroll
-          for (int h = 0; h < L0_NH; ++h) {
+          for (int h = 0; h < HW; ++h) {
 #pragma unroll
             for (int cc = 0; cc < CG; ++cc) {
-              const uint32_t w = pc[cc][h >> 1];
+              const uint32_t w = pv[cc];
               const uint32_t ph = (h & 1) ? (w & 0xffff0000u) | (w >> 16)
                                           : (w << 16) | (w & 0xffffu);
 #pragma unroll
@@ -579,67 +446,78 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
             }
           }
         } else {
-          // ext block: A[r, c] = p[r, c, h], zero-padded to 64 (the MMA reads KE)
-          for (int kc = 0; kc < 32; ++kc) {
-            const int c = 2 * kc;
-            uint32_t lo[2] = {0u, 0u}, hi[2] = {0u, 0u};
-            if (c < g) {
-              if (L0_NH == 4) {
-                const uint2 v = __ldg(reinterpret_cast<const uint2*>(prow + (long long)c * pstride));
-                lo[0] = v.x; lo[1] = v.y;
-              } else {
-                lo[0] = __ldg(reinterpret_cast<const unsigned int*>(prow + (long long)c * pstride));
-              }
-            }
-            if (c + 1 < g) {
-              if (L0_NH == 4) {
-                const uint2 v = __ldg(reinterpret_cast<const uint2*>(prow + (long long)(c + 1) * pstride));
-                hi[0] = v.x; hi[1] = v.y;
-              } else {
-                hi[0] = __ldg(reinterpret_cast<const unsigned int*>(prow + (long long)(c + 1) * pstride));
-              }
-            }
+          // ext stage e: A[r, k] = p[r, 16e + k, h] (k < 16), one MMA K-step per head
+          const int e = st - nmain;
+          ncols = 8;
 #pragma unroll
-            for (int h = 0; h < L0_NH; ++h) {
-              const uint32_t a16 = (h & 1) ? (lo[h >> 1] >> 16) : (lo[h >> 1] & 0xffffu);
-              const uint32_t b16 = (h & 1) ? (hi[h >> 1] >> 16) : (hi[h >> 1] & 0xffffu);
+          for (int kc = 0; kc < 8; ++kc) {
+            const int c0e = 16 * e + 2 * kc;
+            const uint32_t lo = c0e < g ? (rowp ? p_smem(sI, 2 * kc) : p_const(c0e)) : 0u;
+            const uint32_t hi = c0e + 1 < g ? (rowp ? p_smem(sI, 2 * kc + 1) : p_const(c0e + 1))
+                                            : 0u;
+#pragma unroll
+            for (int h = 0; h < HW; ++h) {
+              const uint32_t a16 = (h & 1) ? (lo >> 16) : (lo & 0xffffu);
+              const uint32_t b16 = (h & 1) ? (hi >> 16) : (hi & 0xffffu);
               y[h][kc] = a16 | (b16 << 16);
             }
           }
         }
+        if (warp == 3 && lane == 0) L0_TRACE(4, q);
         asm volatile("bar.sync %0, %1;" ::"r"(5 + cl), "r"(NBAR) : "memory");  // SLOT free
+        if (warp == 3 && lane == 0) L0_TRACE(5, q);
         tc_fence_after();
         const uint32_t slot_t = tbase + lane_off + L0_ACC_COLS + cl * L0_SLOT_COLS;
+        if (ncols == 32) {
 #pragma unroll
-        for (int h = 0; h < L0_NH; ++h) tmem_st32(slot_t + h * 32, y[h]);
+          for (int h = 0; h < HW; ++h) tmem_st32(slot_t + (hh * HW + h) * 32, y[h]);
+        } else {
+#pragma unroll
+          for (int h = 0; h < HW; ++h) {
+            uint32_t y8[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) y8[k] = y[h][k];
+            tmem_st8(slot_t + (hh * HW + h) * 32, y8);
+          }
+        }
         tmem_st_wait();
         tc_fence_before();
         asm volatile("bar.arrive %0, %1;" ::"r"(7 + cl), "r"(NBAR) : "memory");  // READY
-#pragma unroll
-        for (int cc = 0; cc < CG; ++cc) { pc[cc][0] = pn[cc][0]; pc[cc][1] = pn[cc][1]; }
       }
-      // epilogue: ctx (fp32 TMEM) -> bf16 HBM  (pos term folded into the next K_gemm)
+      // epilogue: this warp's 32 rows x HW heads, TMEM -> bf16 -> swizzled smem -> coalesced
+      // 16-byte stores (8 row segments of 64 B per warp instruction)
+      if (warp == 3 && lane == 0) L0_TRACE(6, q);
       mbar_wait(accfull, accphase);
+      if (warp == 3 && lane == 0) L0_TRACE(7, q);
       tc_fence_after();
-      __nv_bfloat16* out = a.ctx + ((long long)n * R + r) * a.D + hg * L0_NH * L0_DH;
+      const long long row0 = (long long)n * R + tile * 128 + quarter * 32;
 #pragma unroll 1
-      for (int cb = 0; cb < ((a.debug_mode & 32) ? 0 : L0_NH * L0_DH); cb += 32) {
+      for (int cb = 0; cb < ((a.debug_mode & 32) ? 0 : HW * L0_DH); cb += 32) {
+        const int col = (hh * HW) * L0_DH + cb;  // column within this head group
         uint32_t v[32];
-        tmem_ld32(tbase + lane_off + cb, v);
+        tmem_ld32(tbase + lane_off + col, v);
         tmem_ld_wait();
-        if (a.debug_mode & 8) {
-          if (v[0] == 0x7fffffffu && v[31] == 0x7fffffffu) out[cb] = __float2bfloat16(1.f);
-          continue;
-        }
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
+        for (int k = 0; k < 4; ++k) {
           uint4 o;
-          o.x = pack_bf16(__uint_as_float(v[j + 0]), __uint_as_float(v[j + 1]));
-          o.y = pack_bf16(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-          o.z = pack_bf16(__uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
-          o.w = pack_bf16(__uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
-          *reinterpret_cast<uint4*>(out + cb + j) = o;
+          o.x = pack_bf16(__uint_as_float(v[8 * k + 0]), __uint_as_float(v[8 * k + 1]));
+          o.y = pack_bf16(__uint_as_float(v[8 * k + 2]), __uint_as_float(v[8 * k + 3]));
+          o.z = pack_bf16(__uint_as_float(v[8 * k + 4]), __uint_as_float(v[8 * k + 5]));
+          o.w = pack_bf16(__uint_as_float(v[8 * k + 6]), __uint_as_float(v[8 * k + 7]));
+          *reinterpret_cast<uint4*>(my_out + lane * 64 + ((k ^ (lane & 3)) << 4)) = o;
         }
+        __syncwarp();
+        if (!(a.debug_mode & 8)) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = i * 8 + (lane >> 2), k = lane & 3;
+            const uint4 o =
+                *reinterpret_cast<const uint4*>(my_out + rr * 64 + ((k ^ (rr & 3)) << 4));
+            *reinterpret_cast<uint4*>(a.ctx + (row0 + rr) * a.D + hg * L0_NH * L0_DH + col +
+                                      k * 8) = o;
+          }
+        }
+        __syncwarp();
       }
       tc_fence_before();  // acc reads precede the next unit's first MMA (via READY)
       accphase ^= 1;
@@ -657,8 +535,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
 cudaError_t launch_l0_node(const L0NodeArgs& a, int num_sms, cudaStream_t st) {
   const int R = a.B * a.S;
   const int nh = a.H % 4 == 0 ? 4 : 2;
-  if (R % 128 || a.S % 128 || 128 % a.wp || a.H % nh || a.D != a.H * L0_DH || a.KE % 16 ||
-      a.KE > 64)
+  if (R % 128 || a.S % 128 || 128 % a.wp || a.H % nh || a.D != a.H * L0_DH || a.KE % 16)
     return cudaErrorInvalidValue;
   const int units = a.n_nodes * (R / 128) * (a.H / nh);
   const int grid = units < num_sms ? units : num_sms;

@@ -211,8 +211,6 @@ def pack_rank(fr: FoldedRank, device) -> PackedRank:
     n0 = len(fr.l0_g)
     gmax = max(fr.l0_g)
     KE = 16 * ((gmax + 15) // 16)
-    if KE > 64:
-        raise ConfigError(f"level-0 group size {gmax} > 64 is not supported by the fused kernel")
     HP = 8 * ((h + 7) // 8)
     f32 = dict(device=device, dtype=torch.float32)
     stream = _lib.stream_handle()

@@ -1,0 +1,155 @@
+"""Functional mirrors of the reference front-end API, on CUDA tensors.
+
+Same names, argument order and meaning as the reference:
+
+* ``tokenize_channels(images, tok_w, tok_b, chan_id, pos, patch)``   -- model.py:51-64
+* ``flat_aggregate(tokens, w, prefix, variant, n_heads)``             -- model.py:67-73
+* ``tree_aggregate(tokens, spec, w, prefix, layer_kind, variant, n_heads)`` -- model.py:76-97
+
+These take already-formed tokens (the fused module path in frontend.py never forms
+them). Each call lowers onto the same sm_100a kernels: dchag_unfold + dchag_gemm_bf16
+(tokenizer), and per tree level a projection GEMM into the node's value/logit space plus
+dchag_combine_strided (softmax-weighted child sum). Weights are dicts of tensors keyed
+by the reference's dotted names, in the reference's [D_in, D_out] layout. Compute is bf16
+with fp32 accumulation. Outputs are fp32 by default.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .config import ConfigError, TreeSpec
+from .fold import consumer_weight
+
+
+def _bf(t):
+    return t.to(device="cuda", dtype=torch.bfloat16).contiguous()
+
+
+def _f32(t):
+    return t.to(device="cuda", dtype=torch.float32).contiguous()
+
+
+def _gemm(A, Mo, Mi, K, sAmo, sAmi, W_nk, bias, outV, sVmo, sVmi, outL=None, sLmo=0,
+          sLmi=0, rowbias=None, rowbias_row=0, rowbias_period=1, outV_f32=False):
+    """One-group dchag_gemm_bf16 call: out[m, n] = A[m, :] . W_nk[n, :] + bias[n] (+ rowbias)."""
+    N = W_nk.shape[0]
+    Nv = outV.shape[-1] if outV is not None else 0
+    # unused strides of size-1 dims still have to be valid (non-zero) TMA strides
+    sAmo = sAmo if Mo > 1 else Mi * sAmi
+    sAg = Mo * Mi * K
+    _lib.call("dchag_gemm_bf16", _lib.ptr(A), 1, Mo, Mi, K, sAg, sAmo, sAmi, _lib.ptr(W_nk), N,
+              N * K, Nv, _lib.ptr(bias), N, _lib.ptr(rowbias), 0, rowbias_row,
+              rowbias_period, _lib.ptr(outV), int(outV_f32), 0, sVmo, sVmi, _lib.ptr(outL), 0,
+              sLmo, sLmi, _lib.stream_handle())
+
+
+def tokenize_channels(images, tok_w, tok_b, chan_id, pos, patch, out_dtype=torch.float32):
+    """[B, Cs, H, W] -> [B, Cs, S, D] tokens (model.py:51-64): unfold (tensor.py:303-323),
+    per-channel GEMM on tcgen05, and tok.b + channel_id + pos fused in the epilogue."""
+    B, C, Hh, Ww = images.shape
+    if Hh % patch or Ww % patch:
+        raise ConfigError(f"image {Hh}x{Ww} not divisible by patch {patch}")
+    S, PP = (Hh // patch) * (Ww // patch), patch * patch
+    D = tok_w.shape[-1]
+    if S % 128 or PP % 16:
+        raise ConfigError("tokenize_channels on sm_100a needs S % 128 == 0 and P*P % 16 == 0")
+    img = _bf(images)
+    patches = torch.empty(B, C, S, PP, device="cuda", dtype=torch.bfloat16)
+    st = _lib.stream_handle()
+    _lib.call("dchag_unfold", _lib.ptr(img), img.stride(0), img.stride(1), B, C, Hh, Ww, patch,
+              _lib.ptr(patches), st)
+    Wt = _bf(tok_w.transpose(1, 2))                   # [C, D, PP]
+    bias = _f32(tok_b) + _f32(chan_id)                # [C, D]
+    rb = _bf(pos)                                     # [S, D]
+    out = torch.empty(B, C, S, D, device="cuda", dtype=out_dtype)
+    _lib.call("dchag_gemm_bf16", _lib.ptr(patches), C, B, S, PP, S * PP, C * S * PP, PP,
+              _lib.ptr(Wt), D, D * PP, D, _lib.ptr(bias), D, _lib.ptr(rb), 0, D, S,
+              _lib.ptr(out), int(out_dtype == torch.float32), S * D, C * S * D, D, 0, 0, 0, 0,
+              st)
+    return out
+
+
+def tree_aggregate(tokens, spec: TreeSpec, w, prefix, layer_kind, variant, n_heads,
+                   out_dtype=torch.float32):
+    """[B, C, S, D] -> [B, 1, S, D] (model.py:76-97): contiguous groups per level, node
+    params under {prefix}.l{level}.g{group}."""
+    if variant != "single_query" and layer_kind != "linear":
+        raise ConfigError("tree_aggregate on sm_100a implements agg_variant='single_query'")
+    B, C, S, D = tokens.shape
+    if sum(spec.levels[0]) != C:
+        raise ConfigError(
+            f"tree level 0 partitions {sum(spec.levels[0])} channels, input has {C}")
+    if S % 128 or D % 64 or (D // n_heads) % 8:
+        raise ConfigError("tree_aggregate on sm_100a needs S % 128 == 0 and D % 64 == 0")
+    H = n_heads
+    R = B * S
+    st = _lib.stream_handle()
+    tw = {k: _f32(v) for k, v in w.items() if k.startswith(prefix + ".")}
+    x = _bf(tokens)
+    # level inputs: x laid out [B][n_in][S][D] (level 0) or [n_in][R][D] (above)
+    x_layout = "bsd"
+    n_in = C
+    depth = len(spec.levels)
+    for li, level in enumerate(spec.levels):
+        attn = layer_kind != "linear"
+        nodes = [f"{prefix}.l{li}.g{gi}" for gi in range(len(level))]
+        firsts, acc = [], 0
+        for g in level:
+            firsts.append(acc)
+            acc += g
+        # 1) project each node's inputs with its consumer weight Wcons = [wv | U] or w
+        V = torch.empty(n_in, R, D, device="cuda", dtype=torch.bfloat16) if x_layout == "nrd" \
+            else torch.empty(B, n_in, S, D, device="cuda", dtype=torch.bfloat16)
+        L = None
+        if attn:
+            L = torch.empty(V.shape[:-1] + (H,), device="cuda", dtype=torch.float32)
+        for node, f, g in zip(nodes, firsts, level):
+            Wc, _ = consumer_weight(tw, node, layer_kind, H)          # [D, D(+H)]
+            Wnk = _bf(Wc.t())
+            zero = torch.zeros(Wnk.shape[0], device="cuda", dtype=torch.float32)
+            if x_layout == "bsd":
+                A = x[:, f:f + g]                                        # rows (b, j, s)
+                _gemm(A, B, g * S, D, C * S * D, D, Wnk, zero, V[:, f:f + g], n_in * S * D, D,
+                      L[:, f:f + g] if attn else None, n_in * S * H, H)
+            else:
+                A = x[f:f + g]
+                _gemm(A, 1, g * R, D, 0, D, Wnk, zero, V[f:f + g], 0, D,
+                      L[f:f + g] if attn else None, 0, H)
+        # 2) combine children per node (+ linear bias b), then 3) node output projection
+        ctx = torch.empty(len(level), R, D, device="cuda", dtype=torch.bfloat16)
+        first_t = torch.tensor(firsts, device="cuda", dtype=torch.int32)
+        g_t = torch.tensor(list(level), device="cuda", dtype=torch.int32)
+        mix = None if attn else torch.cat([tw[f"{n}.mix"] for n in nodes]).contiguous()
+        if x_layout == "bsd":
+            sVj, sVb, sLj, sLb, rows_inner = S * D, n_in * S * D, S * H, n_in * S * H, S
+        else:
+            sVj, sVb, sLj, sLb, rows_inner = R * D, 0, R * H, 0, R
+        _lib.call("dchag_combine_strided", len(level), R, D, H, _lib.ptr(first_t),
+                  _lib.ptr(g_t), max(level), _lib.ptr(V), sVj, sVb, _lib.ptr(L), sLj, sLb,
+                  rows_inner, _lib.ptr(mix), _lib.ptr(ctx), st)
+        # node output y = ctx @ wo + bo (attention) or ctx + b (linear: w applied above)
+        y = torch.empty(len(level), R, D, device="cuda",
+                        dtype=out_dtype if li == depth - 1 else torch.bfloat16)
+        for k, node in enumerate(nodes):
+            if attn:
+                Wo, bo = _bf(tw[f"{node}.wo"].t()), tw[f"{node}.bo"]
+            else:
+                Wo, bo = _bf(torch.eye(D, device="cuda")), tw[f"{node}.b"]
+            _gemm(ctx[k], 1, R, D, 0, D, Wo, bo.contiguous(), y[k], 0, D,
+                  outV_f32=y.dtype == torch.float32)
+        x, x_layout, n_in = y, "nrd", len(level)
+    return x.view(B, 1, S, D) if x.shape[0] == 1 else x.view(1, B, S, D).transpose(0, 1)
+
+
+def flat_aggregate(tokens, w, prefix, variant, n_heads, hooks=None, tag="aggregate",
+                   out_dtype=torch.float32):
+    """[B, Ck, S, D] -> [B, 1, S, D] (model.py:67-73): one node over all Ck tokens."""
+    if hooks is not None:
+        raise ConfigError("head-split hooks are not part of the sm_100a path")
+    Ck = tokens.shape[1]
+    node = {k.replace(prefix, f"{prefix}.__flat.l0.g0", 1): v for k, v in w.items()
+            if k.startswith(prefix + ".")}
+    return tree_aggregate(tokens, TreeSpec(((Ck,),)), node, f"{prefix}.__flat", "cross_attention",
+                          variant, n_heads, out_dtype=out_dtype)

@@ -136,3 +136,61 @@ def test_frontend_forward_entry_and_dtype():
     y = fe(x)
     assert y.shape == (2, 1, 256, 128) and y.dtype == torch.bfloat16
     assert torch.isfinite(y.float()).all()
+
+
+# ---------------------------------------------------- functional API mirrors (ops.py)
+def _ops():
+    from paper_2506_21411_b200 import ops
+    return ops
+
+
+def test_tokenize_channels_matches_oracle():
+    rng = np.random.default_rng(11)
+    C, Hh, Ww, P, D = 6, 64, 64, 4, 128
+    S = (Hh // P) * (Ww // P)
+    tok_w = rng.standard_normal((C, P * P, D)) * 0.1
+    tok_b = rng.standard_normal((C, D)) * 0.1
+    cid = rng.standard_normal((C, D)) * 0.1
+    pos = rng.standard_normal((S, D)) * 0.1
+    img = rng.standard_normal((2, C, Hh, Ww))
+    q = lambda a: _bf(a).float().numpy().astype(np.float64)  # noqa: E731
+    got = _ops().tokenize_channels(torch.from_numpy(img), torch.from_numpy(tok_w),
+                                   torch.from_numpy(tok_b), torch.from_numpy(cid),
+                                   torch.from_numpy(pos), P).cpu().numpy()
+    want = O.tokenize_channels(q(img), q(tok_w), tok_b, cid, q(pos), P)
+    assert got.shape == (2, C, S, D)
+    assert rel_err(got, want) < BF16_TOL
+
+
+@pytest.mark.parametrize("layer_kind", ["cross_attention", "linear"])
+@pytest.mark.parametrize("C,g", [(6, 4), (9, 3), (5, 8)])
+def test_tree_aggregate_matches_oracle(layer_kind, C, g):
+    from paper_2506_21411_b200.config import build_tree_spec
+    rng = np.random.default_rng(C * 10 + g)
+    B, S, D, H = 2, 128, 128, 2
+    spec = build_tree_spec(C, g)
+    specs = O.frontend_param_specs(C, 8 * 16, 16, 8, D, 1, g, layer_kind=layer_kind)
+    w = O.random_params(specs, seed=C, std=0.05, bias_std=0.02)
+    w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
+    tokens = _bf(rng.standard_normal((B, C, S, D))).float().numpy().astype(np.float64)
+    got = _ops().tree_aggregate(torch.from_numpy(tokens), spec,
+                                {k: torch.from_numpy(v) for k, v in w.items()}, "agg.slab0",
+                                layer_kind, "single_query", H).cpu().numpy()
+    want = O.tree_aggregate(tokens, spec.levels, w, "agg.slab0", layer_kind, "single_query", H)
+    assert got.shape == (B, 1, S, D)
+    assert rel_err(got, want) < BF16_TOL
+
+
+def test_flat_aggregate_matches_bruteforce():
+    rng = np.random.default_rng(3)
+    B, Ck, S, D, H = 1, 5, 128, 128, 2
+    w = {f"n.{k}": rng.standard_normal((D, D)) * 0.05 for k in ("wq", "wk", "wv", "wo")}
+    w["n.q"] = rng.standard_normal(D) * 0.05
+    w["n.bo"] = rng.standard_normal(D) * 0.02
+    w = {k: _bf(v).float().numpy().astype(np.float64) for k, v in w.items()}
+    tokens = _bf(rng.standard_normal((B, Ck, S, D))).float().numpy().astype(np.float64)
+    got = _ops().flat_aggregate(torch.from_numpy(tokens),
+                                {k: torch.from_numpy(v) for k, v in w.items()}, "n",
+                                "single_query", H).cpu().numpy()
+    want = O.flat_aggregate(tokens, w, "n", "single_query", H)
+    assert rel_err(got, want) < BF16_TOL
