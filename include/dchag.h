@@ -88,6 +88,15 @@ int dchag_combine_strided(int n_nodes, int R, int D, int H, const int* node_firs
                           long long sVb, const float* L, long long sLj, long long sLb,
                           int rows_inner, const float* mix, void* ctx, void* stream);
 
+/* Backward of dchag_combine (training; reference tape tensor.py:168-205 through
+ * layers.py:103-123 / :141-146).  G fp32 [n][R][D] = dLoss/dctx.  Writes, per child j:
+ * gV_j = p_jh * G[h-blk] (bf16, V's strides), and dL_j = p (dp - sum p dp) (fp32, L's
+ * strides; attention) or dm_j[r] = G[r] . V_j[r] (fp32 [child][R]; linear). */
+int dchag_combine_bwd(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
+                      int max_g, const void* V, long long sVj, const float* L, long long sLj,
+                      const float* mix, const float* G, float* dL, void* gV, float* dm,
+                      void* stream);
+
 /* unfold_patches (tensor.py:303-323): img [B][C][Himg][W] -> out [B][C][S][P*P] bf16. */
 int dchag_unfold(const void* img, long long img_sb, long long img_sc, int B, int C, int Himg,
                  int W, int P, void* out, void* stream);

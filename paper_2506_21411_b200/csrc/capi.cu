@@ -233,6 +233,21 @@ int dchag_combine_strided(int n_nodes, int R, int D, int H, const int* node_firs
   return cuda_status(launch_combine(a, S(stream)), "combine");
 }
 
+int dchag_combine_bwd(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
+                      int max_g, const void* V, long long sVj, const float* L, long long sLj,
+                      const float* mix, const float* G, float* dL, void* gV, float* dm,
+                      void* stream) {
+  if (!mix && (!L || !dL)) return fail(DCHAG_ERR_SHAPE, "combine_bwd: attention needs L and dL");
+  if (mix && !dm) return fail(DCHAG_ERR_SHAPE, "combine_bwd: linear needs dm");
+  CombineBwdArgs a;
+  a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H; a.max_g = max_g;
+  a.node_first = node_first; a.node_g = node_g;
+  a.V = reinterpret_cast<const __nv_bfloat16*>(V); a.sVj = sVj;
+  a.L = L; a.sLj = sLj; a.mix = mix; a.G = G; a.dL = dL;
+  a.gV = reinterpret_cast<__nv_bfloat16*>(gV); a.dm = dm;
+  return cuda_status(launch_combine_bwd(a, S(stream)), "combine_bwd");
+}
+
 int dchag_unfold(const void* img, long long img_sb, long long img_sc, int B, int C, int Himg,
                  int W, int P, void* out, void* stream) {
   if (Himg % P || W % P) return fail(DCHAG_ERR_SHAPE, "unfold: image not divisible by patch");

@@ -101,6 +101,113 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Backward of the combine (layers.py:103-123 / :141-146 restated; reference tape
+// tensor.py:168-205): given g = dLoss/dctx[n][r][:] (fp32) and the saved child values
+// V_j (bf16) and logits L_j (fp32, attention) or mix (linear):
+//   p_jh   = softmax_j(L_j[r,h])                    (recomputed)
+//   dp_jh  = g[r, h-blk] . V_j[r, h-blk]
+//   dL_jh  = p_jh (dp_jh - sum_j' p_j'h dp_j'h)      -> dL  [child][R][H]   (attention)
+//   gV_j   = p_jh * g[r, h-blk]                      -> gV  [child][R][D]   bf16
+//   dmix_j(r) = g[r] . V_j[r]                        -> dm  [child][R]      (linear)
+// One warp per (node, row); lanes own 8-column chunks, head dot products reduced with
+// shuffles inside the dh/8 lanes of a head.
+__global__ void __launch_bounds__(128) combine_bwd_kernel(CombineBwdArgs a) {
+  __shared__ float sp[4][COMB_PTAB];
+  __shared__ float sd[4][COMB_PTAB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long item = (long long)blockIdx.x * 4 + warp;
+  const int n = (int)(item / a.R);
+  const int r = (int)(item - (long long)n * a.R);
+  if (n >= a.n_nodes) return;
+  const int first = __ldg(a.node_first + n), g = __ldg(a.node_g + n);
+  const int H = a.H, dh = a.D / H, cpl = dh / 8;  // chunks per head
+  float* p = sp[warp];
+  float* dp = sd[warp];
+  if (a.mix) {
+    for (int j = lane; j < g; j += 32) p[j] = __ldg(a.mix + first + j);
+  } else if (lane < H) {
+    const float* lr = a.L + (long long)first * a.sLj + (long long)r * H + lane;
+    float m = -INFINITY;
+    for (int j = 0; j < g; ++j) m = fmaxf(m, __ldg(lr + (long long)j * a.sLj));
+    float ssum = 0.f;
+    for (int j = 0; j < g; ++j) {
+      const float e = __expf(__ldg(lr + (long long)j * a.sLj) - m);
+      p[j * H + lane] = e;
+      ssum += e;
+    }
+    const float inv = 1.f / ssum;
+    for (int j = 0; j < g; ++j) p[j * H + lane] *= inv;
+  }
+  __syncwarp();
+  const int nchunk = a.D / 8;
+  const int per_lane = (nchunk + 31) / 32;
+  float gr[8][8];
+  const float* grow = a.G + ((long long)n * a.R + r) * a.D;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (q < per_lane && lane + 32 * q < nchunk) {
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow) + 2 * (lane + 32 * q));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow) + 2 * (lane + 32 * q) + 1);
+      gr[q][0] = g0.x; gr[q][1] = g0.y; gr[q][2] = g0.z; gr[q][3] = g0.w;
+      gr[q][4] = g1.x; gr[q][5] = g1.y; gr[q][6] = g1.z; gr[q][7] = g1.w;
+    }
+  }
+  for (int j = 0; j < g; ++j) {
+    const __nv_bfloat16* vrow = a.V + (long long)(first + j) * a.sVj + (long long)r * a.D;
+    __nv_bfloat16* gvrow = a.gV + (long long)(first + j) * a.sVj + (long long)r * a.D;
+    float dm_part = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float part = 0.f;
+      const int ch = lane + 32 * q;
+      const bool ok = q < per_lane && ch < nchunk;
+      if (ok) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(vrow) + ch);
+        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          part += gr[q][2 * e] * bf16lo(vv[e]) + gr[q][2 * e + 1] * bf16hi(vv[e]);
+        const float pj = a.mix ? p[j] : p[j * H + (ch * 8) / dh];
+        uint4 o;
+        o.x = pack_bf16(pj * gr[q][0], pj * gr[q][1]);
+        o.y = pack_bf16(pj * gr[q][2], pj * gr[q][3]);
+        o.z = pack_bf16(pj * gr[q][4], pj * gr[q][5]);
+        o.w = pack_bf16(pj * gr[q][6], pj * gr[q][7]);
+        reinterpret_cast<uint4*>(gvrow)[ch] = o;
+      }
+      if (a.mix) {
+        dm_part += part;
+      } else {
+        // reduce over the cpl lanes of one head (cpl divides 32: consecutive lanes)
+        for (int off = cpl >> 1; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+        if (ok && (lane % cpl) == 0) dp[j * H + (ch * 8) / dh] = part;
+      }
+    }
+    if (a.mix) {
+      for (int off = 16; off > 0; off >>= 1) dm_part += __shfl_xor_sync(0xffffffffu, dm_part, off);
+      if (lane == 0) a.dm[(long long)(first + j) * a.R + r] = dm_part;
+    }
+  }
+  __syncwarp();
+  if (!a.mix && lane < H) {
+    float s = 0.f;
+    for (int j = 0; j < g; ++j) s += p[j * H + lane] * dp[j * H + lane];
+    for (int j = 0; j < g; ++j)
+      a.dL[(long long)(first + j) * a.sLj + (long long)r * H + lane] =
+          p[j * H + lane] * (dp[j * H + lane] - s);
+  }
+}
+
+cudaError_t launch_combine_bwd(const CombineBwdArgs& a, cudaStream_t st) {
+  const int dh = a.D / a.H;
+  if (a.D % 8 || a.D > 2048 || dh % 8 || 32 % (dh / 8 > 32 ? 64 : dh / 8) || a.H > COMB_MAXH ||
+      a.max_g * (a.mix ? 1 : a.H) > COMB_PTAB)
+    return cudaErrorInvalidValue;
+  const long long items = (long long)a.n_nodes * a.R;
+  combine_bwd_kernel<<<(int)((items + 3) / 4), 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 // images [B][C][H][W] (strided) -> patches [B][C][S][P*P]; one thread per patch row (py)
 __global__ void unfold_kernel(const __nv_bfloat16* img, long long sb, long long sc, int B, int C,
                               int Himg, int W, int P, __nv_bfloat16* out) {

@@ -82,6 +82,23 @@ struct CombineArgs {
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
 
+// Backward of the combine: dL, gV (and dmix for linear nodes) from g = dLoss/dctx
+struct CombineBwdArgs {
+  int n_nodes, R, D, H, max_g;
+  const int* node_first;
+  const int* node_g;
+  const __nv_bfloat16* V;      // child j at V + j*sVj + r*D (same strides for gV)
+  long long sVj;
+  const float* L;              // child logits, j*sLj + r*H (same strides for dL)
+  long long sLj;
+  const float* mix;            // linear mode
+  const float* G;              // [n][R][D] fp32 upstream gradient of ctx
+  float* dL;                   // attention: [child][R][H]
+  __nv_bfloat16* gV;           // [child][R][D]
+  float* dm;                   // linear: [child][R] row dots g . V_j
+};
+cudaError_t launch_combine_bwd(const CombineBwdArgs& a, cudaStream_t st);
+
 // images [B][C][H][W] -> patches [B][C][S][P*P] (bf16)
 cudaError_t launch_unfold(const __nv_bfloat16* img, long long img_sb, long long img_sc, int B,
                           int C, int Himg, int W, int P, __nv_bfloat16* out, cudaStream_t st);

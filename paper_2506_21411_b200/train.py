@@ -1,0 +1,405 @@
+"""Training step of the D-CHAG front end: forward with saved activations + backward.
+
+Reference semantics: `T.backward` over the hot path of forward_loss_dchag_reference /
+dchag_forward_loss (model.py:180-201, strategies.py:195-218, tensor.py:395-413), gather
+backward = local slice (strategies.py:91-94), and the special.pos gradient all-reduced over
+the channel group (strategies.py:251-264).
+
+Forward (`forward_train`) runs the sm_100a kernels: K_p0 + K_l0 for level 0 (tokens never
+formed), and unfolded node projections above it, so every node output y is kept for the
+weight gradients. The AllGather moves the root streams y_r themselves, in rank order. The
+replicated final layer then projects them on every rank, so its gradients are identical
+everywhere, as in the reference.
+
+Backward (`backward`): the non-GEMM parts run on an sm_100a kernel, dchag_combine_bwd
+(softmax-weighted child sum backward: dp, softmax backward, p*g). These are plain GEMMs
+(cuBLAS through torch.matmul, bf16 in / fp32 accumulate):
+  y = ctx wo + bo  ->  d wo = ctx^T g,  g_ctx = g wo^T
+  [V | L] = y_child [wv | U]  ->  d wv = y^T gV,  dU = y^T dL,  g_y = gV wv^T + dL U^T
+At level 0 each node's tokens are recomputed with the tcgen05 tokenizer GEMM
+(dchag_gemm_bf16), one node at a time. That gives d tok.w = patches^T g_x,
+d tok.b = d channel_id = sum_rows g_x, d pos = sum_{b,c} g_x.
+dU -> (wk, q, wq) follows U[:, h] = wk[:, h-blk] (q wq)[h-blk] / sqrt(dh) (fold.py).
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from .config import ConfigError
+from .fold import query_logit_weights
+from .frontend import DchagFrontEnd
+from .payload import payload_nbytes  # noqa: F401  (layout reference)
+
+
+def _bf(t):
+    return t.to(torch.bfloat16).contiguous()
+
+
+def _f32(t):
+    return t.to(torch.float32).contiguous()
+
+
+def _gemm(A, W_dn, bias=None, out_f32=False, rowbias=None, period=1, N_logit=0):
+    """y[m, :] = A[m, :] @ W_dn + bias (+ rowbias[m % period]) with the sm_100a GEMM.
+    A [M, K] bf16 (M % 128 == 0), W_dn [K, N] (reference x @ W layout). Columns >= N - N_logit
+    come back as a separate fp32 tensor."""
+    M, K = A.shape
+    N = W_dn.shape[1]
+    Nv = N - N_logit
+    W = _bf(W_dn.t())
+    b = _f32(bias) if bias is not None else torch.zeros(N, device=A.device)
+    V = torch.empty(M, Nv, device=A.device, dtype=torch.float32 if out_f32 else torch.bfloat16)
+    L = torch.empty(M, max(N_logit, 1), device=A.device, dtype=torch.float32)
+    rb = _bf(rowbias) if rowbias is not None else None
+    _lib.call("dchag_gemm_bf16", _lib.ptr(A), 1, 1, M, K, M * K, M * K, K, _lib.ptr(W), N, N * K,
+              Nv, _lib.ptr(b), N, _lib.ptr(rb), 0, N, period, _lib.ptr(V), int(out_f32), 0, 0, Nv,
+              _lib.ptr(L) if N_logit else 0, 0, 0, N_logit, _lib.stream_handle())
+    return (V, L) if N_logit else V
+
+
+def _u_backward(w, prefix, dU, heads):
+    """Gradients of wk, q, wq from dU where U[:,h] = wk[:,h-blk] q'[h-blk]/sqrt(dh), q' = q wq."""
+    wk, wq, q = w[f"{prefix}.wk"], w[f"{prefix}.wq"], w[f"{prefix}.q"]
+    d = wk.shape[0]
+    dh = d // heads
+    qp = q @ wq
+    s = 1.0 / math.sqrt(dh)
+    d_wk = (dU.view(d, heads, 1) * qp.view(1, heads, dh)).reshape(d, d) * s
+    d_qp = (wk.view(d, heads, dh) * dU.view(d, heads, 1)).sum(0).reshape(d) * s
+    return {f"{prefix}.wk": d_wk, f"{prefix}.wq": torch.outer(q, d_qp), f"{prefix}.q": wq @ d_qp}
+
+
+class DchagTrainer:
+    """Forward + backward of one rank's front end (tp ranks share the final layer)."""
+
+    def __init__(self, fe: DchagFrontEnd):
+        if fe.model.agg_variant != "single_query":
+            raise ConfigError("training path implements agg_variant='single_query'")
+        self.fe = fe
+
+    # ---------------------------------------------------------------- forward
+    def forward_local(self, images):
+        """Slab tokenizer + tree of this rank up to its root stream (saved['y_root'])."""
+        fe = self.fe
+        m = fe.model
+        pk = fe.prepare()
+        w = fe.weights
+        d, h, s = m.embed, m.heads, fe.seq
+        attn = fe.strategy.agg_layer_kind != "linear"
+        off, cnt = fe.slab
+        if images.shape[1] == m.channels and fe.tp > 1:
+            images = images[:, off:off + cnt]
+        img = images.to(torch.bfloat16).contiguous()
+        B = img.shape[0]
+        R = B * s
+        levels = fe.tree.levels
+        pre = f"agg.slab{fe.rank}"
+        saved = {"img": img, "B": B, "R": R}
+        # ---- level 0 context via the fused kernels (p and ctx kept)
+        dev = img.device
+        st = _lib.stream_handle()
+        if pk.attn_l0:
+            poff, acc = [], 0
+            for g in pk.l0_g_list:
+                poff.append(acc)
+                acc += g * R * h
+            poff_t = torch.tensor(poff, device=dev, dtype=torch.int64)
+            pbuf = torch.empty(acc, device=dev, dtype=torch.bfloat16)
+            _lib.call("dchag_l0_logits", _lib.ptr(img), img.stride(0), img.stride(1), B,
+                      m.image_h, m.image_w, m.patch, h, pk.HP, pk.n0, max(pk.l0_g_list),
+                      _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g), _lib.ptr(poff_t), _lib.ptr(pk.WUt),
+                      _lib.ptr(pk.bU), _lib.ptr(pk.posU), _lib.ptr(pbuf), st)
+            prow = 1
+        else:
+            poff_t = (pk.l0_c0.to(torch.int64) * h).contiguous()
+            pbuf, prow = pk.p_const, 0
+        ctx0 = torch.empty(pk.n0, R, d, device=dev, dtype=torch.bfloat16)
+        _lib.call("dchag_l0_node", _lib.ptr(img), img.stride(0), img.stride(1), B, m.image_h,
+                  m.image_w, m.patch, h, d, pk.n0, _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g),
+                  _lib.ptr(poff_t), prow, _lib.ptr(pbuf), _lib.ptr(pk.Mt), pk.C_pad,
+                  _lib.ptr(pk.Et), pk.KE, _lib.ptr(ctx0), st)
+        # positional term of the level-0 context: pos @ Vw_n (x (sum mix) for linear nodes)
+        posV = self._level0_posV()
+        srow = torch.arange(R, device=dev) % s
+        ctx0 = (ctx0.float() + posV[:, srow]).to(torch.bfloat16)       # [n0, R, D]
+        saved["ctx"] = [ctx0]
+        y = torch.empty(len(levels[0]), R, d, device=dev, dtype=torch.bfloat16)
+        for gi in range(len(levels[0])):
+            node = f"{pre}.l0.g{gi}"
+            y[gi] = (_gemm(ctx0[gi], w[f"{node}.wo"], w[f"{node}.bo"]) if attn
+                     else (ctx0[gi].float() + w[f"{node}.b"]).to(torch.bfloat16))
+        saved["y"] = [y]
+        saved["VL"] = []
+        # ---- levels >= 1 (unfolded)
+        for li in range(1, len(levels)):
+            V, L, ctx, ynext = self._level_forward(y, levels[li], li, pre, attn, R)
+            saved["VL"].append((V, L))
+            saved["ctx"].append(ctx)
+            saved["y"].append(ynext)
+            y = ynext
+        saved["y_root"] = y[0].contiguous()
+        return saved
+
+    def forward_train(self, images):
+        """Full forward of this rank: slab tree, AllGather of the root streams (rank order,
+        runtime.py:259), shared final layer.  Returns ([B,1,S,D] fp32, saved)."""
+        saved = self.forward_local(images)
+        fe = self.fe
+        y_root = saved["y_root"]
+        if fe.tp > 1:
+            import torch.distributed as dist
+            y_all = torch.empty((fe.tp,) + tuple(y_root.shape), device=y_root.device,
+                                dtype=torch.bfloat16)
+            dist.all_gather_into_tensor(y_all, y_root, group=fe.process_group)
+        else:
+            y_all = y_root.unsqueeze(0)
+        return self.forward_final(y_all, saved), saved
+
+    def forward_final(self, y_all, saved):
+        """Shared final layer over the gathered streams y_all [tp, R, D] (replicated)."""
+        fe = self.fe
+        w = fe.weights
+        d, h, s = fe.model.embed, fe.model.heads, fe.seq
+        R, B = saved["R"], saved["B"]
+        Wc = torch.cat([w["agg.final.wv"], query_logit_weights(w, "agg.final", h)], dim=1)
+        Vf, Lf = _gemm(y_all.reshape(fe.tp * R, d), Wc, N_logit=h)
+        Vf, Lf = Vf.view(fe.tp, R, d), Lf.view(fe.tp, R, h)
+        ctx_f = self._combine(Vf, Lf, None, [0], [fe.tp], R)
+        out = _gemm(ctx_f[0], w["agg.final.wo"], w["agg.final.bo"], out_f32=True)
+        saved.update(y_all=y_all, Vf=Vf, Lf=Lf, ctx_f=ctx_f)
+        return out.view(B, 1, s, d)
+
+    def _level0_posV(self):
+        fe = self.fe
+        w = fe.weights
+        pre = f"agg.slab{fe.rank}"
+        pos = w["special.pos"]
+        out = []
+        for gi in range(len(fe.tree.levels[0])):
+            node = f"{pre}.l0.g{gi}"
+            if fe.strategy.agg_layer_kind == "linear":
+                out.append(w[f"{node}.mix"].sum() * (pos @ w[f"{node}.w"]))
+            else:
+                out.append(pos @ w[f"{node}.wv"])
+        return torch.stack(out)                                          # [n0, S, D]
+
+    def _combine(self, V, L, mix, firsts, gs, R):
+        n = len(firsts)
+        d = V.shape[-1]
+        h = self.fe.model.heads
+        ctx = torch.empty(n, R, d, device=V.device, dtype=torch.bfloat16)
+        ft = torch.tensor(firsts, device=V.device, dtype=torch.int32)
+        gt = torch.tensor(gs, device=V.device, dtype=torch.int32)
+        _lib.call("dchag_combine", n, R, d, h, _lib.ptr(ft), _lib.ptr(gt), max(gs), _lib.ptr(V),
+                  R * d, _lib.ptr(L), R * h, _lib.ptr(mix), _lib.ptr(ctx), _lib.stream_handle())
+        return ctx
+
+    def _level_forward(self, y_prev, level, li, pre, attn, R):
+        w = self.fe.weights
+        d, h = self.fe.model.embed, self.fe.model.heads
+        nprev = y_prev.shape[0]
+        V = torch.empty(nprev, R, d, device=y_prev.device, dtype=torch.bfloat16)
+        L = torch.empty(nprev, R, h, device=y_prev.device, dtype=torch.float32) if attn else None
+        firsts, acc = [], 0
+        for gi, g in enumerate(level):
+            firsts.append(acc)
+            node = f"{pre}.l{li}.g{gi}"
+            A = y_prev[acc:acc + g].reshape(g * R, d)
+            if attn:
+                Wc = torch.cat([w[f"{node}.wv"], query_logit_weights(w, node, h)], dim=1)
+                v, lg = _gemm(A, Wc, N_logit=h)
+                V[acc:acc + g] = v.view(g, R, d)
+                L[acc:acc + g] = lg.view(g, R, h)
+            else:
+                V[acc:acc + g] = _gemm(A, w[f"{node}.w"]).view(g, R, d)
+            acc += g
+        mix = None if attn else torch.cat([w[f"{pre}.l{li}.g{gi}.mix"]
+                                           for gi in range(len(level))]).float().contiguous()
+        ctx = self._combine(V, L, mix, firsts, list(level), R)
+        y = torch.empty(len(level), R, d, device=y_prev.device, dtype=torch.bfloat16)
+        for gi in range(len(level)):
+            node = f"{pre}.l{li}.g{gi}"
+            y[gi] = (_gemm(ctx[gi], w[f"{node}.wo"], w[f"{node}.bo"]) if attn
+                     else (ctx[gi].float() + w[f"{node}.b"]).to(torch.bfloat16))
+        return V, L, ctx, y
+
+    # ---------------------------------------------------------------- backward
+    def _combine_bwd(self, V, L, mix, G, firsts, gs, R):
+        """-> gV bf16 (V's shape), dL fp32 (attention) or dm fp32 [child, R] (linear)."""
+        n = len(firsts)
+        nch = V.shape[0]
+        d = V.shape[-1]
+        h = self.fe.model.heads
+        gV = torch.empty_like(V)
+        dL = torch.empty(nch, R, h, device=V.device, dtype=torch.float32) if mix is None else None
+        dm = torch.empty(nch, R, device=V.device, dtype=torch.float32) if mix is not None else None
+        ft = torch.tensor(firsts, device=V.device, dtype=torch.int32)
+        gt = torch.tensor(gs, device=V.device, dtype=torch.int32)
+        _lib.call("dchag_combine_bwd", n, R, d, h, _lib.ptr(ft), _lib.ptr(gt), max(gs),
+                  _lib.ptr(V), R * d, _lib.ptr(L), R * h, _lib.ptr(mix), _lib.ptr(_f32(G)),
+                  _lib.ptr(dL), _lib.ptr(gV), _lib.ptr(dm), _lib.stream_handle())
+        return gV, dL, dm
+
+    def backward(self, saved, g_out):
+        """Gradients of sum(out * g_out) w.r.t. this rank's parameters (reference names):
+        the slab's tok.* / channel_id rows, its agg.slab{r}.*, the replicated agg.final.*,
+        and special.pos all-reduced over the tp group."""
+        grads, g_y = self.backward_final(saved, g_out)
+        grads.update(self.backward_local(saved, g_y))
+        if self.fe.tp > 1:
+            import torch.distributed as dist
+            dist.all_reduce(grads["special.pos"], group=self.fe.process_group)
+        return grads
+
+    def backward_final(self, saved, g_out):
+        """Final-layer grads (identical on every rank) and this rank's root-stream gradient
+        (the local slice of the gathered gradient, strategies.py:91-94)."""
+        fe = self.fe
+        w = fe.weights
+        d, h = fe.model.embed, fe.model.heads
+        R = saved["R"]
+        grads = {}
+        g_out = _f32(g_out.reshape(R, d))
+        # ---- final layer (replicated)
+        ctx_f = saved["ctx_f"][0].float()
+        grads["agg.final.bo"] = g_out.sum(0)
+        grads["agg.final.wo"] = ctx_f.t() @ g_out
+        g_ctx = (g_out @ w["agg.final.wo"].t()).view(1, R, d)
+        gV, dL, _ = self._combine_bwd(saved["Vf"], saved["Lf"], None, g_ctx, [0], [fe.tp], R)
+        y_all = saved["y_all"].float().reshape(fe.tp * R, d)
+        grads["agg.final.wv"] = y_all.t() @ gV.float().reshape(fe.tp * R, d)
+        dU = y_all.t() @ dL.reshape(fe.tp * R, h)
+        grads.update(_u_backward(w, "agg.final", dU, h))
+        U_f = query_logit_weights(w, "agg.final", h)
+        # local slice of the gathered gradient (strategies.py:91-94): no collective
+        g_y = (gV[fe.rank].float() @ w["agg.final.wv"].t() + dL[fe.rank] @ U_f.t()).view(1, R, d)
+        return grads, g_y
+
+    def backward_local(self, saved, g_y):
+        """Slab-tree and tokenizer grads from this rank's root-stream gradient g_y [1,R,D];
+        special.pos is this rank's partial (summed over tp by backward())."""
+        fe = self.fe
+        m = fe.model
+        w = fe.weights
+        d, h, s, P = m.embed, m.heads, fe.seq, m.patch
+        R, B = saved["R"], saved["B"]
+        levels = fe.tree.levels
+        pre = f"agg.slab{fe.rank}"
+        attn = fe.strategy.agg_layer_kind != "linear"
+        grads = {}
+        # ---- levels >= 1, top down
+        for li in range(len(levels) - 1, 0, -1):
+            level = levels[li]
+            ctx = saved["ctx"][li].float()
+            V, L = saved["VL"][li - 1]
+            y_prev = saved["y"][li - 1]
+            G = torch.empty(len(level), R, d, device=g_y.device, dtype=torch.float32)
+            for gi in range(len(level)):
+                node = f"{pre}.l{li}.g{gi}"
+                if attn:
+                    grads[f"{node}.bo"] = g_y[gi].sum(0)
+                    grads[f"{node}.wo"] = ctx[gi].t() @ g_y[gi]
+                    G[gi] = g_y[gi] @ w[f"{node}.wo"].t()
+                else:
+                    grads[f"{node}.b"] = g_y[gi].sum(0)
+                    G[gi] = g_y[gi]
+            firsts, acc = [], 0
+            for g in level:
+                firsts.append(acc)
+                acc += g
+            mix = None if attn else torch.cat([w[f"{pre}.l{li}.g{gi}.mix"]
+                                               for gi in range(len(level))]).float().contiguous()
+            gV, dL, dm = self._combine_bwd(V, L, mix, G, firsts, list(level), R)
+            g_prev = torch.empty(y_prev.shape, device=g_y.device, dtype=torch.float32)
+            for gi, (f0, g) in enumerate(zip(firsts, level)):
+                node = f"{pre}.l{li}.g{gi}"
+                Y = y_prev[f0:f0 + g].float().reshape(g * R, d)
+                gv = gV[f0:f0 + g].float().reshape(g * R, d)
+                if attn:
+                    dl = dL[f0:f0 + g].reshape(g * R, h)
+                    grads[f"{node}.wv"] = Y.t() @ gv
+                    grads.update(_u_backward(w, node, Y.t() @ dl, h))
+                    U = query_logit_weights(w, node, h)
+                    g_prev[f0:f0 + g] = (gv @ w[f"{node}.wv"].t() + dl @ U.t()).view(g, R, d)
+                else:
+                    grads[f"{node}.w"] = Y.t() @ gv
+                    grads[f"{node}.mix"] = dm[f0:f0 + g].sum(1)
+                    g_prev[f0:f0 + g] = (gv @ w[f"{node}.w"].t()).view(g, R, d)
+            g_y = g_prev
+        # ---- level 0: node output, then tokens recomputed node by node
+        off, cnt = fe.slab
+        img = saved["img"]
+        ctx0 = saved["ctx"][0].float()
+        pos = w["special.pos"]
+        tokw = w["tok.w"][off:off + cnt]
+        tb = (w["tok.b"] + w["special.channel_id"])[off:off + cnt]
+        d_tokw = torch.zeros_like(tokw)
+        d_tb = torch.zeros_like(tb)
+        d_pos = torch.zeros_like(pos)
+        patches = torch.empty(B, cnt, s, P * P, device=img.device, dtype=torch.bfloat16)
+        _lib.call("dchag_unfold", _lib.ptr(img), img.stride(0), img.stride(1), B, cnt, m.image_h,
+                  m.image_w, P, _lib.ptr(patches), _lib.stream_handle())
+        c0 = 0
+        for gi, g in enumerate(levels[0]):
+            node = f"{pre}.l0.g{gi}"
+            if attn:
+                grads[f"{node}.bo"] = g_y[gi].sum(0)
+                grads[f"{node}.wo"] = ctx0[gi].t() @ g_y[gi]
+                G = (g_y[gi] @ w[f"{node}.wo"].t()).view(1, R, d)
+            else:
+                grads[f"{node}.b"] = g_y[gi].sum(0)
+                G = g_y[gi].view(1, R, d)
+            # tokens of this node's channels, channel-major [g][R][D] (tcgen05 tokenizer GEMM)
+            X = self._tokens(patches, c0, g, B)
+            Xf = X.reshape(g * R, d)
+            if attn:
+                U = query_logit_weights(w, node, h)
+                V, L = _gemm(Xf, torch.cat([w[f"{node}.wv"], U], dim=1), N_logit=h)
+                gV, dL, _ = self._combine_bwd(V.view(g, R, d), L.view(g, R, h).contiguous(), None,
+                                              G, [0], [g], R)
+                gv = gV.float().reshape(g * R, d)
+                dl = dL.reshape(g * R, h)
+                Xf32 = Xf.float()
+                grads[f"{node}.wv"] = Xf32.t() @ gv
+                grads.update(_u_backward(w, node, Xf32.t() @ dl, h))
+                gX = gv @ w[f"{node}.wv"].t() + dl @ U.t()
+            else:
+                V = _gemm(Xf, w[f"{node}.w"])
+                mix = w[f"{node}.mix"].float().contiguous()
+                gV, _, dm = self._combine_bwd(V.view(g, R, d), None, mix, G, [0], [g], R)
+                gv = gV.float().reshape(g * R, d)
+                grads[f"{node}.w"] = Xf.float().t() @ gv
+                grads[f"{node}.mix"] = dm.sum(1)
+                gX = gv @ w[f"{node}.w"].t()
+            gX = gX.view(g, B, s, d)
+            pt = patches[:, c0:c0 + g].float().permute(1, 0, 2, 3).reshape(g, B * s, P * P)
+            d_tokw[c0:c0 + g] = torch.bmm(pt.transpose(1, 2), gX.reshape(g, B * s, d))
+            d_tb[c0:c0 + g] = gX.sum((1, 2))
+            d_pos += gX.sum((0, 1))
+            c0 += g
+        grads["tok.w"] = d_tokw
+        grads["tok.b"] = d_tb
+        grads["special.channel_id"] = d_tb.clone()
+        grads["special.pos"] = d_pos  # partial; backward() all-reduces it (strategies.py:251-264)
+        return grads
+
+    def _tokens(self, patches, c0, g, B):
+        """tokens[c][b*S + s] for slab channels c0..c0+g (tok.w @ patch + tok.b + chan_id + pos)."""
+        fe = self.fe
+        w = fe.weights
+        off = fe.slab[0]
+        d, s, pp = fe.model.embed, fe.seq, fe.model.patch ** 2
+        C = patches.shape[1]
+        Wt = _bf(w["tok.w"][off + c0:off + c0 + g].transpose(1, 2))        # [g, D, PP]
+        bias = _f32((w["tok.b"] + w["special.channel_id"])[off + c0:off + c0 + g])
+        rb = _bf(w["special.pos"])
+        X = torch.empty(g, B * s, d, device=patches.device, dtype=torch.bfloat16)
+        A = patches[:, c0:c0 + g]
+        _lib.call("dchag_gemm_bf16", _lib.ptr(A), g, B, s, pp, s * pp, C * s * pp, pp, _lib.ptr(Wt),
+                  d, d * pp, d, _lib.ptr(bias), d, _lib.ptr(rb), 0, d, s, _lib.ptr(X), 0,
+                  B * s * d, s * d, d, 0, 0, 0, 0, _lib.stream_handle())
+        return X

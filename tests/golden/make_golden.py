@@ -125,6 +125,14 @@ def main():
               tp=1, max_group=8, batch=1, seed=0, round32=True, bias_scale=0.02)
     make_case("T_sq_tp2", channels=16, image=(64, 64), patch=4, embed=128, heads=2,
               tp=2, max_group=4, batch=1, seed=1, round32=True, bias_scale=0.02)
+    # GPU-shaped training cases: gradients of sum(out * probe) through the front end
+    make_case("Tg_sq_tp1", channels=8, image=(64, 32), patch=4, embed=128, heads=2,
+              tp=1, max_group=4, batch=1, seed=2, round32=True, grads=True, bias_scale=0.02)
+    make_case("Tg_sq_tp2", channels=8, image=(64, 32), patch=4, embed=128, heads=2,
+              tp=2, max_group=2, batch=1, seed=3, round32=True, grads=True, bias_scale=0.02)
+    make_case("Tg_lin_tp2", channels=8, image=(64, 32), patch=4, embed=128, heads=2,
+              tp=2, max_group=2, batch=1, layer_kind="linear", seed=4, round32=True, grads=True,
+              bias_scale=0.02)
 
 
 if __name__ == "__main__":

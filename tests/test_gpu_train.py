@@ -1,0 +1,98 @@
+"""GPU training step: forward_train + backward (paper_2506_21411_b200/train.py) against the
+gradients the reference tape produced (tests/golden/Tg_*.npz) and the float64 torch
+autograd restatement (tests/torch_reference.py) on random configs.  All tp ranks run in
+one process: the AllGather is the concatenation of the root streams in rank order, the
+boundary backward is the local slice, and special.pos is summed over ranks
+(strategies.py:83-96, :251-264)."""
+import numpy as np
+import pytest
+import torch
+
+import dchag_oracle as O
+import torch_reference as TR
+from conftest import load_golden, rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def _run(meta, w, images, probe):
+    from paper_2506_21411_b200 import DchagFrontEnd
+    from paper_2506_21411_b200.train import DchagTrainer
+    tp = meta["tp"]
+    img = torch.as_tensor(np.asarray(images, np.float32)).to(torch.bfloat16).cuda()
+    trs, saves = [], []
+    for r in range(tp):
+        fe = DchagFrontEnd(meta["channels"], meta["image_h"], meta["image_w"], meta["patch"],
+                           meta["embed"], meta["heads"], max_group=meta["max_group"],
+                           agg_layer_kind=meta.get("layer_kind", "cross_attention"), tp=tp,
+                           rank=r, out_dtype=torch.float32)
+        fe.load_weights(w)
+        tr = DchagTrainer(fe)
+        off, cnt = fe.slab
+        saves.append(tr.forward_local(img[:, off:off + cnt]))
+        trs.append(tr)
+    y_all = torch.stack([s["y_root"] for s in saves])
+    outs = [tr.forward_final(y_all, s) for tr, s in zip(trs, saves)]
+    g_out = torch.as_tensor(np.asarray(probe, np.float32)).cuda()
+    grads = {}
+    d_pos = None
+    for r, (tr, s) in enumerate(zip(trs, saves)):
+        gf, g_y = tr.backward_final(s, g_out)
+        gl = tr.backward_local(s, g_y)
+        off, cnt = tr.fe.slab
+        for k, v in {**gf, **gl}.items():
+            v = v.detach().double().cpu().numpy()
+            if k in ("tok.w", "tok.b", "special.channel_id"):
+                full = grads.setdefault(k, np.zeros(w[k].shape))
+                full[off:off + cnt] = v
+            elif k == "special.pos":
+                d_pos = v if d_pos is None else d_pos + v
+            elif k.startswith("agg.final."):
+                if k in grads:
+                    assert rel_err(grads[k], v) < 1e-6, f"final-layer grad {k} differs across ranks"
+                grads[k] = v
+            else:
+                grads[k] = v
+    grads["special.pos"] = d_pos
+    torch.cuda.synchronize()
+    return outs[0].cpu().numpy(), grads
+
+
+def _check(out, grads, out_ref, g_ref):
+    assert rel_err(out, out_ref) < TOL
+    missing = set(g_ref) - set(grads)
+    assert not missing, missing
+    bad = {k: rel_err(grads[k], g_ref[k]) for k in g_ref}
+    worst = max(bad.values())
+    assert worst < TOL, sorted(bad.items(), key=lambda kv: -kv[1])[:6]
+
+
+@pytest.mark.parametrize("case", ["Tg_sq_tp1", "Tg_sq_tp2", "Tg_lin_tp2"])
+def test_train_step_matches_reference_tape(case):
+    meta, z, w, g_ref = load_golden(case)
+    out, grads = _run(meta, w, z["images"], z["probe"])
+    _check(out, grads, z["out"], g_ref)
+
+
+@pytest.mark.parametrize("meta", [
+    dict(channels=12, image_h=64, image_w=128, patch=8, embed=256, heads=4, tp=3, max_group=2),
+    dict(channels=9, image_h=32, image_w=64, patch=4, embed=128, heads=2, tp=1, max_group=3,
+         layer_kind="linear"),
+], ids=["P8_tp3_uneven", "P4_linear"])
+def test_train_step_matches_autograd(meta):
+    lk = meta.get("layer_kind", "cross_attention")
+    specs = O.frontend_param_specs(meta["channels"], meta["image_h"], meta["image_w"],
+                                   meta["patch"], meta["embed"], meta["tp"], meta["max_group"],
+                                   layer_kind=lk)
+    w = O.random_params(specs, seed=2, std=0.05, bias_std=0.02)
+    w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
+    rng = np.random.default_rng(4)
+    img = rng.standard_normal((2, meta["channels"], meta["image_h"], meta["image_w"]))
+    img = torch.as_tensor(img.astype(np.float32)).to(torch.bfloat16).float().numpy().astype(np.float64)
+    S = (meta["image_h"] // meta["patch"]) * (meta["image_w"] // meta["patch"])
+    probe = rng.standard_normal((2, 1, S, meta["embed"]))
+    out_ref, g_ref = TR.grads(img, w, probe, patch=meta["patch"], heads=meta["heads"],
+                              tp=meta["tp"], max_group=meta["max_group"], layer_kind=lk)
+    out, grads = _run(dict(meta, layer_kind=lk), w, img, probe)
+    _check(out, grads, out_ref, g_ref)

@@ -1,0 +1,23 @@
+"""Pin the float64 torch autograd restatement (tests/torch_reference.py) to the gradients
+the reference tape produced (tests/golden/*.npz grad:*, make_golden.py)."""
+import numpy as np
+import pytest
+
+import torch_reference as TR
+from conftest import load_golden, rel_err
+
+CASES = ["ref_tiny_sq_tp2", "ref_tiny_lin_tp2", "ref_tiny_sq_tp1_g3", "Tg_sq_tp1", "Tg_sq_tp2",
+         "Tg_lin_tp2"]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_autograd_reference_matches_reference_tape(case):
+    meta, z, w, g_ref = load_golden(case)
+    out, g = TR.grads(z["images"].astype(np.float64), w, z["probe"].astype(np.float64),
+                      patch=meta["patch"], heads=meta["heads"], tp=meta["tp"],
+                      max_group=meta["max_group"], layer_kind=meta["layer_kind"])
+    tol = 1e-10 if z["out"].dtype == np.float64 else 1e-6
+    assert rel_err(out, z["out"]) < tol
+    assert set(g) == set(g_ref)
+    for k in g_ref:
+        assert rel_err(g[k], g_ref[k]) < tol * 10, k
