@@ -31,6 +31,9 @@ WORKLOADS = {
                     depth=2, batch=16),
     "tiny": dict(channels=16, image_h=64, image_w=64, patch=4, embed=128, heads=2, depth=2,
                  batch=2),
+    # training step (fwd+bwd), SURVEY.md section 8(d) "TR": C500 D2048 H32 (dh 64), bf16
+    "train": dict(channels=500, image_h=128, image_w=128, patch=8, embed=2048, heads=32,
+                  depth=3, batch=32, train=True),
 }
 METRIC = "D-CHAG tokenize+aggregate images/sec"
 
@@ -124,7 +127,8 @@ def reference_arm(args, wl, tp, max_group):
 
 
 def workload_config(args, wl, tp, max_group):
-    return {"workload": args.workload, "channels": wl["channels"],
+    return {"workload": args.workload, "step": "fwd+bwd" if wl.get("train") else "fwd",
+            "channels": wl["channels"],
             "image": [wl["image_h"], wl["image_w"]], "patch": wl["patch"],
             "embed": wl["embed"], "heads": wl["heads"], "depth": wl["depth"],
             "max_group": max_group, "tp": tp, "global_batch": args.batch or wl["batch"],
@@ -248,7 +252,16 @@ def b200_arm(args, wl, tp, max_group):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    step = lambda: fe(images)  # noqa: E731
+    if wl.get("train"):
+        from paper_2506_21411_b200.train import DchagTrainer
+        trainer = DchagTrainer(fe)
+        probe = torch.randn(B, 1, fe.seq, wl["embed"], device="cuda", generator=gen)
+
+        def step():
+            out, saved = trainer.forward_train(images)
+            return trainer.backward(saved, probe)
+    else:
+        step = lambda: fe(images)  # noqa: E731
     clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         step()
@@ -265,7 +278,11 @@ def b200_arm(args, wl, tp, max_group):
     ms = max_over_ranks(ms)
     value = B * args.steps / (ms / 1e3)
 
-    # ---- pass B: per-kernel CUDA events on the launching stream
+    # ---- pass B: per-kernel CUDA events on the launching stream (inference plan)
+    if wl.get("train"):
+        step_inf = lambda: fe(images)  # noqa: E731
+    else:
+        step_inf = step
     plan = fe.launch_plan(B)
     site_ms = {s: 0.0 for _, s, _, _ in plan}
     events = []
@@ -287,7 +304,7 @@ def b200_arm(args, wl, tp, max_group):
 
     _lib.set_launch_hook(hook)
     try:
-        timed(step, args.steps, per_step_hook=reset)
+        timed(step_inf, args.steps, per_step_hook=reset)
     finally:
         _lib.set_launch_hook(None)
     for site, a, b in events:
@@ -322,12 +339,18 @@ def b200_arm(args, wl, tp, max_group):
 
     # ---- pass C: end to end through the public API from pinned host memory
     host_img = images.cpu().pin_memory()
-    out_host = torch.empty(B, 1, fe.seq, wl["embed"], dtype=fe.out_dtype).pin_memory()
+    out_host = torch.empty(B, 1, fe.seq, wl["embed"],
+                           dtype=torch.float32 if wl.get("train") else fe.out_dtype).pin_memory()
     dev_img = torch.empty_like(images)
 
     def e2e_step():
         dev_img.copy_(host_img, non_blocking=True)
-        y = fe(dev_img)
+        if wl.get("train"):
+            out, saved = trainer.forward_train(dev_img)
+            trainer.backward(saved, probe)
+            y = out
+        else:
+            y = fe(dev_img)
         if rank == 0:
             out_host.copy_(y, non_blocking=True)
 
@@ -346,7 +369,7 @@ def b200_arm(args, wl, tp, max_group):
         tot_exec = float(t.item()) + [p for p in plan if p[1] == "gemm_final"][0][2]
     else:
         tot_exec = exec_flops
-    b_flops = bflops_per_image(wl, fe.slabs, max_group) * B
+    b_flops = bflops_per_image(wl, fe.slabs, max_group, train=bool(wl.get("train"))) * B
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -388,19 +411,20 @@ def b200_arm(args, wl, tp, max_group):
         dist.destroy_process_group()
 
 
-def bflops_per_image(wl, slabs, max_group):
-    """SURVEY.md section 8(d) 'B' flops: collapsed single_query count, final layer once."""
+def bflops_per_image(wl, slabs, max_group, train=False):
+    """SURVEY.md section 8(d) 'B' flops: collapsed single_query count, final layer once;
+    fwd+bwd = 3 x (nodes + final) + 2 x tokenizer."""
     from paper_2506_21411_b200.config import build_tree_spec
     S = (wl["image_h"] // wl["patch"]) * (wl["image_w"] // wl["patch"])
     D, H, pp = wl["embed"], wl["heads"], wl["patch"] ** 2
-    tot = 0
+    tok = nodes = 0
     for _, c in slabs:
-        tot += 2 * c * S * pp * D
+        tok += 2 * c * S * pp * D
         for level in build_tree_spec(c, max_group).levels:
             for g in level:
-                tot += S * (4 * g * D * H + 4 * D * D)
-    tot += S * (4 * len(slabs) * D * H + 4 * D * D)
-    return tot
+                nodes += S * (4 * g * D * H + 4 * D * D)
+    nodes += S * (4 * len(slabs) * D * H + 4 * D * D)
+    return 3 * nodes + 2 * tok if train else nodes + tok
 
 
 def main():

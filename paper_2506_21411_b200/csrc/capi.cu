@@ -202,6 +202,7 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
   {
     const char* dbg = getenv("DCHAG_L0_DEBUG");
     a.debug_mode = dbg ? atoi(dbg) : 0;
+    a.cluster = getenv("DCHAG_L0_CLUSTER") ? atoi(getenv("DCHAG_L0_CLUSTER")) : 0;
     const char* tr = getenv("DCHAG_L0_TRACE_PTR");
     a.trace = tr ? reinterpret_cast<long long*>(strtoull(tr, nullptr, 0)) : nullptr;
   }

@@ -62,6 +62,7 @@ struct L0NodeArgs {
   int KE;
   __nv_bfloat16* ctx;          // [n_nodes][R][D]
   int debug_mode;              // timing probes: 0 normal, 1 no A build, 2 no MMA
+  int cluster;                 // 0 auto (CTA pairs when the tile count is even), 1 off
   long long* trace;            // optional [8][256] clock64 timeline of CTA 0 (debug)
 };
 cudaError_t launch_l0_node(const L0NodeArgs& a, int num_sms, cudaStream_t st);

@@ -253,49 +253,60 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           continue;
         }
         const int gcols = min(32, args.BN - grp * 32);  // columns of this group in the tile
-        if (gcols == 32 && n0 + 32 <= args.Nv) {
-          // whole group in the value region: stage + coalesced copy-out
+        if ((gcols == 32 || gcols == 16) && n0 + gcols <= args.Nv) {
+          // value region: stage in smem (swizzled) + coalesced copy-out of whole row segments
+          const int nk = gcols / 8;          // 16-byte chunks per row (bf16)
           if (!args.outV_f32) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              uint4 o;
-              o.x = pack_bf16(v[8 * k + 0], v[8 * k + 1]);
-              o.y = pack_bf16(v[8 * k + 2], v[8 * k + 3]);
-              o.z = pack_bf16(v[8 * k + 4], v[8 * k + 5]);
-              o.w = pack_bf16(v[8 * k + 6], v[8 * k + 7]);
-              *reinterpret_cast<uint4*>(my_out + lane * 64 + ((k ^ (lane & 3)) << 4)) = o;
+              if (k < nk) {
+                uint4 o;
+                o.x = pack_bf16(v[8 * k + 0], v[8 * k + 1]);
+                o.y = pack_bf16(v[8 * k + 2], v[8 * k + 3]);
+                o.z = pack_bf16(v[8 * k + 4], v[8 * k + 5]);
+                o.w = pack_bf16(v[8 * k + 6], v[8 * k + 7]);
+                *reinterpret_cast<uint4*>(my_out + lane * 64 + ((k ^ (lane & 3)) << 4)) = o;
+              }
             }
             __syncwarp();
             const int mt0 = mt * GEMM_BM + quarter * 32;
+            const int rows_per = 32 / nk;    // rows written per warp instruction
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int rr = i * 8 + (lane >> 2), k = lane & 3;
-              const int mrow = mt0 + rr;
-              const int mo2 = mrow / args.Mi, mi2 = mrow - mo2 * args.Mi;
-              const uint4 o =
-                  *reinterpret_cast<const uint4*>(my_out + rr * 64 + ((k ^ (rr & 3)) << 4));
-              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.outV) +
-                                        (size_t)g * args.sVg + (size_t)mo2 * args.sVmo +
-                                        (size_t)mi2 * args.sVmi + n0 + k * 8) = o;
+            for (int i = 0; i < 8; ++i) {
+              if (i < nk) {
+                const int rr = i * rows_per + lane / nk, k = lane % nk;
+                const int mrow = mt0 + rr;
+                const int mo2 = mrow / args.Mi, mi2 = mrow - mo2 * args.Mi;
+                const uint4 o =
+                    *reinterpret_cast<const uint4*>(my_out + rr * 64 + ((k ^ (rr & 3)) << 4));
+                *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.outV) +
+                                          (size_t)g * args.sVg + (size_t)mo2 * args.sVmo +
+                                          (size_t)mi2 * args.sVmi + n0 + k * 8) = o;
+              }
             }
             __syncwarp();
           } else {
+            const int nk4 = gcols / 4;       // 16-byte chunks per row (fp32)
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-              *reinterpret_cast<float4*>(my_out + lane * 128 + ((k ^ (lane & 7)) << 4)) =
-                  make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+              if (k < nk4)
+                *reinterpret_cast<float4*>(my_out + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+                    make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
             __syncwarp();
             const int mt0 = mt * GEMM_BM + quarter * 32;
+            const int rows_per = 32 / nk4;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              const int rr = i * 4 + (lane >> 3), k = lane & 7;
-              const int mrow = mt0 + rr;
-              const int mo2 = mrow / args.Mi, mi2 = mrow - mo2 * args.Mi;
-              const float4 o =
-                  *reinterpret_cast<const float4*>(my_out + rr * 128 + ((k ^ (rr & 7)) << 4));
-              *reinterpret_cast<float4*>(reinterpret_cast<float*>(args.outV) +
-                                         (size_t)g * args.sVg + (size_t)mo2 * args.sVmo +
-                                         (size_t)mi2 * args.sVmi + n0 + k * 4) = o;
+              if (i < nk4) {
+                const int rr = i * rows_per + lane / nk4, k = lane % nk4;
+                const int mrow = mt0 + rr;
+                const int mo2 = mrow / args.Mi, mi2 = mrow - mo2 * args.Mi;
+                const float4 o =
+                    *reinterpret_cast<const float4*>(my_out + rr * 128 + ((k ^ (rr & 7)) << 4));
+                *reinterpret_cast<float4*>(reinterpret_cast<float*>(args.outV) +
+                                           (size_t)g * args.sVg + (size_t)mo2 * args.sVmo +
+                                           (size_t)mi2 * args.sVmi + n0 + k * 4) = o;
+              }
             }
             __syncwarp();
           }

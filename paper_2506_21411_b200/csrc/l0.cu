@@ -190,7 +190,10 @@ constexpr uint32_t L0_SLOT_COLS = 4 * 32;          // A slot: 64 bf16 K per head
 // the stage): an already-completed mbarrier try_wait costs ~157 cycles on B200 against ~20
 // for bar.sync, and a global load consumed one stage later still exposed ~800 cycles of L2
 // latency per stage (tools/sync_probe.cu, tools/l0_trace.py).
-template <int PP, int L0_NH>
+// CL = 2: a CTA pair (same node and head group, adjacent row tiles) splits the B blocks of
+// every stage between its two producers and multicasts them, halving the weight fill per CTA
+// (the kernel is L2->SMEM fill bound); empty[] then counts both CTAs' MMA commits.
+template <int PP, int L0_NH, int CL>
 __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
   constexpr int CG = 64 / PP;        // channels per main stage (K = 64 per head per stage)
   constexpr int P = PP == 64 ? 8 : 4;
@@ -210,10 +213,20 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
   const int R = a.B * a.S;
   const int n_tiles = R / 128;
   const int HG = a.H / L0_NH;
-  const int total_units = a.n_nodes * n_tiles * HG;
+  const int crank = CL > 1 ? (int)cluster_rank() : 0;
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  const int total_units = a.n_nodes * (n_tiles / CL) * HG;  // cluster units
+  const uint16_t cmask = (uint16_t)((1u << CL) - 1);
   const bool rowp = a.p_row_mode != 0;
+  // cluster unit u -> (head group, this CTA's row tile, node)
+  auto decode = [&](int u, int& hg, int& tile, int& n) {
+    hg = u % HG;
+    const int rest = u / HG;
+    tile = (rest % (n_tiles / CL)) * CL + crank;
+    n = rest / (n_tiles / CL);
+  };
   auto unit_stages = [&](int u, int& g, int& nmain, int& next) {
-    const int n = (u / HG) / n_tiles;
+    const int n = (u / HG) / (n_tiles / CL);
     g = __ldg(a.node_g + n);
     nmain = (g + CG - 1) / CG;
     next = (g + 15) / 16;
@@ -222,7 +235,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < L0_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);
     }
     mbar_init(&aempty[0], 1);
     mbar_init(&aempty[1], 1);
@@ -232,6 +245,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
   if (warp == 1) tmem_alloc(tslot, 512);
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync();  // the peer multicasts into our barriers from here on
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
@@ -240,11 +254,9 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-        const int hg = u % HG;
-        const int rest = u / HG;
-        const int tile = rest % n_tiles;
-        const int n = rest / n_tiles;
+      for (int u = cid; u < total_units; u += ncl) {
+        int hg, tile, n;
+        decode(u, hg, tile, n);
         const int c0 = __ldg(a.node_c0 + n);
         int g, nmain, next;
         unit_stages(u, g, nmain, next);
@@ -274,11 +286,12 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
                         128 * PP * 2, &full[stage]);
               if (rowp) bulk_load(sP + cc * PROW, pslice(c), PROW, &full[stage]);
             }
-            for (int h = 0; h < L0_NH; ++h)
-              bulk_load(sB + h * (L0_DH * 64 * 2),
-                        a.Mt + ((long long)(hg * L0_NH + h) * a.C_pad + c0 + st * CG) *
-                                   (L0_DH * PP),
-                        L0_DH * 64 * 2, &full[stage]);
+            for (int h = crank * (L0_NH / CL); h < (crank + 1) * (L0_NH / CL); ++h) {
+              const __nv_bfloat16* src =
+                  a.Mt + ((long long)(hg * L0_NH + h) * a.C_pad + c0 + st * CG) * (L0_DH * PP);
+              if (CL == 1) bulk_load(sB + h * (L0_DH * 64 * 2), src, L0_DH * 64 * 2, &full[stage]);
+              else bulk_load_mc(sB + h * (L0_DH * 64 * 2), src, L0_DH * 64 * 2, &full[stage], cmask);
+            }
           } else {
             const int e = st - nmain;
             const int ce = min(16, g - 16 * e);
@@ -286,11 +299,12 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
             if (rowp)
               for (int cc = 0; cc < ce; ++cc)
                 bulk_load(sI + cc * PROW, pslice(16 * e + cc), PROW, &full[stage]);
-            for (int h = 0; h < L0_NH; ++h)
-              bulk_load(sB + h * (L0_DH * 64 * 2),
-                        a.Et + ((long long)n * a.H + hg * L0_NH + h) * (L0_DH * a.KE) +
-                            e * 16 * L0_DH,
-                        L0_DH * 16 * 2, &full[stage]);
+            for (int h = crank * (L0_NH / CL); h < (crank + 1) * (L0_NH / CL); ++h) {
+              const __nv_bfloat16* src = a.Et + ((long long)n * a.H + hg * L0_NH + h) *
+                                                    (L0_DH * a.KE) + e * 16 * L0_DH;
+              if (CL == 1) bulk_load(sB + h * (L0_DH * 64 * 2), src, L0_DH * 16 * 2, &full[stage]);
+              else bulk_load_mc(sB + h * (L0_DH * 64 * 2), src, L0_DH * 16 * 2, &full[stage], cmask);
+            }
           }
           if (++stage == L0_STAGES) { stage = 0; phase ^= 1; }
         }
@@ -298,26 +312,18 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
     }
   } else if (warp == 1) {
     // ------------------------------------------------ gate: slot waits + MMA issue
-    // Order per stage q: READY(q) -> issue(q) -> wait A slot of q+1 (MMAs of q-1 done) ->
-    // SLOT(q+1).  The MMAs of q+1 are thus queued while those of q run.
+    // Per stage q: READY(q) -> issue the stage's MMAs -> commit (stage + A slot).  The builders
+    // wait on the A-slot mbarrier themselves, so a slot hand-off costs one commit->mbarrier
+    // hop plus one named-barrier hop.
     const uint32_t idesc = idesc_bf16_f32(128, L0_DH);
     long long q_total = 0;
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+    for (int u = cid; u < total_units; u += ncl) {
       int g, nmain, next;
       unit_stages(u, g, nmain, next);
       q_total += nmain + next;
     }
-    auto slot_free = [&](long long q) {
-      if (q < q_total) {
-        mbar_wait(&aempty[q & 1], (uint32_t)(((q >> 1) & 1) ^ 1));
-        if (lane == 0) L0_TRACE(1, q);
-        tc_fence_after();
-        asm volatile("bar.arrive %0, %1;" ::"r"(5 + (int)(q & 1)), "r"(NBAR) : "memory");
-      }
-    };
-    slot_free(0);
     long long q = 0;
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+    for (int u = cid; u < total_units; u += ncl) {
       int g, nmain, next;
       unit_stages(u, g, nmain, next);
       for (int st = 0; st < nmain + next; ++st, ++q) {
@@ -344,18 +350,18 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
               mma_ts(tbase + h * L0_DH, at0 + h * 32,
                      bd0 + (uint64_t)((h * (L0_DH * 64 * 2)) >> 4), idesc, 1u);
           }
-          mma_commit(&empty[cs]);
+          if (CL == 1) mma_commit(&empty[cs]);
+          else mma_commit_mc(&empty[cs], cmask);  // the peer multicasts into this stage too
           mma_commit(&aempty[cl]);
           if (st == nmain + next - 1) mma_commit(accfull);
         }
         __syncwarp();
-        slot_free(q + 1);
       }
     }
   } else if (warp == 2) {
     // ------------------------------------------------ image gate: full(q) -> IMG(q)
     long long q_total = 0;
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+    for (int u = cid; u < total_units; u += ncl) {
       int g, nmain, next;
       unit_stages(u, g, nmain, next);
       q_total += nmain + next;
@@ -367,117 +373,138 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
     }
   } else {
     // ------------------------------------------------ builders + epilogue (warps 3..10)
-    constexpr int HW = L0_NH / 2;       // heads per builder warp
+    // Two builder warps per TMEM lane quarter split each stage's K = 64 into halves
+    // (kh = 0: K 0..31, kh = 1: K 32..63) for all NH heads, so every image row is read from
+    // shared memory exactly once (smem bandwidth is shared with TMA writes and MMA reads).
+    constexpr int HW = L0_NH / 2;       // epilogue: heads drained per warp
     const int quarter = warp & 3;
-    const int hh = (warp - 3) >> 2;
+    const int hh = (warp - 3) >> 2;     // K half (build) / head half (epilogue)
     const int m = quarter * 32 + lane;  // row within tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint8_t* my_out = stage_out + (warp - 3) * (32 * 64);
     uint32_t accphase = 0;
     long long q = 0;
     const int i_l = m / a.wp, jj = m - (m / a.wp) * a.wp;
-    // this warp's HW heads of one channel, packed bf16 (HW == 1: low half)
-    auto p_smem = [&](const uint8_t* base, int cc) -> uint32_t {
-      const uint8_t* src = base + cc * PROW + (m * L0_NH + hh * HW) * 2;
-      return HW == 2 ? *reinterpret_cast<const uint32_t*>(src)
-                     : (uint32_t)*reinterpret_cast<const uint16_t*>(src);
+    // all NH heads of one channel for this row, packed bf16 pairs (heads 0-1, 2-3)
+    auto p_smem = [&](const uint8_t* base, int cc, uint32_t (&o)[2]) {
+      const uint8_t* src = base + cc * PROW + m * L0_NH * 2;
+      if (L0_NH == 4) {
+        const uint2 v = *reinterpret_cast<const uint2*>(src);
+        o[0] = v.x; o[1] = v.y;
+      } else {
+        o[0] = *reinterpret_cast<const uint32_t*>(src); o[1] = 0u;
+      }
     };
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-      const int hg = u % HG;
-      const int rest = u / HG;
-      const int tile = rest % n_tiles;
-      const int n = rest / n_tiles;
+    for (int u = cid; u < total_units; u += ncl) {
+      int hg, tile, n;
+      decode(u, hg, tile, n);
       int g, nmain, next;
       unit_stages(u, g, nmain, next);
       const long long poff = __ldg(a.node_poff + n);
       // constant p table (linear-mix nodes): p[poff + c*H + h]
-      auto p_const = [&](int c) -> uint32_t {
-        const __nv_bfloat16* src = a.p + poff + (long long)c * a.H + hg * L0_NH + hh * HW;
-        return HW == 2 ? __ldg(reinterpret_cast<const unsigned int*>(src))
-                       : (uint32_t)__bfloat16_as_ushort(src[0]);
+      auto p_const = [&](int c, uint32_t (&o)[2]) {
+        const __nv_bfloat16* src = a.p + poff + (long long)c * a.H + hg * L0_NH;
+        if (L0_NH == 4) {
+          const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
+          o[0] = v.x; o[1] = v.y;
+        } else {
+          o[0] = __ldg(reinterpret_cast<const unsigned int*>(src)); o[1] = 0u;
+        }
       };
       for (int st = 0; st < nmain + next; ++st, ++q) {
         const int cs = (int)(q % L0_STAGES), cl = (int)(q & 1);
         const uint8_t* sI = smem + cs * L0_STAGE_BYTES;
         const uint8_t* sP = sI + L0_IMG_BYTES;
-        uint32_t y[HW][32];
+        uint32_t y[L0_NH][16];
         asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(q & 3)), "r"(NBAR) : "memory");  // IMG
         if (warp == 3 && lane == 0) L0_TRACE(3, q);
-        int ncols = 32;
+        const bool ext = st >= nmain;
         if (a.debug_mode & 1) {
 #pragma unroll
-          for (int h = 0; h < HW; ++h)
+          for (int h = 0; h < L0_NH; ++h)
 #pragma unroll
-            for (int e = 0; e < 32; ++e) y[h][e] = 0u;
-        } else if (st < nmain) {
-          uint32_t x[32], pv[CG];
+            for (int e = 0; e < 16; ++e) y[h][e] = 0u;
+        } else if (!ext) {
+          // this warp's 16 of the 32 A columns: P == 8 -> pixel rows 4kh..4kh+3 of the one
+          // channel; P == 4 -> channels 2kh, 2kh+1 of the stage's four
+          constexpr int NCC = CG == 1 ? 1 : 2;  // channels touched by this K half
+          uint32_t x[16], pv[NCC][2];
 #pragma unroll
-          for (int cc = 0; cc < CG; ++cc) {
+          for (int ci = 0; ci < NCC; ++ci) {
+            const int cc = CG == 1 ? 0 : 2 * hh + ci;
             const int c = st * CG + cc;
             const bool valid = c < g;
-            pv[cc] = !valid ? 0u : (rowp ? p_smem(sP, cc) : p_const(c));
+            if (!valid) {
+              pv[ci][0] = pv[ci][1] = 0u;
+            } else if (rowp) {
+              p_smem(sP, cc, pv[ci]);
+            } else {
+              p_const(c, pv[ci]);
+            }
             const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(
                                             sI + cc * 128 * PP * 2) +
                                         (i_l * P) * a.W + jj * P;
+            if (P == 8) {
 #pragma unroll
-            for (int py = 0; py < P; ++py) {
-              if (P == 8) {
-                uint4 v = valid ? *reinterpret_cast<const uint4*>(base + py * a.W)
-                                : make_uint4(0, 0, 0, 0);
-                x[cc * 32 + py * 4 + 0] = v.x; x[cc * 32 + py * 4 + 1] = v.y;
-                x[cc * 32 + py * 4 + 2] = v.z; x[cc * 32 + py * 4 + 3] = v.w;
-              } else {
-                uint2 v = valid ? *reinterpret_cast<const uint2*>(base + py * a.W)
-                                : make_uint2(0, 0);
-                x[cc * 8 + py * 2 + 0] = v.x; x[cc * 8 + py * 2 + 1] = v.y;
+              for (int r4 = 0; r4 < 4; ++r4) {
+                const int py = 4 * hh + r4;
+                const uint4 v = valid ? *reinterpret_cast<const uint4*>(base + py * a.W)
+                                      : make_uint4(0, 0, 0, 0);
+                x[r4 * 4 + 0] = v.x; x[r4 * 4 + 1] = v.y; x[r4 * 4 + 2] = v.z; x[r4 * 4 + 3] = v.w;
+              }
+            } else {
+#pragma unroll
+              for (int py = 0; py < 4; ++py) {
+                const uint2 v = valid ? *reinterpret_cast<const uint2*>(base + py * a.W)
+                                      : make_uint2(0, 0);
+                x[ci * 8 + py * 2 + 0] = v.x; x[ci * 8 + py * 2 + 1] = v.y;
               }
             }
           }
 #pragma unroll
-          for (int h = 0; h < HW; ++h) {
+          for (int h = 0; h < L0_NH; ++h) {
 #pragma unroll
-            for (int cc = 0; cc < CG; ++cc) {
-              const uint32_t w = pv[cc];
+            for (int ci = 0; ci < NCC; ++ci) {
+              const uint32_t w = pv[ci][h >> 1];
               const uint32_t ph = (h & 1) ? (w & 0xffff0000u) | (w >> 16)
                                           : (w << 16) | (w & 0xffffu);
 #pragma unroll
-              for (int e = 0; e < 32 / CG; ++e)
-                y[h][cc * (32 / CG) + e] = mul_bf16x2(x[cc * (32 / CG) + e], ph);
+              for (int e = 0; e < 16 / NCC; ++e)
+                y[h][ci * (16 / NCC) + e] = mul_bf16x2(x[ci * (16 / NCC) + e], ph);
             }
           }
         } else {
-          // ext stage e: A[r, k] = p[r, 16e + k, h] (k < 16), one MMA K-step per head
+          // ext stage e: A[r, k] = p[r, 16e + k, h] (k < 16); this warp: k in [8hh, 8hh+8)
           const int e = st - nmain;
-          ncols = 8;
 #pragma unroll
-          for (int kc = 0; kc < 8; ++kc) {
-            const int c0e = 16 * e + 2 * kc;
-            const uint32_t lo = c0e < g ? (rowp ? p_smem(sI, 2 * kc) : p_const(c0e)) : 0u;
-            const uint32_t hi = c0e + 1 < g ? (rowp ? p_smem(sI, 2 * kc + 1) : p_const(c0e + 1))
-                                            : 0u;
+          for (int kc = 0; kc < 4; ++kc) {
+            const int cl0 = 8 * hh + 2 * kc;          // channel within the ext block
+            const int c0e = 16 * e + cl0;
+            uint32_t lo[2] = {0u, 0u}, hi[2] = {0u, 0u};
+            if (c0e < g) { if (rowp) p_smem(sI, cl0, lo); else p_const(c0e, lo); }
+            if (c0e + 1 < g) { if (rowp) p_smem(sI, cl0 + 1, hi); else p_const(c0e + 1, hi); }
 #pragma unroll
-            for (int h = 0; h < HW; ++h) {
-              const uint32_t a16 = (h & 1) ? (lo >> 16) : (lo & 0xffffu);
-              const uint32_t b16 = (h & 1) ? (hi >> 16) : (hi & 0xffffu);
+            for (int h = 0; h < L0_NH; ++h) {
+              const uint32_t a16 = (h & 1) ? (lo[h >> 1] >> 16) : (lo[h >> 1] & 0xffffu);
+              const uint32_t b16 = (h & 1) ? (hi[h >> 1] >> 16) : (hi[h >> 1] & 0xffffu);
               y[h][kc] = a16 | (b16 << 16);
             }
           }
         }
         if (warp == 3 && lane == 0) L0_TRACE(4, q);
-        asm volatile("bar.sync %0, %1;" ::"r"(5 + cl), "r"(NBAR) : "memory");  // SLOT free
+        // A slot free: the MMAs of stage q-2 (same slot) have completed
+        mbar_wait(&aempty[cl], (uint32_t)(((q >> 1) & 1) ^ 1));
         if (warp == 3 && lane == 0) L0_TRACE(5, q);
         tc_fence_after();
         const uint32_t slot_t = tbase + lane_off + L0_ACC_COLS + cl * L0_SLOT_COLS;
-        if (ncols == 32) {
+        if (!ext) {
 #pragma unroll
-          for (int h = 0; h < HW; ++h) tmem_st32(slot_t + (hh * HW + h) * 32, y[h]);
+          for (int h = 0; h < L0_NH; ++h) tmem_st16(slot_t + h * 32 + 16 * hh, y[h]);
         } else {
 #pragma unroll
-          for (int h = 0; h < HW; ++h) {
-            uint32_t y8[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) y8[k] = y[h][k];
-            tmem_st8(slot_t + (hh * HW + h) * 32, y8);
+          for (int h = 0; h < L0_NH; ++h) {
+            uint32_t y4[4] = {y[h][0], y[h][1], y[h][2], y[h][3]};
+            tmem_st4(slot_t + h * 32 + 4 * hh, y4);
           }
         }
         tmem_st_wait();
@@ -526,6 +553,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
 
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tbase, 512);
@@ -537,15 +565,36 @@ cudaError_t launch_l0_node(const L0NodeArgs& a, int num_sms, cudaStream_t st) {
   const int nh = a.H % 4 == 0 ? 4 : 2;
   if (R % 128 || a.S % 128 || 128 % a.wp || a.H % nh || a.D != a.H * L0_DH || a.KE % 16)
     return cudaErrorInvalidValue;
-  const int units = a.n_nodes * (R / 128) * (a.H / nh);
-  const int grid = units < num_sms ? units : num_sms;
+  const int n_tiles = R / 128;
+  const int CL = (n_tiles % 2 == 0 && a.cluster != 1) ? 2 : 1;
+  const int units = a.n_nodes * (n_tiles / CL) * (a.H / nh);
+  const int max_cl = num_sms / CL;
+  const int grid = (units < max_cl ? units : max_cl) * CL;
   void (*kern)(L0NodeArgs) = nullptr;
-  if (a.P == 8) kern = nh == 4 ? l0_node_kernel<64, 4> : l0_node_kernel<64, 2>;
-  else if (a.P == 4) kern = nh == 4 ? l0_node_kernel<16, 4> : l0_node_kernel<16, 2>;
-  else return cudaErrorInvalidValue;
+  if (a.P == 8)
+    kern = nh == 4 ? (CL == 2 ? l0_node_kernel<64, 4, 2> : l0_node_kernel<64, 4, 1>)
+                   : (CL == 2 ? l0_node_kernel<64, 2, 2> : l0_node_kernel<64, 2, 1>);
+  else if (a.P == 4)
+    kern = nh == 4 ? (CL == 2 ? l0_node_kernel<16, 4, 2> : l0_node_kernel<16, 4, 1>)
+                   : (CL == 2 ? l0_node_kernel<16, 2, 2> : l0_node_kernel<16, 2, 1>);
+  else
+    return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L0_SMEM);
   if (e != cudaSuccess) return e;
-  kern<<<grid, L0_THREADS, L0_SMEM, st>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(L0_THREADS);
+  cfg.dynamicSmemBytes = L0_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

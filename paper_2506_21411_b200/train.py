@@ -61,6 +61,11 @@ def _gemm(A, W_dn, bias=None, out_f32=False, rowbias=None, period=1, N_logit=0):
     return (V, L) if N_logit else V
 
 
+def _mm(a, b):
+    """Plain GEMM on tensor cores: bf16 operands, fp32 accumulate (cuBLAS), fp32 result."""
+    return torch.matmul(a.to(torch.bfloat16), b.to(torch.bfloat16)).float()
+
+
 def _u_backward(w, prefix, dU, heads):
     """Gradients of wk, q, wq from dU where U[:,h] = wk[:,h-blk] q'[h-blk]/sqrt(dh), q' = q wq."""
     wk, wq, q = w[f"{prefix}.wk"], w[f"{prefix}.wq"], w[f"{prefix}.q"]
@@ -267,12 +272,12 @@ class DchagTrainer:
         # ---- final layer (replicated)
         ctx_f = saved["ctx_f"][0].float()
         grads["agg.final.bo"] = g_out.sum(0)
-        grads["agg.final.wo"] = ctx_f.t() @ g_out
+        grads["agg.final.wo"] = _mm(ctx_f.t(), g_out)
         g_ctx = (g_out @ w["agg.final.wo"].t()).view(1, R, d)
         gV, dL, _ = self._combine_bwd(saved["Vf"], saved["Lf"], None, g_ctx, [0], [fe.tp], R)
-        y_all = saved["y_all"].float().reshape(fe.tp * R, d)
-        grads["agg.final.wv"] = y_all.t() @ gV.float().reshape(fe.tp * R, d)
-        dU = y_all.t() @ dL.reshape(fe.tp * R, h)
+        y_all = saved["y_all"].reshape(fe.tp * R, d)
+        grads["agg.final.wv"] = _mm(y_all.t(), gV.reshape(fe.tp * R, d))
+        dU = _mm(y_all.t(), dL.reshape(fe.tp * R, h))
         grads.update(_u_backward(w, "agg.final", dU, h))
         U_f = query_logit_weights(w, "agg.final", h)
         # local slice of the gathered gradient (strategies.py:91-94): no collective
@@ -294,7 +299,7 @@ class DchagTrainer:
         # ---- levels >= 1, top down
         for li in range(len(levels) - 1, 0, -1):
             level = levels[li]
-            ctx = saved["ctx"][li].float()
+            ctx = saved["ctx"][li]
             V, L = saved["VL"][li - 1]
             y_prev = saved["y"][li - 1]
             G = torch.empty(len(level), R, d, device=g_y.device, dtype=torch.float32)
@@ -302,8 +307,8 @@ class DchagTrainer:
                 node = f"{pre}.l{li}.g{gi}"
                 if attn:
                     grads[f"{node}.bo"] = g_y[gi].sum(0)
-                    grads[f"{node}.wo"] = ctx[gi].t() @ g_y[gi]
-                    G[gi] = g_y[gi] @ w[f"{node}.wo"].t()
+                    grads[f"{node}.wo"] = _mm(ctx[gi].t(), g_y[gi])
+                    G[gi] = _mm(g_y[gi], w[f"{node}.wo"].t())
                 else:
                     grads[f"{node}.b"] = g_y[gi].sum(0)
                     G[gi] = g_y[gi]
@@ -317,23 +322,23 @@ class DchagTrainer:
             g_prev = torch.empty(y_prev.shape, device=g_y.device, dtype=torch.float32)
             for gi, (f0, g) in enumerate(zip(firsts, level)):
                 node = f"{pre}.l{li}.g{gi}"
-                Y = y_prev[f0:f0 + g].float().reshape(g * R, d)
-                gv = gV[f0:f0 + g].float().reshape(g * R, d)
+                Y = y_prev[f0:f0 + g].reshape(g * R, d)
+                gv = gV[f0:f0 + g].reshape(g * R, d)
                 if attn:
                     dl = dL[f0:f0 + g].reshape(g * R, h)
-                    grads[f"{node}.wv"] = Y.t() @ gv
-                    grads.update(_u_backward(w, node, Y.t() @ dl, h))
+                    grads[f"{node}.wv"] = _mm(Y.t(), gv)
+                    grads.update(_u_backward(w, node, _mm(Y.t(), dl), h))
                     U = query_logit_weights(w, node, h)
-                    g_prev[f0:f0 + g] = (gv @ w[f"{node}.wv"].t() + dl @ U.t()).view(g, R, d)
+                    g_prev[f0:f0 + g] = (_mm(gv, w[f"{node}.wv"].t()) + dl @ U.t()).view(g, R, d)
                 else:
-                    grads[f"{node}.w"] = Y.t() @ gv
+                    grads[f"{node}.w"] = _mm(Y.t(), gv)
                     grads[f"{node}.mix"] = dm[f0:f0 + g].sum(1)
-                    g_prev[f0:f0 + g] = (gv @ w[f"{node}.w"].t()).view(g, R, d)
+                    g_prev[f0:f0 + g] = _mm(gv, w[f"{node}.w"].t()).view(g, R, d)
             g_y = g_prev
         # ---- level 0: node output, then tokens recomputed node by node
         off, cnt = fe.slab
         img = saved["img"]
-        ctx0 = saved["ctx"][0].float()
+        ctx0 = saved["ctx"][0]
         pos = w["special.pos"]
         tokw = w["tok.w"][off:off + cnt]
         tb = (w["tok.b"] + w["special.channel_id"])[off:off + cnt]
@@ -348,8 +353,8 @@ class DchagTrainer:
             node = f"{pre}.l0.g{gi}"
             if attn:
                 grads[f"{node}.bo"] = g_y[gi].sum(0)
-                grads[f"{node}.wo"] = ctx0[gi].t() @ g_y[gi]
-                G = (g_y[gi] @ w[f"{node}.wo"].t()).view(1, R, d)
+                grads[f"{node}.wo"] = _mm(ctx0[gi].t(), g_y[gi])
+                G = _mm(g_y[gi], w[f"{node}.wo"].t()).view(1, R, d)
             else:
                 grads[f"{node}.b"] = g_y[gi].sum(0)
                 G = g_y[gi].view(1, R, d)
@@ -361,25 +366,24 @@ class DchagTrainer:
                 V, L = _gemm(Xf, torch.cat([w[f"{node}.wv"], U], dim=1), N_logit=h)
                 gV, dL, _ = self._combine_bwd(V.view(g, R, d), L.view(g, R, h).contiguous(), None,
                                               G, [0], [g], R)
-                gv = gV.float().reshape(g * R, d)
+                gv = gV.reshape(g * R, d)
                 dl = dL.reshape(g * R, h)
-                Xf32 = Xf.float()
-                grads[f"{node}.wv"] = Xf32.t() @ gv
-                grads.update(_u_backward(w, node, Xf32.t() @ dl, h))
-                gX = gv @ w[f"{node}.wv"].t() + dl @ U.t()
+                grads[f"{node}.wv"] = _mm(Xf.t(), gv)
+                grads.update(_u_backward(w, node, _mm(Xf.t(), dl), h))
+                gX = torch.addmm(_mm(dl, U.t()).to(torch.bfloat16), gv, _bf(w[f"{node}.wv"].t()))
             else:
                 V = _gemm(Xf, w[f"{node}.w"])
                 mix = w[f"{node}.mix"].float().contiguous()
                 gV, _, dm = self._combine_bwd(V.view(g, R, d), None, mix, G, [0], [g], R)
-                gv = gV.float().reshape(g * R, d)
-                grads[f"{node}.w"] = Xf.float().t() @ gv
+                gv = gV.reshape(g * R, d)
+                grads[f"{node}.w"] = _mm(Xf.t(), gv)
                 grads[f"{node}.mix"] = dm.sum(1)
-                gX = gv @ w[f"{node}.w"].t()
-            gX = gX.view(g, B, s, d)
-            pt = patches[:, c0:c0 + g].float().permute(1, 0, 2, 3).reshape(g, B * s, P * P)
-            d_tokw[c0:c0 + g] = torch.bmm(pt.transpose(1, 2), gX.reshape(g, B * s, d))
-            d_tb[c0:c0 + g] = gX.sum((1, 2))
-            d_pos += gX.sum((0, 1))
+                gX = torch.matmul(gv, _bf(w[f"{node}.w"].t()))
+            gX = gX.view(g, B, s, d)                                     # bf16
+            pt = patches[:, c0:c0 + g].permute(1, 0, 2, 3).reshape(g, B * s, P * P)
+            d_tokw[c0:c0 + g] = torch.bmm(pt.transpose(1, 2), gX.reshape(g, B * s, d)).float()
+            d_tb[c0:c0 + g] = gX.sum((1, 2), dtype=torch.float32)
+            d_pos += gX.sum((0, 1), dtype=torch.float32)
             c0 += g
         grads["tok.w"] = d_tokw
         grads["tok.b"] = d_tb

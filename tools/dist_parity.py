@@ -51,6 +51,36 @@ def main():
         worst = max(worst, err)
         print(f"rank {rank}/{tp} C={meta['channels']} slab={fe.slab} {lk}: rel_err={err:.3e}",
               flush=True)
+    # training step over NCCL: forward_train (AllGather of root streams) + backward
+    # (local-slice boundary, special.pos all-reduce), vs float64 autograd of the reference math
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch_reference as TRF
+    from paper_2506_21411_b200.train import DchagTrainer
+    meta = dict(channels=13, image_h=64, image_w=64, patch=8, embed=256, heads=4, max_group=2)
+    specs = O.frontend_param_specs(13, 64, 64, 8, 256, tp, 2)
+    w = O.random_params(specs, seed=9, std=0.05, bias_std=0.02)
+    w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
+    rng = np.random.default_rng(6)
+    img = torch.from_numpy(rng.standard_normal((2, 13, 64, 64)).astype(np.float32)).to(torch.bfloat16)
+    probe = rng.standard_normal((2, 1, 64, 256))
+    img64 = img.float().numpy().astype(np.float64)
+    _, g_ref = TRF.grads(img64, w, probe, patch=8, heads=4, tp=tp, max_group=2)
+    fe = DchagFrontEnd(13, 64, 64, 8, 256, 4, max_group=2, tp=tp, rank=rank,
+                       out_dtype=torch.float32)
+    fe.load_weights(w)
+    trn = DchagTrainer(fe)
+    out, saved = trn.forward_train(img.cuda())
+    grads = trn.backward(saved, torch.from_numpy(probe.astype(np.float32)).cuda())
+    off, cnt = fe.slab
+    errs = {}
+    for k, v in grads.items():
+        v = v.double().cpu().numpy()
+        ref = g_ref[k][off:off + cnt] if k in ("tok.w", "tok.b", "special.channel_id") else g_ref[k]
+        errs[k] = O.rel_err(v, ref)
+    terr = max(errs.values())
+    worst = max(worst, terr)
+    print(f"rank {rank}/{tp} train step: {len(errs)} grads, worst rel_err={terr:.3e} "
+          f"({max(errs, key=errs.get)})", flush=True)
     t = torch.tensor([worst], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
