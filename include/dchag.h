@@ -51,12 +51,15 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
  * WUt bf16 [C][HP][P*P], bU fp32 [C][HP], posU fp32 [n_nodes][S][HP]; HP = H rounded up
  * to a multiple of 8.  Output p bf16, head-group then channel major (a 128-row tile's
  * slice for one (head group, channel) is contiguous, so K_l0 stages it with one bulk copy):
- * p[poff[n] + ((hg*g + c)*R + r)*NH + h%NH], hg = h/NH, NH = 4 if H%4==0 else 2. */
+ * p[poff[n] + ((hg*g + c)*R + r)*NH + h%NH], hg = h/NH, NH = 4 if H%4==0 else 2.
+ * pinv (optional, fp32 [n_nodes][R][H]): when given, p holds the unnormalised
+ * e = exp(logit - max_c logit) and pinv = 1 / sum_c e; dchag_l0_node then applies pinv to
+ * its accumulator (one exp per logit instead of three).  NULL: p is the normalised softmax. */
 int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
                     int P, int H, int HP, int n_nodes, int gmax, const int* node_c0,
                     const int* node_g,
                     const long long* node_poff, const void* WUt, const float* bU,
-                    const float* posU, void* p, void* stream);
+                    const float* posU, void* p, float* pinv, void* stream);
 
 /* Level-0 node context (K_l0, tcgen05 with A in TMEM):
  *   ctx[n][r][h*64:(h+1)*64] = sum_c p[r,c,h] * (patch_c[r] @ M_c[:, h-block])
@@ -66,11 +69,12 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
  * UMMA blocks (dchag_tile_weights); p_row_mode = 1 reads the dchag_l0_logits layout, 0 a constant
  * table p[poff + c*H + h]
  * (linear-mix nodes).  Requires head dim 64, H % 4 == 0, S % 128 == 0, 128 % (W/P) == 0,
- * P in {4, 8}. */
+ * P in {4, 8}.  pinv (optional, the dchag_l0_logits output): ctx row r, head h is scaled by
+ * pinv[n][r][h]. */
 int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
                   int P, int H, int D, int n_nodes, const int* node_c0, const int* node_g,
-                  const long long* node_poff, int p_row_mode, const void* p, const void* Mt,
-                  int C_pad, const void* Et, int KE, void* ctx, void* stream);
+                  const long long* node_poff, int p_row_mode, const void* p, const float* pinv,
+                  const void* Mt, int C_pad, const void* Et, int KE, void* ctx, void* stream);
 
 /* Upper-level / final combine (K_comb): ctx[n][r][:] = sum_j w_j(r,h) V_{first+j}[r][:],
  * w = softmax_j(L_{first+j}[r][h]) (attention; mix == NULL) or mix[first+j] (linear).

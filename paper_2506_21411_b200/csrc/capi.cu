@@ -166,7 +166,7 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
                     int P, int H, int HP, int n_nodes, int gmax, const int* node_c0,
                     const int* node_g,
                     const long long* node_poff, const void* WUt, const float* bU,
-                    const float* posU, void* p, void* stream) {
+                    const float* posU, void* p, float* pinv, void* stream) {
   if (Himg % P || W % P || HP % 8 || HP < H || H % 2 || (P * P) % 16)
     return fail(DCHAG_ERR_SHAPE, "l0_logits: bad shape");
   L0LogitArgs a;
@@ -178,14 +178,18 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
   a.WUt = reinterpret_cast<const __nv_bfloat16*>(WUt);
   a.bU = bU; a.posU = posU;
   a.p = reinterpret_cast<__nv_bfloat16*>(p);
-  if ((B * a.S) % 64) return fail(DCHAG_ERR_SHAPE, "l0_logits: B*S must be a multiple of 64");
+  a.pinv = pinv;
+  if ((B * a.S) % 16) return fail(DCHAG_ERR_SHAPE, "l0_logits: B*S must be a multiple of 16");
+  if ((reinterpret_cast<uintptr_t>(img) | (uintptr_t)(img_sb * 2) | (uintptr_t)(img_sc * 2) |
+       (uintptr_t)(W * 2)) % 16)
+    return fail(DCHAG_ERR_SHAPE, "l0_logits: image base/strides must be 16-byte aligned");
   return cuda_status(launch_l0_logits(a, S(stream)), "l0_logits");
 }
 
 int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
                   int P, int H, int D, int n_nodes, const int* node_c0, const int* node_g,
-                  const long long* node_poff, int p_row_mode, const void* p, const void* Mt,
-                  int C_pad, const void* Et, int KE, void* ctx, void* stream) {
+                  const long long* node_poff, int p_row_mode, const void* p, const float* pinv,
+                  const void* Mt, int C_pad, const void* Et, int KE, void* ctx, void* stream) {
   if (Himg % P || W % P) return fail(DCHAG_ERR_SHAPE, "l0_node: image not divisible by patch");
   L0NodeArgs a;
   a.img = reinterpret_cast<const __nv_bfloat16*>(img);
@@ -194,6 +198,7 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
   a.n_nodes = n_nodes; a.node_c0 = node_c0; a.node_g = node_g; a.node_poff = node_poff;
   a.p_row_mode = p_row_mode;
   a.p = reinterpret_cast<const __nv_bfloat16*>(p);
+  a.pinv = pinv;
   a.Mt = reinterpret_cast<const __nv_bfloat16*>(Mt);
   a.C_pad = C_pad;
   a.Et = reinterpret_cast<const __nv_bfloat16*>(Et);

@@ -39,6 +39,8 @@ struct L0LogitArgs {
   const __nv_bfloat16* WUt;   // [C][HP][PP]  logit weights tok.w[c] @ U_n, transposed
   const float* bU;            // [C][HP]      (tok.b[c]+chan_id[c]) @ U_n
   const float* posU;          // [n_nodes][S][HP]
+  float* pinv;                // optional [n_nodes][R][H]: with it p holds the unnormalised
+                              // e = exp(l - max) and pinv = 1 / sum_c e (K_l0 scales ctx)
   __nv_bfloat16* p;           // p[poff[n] + ((hg*g + c)*R + r)*NH + h%NH], hg = h/NH,
                               // NH = 4 if H % 4 == 0 else 2 (head group of one K_l0 CTA);
                               // a 128-row tile's slice of (hg, c) is one contiguous 1 KB run
@@ -56,6 +58,7 @@ struct L0NodeArgs {
   const long long* node_poff;
   int p_row_mode;              // 1: K_p0 layout (see L0LogitArgs); 0: constant p[poff + c*H + h]
   const __nv_bfloat16* p;
+  const float* pinv;           // optional [n_nodes][R][H] row/head scale of ctx (K_p0 output)
   const __nv_bfloat16* Mt;     // [H][C_pad][dh*PP] canonical no-swizzle K-major blocks
   int C_pad;
   const __nv_bfloat16* Et;     // [n_nodes][H][dh*KE] ext (bias) blocks

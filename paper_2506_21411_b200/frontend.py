@@ -189,7 +189,15 @@ class DchagFrontEnd(torch.nn.Module):
         return self._packed
 
     # ------------------------------------------------------------------ forward
-    def forward(self, images: torch.Tensor, return_payload: bool = False):
+    def forward(self, images: torch.Tensor, return_payload: bool = False, out=None,
+                h2d_chunks: int = 4):
+        """[B, C or slab, H, W] images -> [B, 1, S, D] (model.py:180-201 front end).
+
+        Device images run the rank's kernels on the current stream. Host images (pinned,
+        for overlap) are streamed in `h2d_chunks` batch chunks: the copy of chunk k+1 on a
+        side stream overlaps the kernels of chunk k (positions of different images are
+        independent on this path, so chunking changes no result). `out`, when given, is
+        the result buffer; a host `out` receives each chunk's rows as they finish."""
         pk = self.prepare()
         m = self.model
         if images.dim() != 4:
@@ -203,16 +211,79 @@ class DchagFrontEnd(torch.nn.Module):
         elif cin != cnt:
             raise ConfigError(f"images carry {cin} channels; rank {self.rank} expects {cnt} "
                               f"(its slab) or {m.channels} (all)")
+        if out is not None and (tuple(out.shape) != (b, 1, self.seq, m.embed)
+                                or out.dtype != self.out_dtype or not out.is_contiguous()):
+            raise ConfigError(f"out must be a contiguous {self.out_dtype} tensor of shape "
+                              f"{(b, 1, self.seq, m.embed)}")
+        if not images.is_cuda:
+            if return_payload:
+                raise ConfigError("return_payload needs device images")
+            return self._forward_host(images, pk, out, h2d_chunks)
         if images.dtype != torch.bfloat16:
             images = images.to(torch.bfloat16)
         if images.stride(3) != 1 or images.stride(2) != wimg:
             images = images.contiguous()
-        if not images.is_cuda:
-            raise ConfigError("images must be on the GPU")
         payload = self.local_payload(images, pk)
         gathered = self.gather(payload)
-        out = self.finish(gathered, images.shape[0])
-        return (out, gathered) if return_payload else out
+        dev_out = out if out is not None and out.is_cuda else None
+        res = self.finish(gathered, images.shape[0], out=dev_out)
+        if out is not None and not out.is_cuda:
+            out.copy_(res, non_blocking=True)
+            res = out
+        return (res, gathered) if return_payload else res
+
+    def _forward_host(self, images, pk, out, h2d_chunks):
+        """Chunked H2D -> kernels -> (D2H) pipeline for host-resident images."""
+        b, cnt, himg, wimg = images.shape
+        if images.dtype != torch.bfloat16:
+            images = images.to(torch.bfloat16)  # host-side cast; pass bf16 to avoid it
+        dev = self.device
+        cur = torch.cuda.current_stream(dev)
+        cache = self.__dict__.setdefault("_cache", {})
+        key = ("h2d", dev, b, cnt, himg, wimg)
+        if key not in cache:
+            cache[key] = (torch.empty(b, cnt, himg, wimg, device=dev, dtype=torch.bfloat16),
+                          torch.cuda.Stream(dev))
+        dbuf, side = cache[key]
+        if out is None or out.is_cuda:
+            res = out if out is not None else torch.empty(b, 1, self.seq, self.model.embed,
+                                                          device=dev, dtype=self.out_dtype)
+        else:
+            res = torch.empty(b, 1, self.seq, self.model.embed, device=dev,
+                              dtype=self.out_dtype)
+        n = max(1, min(int(h2d_chunks), b))
+        bounds = [(k * b) // n for k in range(n + 1)]
+        # the staging buffer (and, for a host out, res) may still be read by earlier work
+        side.wait_stream(cur)
+        copied = []
+        contig = images.is_contiguous()
+        for k in range(n):
+            b0, b1 = bounds[k], bounds[k + 1]
+            with torch.cuda.stream(side):
+                if contig:
+                    dbuf[b0:b1].copy_(images[b0:b1], non_blocking=True)
+                else:
+                    for i in range(b0, b1):  # per-image contiguous runs (a channel slab)
+                        dbuf[i].copy_(images[i], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(side)
+            copied.append(ev)
+        for k in range(n):
+            b0, b1 = bounds[k], bounds[k + 1]
+            cur.wait_event(copied[k])
+            payload = self.local_payload(dbuf[b0:b1], pk)
+            gathered = self.gather(payload)
+            self.finish(gathered, b1 - b0, out=res[b0:b1])
+            if out is not None and not out.is_cuda:
+                done = torch.cuda.Event()
+                done.record(cur)
+                side.wait_event(done)
+                with torch.cuda.stream(side):
+                    out[b0:b1].copy_(res[b0:b1], non_blocking=True)
+        if out is not None and not out.is_cuda:
+            cur.wait_stream(side)
+            return out
+        return res
 
     def launch_plan(self, B: int):
         """Kernel launches of one forward in launch order, with the algorithmic work each
@@ -278,19 +349,23 @@ class DchagFrontEnd(torch.nn.Module):
                 acc += g * R * h
             poff = torch.tensor(poff_list, device=dev, dtype=torch.int64)
             pbuf = torch.empty(acc, **bf16)
+            # unnormalised e + 1/sum: K_l0 scales its accumulator (one exp per logit)
+            pinv = torch.empty(pk.n0, R, h, **f32)
             _lib.call("dchag_l0_logits", _lib.ptr(img), isb, isc, B, m.image_h, m.image_w, p,
                       h, pk.HP, pk.n0, max(pk.l0_g_list), _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g),
                       _lib.ptr(poff),
-                      _lib.ptr(pk.WUt), _lib.ptr(pk.bU), _lib.ptr(pk.posU), _lib.ptr(pbuf), st)
+                      _lib.ptr(pk.WUt), _lib.ptr(pk.bU), _lib.ptr(pk.posU), _lib.ptr(pbuf),
+                      _lib.ptr(pinv), st)
             prow = 1
         else:
             poff = (pk.l0_c0.to(torch.int64) * h).contiguous()
             pbuf = pk.p_const
+            pinv = None
             prow = 0
         ctx = torch.empty(pk.n0, R, d, **bf16)
         _lib.call("dchag_l0_node", _lib.ptr(img), isb, isc, B, m.image_h, m.image_w, p, h, d,
                   pk.n0, _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g), _lib.ptr(poff), prow,
-                  _lib.ptr(pbuf), _lib.ptr(pk.Mt), pk.C_pad, _lib.ptr(pk.Et), pk.KE,
+                  _lib.ptr(pbuf), _lib.ptr(pinv), _lib.ptr(pk.Mt), pk.C_pad, _lib.ptr(pk.Et), pk.KE,
                   _lib.ptr(ctx), st)
 
         depth = len(pk.levels)
@@ -322,7 +397,7 @@ class DchagFrontEnd(torch.nn.Module):
                           _lib.ptr(ctx), st)
         return payload
 
-    def finish(self, gathered, B):
+    def finish(self, gathered, B, out=None):
         """Shared final layer over the gathered streams -> [B, 1, S, D]."""
         pk = self.prepare()
         m = self.model
@@ -345,7 +420,8 @@ class DchagFrontEnd(torch.nn.Module):
                       _lib.ptr(ctx_f), st)
         else:
             ctx_f = Vg[:R * d].view(1, R, d)  # softmax over one stream is exactly 1
-        out = torch.empty(R, d, device=dev, dtype=self.out_dtype)
+        if out is None:
+            out = torch.empty(R, d, device=dev, dtype=self.out_dtype)
         _lib.call("dchag_gemm_bf16", _lib.ptr(ctx_f), 1, 1, R, d, R * d, 0, d, _lib.ptr(pk.Wf),
                   d, d * d, d, _lib.ptr(pk.bf), d, 0, 0, 0, 1, _lib.ptr(out),
                   int(self.out_dtype == torch.float32), R * d, 0, d, 0, 0, 0, 0, st)

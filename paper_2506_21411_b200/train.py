@@ -114,18 +114,19 @@ class DchagTrainer:
                 acc += g * R * h
             poff_t = torch.tensor(poff, device=dev, dtype=torch.int64)
             pbuf = torch.empty(acc, device=dev, dtype=torch.bfloat16)
+            pinv = torch.empty(pk.n0, R, h, device=dev, dtype=torch.float32)
             _lib.call("dchag_l0_logits", _lib.ptr(img), img.stride(0), img.stride(1), B,
                       m.image_h, m.image_w, m.patch, h, pk.HP, pk.n0, max(pk.l0_g_list),
                       _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g), _lib.ptr(poff_t), _lib.ptr(pk.WUt),
-                      _lib.ptr(pk.bU), _lib.ptr(pk.posU), _lib.ptr(pbuf), st)
+                      _lib.ptr(pk.bU), _lib.ptr(pk.posU), _lib.ptr(pbuf), _lib.ptr(pinv), st)
             prow = 1
         else:
             poff_t = (pk.l0_c0.to(torch.int64) * h).contiguous()
-            pbuf, prow = pk.p_const, 0
+            pbuf, prow, pinv = pk.p_const, 0, None
         ctx0 = torch.empty(pk.n0, R, d, device=dev, dtype=torch.bfloat16)
         _lib.call("dchag_l0_node", _lib.ptr(img), img.stride(0), img.stride(1), B, m.image_h,
                   m.image_w, m.patch, h, d, pk.n0, _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g),
-                  _lib.ptr(poff_t), prow, _lib.ptr(pbuf), _lib.ptr(pk.Mt), pk.C_pad,
+                  _lib.ptr(poff_t), prow, _lib.ptr(pbuf), _lib.ptr(pinv), _lib.ptr(pk.Mt), pk.C_pad,
                   _lib.ptr(pk.Et), pk.KE, _lib.ptr(ctx0), st)
         # positional term of the level-0 context: pos @ Vw_n (x (sum mix) for linear nodes)
         posV = self._level0_posV()

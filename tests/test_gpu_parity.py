@@ -138,6 +138,30 @@ def test_frontend_forward_entry_and_dtype():
     assert torch.isfinite(y.float()).all()
 
 
+@pytest.mark.parametrize("chunks", [1, 3, 5])
+def test_frontend_host_input_pipeline_matches_device(chunks):
+    """Host images streamed in batch chunks (H2D overlapped with the kernels, output rows
+    copied back into a pinned host tensor) give the same result as device images."""
+    from paper_2506_21411_b200 import DchagFrontEnd
+    fe = DchagFrontEnd(20, 64, 128, 8, 256, 4, max_group=8)
+    fe.init_weights(seed=3)
+    x = torch.randn(5, 20, 64, 128).to(torch.bfloat16)
+    want = fe(x.cuda()).cpu()
+    got_dev = fe(x.pin_memory(), h2d_chunks=chunks)
+    out = torch.empty(5, 1, 128, 256, dtype=torch.bfloat16).pin_memory()
+    got = fe(x.pin_memory(), out=out, h2d_chunks=chunks)
+    torch.cuda.synchronize()
+    assert got is out
+    assert torch.equal(got_dev.cpu(), want)
+    assert torch.equal(out, want)
+    # a strided host slab (what tp > 1 ranks slice out of the full image): per-image runs
+    big = torch.randn(5, 24, 64, 128).to(torch.bfloat16).pin_memory()
+    want3 = fe(big[:, 2:22].cuda()).cpu()
+    got3 = fe(big[:, 2:22], h2d_chunks=chunks)
+    torch.cuda.synchronize()
+    assert torch.equal(got3.cpu(), want3)
+
+
 # ---------------------------------------------------- functional API mirrors (ops.py)
 def _ops():
     from paper_2506_21411_b200 import ops
@@ -194,3 +218,39 @@ def test_flat_aggregate_matches_bruteforce():
                                 "single_query", H).cpu().numpy()
     want = O.flat_aggregate(tokens, w, "n", "single_query", H)
     assert rel_err(got, want) < BF16_TOL
+
+
+@pytest.mark.parametrize("P,W", [(8, 128), (4, 128)])
+def test_l0_logits_normalised_and_unnormalised_agree(P, W):
+    """dchag_l0_logits with pinv (unnormalised e + 1/sum, the forward path) and without
+    (normalised softmax) describe the same p; the softmax matches the oracle."""
+    from paper_2506_21411_b200 import DchagFrontEnd, _lib
+    fe = DchagFrontEnd(12, 64, W, P, 256, 4, max_group=6)
+    fe.init_weights(seed=4)
+    pk = fe.prepare()
+    B, h = 2, 4
+    R = B * fe.seq
+    img = torch.randn(B, 12, 64, W, device="cuda").to(torch.bfloat16)
+    poff, acc = [], 0
+    for g in pk.l0_g_list:
+        poff.append(acc)
+        acc += g * R * h
+    poff = torch.tensor(poff, device="cuda", dtype=torch.int64)
+    outs = []
+    for with_inv in (False, True):
+        p = torch.empty(acc, device="cuda", dtype=torch.bfloat16)
+        inv = torch.empty(pk.n0, R, h, device="cuda") if with_inv else None
+        _lib.call("dchag_l0_logits", _lib.ptr(img), img.stride(0), img.stride(1), B, 64, W, P,
+                  h, pk.HP, pk.n0, max(pk.l0_g_list), _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g),
+                  _lib.ptr(poff), _lib.ptr(pk.WUt), _lib.ptr(pk.bU), _lib.ptr(pk.posU),
+                  _lib.ptr(p), _lib.ptr(inv), _lib.stream_handle())
+        outs.append((p, inv))
+    torch.cuda.synchronize()
+    (pn, _), (pe, inv) = outs
+    # layout p[poff[n] + ((hg*g + c)*R + r)*NH + h%NH] with NH = 4: one head group
+    for n, g in enumerate(pk.l0_g_list):
+        o = int(poff[n])
+        a = pn[o:o + g * R * h].view(g, R, h).float()
+        e = pe[o:o + g * R * h].view(g, R, h).float() * inv[n][None]
+        assert torch.allclose(a.sum(0), torch.ones(R, h, device="cuda"), atol=2e-2)
+        assert (a - e).abs().max().item() < 8e-3
