@@ -65,8 +65,8 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
  *   ctx[n][r][h*64:(h+1)*64] = sum_c p[r,c,h] * (patch_c[r] @ M_c[:, h-block])
  *                             + sum_c p[r,c,h] * E_n[c, h-block]
  * (the positional term pos[s] @ wv_n is folded into the next dchag_gemm_bf16 row bias)
- * Mt bf16 [H][C_pad][64*P*P] and Et bf16 [n_nodes][H][64*KE] are pre-tiled canonical
- * UMMA blocks (dchag_tile_weights); p_row_mode = 1 reads the dchag_l0_logits layout, 0 a constant
+ * Mt bf16 [H][2][32*C_pad*P*P] and Et bf16 [n_nodes][H][2][32*KE] are pre-tiled canonical
+ * UMMA blocks (dchag_tile_weights, N = 32 halves; K runs over channel-major c*P*P + k); p_row_mode = 1 reads the dchag_l0_logits layout, 0 a constant
  * table p[poff + c*H + h]
  * (linear-mix nodes).  Requires head dim 64, H % 4 == 0, S % 128 == 0, 128 % (W/P) == 0,
  * P in {4, 8}.  pinv (optional, the dchag_l0_logits output): ctx row r, head h is scaled by
@@ -106,9 +106,11 @@ int dchag_unfold(const void* img, long long img_sb, long long img_sc, int B, int
                  int W, int P, void* out, void* stream);
 
 /* Re-tile fp32 folded weights into the canonical no-swizzle K-major UMMA blocks read by
- * dchag_l0_node: src fp32 [nblk][K][64] (block b is a K x 64 matrix, column = output
- * feature of one head) -> dst bf16 [nblk][64*K] in [K/8][8][8 rows][8 k] core-matrix order. */
-int dchag_tile_weights(const float* src, int nblk, int K, void* dst, void* stream);
+ * dchag_l0_node: src fp32 [nblk][K][N] (block b is a K x N matrix, column = output feature)
+ * -> dst bf16 [nblk][K*N] in [K/8][N/8][8 rows][8 k] core-matrix order.  dchag_l0_node reads
+ * Mt / Et as N = 32 blocks: each head's 64 output columns split into the two halves the CTAs
+ * of a pair hold (block order [head][half]). */
+int dchag_tile_weights(const float* src, int nblk, int K, int N, void* dst, void* stream);
 
 /* Number of SMs the kernels size their persistent grids for (device of `stream`). */
 int dchag_num_sms(void);

@@ -33,7 +33,7 @@ SIGNATURES = {
     "dchag_combine_bwd": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_vp, c_ll,
                           c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "dchag_unfold": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp],
-    "dchag_tile_weights": [c_vp, c_int, c_int, c_vp, c_vp],
+    "dchag_tile_weights": [c_vp, c_int, c_int, c_int, c_vp, c_vp],
     "dchag_num_sms": [],
 }
 STRING_FNS = ("dchag_version", "dchag_last_error")

@@ -83,14 +83,15 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // ===================================================================== tiling kernel
 namespace dchag {
-__global__ void tile_weights_kernel(const float* src, int nblk, int K, __nv_bfloat16* dst) {
-  const long long total = (long long)nblk * K * 64;
+__global__ void tile_weights_kernel(const float* src, int nblk, int K, int N, __nv_bfloat16* dst) {
+  const long long total = (long long)nblk * K * N;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
-  const int b = (int)(t / (K * 64));
-  const int rem = (int)(t - (long long)b * K * 64);
-  const int k = rem / 64, n = rem % 64;
-  const long long off = (long long)b * K * 64 + ((k / 8) * 8 + (n / 8)) * 64 + (n % 8) * 8 + (k % 8);
+  const int b = (int)(t / ((long long)K * N));
+  const int rem = (int)(t - (long long)b * K * N);
+  const int k = rem / N, n = rem % N;
+  const long long off =
+      (long long)b * K * N + ((k / 8) * (N / 8) + (n / 8)) * 64 + (n % 8) * 8 + (k % 8);
   dst[off] = __float2bfloat16(src[t]);
 }
 }  // namespace dchag
@@ -207,13 +208,20 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
   {
     const char* dbg = getenv("DCHAG_L0_DEBUG");
     a.debug_mode = dbg ? atoi(dbg) : 0;
-    a.cluster = getenv("DCHAG_L0_CLUSTER") ? atoi(getenv("DCHAG_L0_CLUSTER")) : 0;
     const char* tr = getenv("DCHAG_L0_TRACE_PTR");
     a.trace = tr ? reinterpret_cast<long long*>(strtoull(tr, nullptr, 0)) : nullptr;
   }
   if ((reinterpret_cast<uintptr_t>(img) | (uintptr_t)(img_sb * 2) | (uintptr_t)(img_sc * 2)) % 16)
     return fail(DCHAG_ERR_SHAPE, "l0_node: image base/strides must be 16-byte aligned");
-  return cuda_status(launch_l0_node(a, num_sms_cached(), S(stream)), "l0_node");
+  if (reinterpret_cast<uintptr_t>(ctx) % 16 || (D * 2) % 16)
+    return fail(DCHAG_ERR_SHAPE, "l0_node: ctx must be 16-byte aligned");
+  // ctx [n_nodes * R rows][D] bf16; one store box = 64 columns (a head) x 128 rows, 128B swizzle
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)n_nodes * B * a.S};
+  const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+  const cuuint32_t box[2] = {64, 128};
+  if (int rc = make_map(&tm, ctx, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
+  return cuda_status(launch_l0_node(a, tm, num_sms_cached(), S(stream)), "l0_node");
 }
 
 int dchag_combine(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
@@ -263,12 +271,12 @@ int dchag_unfold(const void* img, long long img_sb, long long img_sc, int B, int
                      "unfold");
 }
 
-int dchag_tile_weights(const float* src, int nblk, int K, void* dst, void* stream) {
-  if (K % 8) return fail(DCHAG_ERR_SHAPE, "tile_weights: K must be a multiple of 8");
-  const long long total = (long long)nblk * K * 64;
+int dchag_tile_weights(const float* src, int nblk, int K, int N, void* dst, void* stream) {
+  if (K % 8 || N % 8 || N <= 0) return fail(DCHAG_ERR_SHAPE, "tile_weights: K, N must be multiples of 8");
+  const long long total = (long long)nblk * K * N;
   if (total == 0) return DCHAG_OK;
   tile_weights_kernel<<<(unsigned)((total + 255) / 256), 256, 0, S(stream)>>>(
-      src, nblk, K, reinterpret_cast<__nv_bfloat16*>(dst));
+      src, nblk, K, N, reinterpret_cast<__nv_bfloat16*>(dst));
   return cuda_status(cudaGetLastError(), "tile_weights");
 }
 

@@ -139,6 +139,18 @@ DEV uint32_t lds32(uint32_t addr) {
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
+DEV uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+DEV uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
 DEV void sts128(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
@@ -303,6 +315,25 @@ DEV void tmem_st4(uint32_t taddr, const uint32_t (&r)[4]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr),
                "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
                : "memory");
+}
+// A-operand build + store: tcgen05.st.32x32b.x16 of {x[0..7] * pa, x[8..15] * pb} (bf16x2)
+DEV void tmem_st16_scaled(uint32_t taddr, const uint32_t (&x)[16], uint32_t pa, uint32_t pb) {
+  asm volatile(
+      "{\n.reg .b32 t<16>;\n"
+      "mul.rn.bf16x2 t0, %1, %17;\n mul.rn.bf16x2 t1, %2, %17;\n"
+      "mul.rn.bf16x2 t2, %3, %17;\n mul.rn.bf16x2 t3, %4, %17;\n"
+      "mul.rn.bf16x2 t4, %5, %17;\n mul.rn.bf16x2 t5, %6, %17;\n"
+      "mul.rn.bf16x2 t6, %7, %17;\n mul.rn.bf16x2 t7, %8, %17;\n"
+      "mul.rn.bf16x2 t8, %9, %18;\n mul.rn.bf16x2 t9, %10, %18;\n"
+      "mul.rn.bf16x2 t10, %11, %18;\n mul.rn.bf16x2 t11, %12, %18;\n"
+      "mul.rn.bf16x2 t12, %13, %18;\n mul.rn.bf16x2 t13, %14, %18;\n"
+      "mul.rn.bf16x2 t14, %15, %18;\n mul.rn.bf16x2 t15, %16, %18;\n"
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{t0,t1,t2,t3,t4,t5,t6,t7,t8,t9,t10,t11,t12,t13,t14,t15};\n}\n" ::"r"(taddr),
+      "r"(x[0]), "r"(x[1]), "r"(x[2]), "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7]),
+      "r"(x[8]), "r"(x[9]), "r"(x[10]), "r"(x[11]), "r"(x[12]), "r"(x[13]), "r"(x[14]),
+      "r"(x[15]), "r"(pa), "r"(pb)
+      : "memory");
 }
 DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 

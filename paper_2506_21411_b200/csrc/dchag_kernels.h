@@ -59,16 +59,19 @@ struct L0NodeArgs {
   int p_row_mode;              // 1: K_p0 layout (see L0LogitArgs); 0: constant p[poff + c*H + h]
   const __nv_bfloat16* p;
   const float* pinv;           // optional [n_nodes][R][H] row/head scale of ctx (K_p0 output)
-  const __nv_bfloat16* Mt;     // [H][C_pad][dh*PP] canonical no-swizzle K-major blocks
+  const __nv_bfloat16* Mt;     // [H][2][C_pad*PP/8][4][8][8]: per head, the two 32-column
+                               // halves of M_c (one per CTA of a pair) as canonical no-swizzle
+                               // K-major core-matrix blocks, channels consecutive along K
   int C_pad;
-  const __nv_bfloat16* Et;     // [n_nodes][H][dh*KE] ext (bias) blocks
+  const __nv_bfloat16* Et;     // [n_nodes][H][2][KE/8][4][8][8] ext (bias) blocks, same split
   int KE;
   __nv_bfloat16* ctx;          // [n_nodes][R][D]
-  int debug_mode;              // timing probes: 0 normal, 1 no A build, 2 no MMA
-  int cluster;                 // 0 auto (CTA pairs when the tile count is even), 1 off
+  int debug_mode;              // timing probes: 1 no A build, 2 no MMA, 4 no copies,
+                               // 8 no ctx stores, 32 no drain
   long long* trace;            // optional [8][256] clock64 timeline of CTA 0 (debug)
 };
-cudaError_t launch_l0_node(const L0NodeArgs& a, int num_sms, cudaStream_t st);
+cudaError_t launch_l0_node(const L0NodeArgs& a, const CUtensorMap& tm_ctx, int num_sms,
+                           cudaStream_t st);
 
 // Upper-level combine: ctx[n][r][:] = sum_j p_jh(r) * V_child(j)[r][:]
 struct CombineArgs {

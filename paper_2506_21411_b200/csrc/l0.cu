@@ -334,70 +334,139 @@ constexpr int L0_DH = 64;                          // head dim (MMA N)
 constexpr int L0_STAGES = 4;
 constexpr int L0_IMG_BYTES = 16384;                // 128 rows x 64 K bf16 (or ext: 16 ch of p)
 constexpr int L0_P_BYTES = 4096;                   // p of the stage: CG ch x 128 rows x NH bf16
-constexpr int L0_B_BYTES = 4 * L0_DH * 64 * 2;     // up to 4 heads x [64 x 64] bf16
+constexpr int L0_BH_BYTES = 32 * 64 * 2;           // one head's B half: 32 N x 64 K bf16
+constexpr int L0_B_BYTES = 4 * L0_BH_BYTES;        // up to 4 heads
 constexpr int L0_STAGE_BYTES = L0_IMG_BYTES + L0_P_BYTES + L0_B_BYTES;
-constexpr int L0_STAGE_OUT = 16 * 32 * 32;         // epilogue staging: 16 warps x 32 rows x 32 B
-constexpr int L0_SMEM = L0_STAGES * L0_STAGE_BYTES + L0_STAGE_OUT + 1024 + 256;
-constexpr int L0_THREADS = 576;                    // producer, image gate, 16 builders
+constexpr int L0_OUT_BYTES = 4 * 128 * 128;        // ctx tile staging: 4 heads x 128 rows x 128 B
+constexpr int L0_SMEM = L0_STAGES * L0_STAGE_BYTES + L0_OUT_BYTES + 1024 + 256;
+constexpr int L0_THREADS = 608;                    // producer, image gate, MMA gate, 16 builders
 constexpr uint32_t L0_ACC_COLS = 4 * L0_DH;        // accumulator region (NH * 64 used)
 constexpr uint32_t L0_SLOT_COLS = 4 * 32;          // A slot: 64 bf16 K per head = 32 columns
 
 #define L0_TRACE(ev, idx)                                                                   \
   do {                                                                                      \
-    if (a.trace && blockIdx.x == 0 && (idx) < 256) a.trace[(ev) * 256 + (idx)] = clock64(); \
+    if (a.trace && blockIdx.x < 2 && (idx) < 256)                                           \
+      a.trace[((ev) + 8 * blockIdx.x) * 256 + (idx)] = globaltimer_ns();                    \
   } while (0)
 
-// Stages of one unit (node n, 128-row tile, head group hg of NH heads):
-//   main stage st < nmain: CG channels (K = 64 per head): image rows, p slices, B = M_c blocks
-//   ext stage e < next:    16 channels of the bias K-block: p slices (A = p) and Et K-block
-// Warp roles (one persistent CTA per SM, 18 warps):
+DEV long long globaltimer_ns() {  // comparable across the two SMs of a pair (clock64 is not)
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+DEV void tmem_alloc_pair(uint32_t* slot, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(slot)), "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+DEV void tmem_dealloc_pair(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
+               : "memory");
+}
+// M256 MMA over the CTA pair: A rows from each CTA's TMEM, B split by N across the pair
+DEV void mma_ts_pair(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(a),
+      "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+DEV void commit_pair(uint64_t* bar) {  // arrives on `bar` in both CTAs of the pair
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"((uint16_t)3)
+      : "memory");
+}
+// Arrive on rank 0's copy of bar. Default (.release.cta) semantics, as CUTLASS's cluster
+// barriers use: the data the leader's MMA consumes is TMEM written by tcgen05.st, ordered by
+// tcgen05.wait::st + fence::before_thread_sync; a .release.cluster arrive measured ~1 us.
+DEV void mbar_arrive_rank0(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, 0;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {  // acquire.cluster wait
+  const uint32_t addr = smem_u32(bar);
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (clock64() - t0 > 40000000000LL) __trap();
+  }
+}
+DEV void tma_store_2d(const CUtensorMap* m, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+
+// Level-0 node kernel on CTA pairs (cluster of 2, cta_group::2 MMAs).
+// A cluster unit is (node n, pair of 128-row tiles, head group hg of NH heads); CTA rank r owns
+// tile 2*pair + r (an odd tile count gives the last pair a phantom tile that loads a copy of
+// the last tile and stores nothing). Stages of a unit:
+//   main stage st < nmain: CG channels (K = 64 per head): image rows, p slices, B halves
+//   ext stage e < next:    16 channels of the bias K-block: p slices (A = p), Et halves
+// Each M256 x N64 MMA reads A (p * patch, built by this CTA's builders) from both CTAs' TMEM and
+// B = M_c[:, head] split by N: rank r holds output columns [32r, 32r + 32) of every head. That
+// halves the B operand's shared-memory traffic per SM (TMA write + MMA read), which bounded the
+// single-CTA kernel (~105 KB of smem traffic per 512-cycle stage at ~128 B/cycle).
+// Warp roles (per CTA, 19 warps):
 //   warp 0      producer: 1-D bulk copies of every stage into a 4-deep shared-memory ring.
-//   warp 1      image gate: waits "stage landed" (mbarrier) -> named barrier IMG(q).
-//   warps 2..17 builders, two groups of 8 taking alternate stages (group q & 1 owns A slot
-//               q & 1): A = p[r,c,h] * patch_c[r] (or p itself for ext) -> registers ->
-//               tcgen05.st; the group's first warp then issues the stage's tcgen05.mma
-//               (A from TMEM, B from smem) and commits stage, slot and accumulator barriers.
-// The trace of the previous layout (one gate warp, 8 builders serialising every stage) showed
-// ~1300 cycles per stage against 512 of MMA: the per-stage handshake chain (mbarrier try_wait
-// ~157 cycles, tcgen05.st + wait ~137, named-barrier hops) ran back to back with the build.
-// Two groups overlap one stage's chain with the next stage's build.
-// CL = 2: a CTA pair (same node and head group, adjacent row tiles) splits the B blocks of
-// every stage between its two producers and multicasts them, halving the weight fill per CTA
-// (the kernel is L2->SMEM fill bound); empty[] then counts both CTAs' MMA commits.
-template <int PP, int L0_NH, int CL>
-__global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
+//   warp 1      image gate: "stage landed" (mbarrier) -> named barrier IMG(q); TMEM owner.
+//   warp 2      MMA gate (rank 0 only): READY(q) from both CTAs' builders (cluster mbarrier)
+//               -> the stage's MMAs -> commits to stage, slot and accumulator barriers of
+//               both CTAs.
+//   warps 3..18 builders, two groups of 8 taking alternate stages (group q & 1 owns A slot
+//               q & 1); the two warps of a TMEM lane quarter split K into halves for all NH
+//               heads: A = p[r,c,h] * patch_c[r] -> tcgen05.st -> READY(q). At the end of a
+//               unit they drain the accumulator (x 1/sum_c e) into a 128B-swizzled smem tile
+//               that TMA tensor stores write to ctx in the background of the next unit.
+template <int PP, int L0_NH, bool ROWP>
+__global__ void __launch_bounds__(L0_THREADS, 1)
+    l0_node_kernel(L0NodeArgs a, const __grid_constant__ CUtensorMap tm_ctx) {
   constexpr int CG = 64 / PP;        // channels per main stage (K = 64 per head per stage)
   constexpr int P = PP == 64 ? 8 : 4;
   constexpr int NBAR = 288;          // image gate warp + one group's 8 builder warps
   constexpr int PROW = 128 * L0_NH * 2;  // bytes of one channel's p slice for the tile
+  constexpr bool rowp = ROWP;        // p staged per row (attention) or a constant table (linear)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* stage_out = smem + L0_STAGES * L0_STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + L0_STAGE_OUT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + L0_OUT_BYTES);
   uint64_t* empty = full + L0_STAGES;
   uint64_t* aempty = empty + L0_STAGES;
   uint64_t* accfull = aempty + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(accfull + 1);
+  uint64_t* ready = accfull + 1;  // [2], rank 0's copy is the one used
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(ready + 2);
 
   const int warp = warp_id(), lane = lane_id();
   const int R = a.B * a.S;
   const int n_tiles = R / 128;
+  const int npairs = (n_tiles + 1) / 2;
   const int HG = a.H / L0_NH;
-  const int crank = CL > 1 ? (int)cluster_rank() : 0;
-  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
-  const int total_units = a.n_nodes * (n_tiles / CL) * HG;  // cluster units
-  const uint16_t cmask = (uint16_t)((1u << CL) - 1);
-  const bool rowp = a.p_row_mode != 0;
-  // cluster unit u -> (head group, this CTA's row tile, node)
+  const int crank = (int)cluster_rank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int total_units = a.n_nodes * npairs * HG;
   auto decode = [&](int u, int& hg, int& tile, int& n) {
     hg = u % HG;
     const int rest = u / HG;
-    tile = (rest % (n_tiles / CL)) * CL + crank;
-    n = rest / (n_tiles / CL);
+    tile = (rest % npairs) * 2 + crank;
+    n = rest / npairs;
   };
   auto unit_stages = [&](int u, int& g, int& nmain, int& next) {
-    const int n = (u / HG) / (n_tiles / CL);
+    const int n = (u / HG) / npairs;
     g = __ldg(a.node_g + n);
     nmain = (g + CG - 1) / CG;
     next = (g + 15) / 16;
@@ -406,17 +475,19 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < L0_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);
+      mbar_init(&empty[s], 1);
     }
     mbar_init(&aempty[0], 1);
     mbar_init(&aempty[1], 1);
-    mbar_init(accfull, 2);  // one commit per builder group
+    mbar_init(accfull, 1);
+    mbar_init(&ready[0], 16);  // 8 builder warps x 2 CTAs
+    mbar_init(&ready[1], 16);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tslot, 512);
+  if (warp == 1) tmem_alloc_pair(tslot, 512);
   tc_fence_before();
   __syncthreads();
-  if (CL > 1) cluster_sync();  // the peer multicasts into our barriers from here on
+  cluster_sync();  // barriers of both CTAs initialised before any remote arrive / multicast
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
@@ -428,6 +499,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
       for (int u = cid; u < total_units; u += ncl) {
         int hg, tile, n;
         decode(u, hg, tile, n);
+        if (tile >= n_tiles) tile = n_tiles - 1;  // phantom tile: load a copy
         const int c0 = __ldg(a.node_c0 + n);
         int g, nmain, next;
         unit_stages(u, g, nmain, next);
@@ -436,8 +508,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
         const int b = r0 / a.S, s0 = r0 - b * a.S;
         const __nv_bfloat16* chunk0 =
             a.img + b * a.img_sb + (long long)(s0 / a.wp) * P * a.W;
-        // p slice of (hg, channel c) for this tile
-        auto pslice = [&](int c) {
+        auto pslice = [&](int c) {  // p slice of (hg, channel c) for this tile
           return a.p + poff + (((long long)hg * g + c) * R + r0) * L0_NH;
         };
         for (int st = 0; st < nmain + next; ++st) {
@@ -450,31 +521,33 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
           } else if (st < nmain) {
             const int cv = min(CG, g - st * CG);
             mbar_expect_tx(&full[stage], cv * 128 * PP * 2 + (rowp ? cv * PROW : 0) +
-                                             L0_NH * L0_DH * 64 * 2);
+                                             L0_NH * L0_BH_BYTES);
             for (int cc = 0; cc < cv; ++cc) {
               const int c = st * CG + cc;
               bulk_load(sI + cc * 128 * PP * 2, chunk0 + (long long)(c0 + c) * a.img_sc,
                         128 * PP * 2, &full[stage]);
               if (rowp) bulk_load(sP + cc * PROW, pslice(c), PROW, &full[stage]);
             }
-            for (int h = crank * (L0_NH / CL); h < (crank + 1) * (L0_NH / CL); ++h) {
+            // B halves: Mt [H][2][C_pad*PP/8][4][8][8]; this stage's 64 K rows are contiguous
+            for (int h = 0; h < L0_NH; ++h) {
               const __nv_bfloat16* src =
-                  a.Mt + ((long long)(hg * L0_NH + h) * a.C_pad + c0 + st * CG) * (L0_DH * PP);
-              if (CL == 1) bulk_load(sB + h * (L0_DH * 64 * 2), src, L0_DH * 64 * 2, &full[stage]);
-              else bulk_load_mc(sB + h * (L0_DH * 64 * 2), src, L0_DH * 64 * 2, &full[stage], cmask);
+                  a.Mt + (((long long)(hg * L0_NH + h) * 2 + crank) * a.C_pad + c0 + st * CG) *
+                             (PP * 32);
+              bulk_load(sB + h * L0_BH_BYTES, src, L0_BH_BYTES, &full[stage]);
             }
           } else {
             const int e = st - nmain;
             const int ce = min(16, g - 16 * e);
-            mbar_expect_tx(&full[stage], (rowp ? ce * PROW : 0) + L0_NH * L0_DH * 16 * 2);
+            mbar_expect_tx(&full[stage], (rowp ? ce * PROW : 0) + L0_NH * 16 * 32 * 2);
             if (rowp)
               for (int cc = 0; cc < ce; ++cc)
                 bulk_load(sI + cc * PROW, pslice(16 * e + cc), PROW, &full[stage]);
-            for (int h = crank * (L0_NH / CL); h < (crank + 1) * (L0_NH / CL); ++h) {
-              const __nv_bfloat16* src = a.Et + ((long long)n * a.H + hg * L0_NH + h) *
-                                                    (L0_DH * a.KE) + e * 16 * L0_DH;
-              if (CL == 1) bulk_load(sB + h * (L0_DH * 64 * 2), src, L0_DH * 16 * 2, &full[stage]);
-              else bulk_load_mc(sB + h * (L0_DH * 64 * 2), src, L0_DH * 16 * 2, &full[stage], cmask);
+            // Et [n][H][2][KE/8][4][8][8]
+            for (int h = 0; h < L0_NH; ++h) {
+              const __nv_bfloat16* src =
+                  a.Et + (((long long)n * a.H + hg * L0_NH + h) * 2 + crank) * (32LL * a.KE) +
+                  e * 16 * 32;
+              bulk_load(sB + h * L0_BH_BYTES, src, 16 * 32 * 2, &full[stage]);
             }
           }
           if (++stage == L0_STAGES) { stage = 0; phase ^= 1; }
@@ -483,67 +556,127 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
     }
   } else if (warp == 1) {
     // ------------------------------------------------ image gate: full(q) -> IMG(q)
-    long long q_total = 0;
+    int q_total = 0;
     for (int u = cid; u < total_units; u += ncl) {
       int g, nmain, next;
       unit_stages(u, g, nmain, next);
       q_total += nmain + next;
     }
-    for (long long q = 0; q < q_total; ++q) {
+    for (int q = 0; q < q_total; ++q) {
       mbar_wait(&full[q % L0_STAGES], (uint32_t)((q / L0_STAGES) & 1));
       if (lane == 0) L0_TRACE(0, q);
       asm volatile("bar.arrive %0, %1;" ::"r"(1 + (int)(q & 3)), "r"(NBAR) : "memory");
     }
+  } else if (warp == 2) {
+    // ------------------------------------------------ MMA gate (rank 0): READY(q) -> MMAs
+    // UTCHMMA issue blocks while the tensor pipe is busy, so the issuer is a dedicated warp.
+    // Stages are issued in order: the accumulation order is fixed (bit-reproducible).
+    if (crank == 0) {
+      const uint32_t idesc = idesc_bf16_f32(256, L0_DH);
+      int q = 0;
+      for (int u = cid; u < total_units; u += ncl) {
+        int g, nmain, next;
+        unit_stages(u, g, nmain, next);
+        const int nst = nmain + next;
+        for (int st = 0; st < nst; ++st, ++q) {
+          const int cs = q % L0_STAGES, G = q & 1;
+          mbar_wait(&ready[G], (uint32_t)((q >> 1) & 1));
+          tc_fence_after();
+          if (elect_one()) {
+            L0_TRACE(2, q);
+            const uint32_t sb = smem_u32(smem) + cs * L0_STAGE_BYTES + L0_IMG_BYTES + L0_P_BYTES;
+            const uint32_t at0 = tbase + L0_ACC_COLS + G * L0_SLOT_COLS;
+            if (a.debug_mode & 2) {
+            } else if (st < nmain) {
+#pragma unroll
+              for (int h = 0; h < L0_NH; ++h)
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  mma_ts_pair(tbase + h * L0_DH, at0 + h * 32 + kk * 8,
+                              smem_desc(sb + h * L0_BH_BYTES + kk * 1024, 512, 128, 0), idesc,
+                              (st | kk) != 0);
+            } else {
+#pragma unroll
+              for (int h = 0; h < L0_NH; ++h)
+                mma_ts_pair(tbase + h * L0_DH, at0 + h * 32,
+                            smem_desc(sb + h * L0_BH_BYTES, 512, 128, 0), idesc, 1u);
+            }
+            commit_pair(&empty[cs]);
+            commit_pair(&aempty[G]);
+            if (st == nst - 1) commit_pair(accfull);
+            L0_TRACE(1, q);
+          }
+          __syncwarp();
+        }
+      }
+    }
   } else {
-    // ------------------------------------------------ builders (warps 2..17)
-    // Two groups of 8 warps take alternate stages (group G = q & 1 owns A slot G), so one
-    // group's handshake latencies overlap the other group's build. Within a group the two
-    // warps of a TMEM lane quarter split K = 64 into halves (kh) for all NH heads, so every
-    // image row is read from shared memory once. The group's first warp issues the stage's
-    // MMAs itself (no gate warp hop). The accumulator is zeroed by tcgen05.st after each
-    // drain, so every MMA accumulates and the two groups' MMAs need no mutual ordering.
-    const int bw = warp - 2;
+    // ------------------------------------------------ builders (warps 3..18)
+    const int bw = warp - 3;
     const int G = bw >> 3;
     const int kh = (bw >> 2) & 1;
     const int quarter = warp & 3;       // TMEM lane quarter is fixed by warp id % 4
-    const bool issuer = (bw & 7) == 0;
     const int m = quarter * 32 + lane;  // row within tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     constexpr int EC = L0_NH * 16;      // accumulator columns drained by this warp
     const int ecol = (G * 2 + kh) * EC;
-    uint8_t* my_out = stage_out + bw * 1024;
-    const uint32_t idesc = idesc_bf16_f32(128, L0_DH);
-    const int i_l = m / a.wp, jj = m - (m / a.wp) * a.wp;
-    auto zero_acc = [&]() {
-      uint32_t z[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) z[e] = 0u;
-#pragma unroll
-      for (int cb = 0; cb < EC; cb += 16) tmem_st16(tbase + lane_off + ecol + cb, z);
-      tmem_st_wait();
-      tc_fence_before();
-      asm volatile("bar.sync 7, 512;" ::: "memory");  // ACC: whole accumulator zeroed
-      tc_fence_after();
-    };
-    // all NH heads of one channel for this row, packed bf16 pairs (heads 0-1, 2-3)
-    auto p_smem = [&](const uint8_t* base, int cc, uint32_t (&o)[2]) {
-      const uint8_t* src = base + cc * PROW + m * L0_NH * 2;
+    const bool lead = bw == 0 && lane == 0;  // issues the ctx tensor stores
+    auto p_smem = [&](uint32_t base, int cc, uint32_t (&o)[2]) {  // base has the row offset
+      const uint32_t src = base + cc * PROW;
       if (L0_NH == 4) {
-        const uint2 v = *reinterpret_cast<const uint2*>(src);
+        const uint2 v = lds64(src);
         o[0] = v.x; o[1] = v.y;
       } else {
-        o[0] = *reinterpret_cast<const uint32_t*>(src); o[1] = 0u;
+        o[0] = lds32(src); o[1] = 0u;
       }
     };
-    long long q_total = 0;
-    for (int u = cid; u < total_units; u += ncl) {
-      int g, nmain, next;
-      unit_stages(u, g, nmain, next);
-      q_total += nmain + next;
-    }
-    zero_acc();
     uint32_t accphase = 0;
-    long long q = 0;
+    // epilogue of a finished unit: drain (x 1/sum) into the 128B-swizzled staging tile, TMA
+    // tensor stores write it to ctx in the background. It runs after the builders have
+    // already staged their first A slot of the next unit (overlapping the MMA tail), and
+    // before that slot's READY: the next unit's first MMAs overwrite the accumulator.
+    auto epilogue = [&](int n, int tile, int hg, float sc) {
+      mbar_wait(accfull, accphase);  // the unit's last MMAs
+      accphase ^= 1;
+      if (lead) bulk_wait_read0();   // the previous unit's stores have read the staging
+      tc_fence_after();
+      asm volatile("bar.sync 5, 512;" ::: "memory");  // ACC0: staging free
+      if (!(a.debug_mode & 32)) {
+        const uint32_t sout = smem_u32(stage_out);
+#pragma unroll
+        for (int cb = 0; cb < EC; cb += 32) {
+          const int col = ecol + cb;               // column within the head group
+          const int hd = col / L0_DH, c8 = (col % L0_DH) / 8;
+          uint32_t v[32];
+          tmem_ld32(tbase + lane_off + col, v);
+          tmem_ld_wait();
+          const uint32_t rowb = sout + hd * (128 * 128) + m * 128;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint4 o;
+            o.x = pack_bf16(sc * __uint_as_float(v[8 * k + 0]), sc * __uint_as_float(v[8 * k + 1]));
+            o.y = pack_bf16(sc * __uint_as_float(v[8 * k + 2]), sc * __uint_as_float(v[8 * k + 3]));
+            o.z = pack_bf16(sc * __uint_as_float(v[8 * k + 4]), sc * __uint_as_float(v[8 * k + 5]));
+            o.w = pack_bf16(sc * __uint_as_float(v[8 * k + 6]), sc * __uint_as_float(v[8 * k + 7]));
+            sts128(rowb + ((uint32_t)((c8 + k) ^ (m & 7)) << 4), o);
+          }
+        }
+      }
+      tc_fence_before();
+      fence_async_smem();  // staging writes -> async proxy (TMA store)
+      asm volatile("bar.sync 6, 512;" ::: "memory");  // ACC1: tile staged, accumulator drained
+      tc_fence_after();
+      if (lead && tile < n_tiles && !(a.debug_mode & (8 | 32))) {
+        const uint32_t sout = smem_u32(stage_out);
+        for (int hd = 0; hd < L0_NH; ++hd)
+          tma_store_2d(&tm_ctx, sout + hd * (128 * 128), (hg * L0_NH + hd) * L0_DH,
+                       n * R + tile * 128);
+        bulk_commit();
+      }
+    };
+    int q = 0;
+    int pend_n = -1, pend_tile = 0, pend_hg = 0;  // unit whose epilogue is pending
+    float pend_sc = 1.f;
     for (int u = cid; u < total_units; u += ncl) {
       int hg, tile, n;
       decode(u, hg, tile, n);
@@ -551,8 +684,12 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
       unit_stages(u, g, nmain, next);
       const int nst = nmain + next;
       const long long poff = __ldg(a.node_poff + n);
-      // constant p table (linear-mix nodes): p[poff + c*H + h]
-      auto p_const = [&](int c, uint32_t (&o)[2]) {
+      // softmax normaliser of this row and this warp's head, fetched a unit ahead of its use
+      // (an HBM miss in the drain stalled the whole pair ~1 us)
+      const float sc_u = a.pinv ? __ldg(a.pinv + ((long long)n * R + min(tile, n_tiles - 1) * 128 +
+                                                  m) * a.H + hg * L0_NH + ecol / L0_DH)
+                                : 1.f;
+      auto p_const = [&](int c, uint32_t (&o)[2]) {  // linear-mix nodes: p[poff + c*H + h]
         const __nv_bfloat16* src = a.p + poff + (long long)c * a.H + hg * L0_NH;
         if (L0_NH == 4) {
           const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
@@ -562,18 +699,27 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
         }
       };
       for (int st = 0; st < nst; ++st, ++q) {
-        if ((int)(q & 1) != G) continue;
-        const int cs = (int)(q % L0_STAGES);
-        const uint8_t* sI = smem + cs * L0_STAGE_BYTES;
-        const uint8_t* sP = sI + L0_IMG_BYTES;
+        if ((q & 1) != G) continue;
+        const int cs = q % L0_STAGES;
+        // per-thread address terms are re-derived every stage (hoisted values spilled, and
+        // a spill reload misses the ~25 KB L1 left next to the shared-memory carve-out)
+        const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+        uint32_t tb = tbase + lane_off;
+        asm volatile("" : "+r"(tb));
+        const uint32_t mm = threadIdx.x & 127u;  // == m
+        const uint32_t lwp = (uint32_t)(__ffs(a.wp) - 1);  // W / P divides 128: a power of 2
+        const uint32_t xo = ((((mm >> lwp) * P + (P == 8 ? 4 * kh : 0)) * (uint32_t)a.W +
+                              (mm & (uint32_t)(a.wp - 1)) * P) * 2);
+        const uint32_t wr = (uint32_t)a.W * 2, po = mm * (L0_NH * 2);
+        const uint32_t sI = sbase + cs * L0_STAGE_BYTES;
+        const uint32_t sP = sI + L0_IMG_BYTES;
         const bool ext = st >= nmain;
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(q & 3)), "r"(NBAR) : "memory");  // IMG
-        if (bw == 0 && lane == 0) L0_TRACE(3, q);
-        const uint32_t slot_t = tbase + lane_off + L0_ACC_COLS + G * L0_SLOT_COLS;
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + (q & 3)), "r"(NBAR) : "memory");  // IMG
+        const uint32_t slot_t = tb + L0_ACC_COLS + G * L0_SLOT_COLS;
         if (!ext) {
           // this warp's 16 of the 32 A columns: P == 8 -> pixel rows 4kh..4kh+3 of the one
           // channel; P == 4 -> channels 2kh, 2kh+1 of the stage's four
-          constexpr int NCC = CG == 1 ? 1 : 2;  // channels touched by this K half
+          constexpr int NCC = CG == 1 ? 1 : 2;
           uint32_t x[16], pv[NCC][2];
 #pragma unroll
           for (int ci = 0; ci < NCC; ++ci) {
@@ -583,47 +729,41 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
             if (!valid) {
               pv[ci][0] = pv[ci][1] = 0u;
             } else if (rowp) {
-              p_smem(sP, cc, pv[ci]);
+              p_smem(sP + po, cc, pv[ci]);
             } else {
               p_const(c, pv[ci]);
             }
-            const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(
-                                            sI + cc * 128 * PP * 2) +
-                                        (i_l * P) * a.W + jj * P;
+            const uint32_t base = sI + cc * 128 * PP * 2 + xo;
             if (P == 8) {
 #pragma unroll
               for (int r4 = 0; r4 < 4; ++r4) {
-                const int py = 4 * kh + r4;
-                const uint4 v = valid ? *reinterpret_cast<const uint4*>(base + py * a.W)
-                                      : make_uint4(0, 0, 0, 0);
+                const uint4 v = valid ? lds128(base + r4 * wr) : make_uint4(0, 0, 0, 0);
                 x[r4 * 4 + 0] = v.x; x[r4 * 4 + 1] = v.y; x[r4 * 4 + 2] = v.z; x[r4 * 4 + 3] = v.w;
               }
             } else {
 #pragma unroll
               for (int py = 0; py < 4; ++py) {
-                const uint2 v = valid ? *reinterpret_cast<const uint2*>(base + py * a.W)
-                                      : make_uint2(0, 0);
+                const uint2 v = valid ? lds64(base + py * wr) : make_uint2(0, 0);
                 x[ci * 8 + py * 2 + 0] = v.x; x[ci * 8 + py * 2 + 1] = v.y;
               }
             }
           }
+          if ((bw & 7) == 0 && lane == 0) L0_TRACE(3, q);
           // A slot free: the MMAs of this group's previous stage (same slot) have completed
           mbar_wait(&aempty[G], (uint32_t)(((q >> 1) & 1) ^ 1));
           tc_fence_after();
 #pragma unroll
           for (int h = 0; h < L0_NH; ++h) {
-            uint32_t y[16];
+            uint32_t ph[2];
 #pragma unroll
-            for (int ci = 0; ci < NCC; ++ci) {
-              const uint32_t w = pv[ci][h >> 1];
-              const uint32_t ph = (h & 1) ? (w & 0xffff0000u) | (w >> 16)
-                                          : (w << 16) | (w & 0xffffu);
-#pragma unroll
-              for (int e = 0; e < 16 / NCC; ++e)
-                y[ci * (16 / NCC) + e] =
-                    (a.debug_mode & 1) ? 0u : mul_bf16x2(x[ci * (16 / NCC) + e], ph);
+            for (int ci = 0; ci < 2; ++ci) {
+              const uint32_t w = pv[NCC == 1 ? 0 : ci][h >> 1];
+              ph[ci] = (a.debug_mode & 1) ? 0u
+                       : (h & 1) ? (w & 0xffff0000u) | (w >> 16) : (w << 16) | (w & 0xffffu);
             }
-            tmem_st16(slot_t + h * 32 + 16 * kh, y);
+            // multiply + tcgen05.st in one asm block (the products never become C values, so
+            // the compiler cannot keep all heads' products live at once)
+            tmem_st16_scaled(slot_t + h * 32 + 16 * kh, x, ph[0], ph[1]);
           }
         } else {
           // ext stage e: A[r, k] = p[r, 16e + k, h] (k < 16); this warp: k in [8kh, 8kh+8)
@@ -634,8 +774,8 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
             const int cl0 = 8 * kh + 2 * kc;          // channel within the ext block
             const int c0e = 16 * e + cl0;
             lo[kc][0] = lo[kc][1] = hi[kc][0] = hi[kc][1] = 0u;
-            if (c0e < g) { if (rowp) p_smem(sI, cl0, lo[kc]); else p_const(c0e, lo[kc]); }
-            if (c0e + 1 < g) { if (rowp) p_smem(sI, cl0 + 1, hi[kc]); else p_const(c0e + 1, hi[kc]); }
+            if (c0e < g) { if (rowp) p_smem(sI + po, cl0, lo[kc]); else p_const(c0e, lo[kc]); }
+            if (c0e + 1 < g) { if (rowp) p_smem(sI + po, cl0 + 1, hi[kc]); else p_const(c0e + 1, hi[kc]); }
           }
           mbar_wait(&aempty[G], (uint32_t)(((q >> 1) & 1) ^ 1));
           tc_fence_after();
@@ -653,126 +793,50 @@ __global__ void __launch_bounds__(L0_THREADS, 1) l0_node_kernel(L0NodeArgs a) {
         }
         tmem_st_wait();
         tc_fence_before();
-        if (bw == 0 && lane == 0) L0_TRACE(4, q);
-        if (!issuer) {
-          asm volatile("bar.arrive %0, 256;" ::"r"(5 + G) : "memory");  // GRP: slot written
-        } else {
-          asm volatile("bar.sync %0, 256;" ::"r"(5 + G) : "memory");
-          // fixed MMA order across the two groups (bit-reproducible accumulation): wait
-          // until the other group's issuer has issued stage q-1
-          if (q > 0) asm volatile("bar.sync %0, 64;" ::"r"(8 + G) : "memory");
-          tc_fence_after();
-          if (elect_one()) {
-            if (bw == 0) L0_TRACE(2, q);
-            const uint64_t bd0 = smem_desc(smem_u32(sI + L0_IMG_BYTES + L0_P_BYTES), 1024, 128, 0);
-            const uint32_t at0 = tbase + L0_ACC_COLS + G * L0_SLOT_COLS;
-            if (a.debug_mode & 2) {
-            } else if (!ext) {
-#pragma unroll
-              for (int h = 0; h < L0_NH; ++h)
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                  mma_ts(tbase + h * L0_DH, at0 + h * 32 + kk * 8,
-                         bd0 + (uint64_t)((h * (L0_DH * 64 * 2) + kk * 2048) >> 4), idesc, 1u);
-            } else {
-#pragma unroll
-              for (int h = 0; h < L0_NH; ++h)
-                mma_ts(tbase + h * L0_DH, at0 + h * 32,
-                       bd0 + (uint64_t)((h * (L0_DH * 64 * 2)) >> 4), idesc, 1u);
-            }
-            if (CL == 1) mma_commit(&empty[cs]);
-            else mma_commit_mc(&empty[cs], cmask);  // the peer multicasts into this stage too
-            mma_commit(&aempty[G]);
-            if (st + 2 >= nst) mma_commit(accfull);  // this group's last stage of the unit
-          }
-          __syncwarp();
-          if (q + 1 < q_total) asm volatile("bar.arrive %0, 64;" ::"r"(9 - G) : "memory");
-        }
-      }
-      // epilogue: this warp's 32 rows x EC columns, TMEM -> bf16 -> swizzled smem (1 KB)
-      // -> coalesced 32-byte row segments; then zero the columns for the next unit
-      if (bw == 0 && lane == 0) L0_TRACE(6, q);
-      // softmax normaliser of this row and this warp's head (unnormalised p from K_p0)
-      const float sc = a.pinv ? __ldg(a.pinv + ((long long)n * R + tile * 128 + m) * a.H +
-                                      hg * L0_NH + ecol / L0_DH)
-                              : 1.f;
-      mbar_wait(accfull, accphase);  // both groups' last MMAs of the unit (count 2)
-      accphase ^= 1;
-      if (bw == 0 && lane == 0) L0_TRACE(7, q);
-      tc_fence_after();
-      const long long row0 = (long long)n * R + tile * 128 + quarter * 32;
-#pragma unroll 1
-      for (int cb = 0; cb < ((a.debug_mode & 32) ? 0 : EC); cb += 16) {
-        const int col = ecol + cb;  // column within this head group
-        uint32_t v[16];
-        tmem_ld16(tbase + lane_off + col, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          uint4 o;
-          o.x = pack_bf16(sc * __uint_as_float(v[8 * k + 0]), sc * __uint_as_float(v[8 * k + 1]));
-          o.y = pack_bf16(sc * __uint_as_float(v[8 * k + 2]), sc * __uint_as_float(v[8 * k + 3]));
-          o.z = pack_bf16(sc * __uint_as_float(v[8 * k + 4]), sc * __uint_as_float(v[8 * k + 5]));
-          o.w = pack_bf16(sc * __uint_as_float(v[8 * k + 6]), sc * __uint_as_float(v[8 * k + 7]));
-          *reinterpret_cast<uint4*>(my_out + lane * 32 + ((k ^ ((lane >> 2) & 1)) << 4)) = o;
+        if ((bw & 7) == 0 && lane == 0) L0_TRACE(4, q);
+        if (pend_n >= 0) {  // first own stage of this unit staged: finish the previous unit
+          epilogue(pend_n, pend_tile, pend_hg, pend_sc);
+          pend_n = -1;
         }
         __syncwarp();
-        if (a.debug_mode & (64 | 128)) {
-          // timing experiment: the same bytes as one contiguous 1 KB run per warp chunk
-          __nv_bfloat16* dst = a.ctx + ((((long long)u * 16 + bw) * (EC / 16) + cb / 16) << 9);
-          if (a.debug_mode & 64) {
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-              *reinterpret_cast<uint4*>(dst + i * 256 + lane * 8) =
-                  *reinterpret_cast<const uint4*>(my_out + i * 512 + lane * 16);
-          } else {
-            fence_async_smem();
-            if (lane == 0) { bulk_store(dst, my_out, 1024); bulk_commit(); bulk_wait_read0(); }
-          }
-        } else if (!(a.debug_mode & 8)) {
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int rr = i * 16 + (lane >> 1), k = lane & 1;
-            const uint4 o =
-                *reinterpret_cast<const uint4*>(my_out + rr * 32 + ((k ^ ((rr >> 2) & 1)) << 4));
-            *reinterpret_cast<uint4*>(a.ctx + (row0 + rr) * a.D + hg * L0_NH * L0_DH + col +
-                                      k * 8) = o;
-          }
-        }
-        __syncwarp();
+        if (lane == 0) mbar_arrive_rank0(&ready[G]);  // READY(q): this warp's A is in TMEM
       }
-      zero_acc();
+      pend_n = n; pend_tile = tile; pend_hg = hg; pend_sc = sc_u;
     }
+    if (pend_n >= 0) epilogue(pend_n, pend_tile, pend_hg, pend_sc);
+    if (lead) bulk_wait0();
   }
 
   tc_fence_before();
   __syncthreads();
-  if (CL > 1) cluster_sync();
+  cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tbase, 512);
+    tmem_dealloc_pair(tbase, 512);
   }
 }
 
-cudaError_t launch_l0_node(const L0NodeArgs& a, int num_sms, cudaStream_t st) {
+cudaError_t launch_l0_node(const L0NodeArgs& a, const CUtensorMap& tm_ctx, int num_sms,
+                           cudaStream_t st) {
   const int R = a.B * a.S;
   const int nh = a.H % 4 == 0 ? 4 : 2;
   if (R % 128 || a.S % 128 || 128 % a.wp || a.H % nh || a.D != a.H * L0_DH || a.KE % 16)
     return cudaErrorInvalidValue;
   const int n_tiles = R / 128;
-  const int CL = (n_tiles % 2 == 0 && a.cluster != 1) ? 2 : 1;
-  const int units = a.n_nodes * (n_tiles / CL) * (a.H / nh);
-  const int max_cl = num_sms / CL;
-  const int grid = (units < max_cl ? units : max_cl) * CL;
-  void (*kern)(L0NodeArgs) = nullptr;
-  if (a.P == 8)
-    kern = nh == 4 ? (CL == 2 ? l0_node_kernel<64, 4, 2> : l0_node_kernel<64, 4, 1>)
-                   : (CL == 2 ? l0_node_kernel<64, 2, 2> : l0_node_kernel<64, 2, 1>);
-  else if (a.P == 4)
-    kern = nh == 4 ? (CL == 2 ? l0_node_kernel<16, 4, 2> : l0_node_kernel<16, 4, 1>)
-                   : (CL == 2 ? l0_node_kernel<16, 2, 2> : l0_node_kernel<16, 2, 1>);
-  else
+  const int units = a.n_nodes * ((n_tiles + 1) / 2) * (a.H / nh);
+  const int max_cl = num_sms / 2;
+  const int grid = (units < max_cl ? units : max_cl) * 2;
+  void (*kern)(L0NodeArgs, const CUtensorMap) = nullptr;
+  const bool rp = a.p_row_mode != 0;
+#define L0N_PICK(PP_, NH_) kern = rp ? l0_node_kernel<PP_, NH_, true> : l0_node_kernel<PP_, NH_, false>;
+  if (a.P == 8) {
+    if (nh == 4) { L0N_PICK(64, 4) } else { L0N_PICK(64, 2) }
+  } else if (a.P == 4) {
+    if (nh == 4) { L0N_PICK(16, 4) } else { L0N_PICK(16, 2) }
+  } else {
     return cudaErrorInvalidValue;
+  }
+#undef L0N_PICK
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L0_SMEM);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -782,12 +846,12 @@ cudaError_t launch_l0_node(const L0NodeArgs& a, int num_sms, cudaStream_t st) {
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, a);
+  e = cudaLaunchKernelEx(&cfg, kern, a, tm_ctx);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

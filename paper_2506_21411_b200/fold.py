@@ -215,21 +215,22 @@ def pack_rank(fr: FoldedRank, device) -> PackedRank:
     f32 = dict(device=device, dtype=torch.float32)
     stream = _lib.stream_handle()
 
-    def tile(src, nblk, K):
+    def tile(src, nblk, K, N):
         src = src.to(**f32).contiguous()
-        dst = torch.empty(nblk * 64 * K, device=device, dtype=torch.bfloat16)
-        _lib.call("dchag_tile_weights", _lib.ptr(src), nblk, K, _lib.ptr(dst), stream)
+        dst = torch.empty(nblk * N * K, device=device, dtype=torch.bfloat16)
+        _lib.call("dchag_tile_weights", _lib.ptr(src), nblk, K, N, _lib.ptr(dst), stream)
         return dst
 
-    # Mt [H][C_pad][PP][64] blocks
-    Msrc = torch.zeros(h, C_pad, pp, 64, **f32)
-    Msrc[:, :C] = fr.M.to(**f32).view(C, pp, h, 64).permute(2, 0, 1, 3)
-    Mt = tile(Msrc, h * C_pad, pp)
-    # Et [n0][H][KE][64] blocks: row k = node-local channel
-    Esrc = torch.zeros(n0, h, KE, 64, **f32)
+    # Mt [H][2 halves][C_pad*PP (channel-major K)][32]: a CTA pair splits each head's 64
+    # output columns, and one stage's K rows (CG channels) are one contiguous block per half
+    Msrc = torch.zeros(h, C_pad, pp, 2, 32, **f32)
+    Msrc[:, :C] = fr.M.to(**f32).view(C, pp, h, 2, 32).permute(2, 0, 1, 3, 4)
+    Mt = tile(Msrc.permute(0, 3, 1, 2, 4).reshape(h * 2, C_pad * pp, 32), h * 2, C_pad * pp, 32)
+    # Et [n0][H][2][KE][32]: row k = node-local channel
+    Esrc = torch.zeros(n0, h, KE, 2, 32, **f32)
     for n, (c0, g) in enumerate(zip(fr.l0_c0, fr.l0_g)):
-        Esrc[n, :, :g] = fr.Cb[c0:c0 + g].to(**f32).view(g, h, 64).permute(1, 0, 2)
-    Et = tile(Esrc, n0 * h, KE)
+        Esrc[n, :, :g] = fr.Cb[c0:c0 + g].to(**f32).view(g, h, 2, 32).permute(1, 0, 2, 3)
+    Et = tile(Esrc.permute(0, 1, 3, 2, 4).reshape(n0 * h * 2, KE, 32), n0 * h * 2, KE, 32)
     rowbias0 = torch.einsum("nsd,ndk->nsk", fr.posV.to(**f32), fr.Wp[0].to(**f32))
     rowbias0 = rowbias0.to(torch.bfloat16).contiguous()
     WUt = bU = posU = p_const = None
