@@ -64,17 +64,18 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
 /* Level-0 node context (K_l0, tcgen05 with A in TMEM):
  *   ctx[n][r][h*64:(h+1)*64] = sum_c p[r,c,h] * (patch_c[r] @ M_c[:, h-block])
  *                             + sum_c p[r,c,h] * E_n[c, h-block]
- * (the positional term pos[s] @ wv_n is folded into the next dchag_gemm_bf16 row bias)
  * Mt bf16 [H][2][32*C_pad*P*P] and Et bf16 [n_nodes][H][2][32*KE] are pre-tiled canonical
  * UMMA blocks (dchag_tile_weights, N = 32 halves; K runs over channel-major c*P*P + k); p_row_mode = 1 reads the dchag_l0_logits layout, 0 a constant
  * table p[poff + c*H + h]
  * (linear-mix nodes).  Requires head dim 64, H % 4 == 0, S % 128 == 0, 128 % (W/P) == 0,
  * P in {4, 8}.  pinv (optional, the dchag_l0_logits output): ctx row r, head h is scaled by
- * pinv[n][r][h]. */
+ * pinv[n][r][h].  posV (optional, bf16 [n_nodes][S][D]): the node's positional term
+ * pos[s] @ wv_n (x sum(mix) for linear nodes), added to ctx row r = (b, s). */
 int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
                   int P, int H, int D, int n_nodes, const int* node_c0, const int* node_g,
                   const long long* node_poff, int p_row_mode, const void* p, const float* pinv,
-                  const void* Mt, int C_pad, const void* Et, int KE, void* ctx, void* stream);
+                  const void* Mt, int C_pad, const void* Et, int KE, const void* posV, void* ctx,
+                  void* stream);
 
 /* Upper-level / final combine (K_comb): ctx[n][r][:] = sum_j w_j(r,h) V_{first+j}[r][:],
  * w = softmax_j(L_{first+j}[r][h]) (attention; mix == NULL) or mix[first+j] (linear).

@@ -25,7 +25,7 @@ SIGNATURES = {
     "dchag_l0_logits": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                         c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "dchag_l0_node": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
-                      c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_int, c_vp, c_vp],
+                      c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp],
     "dchag_combine": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_vp, c_ll,
                       c_vp, c_vp, c_vp],
     "dchag_combine_strided": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_ll,

@@ -117,20 +117,14 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
   if ((sAmi * 2) % 16 || (sAmo * 2) % 16 || (sAg * 2) % 16 || (sWg * 2) % 16)
     return fail(DCHAG_ERR_SHAPE, "gemm: strides must be multiples of 16 bytes");
   const int bk = (K % 64 == 0) ? 64 : (K % 32 == 0 ? 32 : 16);
-  // N tiling: <= 256 columns per tile; prefer an even tile count (enables the N-pair cluster)
-  int ntn = (N + 255) / 256;
-  int bn = ((N + ntn - 1) / ntn + 15) / 16 * 16;
-  if (ntn > 1 && ntn % 2) {
-    const int bn2 = ((N + ntn) / (ntn + 1) + 15) / 16 * 16;
-    if ((long long)bn2 * (ntn + 1) <= (long long)N * 105 / 100) { ++ntn; bn = bn2; }
-  }
+  // N tiling: <= 256 columns per tile, as even as possible (N = 1040 -> 5 x 208)
+  const int ntn = (N + 255) / 256;
+  const int bn = ((N + ntn - 1) / ntn + 15) / 16 * 16;
   const int ntm = Mo * Mi / 128;
-  // clusters (TMA multicast) only on the K-64 path and when the tile grid divides evenly
-  int cm = 1, cn = 1;  // clusters measured no faster on B200; opt-in for probes
-  if (const char* f = getenv("DCHAG_GEMM_CLUSTER")) {  // experiment override, e.g. "21"
-    if (f[0] == '2' && bk == 64 && ntm % 2 == 0 && (bn / 2) % 8 == 0) cm = 2;
-    if (f[0] && f[1] == '2' && bk == 64 && ((N + bn - 1) / bn) % 2 == 0) cn = 2;
-  }
+  // CTA pairs (M = 256 tiles, W split across the pair) on the K-64 path when the M tiles pair
+  // up; DCHAG_GEMM_PAIR=0 selects the single-CTA kernel (A/B probes)
+  int pair = bk == 64 && ntm % 2 == 0 && (bn / 2) % 8 == 0;
+  if (const char* f = getenv("DCHAG_GEMM_PAIR")) pair = pair && atoi(f) != 0;
   const CUtensorMapSwizzle swz = bk == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
                                  : bk == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
                                             : CU_TENSOR_MAP_SWIZZLE_32B;
@@ -138,21 +132,33 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
   {
     cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)Mi, (cuuint64_t)Mo, (cuuint64_t)G};
     cuuint64_t str[3] = {(cuuint64_t)sAmi * 2, (cuuint64_t)sAmo * 2, (cuuint64_t)sAg * 2};
-    cuuint32_t box[4] = {(cuuint32_t)bk, (cuuint32_t)(128 / cn), 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)bk, 128u, 1, 1};
     int rc = make_map(&tA, A, 4, dims, str, box, swz);
     if (rc) return rc;
   }
   {
     cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)N, (cuuint64_t)G};
     cuuint64_t str[2] = {(cuuint64_t)K * 2, (cuuint64_t)sWg * 2};
-    cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)(bn / cm), 1};
+    cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)(pair ? bn / 2 : bn), 1};
     int rc = make_map(&tW, W, 3, dims, str, box, swz);
     if (rc) return rc;
   }
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.G = G; a.M = Mo * Mi; a.Mi = Mi; a.N = N; a.Nv = Nv; a.K = K; a.BN = bn;
-  a.cm = cm; a.cn = cn;
+  a.pair = pair;
+  // value columns by TMA tensor store (bf16 output, 16-byte aligned strides, 32-row boxes)
+  CUtensorMap tV;
+  memset(&tV, 0, sizeof(tV));
+  if (outV && !outV_f32 && Nv >= 32 && Mi % 32 == 0 &&
+      ((reinterpret_cast<uintptr_t>(outV) | (uintptr_t)(sVmi * 2) | (uintptr_t)(sVmo * 2) |
+        (uintptr_t)(sVg * 2)) % 16) == 0 && !getenv("DCHAG_GEMM_NO_TMA_STORE")) {
+    cuuint64_t dims[4] = {(cuuint64_t)Nv, (cuuint64_t)Mi, (cuuint64_t)Mo, (cuuint64_t)G};
+    cuuint64_t str[3] = {(cuuint64_t)sVmi * 2, (cuuint64_t)(Mo > 1 ? sVmo : Mi * sVmi) * 2,
+                         (cuuint64_t)(G > 1 ? sVg : Mo * (Mo > 1 ? sVmo : Mi * sVmi)) * 2};
+    cuuint32_t box[4] = {32, 32, 1, 1};
+    if (make_map(&tV, outV, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B) == DCHAG_OK) a.v_tma = 1;
+  }
   a.debug = getenv("DCHAG_GEMM_DEBUG") ? atoi(getenv("DCHAG_GEMM_DEBUG")) : 0;
   a.bias = bias; a.bias_g = bias_g;
   a.rowbias = reinterpret_cast<const __nv_bfloat16*>(rowbias);
@@ -160,7 +166,7 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
   a.rowbias_period = rowbias_period > 0 ? rowbias_period : 1;
   a.outV = outV; a.outV_f32 = outV_f32; a.sVg = sVg; a.sVmo = sVmo; a.sVmi = sVmi;
   a.outL = outL; a.sLg = sLg; a.sLmo = sLmo; a.sLmi = sLmi;
-  return cuda_status(launch_gemm(tA, tW, a, bk, num_sms_cached(), S(stream)), "gemm");
+  return cuda_status(launch_gemm(tA, tW, tV, a, bk, num_sms_cached(), S(stream)), "gemm");
 }
 
 int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
@@ -190,7 +196,8 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
 int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
                   int P, int H, int D, int n_nodes, const int* node_c0, const int* node_g,
                   const long long* node_poff, int p_row_mode, const void* p, const float* pinv,
-                  const void* Mt, int C_pad, const void* Et, int KE, void* ctx, void* stream) {
+                  const void* Mt, int C_pad, const void* Et, int KE, const void* posV, void* ctx,
+                  void* stream) {
   if (Himg % P || W % P) return fail(DCHAG_ERR_SHAPE, "l0_node: image not divisible by patch");
   L0NodeArgs a;
   a.img = reinterpret_cast<const __nv_bfloat16*>(img);
@@ -221,7 +228,17 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
   const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
   const cuuint32_t box[2] = {64, 128};
   if (int rc = make_map(&tm, ctx, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
-  return cuda_status(launch_l0_node(a, tm, num_sms_cached(), S(stream)), "l0_node");
+  // posV [n_nodes * S rows][D] bf16, same box geometry (loaded into the staging tile)
+  CUtensorMap tp;
+  memset(&tp, 0, sizeof(tp));
+  a.has_pos = posV != nullptr;
+  if (posV) {
+    if (reinterpret_cast<uintptr_t>(posV) % 16)
+      return fail(DCHAG_ERR_SHAPE, "l0_node: posV must be 16-byte aligned");
+    const cuuint64_t pdims[2] = {(cuuint64_t)D, (cuuint64_t)n_nodes * a.S};
+    if (int rc = make_map(&tp, posV, 2, pdims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;
+  }
+  return cuda_status(launch_l0_node(a, tm, tp, num_sms_cached(), S(stream)), "l0_node");
 }
 
 int dchag_combine(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,

@@ -11,7 +11,9 @@ namespace dchag {
 struct GemmArgs {
   int G, M, Mi, N, Nv, K, BN;   // M = Mo * Mi rows per group
   int debug;                    // timing probes (DCHAG_GEMM_DEBUG)
-  int cm, cn;                   // cluster shape (TMA boxes are built with 128/cn, BN/cm rows)
+  int pair;                     // 1: CTA-pair kernel (W TMA box built with BN/2 rows)
+  int v_tma;                    // 1: bf16 value columns leave through TMA stores (tensor map
+                                //    over outV, box 32 columns x 32 rows, 64B swizzle)
   const float* bias;            // [G][bias_g] fp32 or null
   long long bias_g;
   const __nv_bfloat16* rowbias; // [G][rowbias_g] with row (mi % period) * rowbias_row, or null
@@ -24,8 +26,8 @@ struct GemmArgs {
   long long sLg, sLmo, sLmi;
 };
 
-cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const GemmArgs& a,
-                        int bk, int num_sms, cudaStream_t st);
+cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUtensorMap& tV,
+                        const GemmArgs& a, int bk, int num_sms, cudaStream_t st);
 
 // Level-0 node: logits + softmax over the node's channels (tensor cores via mma.sync)
 struct L0LogitArgs {
@@ -66,12 +68,13 @@ struct L0NodeArgs {
   const __nv_bfloat16* Et;     // [n_nodes][H][2][KE/8][4][8][8] ext (bias) blocks, same split
   int KE;
   __nv_bfloat16* ctx;          // [n_nodes][R][D]
+  int has_pos;                 // 1: ctx += posV[n][s] (tensor map tm_pos over [n_nodes*S][D])
   int debug_mode;              // timing probes: 1 no A build, 2 no MMA, 4 no copies,
                                // 8 no ctx stores, 32 no drain
   long long* trace;            // optional [8][256] clock64 timeline of CTA 0 (debug)
 };
-cudaError_t launch_l0_node(const L0NodeArgs& a, const CUtensorMap& tm_ctx, int num_sms,
-                           cudaStream_t st);
+cudaError_t launch_l0_node(const L0NodeArgs& a, const CUtensorMap& tm_ctx,
+                           const CUtensorMap& tm_pos, int num_sms, cudaStream_t st);
 
 // Upper-level combine: ctx[n][r][:] = sum_j p_jh(r) * V_child(j)[r][:]
 struct CombineArgs {

@@ -19,14 +19,15 @@ constexpr int GEMM_BM = 128;
 constexpr int GEMM_BN_MAX = 256;
 constexpr int GEMM_THREADS = 320;  // producer, MMA, 8 epilogue warps
 constexpr int GEMM_STAGE_OUT = 8 * 32 * 128;  // epilogue staging: 8 warps x 32 rows x 128 B
+constexpr int GEMM_BIAS_SMEM = 8 * 4 * 32 * 4;  // per-warp bias of its 4 column groups (fp32)
 
-template <int BK, int STAGES>
+template <int BK, int STAGES, bool PAIR = false>
 struct GemmSmem {
   static constexpr int A_BYTES = GEMM_BM * BK * 2;
-  static constexpr int W_BYTES = GEMM_BN_MAX * BK * 2;
+  static constexpr int W_BYTES = (PAIR ? GEMM_BN_MAX / 2 : GEMM_BN_MAX) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + W_BYTES;
   static constexpr int TOTAL =
-      STAGES * STAGE_BYTES + GEMM_STAGE_OUT + 1024 /*align*/ + 256 /*barriers*/;
+      STAGES * STAGE_BYTES + GEMM_STAGE_OUT + GEMM_BIAS_SMEM + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 template <int BK>
@@ -34,22 +35,59 @@ DEV uint32_t swz_layout() {
   return BK == 64 ? 2u : (BK == 32 ? 4u : 6u);
 }
 
-// Cluster CM x CN (TMA multicast): the CM CTAs of a cluster that share an N-tile load one
-// 1/CM row slice of the W tile each and multicast it; the CN CTAs sharing an M-tile do the
-// same for A.  A CTA's empty[] barrier therefore counts the MMA commits of every CTA that
-// writes into its shared memory (itself, its M-partner, its N-partner).  This cuts the
-// L2->SMEM fill per CTA (the measured limiter, ~50 B/cycle/SM) by up to 2x.
-template <int BK, int STAGES, int CM, int CN>
+// PAIR: a CTA pair (cluster of 2, cta_group::2) computes a 256 x BN tile. Rank r loads rows
+// [128r, 128r + 128) of the A tile and rows [r BN/2, (r+1) BN/2) of the W tile into its own
+// shared memory, both signalling the leader's full barrier (.cta_group::2 TMA); the leader
+// issues M256 MMAs that read A from each CTA and W split by N across the pair, so each SM's
+// shared memory carries half the W traffic (the 1-CTA kernel was bound at ~216 B/cycle of
+// TMA writes + MMA reads per SM against ~128 available). Each CTA drains its own 128 rows.
+DEV void mma_ss_pair(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d), "l"(ad), "l"(bd),
+      "r"(idesc), "r"(acc)
+      : "memory");
+}
+DEV void commit_pair_g(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"((uint16_t)3)
+      : "memory");
+}
+DEV uint32_t rank0_addr(const void* p) {  // shared::cluster address of rank 0's copy
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+DEV void tma_load_4d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cl, int c0, int c1,
+                          int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".cta_group::2 [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cl), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+DEV void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cl, int c0, int c1,
+                          int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".cta_group::2 [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cl), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+template <int BK, int STAGES, bool PAIR>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
-                GemmArgs args) {
-  using SM = GemmSmem<BK, STAGES>;
-  constexpr int CL = CM * CN;
+                const __grid_constant__ CUtensorMap tmV, GemmArgs args) {
+  using SM = GemmSmem<BK, STAGES, PAIR>;
+  constexpr int CL = PAIR ? 2 : 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* stage_out = smem + STAGES * SM::STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + GEMM_STAGE_OUT);
+  float* bias_smem = reinterpret_cast<float*>(stage_out + GEMM_STAGE_OUT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + GEMM_STAGE_OUT + GEMM_BIAS_SMEM);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -59,24 +97,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int lane = lane_id();
   const int n_tiles_n = (args.N + args.BN - 1) / args.BN;
   const int n_tiles_m = args.M / GEMM_BM;
-  const int ctiles_n = n_tiles_n / CN, ctiles_m = n_tiles_m / CM;
+  const int ctiles_n = n_tiles_n, ctiles_m = n_tiles_m / CL;
   const int ctiles_per_g = ctiles_m * ctiles_n;
   const int total_ct = ctiles_per_g * args.G;
   const int k_steps = args.K / BK;
-  const int crank = CL > 1 ? (int)cluster_rank() : 0;
-  const int rm = crank % CM, rn = crank / CM;
+  const int crank = PAIR ? (int)cluster_rank() : 0;
   const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
-  // CTAs that write into this CTA's shared memory (and that this CTA writes into)
-  const uint16_t m_mask = CM == 1 ? 0 : (uint16_t)((1u << crank) | (1u << ((rm ^ 1) + rn * CM)));
-  const uint16_t n_mask = CN == 1 ? 0 : (uint16_t)((1u << crank) | (1u << (rm + (rn ^ 1) * CM)));
-  const uint16_t peer_mask = (uint16_t)((1u << crank) | m_mask | n_mask);
   auto decode = [&](int ct, int& g, int& mt, int& nt) {
     g = ct / ctiles_per_g;
     const int rem = ct - g * ctiles_per_g;
     const int mc = rem / ctiles_n;
-    const int nc = rem - mc * ctiles_n;
-    mt = mc * CM + rm;
-    nt = nc * CN + rn;
+    nt = rem - mc * ctiles_n;
+    mt = mc * CL + crank;
   };
 
   if (warp == 0 && lane == 0) {
@@ -84,18 +116,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch(&tmW);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], (CM > 1) + (CN > 1) + 1);
+      mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);
+      mbar_init(&tempty[a], 8 * CL);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tslot, 512);
+  if (warp == 1) {
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(tslot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      tmem_alloc(tslot, 512);
+    }
+  }
   tc_fence_before();
   __syncthreads();
-  if (CL > 1) cluster_sync();  // peers multicast into our barriers from here on
+  if (PAIR) cluster_sync();  // the pair signals each other's barriers from here on
   tc_fence_after();
   const uint32_t tmem_base = *tslot;
 
@@ -104,7 +145,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      const int a_rows = GEMM_BM / CN, w_rows = args.BN / CM;
+      const int w_rows = args.BN / CL;
       for (int ct = cid; ct < total_ct; ct += ncl) {
         int g, mt, nt;
         decode(ct, g, mt, nt);
@@ -114,53 +155,63 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * SM::STAGE_BYTES;
           uint8_t* sW = sA + SM::A_BYTES;
-          mbar_expect_tx(&full[stage], SM::A_BYTES + args.BN * BK * 2);
-          if (CN == 1)
+          if (PAIR) {
+            // both CTAs' bytes complete on the leader's full barrier
+            if (crank == 0)
+              mbar_expect_tx(&full[stage], 2 * (SM::A_BYTES + w_rows * BK * 2));
+            const uint32_t fb = rank0_addr(&full[stage]);
+            tma_load_4d_pair(sA, &tmA, fb, ks * BK, mi, mo, g);
+            tma_load_3d_pair(sW, &tmW, fb, ks * BK, nt * args.BN + crank * w_rows, g);
+          } else {
+            mbar_expect_tx(&full[stage], SM::A_BYTES + args.BN * BK * 2);
             tma_load_4d(sA, &tmA, &full[stage], ks * BK, mi, mo, g);
-          else  // my half of the A tile, to me and my N-partner (same M-tile)
-            tma_load_4d_mc(sA + rn * a_rows * BK * 2, &tmA, &full[stage], ks * BK,
-                           mi + rn * a_rows, mo, g, n_mask);
-          if (CM == 1)
             tma_load_3d(sW, &tmW, &full[stage], ks * BK, nt * args.BN, g);
-          else  // my slice of the W tile, to me and my M-partner (same N-tile)
-            tma_load_3d_mc(sW + rm * w_rows * BK * 2, &tmW, &full[stage], ks * BK,
-                           nt * args.BN + rm * w_rows, g, m_mask);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    const uint32_t idesc = idesc_bf16_f32(GEMM_BM, args.BN);
-    constexpr uint32_t SBO = 8 * BK * 2;  // 8 rows x swizzle width
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int ct = cid; ct < total_ct; ct += ncl) {
-      mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator buffer
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * GEMM_BN_MAX;
-      for (int ks = 0; ks < k_steps; ++ks) {
-        mbar_wait(&full[stage], phase);
+    // ------------------------------------------------ MMA issuer (the leader of a pair)
+    if (crank == 0) {
+      const uint32_t idesc = idesc_bf16_f32(GEMM_BM * CL, args.BN);
+      constexpr uint32_t SBO = 8 * BK * 2;  // 8 rows x swizzle width
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int ct = cid; ct < total_ct; ct += ncl) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogues drained this accumulator buffer
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t a_addr = smem_u32(smem + stage * SM::STAGE_BYTES);
-          const uint32_t w_addr = a_addr + SM::A_BYTES;
+        const uint32_t d_tmem = tmem_base + acc * GEMM_BN_MAX;
+        for (int ks = 0; ks < k_steps; ++ks) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a_addr = smem_u32(smem + stage * SM::STAGE_BYTES);
+            const uint32_t w_addr = a_addr + SM::A_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = smem_desc(a_addr + kk * 32, 16, SBO, swz_layout<BK>());
-            const uint64_t wd = smem_desc(w_addr + kk * 32, 16, SBO, swz_layout<BK>());
-            if (!(args.debug & 4)) mma_ss(d_tmem, ad, wd, idesc, (ks | kk) != 0);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t ad = smem_desc(a_addr + kk * 32, 16, SBO, swz_layout<BK>());
+              const uint64_t wd = smem_desc(w_addr + kk * 32, 16, SBO, swz_layout<BK>());
+              if (!(args.debug & 4)) {
+                if (PAIR) mma_ss_pair(d_tmem, ad, wd, idesc, (ks | kk) != 0);
+                else mma_ss(d_tmem, ad, wd, idesc, (ks | kk) != 0);
+              }
+            }
+            if (PAIR) {
+              commit_pair_g(&empty[stage]);
+              if (ks == k_steps - 1) commit_pair_g(&tfull[acc]);
+            } else {
+              mma_commit(&empty[stage]);
+              if (ks == k_steps - 1) mma_commit(&tfull[acc]);
+            }
           }
-          if (CL == 1) mma_commit(&empty[stage]);
-          else mma_commit_mc(&empty[stage], peer_mask);
-          if (ks == k_steps - 1) mma_commit(&tfull[acc]);
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else {
     // ------------------------------------------------ epilogue (warps 2..9)
@@ -173,6 +224,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int row_in_tile = quarter * 32 + lane;
     const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
     uint8_t* my_out = stage_out + (warp - 2) * (32 * 128);
+    int vbuf = 0;  // TMA-store staging buffer of this warp (two of 2 KB)
     const int n_groups = (args.BN + 31) / 32;
     const bool rb_vec = (args.rowbias_row & 7) == 0 && (args.rowbias_g & 7) == 0;
     const bool b_vec = (args.bias_g & 3) == 0;
@@ -186,7 +238,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // prefetch this thread's row bias for its column groups (in flight during the wait)
       uint4 rbv[4][4];
       const __nv_bfloat16* rb =
-          args.rowbias ? args.rowbias + (size_t)g * args.rowbias_g +
+          (args.rowbias && !(args.debug & 2)) ? args.rowbias + (size_t)g * args.rowbias_g +
                              (size_t)(mi % args.rowbias_period) * args.rowbias_row
                        : nullptr;
 #pragma unroll
@@ -212,12 +264,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
       }
-      const float* bias = args.bias ? args.bias + (size_t)g * args.bias_g : nullptr;
+      const float* bias =
+          (args.bias && !(args.debug & 2)) ? args.bias + (size_t)g * args.bias_g : nullptr;
+      // this warp's bias columns (groups hf, hf+2, hf+4, hf+6) -> shared memory with one
+      // coalesced load per lane, read back as broadcasts (the per-group global loads of every
+      // lane were the epilogue's largest cost)
+      float* wbias = bias_smem + (warp - 2) * 128;
+      if (bias) {
+        __syncwarp();  // the previous tile's broadcast reads are done
+        const int n = nt * args.BN + (hf + 2 * (lane >> 3)) * 32 + (lane & 7) * 4;
+        float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (b_vec && n + 4 <= args.N) {
+          b4 = __ldg(reinterpret_cast<const float4*>(bias + n));
+        } else {
+          if (n < args.N) b4.x = __ldg(bias + n);
+          if (n + 1 < args.N) b4.y = __ldg(bias + n + 1);
+          if (n + 2 < args.N) b4.z = __ldg(bias + n + 2);
+          if (n + 3 < args.N) b4.w = __ldg(bias + n + 3);
+        }
+        reinterpret_cast<float4*>(wbias)[lane] = b4;
+        __syncwarp();
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = lane_base + acc * GEMM_BN_MAX;
 #pragma unroll
-      for (int gi = 0; gi < 4; ++gi) {
+      for (int gi = 0; gi < ((args.debug & 8) ? 0 : 4); ++gi) {
         const int grp = hf + 2 * gi;
         if (grp >= n_groups) break;
         const int n0 = nt * args.BN + grp * 32;
@@ -236,16 +308,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         if (bias) {
-          if (b_vec && n0 + 32 <= args.N) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + n0 + j));
-              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (n0 + j < args.N) v[j] += __ldg(bias + n0 + j);
+          for (int j = 0; j < 32; j += 4) {
+            const float4 b4 = reinterpret_cast<const float4*>(wbias + gi * 32)[j / 4];
+            v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
           }
         }
         if (args.debug & 1) {
@@ -256,7 +322,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if ((gcols == 32 || gcols == 16) && n0 + gcols <= args.Nv) {
           // value region: stage in smem (swizzled) + coalesced copy-out of whole row segments
           const int nk = gcols / 8;          // 16-byte chunks per row (bf16)
-          if (!args.outV_f32) {
+          if (!args.outV_f32 && args.v_tma && gcols == 32) {
+            // 32 rows x 32 columns -> 64B-swizzled staging (two buffers per warp) -> one TMA
+            // tensor store; the store drains asynchronously while the warp moves on
+            uint8_t* buf = my_out + vbuf * 2048;
+            if (lane == 0) bulk_wait_read1();  // this buffer's previous store has read it
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              uint4 o;
+              o.x = pack_bf16(v[8 * k + 0], v[8 * k + 1]);
+              o.y = pack_bf16(v[8 * k + 2], v[8 * k + 3]);
+              o.z = pack_bf16(v[8 * k + 4], v[8 * k + 5]);
+              o.w = pack_bf16(v[8 * k + 6], v[8 * k + 7]);
+              *reinterpret_cast<uint4*>(buf + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) = o;
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const int r0 = mt * GEMM_BM + quarter * 32;
+              const int mo0 = r0 / args.Mi, mi0 = r0 - mo0 * args.Mi;
+              tma_store_4d(&tmV, smem_u32(buf), n0, mi0, mo0, g);
+              bulk_commit();
+            }
+            vbuf ^= 1;
+          } else if (!args.outV_f32) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               if (k < nk) {
@@ -334,30 +424,43 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (PAIR)  // the leader's MMA warp waits for both CTAs' drains
+          asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(rank0_addr(&tempty[acc]))
+                       : "memory");
+        else
+          mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) bulk_wait0();  // this warp's tensor stores complete before exit
   }
 
   tc_fence_before();
   __syncthreads();
-  if (CL > 1) cluster_sync();  // no CTA leaves while peers may still signal its barriers
+  if (PAIR) cluster_sync();  // no CTA leaves while its peer may still signal its barriers
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
+                   : "memory");
+    else
+      tmem_dealloc(tmem_base, 512);
   }
 }
 
-template <int BK, int STAGES, int CM, int CN>
+template <int BK, int STAGES, bool PAIR>
 static cudaError_t launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tW,
-                                 const GemmArgs& a, int num_sms, cudaStream_t st) {
-  using SM = GemmSmem<BK, STAGES>;
-  auto kern = gemm_kernel<BK, STAGES, CM, CN>;
+                                 const CUtensorMap& tV, const GemmArgs& a, int num_sms,
+                                 cudaStream_t st) {
+  using SM = GemmSmem<BK, STAGES, PAIR>;
+  static_assert(SM::TOTAL <= 227 * 1024, "shared memory");
+  auto kern = gemm_kernel<BK, STAGES, PAIR>;
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
   if (e != cudaSuccess) return e;
-  constexpr int CL = CM * CN;
-  const int ctiles = a.G * (a.M / GEMM_BM / CM) * ((a.N + a.BN - 1) / a.BN / CN);
+  constexpr int CL = PAIR ? 2 : 1;
+  const int ctiles = a.G * (a.M / GEMM_BM / CL) * ((a.N + a.BN - 1) / a.BN);
   const int max_cl = num_sms / CL;
   const int grid = (ctiles < max_cl ? ctiles : max_cl) * CL;
   cudaLaunchConfig_t cfg = {};
@@ -372,22 +475,19 @@ static cudaError_t launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tW,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, tA, tW, a);
+  e = cudaLaunchKernelEx(&cfg, kern, tA, tW, tV, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const GemmArgs& a,
-                        int bk, int num_sms, cudaStream_t st) {
-  const bool cm = a.cm == 2, cn = a.cn == 2;
+cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUtensorMap& tV,
+                        const GemmArgs& a, int bk, int num_sms, cudaStream_t st) {
   switch (bk) {
     case 64:
-      if (cm && cn) return launch_gemm_t<64, 4, 2, 2>(tA, tW, a, num_sms, st);
-      if (cm) return launch_gemm_t<64, 4, 2, 1>(tA, tW, a, num_sms, st);
-      if (cn) return launch_gemm_t<64, 4, 1, 2>(tA, tW, a, num_sms, st);
-      return launch_gemm_t<64, 4, 1, 1>(tA, tW, a, num_sms, st);
-    case 32: return launch_gemm_t<32, 6, 1, 1>(tA, tW, a, num_sms, st);
-    case 16: return launch_gemm_t<16, 8, 1, 1>(tA, tW, a, num_sms, st);
+      if (a.pair) return launch_gemm_t<64, 5, true>(tA, tW, tV, a, num_sms, st);
+      return launch_gemm_t<64, 3, false>(tA, tW, tV, a, num_sms, st);
+    case 32: return launch_gemm_t<32, 6, false>(tA, tW, tV, a, num_sms, st);
+    case 16: return launch_gemm_t<16, 8, false>(tA, tW, tV, a, num_sms, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -434,7 +434,8 @@ DEV void tma_store_2d(const CUtensorMap* m, uint32_t src, int c0, int c1) {
 //               that TMA tensor stores write to ctx in the background of the next unit.
 template <int PP, int L0_NH, bool ROWP>
 __global__ void __launch_bounds__(L0_THREADS, 1)
-    l0_node_kernel(L0NodeArgs a, const __grid_constant__ CUtensorMap tm_ctx) {
+    l0_node_kernel(L0NodeArgs a, const __grid_constant__ CUtensorMap tm_ctx,
+                   const __grid_constant__ CUtensorMap tm_pos) {
   constexpr int CG = 64 / PP;        // channels per main stage (K = 64 per head per stage)
   constexpr int P = PP == 64 ? 8 : 4;
   constexpr int NBAR = 288;          // image gate warp + one group's 8 builder warps
@@ -449,7 +450,8 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
   uint64_t* aempty = empty + L0_STAGES;
   uint64_t* accfull = aempty + 2;
   uint64_t* ready = accfull + 1;  // [2], rank 0's copy is the one used
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(ready + 2);
+  uint64_t* posv_full = ready + 2;  // the unit's positional tile landed in the staging tile
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(posv_full + 1);
 
   const int warp = warp_id(), lane = lane_id();
   const int R = a.B * a.S;
@@ -482,6 +484,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
     mbar_init(accfull, 1);
     mbar_init(&ready[0], 16);  // 8 builder warps x 2 CTAs
     mbar_init(&ready[1], 16);
+    mbar_init(posv_full, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_pair(tslot, 512);
@@ -635,12 +638,32 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
     // tensor stores write it to ctx in the background. It runs after the builders have
     // already staged their first A slot of the next unit (overlapping the MMA tail), and
     // before that slot's READY: the next unit's first MMAs overwrite the accumulator.
+    // positional tile of a unit: TMA loads of posV[n][s0 .. s0+128][head group] into the
+    // staging tile (the drain adds it in place), issued once the previous unit's ctx stores
+    // have read the staging
+    uint32_t pos_phase = 0;
+    bool pos_issued_cur = false, pos_issued_pend = false;
+    auto issue_pos = [&](int n, int tile, int hg) {
+      bulk_wait_read0();
+      const int s0 = (min(tile, n_tiles - 1) * 128) % a.S;
+      mbar_expect_tx(posv_full, L0_NH * 128 * 128);
+      for (int hd = 0; hd < L0_NH; ++hd)
+        tma_load_2d(stage_out + hd * (128 * 128), &tm_pos, posv_full, (hg * L0_NH + hd) * L0_DH,
+                    n * a.S + s0);
+    };
     auto epilogue = [&](int n, int tile, int hg, float sc) {
       mbar_wait(accfull, accphase);  // the unit's last MMAs
       accphase ^= 1;
-      if (lead) bulk_wait_read0();   // the previous unit's stores have read the staging
+      if (a.has_pos) {
+        // the staging tile holds this unit's positional rows (posV[n][s][head group])
+        if (lead && !pos_issued_pend) issue_pos(n, tile, hg);
+        mbar_wait(posv_full, pos_phase);
+        pos_phase ^= 1;
+      } else {
+        if (lead) bulk_wait_read0();   // the previous unit's stores have read the staging
+        asm volatile("bar.sync 5, 512;" ::: "memory");  // ACC0: staging free
+      }
       tc_fence_after();
-      asm volatile("bar.sync 5, 512;" ::: "memory");  // ACC0: staging free
       if (!(a.debug_mode & 32)) {
         const uint32_t sout = smem_u32(stage_out);
 #pragma unroll
@@ -653,12 +676,25 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
           const uint32_t rowb = sout + hd * (128 * 128) + m * 128;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
+            const uint32_t addr = rowb + ((uint32_t)((c8 + k) ^ (m & 7)) << 4);
+            float f[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = sc * __uint_as_float(v[8 * k + e]);
+            if (a.has_pos) {  // + posV (the token's positional term through wv_n)
+              const uint4 pv4 = lds128(addr);
+              const uint32_t pw[4] = {pv4.x, pv4.y, pv4.z, pv4.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                f[2 * e] += bf16lo(pw[e]);
+                f[2 * e + 1] += bf16hi(pw[e]);
+              }
+            }
             uint4 o;
-            o.x = pack_bf16(sc * __uint_as_float(v[8 * k + 0]), sc * __uint_as_float(v[8 * k + 1]));
-            o.y = pack_bf16(sc * __uint_as_float(v[8 * k + 2]), sc * __uint_as_float(v[8 * k + 3]));
-            o.z = pack_bf16(sc * __uint_as_float(v[8 * k + 4]), sc * __uint_as_float(v[8 * k + 5]));
-            o.w = pack_bf16(sc * __uint_as_float(v[8 * k + 6]), sc * __uint_as_float(v[8 * k + 7]));
-            sts128(rowb + ((uint32_t)((c8 + k) ^ (m & 7)) << 4), o);
+            o.x = pack_bf16(f[0], f[1]);
+            o.y = pack_bf16(f[2], f[3]);
+            o.z = pack_bf16(f[4], f[5]);
+            o.w = pack_bf16(f[6], f[7]);
+            sts128(addr, o);
           }
         }
       }
@@ -797,11 +833,16 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
         if (pend_n >= 0) {  // first own stage of this unit staged: finish the previous unit
           epilogue(pend_n, pend_tile, pend_hg, pend_sc);
           pend_n = -1;
+        } else if (a.has_pos && lead && !pos_issued_cur) {
+          issue_pos(n, tile, hg);  // the previous unit's stores were issued a stage ago
+          pos_issued_cur = true;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_rank0(&ready[G]);  // READY(q): this warp's A is in TMEM
       }
       pend_n = n; pend_tile = tile; pend_hg = hg; pend_sc = sc_u;
+      pos_issued_pend = pos_issued_cur;
+      pos_issued_cur = false;
     }
     if (pend_n >= 0) epilogue(pend_n, pend_tile, pend_hg, pend_sc);
     if (lead) bulk_wait0();
@@ -816,8 +857,8 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
   }
 }
 
-cudaError_t launch_l0_node(const L0NodeArgs& a, const CUtensorMap& tm_ctx, int num_sms,
-                           cudaStream_t st) {
+cudaError_t launch_l0_node(const L0NodeArgs& a, const CUtensorMap& tm_ctx,
+                           const CUtensorMap& tm_pos, int num_sms, cudaStream_t st) {
   const int R = a.B * a.S;
   const int nh = a.H % 4 == 0 ? 4 : 2;
   if (R % 128 || a.S % 128 || 128 % a.wp || a.H % nh || a.D != a.H * L0_DH || a.KE % 16)
@@ -826,7 +867,7 @@ cudaError_t launch_l0_node(const L0NodeArgs& a, const CUtensorMap& tm_ctx, int n
   const int units = a.n_nodes * ((n_tiles + 1) / 2) * (a.H / nh);
   const int max_cl = num_sms / 2;
   const int grid = (units < max_cl ? units : max_cl) * 2;
-  void (*kern)(L0NodeArgs, const CUtensorMap) = nullptr;
+  void (*kern)(L0NodeArgs, const CUtensorMap, const CUtensorMap) = nullptr;
   const bool rp = a.p_row_mode != 0;
 #define L0N_PICK(PP_, NH_) kern = rp ? l0_node_kernel<PP_, NH_, true> : l0_node_kernel<PP_, NH_, false>;
   if (a.P == 8) {
@@ -851,7 +892,7 @@ cudaError_t launch_l0_node(const L0NodeArgs& a, const CUtensorMap& tm_ctx, int n
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, a, tm_ctx);
+  e = cudaLaunchKernelEx(&cfg, kern, a, tm_ctx, tm_pos);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

@@ -188,7 +188,7 @@ class PackedRank:
     posU: torch.Tensor | None
     Mt: torch.Tensor
     Et: torch.Tensor
-    rowbias0: torch.Tensor   # [n0][S][N_0] bf16: (pos @ Vw_n) @ Wp_0[n], level-0 gemm row bias
+    posV0: torch.Tensor      # [n0][S][D] bf16: pos @ Vw_n, added to ctx by K_l0
     p_const: torch.Tensor | None
     Wp: list      # [n_l, N_l, D] bf16
     bp: list      # [n_l, N_l] fp32
@@ -231,8 +231,7 @@ def pack_rank(fr: FoldedRank, device) -> PackedRank:
     for n, (c0, g) in enumerate(zip(fr.l0_c0, fr.l0_g)):
         Esrc[n, :, :g] = fr.Cb[c0:c0 + g].to(**f32).view(g, h, 2, 32).permute(1, 0, 2, 3)
     Et = tile(Esrc.permute(0, 1, 3, 2, 4).reshape(n0 * h * 2, KE, 32), n0 * h * 2, KE, 32)
-    rowbias0 = torch.einsum("nsd,ndk->nsk", fr.posV.to(**f32), fr.Wp[0].to(**f32))
-    rowbias0 = rowbias0.to(torch.bfloat16).contiguous()
+    posV0 = fr.posV.to(**f32).to(torch.bfloat16).contiguous()
     WUt = bU = posU = p_const = None
     if fr.attn_l0:
         wu = torch.zeros(C, HP, pp, **f32)
@@ -257,7 +256,7 @@ def pack_rank(fr: FoldedRank, device) -> PackedRank:
     return PackedRank(
         n0=n0, C=C, C_pad=C_pad, KE=KE, HP=HP, attn_l0=fr.attn_l0,
         l0_c0=torch.tensor(fr.l0_c0, **i32), l0_g=torch.tensor(fr.l0_g, **i32),
-        l0_g_list=list(fr.l0_g), WUt=WUt, bU=bU, posU=posU, Mt=Mt, Et=Et, rowbias0=rowbias0,
+        l0_g_list=list(fr.l0_g), WUt=WUt, bU=bU, posU=posU, Mt=Mt, Et=Et, posV0=posV0,
         p_const=p_const, Wp=Wp, bp=bp, N=N, comb_first=comb_first, comb_g=comb_g,
         comb_mix=comb_mix,
         Wf=fr.Wf.to(**f32).t().to(torch.bfloat16).contiguous(),

@@ -366,6 +366,7 @@ class DchagFrontEnd(torch.nn.Module):
         _lib.call("dchag_l0_node", _lib.ptr(img), isb, isc, B, m.image_h, m.image_w, p, h, d,
                   pk.n0, _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g), _lib.ptr(poff), prow,
                   _lib.ptr(pbuf), _lib.ptr(pinv), _lib.ptr(pk.Mt), pk.C_pad, _lib.ptr(pk.Et), pk.KE,
+                  _lib.ptr(pk.posV0),
                   _lib.ptr(ctx), st)
 
         depth = len(pk.levels)
@@ -382,8 +383,7 @@ class DchagFrontEnd(torch.nn.Module):
             else:
                 V = torch.empty(n_l, R, d, **bf16)
                 L = torch.empty(n_l, R, h, **f32) if logits else None
-            # level 0: the positional term (pos @ wv_n) @ Wp enters as a per-row bias
-            rb = pk.rowbias0 if li == 0 else None
+            rb = None  # level 0's positional term is added by K_l0 (posV0)
             _lib.call("dchag_gemm_bf16", _lib.ptr(ctx), n_l, 1, R, d, R * d, 0, d,
                       _lib.ptr(pk.Wp[li]), N, N * d, d, _lib.ptr(pk.bp[li]), N, _lib.ptr(rb),
                       s * N, N, s, _lib.ptr(V), 0, R * d, 0, d, _lib.ptr(L), R * h, 0, h, st)

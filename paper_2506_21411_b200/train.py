@@ -124,14 +124,13 @@ class DchagTrainer:
             poff_t = (pk.l0_c0.to(torch.int64) * h).contiguous()
             pbuf, prow, pinv = pk.p_const, 0, None
         ctx0 = torch.empty(pk.n0, R, d, device=dev, dtype=torch.bfloat16)
+        # positional term of the level-0 context, pos @ Vw_n (x sum(mix) for linear nodes),
+        # added by K_l0 in its drain
+        posV0 = self._level0_posV().to(torch.bfloat16).contiguous()
         _lib.call("dchag_l0_node", _lib.ptr(img), img.stride(0), img.stride(1), B, m.image_h,
                   m.image_w, m.patch, h, d, pk.n0, _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g),
                   _lib.ptr(poff_t), prow, _lib.ptr(pbuf), _lib.ptr(pinv), _lib.ptr(pk.Mt), pk.C_pad,
-                  _lib.ptr(pk.Et), pk.KE, _lib.ptr(ctx0), st)
-        # positional term of the level-0 context: pos @ Vw_n (x (sum mix) for linear nodes)
-        posV = self._level0_posV()
-        srow = torch.arange(R, device=dev) % s
-        ctx0 = (ctx0.float() + posV[:, srow]).to(torch.bfloat16)       # [n0, R, D]
+                  _lib.ptr(pk.Et), pk.KE, _lib.ptr(posV0), _lib.ptr(ctx0), st)
         saved["ctx"] = [ctx0]
         y = torch.empty(len(levels[0]), R, d, device=dev, dtype=torch.bfloat16)
         for gi in range(len(levels[0])):
