@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--h2d-chunks", type=int, default=4,
+    ap.add_argument("--h2d-chunks", type=int, default=8,
                     help="batch chunks of the e2e host-input pipeline (copy/compute overlap)")
     ap.add_argument("--cpu-tokens", type=int, default=None,
                     help="tokens per CPU sample (default: 1/8 of an image)")

@@ -16,9 +16,11 @@ constexpr int COMB_MAXH = 32;
 
 // One warp per (node, row).  Phase 1: lanes < H own one head each and compute the
 // softmax over the g children from coalesced logit rows; weights go to shared memory.
-// Phase 2: every lane owns 8-column (16-byte) chunks and streams the g child rows,
-// unrolled so each lane keeps several independent 16-byte loads in flight.
-__global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
+// Phase 2: every lane owns CH 8-column (16-byte) chunks (D = 256 CH) and streams the g
+// child rows two at a time, so each lane keeps 2 CH independent 16-byte loads in flight.
+// CH is a template parameter so the register arrays are exactly sized (occupancy).
+template <int CH>
+__global__ void __launch_bounds__(256, CH >= 8 ? 1 : (CH >= 4 ? 2 : 4)) combine_kernel(CombineArgs a) {
   __shared__ float sp[8][COMB_PTAB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long item = (long long)blockIdx.x * 8 + warp;
@@ -47,57 +49,75 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
     for (int j = 0; j < g; ++j) p[j * H + lane] *= inv;
   }
   __syncwarp();
-  const int nchunk = a.D / 8;  // <= 256 (D <= 2048)
-  float acc[8][8];
+  float acc[CH][8];
 #pragma unroll
-  for (int q = 0; q < 8; ++q)
+  for (int q = 0; q < CH; ++q)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[q][e] = 0.f;
   const __nv_bfloat16* vbase =
       a.V + (long long)first * a.sVj + (long long)rb * a.sVb + (long long)rs * a.D;
-  const int per_lane = (nchunk + 31) / 32;
-  for (int j = 0; j < g; ++j) {
-    const __nv_bfloat16* vrow = vbase + (long long)j * a.sVj;
-    uint4 v[8];
+  const int nchunk = a.D / 8;  // chunks of this row; lanes past it idle (D < 256)
+  int hq[CH];  // head of each of this lane's chunks
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (q < per_lane && lane + 32 * q < nchunk)
-        v[q] = __ldg(reinterpret_cast<const uint4*>(vrow) + lane + 32 * q);
+  for (int q = 0; q < CH; ++q) hq[q] = ((lane + 32 * q) * 8) / dh;
+  const bool act = lane < nchunk;  // D >= 256 is a multiple of 256: all lanes active
+  auto accumulate = [&](const uint4 (&v)[CH], int j) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (q < per_lane && lane + 32 * q < nchunk) {
-        const int ch = lane + 32 * q;
-        const float pj = a.mix ? p[j] : p[j * H + (ch * 8) / dh];
-        const uint32_t vv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+    for (int q = 0; q < CH; ++q) {
+      const float pj = a.mix ? p[j] : p[j * H + hq[q]];
+      const uint32_t vv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          acc[q][2 * e] += pj * bf16lo(vv[e]);
-          acc[q][2 * e + 1] += pj * bf16hi(vv[e]);
-        }
+      for (int e = 0; e < 4; ++e) {
+        acc[q][2 * e] += pj * bf16lo(vv[e]);
+        acc[q][2 * e + 1] += pj * bf16hi(vv[e]);
       }
     }
+  };
+  int j = 0;
+  for (; j + 2 <= g; j += 2) {
+    const uint4* r0 = reinterpret_cast<const uint4*>(vbase + (long long)j * a.sVj);
+    const uint4* r1 = reinterpret_cast<const uint4*>(vbase + (long long)(j + 1) * a.sVj);
+    uint4 v0[CH], v1[CH];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) v0[q] = act ? __ldg(r0 + lane + 32 * q) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int q = 0; q < CH; ++q) v1[q] = act ? __ldg(r1 + lane + 32 * q) : make_uint4(0, 0, 0, 0);
+    accumulate(v0, j);
+    accumulate(v1, j + 1);
+  }
+  if (j < g) {
+    const uint4* r0 = reinterpret_cast<const uint4*>(vbase + (long long)j * a.sVj);
+    uint4 v0[CH];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) v0[q] = act ? __ldg(r0 + lane + 32 * q) : make_uint4(0, 0, 0, 0);
+    accumulate(v0, j);
   }
   __nv_bfloat16* orow = a.ctx + ((long long)n * a.R + r) * a.D;
+  if (!act) return;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    if (q < per_lane && lane + 32 * q < nchunk) {
-      uint4 o;
-      o.x = pack_bf16(acc[q][0], acc[q][1]);
-      o.y = pack_bf16(acc[q][2], acc[q][3]);
-      o.z = pack_bf16(acc[q][4], acc[q][5]);
-      o.w = pack_bf16(acc[q][6], acc[q][7]);
-      reinterpret_cast<uint4*>(orow)[lane + 32 * q] = o;
-    }
+  for (int q = 0; q < CH; ++q) {
+    uint4 o;
+    o.x = pack_bf16(acc[q][0], acc[q][1]);
+    o.y = pack_bf16(acc[q][2], acc[q][3]);
+    o.z = pack_bf16(acc[q][4], acc[q][5]);
+    o.w = pack_bf16(acc[q][6], acc[q][7]);
+    reinterpret_cast<uint4*>(orow)[lane + 32 * q] = o;
   }
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
-  if (a.D % 8 || a.D > 2048 || (a.D / a.H) % 8 || a.H > COMB_MAXH ||
+  if ((a.D > 256 ? a.D % 256 : a.D % 8) || a.D > 2048 || (a.D / a.H) % 8 || a.H > COMB_MAXH ||
       a.max_g * (a.mix ? 1 : a.H) > COMB_PTAB)
     return cudaErrorInvalidValue;
   const long long items = (long long)a.n_nodes * a.R;
   const int grid = (int)((items + 7) / 8);
-  combine_kernel<<<grid, 256, 0, st>>>(a);
+  switch ((a.D + 255) / 256) {
+    case 1: combine_kernel<1><<<grid, 256, 0, st>>>(a); break;
+    case 2: combine_kernel<2><<<grid, 256, 0, st>>>(a); break;
+    case 4: combine_kernel<4><<<grid, 256, 0, st>>>(a); break;
+    case 8: combine_kernel<8><<<grid, 256, 0, st>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
