@@ -190,7 +190,7 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
   if ((reinterpret_cast<uintptr_t>(img) | (uintptr_t)(img_sb * 2) | (uintptr_t)(img_sc * 2) |
        (uintptr_t)(W * 2)) % 16)
     return fail(DCHAG_ERR_SHAPE, "l0_logits: image base/strides must be 16-byte aligned");
-  return cuda_status(launch_l0_logits(a, S(stream)), "l0_logits");
+  return cuda_status(launch_l0_logits(a, num_sms_cached(), S(stream)), "l0_logits");
 }
 
 int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,

@@ -47,7 +47,7 @@ struct L0LogitArgs {
                               // NH = 4 if H % 4 == 0 else 2 (head group of one K_l0 CTA);
                               // a 128-row tile's slice of (hg, c) is one contiguous 1 KB run
 };
-cudaError_t launch_l0_logits(const L0LogitArgs& a, cudaStream_t st);
+cudaError_t launch_l0_logits(const L0LogitArgs& a, int num_sms, cudaStream_t st);
 
 // Level-0 node: ctx[n][r][h*dh:(h+1)*dh] = sum_c p[r,c,h] * (patch_c[r] @ M_c[:,h]) + ext
 struct L0NodeArgs {

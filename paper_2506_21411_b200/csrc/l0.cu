@@ -31,76 +31,71 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// One CTA = (node n, block of RB rows), 8 warps: warp w takes the m16 row tile w % (RB/16)
-// and the channels c = w / (RB/16) mod CS (CS = 128 / RB channel phases). The block's rows of
-// every channel of the node are one contiguous image run each (RB % (W/P) == 0), so the node
-// slice lands in shared memory with g 1-D bulk copies (images are read from HBM once); the
-// logit weights are staged with a 16-byte XOR swizzle (conflict-free ldmatrix rows). Pass 1:
-// per-warp online max/sum over its channels, merged through shared memory; pass 2: p.
-// Fragments come from ldmatrix (P = 8: a 16-wide K step is two whole patch pixel rows) or
-// 32-bit shared loads (P = 4), all on precomputed 32-bit shared addresses.
+// Persistent CTAs over work items (node n, block of RB rows); each CTA takes a contiguous
+// range of items (so the node, and the staged logit weights, rarely change) and
+// double-buffers the image slices: while the 8 warps compute item k, the bulk copies of item
+// k+1 are in flight. Warp w takes the m16 row tile w % MT and the channels
+// c = w / MT mod CS (CS = 8 / MT). An item's rows of every channel of the node are one
+// contiguous image run (RB % (W/P) == 0): g 1-D bulk copies per item, images read from HBM
+// once. Logit weights (16-byte XOR swizzle, conflict-free ldmatrix) and the bias rows live
+// in shared memory. Pass 1: max over the node's channels (merged across channel phases
+// through shared memory); pass 2: e = 2^(t - max), sums; pass 3 (no pinv): p = e / sum.
 template <int NT, int P, int MT>  // NT = HP / 8 head tiles, MT = RB / 16 row tiles
-__global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a) {
+__global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items_per_cta, int nbuf) {
   constexpr int RB = MT * 16, CS = 8 / MT;
   extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t landed;
+  __shared__ __align__(8) uint64_t landed[2];
   constexpr int PP = P * P;
   constexpr int KS = PP / 16;
   constexpr int CPR = PP * 2 / 16;  // 16-byte chunks per weight row
   const uint32_t sbase = (smem_u32(smem_raw) + 127) & ~127u;
   const int R = a.B * a.S;
-  const int blocks_per_node = R / RB;
-  const int n = blockIdx.x / blocks_per_node;
-  const int rblk = blockIdx.x - n * blocks_per_node;
+  const int bpn = R / RB;            // items per node
+  const int total = a.n_nodes * bpn;
+  const int it0 = blockIdx.x * items_per_cta;
+  const int it1 = min(total, it0 + items_per_cta);
+  if (it0 >= it1) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int mt = warp % MT, cph = warp / MT;
-  const int c0 = __ldg(a.node_c0 + n), g = __ldg(a.node_g + n);
-  const long long poff = __ldg(a.node_poff + n);
-  const int r0 = rblk * RB;
-  const uint32_t chunk = (uint32_t)RB * PP * 2;            // bytes of one channel's image block
-  const uint32_t sW = sbase + (uint32_t)a.gmax * chunk;    // [g*HP][PP] swizzled weights
-  const uint32_t wrow = (uint32_t)a.HP * PP * 2;           // weight bytes per channel
-  float2* stats = reinterpret_cast<float2*>(smem_raw + (sW - smem_u32(smem_raw)) +
-                                            (size_t)a.gmax * wrow);
-  if (threadIdx.x == 0) {
-    mbar_init(&landed, 1);
-    fence_barrier_init();
+  const uint32_t chunk = (uint32_t)RB * PP * 2;             // bytes of one channel's block
+  const uint32_t ibuf = (uint32_t)a.gmax * chunk;           // one item's image buffer
+  const uint32_t sW = sbase + nbuf * ibuf;                  // [g*HP][PP] swizzled weights
+  const uint32_t wrow = (uint32_t)a.HP * PP * 2;            // weight bytes per channel
+  const uint32_t sU = sW + (uint32_t)a.gmax * wrow;         // [g][HP] fp32 bias rows
+  float* stat = reinterpret_cast<float*>(smem_raw + (sU - smem_u32(smem_raw)) +
+                                         (size_t)a.gmax * a.HP * 4);  // [CS][MT][NT][4][32]
+  const int lwp = __ffs(a.wp) - 1;   // W / P divides 128: a power of two
+  auto issue = [&](int it, int buf) {  // thread 0: bulk copies of item it into buffer buf
+    const int n = it / bpn, r0 = (it - n * bpn) * RB;
+    const int c0 = __ldg(a.node_c0 + n), g = __ldg(a.node_g + n);
     const int b = r0 / a.S, s0 = r0 - b * a.S;
-    const __nv_bfloat16* src0 = a.img + b * a.img_sb + (long long)(s0 / a.wp) * P * a.W;
-    mbar_expect_tx(&landed, chunk * g);
-    for (int c = 0; c < g; ++c) {
-      const uint32_t dst = sbase + c * chunk;
+    const __nv_bfloat16* src0 = a.img + b * a.img_sb + (long long)(s0 >> lwp) * P * a.W;
+    mbar_expect_tx(&landed[buf], chunk * g);
+    for (int c = 0; c < g; ++c)
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-          ::"r"(dst), "l"(src0 + (long long)(c0 + c) * a.img_sc), "r"(chunk),
-          "r"(smem_u32(&landed))
+          ::"r"(sbase + buf * ibuf + c * chunk), "l"(src0 + (long long)(c0 + c) * a.img_sc),
+          "r"(chunk), "r"(smem_u32(&landed[buf]))
           : "memory");
-    }
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&landed[0], 1);
+    mbar_init(&landed[1], 1);
+    fence_barrier_init();
+    issue(it0, 0);
   }
   auto wswz = [&](int row, int ch) -> uint32_t {  // byte offset of chunk ch of weight row
     const int f = CPR >= 8 ? (row & 7) : ((row / (8 / CPR)) & (CPR - 1));
     return (uint32_t)(row * (PP * 2) + ((ch ^ f) << 4));
   };
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(a.WUt + (long long)c0 * a.HP * PP);
-    const int nchunks = g * a.HP * CPR;
-    for (int i = threadIdx.x; i < nchunks; i += 256) sts128(sW + wswz(i / CPR, i % CPR), __ldg(src + i));
-  }
-
-  int rows[2], srow[2];
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    rows[q] = r0 + mt * 16 + gid + 8 * q;
-    srow[q] = rows[q] % a.S;
-  }
-  // per-thread shared byte offsets inside a channel block / weight slice
+  // per-thread shared byte offsets inside a channel block / weight slice (item independent)
   uint32_t aoff[KS], boff[KS][NT / 2 > 0 ? NT / 2 : 1];
   uint32_t aoff4[4];
   if (P == 8) {
     const int mat = lane >> 3, rr = lane & 7;
     const int rl = mt * 16 + (mat & 1) * 8 + rr;
-    const int i = rl / a.wp, j = rl - i * a.wp;
+    const int i = rl >> lwp, j = rl & (a.wp - 1);
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks)
       aoff[ks] = (uint32_t)(((i * P + 2 * ks + (mat >> 1)) * a.W + j * P) * 2);
@@ -108,7 +103,7 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {  // a0..a3: rows gid / gid+8, k = 2tig (+8)
       const int rl = mt * 16 + gid + 8 * (e & 1);
-      const int i = rl / a.wp, j = rl - i * a.wp;
+      const int i = rl >> lwp, j = rl & (a.wp - 1);
       const int k = 2 * tig + 8 * (e >> 1);
       aoff4[e] = (uint32_t)(((i * P + k / P) * a.W + j * P + k % P) * 2);
     }
@@ -121,198 +116,234 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a) {
       for (int np = 0; np < (NT + 1) / 2; ++np) {
         // x4: matrices (nt = 2np + mat/2, k half = mat%2); x2 (NT == 1): (nt 0, k half mat)
         const int nt = NT == 1 ? 0 : 2 * np + (mat >> 1);
-        const int kh = NT == 1 ? (mat & 1) : (mat & 1);
-        boff[ks][np] = wswz(nt * 8 + rr, ks * 2 + kh);
+        boff[ks][np] = wswz(nt * 8 + rr, ks * 2 + (mat & 1));
       }
   }
-  float pu[NT][4];
+  constexpr float LOG2E = 1.4426950408889634f;
+  auto sidx = [&](int k, int nt, int e) { return (((k * MT + mt) * NT + nt) * 4 + e) * 32 + lane; };
+  const int nh = (a.H % 4 == 0) ? 4 : 2;
+  const bool unnorm = a.pinv != nullptr;
+  int cur_node = -1;
+  uint32_t ph[2] = {0u, 0u};
+  for (int it = it0, k = 0; it < it1; ++it, ++k) {
+    const int buf = nbuf == 2 ? (k & 1) : 0;
+    const int n = it / bpn, r0 = (it - n * bpn) * RB;
+    const int c0 = __ldg(a.node_c0 + n), g = __ldg(a.node_g + n);
+    const long long poff = __ldg(a.node_poff + n);
+    // item k-1 is finished by every warp (end-of-item barrier): its buffer takes item k+1
+    if (nbuf == 2 && threadIdx.x == 0 && it + 1 < it1) issue(it + 1, buf ^ 1);
+    if (n != cur_node) {  // stage this node's logit weights and bias rows
+      const uint4* src = reinterpret_cast<const uint4*>(a.WUt + (long long)c0 * a.HP * PP);
+      const int nchunks = g * a.HP * CPR;
+      for (int i = threadIdx.x; i < nchunks; i += 256)
+        sts128(sW + wswz(i / CPR, i % CPR), __ldg(src + i));
+      const float* bsrc = a.bU + (long long)c0 * a.HP;
+      for (int i = threadIdx.x; i < g * a.HP; i += 256)
+        reinterpret_cast<float*>(smem_raw + (sU - smem_u32(smem_raw)))[i] = __ldg(bsrc + i);
+      cur_node = n;
+      __syncthreads();
+    }
+    const float* sUf = reinterpret_cast<const float*>(smem_raw + (sU - smem_u32(smem_raw)));
+    int rows[2];
+    float pu[NT][4];
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const float* pr0 = a.posU + ((long long)n * a.S + srow[0]) * a.HP + nt * 8 + 2 * tig;
-    const float* pr1 = a.posU + ((long long)n * a.S + srow[1]) * a.HP + nt * 8 + 2 * tig;
-    pu[nt][0] = pr0[0]; pu[nt][1] = pr0[1];
-    pu[nt][2] = pr1[0]; pu[nt][3] = pr1[1];
-  }
-  __syncthreads();  // barrier init + weights visible
-  mbar_wait(&landed, 0);
-
-  auto logits = [&](int c, float (&L)[NT][4]) {
-    const uint32_t ab = sbase + c * chunk;
-    const uint32_t wb = sW + c * wrow;
+    for (int q = 0; q < 2; ++q) rows[q] = r0 + mt * 16 + gid + 8 * q;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      const float* bu = a.bU + (long long)(c0 + c) * a.HP + nt * 8 + 2 * tig;
-      const float2 bb = __ldg(reinterpret_cast<const float2*>(bu));
-      L[nt][0] = pu[nt][0] + bb.x;
-      L[nt][1] = pu[nt][1] + bb.y;
-      L[nt][2] = pu[nt][2] + bb.x;
-      L[nt][3] = pu[nt][3] + bb.y;
+      const float* pr0 = a.posU + ((long long)n * a.S + rows[0] % a.S) * a.HP + nt * 8 + 2 * tig;
+      const float* pr1 = a.posU + ((long long)n * a.S + rows[1] % a.S) * a.HP + nt * 8 + 2 * tig;
+      const float2 u0 = __ldg(reinterpret_cast<const float2*>(pr0));
+      const float2 u1 = __ldg(reinterpret_cast<const float2*>(pr1));
+      pu[nt][0] = u0.x; pu[nt][1] = u0.y; pu[nt][2] = u1.x; pu[nt][3] = u1.y;
     }
+    mbar_wait(&landed[buf], ph[buf]);
+    ph[buf] ^= 1;
+    const uint32_t ibase = sbase + buf * ibuf;
+    auto logits = [&](int c, float (&L)[NT][4]) {
+      const uint32_t ab = ibase + c * chunk;
+      const uint32_t wb = sW + c * wrow;
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      uint32_t af[4];
-      if (P == 8) {
-        ldsm_x4(ab + aoff[ks], af);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) af[e] = lds32(ab + aoff4[e]);
+      for (int nt = 0; nt < NT; ++nt) {
+        const float2 bb = *reinterpret_cast<const float2*>(sUf + c * a.HP + nt * 8 + 2 * tig);
+        L[nt][0] = pu[nt][0] + bb.x;
+        L[nt][1] = pu[nt][1] + bb.y;
+        L[nt][2] = pu[nt][2] + bb.x;
+        L[nt][3] = pu[nt][3] + bb.y;
       }
-      if (NT == 1) {
-        uint32_t bf[2];
-        ldsm_x2(wb + boff[ks][0], bf);
-        mma_bf16_16816(L[0], af, bf[0], bf[1]);
-      } else {
 #pragma unroll
-        for (int np = 0; np < NT / 2; ++np) {
-          uint32_t bf[4];
-          ldsm_x4(wb + boff[ks][np], bf);
-          mma_bf16_16816(L[2 * np], af, bf[0], bf[1]);
-          mma_bf16_16816(L[2 * np + 1], af, bf[2], bf[3]);
+      for (int ks = 0; ks < KS; ++ks) {
+        uint32_t af[4];
+        if (P == 8) {
+          ldsm_x4(ab + aoff[ks], af);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) af[e] = lds32(ab + aoff4[e]);
+        }
+        if (NT == 1) {
+          uint32_t bf[2];
+          ldsm_x2(wb + boff[ks][0], bf);
+          mma_bf16_16816(L[0], af, bf[0], bf[1]);
+        } else {
+#pragma unroll
+          for (int np = 0; np < NT / 2; ++np) {
+            uint32_t bf[4];
+            ldsm_x4(wb + boff[ks][np], bf);
+            mma_bf16_16816(L[2 * np], af, bf[0], bf[1]);
+            mma_bf16_16816(L[2 * np + 1], af, bf[2], bf[3]);
+          }
         }
       }
-    }
-  };
-
-  // softmax over the node's channels in base 2: t = logit * log2(e)
-  constexpr float LOG2E = 1.4426950408889634f;
-  float* stat = reinterpret_cast<float*>(stats);  // [CS][MT][NT][4][32]
-  auto sidx = [&](int k, int nt, int e) { return (((k * MT + mt) * NT + nt) * 4 + e) * 32 + lane; };
-  // pass 1: max only
-  float mx[NT][4];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) mx[nt][e] = -INFINITY;
-#pragma unroll 2
-  for (int c = cph; c < g; c += CS) {
-    float L[NT][4];
-    logits(c, L);
+    };
+    // pass 1: max only
+    float mx[NT][4];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) mx[nt][e] = fmaxf(mx[nt][e], L[nt][e]);
-  }
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) stat[sidx(cph, nt, e)] = mx[nt][e];
-  __syncthreads();
-  float nmx[NT][4];  // -max * log2(e)
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      float m = stat[sidx(0, nt, e)];
-#pragma unroll
-      for (int k = 1; k < CS; ++k) m = fmaxf(m, stat[sidx(k, nt, e)]);
-      nmx[nt][e] = -m * LOG2E;
-    }
-  __syncthreads();  // stat reused for the sums
-  const int nh = (a.H % 4 == 0) ? 4 : 2;
-  // p / e store offsets (elements, relative to the node's p block) for channel 0
-  int poff_e[NT][2];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int h = nt * 8 + 2 * tig, hg = h / nh, hl = h - hg * nh;
-#pragma unroll
-    for (int q = 0; q < 2; ++q) poff_e[nt][q] = ((hg * g) * R + rows[q]) * nh + hl;
-  }
-  __nv_bfloat16* pn = a.p + poff;
-  const int cstride = R * nh;  // elements between consecutive channels of one head group
-  const bool unnorm = a.pinv != nullptr;
-  // pass 2: e = 2^(t - max), sums; with pinv the unnormalised e is the output
-  float sm_[NT][4];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) sm_[nt][e] = 0.f;
+      for (int e = 0; e < 4; ++e) mx[nt][e] = -INFINITY;
 #pragma unroll 2
-  for (int c = cph; c < g; c += CS) {
-    float L[NT][4];
-    logits(c, L);
+    for (int c = cph; c < g; c += CS) {
+      float L[NT][4];
+      logits(c, L);
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      float ev[4];
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) mx[nt][e] = fmaxf(mx[nt][e], L[nt][e]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) stat[sidx(cph, nt, e)] = mx[nt][e];
+    __syncthreads();
+    float nmx[NT][4];  // -max * log2(e)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        ev[e] = ex2_approx(fmaf(L[nt][e], LOG2E, nmx[nt][e]));
-        sm_[nt][e] += ev[e];
+        float m = stat[sidx(0, nt, e)];
+#pragma unroll
+        for (int kk = 1; kk < CS; ++kk) m = fmaxf(m, stat[sidx(kk, nt, e)]);
+        nmx[nt][e] = -m * LOG2E;
       }
-      if (unnorm && nt * 8 + 2 * tig < a.H) {
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-          *reinterpret_cast<uint32_t*>(pn + poff_e[nt][q] + c * cstride) =
-              pack_bf16(ev[2 * q], ev[2 * q + 1]);
-      }
-    }
-  }
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) stat[sidx(cph, nt, e)] = sm_[nt][e];
-  __syncthreads();
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      float t = stat[sidx(0, nt, e)];
-#pragma unroll
-      for (int k = 1; k < CS; ++k) t += stat[sidx(k, nt, e)];
-      sm_[nt][e] = 1.f / t;
-    }
-  if (unnorm) {
-    if (cph == 0) {
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int h = nt * 8 + 2 * tig;
-        if (h < a.H) {
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-            *reinterpret_cast<float2*>(a.pinv + ((long long)n * R + rows[q]) * a.H + h) =
-                make_float2(sm_[nt][2 * q], sm_[nt][2 * q + 1]);
-        }
-      }
-    }
-    return;
-  }
-  // pass 3 (normalised output): p = e / sum
-#pragma unroll 2
-  for (int c = cph; c < g; c += CS) {
-    float L[NT][4];
-    logits(c, L);
+    __syncthreads();  // stat reused for the sums
+    // p / e store offsets (elements, relative to the node's p block) for channel 0
+    int poff_e[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      if (nt * 8 + 2 * tig < a.H) {
+      const int h = nt * 8 + 2 * tig, hg = h / nh, hl = h - hg * nh;
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const float p0 = ex2_approx(fmaf(L[nt][2 * q], LOG2E, nmx[nt][2 * q])) * sm_[nt][2 * q];
-          const float p1 =
-              ex2_approx(fmaf(L[nt][2 * q + 1], LOG2E, nmx[nt][2 * q + 1])) * sm_[nt][2 * q + 1];
-          *reinterpret_cast<uint32_t*>(pn + poff_e[nt][q] + c * cstride) = pack_bf16(p0, p1);
+      for (int q = 0; q < 2; ++q) poff_e[nt][q] = ((hg * g) * R + rows[q]) * nh + hl;
+    }
+    __nv_bfloat16* pn = a.p + poff;
+    const int cstride = R * nh;  // elements between consecutive channels of one head group
+    // pass 2: e = 2^(t - max), sums; with pinv the unnormalised e is the output
+    float sm_[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sm_[nt][e] = 0.f;
+#pragma unroll 2
+    for (int c = cph; c < g; c += CS) {
+      float L[NT][4];
+      logits(c, L);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        float ev[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          ev[e] = ex2_approx(fmaf(L[nt][e], LOG2E, nmx[nt][e]));
+          sm_[nt][e] += ev[e];
+        }
+        if (unnorm && nt * 8 + 2 * tig < a.H) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            *reinterpret_cast<uint32_t*>(pn + poff_e[nt][q] + c * cstride) =
+                pack_bf16(ev[2 * q], ev[2 * q + 1]);
         }
       }
     }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) stat[sidx(cph, nt, e)] = sm_[nt][e];
+    __syncthreads();
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float t = stat[sidx(0, nt, e)];
+#pragma unroll
+        for (int kk = 1; kk < CS; ++kk) t += stat[sidx(kk, nt, e)];
+        sm_[nt][e] = 1.f / t;
+      }
+    if (unnorm) {
+      if (cph == 0) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int h = nt * 8 + 2 * tig;
+          if (h < a.H) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              *reinterpret_cast<float2*>(a.pinv + ((long long)n * R + rows[q]) * a.H + h) =
+                  make_float2(sm_[nt][2 * q], sm_[nt][2 * q + 1]);
+          }
+        }
+      }
+    } else {
+      // pass 3 (normalised output): p = e / sum
+#pragma unroll 2
+      for (int c = cph; c < g; c += CS) {
+        float L[NT][4];
+        logits(c, L);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          if (nt * 8 + 2 * tig < a.H) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const float p0 =
+                  ex2_approx(fmaf(L[nt][2 * q], LOG2E, nmx[nt][2 * q])) * sm_[nt][2 * q];
+              const float p1 =
+                  ex2_approx(fmaf(L[nt][2 * q + 1], LOG2E, nmx[nt][2 * q + 1])) * sm_[nt][2 * q + 1];
+              *reinterpret_cast<uint32_t*>(pn + poff_e[nt][q] + c * cstride) = pack_bf16(p0, p1);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // item done: its image buffer and the stat area may be reused
+    if (nbuf == 1 && threadIdx.x == 0 && it + 1 < it1) issue(it + 1, 0);
   }
 }
 
-cudaError_t launch_l0_logits(const L0LogitArgs& a, cudaStream_t st) {
+cudaError_t launch_l0_logits(const L0LogitArgs& a, int num_sms, cudaStream_t st) {
   const int R = a.B * a.S;
   const int PP = a.P * a.P;
-  // rows per CTA: a multiple of the patch-row width (one contiguous run per channel), as
-  // large as 64 while the node slice stays <= 64 KB (two CTAs per SM overlap copies)
-  int RB = 0;
+  const int NTv = a.HP / 8;
+  // rows per item: a multiple of the patch-row width (one contiguous run per channel); two
+  // CTAs per SM, each holding two image buffers, the node's weights and bias rows
+  auto smem_for = [&](int rb, int nbuf) {
+    const int cs = 8 / (rb / 16);
+    return (long long)nbuf * a.gmax * rb * PP * 2 + (long long)a.gmax * a.HP * PP * 2 +
+           (long long)a.gmax * a.HP * 4 + (long long)cs * (rb / 16) * NTv * 4 * 32 * 4 + 128;
+  };
+  // item rows: a multiple of the patch-row width (one contiguous run per channel), the
+  // largest <= 32 that keeps two CTAs per SM; the image slice is double-buffered only when
+  // that still fits two CTAs (measured: two single-buffered CTAs beat one double-buffered)
+  int RB = 0, nbuf = 1;
   for (int rb = 128; rb >= 16; rb >>= 1) {
     if (rb % a.wp || R % rb) continue;
     RB = rb;  // smallest valid so far
-    if (rb <= 64 && (long long)a.gmax * rb * PP * 2 <= 64 * 1024) break;
+    if (rb <= 32 && smem_for(rb, 1) <= 113 * 1024) break;
   }
   if (RB == 0) return cudaErrorInvalidValue;
-  const int NTv = a.HP / 8;
-  const long long smem = (long long)a.gmax * RB * PP * 2 + (long long)a.gmax * a.HP * PP * 2 +
-                         8LL * NTv * 4 * 32 * 8 + 128;
+  if (const char* f = getenv("DCHAG_P0_RB")) {  // experiment override
+    const int rb = atoi(f);
+    if (rb >= 16 && rb % a.wp == 0 && R % rb == 0) RB = rb;
+  }
+  if (smem_for(RB, 2) <= 113 * 1024) nbuf = 2;
+  if (const char* f = getenv("DCHAG_P0_NBUF")) nbuf = atoi(f) == 2 ? 2 : 1;
+  const long long smem = smem_for(RB, nbuf);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  const int grid = a.n_nodes * (R / RB);
-  void (*k)(L0LogitArgs) = nullptr;
+  void (*k)(L0LogitArgs, int, int) = nullptr;
 #define L0L_PICK(NTv_, P_)                                                                    \
   k = RB == 16 ? l0_logits_kernel<NTv_, P_, 1> : RB == 32 ? l0_logits_kernel<NTv_, P_, 2>     \
     : RB == 64 ? l0_logits_kernel<NTv_, P_, 4> : l0_logits_kernel<NTv_, P_, 8>;
@@ -325,7 +356,11 @@ cudaError_t launch_l0_logits(const L0LogitArgs& a, cudaStream_t st) {
   if (!k) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<grid, 256, (size_t)smem, st>>>(a);
+  const int total = a.n_nodes * (R / RB);
+  const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+  const int ctas = min(total, per_sm * num_sms);
+  const int per_cta = (total + ctas - 1) / ctas;
+  k<<<(total + per_cta - 1) / per_cta, 256, (size_t)smem, st>>>(a, per_cta, nbuf);
   return cudaGetLastError();
 }
 
