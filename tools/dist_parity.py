@@ -56,16 +56,15 @@ def main():
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import torch_reference as TRF
     from paper_2506_21411_b200.train import DchagTrainer
-    meta = dict(channels=13, image_h=64, image_w=64, patch=8, embed=256, heads=4, max_group=2)
-    specs = O.frontend_param_specs(13, 64, 64, 8, 256, tp, 2)
+    specs = O.frontend_param_specs(13, 64, 128, 8, 256, tp, 2)
     w = O.random_params(specs, seed=9, std=0.05, bias_std=0.02)
     w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
     rng = np.random.default_rng(6)
-    img = torch.from_numpy(rng.standard_normal((2, 13, 64, 64)).astype(np.float32)).to(torch.bfloat16)
-    probe = rng.standard_normal((2, 1, 64, 256))
+    img = torch.from_numpy(rng.standard_normal((2, 13, 64, 128)).astype(np.float32)).to(torch.bfloat16)
+    probe = rng.standard_normal((2, 1, 128, 256))
     img64 = img.float().numpy().astype(np.float64)
     _, g_ref = TRF.grads(img64, w, probe, patch=8, heads=4, tp=tp, max_group=2)
-    fe = DchagFrontEnd(13, 64, 64, 8, 256, 4, max_group=2, tp=tp, rank=rank,
+    fe = DchagFrontEnd(13, 64, 128, 8, 256, 4, max_group=2, tp=tp, rank=rank,
                        out_dtype=torch.float32)
     fe.load_weights(w)
     trn = DchagTrainer(fe)
