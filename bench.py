@@ -35,6 +35,13 @@ WORKLOADS = {
     "train": dict(channels=500, image_h=128, image_w=128, patch=8, embed=2048, heads=32,
                   depth=3, batch=32, train=True),
 }
+# scaling sweep: C 64..1024 x D 1024 (16 heads) / 4096 (32 heads,
+# dh = 128), 128x128 P8, B 32, max_group 16 with the depth derived per slab
+for _c in (64, 128, 256, 512, 1024):
+    for _d, _h in ((1024, 16), (4096, 32)):
+        WORKLOADS[f"sweep_c{_c}_d{_d}"] = dict(channels=_c, image_h=128, image_w=128, patch=8,
+                                               embed=_d, heads=_h, depth=None, max_group=16,
+                                               batch=32)
 METRIC = "D-CHAG tokenize+aggregate images/sec"
 
 
@@ -436,9 +443,13 @@ def main():
     tp = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if args.impl == "reference":
         tp = args.gpus
-    from paper_2506_21411_b200.config import channel_slabs, max_group_for_depth
-    max_group = max_group_for_depth([n for _, n in channel_slabs(wl["channels"], tp)],
-                                    wl["depth"])
+    from paper_2506_21411_b200.config import build_tree_spec, channel_slabs, max_group_for_depth
+    slabs = [n for _, n in channel_slabs(wl["channels"], tp)]
+    if wl.get("max_group"):
+        max_group = wl["max_group"]
+        wl = dict(wl, depth=max(build_tree_spec(n, max_group).depth for n in slabs))
+    else:
+        max_group = max_group_for_depth(slabs, wl["depth"])
     if args.impl == "reference":
         reference_arm(args, wl, tp, max_group)
     else:

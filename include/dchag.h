@@ -51,12 +51,13 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
  * WUt bf16 [C][HP][P*P], bU fp32 [C][HP], posU fp32 [n_nodes][S][HP]; HP = H rounded up
  * to a multiple of 8.  Output p bf16, head-group then channel major (a 128-row tile's
  * slice for one (head group, channel) is contiguous, so K_l0 stages it with one bulk copy):
- * p[poff[n] + ((hg*g + c)*R + r)*NH + h%NH], hg = h/NH, NH = 4 if H%4==0 else 2.
+ * p[poff[n] + ((hg*g + c)*R + r)*NH + h%NH], hg = h/NH, NH = nh = dchag_l0_node's heads per
+ * unit: 2 if the head dim is 128, else 4 if H%4==0, else 2.
  * pinv (optional, fp32 [n_nodes][R][H]): when given, p holds the unnormalised
  * e = exp(logit - max_c logit) and pinv = 1 / sum_c e; dchag_l0_node then applies pinv to
  * its accumulator (one exp per logit instead of three).  NULL: p is the normalised softmax. */
 int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
-                    int P, int H, int HP, int n_nodes, int gmax, const int* node_c0,
+                    int P, int H, int HP, int nh, int n_nodes, int gmax, const int* node_c0,
                     const int* node_g,
                     const long long* node_poff, const void* WUt, const float* bU,
                     const float* posU, void* p, float* pinv, void* stream);
@@ -67,7 +68,7 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
  * Mt bf16 [H][2][32*C_pad*P*P] and Et bf16 [n_nodes][H][2][32*KE] are pre-tiled canonical
  * UMMA blocks (dchag_tile_weights, N = 32 halves; K runs over channel-major c*P*P + k); p_row_mode = 1 reads the dchag_l0_logits layout, 0 a constant
  * table p[poff + c*H + h]
- * (linear-mix nodes).  Requires head dim 64, H % 4 == 0, S % 128 == 0, 128 % (W/P) == 0,
+ * (linear-mix nodes).  Requires head dim 64 or 128, S % 128 == 0, 128 % (W/P) == 0,
  * P in {4, 8}.  pinv (optional, the dchag_l0_logits output): ctx row r, head h is scaled by
  * pinv[n][r][h].  posV (optional, bf16 [n_nodes][S][D]): the node's positional term
  * pos[s] @ wv_n (x sum(mix) for linear nodes), added to ctx row r = (b, s). */

@@ -23,7 +23,7 @@ SIGNATURES = {
                         c_int, c_vp, c_ll, c_vp, c_ll, c_ll, c_int, c_vp, c_int, c_ll, c_ll,
                         c_ll, c_vp, c_ll, c_ll, c_ll, c_vp],
     "dchag_l0_logits": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
-                        c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
+                        c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "dchag_l0_node": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
                       c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp],
     "dchag_combine": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_vp, c_ll,

@@ -170,17 +170,19 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
 }
 
 int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
-                    int P, int H, int HP, int n_nodes, int gmax, const int* node_c0,
+                    int P, int H, int HP, int nh, int n_nodes, int gmax, const int* node_c0,
                     const int* node_g,
                     const long long* node_poff, const void* WUt, const float* bU,
                     const float* posU, void* p, float* pinv, void* stream) {
-  if (Himg % P || W % P || HP % 8 || HP < H || H % 2 || (P * P) % 16)
+  if (Himg % P || W % P || HP % 8 || HP < H || H % 2 || (P * P) % 16 || (nh != 2 && nh != 4) ||
+      H % nh)
     return fail(DCHAG_ERR_SHAPE, "l0_logits: bad shape");
   L0LogitArgs a;
   a.img = reinterpret_cast<const __nv_bfloat16*>(img);
   a.img_sb = img_sb; a.img_sc = img_sc;
   a.B = B; a.S = (Himg / P) * (W / P); a.W = W; a.P = P; a.wp = W / P; a.H = H; a.HP = HP;
   a.n_nodes = n_nodes; a.gmax = gmax;
+  a.nh = nh;
   a.node_c0 = node_c0; a.node_g = node_g; a.node_poff = node_poff;
   a.WUt = reinterpret_cast<const __nv_bfloat16*>(WUt);
   a.bU = bU; a.posU = posU;
@@ -204,6 +206,7 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
   a.img_sb = img_sb; a.img_sc = img_sc;
   a.B = B; a.S = (Himg / P) * (W / P); a.W = W; a.P = P; a.wp = W / P; a.H = H; a.D = D;
   a.n_nodes = n_nodes; a.node_c0 = node_c0; a.node_g = node_g; a.node_poff = node_poff;
+  a.nh = (H > 0 && D / H == 128) ? 2 : (H % 4 == 0 ? 4 : 2);
   a.p_row_mode = p_row_mode;
   a.p = reinterpret_cast<const __nv_bfloat16*>(p);
   a.pinv = pinv;

@@ -35,6 +35,7 @@ struct L0LogitArgs {
   long long img_sb, img_sc;
   int B, S, W, P, wp, H, HP;  // H heads, HP = H padded to a multiple of 8
   int n_nodes, gmax;          // gmax >= every node_g (host-known)
+  int nh;                     // heads per K_l0 unit: 2 if dh == 128, else 4 if H % 4 == 0, else 2
   const int* node_c0;         // first slab channel of node n
   const int* node_g;          // channel count of node n
   const long long* node_poff; // element offset of node n in p
@@ -54,6 +55,7 @@ struct L0NodeArgs {
   const __nv_bfloat16* img;
   long long img_sb, img_sc;
   int B, S, W, P, wp, H, D;
+  int nh;                      // heads per unit (NH * dh <= 256), matches L0LogitArgs::nh
   int n_nodes;
   const int* node_c0;
   const int* node_g;
@@ -61,11 +63,11 @@ struct L0NodeArgs {
   int p_row_mode;              // 1: K_p0 layout (see L0LogitArgs); 0: constant p[poff + c*H + h]
   const __nv_bfloat16* p;
   const float* pinv;           // optional [n_nodes][R][H] row/head scale of ctx (K_p0 output)
-  const __nv_bfloat16* Mt;     // [H][2][C_pad*PP/8][4][8][8]: per head, the two 32-column
+  const __nv_bfloat16* Mt;     // [H][2][C_pad*PP/8][dh/16][8][8]: per head, the two dh/2-column
                                // halves of M_c (one per CTA of a pair) as canonical no-swizzle
                                // K-major core-matrix blocks, channels consecutive along K
   int C_pad;
-  const __nv_bfloat16* Et;     // [n_nodes][H][2][KE/8][4][8][8] ext (bias) blocks, same split
+  const __nv_bfloat16* Et;     // [n_nodes][H][2][KE/8][dh/16][8][8] ext (bias) blocks, same split
   int KE;
   __nv_bfloat16* ctx;          // [n_nodes][R][D]
   int has_pos;                 // 1: ctx += posV[n][s] (tensor map tm_pos over [n_nodes*S][D])

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
   }
   constexpr float LOG2E = 1.4426950408889634f;
   auto sidx = [&](int k, int nt, int e) { return (((k * MT + mt) * NT + nt) * 4 + e) * 32 + lane; };
-  const int nh = (a.H % 4 == 0) ? 4 : 2;
+  const int nh = a.nh;  // heads per K_l0 unit (the p layout's head-group width)
   const bool unnorm = a.pinv != nullptr;
   int cur_node = -1;
   uint32_t ph[2] = {0u, 0u};
@@ -365,17 +365,15 @@ cudaError_t launch_l0_logits(const L0LogitArgs& a, int num_sms, cudaStream_t st)
 }
 
 // =====================================================================  K_l0
-constexpr int L0_DH = 64;                          // head dim (MMA N)
 constexpr int L0_STAGES = 4;
 constexpr int L0_IMG_BYTES = 16384;                // 128 rows x 64 K bf16 (or ext: 16 ch of p)
 constexpr int L0_P_BYTES = 4096;                   // p of the stage: CG ch x 128 rows x NH bf16
-constexpr int L0_BH_BYTES = 32 * 64 * 2;           // one head's B half: 32 N x 64 K bf16
-constexpr int L0_B_BYTES = 4 * L0_BH_BYTES;        // up to 4 heads
+constexpr int L0_B_BYTES = 128 * 64 * 2;          // B halves of a head group: 128 N x 64 K bf16
 constexpr int L0_STAGE_BYTES = L0_IMG_BYTES + L0_P_BYTES + L0_B_BYTES;
 constexpr int L0_OUT_BYTES = 4 * 128 * 128;        // ctx tile staging: 4 heads x 128 rows x 128 B
 constexpr int L0_SMEM = L0_STAGES * L0_STAGE_BYTES + L0_OUT_BYTES + 1024 + 256;
 constexpr int L0_THREADS = 608;                    // producer, image gate, MMA gate, 16 builders
-constexpr uint32_t L0_ACC_COLS = 4 * L0_DH;        // accumulator region (NH * 64 used)
+constexpr uint32_t L0_ACC_COLS = 256;              // accumulator: NH heads x DH <= 256 columns
 constexpr uint32_t L0_SLOT_COLS = 4 * 32;          // A slot: 64 bf16 K per head = 32 columns
 
 #define L0_TRACE(ev, idx)                                                                   \
@@ -467,11 +465,14 @@ DEV void tma_store_2d(const CUtensorMap* m, uint32_t src, int c0, int c1) {
 //               heads: A = p[r,c,h] * patch_c[r] -> tcgen05.st -> READY(q). At the end of a
 //               unit they drain the accumulator (x 1/sum_c e) into a 128B-swizzled smem tile
 //               that TMA tensor stores write to ctx in the background of the next unit.
-template <int PP, int L0_NH, bool ROWP>
+template <int PP, int L0_NH, int L0_DH, bool ROWP>
 __global__ void __launch_bounds__(L0_THREADS, 1)
     l0_node_kernel(L0NodeArgs a, const __grid_constant__ CUtensorMap tm_ctx,
                    const __grid_constant__ CUtensorMap tm_pos) {
   constexpr int CG = 64 / PP;        // channels per main stage (K = 64 per head per stage)
+  constexpr int L0_BH_BYTES = L0_DH * 64;  // one head's B half: DH/2 N x 64 K bf16
+  constexpr uint32_t BLBO = L0_DH * 8;     // bytes between K-adjacent core matrices of a half
+  static_assert(L0_NH * L0_DH <= 256, "head group exceeds the accumulator");
   constexpr int P = PP == 64 ? 8 : 4;
   constexpr int NBAR = 288;          // image gate warp + one group's 8 builder warps
   constexpr int PROW = 128 * L0_NH * 2;  // bytes of one channel's p slice for the tile
@@ -566,26 +567,26 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
                         128 * PP * 2, &full[stage]);
               if (rowp) bulk_load(sP + cc * PROW, pslice(c), PROW, &full[stage]);
             }
-            // B halves: Mt [H][2][C_pad*PP/8][4][8][8]; this stage's 64 K rows are contiguous
+            // B halves: Mt [H][2][C_pad*PP/8][DH/16][8][8]; the stage's 64 K rows are contiguous
             for (int h = 0; h < L0_NH; ++h) {
               const __nv_bfloat16* src =
                   a.Mt + (((long long)(hg * L0_NH + h) * 2 + crank) * a.C_pad + c0 + st * CG) *
-                             (PP * 32);
+                             (PP * (L0_DH / 2));
               bulk_load(sB + h * L0_BH_BYTES, src, L0_BH_BYTES, &full[stage]);
             }
           } else {
             const int e = st - nmain;
             const int ce = min(16, g - 16 * e);
-            mbar_expect_tx(&full[stage], (rowp ? ce * PROW : 0) + L0_NH * 16 * 32 * 2);
+            mbar_expect_tx(&full[stage], (rowp ? ce * PROW : 0) + L0_NH * 16 * L0_DH);
             if (rowp)
               for (int cc = 0; cc < ce; ++cc)
                 bulk_load(sI + cc * PROW, pslice(16 * e + cc), PROW, &full[stage]);
-            // Et [n][H][2][KE/8][4][8][8]
+            // Et [n][H][2][KE/8][DH/16][8][8]
             for (int h = 0; h < L0_NH; ++h) {
               const __nv_bfloat16* src =
-                  a.Et + (((long long)n * a.H + hg * L0_NH + h) * 2 + crank) * (32LL * a.KE) +
-                  e * 16 * 32;
-              bulk_load(sB + h * L0_BH_BYTES, src, 16 * 32 * 2, &full[stage]);
+                  a.Et + (((long long)n * a.H + hg * L0_NH + h) * 2 + crank) *
+                             ((long long)(L0_DH / 2) * a.KE) + e * 16 * (L0_DH / 2);
+              bulk_load(sB + h * L0_BH_BYTES, src, 16 * L0_DH, &full[stage]);
             }
           }
           if (++stage == L0_STAGES) { stage = 0; phase ^= 1; }
@@ -631,13 +632,13 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
                   mma_ts_pair(tbase + h * L0_DH, at0 + h * 32 + kk * 8,
-                              smem_desc(sb + h * L0_BH_BYTES + kk * 1024, 512, 128, 0), idesc,
+                              smem_desc(sb + h * L0_BH_BYTES + kk * 2 * BLBO, BLBO, 128, 0), idesc,
                               (st | kk) != 0);
             } else {
 #pragma unroll
               for (int h = 0; h < L0_NH; ++h)
                 mma_ts_pair(tbase + h * L0_DH, at0 + h * 32,
-                            smem_desc(sb + h * L0_BH_BYTES, 512, 128, 0), idesc, 1u);
+                            smem_desc(sb + h * L0_BH_BYTES, BLBO, 128, 0), idesc, 1u);
             }
             commit_pair(&empty[cs]);
             commit_pair(&aempty[G]);
@@ -656,7 +657,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
     const int quarter = warp & 3;       // TMEM lane quarter is fixed by warp id % 4
     const int m = quarter * 32 + lane;  // row within tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    constexpr int EC = L0_NH * 16;      // accumulator columns drained by this warp
+    constexpr int EC = L0_NH * L0_DH / 4;  // accumulator columns drained by this warp
     const int ecol = (G * 2 + kh) * EC;
     const bool lead = bw == 0 && lane == 0;  // issues the ctx tensor stores
     auto p_smem = [&](uint32_t base, int cc, uint32_t (&o)[2]) {  // base has the row offset
@@ -681,10 +682,11 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
     auto issue_pos = [&](int n, int tile, int hg) {
       bulk_wait_read0();
       const int s0 = (min(tile, n_tiles - 1) * 128) % a.S;
-      mbar_expect_tx(posv_full, L0_NH * 128 * 128);
-      for (int hd = 0; hd < L0_NH; ++hd)
-        tma_load_2d(stage_out + hd * (128 * 128), &tm_pos, posv_full, (hg * L0_NH + hd) * L0_DH,
-                    n * a.S + s0);
+      constexpr int NSUB = L0_NH * L0_DH / 64;  // 64-column sub-tiles of the head group
+      mbar_expect_tx(posv_full, NSUB * 128 * 128);
+      for (int sub = 0; sub < NSUB; ++sub)
+        tma_load_2d(stage_out + sub * (128 * 128), &tm_pos, posv_full,
+                    hg * L0_NH * L0_DH + sub * 64, n * a.S + s0);
     };
     auto epilogue = [&](int n, int tile, int hg, float sc) {
       mbar_wait(accfull, accphase);  // the unit's last MMAs
@@ -704,7 +706,7 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
 #pragma unroll
         for (int cb = 0; cb < EC; cb += 32) {
           const int col = ecol + cb;               // column within the head group
-          const int hd = col / L0_DH, c8 = (col % L0_DH) / 8;
+          const int hd = col / 64, c8 = (col % 64) / 8;  // 64-column sub-tile, 16-B chunk
           uint32_t v[32];
           tmem_ld32(tbase + lane_off + col, v);
           tmem_ld_wait();
@@ -739,8 +741,8 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
       tc_fence_after();
       if (lead && tile < n_tiles && !(a.debug_mode & (8 | 32))) {
         const uint32_t sout = smem_u32(stage_out);
-        for (int hd = 0; hd < L0_NH; ++hd)
-          tma_store_2d(&tm_ctx, sout + hd * (128 * 128), (hg * L0_NH + hd) * L0_DH,
+        for (int sub = 0; sub < L0_NH * L0_DH / 64; ++sub)
+          tma_store_2d(&tm_ctx, sout + sub * (128 * 128), hg * L0_NH * L0_DH + sub * 64,
                        n * R + tile * 128);
         bulk_commit();
       }
@@ -895,8 +897,10 @@ __global__ void __launch_bounds__(L0_THREADS, 1)
 cudaError_t launch_l0_node(const L0NodeArgs& a, const CUtensorMap& tm_ctx,
                            const CUtensorMap& tm_pos, int num_sms, cudaStream_t st) {
   const int R = a.B * a.S;
-  const int nh = a.H % 4 == 0 ? 4 : 2;
-  if (R % 128 || a.S % 128 || 128 % a.wp || a.H % nh || a.D != a.H * L0_DH || a.KE % 16)
+  const int dh = a.D / a.H;
+  const int nh = dh == 128 ? 2 : (a.H % 4 == 0 ? 4 : 2);  // heads per unit: NH * dh <= 256
+  if (R % 128 || a.S % 128 || 128 % a.wp || a.H % nh || a.D != a.H * dh ||
+      (dh != 64 && dh != 128) || a.KE % 16 || a.nh != nh)
     return cudaErrorInvalidValue;
   const int n_tiles = R / 128;
   const int units = a.n_nodes * ((n_tiles + 1) / 2) * (a.H / nh);
@@ -904,11 +908,12 @@ cudaError_t launch_l0_node(const L0NodeArgs& a, const CUtensorMap& tm_ctx,
   const int grid = (units < max_cl ? units : max_cl) * 2;
   void (*kern)(L0NodeArgs, const CUtensorMap, const CUtensorMap) = nullptr;
   const bool rp = a.p_row_mode != 0;
-#define L0N_PICK(PP_, NH_) kern = rp ? l0_node_kernel<PP_, NH_, true> : l0_node_kernel<PP_, NH_, false>;
+#define L0N_PICK(PP_, NH_, DH_) \
+  kern = rp ? l0_node_kernel<PP_, NH_, DH_, true> : l0_node_kernel<PP_, NH_, DH_, false>;
   if (a.P == 8) {
-    if (nh == 4) { L0N_PICK(64, 4) } else { L0N_PICK(64, 2) }
+    if (dh == 128) { L0N_PICK(64, 2, 128) } else if (nh == 4) { L0N_PICK(64, 4, 64) } else { L0N_PICK(64, 2, 64) }
   } else if (a.P == 4) {
-    if (nh == 4) { L0N_PICK(16, 4) } else { L0N_PICK(16, 2) }
+    if (dh == 128) { L0N_PICK(16, 2, 128) } else if (nh == 4) { L0N_PICK(16, 4, 64) } else { L0N_PICK(16, 2, 64) }
   } else {
     return cudaErrorInvalidValue;
   }

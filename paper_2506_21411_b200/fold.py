@@ -179,6 +179,7 @@ class PackedRank:
     C_pad: int
     KE: int
     HP: int
+    NH: int                  # heads per K_l0 unit (fold.unit_heads)
     attn_l0: bool
     l0_c0: torch.Tensor
     l0_g: torch.Tensor
@@ -201,6 +202,12 @@ class PackedRank:
     levels: tuple
 
 
+def unit_heads(embed: int, heads: int) -> int:
+    """Heads per K_l0 unit (its accumulator holds NH * dh <= 256 columns); also the head-group
+    width of the K_p0 p layout."""
+    return 2 if embed // heads == 128 else (4 if heads % 4 == 0 else 2)
+
+
 def pack_rank(fr: FoldedRank, device) -> PackedRank:
     from . import _lib
 
@@ -221,16 +228,18 @@ def pack_rank(fr: FoldedRank, device) -> PackedRank:
         _lib.call("dchag_tile_weights", _lib.ptr(src), nblk, K, N, _lib.ptr(dst), stream)
         return dst
 
-    # Mt [H][2 halves][C_pad*PP (channel-major K)][32]: a CTA pair splits each head's 64
+    # Mt [H][2 halves][C_pad*PP (channel-major K)][dh/2]: a CTA pair splits each head's dh
     # output columns, and one stage's K rows (CG channels) are one contiguous block per half
-    Msrc = torch.zeros(h, C_pad, pp, 2, 32, **f32)
-    Msrc[:, :C] = fr.M.to(**f32).view(C, pp, h, 2, 32).permute(2, 0, 1, 3, 4)
-    Mt = tile(Msrc.permute(0, 3, 1, 2, 4).reshape(h * 2, C_pad * pp, 32), h * 2, C_pad * pp, 32)
-    # Et [n0][H][2][KE][32]: row k = node-local channel
-    Esrc = torch.zeros(n0, h, KE, 2, 32, **f32)
+    dh = d // h
+    hw = dh // 2
+    Msrc = torch.zeros(h, C_pad, pp, 2, hw, **f32)
+    Msrc[:, :C] = fr.M.to(**f32).view(C, pp, h, 2, hw).permute(2, 0, 1, 3, 4)
+    Mt = tile(Msrc.permute(0, 3, 1, 2, 4).reshape(h * 2, C_pad * pp, hw), h * 2, C_pad * pp, hw)
+    # Et [n0][H][2][KE][dh/2]: row k = node-local channel
+    Esrc = torch.zeros(n0, h, KE, 2, hw, **f32)
     for n, (c0, g) in enumerate(zip(fr.l0_c0, fr.l0_g)):
-        Esrc[n, :, :g] = fr.Cb[c0:c0 + g].to(**f32).view(g, h, 2, 32).permute(1, 0, 2, 3)
-    Et = tile(Esrc.permute(0, 1, 3, 2, 4).reshape(n0 * h * 2, KE, 32), n0 * h * 2, KE, 32)
+        Esrc[n, :, :g] = fr.Cb[c0:c0 + g].to(**f32).view(g, h, 2, hw).permute(1, 0, 2, 3)
+    Et = tile(Esrc.permute(0, 1, 3, 2, 4).reshape(n0 * h * 2, KE, hw), n0 * h * 2, KE, hw)
     posV0 = fr.posV.to(**f32).to(torch.bfloat16).contiguous()
     WUt = bU = posU = p_const = None
     if fr.attn_l0:
@@ -254,7 +263,7 @@ def pack_rank(fr: FoldedRank, device) -> PackedRank:
     comb_g = [torch.tensor(g, **i32) for g in fr.comb_g]
     comb_mix = [None if m is None else m.to(**f32).contiguous() for m in fr.comb_mix]
     return PackedRank(
-        n0=n0, C=C, C_pad=C_pad, KE=KE, HP=HP, attn_l0=fr.attn_l0,
+        n0=n0, C=C, C_pad=C_pad, KE=KE, HP=HP, NH=unit_heads(d, h), attn_l0=fr.attn_l0,
         l0_c0=torch.tensor(fr.l0_c0, **i32), l0_g=torch.tensor(fr.l0_g, **i32),
         l0_g_list=list(fr.l0_g), WUt=WUt, bU=bU, posU=posU, Mt=Mt, Et=Et, posV0=posV0,
         p_const=p_const, Wp=Wp, bp=bp, N=N, comb_first=comb_first, comb_g=comb_g,

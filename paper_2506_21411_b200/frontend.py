@@ -107,8 +107,8 @@ class DchagFrontEnd(torch.nn.Module):
         s = m.seq
         wp = m.image_w // m.patch
         probs = []
-        if dh != 64:
-            probs.append(f"head dim {dh} != 64")
+        if dh not in (64, 128):
+            probs.append(f"head dim {dh} not in (64, 128)")
         if m.heads % 2:
             probs.append(f"heads {m.heads} not even")
         if m.patch not in (4, 8):
@@ -352,7 +352,7 @@ class DchagFrontEnd(torch.nn.Module):
             # unnormalised e + 1/sum: K_l0 scales its accumulator (one exp per logit)
             pinv = torch.empty(pk.n0, R, h, **f32)
             _lib.call("dchag_l0_logits", _lib.ptr(img), isb, isc, B, m.image_h, m.image_w, p,
-                      h, pk.HP, pk.n0, max(pk.l0_g_list), _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g),
+                      h, pk.HP, pk.NH, pk.n0, max(pk.l0_g_list), _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g),
                       _lib.ptr(poff),
                       _lib.ptr(pk.WUt), _lib.ptr(pk.bU), _lib.ptr(pk.posU), _lib.ptr(pbuf),
                       _lib.ptr(pinv), st)

@@ -116,7 +116,7 @@ class DchagTrainer:
             pbuf = torch.empty(acc, device=dev, dtype=torch.bfloat16)
             pinv = torch.empty(pk.n0, R, h, device=dev, dtype=torch.float32)
             _lib.call("dchag_l0_logits", _lib.ptr(img), img.stride(0), img.stride(1), B,
-                      m.image_h, m.image_w, m.patch, h, pk.HP, pk.n0, max(pk.l0_g_list),
+                      m.image_h, m.image_w, m.patch, h, pk.HP, pk.NH, pk.n0, max(pk.l0_g_list),
                       _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g), _lib.ptr(poff_t), _lib.ptr(pk.WUt),
                       _lib.ptr(pk.bU), _lib.ptr(pk.posU), _lib.ptr(pbuf), _lib.ptr(pinv), st)
             prow = 1

@@ -106,6 +106,11 @@ CONFIGS = [
     dict(channels=22, image_h=64, image_w=128, patch=8, embed=256, heads=4, tp=3, max_group=3),
     dict(channels=40, image_h=64, image_w=64, patch=4, embed=256, heads=4, tp=2, max_group=16),
     dict(channels=37, image_h=128, image_w=128, patch=8, embed=512, heads=8, tp=1, max_group=4),
+    # head dim 128 (the D = 4096 / 32-head sweep configs): two heads per K_l0 unit
+    dict(channels=20, image_h=64, image_w=128, patch=8, embed=256, heads=2, tp=1, max_group=8),
+    dict(channels=18, image_h=64, image_w=64, patch=4, embed=512, heads=4, tp=2, max_group=4),
+    dict(channels=24, image_h=64, image_w=128, patch=8, embed=256, heads=2, tp=1, max_group=6,
+         layer_kind="linear"),
 ]
 
 
@@ -241,7 +246,7 @@ def test_l0_logits_normalised_and_unnormalised_agree(P, W):
         p = torch.empty(acc, device="cuda", dtype=torch.bfloat16)
         inv = torch.empty(pk.n0, R, h, device="cuda") if with_inv else None
         _lib.call("dchag_l0_logits", _lib.ptr(img), img.stride(0), img.stride(1), B, 64, W, P,
-                  h, pk.HP, pk.n0, max(pk.l0_g_list), _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g),
+                  h, pk.HP, pk.NH, pk.n0, max(pk.l0_g_list), _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g),
                   _lib.ptr(poff), _lib.ptr(pk.WUt), _lib.ptr(pk.bU), _lib.ptr(pk.posU),
                   _lib.ptr(p), _lib.ptr(inv), _lib.stream_handle())
         outs.append((p, inv))
