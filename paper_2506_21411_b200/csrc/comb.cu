@@ -23,12 +23,17 @@ template <int CH>
 __global__ void __launch_bounds__(256, CH >= 8 ? 1 : (CH >= 4 ? 2 : 4)) combine_kernel(CombineArgs a) {
   __shared__ float sp[8][COMB_PTAB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // item = (node, row, column segment of <= 2048 columns; D = 4096 rows take two warps)
+  const int nseg = (a.D + 2047) / 2048;
   const long long item = (long long)blockIdx.x * 8 + warp;
-  const int n = (int)(item / a.R);
-  const int r = (int)(item - (long long)n * a.R);
+  const long long nr = item / nseg;
+  const int seg = (int)(item - nr * nseg);
+  const int n = (int)(nr / a.R);
+  const int r = (int)(nr - (long long)n * a.R);
   if (n >= a.n_nodes) return;
   const int first = __ldg(a.node_first + n), g = __ldg(a.node_g + n);
   const int H = a.H, dh = a.D / H;
+  const int col0 = seg * 2048, dseg = min(2048, a.D - col0);
   // row r = (rb, rs) with rs < rows_inner: child rows may be interleaved with other channels
   const int rb = r / a.rows_inner, rs = r - rb * a.rows_inner;
   float* p = sp[warp];
@@ -55,11 +60,11 @@ __global__ void __launch_bounds__(256, CH >= 8 ? 1 : (CH >= 4 ? 2 : 4)) combine_
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[q][e] = 0.f;
   const __nv_bfloat16* vbase =
-      a.V + (long long)first * a.sVj + (long long)rb * a.sVb + (long long)rs * a.D;
-  const int nchunk = a.D / 8;  // chunks of this row; lanes past it idle (D < 256)
+      a.V + (long long)first * a.sVj + (long long)rb * a.sVb + (long long)rs * a.D + col0;
+  const int nchunk = dseg / 8;  // chunks of this segment; lanes past it idle (D < 256)
   int hq[CH];  // head of each of this lane's chunks
 #pragma unroll
-  for (int q = 0; q < CH; ++q) hq[q] = ((lane + 32 * q) * 8) / dh;
+  for (int q = 0; q < CH; ++q) hq[q] = (col0 + (lane + 32 * q) * 8) / dh;
   const bool act = lane < nchunk;  // D >= 256 is a multiple of 256: all lanes active
   auto accumulate = [&](const uint4 (&v)[CH], int j) {
 #pragma unroll
@@ -92,7 +97,7 @@ __global__ void __launch_bounds__(256, CH >= 8 ? 1 : (CH >= 4 ? 2 : 4)) combine_
     for (int q = 0; q < CH; ++q) v0[q] = act ? __ldg(r0 + lane + 32 * q) : make_uint4(0, 0, 0, 0);
     accumulate(v0, j);
   }
-  __nv_bfloat16* orow = a.ctx + ((long long)n * a.R + r) * a.D;
+  __nv_bfloat16* orow = a.ctx + ((long long)n * a.R + r) * a.D + col0;
   if (!act) return;
 #pragma unroll
   for (int q = 0; q < CH; ++q) {
@@ -106,12 +111,13 @@ __global__ void __launch_bounds__(256, CH >= 8 ? 1 : (CH >= 4 ? 2 : 4)) combine_
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
-  if ((a.D > 256 ? a.D % 256 : a.D % 8) || a.D > 2048 || (a.D / a.H) % 8 || a.H > COMB_MAXH ||
+  if ((a.D > 256 ? a.D % 256 : a.D % 8) || (a.D > 2048 && a.D % 2048) || (a.D / a.H) % 8 ||
+      a.H > COMB_MAXH ||
       a.max_g * (a.mix ? 1 : a.H) > COMB_PTAB)
     return cudaErrorInvalidValue;
-  const long long items = (long long)a.n_nodes * a.R;
+  const long long items = (long long)a.n_nodes * a.R * ((a.D + 2047) / 2048);
   const int grid = (int)((items + 7) / 8);
-  switch ((a.D + 255) / 256) {
+  switch ((min(a.D, 2048) + 255) / 256) {
     case 1: combine_kernel<1><<<grid, 256, 0, st>>>(a); break;
     case 2: combine_kernel<2><<<grid, 256, 0, st>>>(a); break;
     case 4: combine_kernel<4><<<grid, 256, 0, st>>>(a); break;

@@ -111,6 +111,8 @@ CONFIGS = [
     dict(channels=18, image_h=64, image_w=64, patch=4, embed=512, heads=4, tp=2, max_group=4),
     dict(channels=24, image_h=64, image_w=128, patch=8, embed=256, heads=2, tp=1, max_group=6,
          layer_kind="linear"),
+    # D = 4096, 32 heads (sweep): combine rows split in 2048-column segments
+    dict(channels=10, image_h=64, image_w=128, patch=8, embed=4096, heads=32, tp=1, max_group=4),
 ]
 
 
