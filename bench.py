@@ -33,7 +33,7 @@ WORKLOADS = {
                  batch=2),
     # training step (fwd+bwd), SURVEY.md section 8(d) "TR": C500 D2048 H32 (dh 64), bf16
     "train": dict(channels=500, image_h=128, image_w=128, patch=8, embed=2048, heads=32,
-                  depth=3, batch=32, train=True),
+                  depth=3, batch=32, train=True, final_split=True),
 }
 # scaling sweep: C 64..1024 x D 1024 (16 heads) / 4096 (32 heads,
 # dh = 128), 128x128 P8, B 32, max_group 16 with the depth derived per slab
@@ -141,6 +141,7 @@ def workload_config(args, wl, tp, max_group):
             "image": [wl["image_h"], wl["image_w"]], "patch": wl["patch"],
             "embed": wl["embed"], "heads": wl["heads"], "depth": wl["depth"],
             "max_group": max_group, "tp": tp, "global_batch": args.batch or wl["batch"],
+            "final_layer": "head-split" if wl.get("final_split") and tp > 1 else "replicated",
             "parallelism": f"dchag-tp{tp}",
             "l2": "flushed between timed steps (256 MiB write)"}
 
@@ -224,8 +225,11 @@ def b200_arm(args, wl, tp, max_group):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B = args.batch or wl["batch"]
+    # the training config's final layer is head-split over the tp group (reduce-scatter of the
+    # boundary gradient in backward, BASELINE.json configs[3])
     fe = DchagFrontEnd(wl["channels"], wl["image_h"], wl["image_w"], wl["patch"], wl["embed"],
-                       wl["heads"], max_group=max_group, tp=tp, rank=rank)
+                       wl["heads"], max_group=max_group, tp=tp, rank=rank,
+                       final_layer_tp_split=bool(wl.get("final_split")) and tp > 1)
     fe.init_weights(seed=0, all_ranks=False)
     fe.prepare()
     off, cnt = fe.slab

@@ -83,8 +83,6 @@ class DchagFrontEnd(torch.nn.Module):
             raise ConfigError(
                 f"depth {depth} disagrees with build_tree_spec(local_channels, {max_group}): "
                 f"{sorted({t.depth for t in trees})}")
-        if final_layer_tp_split:
-            raise ConfigError("final_layer_tp_split is not implemented on the B200 path yet")
         if not 0 <= rank < tp:
             raise ConfigError(f"rank {rank} outside tp {tp}")
         self._check_gpu_shape()
@@ -422,9 +420,40 @@ class DchagFrontEnd(torch.nn.Module):
             ctx_f = Vg[:R * d].view(1, R, d)  # softmax over one stream is exactly 1
         if out is None:
             out = torch.empty(R, d, device=dev, dtype=self.out_dtype)
+        if self.strategy.final_layer_tp_split and self.tp > 1:
+            return self._finish_head_split(ctx_f, B, out)
         _lib.call("dchag_gemm_bf16", _lib.ptr(ctx_f), 1, 1, R, d, R * d, 0, d, _lib.ptr(pk.Wf),
                   d, d * d, d, _lib.ptr(pk.bf), d, 0, 0, 0, 1, _lib.ptr(out),
                   int(self.out_dtype == torch.float32), R * d, 0, d, 0, 0, 0, 0, st)
+        return out.view(B, 1, s, d)
+
+    def _finish_head_split(self, ctx_f, B, out):
+        """final_layer_tp_split (strategies.py:211-215, layers.py:102-122 with TpHooks): this
+        rank owns heads [r H/tp, (r+1) H/tp); its partial output ctx[:, own columns] @
+        wo[own rows] (+ bo on rank 0) is summed over the tp group (the reference's allsum =
+        ReduceScatter + AllGather, one NCCL all-reduce here)."""
+        import torch.distributed as dist
+        pk = self.prepare()
+        m = self.model
+        d, s = m.embed, self.seq
+        R = B * s
+        dev = ctx_f.device
+        kc = d // self.tp
+        c0 = self.rank * kc
+        key = ("head_split_w", dev)
+        cache = self.__dict__.setdefault("_cache", {})
+        if key not in cache:
+            wf_loc = pk.Wf[:, c0:c0 + kc].contiguous()            # [D_out][D/tp] n-major
+            b_loc = pk.bf if self.rank == 0 else torch.zeros_like(pk.bf)
+            cache[key] = (wf_loc, b_loc)
+        wf_loc, b_loc = cache[key]
+        part = torch.empty(R, d, device=dev, dtype=torch.float32)
+        a = ctx_f.view(R, d)[:, c0:]                                # K = D/tp columns, row stride D
+        _lib.call("dchag_gemm_bf16", _lib.ptr(a), 1, 1, R, kc, R * d, 0, d, _lib.ptr(wf_loc),
+                  d, d * kc, d, _lib.ptr(b_loc), d, 0, 0, 0, 1, _lib.ptr(part), 1, R * d, 0, d,
+                  0, 0, 0, 0, _lib.stream_handle())
+        dist.all_reduce(part, group=self.process_group)
+        out.copy_(part.view_as(out))
         return out.view(B, 1, s, d)
 
     def _final_first(self, dev):

@@ -167,6 +167,8 @@ class DchagTrainer:
     def forward_final(self, y_all, saved):
         """Shared final layer over the gathered streams y_all [tp, R, D] (replicated)."""
         fe = self.fe
+        if fe.strategy.final_layer_tp_split and fe.tp > 1:
+            return self._forward_final_split(y_all, saved)
         w = fe.weights
         d, h, s = fe.model.embed, fe.model.heads, fe.seq
         R, B = saved["R"], saved["B"]
@@ -192,10 +194,10 @@ class DchagTrainer:
                 out.append(pos @ w[f"{node}.wv"])
         return torch.stack(out)                                          # [n0, S, D]
 
-    def _combine(self, V, L, mix, firsts, gs, R):
+    def _combine(self, V, L, mix, firsts, gs, R, heads=None):
         n = len(firsts)
         d = V.shape[-1]
-        h = self.fe.model.heads
+        h = heads or self.fe.model.heads
         ctx = torch.empty(n, R, d, device=V.device, dtype=torch.bfloat16)
         ft = torch.tensor(firsts, device=V.device, dtype=torch.int32)
         gt = torch.tensor(gs, device=V.device, dtype=torch.int32)
@@ -233,12 +235,12 @@ class DchagTrainer:
         return V, L, ctx, y
 
     # ---------------------------------------------------------------- backward
-    def _combine_bwd(self, V, L, mix, G, firsts, gs, R):
+    def _combine_bwd(self, V, L, mix, G, firsts, gs, R, heads=None):
         """-> gV bf16 (V's shape), dL fp32 (attention) or dm fp32 [child, R] (linear)."""
         n = len(firsts)
         nch = V.shape[0]
         d = V.shape[-1]
-        h = self.fe.model.heads
+        h = heads or self.fe.model.heads
         gV = torch.empty_like(V)
         dL = torch.empty(nch, R, h, device=V.device, dtype=torch.float32) if mix is None else None
         dm = torch.empty(nch, R, device=V.device, dtype=torch.float32) if mix is not None else None
@@ -260,10 +262,79 @@ class DchagTrainer:
             dist.all_reduce(grads["special.pos"], group=self.fe.process_group)
         return grads
 
+    def _own_heads(self):
+        fe = self.fe
+        h, d = fe.model.heads, fe.model.embed
+        hc = h // fe.tp
+        dh = d // h
+        h0 = fe.rank * hc
+        return h0, hc, slice(h0 * dh, (h0 + hc) * dh), slice(h0, h0 + hc)
+
+    def _forward_final_split(self, y_all, saved):
+        """final_layer_tp_split (strategies.py:211-215): this rank projects the gathered
+        streams onto its own heads only (wv / wk / wq column shards, params.py:166-177),
+        combines them, and its partial ctx_own @ wo[own rows] is summed over the tp group
+        (TpHooks.allsum = ReduceScatter + AllGather; one all-reduce), bo added once."""
+        import torch.distributed as dist
+        fe = self.fe
+        w = fe.weights
+        d, h, s = fe.model.embed, fe.model.heads, fe.seq
+        R, B = saved["R"], saved["B"]
+        _, hc, cols, hs = self._own_heads()
+        U = query_logit_weights(w, "agg.final", h)
+        Wc = torch.cat([w["agg.final.wv"][:, cols], U[:, hs]], dim=1)
+        dl = cols.stop - cols.start
+        Vf, Lf = _gemm(y_all.reshape(fe.tp * R, d), Wc, N_logit=hc)
+        Vf, Lf = Vf.view(fe.tp, R, dl), Lf.view(fe.tp, R, hc)
+        ctx_f = self._combine(Vf, Lf, None, [0], [fe.tp], R, heads=hc)
+        bo = w["agg.final.bo"] if fe.rank == 0 else torch.zeros_like(w["agg.final.bo"])
+        out = _gemm(ctx_f[0], w["agg.final.wo"][cols], bo, out_f32=True)
+        dist.all_reduce(out, group=fe.process_group)
+        saved.update(y_all=y_all, Vf=Vf, Lf=Lf, ctx_f=ctx_f)
+        return out.view(B, 1, s, d)
+
+    def _backward_final_split(self, saved, g_out):
+        """Backward of the head-split final layer: shard grads (wv/wk/wq columns, wo rows of
+        the own heads; bo and the fanned-out q in full), and the root-stream gradient by a
+        ReduceScatter of every rank's partial gathered-stream gradient along the stream axis
+        (the fused TpHooks.fanout RS + AG and gather slice, strategies.py:54-67, :91-94)."""
+        import torch.distributed as dist
+        fe = self.fe
+        w = fe.weights
+        d, h = fe.model.embed, fe.model.heads
+        R = saved["R"]
+        _, hc, cols, hs = self._own_heads()
+        grads = {}
+        g_out = _f32(g_out.reshape(R, d))
+        ctx_f = saved["ctx_f"][0].float()
+        grads["agg.final.bo"] = g_out.sum(0)
+        grads["agg.final.wo"] = _mm(ctx_f.t(), g_out)                      # own rows
+        g_ctx = (g_out @ w["agg.final.wo"][cols].t()).view(1, R, -1)
+        gV, dL, _ = self._combine_bwd(saved["Vf"], saved["Lf"], None, g_ctx, [0], [fe.tp], R,
+                                      heads=hc)
+        y_all = saved["y_all"].reshape(fe.tp * R, d)
+        grads["agg.final.wv"] = _mm(y_all.t(), gV.reshape(fe.tp * R, -1))  # own columns
+        dU = torch.zeros(d, h, device=g_out.device, dtype=torch.float32)
+        dU[:, hs] = _mm(y_all.t(), dL.reshape(fe.tp * R, hc))
+        gu = _u_backward(w, "agg.final", dU, h)
+        grads["agg.final.wk"] = gu["agg.final.wk"][:, cols].contiguous()
+        grads["agg.final.wq"] = gu["agg.final.wq"][:, cols].contiguous()
+        q_grad = gu["agg.final.q"].contiguous()
+        dist.all_reduce(q_grad, group=fe.process_group)                   # fanout of q
+        grads["agg.final.q"] = q_grad
+        U_own = query_logit_weights(w, "agg.final", h)[:, hs]
+        g_part = (gV.float() @ w["agg.final.wv"][:, cols].t() +
+                  dL @ U_own.t()).contiguous()                            # [tp, R, D]
+        g_y = torch.empty(R, d, device=g_out.device, dtype=torch.float32)
+        dist.reduce_scatter_tensor(g_y, g_part.view(fe.tp * R, d), group=fe.process_group)
+        return grads, g_y.view(1, R, d)
+
     def backward_final(self, saved, g_out):
         """Final-layer grads (identical on every rank) and this rank's root-stream gradient
         (the local slice of the gathered gradient, strategies.py:91-94)."""
         fe = self.fe
+        if fe.strategy.final_layer_tp_split and fe.tp > 1:
+            return self._backward_final_split(saved, g_out)
         w = fe.weights
         d, h = fe.model.embed, fe.model.heads
         R = saved["R"]

@@ -29,7 +29,7 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     tp, rank = dist.get_world_size(), dist.get_rank()
     worst = 0.0
-    for meta in CASES:
+    for meta, split in [(m, sp) for m in CASES for sp in (False, True)]:
         lk = meta.get("layer_kind", "cross_attention")
         specs = O.frontend_param_specs(meta["channels"], meta["image_h"], meta["image_w"],
                                        meta["patch"], meta["embed"], tp, meta["max_group"],
@@ -41,7 +41,8 @@ def main():
         img_bf = torch.from_numpy(img.astype(np.float32)).to(torch.bfloat16)
         fe = DchagFrontEnd(meta["channels"], meta["image_h"], meta["image_w"], meta["patch"],
                            meta["embed"], meta["heads"], max_group=meta["max_group"],
-                           agg_layer_kind=lk, tp=tp, rank=rank, out_dtype=torch.float32)
+                           agg_layer_kind=lk, tp=tp, rank=rank, out_dtype=torch.float32,
+                           final_layer_tp_split=split)
         fe.load_weights(w)
         out = fe(img_bf.cuda()).cpu().numpy()  # full images: the rank slices its own slab
         want = O.dchag_frontend(img_bf.float().numpy().astype(np.float64), w,
@@ -49,8 +50,8 @@ def main():
                                 max_group=meta["max_group"], layer_kind=lk)
         err = O.rel_err(out, want)
         worst = max(worst, err)
-        print(f"rank {rank}/{tp} C={meta['channels']} slab={fe.slab} {lk}: rel_err={err:.3e}",
-              flush=True)
+        print(f"rank {rank}/{tp} C={meta['channels']} slab={fe.slab} {lk}"
+              f"{' head-split final' if split else ''}: rel_err={err:.3e}", flush=True)
     # training step over NCCL: forward_train (AllGather of root streams) + backward
     # (local-slice boundary, special.pos all-reduce), vs float64 autograd of the reference math
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -64,22 +65,33 @@ def main():
     probe = rng.standard_normal((2, 1, 128, 256))
     img64 = img.float().numpy().astype(np.float64)
     _, g_ref = TRF.grads(img64, w, probe, patch=8, heads=4, tp=tp, max_group=2)
-    fe = DchagFrontEnd(13, 64, 128, 8, 256, 4, max_group=2, tp=tp, rank=rank,
-                       out_dtype=torch.float32)
-    fe.load_weights(w)
-    trn = DchagTrainer(fe)
-    out, saved = trn.forward_train(img.cuda())
-    grads = trn.backward(saved, torch.from_numpy(probe.astype(np.float32)).cuda())
-    off, cnt = fe.slab
-    errs = {}
-    for k, v in grads.items():
-        v = v.double().cpu().numpy()
-        ref = g_ref[k][off:off + cnt] if k in ("tok.w", "tok.b", "special.channel_id") else g_ref[k]
-        errs[k] = O.rel_err(v, ref)
-    terr = max(errs.values())
-    worst = max(worst, terr)
-    print(f"rank {rank}/{tp} train step: {len(errs)} grads, worst rel_err={terr:.3e} "
-          f"({max(errs, key=errs.get)})", flush=True)
+    for split in (False, True):
+        fe = DchagFrontEnd(13, 64, 128, 8, 256, 4, max_group=2, tp=tp, rank=rank,
+                           out_dtype=torch.float32, final_layer_tp_split=split)
+        fe.load_weights(w)
+        trn = DchagTrainer(fe)
+        out, saved = trn.forward_train(img.cuda())
+        grads = trn.backward(saved, torch.from_numpy(probe.astype(np.float32)).cuda())
+        off, cnt = fe.slab
+        dh = 256 // 4
+        hc = 4 // tp
+        cols = slice(rank * hc * dh, (rank + 1) * hc * dh)
+        errs = {}
+        for k, v in grads.items():
+            v = v.double().cpu().numpy()
+            ref = g_ref[k]
+            if k in ("tok.w", "tok.b", "special.channel_id"):
+                ref = ref[off:off + cnt]
+            elif split and k in ("agg.final.wv", "agg.final.wk", "agg.final.wq"):
+                ref = ref[:, cols]          # column shards of the own heads (params.py:166-177)
+            elif split and k == "agg.final.wo":
+                ref = ref[cols]             # row shard
+            errs[k] = O.rel_err(v, ref)
+        terr = max(errs.values())
+        worst = max(worst, terr)
+        print(f"rank {rank}/{tp} train step{' (head-split final)' if split else ''}: "
+              f"{len(errs)} grads, worst rel_err={terr:.3e} ({max(errs, key=errs.get)})",
+              flush=True)
     t = torch.tensor([worst], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
