@@ -78,6 +78,21 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
                   const void* Mt, int C_pad, const void* Et, int KE, const void* posV, void* ctx,
                   void* stream);
 
+/* full_cross node weights (layers.py:125-138 with sdp_attention layers.py:49-64): per node
+ * and row, with q/k of child j at QK + j*sQj + r*ldq (k at +D, bf16) and u_jh = V_j,h .
+ * (wo rq)_h / sqrt(D) at u + j*sUj + r*H (fp32):  S^h = softmax_j(q_i,h . k_j,h / sqrt(dh)),
+ * s_i = sum_h sum_j S^h_ij u_jh,  p2 = softmax_i(s),  w[n][r][j][h] = sum_i p2_i S^h_ij.
+ * The node output is then (sum_j w_jh V_j,h) @ wo + bo (dchag_combine_weighted + GEMM).
+ * max_g <= 32, H <= 32. */
+int dchag_fullcross_weights(int n_nodes, int R, int D, int H, const int* node_first,
+                            const int* node_g, int max_g, const void* QK, long long sQj,
+                            long long ldq, const float* u, long long sUj, float* w, void* stream);
+
+/* ctx[n][r][h-blk] = sum_j w[n][r][j][h] V_j[r][h-blk]; V_j row r at V + j*sVj + r*ldv (bf16). */
+int dchag_combine_weighted(int n_nodes, int R, int D, int H, const int* node_first,
+                           const int* node_g, int max_g, const void* V, long long sVj,
+                           long long ldv, const float* w, void* ctx, void* stream);
+
 /* Upper-level / final combine (K_comb): ctx[n][r][:] = sum_j w_j(r,h) V_{first+j}[r][:],
  * w = softmax_j(L_{first+j}[r][h]) (attention; mix == NULL) or mix[first+j] (linear).
  * Child j's V at V + j*sVj + r*D (bf16), logits at L + j*sLj + r*H (fp32).

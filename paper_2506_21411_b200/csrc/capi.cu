@@ -258,6 +258,7 @@ int dchag_combine_strided(int n_nodes, int R, int D, int H, const int* node_firs
   if (!mix && !L) return fail(DCHAG_ERR_SHAPE, "combine: need logits or mix");
   if (rows_inner < 1) return fail(DCHAG_ERR_SHAPE, "combine: rows_inner must be >= 1");
   CombineArgs a;
+  memset(&a, 0, sizeof(a));
   a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H; a.max_g = max_g;
   a.rows_inner = rows_inner; a.sVb = sVb; a.sLb = sLb;
   a.node_first = node_first; a.node_g = node_g;
@@ -265,6 +266,34 @@ int dchag_combine_strided(int n_nodes, int R, int D, int H, const int* node_firs
   a.L = L; a.sLj = sLj; a.mix = mix;
   a.ctx = reinterpret_cast<__nv_bfloat16*>(ctx);
   return cuda_status(launch_combine(a, S(stream)), "combine");
+}
+
+int dchag_fullcross_weights(int n_nodes, int R, int D, int H, const int* node_first,
+                            const int* node_g, int max_g, const void* QK, long long sQj,
+                            long long ldq, const float* u, long long sUj, float* w, void* stream) {
+  if (D % H || (D / H) % 8 || max_g < 1 || max_g > 32 || H > 32 || ldq < 2 * D || (ldq * 2) % 16 ||
+      (sQj * 2) % 16 || reinterpret_cast<uintptr_t>(QK) % 16)
+    return fail(DCHAG_ERR_SHAPE, "fullcross_weights: bad shape");
+  FullCrossArgs a;
+  a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H; a.max_g = max_g;
+  a.node_first = node_first; a.node_g = node_g;
+  a.QK = reinterpret_cast<const __nv_bfloat16*>(QK); a.sQj = sQj; a.ldq = ldq;
+  a.u = u; a.sUj = sUj; a.w = w;
+  return cuda_status(launch_fullcross_weights(a, S(stream)), "fullcross_weights");
+}
+
+int dchag_combine_weighted(int n_nodes, int R, int D, int H, const int* node_first,
+                           const int* node_g, int max_g, const void* V, long long sVj,
+                           long long ldv, const float* w, void* ctx, void* stream) {
+  CombineArgs a;
+  memset(&a, 0, sizeof(a));
+  a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H; a.max_g = max_g;
+  a.rows_inner = R; a.node_first = node_first; a.node_g = node_g;
+  a.V = reinterpret_cast<const __nv_bfloat16*>(V); a.sVj = sVj; a.ldv = ldv;
+  a.W = w;
+  a.ctx = reinterpret_cast<__nv_bfloat16*>(ctx);
+  if (!w || (ldv * 2) % 16) return fail(DCHAG_ERR_SHAPE, "combine_weighted: bad arguments");
+  return cuda_status(launch_combine(a, S(stream)), "combine_weighted");
 }
 
 int dchag_combine_bwd(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,

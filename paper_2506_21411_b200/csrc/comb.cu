@@ -37,7 +37,11 @@ __global__ void __launch_bounds__(256, CH >= 8 ? 1 : (CH >= 4 ? 2 : 4)) combine_
   // row r = (rb, rs) with rs < rows_inner: child rows may be interleaved with other channels
   const int rb = r / a.rows_inner, rs = r - rb * a.rows_inner;
   float* p = sp[warp];
-  if (a.mix) {
+  const long long ldv = a.ldv ? a.ldv : a.D;
+  if (a.W) {  // explicit per-(child, head) weights (full_cross)
+    const float* wr = a.W + ((long long)n * a.R + r) * a.max_g * H;
+    for (int i = lane; i < g * H; i += 32) p[i] = __ldg(wr + i);
+  } else if (a.mix) {
     for (int j = lane; j < g; j += 32) p[j] = __ldg(a.mix + first + j);
   } else if (lane < H) {
     const float* lr = a.L + (long long)first * a.sLj + (long long)rb * a.sLb +
@@ -60,7 +64,7 @@ __global__ void __launch_bounds__(256, CH >= 8 ? 1 : (CH >= 4 ? 2 : 4)) combine_
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[q][e] = 0.f;
   const __nv_bfloat16* vbase =
-      a.V + (long long)first * a.sVj + (long long)rb * a.sVb + (long long)rs * a.D + col0;
+      a.V + (long long)first * a.sVj + (long long)rb * a.sVb + (long long)rs * ldv + col0;
   const int nchunk = dseg / 8;  // chunks of this segment; lanes past it idle (D < 256)
   int hq[CH];  // head of each of this lane's chunks
 #pragma unroll
@@ -69,7 +73,7 @@ __global__ void __launch_bounds__(256, CH >= 8 ? 1 : (CH >= 4 ? 2 : 4)) combine_
   auto accumulate = [&](const uint4 (&v)[CH], int j) {
 #pragma unroll
     for (int q = 0; q < CH; ++q) {
-      const float pj = a.mix ? p[j] : p[j * H + hq[q]];
+      const float pj = (a.mix && !a.W) ? p[j] : p[j * H + hq[q]];
       const uint32_t vv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -124,6 +128,100 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
     case 8: combine_kernel<8><<<grid, 256, 0, st>>>(a); break;
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+// full_cross node weights (see FullCrossArgs). One CTA per (node, row), one warp per head;
+// lane j owns child j (g <= 32): it keeps k_j,h in registers and computes the row of logits
+// L_ij = q_i . k_j / sqrt(dh) against q_i broadcast from shared memory; the per-i softmax,
+// the head-sum of sum_j S_ij u_jh and the softmax over i are warp / CTA reductions.
+__global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a) {
+  extern __shared__ float fsm[];  // q: [H][g][dh] fp32, then t: [H][32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long item = blockIdx.x;
+  const int n = (int)(item / a.R);
+  const int r = (int)(item - (long long)n * a.R);
+  const int first = __ldg(a.node_first + n), g = __ldg(a.node_g + n);
+  const int H = a.H, dh = a.D / H, h = warp;
+  const int G = a.max_g;
+  float* q = fsm;                                 // [H][G][dh]
+  float* t = fsm + (size_t)H * G * dh;            // [H][32]
+  // stage q_i,h for all children (coalesced over the head's dh columns)
+  for (int i = 0; i < g; ++i) {
+    const __nv_bfloat16* qr = a.QK + (long long)(first + i) * a.sQj + (long long)r * a.ldq + h * dh;
+    for (int e = lane; e < dh; e += 32) q[((size_t)h * G + i) * dh + e] = __bfloat162float(qr[e]);
+  }
+  __syncwarp();
+  float S[32];
+  float uj = 0.f;
+  const bool act = lane < g;
+  if (act) {
+    const __nv_bfloat16* kr =
+        a.QK + (long long)(first + lane) * a.sQj + (long long)r * a.ldq + a.D + h * dh;
+    uj = __ldg(a.u + (long long)(first + lane) * a.sUj + (long long)r * H + h);
+    const float sc = rsqrtf((float)dh);
+#pragma unroll 4
+    for (int i = 0; i < 32; ++i) S[i] = 0.f;
+    for (int e0 = 0; e0 < dh; e0 += 8) {
+      const uint4 kv = *reinterpret_cast<const uint4*>(kr + e0);
+      const uint32_t kw[4] = {kv.x, kv.y, kv.z, kv.w};
+      float kf[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) { kf[2 * e] = bf16lo(kw[e]); kf[2 * e + 1] = bf16hi(kw[e]); }
+      for (int i = 0; i < g; ++i) {
+        const float* qi = q + ((size_t)h * G + i) * dh + e0;
+        float acc = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc += qi[e] * kf[e];
+        S[i] += acc;
+      }
+    }
+    for (int i = 0; i < g; ++i) S[i] *= sc;
+  }
+  // softmax over j (across lanes) for every query i; t_i = sum_j S_ij u_jh
+  for (int i = 0; i < g; ++i) {
+    float m = act ? S[i] : -INFINITY;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float e = act ? __expf(S[i] - m) : 0.f;
+    float sum = e;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    S[i] = e / sum;
+    float tu = S[i] * uj;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tu += __shfl_xor_sync(0xffffffffu, tu, o);
+    if (lane == 0) t[h * 32 + i] = tu;
+  }
+  __syncthreads();
+  // s_i = sum_h t[h][i] -> p2 = softmax_i(s) (every warp, lane i); w_jh = sum_i p2_i S_ij
+  float s = -INFINITY;
+  if (lane < g) {
+    s = 0.f;
+    for (int hh = 0; hh < H; ++hh) s += t[hh * 32 + lane];
+  }
+  float m = s;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float e = lane < g ? __expf(s - m) : 0.f;
+  float sum = e;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float p2 = e / sum;  // lane i holds p2_i
+  float wj = 0.f;
+  for (int i = 0; i < g; ++i) wj += __shfl_sync(0xffffffffu, p2, i) * (act ? S[i] : 0.f);
+  if (act) a.w[(((long long)n * a.R + r) * a.max_g + lane) * H + h] = wj;
+}
+
+cudaError_t launch_fullcross_weights(const FullCrossArgs& a, cudaStream_t st) {
+  const int dh = a.D / a.H;
+  if (a.max_g > 32 || a.H > 32 || dh % 8 || a.H < 1) return cudaErrorInvalidValue;
+  const size_t smem = ((size_t)a.H * a.max_g * dh + (size_t)a.H * 32) * sizeof(float);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(fullcross_weights_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fullcross_weights_kernel<<<(unsigned)((long long)a.n_nodes * a.R), a.H * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -91,8 +91,25 @@ struct CombineArgs {
   int rows_inner;              // row r = rb * rows_inner + rs; child row offset
   long long sVb, sLb;          //   = j*sVj + rb*sVb + rs*D   (L: j*sLj + rb*sLb + rs*H)
   __nv_bfloat16* ctx;          // [n][R][D]
+  long long ldv;               // elements between a child's V rows (0: D)
+  const float* W;              // explicit weights [n][R][max_g][H] (full_cross), or null
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
+
+// full_cross node weights (layers.py:125-138 folded): per (node, row), heads h:
+//   S^h = softmax_j(q_i,h . k_j,h / sqrt(dh)),  s_i = sum_h sum_j S^h_ij u_jh,
+//   p2 = softmax_i(s),  w_jh = sum_i p2_i S^h_ij        (ctx_h = sum_j w_jh V_j,h)
+struct FullCrossArgs {
+  int n_nodes, R, D, H, max_g;
+  const int* node_first;
+  const int* node_g;
+  const __nv_bfloat16* QK;     // child j row r: q at QK + j*sQj + r*ldq, k at + D
+  long long sQj, ldq;
+  const float* u;              // child j row r: u at u + j*sUj + r*H  (V_j,h . (wo rq)_h / sqrt D)
+  long long sUj;
+  float* w;                    // [n][R][max_g][H]
+};
+cudaError_t launch_fullcross_weights(const FullCrossArgs& a, cudaStream_t st);
 
 // Backward of the combine: dL, gV (and dmix for linear nodes) from g = dLoss/dctx
 struct CombineBwdArgs {

@@ -174,6 +174,10 @@ class DchagFrontEnd(torch.nn.Module):
 
     def prepare(self):
         """Fold + pack the weights for the kernels (cached until weights change)."""
+        if self._full_cross():
+            if not self.weights:
+                raise RuntimeError("no weights loaded")
+            return None  # the full_cross path reads the reference weights directly
         if self._packed is None:
             if not self.weights:
                 raise RuntimeError("no weights loaded")
@@ -187,6 +191,40 @@ class DchagFrontEnd(torch.nn.Module):
         return self._packed
 
     # ------------------------------------------------------------------ forward
+    def _full_cross(self):
+        return self.model.agg_variant == "full_cross"
+
+    def _forward_full_cross(self, images, out=None):
+        """agg_variant='full_cross' (layers.py:125-138): the tokens are materialised
+        (ops.tokenize_channels), each rank aggregates its slab with full_cross tree nodes
+        (ops.tree_aggregate), the [B,1,S,D] root streams are all-gathered in rank order and the
+        shared final node runs over them (model.py:180-201 / strategies.py:199-218)."""
+        from . import ops
+        w = self.weights
+        m = self.model
+        off, cnt = self.slab
+        sl = slice(off, off + cnt)
+        tok = ops.tokenize_channels(images, w["tok.w"][sl], w["tok.b"][sl],
+                                    w["special.channel_id"][sl], w["special.pos"], m.patch,
+                                    out_dtype=torch.bfloat16)
+        y = ops.tree_aggregate(tok, self.tree, w, f"agg.slab{self.rank}",
+                               self.strategy.agg_layer_kind, "full_cross", m.heads,
+                               out_dtype=torch.bfloat16)                       # [B,1,S,D]
+        if self.tp > 1:
+            import torch.distributed as dist
+            y = y.contiguous()
+            allg = torch.empty((self.tp,) + tuple(y.shape), device=y.device, dtype=y.dtype)
+            dist.all_gather_into_tensor(allg, y, group=self.process_group)
+            gathered = allg.squeeze(2).permute(1, 0, 2, 3)                     # [B,tp,S,D]
+        else:
+            gathered = y
+        res = ops.flat_aggregate(gathered, w, "agg.final", "full_cross", m.heads,
+                                 out_dtype=self.out_dtype)
+        if out is not None:
+            out.copy_(res)
+            return out
+        return res
+
     def forward(self, images: torch.Tensor, return_payload: bool = False, out=None,
                 h2d_chunks: int = 4):
         """[B, C or slab, H, W] images -> [B, 1, S, D] (model.py:180-201 front end).
@@ -213,6 +251,10 @@ class DchagFrontEnd(torch.nn.Module):
                                 or out.dtype != self.out_dtype or not out.is_contiguous()):
             raise ConfigError(f"out must be a contiguous {self.out_dtype} tensor of shape "
                               f"{(b, 1, self.seq, m.embed)}")
+        if self._full_cross():
+            if not images.is_cuda or return_payload:
+                raise ConfigError("agg_variant='full_cross' takes device images")
+            return self._forward_full_cross(images, out)
         if not images.is_cuda:
             if return_payload:
                 raise ConfigError("return_payload needs device images")

@@ -71,12 +71,75 @@ def tokenize_channels(images, tok_w, tok_b, chan_id, pos, patch, out_dtype=torch
     return out
 
 
+def _full_cross_tree(tokens, spec: TreeSpec, w, prefix, n_heads, out_dtype):
+    """full_cross nodes (layers.py:125-138): per node, the g children attend over each other
+    (sdp_attention, layers.py:49-64), then a learned query rq reduces the g outputs. Folded:
+    one projection GEMM per node gives [q | k | v | u] with u_jh = v_j,h . (wo rq)_h / sqrt(D)
+    (the reduce's scores are linear in the attention outputs); dchag_fullcross_weights turns
+    q, k, u into per-(child, head) weights w; dchag_combine_weighted sums the v rows; the
+    node output is that sum @ wo + bo (exact: the reduce's softmax weights sum to 1)."""
+    B, C, S, D = tokens.shape
+    H = n_heads
+    R = B * S
+    st = _lib.stream_handle()
+    tw = {k: _f32(v) for k, v in w.items() if k.startswith(prefix + ".")}
+    # node-major rows: x[j] is child j's [R, D]
+    x = _bf(tokens).permute(1, 0, 2, 3).reshape(C, R, D).contiguous()
+    depth = len(spec.levels)
+    dh = D // H
+    for li, level in enumerate(spec.levels):
+        n_in = x.shape[0]
+        firsts, acc = [], 0
+        for g in level:
+            firsts.append(acc)
+            acc += g
+        QKV = torch.empty(n_in, R, 3 * D, device="cuda", dtype=torch.bfloat16)
+        U = torch.empty(n_in, R, H, device="cuda", dtype=torch.float32)
+        nodes = [f"{prefix}.l{li}.g{gi}" for gi in range(len(level))]
+        for node, f, g in zip(nodes, firsts, level):
+            wr = tw[f"{node}.wo"] @ tw[f"{node}.rq"] / (D ** 0.5)                    # [D]
+            Wu = (tw[f"{node}.wv"].view(D, H, dh) * wr.view(1, H, dh)).sum(-1)        # [D, H]
+            Wc = torch.cat([tw[f"{node}.wq"], tw[f"{node}.wk"], tw[f"{node}.wv"], Wu], dim=1)
+            Wnk = _bf(Wc.t())
+            zero = torch.zeros(Wnk.shape[0], device="cuda", dtype=torch.float32)
+            _gemm(x[f:f + g], 1, g * R, D, 0, D, Wnk, zero, QKV[f:f + g], 0, 3 * D,
+                  U[f:f + g], 0, H)
+        first_t = torch.tensor(firsts, device="cuda", dtype=torch.int32)
+        g_t = torch.tensor(list(level), device="cuda", dtype=torch.int32)
+        gmax = max(level)
+        wts = torch.empty(len(level), R, gmax, H, device="cuda", dtype=torch.float32)
+        _lib.call("dchag_fullcross_weights", len(level), R, D, H, _lib.ptr(first_t),
+                  _lib.ptr(g_t), gmax, _lib.ptr(QKV), R * 3 * D, 3 * D, _lib.ptr(U), R * H,
+                  _lib.ptr(wts), st)
+        ctx = torch.empty(len(level), R, D, device="cuda", dtype=torch.bfloat16)
+        _lib.call("dchag_combine_weighted", len(level), R, D, H, _lib.ptr(first_t),
+                  _lib.ptr(g_t), gmax, _lib.ptr(QKV[:, :, 2 * D:]), R * 3 * D, 3 * D,
+                  _lib.ptr(wts), _lib.ptr(ctx), st)
+        last = li == depth - 1
+        y = torch.empty(len(level), R, D, device="cuda",
+                        dtype=out_dtype if last else torch.bfloat16)
+        for k, node in enumerate(nodes):
+            Wo = _bf(tw[f"{node}.wo"].t())
+            _gemm(ctx[k], 1, R, D, 0, D, Wo, tw[f"{node}.bo"].contiguous(), y[k], 0, D,
+                  outV_f32=y.dtype == torch.float32)
+        x = y
+    return x.view(B, 1, S, D) if x.shape[0] == 1 else x.view(1, B, S, D).transpose(0, 1)
+
+
 def tree_aggregate(tokens, spec: TreeSpec, w, prefix, layer_kind, variant, n_heads,
                    out_dtype=torch.float32):
     """[B, C, S, D] -> [B, 1, S, D] (model.py:76-97): contiguous groups per level, node
     params under {prefix}.l{level}.g{group}."""
+    if variant == "full_cross" and layer_kind != "linear":
+        if sum(spec.levels[0]) != tokens.shape[1]:
+            raise ConfigError(
+                f"tree level 0 partitions {sum(spec.levels[0])} channels, input has "
+                f"{tokens.shape[1]}")
+        if max(max(lv) for lv in spec.levels) > 32:
+            raise ConfigError("full_cross on sm_100a supports groups of <= 32 channels")
+        return _full_cross_tree(tokens, spec, w, prefix, n_heads, out_dtype)
     if variant != "single_query" and layer_kind != "linear":
-        raise ConfigError("tree_aggregate on sm_100a implements agg_variant='single_query'")
+        raise ConfigError(f"unknown agg_variant {variant!r}")
     B, C, S, D = tokens.shape
     if sum(spec.levels[0]) != C:
         raise ConfigError(

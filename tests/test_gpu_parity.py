@@ -261,3 +261,58 @@ def test_l0_logits_normalised_and_unnormalised_agree(P, W):
         e = pe[o:o + g * R * h].view(g, R, h).float() * inv[n][None]
         assert torch.allclose(a.sum(0), torch.ones(R, h, device="cuda"), atol=2e-2)
         assert (a - e).abs().max().item() < 8e-3
+
+
+# ------------------------------------------------------------ agg_variant = full_cross (a9)
+FC_CONFIGS = [
+    dict(channels=8, image_h=64, image_w=64, patch=4, embed=128, heads=2, tp=1, max_group=4),
+    dict(channels=12, image_h=64, image_w=128, patch=8, embed=256, heads=4, tp=1, max_group=6),
+    dict(channels=13, image_h=64, image_w=64, patch=4, embed=128, heads=2, tp=2, max_group=3),
+    dict(channels=10, image_h=64, image_w=128, patch=8, embed=256, heads=4, tp=1, max_group=4,
+         layer_kind="linear"),
+]
+
+
+@pytest.mark.parametrize("meta", FC_CONFIGS, ids=lambda m: "C{channels}D{embed}tp{tp}g{max_group}".format(**m) + m.get("layer_kind", ""))
+def test_full_cross_matches_oracle(meta):
+    """full_cross nodes (layers.py:125-138) through the functional mirrors: per-slab tokenize
+    + tree, streams concatenated in rank order, final full_cross node; and the module path at
+    tp = 1."""
+    from paper_2506_21411_b200 import DchagFrontEnd, ops
+    from paper_2506_21411_b200.config import build_tree_spec, channel_slabs
+    lk = meta.get("layer_kind", "cross_attention")
+    specs = O.frontend_param_specs(meta["channels"], meta["image_h"], meta["image_w"],
+                                   meta["patch"], meta["embed"], meta["tp"], meta["max_group"],
+                                   variant="full_cross", layer_kind=lk)
+    w = O.random_params(specs, seed=11, std=0.05, bias_std=0.02)
+    w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
+    rng = np.random.default_rng(4)
+    images = rng.standard_normal((2, meta["channels"], meta["image_h"], meta["image_w"]))
+    images = _bf(images).float().numpy().astype(np.float64)
+    want = O.dchag_frontend(images, w, patch=meta["patch"], heads=meta["heads"], tp=meta["tp"],
+                            max_group=meta["max_group"], variant="full_cross", layer_kind=lk)
+    wt = {k: torch.tensor(v, dtype=torch.float32, device="cuda") for k, v in w.items()}
+    img = torch.tensor(images, dtype=torch.float32, device="cuda")
+    streams = []
+    for r, (off, cnt) in enumerate(channel_slabs(meta["channels"], meta["tp"])):
+        tok = ops.tokenize_channels(img[:, off:off + cnt], wt["tok.w"][off:off + cnt],
+                                    wt["tok.b"][off:off + cnt],
+                                    wt["special.channel_id"][off:off + cnt], wt["special.pos"],
+                                    meta["patch"], out_dtype=torch.bfloat16)
+        streams.append(ops.tree_aggregate(tok, build_tree_spec(cnt, meta["max_group"]), wt,
+                                          f"agg.slab{r}", lk, "full_cross", meta["heads"],
+                                          out_dtype=torch.bfloat16))
+    out = ops.flat_aggregate(torch.cat(streams, dim=1), wt, "agg.final", "full_cross",
+                             meta["heads"])
+    torch.cuda.synchronize()
+    err = rel_err(out.float().cpu().numpy(), want)
+    assert err < BF16_TOL, err
+    if meta["tp"] == 1:
+        fe = DchagFrontEnd(meta["channels"], meta["image_h"], meta["image_w"], meta["patch"],
+                           meta["embed"], meta["heads"], max_group=meta["max_group"],
+                           agg_variant="full_cross", agg_layer_kind=lk, out_dtype=torch.float32)
+        fe.load_weights(w)
+        y = fe(img.to(torch.bfloat16))
+        torch.cuda.synchronize()
+        err2 = rel_err(y.float().cpu().numpy(), want)
+        assert err2 < BF16_TOL, err2
