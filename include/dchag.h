@@ -78,6 +78,12 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
                   const void* Mt, int C_pad, const void* Et, int KE, const void* posV, void* ctx,
                   void* stream);
 
+/* fp32 parity mode combine: as dchag_combine with fp32 child values V (row r of child j at
+ * V + j*sVj + r*D) and an fp32 context (precise expf, fp32 accumulation). */
+int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
+                      int max_g, const float* V, long long sVj, const float* L, long long sLj,
+                      const float* mix, float* ctx, void* stream);
+
 /* full_cross node weights (layers.py:125-138 with sdp_attention layers.py:49-64): per node
  * and row, with q/k of child j at QK + j*sQj + r*ldq (k at +D, bf16) and u_jh = V_j,h .
  * (wo rq)_h / sqrt(D) at u + j*sUj + r*H (fp32):  S^h = softmax_j(q_i,h . k_j,h / sqrt(dh)),

@@ -268,6 +268,17 @@ int dchag_combine_strided(int n_nodes, int R, int D, int H, const int* node_firs
   return cuda_status(launch_combine(a, S(stream)), "combine");
 }
 
+int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
+                      int max_g, const float* V, long long sVj, const float* L, long long sLj,
+                      const float* mix, float* ctx, void* stream) {
+  if (!mix && !L) return fail(DCHAG_ERR_SHAPE, "combine_f32: need logits or mix");
+  CombineF32Args a;
+  a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H; a.max_g = max_g;
+  a.node_first = node_first; a.node_g = node_g;
+  a.V = V; a.sVj = sVj; a.L = L; a.sLj = sLj; a.mix = mix; a.ctx = ctx;
+  return cuda_status(launch_combine_f32(a, S(stream)), "combine_f32");
+}
+
 int dchag_fullcross_weights(int n_nodes, int R, int D, int H, const int* node_first,
                             const int* node_g, int max_g, const void* QK, long long sQj,
                             long long ldq, const float* u, long long sUj, float* w, void* stream) {

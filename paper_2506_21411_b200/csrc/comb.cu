@@ -131,6 +131,51 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// fp32 combine for the fp32 parity mode: ctx[n][r][:] = sum_j w_j(r,h) V_j[r][:] with fp32 V,
+// logits / mix as in combine_kernel. One warp per (node, row); lanes over columns.
+__global__ void __launch_bounds__(256) combine_f32_kernel(CombineF32Args a) {
+  __shared__ float sp[8][COMB_PTAB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long item = (long long)blockIdx.x * 8 + warp;
+  const int n = (int)(item / a.R);
+  const int r = (int)(item - (long long)n * a.R);
+  if (n >= a.n_nodes) return;
+  const int first = __ldg(a.node_first + n), g = __ldg(a.node_g + n);
+  const int H = a.H, dh = a.D / H;
+  float* p = sp[warp];
+  if (a.mix) {
+    for (int j = lane; j < g; j += 32) p[j] = __ldg(a.mix + first + j);
+  } else if (lane < H) {
+    const float* lr = a.L + (long long)first * a.sLj + (long long)r * H + lane;
+    float m = -INFINITY;
+    for (int j = 0; j < g; ++j) m = fmaxf(m, __ldg(lr + (long long)j * a.sLj));
+    float ssum = 0.f;
+    for (int j = 0; j < g; ++j) {
+      const float e = expf(__ldg(lr + (long long)j * a.sLj) - m);
+      p[j * H + lane] = e;
+      ssum += e;
+    }
+    for (int j = 0; j < g; ++j) p[j * H + lane] /= ssum;
+  }
+  __syncwarp();
+  for (int c = lane; c < a.D; c += 32) {
+    const int h = c / dh;
+    float acc = 0.f;
+    for (int j = 0; j < g; ++j)
+      acc += (a.mix ? p[j] : p[j * H + h]) *
+             __ldg(a.V + (long long)(first + j) * a.sVj + (long long)r * a.D + c);
+    a.ctx[((long long)n * a.R + r) * a.D + c] = acc;
+  }
+}
+
+cudaError_t launch_combine_f32(const CombineF32Args& a, cudaStream_t st) {
+  if (a.H > COMB_MAXH || a.max_g * (a.mix ? 1 : a.H) > COMB_PTAB || a.D % a.H)
+    return cudaErrorInvalidValue;
+  const long long items = (long long)a.n_nodes * a.R;
+  combine_f32_kernel<<<(unsigned)((items + 7) / 8), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 // full_cross node weights (see FullCrossArgs). One CTA per (node, row), one warp per head;
 // lane j owns child j (g <= 32): it keeps k_j,h in registers and computes the row of logits
 // L_ij = q_i . k_j / sqrt(dh) against q_i broadcast from shared memory; the per-i softmax,

@@ -96,6 +96,20 @@ struct CombineArgs {
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
 
+// fp32 combine (fp32 parity mode): V, L, ctx fp32; rows contiguous (child j row r at j*sVj + r*D)
+struct CombineF32Args {
+  int n_nodes, R, D, H, max_g;
+  const int* node_first;
+  const int* node_g;
+  const float* V;
+  long long sVj;
+  const float* L;
+  long long sLj;
+  const float* mix;
+  float* ctx;
+};
+cudaError_t launch_combine_f32(const CombineF32Args& a, cudaStream_t st);
+
 // full_cross node weights (layers.py:125-138 folded): per (node, row), heads h:
 //   S^h = softmax_j(q_i,h . k_j,h / sqrt(dh)),  s_i = sum_h sum_j S^h_ij u_jh,
 //   p2 = softmax_i(s),  w_jh = sum_i p2_i S^h_ij        (ctx_h = sum_j w_jh V_j,h)

@@ -62,7 +62,8 @@ class DchagFrontEnd(torch.nn.Module):
                  heads: int, max_group: int | None = None, depth: int | None = None,
                  agg_variant: str = "single_query", agg_layer_kind: str = "cross_attention",
                  tp: int = 1, rank: int = 0, final_layer_tp_split: bool = False,
-                 process_group=None, out_dtype=torch.bfloat16, device=None):
+                 process_group=None, out_dtype=torch.bfloat16, device=None,
+                 precision: str = "bf16"):
         super().__init__()
         self.model = ModelConfig(channels=channels, image_h=image_h, image_w=image_w,
                                  patch=patch, embed=embed, heads=heads,
@@ -92,6 +93,13 @@ class DchagFrontEnd(torch.nn.Module):
         self.tree: TreeSpec = trees[rank]
         self.process_group = process_group
         self.out_dtype = out_dtype
+        if precision not in ("bf16", "fp32"):
+            raise ConfigError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
+        if precision == "fp32" and agg_variant != "single_query":
+            raise ConfigError("the fp32 parity mode implements agg_variant='single_query'")
+        # "fp32": parity mode, results within 1e-4 of the float64 reference (BASELINE.json);
+        # "bf16": the throughput path (bf16 operands, fp32 accumulation, within 2e-2)
+        self.precision = precision
         self.device = torch.device(device) if device is not None else (
             torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
             else torch.device("cpu"))
@@ -174,10 +182,10 @@ class DchagFrontEnd(torch.nn.Module):
 
     def prepare(self):
         """Fold + pack the weights for the kernels (cached until weights change)."""
-        if self._full_cross():
+        if self._unfolded():
             if not self.weights:
                 raise RuntimeError("no weights loaded")
-            return None  # the full_cross path reads the reference weights directly
+            return None  # full_cross / fp32 run the unfolded ops path on the reference weights
         if self._packed is None:
             if not self.weights:
                 raise RuntimeError("no weights loaded")
@@ -191,8 +199,8 @@ class DchagFrontEnd(torch.nn.Module):
         return self._packed
 
     # ------------------------------------------------------------------ forward
-    def _full_cross(self):
-        return self.model.agg_variant == "full_cross"
+    def _unfolded(self):
+        return self.model.agg_variant == "full_cross" or self.precision == "fp32"
 
     def _forward_full_cross(self, images, out=None):
         """agg_variant='full_cross' (layers.py:125-138): the tokens are materialised
@@ -204,6 +212,8 @@ class DchagFrontEnd(torch.nn.Module):
         m = self.model
         off, cnt = self.slab
         sl = slice(off, off + cnt)
+        if self.precision == "fp32":
+            return self._forward_fp32(images, out)
         tok = ops.tokenize_channels(images, w["tok.w"][sl], w["tok.b"][sl],
                                     w["special.channel_id"][sl], w["special.pos"], m.patch,
                                     out_dtype=torch.bfloat16)
@@ -220,6 +230,31 @@ class DchagFrontEnd(torch.nn.Module):
             gathered = y
         res = ops.flat_aggregate(gathered, w, "agg.final", "full_cross", m.heads,
                                  out_dtype=self.out_dtype)
+        if out is not None:
+            out.copy_(res)
+            return out
+        return res
+
+    def _forward_fp32(self, images, out=None):
+        """fp32 parity mode (results within 1e-4 of the float64 reference): tokens, tree and
+        final layer with fp32-accurate split-bf16 GEMMs and fp32 combines (ops.*_fp32)."""
+        from . import ops
+        w = self.weights
+        m = self.model
+        off, cnt = self.slab
+        sl = slice(off, off + cnt)
+        tok = ops.tokenize_channels_fp32(images.float(), w["tok.w"][sl], w["tok.b"][sl],
+                                         w["special.channel_id"][sl], w["special.pos"], m.patch)
+        y = ops.tree_aggregate_fp32(tok, self.tree, w, f"agg.slab{self.rank}",
+                                    self.strategy.agg_layer_kind, m.heads).contiguous()
+        if self.tp > 1:
+            import torch.distributed as dist
+            allg = torch.empty((self.tp,) + tuple(y.shape), device=y.device, dtype=y.dtype)
+            dist.all_gather_into_tensor(allg, y, group=self.process_group)
+            gathered = allg.squeeze(2).permute(1, 0, 2, 3)
+        else:
+            gathered = y
+        res = ops.flat_aggregate_fp32(gathered, w, "agg.final", m.heads).to(self.out_dtype)
         if out is not None:
             out.copy_(res)
             return out
@@ -251,7 +286,7 @@ class DchagFrontEnd(torch.nn.Module):
                                 or out.dtype != self.out_dtype or not out.is_contiguous()):
             raise ConfigError(f"out must be a contiguous {self.out_dtype} tensor of shape "
                               f"{(b, 1, self.seq, m.embed)}")
-        if self._full_cross():
+        if self._unfolded():
             if not images.is_cuda or return_payload:
                 raise ConfigError("agg_variant='full_cross' takes device images")
             return self._forward_full_cross(images, out)

@@ -316,3 +316,54 @@ def test_full_cross_matches_oracle(meta):
         torch.cuda.synchronize()
         err2 = rel_err(y.float().cpu().numpy(), want)
         assert err2 < BF16_TOL, err2
+
+
+# ------------------------------------------------------------ fp32 parity mode (<= 1e-4)
+FP32_TOL = 1e-4
+
+
+@pytest.mark.parametrize("case", ["T_sq_tp1", "T_sq_tp2"])
+def test_fp32_mode_matches_reference_golden(case):
+    """precision='fp32': split-bf16 tcgen05 GEMMs + fp32 combines reproduce the reference's
+    float64 output within the fp32 tolerance of BASELINE.json (max rel err <= 1e-4)."""
+    from paper_2506_21411_b200 import ops
+    from paper_2506_21411_b200.config import build_tree_spec, channel_slabs
+    meta, z, w, _ = load_golden(case)
+    wt = {k: torch.tensor(v, dtype=torch.float32, device="cuda") for k, v in w.items()}
+    img = torch.tensor(z["images"], dtype=torch.float32, device="cuda")
+    streams = []
+    for r, (off, cnt) in enumerate(channel_slabs(meta["channels"], meta["tp"])):
+        tok = ops.tokenize_channels_fp32(img[:, off:off + cnt], wt["tok.w"][off:off + cnt],
+                                         wt["tok.b"][off:off + cnt],
+                                         wt["special.channel_id"][off:off + cnt],
+                                         wt["special.pos"], meta["patch"])
+        streams.append(ops.tree_aggregate_fp32(tok, build_tree_spec(cnt, meta["max_group"]), wt,
+                                               f"agg.slab{r}", "cross_attention", meta["heads"]))
+    out = ops.flat_aggregate_fp32(torch.cat(streams, dim=1), wt, "agg.final", meta["heads"])
+    torch.cuda.synchronize()
+    err = rel_err(out.cpu().numpy(), z["out"])
+    assert err < FP32_TOL, err
+
+
+@pytest.mark.parametrize("meta", [CONFIGS[1], CONFIGS[2], CONFIGS[6]],
+                         ids=["C20P8D256", "C20P8D256linear", "C20P8D256dh128"])
+def test_fp32_module_matches_oracle(meta):
+    from paper_2506_21411_b200 import DchagFrontEnd
+    lk = meta.get("layer_kind", "cross_attention")
+    specs = O.frontend_param_specs(meta["channels"], meta["image_h"], meta["image_w"],
+                                   meta["patch"], meta["embed"], 1, meta["max_group"],
+                                   layer_kind=lk)
+    w = O.random_params(specs, seed=5, std=0.05, bias_std=0.02)
+    w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
+    images = np.random.default_rng(2).standard_normal(
+        (2, meta["channels"], meta["image_h"], meta["image_w"])).astype(np.float32)
+    want = O.dchag_frontend(images.astype(np.float64), w, patch=meta["patch"],
+                            heads=meta["heads"], tp=1, max_group=meta["max_group"], layer_kind=lk)
+    fe = DchagFrontEnd(meta["channels"], meta["image_h"], meta["image_w"], meta["patch"],
+                       meta["embed"], meta["heads"], max_group=meta["max_group"],
+                       agg_layer_kind=lk, out_dtype=torch.float32, precision="fp32")
+    fe.load_weights(w)
+    y = fe(torch.from_numpy(images).cuda())
+    torch.cuda.synchronize()
+    err = rel_err(y.cpu().numpy(), want)
+    assert err < FP32_TOL, err
