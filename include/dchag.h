@@ -78,6 +78,16 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
                   const void* Mt, int C_pad, const void* Et, int KE, const void* posV, void* ctx,
                   void* stream);
 
+/* Level-0 node backward, row stage (training; backward of layers.py:103-123 / :141-146 at
+ * tree level 0 with the tokenizer folded): V [g][R][D] bf16 = x_c wv, G [R][D] fp32 =
+ * dLoss/dctx, ctx [R][D] bf16, p = the node's block of the normalised dchag_l0_logits
+ * output ([H/nh][g][R][nh]).  Attention: dl[j][r][h] = p (G_h . V_j,h - G_h . ctx_h),
+ * dV[j][r] = p_jh G_h.  Linear (mix != NULL): dV[j][r] = mix_j G, dm[j][r] = G . V_j[r].
+ * D <= 2048 (a multiple of 256 above 256). */
+int dchag_l0_bwd_rows(int g, int R, int D, int H, int nh, const void* V, const float* G,
+                      const void* ctx, const void* p, const float* mix, float* dl, void* dV,
+                      float* dm, void* stream);
+
 /* fp32 parity mode combine: as dchag_combine with fp32 child values V (row r of child j at
  * V + j*sVj + r*D) and an fp32 context (precise expf, fp32 accumulation). */
 int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,

@@ -268,6 +268,20 @@ int dchag_combine_strided(int n_nodes, int R, int D, int H, const int* node_firs
   return cuda_status(launch_combine(a, S(stream)), "combine");
 }
 
+int dchag_l0_bwd_rows(int g, int R, int D, int H, int nh, const void* V, const float* G,
+                      const void* ctx, const void* p, const float* mix, float* dl, void* dV,
+                      float* dm, void* stream) {
+  if (!mix && (!ctx || !p || !dl)) return fail(DCHAG_ERR_SHAPE, "l0_bwd_rows: attention needs ctx, p, dl");
+  if (mix && !dm) return fail(DCHAG_ERR_SHAPE, "l0_bwd_rows: linear needs dm");
+  L0BwdRowsArgs a;
+  a.g = g; a.R = R; a.D = D; a.H = H; a.NH = nh;
+  a.V = reinterpret_cast<const __nv_bfloat16*>(V); a.G = G;
+  a.ctx = reinterpret_cast<const __nv_bfloat16*>(ctx);
+  a.p = reinterpret_cast<const __nv_bfloat16*>(p); a.mix = mix;
+  a.dl = dl; a.dV = reinterpret_cast<__nv_bfloat16*>(dV); a.dm = dm;
+  return cuda_status(launch_l0_bwd_rows(a, S(stream)), "l0_bwd_rows");
+}
+
 int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
                       int max_g, const float* V, long long sVj, const float* L, long long sLj,
                       const float* mix, float* ctx, void* stream) {

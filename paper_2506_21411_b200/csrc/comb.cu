@@ -176,6 +176,94 @@ cudaError_t launch_combine_f32(const CombineF32Args& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Level-0 node backward, row stage (training; the folded level-0 backward in train.py).
+// One warp per row r of the node: with G = dLoss/dctx[r] and ctx[r] kept in registers, for
+// each channel j of the node:
+//   dp_jh = G_h . V_j,h   (V_j = x_j wv, recomputed by a K = P^2 GEMM)
+//   attention: dl_jh = p_jh (dp_jh - G_h . ctx_h),  dV_j = p_jh G_h   (layers.py:103-123 bwd)
+//   linear:    dV_j = mix_j G,  dm_j[r] = G . V_j                      (layers.py:141-146 bwd)
+// Lanes own 8-column chunks (chunk c = lane + 32 i); a head's chunks are dh/8 adjacent lanes.
+template <int CPL>  // chunks per lane = ceil(D / 256); lanes past D / 8 chunks idle
+__global__ void __launch_bounds__(256) l0_bwd_rows_kernel(L0BwdRowsArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long r = (long long)blockIdx.x * 8 + warp;
+  if (r >= a.R) return;
+  const int D = a.D, H = a.H, dh = D / H, lpg = dh / 8;  // lanes per head group
+  const bool act = lane < D / 8;  // D >= 256 is a multiple of 256: every lane active
+  float gv[CPL][8];
+  float gc[CPL];  // G_h . ctx_h of this lane's head per chunk (after reduction)
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    const int c = act ? lane + 32 * i : 0;
+    const float4 g0 = *reinterpret_cast<const float4*>(a.G + r * D + c * 8);
+    const float4 g1 = *reinterpret_cast<const float4*>(a.G + r * D + c * 8 + 4);
+    gv[i][0] = g0.x; gv[i][1] = g0.y; gv[i][2] = g0.z; gv[i][3] = g0.w;
+    gv[i][4] = g1.x; gv[i][5] = g1.y; gv[i][6] = g1.z; gv[i][7] = g1.w;
+    float s = 0.f;
+    if (!a.mix) {
+      const uint4 cx = *reinterpret_cast<const uint4*>(a.ctx + r * D + c * 8);
+      const uint32_t cw[4] = {cx.x, cx.y, cx.z, cx.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s += gv[i][2 * e] * bf16lo(cw[e]) + gv[i][2 * e + 1] * bf16hi(cw[e]);
+      if (!act) s = 0.f;
+      for (int o = 1; o < lpg; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    }
+    gc[i] = s;
+  }
+  for (int j = 0; j < a.g; ++j) {
+    const __nv_bfloat16* vr = a.V + ((long long)j * a.R + r) * D;
+    __nv_bfloat16* dvr = a.dV + ((long long)j * a.R + r) * D;
+    float dmr = 0.f;
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const int c = act ? lane + 32 * i : 0;
+      const int h = (c * 8) / dh;
+      const uint4 vx = *reinterpret_cast<const uint4*>(vr + c * 8);
+      const uint32_t vw[4] = {vx.x, vx.y, vx.z, vx.w};
+      float dp = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dp += gv[i][2 * e] * bf16lo(vw[e]) + gv[i][2 * e + 1] * bf16hi(vw[e]);
+      if (!act) dp = 0.f;
+      float pj;
+      if (a.mix) {
+        dmr += dp;
+        pj = a.mix[j];
+      } else {
+        for (int o = 1; o < lpg; o <<= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
+        pj = __bfloat162float(a.p[(((long long)(h / a.NH) * a.g + j) * a.R + r) * a.NH + h % a.NH]);
+        if (act && (lane % lpg) == 0) a.dl[((long long)j * a.R + r) * H + h] = pj * (dp - gc[i]);
+      }
+      uint4 o;
+      o.x = pack_bf16(pj * gv[i][0], pj * gv[i][1]);
+      o.y = pack_bf16(pj * gv[i][2], pj * gv[i][3]);
+      o.z = pack_bf16(pj * gv[i][4], pj * gv[i][5]);
+      o.w = pack_bf16(pj * gv[i][6], pj * gv[i][7]);
+      if (act) *reinterpret_cast<uint4*>(dvr + c * 8) = o;
+    }
+    if (a.mix) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) dmr += __shfl_xor_sync(0xffffffffu, dmr, o);
+      if (lane == 0) a.dm[(long long)j * a.R + r] = dmr;
+    }
+  }
+}
+
+cudaError_t launch_l0_bwd_rows(const L0BwdRowsArgs& a, cudaStream_t st) {
+  const int dh = a.D / a.H;
+  if ((a.D > 256 ? a.D % 256 : a.D % 8) || a.D > 2048 || dh % 8 || dh / 8 > 32 ||
+      32 % (dh / 8))
+    return cudaErrorInvalidValue;
+  const int grid = (a.R + 7) / 8;
+  switch ((a.D + 255) / 256) {
+    case 1: l0_bwd_rows_kernel<1><<<grid, 256, 0, st>>>(a); break;
+    case 2: l0_bwd_rows_kernel<2><<<grid, 256, 0, st>>>(a); break;
+    case 4: l0_bwd_rows_kernel<4><<<grid, 256, 0, st>>>(a); break;
+    case 8: l0_bwd_rows_kernel<8><<<grid, 256, 0, st>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 // full_cross node weights (see FullCrossArgs). One CTA per (node, row), one warp per head;
 // lane j owns child j (g <= 32): it keeps k_j,h in registers and computes the row of logits
 // L_ij = q_i . k_j / sqrt(dh) against q_i broadcast from shared memory; the per-i softmax,

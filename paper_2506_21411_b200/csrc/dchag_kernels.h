@@ -110,6 +110,20 @@ struct CombineF32Args {
 };
 cudaError_t launch_combine_f32(const CombineF32Args& a, cudaStream_t st);
 
+// Level-0 node backward, row stage (see comb.cu)
+struct L0BwdRowsArgs {
+  int g, R, D, H, NH;
+  const __nv_bfloat16* V;      // [g][R][D] child values x_c wv
+  const float* G;              // [R][D] dLoss/dctx
+  const __nv_bfloat16* ctx;    // [R][D] the node's context (attention)
+  const __nv_bfloat16* p;      // node block of the K_p0 layout [H/NH][g][R][NH] (attention)
+  const float* mix;            // [g] (linear) or null
+  float* dl;                   // [g][R][H] (attention)
+  __nv_bfloat16* dV;           // [g][R][D]
+  float* dm;                   // [g][R] (linear)
+};
+cudaError_t launch_l0_bwd_rows(const L0BwdRowsArgs& a, cudaStream_t st);
+
 // full_cross node weights (layers.py:125-138 folded): per (node, row), heads h:
 //   S^h = softmax_j(q_i,h . k_j,h / sqrt(dh)),  s_i = sum_h sum_j S^h_ij u_jh,
 //   p2 = softmax_i(s),  w_jh = sum_i p2_i S^h_ij        (ctx_h = sum_j w_jh V_j,h)

@@ -406,55 +406,103 @@ class DchagTrainer:
                     grads[f"{node}.mix"] = dm[f0:f0 + g].sum(1)
                     g_prev[f0:f0 + g] = _mm(gv, w[f"{node}.w"].t()).view(g, R, d)
             g_y = g_prev
-        # ---- level 0: node output, then tokens recomputed node by node
+        # ---- level 0, folded: tokens are never formed (their gradient neither). With
+        # x_c = patch_c W_c + b_c + pos (model.py:51-64) and V_c = x_c wv, per node:
+        #   V_c = patch_c (W_c wv) + b_c wv + pos wv     (K = P^2 GEMM per channel, tcgen05)
+        #   dV_c = p_c * G (per head),  dp_c = G . V_c (per head),  dl_c = p_c (dp_c - G . ctx)
+        #   T_c = patch_c^T dV_c  (P^2 x D),  E_c = patch_c^T dl_c  (P^2 x H)
+        #   d wv = sum_c W_c^T T_c + b_c^T colsum(dV_c) + pos^T sum_b G
+        #   d U  = sum_c W_c^T E_c + b_c^T colsum(dl_c)               (sum_c dl_c = 0)
+        #   d W_c = T_c wv^T + E_c U^T,  d b_c = colsum(dV_c) wv^T + colsum(dl_c) U^T
+        #   d pos[s] = sum_b G[b, s] wv^T
+        # (linear nodes: p_c = mix_c, no dl, d mix_c = sum_r G . V_c)
         off, cnt = fe.slab
         img = saved["img"]
         ctx0 = saved["ctx"][0]
         pos = w["special.pos"]
-        tokw = w["tok.w"][off:off + cnt]
-        tb = (w["tok.b"] + w["special.channel_id"])[off:off + cnt]
+        tokw = w["tok.w"][off:off + cnt]                                # [cnt, PP, D]
+        tb = (w["tok.b"] + w["special.channel_id"])[off:off + cnt]      # [cnt, D]
+        pp = P * P
         d_tokw = torch.zeros_like(tokw)
         d_tb = torch.zeros_like(tb)
         d_pos = torch.zeros_like(pos)
-        patches = torch.empty(B, cnt, s, P * P, device=img.device, dtype=torch.bfloat16)
+        patches = torch.empty(B, cnt, s, pp, device=img.device, dtype=torch.bfloat16)
         _lib.call("dchag_unfold", _lib.ptr(img), img.stride(0), img.stride(1), B, cnt, m.image_h,
                   m.image_w, P, _lib.ptr(patches), _lib.stream_handle())
-        c0 = 0
+        pk = fe.prepare()
+        pnorm = None
+        if attn:  # normalised level-0 softmax (K_p0, no pinv), layout [node][hg][g][R][NH]
+            poff, acc = [], 0
+            for g in pk.l0_g_list:
+                poff.append(acc)
+                acc += g * R * h
+            poff_t = torch.tensor(poff, device=img.device, dtype=torch.int64)
+            pnorm = torch.empty(acc, device=img.device, dtype=torch.bfloat16)
+            _lib.call("dchag_l0_logits", _lib.ptr(img), img.stride(0), img.stride(1), B,
+                      m.image_h, m.image_w, P, h, pk.HP, pk.NH, pk.n0, max(pk.l0_g_list),
+                      _lib.ptr(pk.l0_c0), _lib.ptr(pk.l0_g), _lib.ptr(poff_t), _lib.ptr(pk.WUt),
+                      _lib.ptr(pk.bU), _lib.ptr(pk.posU), _lib.ptr(pnorm), 0,
+                      _lib.stream_handle())
+        dh = d // h
+        c0, p_at = 0, 0
         for gi, g in enumerate(levels[0]):
             node = f"{pre}.l0.g{gi}"
+            Wv = w[f"{node}.wv"] if attn else w[f"{node}.w"]
             if attn:
                 grads[f"{node}.bo"] = g_y[gi].sum(0)
                 grads[f"{node}.wo"] = _mm(ctx0[gi].t(), g_y[gi])
-                G = _mm(g_y[gi], w[f"{node}.wo"].t()).view(1, R, d)
+                G = _mm(g_y[gi], w[f"{node}.wo"].t())                   # [R, D] fp32
             else:
                 grads[f"{node}.b"] = g_y[gi].sum(0)
-                G = g_y[gi].view(1, R, d)
-            # tokens of this node's channels, channel-major [g][R][D] (tcgen05 tokenizer GEMM)
-            X = self._tokens(patches, c0, g, B)
-            Xf = X.reshape(g * R, d)
+                G = _f32(g_y[gi])
+            Gb = G.to(torch.bfloat16)
+            # V_c for the node's channels [g][R][D] (bf16): K = P^2 tcgen05 GEMM
+            Wc = tokw[c0:c0 + g]                                        # [g, PP, D]
+            Mt = _bf(_mm(Wc.reshape(g * pp, d), Wv).view(g, pp, d).transpose(1, 2))  # [g, D, PP]
+            Cb = _mm(tb[c0:c0 + g], Wv).contiguous()                   # [g, D]
+            posV = _bf(_mm(pos, Wv))                                   # [S, D]
+            V = torch.empty(g, R, d, device=img.device, dtype=torch.bfloat16)
+            A = patches[:, c0:c0 + g]
+            _lib.call("dchag_gemm_bf16", _lib.ptr(A), g, B, s, pp, s * pp, cnt * s * pp, pp,
+                      _lib.ptr(Mt), d, d * pp, d, _lib.ptr(Cb), d, _lib.ptr(posV), 0, d, s,
+                      _lib.ptr(V), 0, R * d, s * d, d, 0, 0, 0, 0, _lib.stream_handle())
+            # row stage (one fused kernel): dp, dl, dV = p G  (or mix G and d mix)
+            dV = torch.empty(g, R, d, device=img.device, dtype=torch.bfloat16)
+            Gc = G.contiguous()
+            if attn:
+                pblk = pnorm[p_at:p_at + g * R * h]
+                p_at += g * R * h
+                dl = torch.empty(g, R, h, device=img.device, dtype=torch.float32)
+                _lib.call("dchag_l0_bwd_rows", g, R, d, h, pk.NH, _lib.ptr(V), _lib.ptr(Gc),
+                          _lib.ptr(ctx0[gi]), _lib.ptr(pblk), 0, _lib.ptr(dl), _lib.ptr(dV), 0,
+                          _lib.stream_handle())
+            else:
+                mixv = w[f"{node}.mix"].float().contiguous()
+                dm = torch.empty(g, R, device=img.device, dtype=torch.float32)
+                _lib.call("dchag_l0_bwd_rows", g, R, d, h, 1, _lib.ptr(V), _lib.ptr(Gc), 0, 0,
+                          _lib.ptr(mixv), 0, _lib.ptr(dV), _lib.ptr(dm), _lib.stream_handle())
+                grads[f"{node}.mix"] = dm.sum(1)
+                dl = None
+            pt = patches[:, c0:c0 + g].permute(1, 3, 0, 2).reshape(g, pp, R)   # patch_c^T
+            T = torch.bmm(pt, dV).float()                               # [g, PP, D]
+            colV = dV.sum(1, dtype=torch.float32)                       # [g, D]
+            dWv = _mm(Wc.reshape(g * pp, d).t(), T.reshape(g * pp, d)) + _mm(tb[c0:c0 + g].t(), colV)
+            d_tokw[c0:c0 + g] = _mm(T.reshape(g * pp, d), Wv.t()).view(g, pp, d)
+            d_tb[c0:c0 + g] = _mm(colV, Wv.t())
             if attn:
                 U = query_logit_weights(w, node, h)
-                V, L = _gemm(Xf, torch.cat([w[f"{node}.wv"], U], dim=1), N_logit=h)
-                gV, dL, _ = self._combine_bwd(V.view(g, R, d), L.view(g, R, h).contiguous(), None,
-                                              G, [0], [g], R)
-                gv = gV.reshape(g * R, d)
-                dl = dL.reshape(g * R, h)
-                grads[f"{node}.wv"] = _mm(Xf.t(), gv)
-                grads.update(_u_backward(w, node, _mm(Xf.t(), dl), h))
-                gX = torch.addmm(_mm(dl, U.t()).to(torch.bfloat16), gv, _bf(w[f"{node}.wv"].t()))
-            else:
-                V = _gemm(Xf, w[f"{node}.w"])
-                mix = w[f"{node}.mix"].float().contiguous()
-                gV, _, dm = self._combine_bwd(V.view(g, R, d), None, mix, G, [0], [g], R)
-                gv = gV.reshape(g * R, d)
-                grads[f"{node}.w"] = _mm(Xf.t(), gv)
-                grads[f"{node}.mix"] = dm.sum(1)
-                gX = torch.matmul(gv, _bf(w[f"{node}.w"].t()))
-            gX = gX.view(g, B, s, d)                                     # bf16
-            pt = patches[:, c0:c0 + g].permute(1, 0, 2, 3).reshape(g, B * s, P * P)
-            d_tokw[c0:c0 + g] = torch.bmm(pt.transpose(1, 2), gX.reshape(g, B * s, d)).float()
-            d_tb[c0:c0 + g] = gX.sum((1, 2), dtype=torch.float32)
-            d_pos += gX.sum((0, 1), dtype=torch.float32)
+                E = torch.bmm(pt, dl.to(torch.bfloat16)).float()        # [g, PP, H]
+                coll = dl.sum(1)                                        # [g, H]
+                dU = _mm(Wc.reshape(g * pp, d).t(), E.reshape(g * pp, h)) + tb[c0:c0 + g].t() @ coll
+                grads.update(_u_backward(w, node, dU, h))
+                d_tokw[c0:c0 + g] += _mm(E.reshape(g * pp, h), U.t()).view(g, pp, d)
+                d_tb[c0:c0 + g] += coll @ U.t()
+            # positional term: sum_c dV_c = G (attention, sum_c p = 1) or (sum_c mix_c) G
+            pscale = 1.0 if attn else float(w[f"{node}.mix"].sum())
+            Gs = G.view(B, s, d).sum(0) * pscale
+            d_pos += _mm(Gs, Wv.t())
+            dWv = dWv + _mm(pos.t(), Gs)
+            grads[f"{node}.wv" if attn else f"{node}.w"] = dWv
             c0 += g
         grads["tok.w"] = d_tokw
         grads["tok.b"] = d_tb
