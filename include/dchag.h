@@ -83,7 +83,7 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
  * dLoss/dctx, ctx [R][D] bf16, p = the node's block of the normalised dchag_l0_logits
  * output ([H/nh][g][R][nh]).  Attention: dl[j][r][h] = p (G_h . V_j,h - G_h . ctx_h),
  * dV[j][r] = p_jh G_h.  Linear (mix != NULL): dV[j][r] = mix_j G, dm[j][r] = G . V_j[r].
- * D <= 2048 (a multiple of 256 above 256). */
+ * D: a multiple of 256 above 256 (of 1024 above 1024). */
 int dchag_l0_bwd_rows(int g, int R, int D, int H, int nh, const void* V, const float* G,
                       const void* ctx, const void* p, const float* mix, float* dl, void* dV,
                       float* dm, void* stream);

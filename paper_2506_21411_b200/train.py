@@ -50,7 +50,7 @@ def _gemm(A, W_dn, bias=None, out_f32=False, rowbias=None, period=1, N_logit=0):
     M, K = A.shape
     N = W_dn.shape[1]
     Nv = N - N_logit
-    W = _bf(W_dn.t())
+    W = _bf_t(W_dn)
     b = _f32(bias) if bias is not None else torch.zeros(N, device=A.device)
     V = torch.empty(M, Nv, device=A.device, dtype=torch.float32 if out_f32 else torch.bfloat16)
     L = torch.empty(M, max(N_logit, 1), device=A.device, dtype=torch.float32)
@@ -62,8 +62,44 @@ def _gemm(A, W_dn, bias=None, out_f32=False, rowbias=None, period=1, N_logit=0):
 
 
 def _mm(a, b):
-    """Plain GEMM on tensor cores: bf16 operands, fp32 accumulate (cuBLAS), fp32 result."""
-    return torch.matmul(a.to(torch.bfloat16), b.to(torch.bfloat16)).float()
+    """Plain GEMM on tensor cores: bf16 operands, fp32 accumulate (cuBLAS), fp32 result.
+    bf16 copies of (fp32) weight operands are cached per tensor version."""
+    return torch.matmul(_bfc(a), _bfc(b)).float()
+
+
+_BF_CACHE: dict = {}
+_BF_WEIGHTS: set = set()   # data_ptrs of the module's parameter tensors (DchagTrainer)
+
+
+def _bf_t(w):
+    """Contiguous bf16 transpose of w; cached for the module's parameters (and views of them)."""
+    base = w._base if w._base is not None else w
+    if base.data_ptr() in _BF_WEIGHTS:
+        key = ("T", base.data_ptr(), base._version, w.stride(), w.storage_offset(), tuple(w.shape))
+        v = _BF_CACHE.get(key)
+        if v is None:
+            if len(_BF_CACHE) > 4096:
+                _BF_CACHE.clear()
+            v = _BF_CACHE[key] = _bf(w.t())
+        return v
+    return _bf(w.t())
+
+
+def _bfc(t):
+    """bf16 view of t; the module's fp32 parameters are converted once per version and cached
+    (their .t() / slice views too). Temporaries are never cached (their storage is reused)."""
+    if t.dtype == torch.bfloat16:
+        return t
+    base = t._base if t._base is not None else t
+    if base.data_ptr() in _BF_WEIGHTS and base.numel() >= 4096:
+        key = (base.data_ptr(), base._version, t.stride(), t.storage_offset(), tuple(t.shape))
+        v = _BF_CACHE.get(key)
+        if v is None:
+            if len(_BF_CACHE) > 4096:
+                _BF_CACHE.clear()
+            v = _BF_CACHE[key] = t.to(torch.bfloat16)
+        return v
+    return t.to(torch.bfloat16)
 
 
 def _u_backward(w, prefix, dU, heads):
@@ -152,6 +188,8 @@ class DchagTrainer:
     def forward_train(self, images):
         """Full forward of this rank: slab tree, AllGather of the root streams (rank order,
         runtime.py:259), shared final layer.  Returns ([B,1,S,D] fp32, saved)."""
+        _BF_WEIGHTS.clear()
+        _BF_WEIGHTS.update(v.data_ptr() for v in self.fe.weights.values())
         saved = self.forward_local(images)
         fe = self.fe
         y_root = saved["y_root"]
@@ -255,6 +293,8 @@ class DchagTrainer:
         """Gradients of sum(out * g_out) w.r.t. this rank's parameters (reference names):
         the slab's tok.* / channel_id rows, its agg.slab{r}.*, the replicated agg.final.*,
         and special.pos all-reduced over the tp group."""
+        _BF_WEIGHTS.clear()
+        _BF_WEIGHTS.update(v.data_ptr() for v in self.fe.weights.values())
         grads, g_y = self.backward_final(saved, g_out)
         grads.update(self.backward_local(saved, g_y))
         if self.fe.tp > 1:
@@ -309,7 +349,7 @@ class DchagTrainer:
         ctx_f = saved["ctx_f"][0].float()
         grads["agg.final.bo"] = g_out.sum(0)
         grads["agg.final.wo"] = _mm(ctx_f.t(), g_out)                      # own rows
-        g_ctx = (g_out @ w["agg.final.wo"][cols].t()).view(1, R, -1)
+        g_ctx = _mm(g_out, w["agg.final.wo"][cols].t()).view(1, R, -1)
         gV, dL, _ = self._combine_bwd(saved["Vf"], saved["Lf"], None, g_ctx, [0], [fe.tp], R,
                                       heads=hc)
         y_all = saved["y_all"].reshape(fe.tp * R, d)
@@ -323,7 +363,7 @@ class DchagTrainer:
         dist.all_reduce(q_grad, group=fe.process_group)                   # fanout of q
         grads["agg.final.q"] = q_grad
         U_own = query_logit_weights(w, "agg.final", h)[:, hs]
-        g_part = (gV.float() @ w["agg.final.wv"][:, cols].t() +
+        g_part = (_mm(gV, w["agg.final.wv"][:, cols].t()) +
                   dL @ U_own.t()).contiguous()                            # [tp, R, D]
         g_y = torch.empty(R, d, device=g_out.device, dtype=torch.float32)
         dist.reduce_scatter_tensor(g_y, g_part.view(fe.tp * R, d), group=fe.process_group)
@@ -344,7 +384,7 @@ class DchagTrainer:
         ctx_f = saved["ctx_f"][0].float()
         grads["agg.final.bo"] = g_out.sum(0)
         grads["agg.final.wo"] = _mm(ctx_f.t(), g_out)
-        g_ctx = (g_out @ w["agg.final.wo"].t()).view(1, R, d)
+        g_ctx = _mm(g_out, w["agg.final.wo"].t()).view(1, R, d)
         gV, dL, _ = self._combine_bwd(saved["Vf"], saved["Lf"], None, g_ctx, [0], [fe.tp], R)
         y_all = saved["y_all"].reshape(fe.tp * R, d)
         grads["agg.final.wv"] = _mm(y_all.t(), gV.reshape(fe.tp * R, d))
@@ -352,7 +392,7 @@ class DchagTrainer:
         grads.update(_u_backward(w, "agg.final", dU, h))
         U_f = query_logit_weights(w, "agg.final", h)
         # local slice of the gathered gradient (strategies.py:91-94): no collective
-        g_y = (gV[fe.rank].float() @ w["agg.final.wv"].t() + dL[fe.rank] @ U_f.t()).view(1, R, d)
+        g_y = (_mm(gV[fe.rank], w["agg.final.wv"].t()) + _mm(dL[fe.rank], U_f.t())).view(1, R, d)
         return grads, g_y
 
     def backward_local(self, saved, g_y):
@@ -400,7 +440,7 @@ class DchagTrainer:
                     grads[f"{node}.wv"] = _mm(Y.t(), gv)
                     grads.update(_u_backward(w, node, _mm(Y.t(), dl), h))
                     U = query_logit_weights(w, node, h)
-                    g_prev[f0:f0 + g] = (_mm(gv, w[f"{node}.wv"].t()) + dl @ U.t()).view(g, R, d)
+                    g_prev[f0:f0 + g] = (_mm(gv, w[f"{node}.wv"].t()) + _mm(dl, U.t())).view(g, R, d)
                 else:
                     grads[f"{node}.w"] = _mm(Y.t(), gv)
                     grads[f"{node}.mix"] = dm[f0:f0 + g].sum(1)
@@ -485,7 +525,12 @@ class DchagTrainer:
                 dl = None
             pt = patches[:, c0:c0 + g].permute(1, 3, 0, 2).reshape(g, pp, R)   # patch_c^T
             T = torch.bmm(pt, dV).float()                               # [g, PP, D]
-            colV = dV.sum(1, dtype=torch.float32)                       # [g, D]
+            if attn:  # colsum_r dV_j = sum_r p_jrh G_r (per head): a small GEMM, not a dV pass
+                pj = pblk.view(h // pk.NH, g, R, pk.NH).permute(1, 0, 3, 2).reshape(g, h, R)
+                colV = torch.bmm(pj.permute(1, 0, 2), _bfc(G).view(R, h, dh).permute(1, 0, 2))
+                colV = colV.float().permute(1, 0, 2).reshape(g, d)     # [g, D]
+            else:
+                colV = w[f"{node}.mix"].float().view(g, 1) * G.sum(0).view(1, d)
             dWv = _mm(Wc.reshape(g * pp, d).t(), T.reshape(g * pp, d)) + _mm(tb[c0:c0 + g].t(), colV)
             d_tokw[c0:c0 + g] = _mm(T.reshape(g * pp, d), Wv.t()).view(g, pp, d)
             d_tb[c0:c0 + g] = _mm(colV, Wv.t())

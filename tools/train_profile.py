@@ -41,7 +41,14 @@ with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA], record_sh
     out, saved = tr.forward_train(x)
     tr.backward(saved, g)
     torch.cuda.synchronize()
-print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25, max_name_column_width=60))
-print(prof.key_averages(group_by_input_shape=True).table(sort_by="cuda_time_total", row_limit=40,
-                                                         max_name_column_width=40,
-                                                         max_shapes_column_width=80))
+evs = [e for e in prof.key_averages() if e.device_time_total > 0]
+evs.sort(key=lambda e: -e.self_device_time_total)
+tot = sum(e.self_device_time_total for e in evs)
+print(f"total GPU time {tot / 1e3:.1f} ms")
+for e in evs[:30]:
+    print(f"{e.self_device_time_total / 1e3:8.2f} ms {e.count:5d}  {e.key[:90]}")
+shp = [e for e in prof.key_averages(group_by_input_shape=True) if e.self_device_time_total > 0]
+shp.sort(key=lambda e: -e.self_device_time_total)
+print("-- by input shape")
+for e in shp[:25]:
+    print(f"{e.self_device_time_total / 1e3:8.2f} ms {e.count:5d}  {e.key[:30]:30s} {str(e.input_shapes)[:110]}")
