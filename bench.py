@@ -128,7 +128,10 @@ def reference_arm(args, wl, tp, max_group):
         "config": workload_config(args, wl, tp, max_group),
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "port",
                          "sample": f"1 image x {tok}/{S} tokens per step (float64 numpy "
-                                   f"restatement of the reference, {blas})"},
+                                   f"restatement of the reference, {blas})"
+                                   + ("; forward only: the oracle has no backward, so the "
+                                      "CPU side of the fwd+bwd step is not timed"
+                                      if wl.get("train") else "")},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -393,7 +396,9 @@ def b200_arm(args, wl, tp, max_group):
         threads, blas = blas_threads()
         cpu = {"value": v, "unit": "images/s", "cores": threads, "kind": "port",
                "sample": f"1 image x {tok}/{S} tokens, {dt:.1f} s (float64 numpy restatement "
-                         f"of the reference hot path, {blas})"}
+                         f"of the reference hot path, {blas})"
+                         + ("; forward only: the oracle has no backward" if wl.get("train")
+                            else "")}
 
     clk.__exit__()
     if rank == 0:
