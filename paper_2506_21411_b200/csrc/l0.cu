@@ -357,7 +357,10 @@ cudaError_t launch_l0_logits(const L0LogitArgs& a, int num_sms, cudaStream_t st)
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int total = a.n_nodes * (R / RB);
-  const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+  int per_sm = (int)((227 * 1024) / smem);  // co-resident CTAs (smem-limited), at most 4
+  if (per_sm > 4) per_sm = 4;
+  if (per_sm < 1) per_sm = 1;
+  if (const char* f = getenv("DCHAG_P0_PERSM")) per_sm = atoi(f) > 0 ? atoi(f) : per_sm;
   const int ctas = min(total, per_sm * num_sms);
   const int per_cta = (total + ctas - 1) / ctas;
   k<<<(total + per_cta - 1) / per_cta, 256, (size_t)smem, st>>>(a, per_cta, nbuf);
