@@ -388,8 +388,8 @@ def b200_arm(args, wl, tp, max_group):
         tot_exec = exec_flops
     b_flops = bflops_per_image(wl, fe.slabs, max_group, train=bool(wl.get("train"))) * B
 
-    cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    cpu = None  # the CPU oracle is timed on rank 0 at N = 1 only (torchrun pins 1 OMP thread)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         S = fe.seq
         tokens = args.cpu_tokens or max(S // 2, wl["image_w"] // wl["patch"])
         v, tok, dt = cpu_sample(wl, tp, max_group, tokens)
