@@ -111,6 +111,12 @@ def reference_arm(args, wl, tp, max_group):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # torchrun pins OMP_NUM_THREADS=1; the reference arm uses every host core
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=len(os.sched_getaffinity(0)))
+    except Exception:
+        pass
     S = (wl["image_h"] // wl["patch"]) * (wl["image_w"] // wl["patch"])
     tokens = args.cpu_tokens or max(S // 8, wl["image_w"] // wl["patch"])
     vals = []
