@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) l0_bwd_rows_kernel(L0BwdRowsArgs a) {
     }
   }
   float gv[CPL][8];
-  float gc[CPL];  // G_h . ctx_h of this lane's head per chunk (after reduction)
+  float gc[CPL];  // sum_j p_jh dp_jh of this lane's head per chunk
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
     const int c = act ? lane + 32 * i : 0;
@@ -215,16 +215,7 @@ __global__ void __launch_bounds__(256) l0_bwd_rows_kernel(L0BwdRowsArgs a) {
     const float4 g1 = *reinterpret_cast<const float4*>(a.G + off + 4);
     gv[i][0] = g0.x; gv[i][1] = g0.y; gv[i][2] = g0.z; gv[i][3] = g0.w;
     gv[i][4] = g1.x; gv[i][5] = g1.y; gv[i][6] = g1.z; gv[i][7] = g1.w;
-    float s = 0.f;
-    if (!a.mix) {
-      const uint4 cx = *reinterpret_cast<const uint4*>(a.ctx + off);
-      const uint32_t cw[4] = {cx.x, cx.y, cx.z, cx.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) s += gv[i][2 * e] * bf16lo(cw[e]) + gv[i][2 * e + 1] * bf16hi(cw[e]);
-      if (!act) s = 0.f;
-      for (int o = 1; o < lpg; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    }
-    gc[i] = s;
+    gc[i] = 0.f;
   }
   __syncwarp();
   for (int j = 0; j < a.g; ++j) {
@@ -251,8 +242,8 @@ __global__ void __launch_bounds__(256) l0_bwd_rows_kernel(L0BwdRowsArgs a) {
       } else {
         for (int o = 1; o < lpg; o <<= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
         pj = ps[j * hseg + hl];
-        if (act && (lane % lpg) == 0)
-          a.dl[((long long)j * a.R + r) * H + h0 + hl] = pj * (dp - gc[i]);
+        gc[i] += pj * dp;  // sum_j p_jh dp_jh (== G_h . ctx_h in exact arithmetic)
+        if (act && (lane % lpg) == 0) a.dl[((long long)j * a.R + r) * H + h0 + hl] = dp;
       }
       uint4 o;
       o.x = pack_bf16(pj * gv[i][0], pj * gv[i][1]);
@@ -265,6 +256,21 @@ __global__ void __launch_bounds__(256) l0_bwd_rows_kernel(L0BwdRowsArgs a) {
 #pragma unroll
       for (int o = 16; o; o >>= 1) dmr += __shfl_xor_sync(0xffffffffu, dmr, o);
       if (lane == 0) atomicAdd(a.dm + (long long)j * a.R + r, dmr);  // segments of the row
+    }
+  }
+  if (a.mix) return;
+  // softmax backward with the same dp values: dl_jh = p_jh (dp_jh - sum_j' p_j'h dp_j'h), so
+  // sum_j dl_jh = 0 exactly (a one-channel node gets exactly zero logit gradient)
+  __syncwarp();
+  for (int j = 0; j < a.g; ++j) {
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const int c = act ? lane + 32 * i : 0;
+      const int hl = (c * 8) / dh;
+      if (act && (lane % lpg) == 0) {
+        float* dst = a.dl + ((long long)j * a.R + r) * H + h0 + hl;
+        *dst = ps[j * hseg + hl] * (*dst - gc[i]);
+      }
     }
   }
 }

@@ -87,7 +87,12 @@ def main():
                 ref = ref[:, cols]          # column shards of the own heads (params.py:166-177)
             elif split and k == "agg.final.wo":
                 ref = ref[cols]             # row shard
-            errs[k] = O.rel_err(v, ref)
+            if np.abs(ref).max() < 1e-12:
+                # exactly-zero reference gradient (e.g. the logit weights of a one-channel
+                # node: its softmax is identically 1): require ours to be ~0 too
+                errs[k] = float(np.abs(v).max() > 1e-6)
+            else:
+                errs[k] = O.rel_err(v, ref)
         terr = max(errs.values())
         worst = max(worst, terr)
         print(f"rank {rank}/{tp} train step{' (head-split final)' if split else ''}: "
