@@ -63,7 +63,7 @@ class DchagFrontEnd(torch.nn.Module):
                  agg_variant: str = "single_query", agg_layer_kind: str = "cross_attention",
                  tp: int = 1, rank: int = 0, final_layer_tp_split: bool = False,
                  process_group=None, out_dtype=torch.bfloat16, device=None,
-                 precision: str = "bf16"):
+                 precision: str = "bf16", final_position_split: bool = True):
         super().__init__()
         self.model = ModelConfig(channels=channels, image_h=image_h, image_w=image_w,
                                  patch=patch, embed=embed, heads=heads,
@@ -93,6 +93,12 @@ class DchagFrontEnd(torch.nn.Module):
         self.tree: TreeSpec = trees[rank]
         self.process_group = process_group
         self.out_dtype = out_dtype
+        # tp > 1: exchange the root payload by position (all-to-all) and run the final
+        # layer on R/tp rows per rank, then all-gather the outputs. The
+        # per-row arithmetic is the same kernels on the same operands as the AllGather
+        # schedule, so the result is bit-identical; only the bytes moved and the final
+        # layer's work per rank shrink by ~tp.
+        self.final_position_split = bool(final_position_split)
         if precision not in ("bf16", "fp32"):
             raise ConfigError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
         if precision == "fp32" and agg_variant != "single_query":
@@ -299,9 +305,12 @@ class DchagFrontEnd(torch.nn.Module):
         if images.stride(3) != 1 or images.stride(2) != wimg:
             images = images.contiguous()
         payload = self.local_payload(images, pk)
-        gathered = self.gather(payload)
         dev_out = out if out is not None and out.is_cuda else None
-        res = self.finish(gathered, images.shape[0], out=dev_out)
+        if return_payload or not self._position_split(images.shape[0]):
+            gathered = self.gather(payload)
+            res = self.finish(gathered, images.shape[0], out=dev_out)
+        else:
+            res = self.exchange_finish(payload, images.shape[0], out=dev_out)
         if out is not None and not out.is_cuda:
             out.copy_(res, non_blocking=True)
             res = out
@@ -347,8 +356,10 @@ class DchagFrontEnd(torch.nn.Module):
             b0, b1 = bounds[k], bounds[k + 1]
             cur.wait_event(copied[k])
             payload = self.local_payload(dbuf[b0:b1], pk)
-            gathered = self.gather(payload)
-            self.finish(gathered, b1 - b0, out=res[b0:b1])
+            if self._position_split(b1 - b0):
+                self.exchange_finish(payload, b1 - b0, out=res[b0:b1])
+            else:
+                self.finish(self.gather(payload), b1 - b0, out=res[b0:b1])
             if out is not None and not out.is_cuda:
                 done = torch.cuda.Event()
                 done.record(cur)
@@ -385,11 +396,12 @@ class DchagFrontEnd(torch.nn.Module):
                 n_next = len(pk.levels[li + 1])
                 plan.append(("dchag_combine", f"combine_l{li + 1}", 2 * R * n_l * d,
                              n_l * R * (d * 2 + h * 4) + n_next * R * d * 2))
+        Rf = R // self.tp if self._position_split(B) else R   # rows of this rank's final
         if self.tp > 1:
-            plan.append(("dchag_combine", "combine_final", 2 * R * self.tp * d,
-                         self.tp * R * (d * 2 + h * 4) + R * d * 2))
-        plan.append(("dchag_gemm_bf16", "gemm_final", 2 * R * d * d,
-                     R * d * 2 + R * d * (4 if self.out_dtype == torch.float32 else 2)))
+            plan.append(("dchag_combine", "combine_final", 2 * Rf * self.tp * d,
+                         self.tp * Rf * (d * 2 + h * 4) + Rf * d * 2))
+        plan.append(("dchag_gemm_bf16", "gemm_final", 2 * Rf * d * d,
+                     Rf * d * 2 + Rf * d * (4 if self.out_dtype == torch.float32 else 2)))
         return plan
 
     def gather(self, payload):
@@ -401,6 +413,44 @@ class DchagFrontEnd(torch.nn.Module):
                                dtype=torch.uint8)
         dist.all_gather_into_tensor(gathered, payload, group=self.process_group)
         return gathered
+
+    def _position_split(self, B):
+        rows = B * self.seq
+        return (self.final_position_split and self.tp > 1
+                and not self.strategy.final_layer_tp_split
+                and rows % (self.tp * 128) == 0)
+
+    def exchange_finish(self, payload, B, out=None):
+        """Position-split final layer: rank j receives rows [j R/tp, (j+1) R/tp) of every
+        rank's root payload (one all-to-all of V and one of L), combines those tp streams
+        and applies the final projection on its R/tp rows, and the outputs are all-gathered
+        in rank (= row) order. Same per-row math as gather() + finish()."""
+        import torch.distributed as dist
+        pk = self.prepare()
+        m = self.model
+        d, h, s = m.embed, m.heads, self.seq
+        R = B * s
+        tp = self.tp
+        Rl = R // tp
+        dev = payload.device
+        st = _lib.stream_handle()
+        V, L = views(payload, R, d, h)
+        Vx = torch.empty(tp, Rl, d, device=dev, dtype=torch.bfloat16)
+        Lx = torch.empty(tp, Rl, h, device=dev, dtype=torch.float32)
+        dist.all_to_all_single(Vx, V.view(tp, Rl, d), group=self.process_group)
+        dist.all_to_all_single(Lx, L.view(tp, Rl, h), group=self.process_group)
+        ctx_f = torch.empty(1, Rl, d, device=dev, dtype=torch.bfloat16)
+        first = self._final_first(dev)
+        _lib.call("dchag_combine", 1, Rl, d, h, _lib.ptr(first[0]), _lib.ptr(first[1]), tp,
+                  _lib.ptr(Vx), Rl * d, _lib.ptr(Lx), Rl * h, 0, _lib.ptr(ctx_f), st)
+        part = torch.empty(Rl, d, device=dev, dtype=self.out_dtype)
+        _lib.call("dchag_gemm_bf16", _lib.ptr(ctx_f), 1, 1, Rl, d, Rl * d, 0, d,
+                  _lib.ptr(pk.Wf), d, d * d, d, _lib.ptr(pk.bf), d, 0, 0, 0, 1, _lib.ptr(part),
+                  int(self.out_dtype == torch.float32), Rl * d, 0, d, 0, 0, 0, 0, st)
+        if out is None:
+            out = torch.empty(R, d, device=dev, dtype=self.out_dtype)
+        dist.all_gather_into_tensor(out.view(R, d), part, group=self.process_group)
+        return out.view(B, 1, s, d)
 
     def local_payload(self, img, pk=None):
         """Rank-local part: slab tree -> root payload [V bf16 R*D | L fp32 R*H] (bytes),

@@ -31,6 +31,8 @@ def main():
     worst = 0.0
     for meta, split in [(m, sp) for m in CASES for sp in (False, True)
                         if not sp or m["heads"] % tp == 0]:
+        # batch 8: B*S = 1024 rows, so the position-split final layer (rows % (128 tp) == 0)
+        # runs at tp <= 8; the AllGather schedule runs alongside and must match it bitwise
         lk = meta.get("layer_kind", "cross_attention")
         specs = O.frontend_param_specs(meta["channels"], meta["image_h"], meta["image_w"],
                                        meta["patch"], meta["embed"], tp, meta["max_group"],
@@ -38,7 +40,7 @@ def main():
         w = O.random_params(specs, seed=7, std=0.05, bias_std=0.02)
         w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
         img = np.random.default_rng(3).standard_normal(
-            (2, meta["channels"], meta["image_h"], meta["image_w"]))
+            (8, meta["channels"], meta["image_h"], meta["image_w"]))
         img_bf = torch.from_numpy(img.astype(np.float32)).to(torch.bfloat16)
         fe = DchagFrontEnd(meta["channels"], meta["image_h"], meta["image_w"], meta["patch"],
                            meta["embed"], meta["heads"], max_group=meta["max_group"],
@@ -46,13 +48,23 @@ def main():
                            final_layer_tp_split=split)
         fe.load_weights(w)
         out = fe(img_bf.cuda()).cpu().numpy()  # full images: the rank slices its own slab
+        if not split:
+            fe.final_position_split = False
+            out_ag = fe(img_bf.cuda()).cpu().numpy()
+            fe.final_position_split = True
+            if not np.array_equal(out, out_ag):
+                print(f"rank {rank}: position-split final differs from the AllGather schedule "
+                      f"(max |diff| {np.abs(out - out_ag).max():.3e})", flush=True)
+                worst = max(worst, 1.0)
         want = O.dchag_frontend(img_bf.float().numpy().astype(np.float64), w,
                                 patch=meta["patch"], heads=meta["heads"], tp=tp,
                                 max_group=meta["max_group"], layer_kind=lk)
         err = O.rel_err(out, want)
         worst = max(worst, err)
-        print(f"rank {rank}/{tp} C={meta['channels']} slab={fe.slab} {lk}"
-              f"{' head-split final' if split else ''}: rel_err={err:.3e}", flush=True)
+        mode = " head-split final" if split else (
+            " position-split final (== AllGather bitwise)" if fe._position_split(8) else "")
+        print(f"rank {rank}/{tp} C={meta['channels']} slab={fe.slab} {lk}{mode}: "
+              f"rel_err={err:.3e}", flush=True)
     # training step over NCCL: forward_train (AllGather of root streams) + backward
     # (local-slice boundary, special.pos all-reduce), vs float64 autograd of the reference math
     sys.path.insert(0, os.path.join(ROOT, "tests"))
