@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="training workload: launch the step eagerly instead of replaying its "
+                         "CUDA graph")
     ap.add_argument("--h2d-chunks", type=int, default=8,
                     help="batch chunks of the e2e host-input pipeline (copy/compute overlap)")
     ap.add_argument("--cpu-tokens", type=int, default=None,
@@ -150,9 +153,20 @@ def workload_config(args, wl, tp, max_group):
             "image": [wl["image_h"], wl["image_w"]], "patch": wl["patch"],
             "embed": wl["embed"], "heads": wl["heads"], "depth": wl["depth"],
             "max_group": max_group, "tp": tp, "global_batch": args.batch or wl["batch"],
-            "final_layer": "head-split" if wl.get("final_split") and tp > 1 else "replicated",
+            "final_layer": final_layer_mode(args, wl, tp),
             "parallelism": f"dchag-tp{tp}",
+            **({"launch": "eager" if args.no_graph else "cuda graph (whole step)"}
+               if wl.get("train") else {}),
             "l2": "flushed between timed steps (256 MiB write)"}
+
+
+def final_layer_mode(args, wl, tp):
+    if tp == 1:
+        return "single stream"
+    if wl.get("final_split"):
+        return "head-split"
+    rows = (args.batch or wl["batch"]) * (wl["image_h"] // wl["patch"]) * (wl["image_w"] // wl["patch"])
+    return "position-split" if wl.get("train") is None and rows % (tp * 128) == 0 else "replicated"
 
 
 # ----------------------------------------------------------------- B200 arm
@@ -279,9 +293,15 @@ def b200_arm(args, wl, tp, max_group):
         trainer = DchagTrainer(fe)
         probe = torch.randn(B, 1, fe.seq, wl["embed"], device="cuda", generator=gen)
 
-        def step():
-            out, saved = trainer.forward_train(images)
-            return trainer.backward(saved, probe)
+        if args.no_graph:
+            def step():
+                out, saved = trainer.forward_train(images)
+                return trainer.backward(saved, probe)
+        else:
+            # the whole step (forward_train + backward, collectives included) as one CUDA
+            # graph over the static image / probe buffers: a replay re-runs every kernel
+            gstep = trainer.capture(images, probe)
+            step = gstep.replay
     else:
         step = lambda: fe(images)  # noqa: E731
     clk = ClockSampler(local).__enter__()
@@ -367,9 +387,14 @@ def b200_arm(args, wl, tp, max_group):
 
     def e2e_step():
         if wl.get("train"):
-            dev_img.copy_(host_img, non_blocking=True)
-            out, saved = trainer.forward_train(dev_img)
-            trainer.backward(saved, probe)
+            if args.no_graph:
+                dev_img.copy_(host_img, non_blocking=True)
+                out, saved = trainer.forward_train(dev_img)
+                trainer.backward(saved, probe)
+            else:
+                images.copy_(host_img, non_blocking=True)   # the graph's static input
+                gstep.replay()
+                out = gstep.out
             if rank == 0:
                 out_host.copy_(out, non_blocking=True)
         else:

@@ -43,6 +43,17 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
                     int outV_f32, long long sVg, long long sVmo, long long sVmi, float* outL,
                     long long sLg, long long sLmo, long long sLmi, void* stream);
 
+/* Row-dot GEMM for the level-0 backward (the `dp = G . V` term of the softmax backward,
+ * layers.py:103-121 differentiated by tensor.py:395-413): the product rows
+ * V[g][m][:] = A[g][m][:] W[g]^T + bias[g] are never stored; for every 32-column group
+ * dot_out[(g*N/32 + n/32)*M + m] = sum_{n in group} V[g][m][n] * Gmat[m][n] (fp32),
+ * M = Mo*Mi, Gmat bf16 [M][ldG] shared by all g. A, W, strides as dchag_gemm_bf16;
+ * N % 32 == 0. */
+int dchag_gemm_rowdot(const void* A, int G, int Mo, int Mi, int K, long long sAg,
+                      long long sAmo, long long sAmi, const void* W, int N, long long sWg,
+                      const float* bias, long long bias_g, const void* Gmat, long long ldG,
+                      float* dot_out, void* stream);
+
 /* Level-0 logits + softmax over each node's channels (K_p0): replaces the
  * q@wq / x@wk / logits / softmax part of layers.py:103-121 for tree level 0 with the
  * tokenizer (model.py:51-64) folded in.  img: bf16 [B][*][Himg][W] with batch stride
@@ -87,6 +98,16 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
 int dchag_l0_bwd_rows(int g, int R, int D, int H, int nh, const void* V, const float* G,
                       const void* ctx, const void* p, const float* mix, float* dl, void* dV,
                       float* dm, void* stream);
+
+/* Level-0 node backward, value gradient (training): dV[c][r][d] = p_c[r][h] * G[r][d]
+ * for the node's g channels, p = the node's block of the normalised dchag_l0_logits output
+ * ([H/nh][g][R][nh] bf16), or dV[c] = mix[c] * G for linear nodes (mix != NULL). With posV
+ * (fp32 [S][D], row r uses r % S) also Gpos[r][h] = sum_{d in head h} G[r][d] posV[r % S][d]
+ * (fp32 [R][H]), the positional part of dp = G . V. G, dV bf16 [R][D] / [g][R][D], 16-byte
+ * aligned; D/H a power of two in 8..256. */
+int dchag_l0_dv(int g, int R, int D, int H, int nh, const void* p, const float* mix,
+                const void* G, const float* posV, int period, float* Gpos, void* dV,
+                void* stream);
 
 /* fp32 parity mode combine: as dchag_combine with fp32 child values V (row r of child j at
  * V + j*sVj + r*D) and an fp32 context (precise expf, fp32 accumulation). */

@@ -22,6 +22,8 @@ SIGNATURES = {
     "dchag_gemm_bf16": [c_vp, c_int, c_int, c_int, c_int, c_ll, c_ll, c_ll, c_vp, c_int, c_ll,
                         c_int, c_vp, c_ll, c_vp, c_ll, c_ll, c_int, c_vp, c_int, c_ll, c_ll,
                         c_ll, c_vp, c_ll, c_ll, c_ll, c_vp],
+    "dchag_gemm_rowdot": [c_vp, c_int, c_int, c_int, c_int, c_ll, c_ll, c_ll, c_vp, c_int,
+                          c_ll, c_vp, c_ll, c_vp, c_ll, c_vp, c_vp],
     "dchag_l0_logits": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                         c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "dchag_l0_node": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
@@ -30,6 +32,8 @@ SIGNATURES = {
                       c_vp, c_vp, c_vp],
     "dchag_l0_bwd_rows": [c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                           c_vp, c_vp, c_vp],
+    "dchag_l0_dv": [c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp,
+                    c_vp, c_vp],
     "dchag_combine_f32": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_vp, c_ll,
                           c_vp, c_vp, c_vp],
     "dchag_fullcross_weights": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_ll,

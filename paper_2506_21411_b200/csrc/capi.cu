@@ -102,18 +102,20 @@ const char* dchag_version(void) { return "dchag-b200 0.1.0 (sm_100a)"; }
 const char* dchag_last_error(void) { return g_err.c_str(); }
 int dchag_num_sms(void) { return num_sms_cached(); }
 
-int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, long long sAmo,
-                    long long sAmi, const void* W, int N, long long sWg, int Nv,
-                    const float* bias, long long bias_g, const void* rowbias,
-                    long long rowbias_g, long long rowbias_row, int rowbias_period, void* outV,
-                    int outV_f32, long long sVg, long long sVmo, long long sVmi, float* outL,
-                    long long sLg, long long sLmo, long long sLmi, void* stream) {
+static int gemm_impl(const void* A, int G, int Mo, int Mi, int K, long long sAg, long long sAmo,
+                     long long sAmi, const void* W, int N, long long sWg, int Nv,
+                     const float* bias, long long bias_g, const void* rowbias,
+                     long long rowbias_g, long long rowbias_row, int rowbias_period, void* outV,
+                     int outV_f32, long long sVg, long long sVmo, long long sVmi, float* outL,
+                     long long sLg, long long sLmo, long long sLmi, const void* dotG,
+                     long long ldG, float* dotOut, void* stream) {
+  const bool dot = dotOut != nullptr;
   if (G < 1 || Mo < 1 || Mi < 128 || Mi % 128 || K < 16 || K % 16 || N < 16 || Nv < 0 ||
       Nv > N || Nv % 16)
     return fail(DCHAG_ERR_SHAPE, "gemm: bad shape G=%d Mo=%d Mi=%d K=%d N=%d Nv=%d", G, Mo, Mi,
                 K, N, Nv);
-  if (Nv < N && !outL) return fail(DCHAG_ERR_SHAPE, "gemm: N > Nv needs outL");
-  if (Nv > 0 && !outV) return fail(DCHAG_ERR_SHAPE, "gemm: Nv > 0 needs outV");
+  if (!dot && Nv < N && !outL) return fail(DCHAG_ERR_SHAPE, "gemm: N > Nv needs outL");
+  if (!dot && Nv > 0 && !outV) return fail(DCHAG_ERR_SHAPE, "gemm: Nv > 0 needs outV");
   if ((sAmi * 2) % 16 || (sAmo * 2) % 16 || (sAg * 2) % 16 || (sWg * 2) % 16)
     return fail(DCHAG_ERR_SHAPE, "gemm: strides must be multiples of 16 bytes");
   const int bk = (K % 64 == 0) ? 64 : (K % 32 == 0 ? 32 : 16);
@@ -166,7 +168,34 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
   a.rowbias_period = rowbias_period > 0 ? rowbias_period : 1;
   a.outV = outV; a.outV_f32 = outV_f32; a.sVg = sVg; a.sVmo = sVmo; a.sVmi = sVmi;
   a.outL = outL; a.sLg = sLg; a.sLmo = sLmo; a.sLmi = sLmi;
+  if (dot) {
+    if (N % 32 || bn % 32 || ldG % 8 || !dotG || (reinterpret_cast<uintptr_t>(dotG) % 16))
+      return fail(DCHAG_ERR_SHAPE, "gemm_rowdot: N, tile width and ldG must suit 32-column "
+                                   "groups of 16-byte aligned rows (N=%d ldG=%lld)", N, ldG);
+    a.v_tma = 0; a.rowbias = nullptr; a.outV = nullptr; a.outL = nullptr; a.Nv = N;
+    a.dotG = reinterpret_cast<const __nv_bfloat16*>(dotG); a.ldG = ldG; a.dotOut = dotOut;
+  }
   return cuda_status(launch_gemm(tA, tW, tV, a, bk, num_sms_cached(), S(stream)), "gemm");
+}
+
+int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, long long sAmo,
+                    long long sAmi, const void* W, int N, long long sWg, int Nv,
+                    const float* bias, long long bias_g, const void* rowbias,
+                    long long rowbias_g, long long rowbias_row, int rowbias_period, void* outV,
+                    int outV_f32, long long sVg, long long sVmo, long long sVmi, float* outL,
+                    long long sLg, long long sLmo, long long sLmi, void* stream) {
+  return gemm_impl(A, G, Mo, Mi, K, sAg, sAmo, sAmi, W, N, sWg, Nv, bias, bias_g, rowbias,
+                   rowbias_g, rowbias_row, rowbias_period, outV, outV_f32, sVg, sVmo, sVmi, outL,
+                   sLg, sLmo, sLmi, nullptr, 0, nullptr, stream);
+}
+
+int dchag_gemm_rowdot(const void* A, int G, int Mo, int Mi, int K, long long sAg,
+                      long long sAmo, long long sAmi, const void* W, int N, long long sWg,
+                      const float* bias, long long bias_g, const void* Gmat, long long ldG,
+                      float* dot_out, void* stream) {
+  if (!dot_out) return fail(DCHAG_ERR_SHAPE, "gemm_rowdot: dot_out is null");
+  return gemm_impl(A, G, Mo, Mi, K, sAg, sAmo, sAmi, W, N, sWg, N, bias, bias_g, nullptr, 0, 0,
+                   1, nullptr, 0, 0, 0, 0, nullptr, 0, 0, 0, Gmat, ldG, dot_out, stream);
 }
 
 int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
@@ -280,6 +309,22 @@ int dchag_l0_bwd_rows(int g, int R, int D, int H, int nh, const void* V, const f
   a.p = reinterpret_cast<const __nv_bfloat16*>(p); a.mix = mix;
   a.dl = dl; a.dV = reinterpret_cast<__nv_bfloat16*>(dV); a.dm = dm;
   return cuda_status(launch_l0_bwd_rows(a, S(stream)), "l0_bwd_rows");
+}
+
+int dchag_l0_dv(int g, int R, int D, int H, int nh, const void* p, const float* mix,
+                const void* G, const float* posV, int period, float* Gpos, void* dV, void* stream) {
+  if (!mix && !p) return fail(DCHAG_ERR_SHAPE, "l0_dv: need p or mix");
+  const int dh = H > 0 ? D / H : 0;
+  if (H < 1 || D % H || dh % 8 || dh > 256 || ((dh / 8) & (dh / 8 - 1)) ||
+      ((long long)R * (D / 8)) % 32 || (!mix && (nh < 1 || H % nh)) ||
+      (posV && (!Gpos || period < 1 || R % period)) ||
+      (reinterpret_cast<uintptr_t>(G) | reinterpret_cast<uintptr_t>(dV) |
+       reinterpret_cast<uintptr_t>(posV)) % 16)
+    return fail(DCHAG_ERR_SHAPE, "l0_dv: bad shape R=%d D=%d H=%d nh=%d", R, D, H, nh);
+  return cuda_status(launch_l0_dv(g, R, D, H, nh, reinterpret_cast<const __nv_bfloat16*>(p), mix,
+                                  reinterpret_cast<const __nv_bfloat16*>(G), posV, period, Gpos,
+                                  reinterpret_cast<__nv_bfloat16*>(dV), S(stream)),
+                     "l0_dv");
 }
 
 int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,

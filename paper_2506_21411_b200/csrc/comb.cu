@@ -296,6 +296,63 @@ cudaError_t launch_l0_bwd_rows(const L0BwdRowsArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Level-0 backward value gradient: dV[c][r][d] = p_c[r][h(d)] * G[r][d] (or mix[c] * G), and
+// (posV != null) the positional part of dp, Gpos[r][h] = sum_{d in h} G[r][d] posV[r % S][d].
+// One thread per (row, 8 columns): G is read once (16 B) and the node's g outputs are
+// written as 16-byte stores, consecutive threads on consecutive columns; the dh/8 lanes of
+// a head reduce Gpos with shuffles (a row's D/8 chunks and a head's chunks align with warps).
+__global__ void __launch_bounds__(256) l0_dv_kernel(int g, int R, int D, int H, int NH,
+                                                   const __nv_bfloat16* __restrict__ p,
+                                                   const float* __restrict__ mix,
+                                                   const __nv_bfloat16* __restrict__ G,
+                                                   const float* __restrict__ posV, int S,
+                                                   float* __restrict__ Gpos,
+                                                   __nv_bfloat16* __restrict__ out) {
+  const int dchunks = D >> 3;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)R * dchunks) return;  // R * D/8 is a multiple of 32: whole warps
+  const int r = (int)(idx / dchunks);
+  const int d0 = (int)(idx - (long long)r * dchunks) * 8;
+  const uint4 gv = __ldg(reinterpret_cast<const uint4*>(G + (size_t)r * D + d0));
+  const int dh = D / H;
+  const int h = d0 / dh;
+  const int hg = h / NH, hn = h - hg * NH;
+  const float gf[8] = {bf16lo(gv.x), bf16hi(gv.x), bf16lo(gv.y), bf16hi(gv.y),
+                       bf16lo(gv.z), bf16hi(gv.z), bf16lo(gv.w), bf16hi(gv.w)};
+  if (posV) {
+    const float4* pv = reinterpret_cast<const float4*>(posV + (size_t)(r % S) * D + d0);
+    const float4 a = __ldg(pv), b = __ldg(pv + 1);
+    float acc = gf[0] * a.x + gf[1] * a.y + gf[2] * a.z + gf[3] * a.w +
+                gf[4] * b.x + gf[5] * b.y + gf[6] * b.z + gf[7] * b.w;
+    const int lanes = dh >> 3;  // 1..32, a power of two
+    for (int off = lanes >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((threadIdx.x & (lanes - 1)) == 0) Gpos[(size_t)r * H + h] = acc;
+  }
+  for (int c = 0; c < g; ++c) {
+    const float pc = mix ? __ldg(mix + c)
+                         : __bfloat162float(p[((size_t)(hg * g + c) * R + r) * NH + hn]);
+    uint4 o;
+    o.x = pack_bf16(pc * gf[0], pc * gf[1]);
+    o.y = pack_bf16(pc * gf[2], pc * gf[3]);
+    o.z = pack_bf16(pc * gf[4], pc * gf[5]);
+    o.w = pack_bf16(pc * gf[6], pc * gf[7]);
+    *reinterpret_cast<uint4*>(out + ((size_t)c * R + r) * D + d0) = o;
+  }
+}
+
+cudaError_t launch_l0_dv(int g, int R, int D, int H, int NH, const __nv_bfloat16* p,
+                         const float* mix, const __nv_bfloat16* G, const float* posV, int S,
+                         float* Gpos, __nv_bfloat16* out, cudaStream_t st) {
+  const int dh = D / H;
+  if (D % H || dh % 8 || dh > 256 || ((dh / 8) & (dh / 8 - 1)) || ((long long)R * (D / 8)) % 32 ||
+      (!mix && (NH < 1 || H % NH)) || (posV && (!Gpos || S < 1)))
+    return cudaErrorInvalidValue;
+  const long long n = (long long)R * (D / 8);
+  l0_dv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, R, D, H, NH, p, mix, G, posV, S,
+                                                             Gpos, out);
+  return cudaGetLastError();
+}
+
 // full_cross node weights (see FullCrossArgs). One CTA per (node, row), one warp per head;
 // lane j owns child j (g <= 32): it keeps k_j,h in registers and computes the row of logits
 // L_ij = q_i . k_j / sqrt(dh) against q_i broadcast from shared memory; the per-i softmax,

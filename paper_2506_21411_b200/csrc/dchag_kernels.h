@@ -24,6 +24,11 @@ struct GemmArgs {
   long long sVg, sVmo, sVmi;
   float* outL;                  // columns [Nv, N): fp32
   long long sLg, sLmo, sLmi;
+  // row-dot mode (dotOut != null): nothing is stored; each 32-column group's
+  // sum_n (acc + bias)[m][n] * dotG[m][n] goes to dotOut[(g * N/32 + n/32) * M + m]
+  const __nv_bfloat16* dotG;    // [M][ldG] bf16, shared by all groups
+  long long ldG;
+  float* dotOut;
 };
 
 cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUtensorMap& tV,
@@ -123,6 +128,9 @@ struct L0BwdRowsArgs {
   float* dm;                   // [g][R] (linear)
 };
 cudaError_t launch_l0_bwd_rows(const L0BwdRowsArgs& a, cudaStream_t st);
+cudaError_t launch_l0_dv(int g, int R, int D, int H, int NH, const __nv_bfloat16* p,
+                         const float* mix, const __nv_bfloat16* G, const float* posV, int S,
+                         float* Gpos, __nv_bfloat16* out, cudaStream_t st);
 
 // full_cross node weights (layers.py:125-138 folded): per (node, row), heads h:
 //   S^h = softmax_j(q_i,h . k_j,h / sqrt(dh)),  s_i = sum_h sum_j S^h_ij u_jh,

@@ -237,8 +237,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int mo = m_row / args.Mi, mi = m_row - mo * args.Mi;
       // prefetch this thread's row bias for its column groups (in flight during the wait)
       uint4 rbv[4][4];
+      // row-dot mode: the same registers carry this row's dotG columns instead
+      const bool dot = args.dotOut != nullptr;
       const __nv_bfloat16* rb =
-          (args.rowbias && !(args.debug & 2)) ? args.rowbias + (size_t)g * args.rowbias_g +
+          dot ? args.dotG + (size_t)m_row * args.ldG
+          : (args.rowbias && !(args.debug & 2)) ? args.rowbias + (size_t)g * args.rowbias_g +
                              (size_t)(mi % args.rowbias_period) * args.rowbias_row
                        : nullptr;
 #pragma unroll
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           rbv[gi][j] = make_uint4(0, 0, 0, 0);
           const int n = n0 + 8 * j;
           if (rb && hf + 2 * gi < n_groups && n < args.N) {
-            if (rb_vec && n + 8 <= args.N) {
+            if ((dot || rb_vec) && n + 8 <= args.N) {
               rbv[gi][j] = __ldg(reinterpret_cast<const uint4*>(rb + n));
             } else {
               uint32_t w[4];
@@ -298,6 +301,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tmem_ld32(t_row + grp * 32, r);
         tmem_ld_wait();
         float v[32];
+        if (dot) {
+          // sum over the group's 32 columns of (acc + bias) * dotG (fp32)
+          float sdot = 0.f;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t q[4] = {rbv[gi][j].x, rbv[gi][j].y, rbv[gi][j].z, rbv[gi][j].w};
+            float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;
+            if (bias) {
+              b0 = reinterpret_cast<const float4*>(wbias + gi * 32)[2 * j];
+              b1 = reinterpret_cast<const float4*>(wbias + gi * 32)[2 * j + 1];
+            }
+            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              sdot = fmaf(__uint_as_float(r[8 * j + 2 * e]) + bb[2 * e], bf16lo(q[e]), sdot);
+              sdot = fmaf(__uint_as_float(r[8 * j + 2 * e + 1]) + bb[2 * e + 1], bf16hi(q[e]),
+                          sdot);
+            }
+          }
+          args.dotOut[((size_t)g * (args.N >> 5) + (n0 >> 5)) * args.M + m_row] = sdot;
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint32_t q[4] = {rbv[gi][j].x, rbv[gi][j].y, rbv[gi][j].z, rbv[gi][j].w};

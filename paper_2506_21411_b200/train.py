@@ -25,6 +25,7 @@ dU -> (wk, q, wq) follows U[:, h] = wk[:, h-blk] (q wq)[h-blk] / sqrt(dh) (fold.
 from __future__ import annotations
 
 import math
+import weakref
 
 import torch
 
@@ -43,17 +44,21 @@ def _f32(t):
     return t.to(torch.float32).contiguous()
 
 
-def _gemm(A, W_dn, bias=None, out_f32=False, rowbias=None, period=1, N_logit=0):
+def _gemm(A, W_dn, bias=None, out_f32=False, rowbias=None, period=1, N_logit=0, out=None,
+          out_l=None):
     """y[m, :] = A[m, :] @ W_dn + bias (+ rowbias[m % period]) with the sm_100a GEMM.
     A [M, K] bf16 (M % 128 == 0), W_dn [K, N] (reference x @ W layout). Columns >= N - N_logit
-    come back as a separate fp32 tensor."""
+    come back as a separate fp32 tensor. `out` / `out_l` (contiguous) receive the results
+    in place."""
     M, K = A.shape
     N = W_dn.shape[1]
     Nv = N - N_logit
     W = _bf_t(W_dn)
     b = _f32(bias) if bias is not None else torch.zeros(N, device=A.device)
-    V = torch.empty(M, Nv, device=A.device, dtype=torch.float32 if out_f32 else torch.bfloat16)
-    L = torch.empty(M, max(N_logit, 1), device=A.device, dtype=torch.float32)
+    V = out if out is not None else torch.empty(
+        M, Nv, device=A.device, dtype=torch.float32 if out_f32 else torch.bfloat16)
+    L = out_l if out_l is not None else torch.empty(M, max(N_logit, 1), device=A.device,
+                                                   dtype=torch.float32)
     rb = _bf(rowbias) if rowbias is not None else None
     _lib.call("dchag_gemm_bf16", _lib.ptr(A), 1, 1, M, K, M * K, M * K, K, _lib.ptr(W), N, N * K,
               Nv, _lib.ptr(b), N, _lib.ptr(rb), 0, N, period, _lib.ptr(V), int(out_f32), 0, 0, Nv,
@@ -64,25 +69,44 @@ def _gemm(A, W_dn, bias=None, out_f32=False, rowbias=None, period=1, N_logit=0):
 def _mm(a, b):
     """Plain GEMM on tensor cores: bf16 operands, fp32 accumulate (cuBLAS), fp32 result.
     bf16 copies of (fp32) weight operands are cached per tensor version."""
-    return torch.matmul(_bfc(a), _bfc(b)).float()
+    a, b = _bfc(a), _bfc(b)
+    if a.dim() == 2 and b.dim() == 2:
+        return torch.mm(a, b, out_dtype=torch.float32)
+    if a.dim() == 3 and b.dim() == 3:
+        return torch.bmm(a, b, out_dtype=torch.float32)
+    return torch.matmul(a, b).float()
 
 
-_BF_CACHE: dict = {}
-_BF_WEIGHTS: set = set()   # data_ptrs of the module's parameter tensors (DchagTrainer)
+# bf16 copies of the module's fp32 parameters (and their .t() / slice views), per parameter
+# tensor object (checked through a weak reference, so a new tensor that reuses a freed
+# address or id never sees a stale copy) and per tensor version
+_BF_CACHE: dict = {}       # id(tensor) -> (weakref to it, {view key: bf16 copy})
+_BF_WEIGHTS: set = set()   # ids of the module's parameter tensors (DchagTrainer)
+_CAPTURING = [False]       # inside a CUDA-graph capture: conversions are recorded, not cached
+
+
+def _cached(t, tag, make):
+    base = t._base if t._base is not None else t
+    if id(base) not in _BF_WEIGHTS or _CAPTURING[0] or base.numel() < 4096:
+        return make()
+    ent = _BF_CACHE.get(id(base))
+    if ent is None or ent[0]() is not base:
+        if len(_BF_CACHE) > 4096:
+            _BF_CACHE.clear()
+        ent = _BF_CACHE[id(base)] = (weakref.ref(base), {})
+    per = ent[1]
+    key = (tag, base._version, t.stride(), t.storage_offset(), tuple(t.shape))
+    v = per.get(key)
+    if v is None:
+        if len(per) > 64:
+            per.clear()
+        v = per[key] = make()
+    return v
 
 
 def _bf_t(w):
     """Contiguous bf16 transpose of w; cached for the module's parameters (and views of them)."""
-    base = w._base if w._base is not None else w
-    if base.data_ptr() in _BF_WEIGHTS:
-        key = ("T", base.data_ptr(), base._version, w.stride(), w.storage_offset(), tuple(w.shape))
-        v = _BF_CACHE.get(key)
-        if v is None:
-            if len(_BF_CACHE) > 4096:
-                _BF_CACHE.clear()
-            v = _BF_CACHE[key] = _bf(w.t())
-        return v
-    return _bf(w.t())
+    return _cached(w, "T", lambda: _bf(w.t()))
 
 
 def _bfc(t):
@@ -90,16 +114,7 @@ def _bfc(t):
     (their .t() / slice views too). Temporaries are never cached (their storage is reused)."""
     if t.dtype == torch.bfloat16:
         return t
-    base = t._base if t._base is not None else t
-    if base.data_ptr() in _BF_WEIGHTS and base.numel() >= 4096:
-        key = (base.data_ptr(), base._version, t.stride(), t.storage_offset(), tuple(t.shape))
-        v = _BF_CACHE.get(key)
-        if v is None:
-            if len(_BF_CACHE) > 4096:
-                _BF_CACHE.clear()
-            v = _BF_CACHE[key] = t.to(torch.bfloat16)
-        return v
-    return t.to(torch.bfloat16)
+    return _cached(t, "bf", lambda: t.to(torch.bfloat16))
 
 
 def _u_backward(w, prefix, dU, heads):
@@ -121,6 +136,41 @@ class DchagTrainer:
         if fe.model.agg_variant != "single_query":
             raise ConfigError("training path implements agg_variant='single_query'")
         self.fe = fe
+        self._ints = {}
+
+    def _dev_ints(self, vals, dtype, dev):
+        """Small host-known index arrays on the device, made once (no copies inside a step,
+        so the step can be captured in a CUDA graph)."""
+        key = (tuple(int(v) for v in vals), dtype, str(dev))
+        t = self._ints.get(key)
+        if t is None:
+            t = self._ints[key] = torch.tensor(key[0], device=dev, dtype=dtype)
+        return t
+
+    def capture(self, images, g_out, warmup: int = 2):
+        """One training step (forward_train + backward) captured as a CUDA graph over the
+        static buffers `images` / `g_out`: refill them in place and call .replay(). The
+        folded kernel weights are read by pointer, so reload weights (or refold) before
+        capturing again. Returns a GraphedStep with .out, .grads (written by every replay)
+        and .launches (library kernel launches per replay)."""
+        cur = torch.cuda.current_stream()
+        side = torch.cuda.Stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                out, saved = self.forward_train(images)
+                self.backward(saved, g_out)
+        cur.wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        n0 = _lib.LAUNCH_COUNT["n"]
+        _CAPTURING[0] = True
+        try:
+            with torch.cuda.graph(graph):
+                out, saved = self.forward_train(images)
+                grads = self.backward(saved, g_out)
+        finally:
+            _CAPTURING[0] = False
+        return GraphedStep(graph, out, grads, _lib.LAUNCH_COUNT["n"] - n0)
 
     # ---------------------------------------------------------------- forward
     def forward_local(self, images):
@@ -148,7 +198,7 @@ class DchagTrainer:
             for g in pk.l0_g_list:
                 poff.append(acc)
                 acc += g * R * h
-            poff_t = torch.tensor(poff, device=dev, dtype=torch.int64)
+            poff_t = self._dev_ints(poff, torch.int64, dev)
             pbuf = torch.empty(acc, device=dev, dtype=torch.bfloat16)
             pinv = torch.empty(pk.n0, R, h, device=dev, dtype=torch.float32)
             _lib.call("dchag_l0_logits", _lib.ptr(img), img.stride(0), img.stride(1), B,
@@ -171,8 +221,10 @@ class DchagTrainer:
         y = torch.empty(len(levels[0]), R, d, device=dev, dtype=torch.bfloat16)
         for gi in range(len(levels[0])):
             node = f"{pre}.l0.g{gi}"
-            y[gi] = (_gemm(ctx0[gi], w[f"{node}.wo"], w[f"{node}.bo"]) if attn
-                     else (ctx0[gi].float() + w[f"{node}.b"]).to(torch.bfloat16))
+            if attn:
+                _gemm(ctx0[gi], w[f"{node}.wo"], w[f"{node}.bo"], out=y[gi])
+            else:
+                torch.add(ctx0[gi], w[f"{node}.b"], out=y[gi])
         saved["y"] = [y]
         saved["VL"] = []
         # ---- levels >= 1 (unfolded)
@@ -189,7 +241,7 @@ class DchagTrainer:
         """Full forward of this rank: slab tree, AllGather of the root streams (rank order,
         runtime.py:259), shared final layer.  Returns ([B,1,S,D] fp32, saved)."""
         _BF_WEIGHTS.clear()
-        _BF_WEIGHTS.update(v.data_ptr() for v in self.fe.weights.values())
+        _BF_WEIGHTS.update(id(v) for v in self.fe.weights.values())
         saved = self.forward_local(images)
         fe = self.fe
         y_root = saved["y_root"]
@@ -237,8 +289,8 @@ class DchagTrainer:
         d = V.shape[-1]
         h = heads or self.fe.model.heads
         ctx = torch.empty(n, R, d, device=V.device, dtype=torch.bfloat16)
-        ft = torch.tensor(firsts, device=V.device, dtype=torch.int32)
-        gt = torch.tensor(gs, device=V.device, dtype=torch.int32)
+        ft = self._dev_ints(firsts, torch.int32, V.device)
+        gt = self._dev_ints(gs, torch.int32, V.device)
         _lib.call("dchag_combine", n, R, d, h, _lib.ptr(ft), _lib.ptr(gt), max(gs), _lib.ptr(V),
                   R * d, _lib.ptr(L), R * h, _lib.ptr(mix), _lib.ptr(ctx), _lib.stream_handle())
         return ctx
@@ -256,11 +308,10 @@ class DchagTrainer:
             A = y_prev[acc:acc + g].reshape(g * R, d)
             if attn:
                 Wc = torch.cat([w[f"{node}.wv"], query_logit_weights(w, node, h)], dim=1)
-                v, lg = _gemm(A, Wc, N_logit=h)
-                V[acc:acc + g] = v.view(g, R, d)
-                L[acc:acc + g] = lg.view(g, R, h)
+                _gemm(A, Wc, N_logit=h, out=V[acc:acc + g].view(g * R, d),
+                      out_l=L[acc:acc + g].view(g * R, h))
             else:
-                V[acc:acc + g] = _gemm(A, w[f"{node}.w"]).view(g, R, d)
+                _gemm(A, w[f"{node}.w"], out=V[acc:acc + g].view(g * R, d))
             acc += g
         mix = None if attn else torch.cat([w[f"{pre}.l{li}.g{gi}.mix"]
                                            for gi in range(len(level))]).float().contiguous()
@@ -268,8 +319,10 @@ class DchagTrainer:
         y = torch.empty(len(level), R, d, device=y_prev.device, dtype=torch.bfloat16)
         for gi in range(len(level)):
             node = f"{pre}.l{li}.g{gi}"
-            y[gi] = (_gemm(ctx[gi], w[f"{node}.wo"], w[f"{node}.bo"]) if attn
-                     else (ctx[gi].float() + w[f"{node}.b"]).to(torch.bfloat16))
+            if attn:
+                _gemm(ctx[gi], w[f"{node}.wo"], w[f"{node}.bo"], out=y[gi])
+            else:
+                torch.add(ctx[gi], w[f"{node}.b"], out=y[gi])
         return V, L, ctx, y
 
     # ---------------------------------------------------------------- backward
@@ -282,8 +335,8 @@ class DchagTrainer:
         gV = torch.empty_like(V)
         dL = torch.empty(nch, R, h, device=V.device, dtype=torch.float32) if mix is None else None
         dm = torch.empty(nch, R, device=V.device, dtype=torch.float32) if mix is not None else None
-        ft = torch.tensor(firsts, device=V.device, dtype=torch.int32)
-        gt = torch.tensor(gs, device=V.device, dtype=torch.int32)
+        ft = self._dev_ints(firsts, torch.int32, V.device)
+        gt = self._dev_ints(gs, torch.int32, V.device)
         _lib.call("dchag_combine_bwd", n, R, d, h, _lib.ptr(ft), _lib.ptr(gt), max(gs),
                   _lib.ptr(V), R * d, _lib.ptr(L), R * h, _lib.ptr(mix), _lib.ptr(_f32(G)),
                   _lib.ptr(dL), _lib.ptr(gV), _lib.ptr(dm), _lib.stream_handle())
@@ -294,7 +347,7 @@ class DchagTrainer:
         the slab's tok.* / channel_id rows, its agg.slab{r}.*, the replicated agg.final.*,
         and special.pos all-reduced over the tp group."""
         _BF_WEIGHTS.clear()
-        _BF_WEIGHTS.update(v.data_ptr() for v in self.fe.weights.values())
+        _BF_WEIGHTS.update(id(v) for v in self.fe.weights.values())
         grads, g_y = self.backward_final(saved, g_out)
         grads.update(self.backward_local(saved, g_y))
         if self.fe.tp > 1:
@@ -465,7 +518,6 @@ class DchagTrainer:
         pp = P * P
         d_tokw = torch.zeros_like(tokw)
         d_tb = torch.zeros_like(tb)
-        d_pos = torch.zeros_like(pos)
         patches = torch.empty(B, cnt, s, pp, device=img.device, dtype=torch.bfloat16)
         _lib.call("dchag_unfold", _lib.ptr(img), img.stride(0), img.stride(1), B, cnt, m.image_h,
                   m.image_w, P, _lib.ptr(patches), _lib.stream_handle())
@@ -476,7 +528,7 @@ class DchagTrainer:
             for g in pk.l0_g_list:
                 poff.append(acc)
                 acc += g * R * h
-            poff_t = torch.tensor(poff, device=img.device, dtype=torch.int64)
+            poff_t = self._dev_ints(poff, torch.int64, img.device)
             pnorm = torch.empty(acc, device=img.device, dtype=torch.bfloat16)
             _lib.call("dchag_l0_logits", _lib.ptr(img), img.stride(0), img.stride(1), B,
                       m.image_h, m.image_w, P, h, pk.HP, pk.NH, pk.n0, max(pk.l0_g_list),
@@ -484,71 +536,94 @@ class DchagTrainer:
                       _lib.ptr(pk.bU), _lib.ptr(pk.posU), _lib.ptr(pnorm), 0,
                       _lib.stream_handle())
         dh = d // h
+        n0 = len(levels[0])
+        wname = "wv" if attn else "w"
+        # positional terms of every node at once (batched tensor-core GEMMs):
+        # posV_n = pos Wv_n, and after the loop d pos = sum_n Gs_n Wv_n^T, d Wv_n += pos^T Gs_n
+        Wv_all = torch.stack([_bfc(w[f"{pre}.l0.g{gi}.{wname}"]) for gi in range(n0)])
+        pos_bf = _bfc(pos)
+        posV_all = torch.bmm(pos_bf.unsqueeze(0).expand(n0, s, d), Wv_all,
+                             out_dtype=torch.float32)                        # [n0, S, D]
+        Gs_all = torch.empty(n0, s, d, device=img.device, dtype=torch.float32)
         c0, p_at = 0, 0
         for gi, g in enumerate(levels[0]):
             node = f"{pre}.l0.g{gi}"
-            Wv = w[f"{node}.wv"] if attn else w[f"{node}.w"]
+            Wv = w[f"{node}.{wname}"]
+            gyb = _bfc(g_y[gi])
             if attn:
                 grads[f"{node}.bo"] = g_y[gi].sum(0)
-                grads[f"{node}.wo"] = _mm(ctx0[gi].t(), g_y[gi])
-                G = _mm(g_y[gi], w[f"{node}.wo"].t())                   # [R, D] fp32
+                grads[f"{node}.wo"] = _mm(ctx0[gi].t(), gyb)
+                Gb = torch.mm(gyb, _bfc(w[f"{node}.wo"]).t())            # [R, D] bf16
             else:
                 grads[f"{node}.b"] = g_y[gi].sum(0)
-                G = _f32(g_y[gi])
-            Gb = G.to(torch.bfloat16)
-            # V_c for the node's channels [g][R][D] (bf16): K = P^2 tcgen05 GEMM
-            Wc = tokw[c0:c0 + g]                                        # [g, PP, D]
-            Mt = _bf(_mm(Wc.reshape(g * pp, d), Wv).view(g, pp, d).transpose(1, 2))  # [g, D, PP]
-            Cb = _mm(tb[c0:c0 + g], Wv).contiguous()                   # [g, D]
-            posV = _bf(_mm(pos, Wv))                                   # [S, D]
-            V = torch.empty(g, R, d, device=img.device, dtype=torch.bfloat16)
-            A = patches[:, c0:c0 + g]
-            _lib.call("dchag_gemm_bf16", _lib.ptr(A), g, B, s, pp, s * pp, cnt * s * pp, pp,
-                      _lib.ptr(Mt), d, d * pp, d, _lib.ptr(Cb), d, _lib.ptr(posV), 0, d, s,
-                      _lib.ptr(V), 0, R * d, s * d, d, 0, 0, 0, 0, _lib.stream_handle())
-            # row stage (one fused kernel): dp, dl, dV = p G  (or mix G and d mix)
+                Gb = gyb
+            # d(Loss)/dV_c = p_c * G per head (bf16, the operand of T_c = patch_c^T dV_c); the
+            # same pass reduces the positional part of dp: Gpos[r, h] = G[r, h] . posV[s, h]
             dV = torch.empty(g, R, d, device=img.device, dtype=torch.bfloat16)
-            Gc = G.contiguous()
+            Gpos = torch.empty(R, h, device=img.device, dtype=torch.float32)
             if attn:
                 pblk = pnorm[p_at:p_at + g * R * h]
                 p_at += g * R * h
-                dl = torch.empty(g, R, h, device=img.device, dtype=torch.float32)
-                _lib.call("dchag_l0_bwd_rows", g, R, d, h, pk.NH, _lib.ptr(V), _lib.ptr(Gc),
-                          _lib.ptr(ctx0[gi]), _lib.ptr(pblk), 0, _lib.ptr(dl), _lib.ptr(dV), 0,
+                _lib.call("dchag_l0_dv", g, R, d, h, pk.NH, _lib.ptr(pblk), 0, _lib.ptr(Gb),
+                          _lib.ptr(posV_all[gi]), s, _lib.ptr(Gpos), _lib.ptr(dV),
                           _lib.stream_handle())
             else:
                 mixv = w[f"{node}.mix"].float().contiguous()
-                dm = torch.empty(g, R, device=img.device, dtype=torch.float32)
-                _lib.call("dchag_l0_bwd_rows", g, R, d, h, 1, _lib.ptr(V), _lib.ptr(Gc), 0, 0,
-                          _lib.ptr(mixv), 0, _lib.ptr(dV), _lib.ptr(dm), _lib.stream_handle())
-                grads[f"{node}.mix"] = dm.sum(1)
+                _lib.call("dchag_l0_dv", g, R, d, h, 1, 0, _lib.ptr(mixv), _lib.ptr(Gb),
+                          _lib.ptr(posV_all[gi]), s, _lib.ptr(Gpos), _lib.ptr(dV),
+                          _lib.stream_handle())
+            # dp_c[r, h] = G[r, h-cols] . V_c[r, h-cols] with V_c = patch_c Mt_c + Cb_c + posV:
+            # the K = P^2 tcgen05 GEMM reduces each 32-column group of V_c against G in its
+            # epilogue (V_c never reaches memory)
+            Wc = tokw[c0:c0 + g]                                        # [g, PP, D]
+            Mt = _bf(_mm(Wc.reshape(g * pp, d), Wv).view(g, pp, d).transpose(1, 2))  # [g, D, PP]
+            Cb = _mm(tb[c0:c0 + g], Wv).contiguous()                   # [g, D]
+            dpp = torch.empty(g, d // 32, R, device=img.device, dtype=torch.float32)
+            A = patches[:, c0:c0 + g]
+            _lib.call("dchag_gemm_rowdot", _lib.ptr(A), g, B, s, pp, s * pp, cnt * s * pp, pp,
+                      _lib.ptr(Mt), d, d * pp, _lib.ptr(Cb), d, _lib.ptr(Gb), d, _lib.ptr(dpp),
+                      _lib.stream_handle())
+            dp = dpp.view(g, h, dh // 32, R).sum(2) + Gpos.t().unsqueeze(0)   # [g, H, R]
+            if attn:
+                pj = pblk.view(h // pk.NH, g, R, pk.NH).permute(1, 0, 3, 2).reshape(g, h, R)
+                pf = pj.float()
+                # softmax backward over the node's channels: dl = p (dp - sum_c p dp)
+                dl = (pf * (dp - (pf * dp).sum(0, keepdim=True))).permute(0, 2, 1).contiguous()
+            else:
+                grads[f"{node}.mix"] = dp.sum((1, 2))
                 dl = None
             pt = patches[:, c0:c0 + g].permute(1, 3, 0, 2).reshape(g, pp, R)   # patch_c^T
-            T = torch.bmm(pt, dV).float()                               # [g, PP, D]
+            T = torch.bmm(pt, dV, out_dtype=torch.float32)              # [g, PP, D]
             if attn:  # colsum_r dV_j = sum_r p_jrh G_r (per head): a small GEMM, not a dV pass
-                pj = pblk.view(h // pk.NH, g, R, pk.NH).permute(1, 0, 3, 2).reshape(g, h, R)
-                colV = torch.bmm(pj.permute(1, 0, 2), _bfc(G).view(R, h, dh).permute(1, 0, 2))
-                colV = colV.float().permute(1, 0, 2).reshape(g, d)     # [g, D]
+                colV = torch.bmm(pj.permute(1, 0, 2), Gb.view(R, h, dh).permute(1, 0, 2),
+                                 out_dtype=torch.float32)
+                colV = colV.permute(1, 0, 2).reshape(g, d)             # [g, D]
             else:
-                colV = w[f"{node}.mix"].float().view(g, 1) * G.sum(0).view(1, d)
+                colV = w[f"{node}.mix"].float().view(g, 1) * Gb.sum(0, dtype=torch.float32).view(1, d)
             dWv = _mm(Wc.reshape(g * pp, d).t(), T.reshape(g * pp, d)) + _mm(tb[c0:c0 + g].t(), colV)
             d_tokw[c0:c0 + g] = _mm(T.reshape(g * pp, d), Wv.t()).view(g, pp, d)
             d_tb[c0:c0 + g] = _mm(colV, Wv.t())
             if attn:
                 U = query_logit_weights(w, node, h)
-                E = torch.bmm(pt, dl.to(torch.bfloat16)).float()        # [g, PP, H]
+                E = torch.bmm(pt, dl.to(torch.bfloat16), out_dtype=torch.float32)  # [g, PP, H]
                 coll = dl.sum(1)                                        # [g, H]
                 dU = _mm(Wc.reshape(g * pp, d).t(), E.reshape(g * pp, h)) + tb[c0:c0 + g].t() @ coll
                 grads.update(_u_backward(w, node, dU, h))
                 d_tokw[c0:c0 + g] += _mm(E.reshape(g * pp, h), U.t()).view(g, pp, d)
                 d_tb[c0:c0 + g] += coll @ U.t()
             # positional term: sum_c dV_c = G (attention, sum_c p = 1) or (sum_c mix_c) G
-            pscale = 1.0 if attn else float(w[f"{node}.mix"].sum())
-            Gs = G.view(B, s, d).sum(0) * pscale
-            d_pos += _mm(Gs, Wv.t())
-            dWv = dWv + _mm(pos.t(), Gs)
-            grads[f"{node}.wv" if attn else f"{node}.w"] = dWv
+            Gs = Gs_all[gi]
+            torch.sum(Gb.view(B, s, d), 0, dtype=torch.float32, out=Gs)
+            if not attn:
+                Gs.mul_(w[f"{node}.mix"].float().sum())
+            grads[f"{node}.{wname}"] = dWv
             c0 += g
+        Gs_bf = Gs_all.to(torch.bfloat16)
+        d_pos = torch.bmm(Gs_bf, Wv_all.transpose(1, 2), out_dtype=torch.float32).sum(0)
+        dWv_pos = torch.bmm(pos_bf.t().unsqueeze(0).expand(n0, d, s), Gs_bf,
+                            out_dtype=torch.float32)                    # [n0, D, D]
+        for gi in range(n0):
+            grads[f"{pre}.l0.g{gi}.{wname}"] += dWv_pos[gi]
         grads["tok.w"] = d_tokw
         grads["tok.b"] = d_tb
         grads["special.channel_id"] = d_tb.clone()
@@ -571,3 +646,15 @@ class DchagTrainer:
                   d, d * pp, d, _lib.ptr(bias), d, _lib.ptr(rb), 0, d, s, _lib.ptr(X), 0,
                   B * s * d, s * d, d, 0, 0, 0, 0, _lib.stream_handle())
         return X
+
+
+class GraphedStep:
+    """A captured training step (DchagTrainer.capture)."""
+
+    def __init__(self, graph, out, grads, launches):
+        self.graph, self.out, self.grads, self.launches = graph, out, grads, launches
+
+    def replay(self):
+        self.graph.replay()
+        _lib.LAUNCH_COUNT["n"] += self.launches
+        return self.grads

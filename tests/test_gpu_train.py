@@ -96,3 +96,32 @@ def test_train_step_matches_autograd(meta):
                               tp=meta["tp"], max_group=meta["max_group"], layer_kind=lk)
     out, grads = _run(dict(meta, layer_kind=lk), w, img, probe)
     _check(out, grads, out_ref, g_ref)
+
+
+@pytest.mark.parametrize("lk", ["cross_attention", "linear"])
+def test_train_step_cuda_graph_replay(lk):
+    """DchagTrainer.capture: the replayed graph recomputes the step on new inputs written
+    into the static buffers, and matches the eager step on those inputs."""
+    from paper_2506_21411_b200 import DchagFrontEnd
+    from paper_2506_21411_b200.train import DchagTrainer
+    fe = DchagFrontEnd(12, 64, 128, 8, 256, 4, max_group=3, agg_layer_kind=lk,
+                       out_dtype=torch.float32)
+    fe.init_weights(seed=3, all_ranks=False)
+    tr = DchagTrainer(fe)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    img = torch.randn(2, 12, 64, 128, device="cuda", generator=gen).to(torch.bfloat16)
+    probe = torch.randn(2, 1, fe.seq, 256, device="cuda", generator=gen)
+    gs = tr.capture(img, probe)
+    assert gs.launches > 0
+    img2 = torch.randn(2, 12, 64, 128, device="cuda", generator=gen).to(torch.bfloat16)
+    probe2 = torch.randn(2, 1, fe.seq, 256, device="cuda", generator=gen)
+    img.copy_(img2)
+    probe.copy_(probe2)
+    grads = {k: v.clone() for k, v in gs.replay().items()}
+    out_g = gs.out.clone()
+    out_e, saved = tr.forward_train(img2)
+    grads_e = tr.backward(saved, probe2)
+    torch.cuda.synchronize()
+    assert torch.equal(out_g, out_e)
+    for k, v in grads_e.items():
+        assert rel_err(grads[k].double().cpu().numpy(), v.double().cpu().numpy()) < 1e-5, k
