@@ -103,11 +103,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int k_steps = args.K / BK;
   const int crank = PAIR ? (int)cluster_rank() : 0;
   const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  // Row-dot mode walks the groups innermost over a contiguous chunk of tiles per CTA, so
+  // consecutive tiles of a CTA share (mt, nt) and the epilogue keeps its dotG rows in
+  // registers across the groups; otherwise tiles are strided over the CTAs, groups outermost.
+  const bool dot_mode = args.dotOut != nullptr;
+  const int chunk = (total_ct + ncl - 1) / ncl;
+  const int ct_begin = dot_mode ? cid * chunk : cid;
+  const int ct_end = dot_mode ? min(total_ct, ct_begin + chunk) : total_ct;
+  const int ct_step = dot_mode ? 1 : ncl;
   auto decode = [&](int ct, int& g, int& mt, int& nt) {
-    g = ct / ctiles_per_g;
-    const int rem = ct - g * ctiles_per_g;
-    const int mc = rem / ctiles_n;
-    nt = rem - mc * ctiles_n;
+    int mc;
+    if (dot_mode) {
+      g = ct % args.G;
+      const int rest = ct / args.G;
+      mc = rest / ctiles_n;
+      nt = rest - mc * ctiles_n;
+    } else {
+      g = ct / ctiles_per_g;
+      const int rem = ct - g * ctiles_per_g;
+      mc = rem / ctiles_n;
+      nt = rem - mc * ctiles_n;
+    }
     mt = mc * CL + crank;
   };
 
@@ -146,7 +162,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       const int w_rows = args.BN / CL;
-      for (int ct = cid; ct < total_ct; ct += ncl) {
+      for (int ct = ct_begin; ct < ct_end; ct += ct_step) {
         int g, mt, nt;
         decode(ct, g, mt, nt);
         const int m0 = mt * GEMM_BM;
@@ -180,7 +196,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int ct = cid; ct < total_ct; ct += ncl) {
+      for (int ct = ct_begin; ct < ct_end; ct += ct_step) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogues drained this accumulator buffer
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * GEMM_BN_MAX;
@@ -230,13 +246,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const bool b_vec = (args.bias_g & 3) == 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cid; t < total_ct; t += ncl) {
+    int prev_mt = -1, prev_nt = -1;
+    uint4 rbv[4][4];  // row bias (or, in row-dot mode, dotG) of this thread's row, 4 groups
+    for (int t = ct_begin; t < ct_end; t += ct_step) {
       int g, mt, nt;
       decode(t, g, mt, nt);
       const int m_row = mt * GEMM_BM + row_in_tile;
       const int mo = m_row / args.Mi, mi = m_row - mo * args.Mi;
       // prefetch this thread's row bias for its column groups (in flight during the wait)
-      uint4 rbv[4][4];
       // row-dot mode: the same registers carry this row's dotG columns instead
       const bool dot = args.dotOut != nullptr;
       const __nv_bfloat16* rb =
@@ -244,8 +261,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           : (args.rowbias && !(args.debug & 2)) ? args.rowbias + (size_t)g * args.rowbias_g +
                              (size_t)(mi % args.rowbias_period) * args.rowbias_row
                        : nullptr;
+      const bool reload = !dot || mt != prev_mt || nt != prev_nt;
+      prev_mt = mt;
+      prev_nt = nt;
 #pragma unroll
       for (int gi = 0; gi < 4; ++gi) {
+        if (!reload) break;
         const int n0 = nt * args.BN + (hf + 2 * gi) * 32;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
