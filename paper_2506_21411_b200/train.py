@@ -470,11 +470,12 @@ class DchagTrainer:
             for gi in range(len(level)):
                 node = f"{pre}.l{li}.g{gi}"
                 if attn:
-                    grads[f"{node}.bo"] = g_y[gi].sum(0)
+                    grads[f"{node}.bo"] = g_y[gi].sum(0, dtype=torch.float32)
                     grads[f"{node}.wo"] = _mm(ctx[gi].t(), g_y[gi])
-                    G[gi] = _mm(g_y[gi], w[f"{node}.wo"].t())
+                    torch.mm(_bfc(g_y[gi]), _bfc(w[f"{node}.wo"]).t(), out_dtype=torch.float32,
+                             out=G[gi])
                 else:
-                    grads[f"{node}.b"] = g_y[gi].sum(0)
+                    grads[f"{node}.b"] = g_y[gi].sum(0, dtype=torch.float32)
                     G[gi] = g_y[gi]
             firsts, acc = [], 0
             for g in level:
@@ -483,7 +484,9 @@ class DchagTrainer:
             mix = None if attn else torch.cat([w[f"{pre}.l{li}.g{gi}.mix"]
                                                for gi in range(len(level))]).float().contiguous()
             gV, dL, dm = self._combine_bwd(V, L, mix, G, firsts, list(level), R)
-            g_prev = torch.empty(y_prev.shape, device=g_y.device, dtype=torch.float32)
+            # bf16 stream gradient (the operand every consumer GEMM takes), written in place:
+            # g_prev = dl U^T, then += gV wv^T (cuBLAS, fp32 accumulation)
+            g_prev = torch.empty(y_prev.shape, device=g_y.device, dtype=torch.bfloat16)
             for gi, (f0, g) in enumerate(zip(firsts, level)):
                 node = f"{pre}.l{li}.g{gi}"
                 Y = y_prev[f0:f0 + g].reshape(g * R, d)
@@ -493,11 +496,13 @@ class DchagTrainer:
                     grads[f"{node}.wv"] = _mm(Y.t(), gv)
                     grads.update(_u_backward(w, node, _mm(Y.t(), dl), h))
                     U = query_logit_weights(w, node, h)
-                    g_prev[f0:f0 + g] = (_mm(gv, w[f"{node}.wv"].t()) + _mm(dl, U.t())).view(g, R, d)
+                    gp = g_prev[f0:f0 + g].view(g * R, d)
+                    torch.mm(dl.to(torch.bfloat16), _bfc(U).t(), out=gp)
+                    gp.addmm_(gv, _bfc(w[f"{node}.wv"]).t())
                 else:
                     grads[f"{node}.w"] = _mm(Y.t(), gv)
                     grads[f"{node}.mix"] = dm[f0:f0 + g].sum(1)
-                    g_prev[f0:f0 + g] = _mm(gv, w[f"{node}.w"].t()).view(g, R, d)
+                    torch.mm(gv, _bfc(w[f"{node}.w"]).t(), out=g_prev[f0:f0 + g].view(g * R, d))
             g_y = g_prev
         # ---- level 0, folded: tokens are never formed (their gradient neither). With
         # x_c = patch_c W_c + b_c + pos (model.py:51-64) and V_c = x_c wv, per node:
@@ -551,11 +556,11 @@ class DchagTrainer:
             Wv = w[f"{node}.{wname}"]
             gyb = _bfc(g_y[gi])
             if attn:
-                grads[f"{node}.bo"] = g_y[gi].sum(0)
+                grads[f"{node}.bo"] = g_y[gi].sum(0, dtype=torch.float32)
                 grads[f"{node}.wo"] = _mm(ctx0[gi].t(), gyb)
                 Gb = torch.mm(gyb, _bfc(w[f"{node}.wo"]).t())            # [R, D] bf16
             else:
-                grads[f"{node}.b"] = g_y[gi].sum(0)
+                grads[f"{node}.b"] = g_y[gi].sum(0, dtype=torch.float32)
                 Gb = gyb
             # d(Loss)/dV_c = p_c * G per head (bf16, the operand of T_c = patch_c^T dV_c); the
             # same pass reduces the positional part of dp: Gpos[r, h] = G[r, h] . posV[s, h]
@@ -607,10 +612,10 @@ class DchagTrainer:
                 U = query_logit_weights(w, node, h)
                 E = torch.bmm(pt, dl.to(torch.bfloat16), out_dtype=torch.float32)  # [g, PP, H]
                 coll = dl.sum(1)                                        # [g, H]
-                dU = _mm(Wc.reshape(g * pp, d).t(), E.reshape(g * pp, h)) + tb[c0:c0 + g].t() @ coll
+                dU = _mm(Wc.reshape(g * pp, d).t(), E.reshape(g * pp, h)) + _mm(tb[c0:c0 + g].t(), coll)
                 grads.update(_u_backward(w, node, dU, h))
                 d_tokw[c0:c0 + g] += _mm(E.reshape(g * pp, h), U.t()).view(g, pp, d)
-                d_tb[c0:c0 + g] += coll @ U.t()
+                d_tb[c0:c0 + g] += _mm(coll, U.t())
             # positional term: sum_c dV_c = G (attention, sum_c p = 1) or (sum_c mix_c) G
             Gs = Gs_all[gi]
             torch.sum(Gb.view(B, s, d), 0, dtype=torch.float32, out=Gs)
