@@ -288,6 +288,7 @@ def b200_arm(args, wl, tp, max_group):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    gstep = None
     if wl.get("train"):
         from paper_2506_21411_b200.train import DchagTrainer
         trainer = DchagTrainer(fe)
@@ -456,6 +457,9 @@ def b200_arm(args, wl, tp, max_group):
             "kernels": kernels,
         }
         print(json.dumps(line), flush=True)
+    if gstep is not None:
+        torch.cuda.synchronize()
+        gstep.graph.reset()  # release the captured NCCL work before the group goes away
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
