@@ -194,26 +194,47 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
         }
       }
     };
-    // pass 1: max only
+    // pass 1: max only. With at most KEEP channels per warp the logits stay in registers, so
+    // the image buffer is free after this pass and the next item's copies start right away
+    // (they overlap the softmax passes); otherwise passes 2/3 recompute them.
+    constexpr int KEEP = 4;
+    const bool keep = g <= KEEP * CS;
+    float Lk[KEEP][NT][4];
     float mx[NT][4];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) mx[nt][e] = -INFINITY;
+    if (keep) {
+#pragma unroll
+      for (int i = 0; i < KEEP; ++i) {
+        const int c = cph + i * CS;
+        if (c < g) {
+          logits(c, Lk[i]);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) mx[nt][e] = fmaxf(mx[nt][e], Lk[i][nt][e]);
+        }
+      }
+    } else {
 #pragma unroll 2
-    for (int c = cph; c < g; c += CS) {
-      float L[NT][4];
-      logits(c, L);
+      for (int c = cph; c < g; c += CS) {
+        float L[NT][4];
+        logits(c, L);
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) mx[nt][e] = fmaxf(mx[nt][e], L[nt][e]);
+          for (int e = 0; e < 4; ++e) mx[nt][e] = fmaxf(mx[nt][e], L[nt][e]);
+      }
     }
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) stat[sidx(cph, nt, e)] = mx[nt][e];
     __syncthreads();
+    const bool early = keep && nbuf == 1 && it + 1 < it1;
+    if (early && threadIdx.x == 0) issue(it + 1, 0);  // every warp is done with the image
     float nmx[NT][4];  // -max * log2(e)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
@@ -241,10 +262,7 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) sm_[nt][e] = 0.f;
-#pragma unroll 2
-    for (int c = cph; c < g; c += CS) {
-      float L[NT][4];
-      logits(c, L);
+    auto pass2 = [&](int c, const float (&L)[NT][4]) {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         float ev[4];
@@ -259,6 +277,18 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
             *reinterpret_cast<uint32_t*>(pn + poff_e[nt][q] + c * cstride) =
                 pack_bf16(ev[2 * q], ev[2 * q + 1]);
         }
+      }
+    };
+    if (keep) {
+#pragma unroll
+      for (int i = 0; i < KEEP; ++i)
+        if (cph + i * CS < g) pass2(cph + i * CS, Lk[i]);
+    } else {
+#pragma unroll 2
+      for (int c = cph; c < g; c += CS) {
+        float L[NT][4];
+        logits(c, L);
+        pass2(c, L);
       }
     }
 #pragma unroll
@@ -290,10 +320,7 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
       }
     } else {
       // pass 3 (normalised output): p = e / sum
-#pragma unroll 2
-      for (int c = cph; c < g; c += CS) {
-        float L[NT][4];
-        logits(c, L);
+      auto pass3 = [&](int c, const float (&L)[NT][4]) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           if (nt * 8 + 2 * tig < a.H) {
@@ -307,10 +334,22 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
             }
           }
         }
+      };
+      if (keep) {
+#pragma unroll
+        for (int i = 0; i < KEEP; ++i)
+          if (cph + i * CS < g) pass3(cph + i * CS, Lk[i]);
+      } else {
+#pragma unroll 2
+        for (int c = cph; c < g; c += CS) {
+          float L[NT][4];
+          logits(c, L);
+          pass3(c, L);
+        }
       }
     }
     __syncthreads();  // item done: its image buffer and the stat area may be reused
-    if (nbuf == 1 && threadIdx.x == 0 && it + 1 < it1) issue(it + 1, 0);
+    if (nbuf == 1 && !early && threadIdx.x == 0 && it + 1 < it1) issue(it + 1, 0);
   }
 }
 
