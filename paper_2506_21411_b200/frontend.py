@@ -99,6 +99,7 @@ class DchagFrontEnd(torch.nn.Module):
         # schedule, so the result is bit-identical; only the bytes moved and the final
         # layer's work per rank shrink by ~tp.
         self.final_position_split = bool(final_position_split)
+        self.ledger = None  # optional ledger.CommLedger: every collective issued is recorded
         if precision not in ("bf16", "fp32"):
             raise ConfigError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
         if precision == "fp32" and agg_variant != "single_query":
@@ -231,6 +232,7 @@ class DchagFrontEnd(torch.nn.Module):
             y = y.contiguous()
             allg = torch.empty((self.tp,) + tuple(y.shape), device=y.device, dtype=y.dtype)
             dist.all_gather_into_tensor(allg, y, group=self.process_group)
+            self._log("AllGather", "forward", "dchag-boundary", y.numel() * y.element_size())
             gathered = allg.squeeze(2).permute(1, 0, 2, 3)                     # [B,tp,S,D]
         else:
             gathered = y
@@ -257,6 +259,7 @@ class DchagFrontEnd(torch.nn.Module):
             import torch.distributed as dist
             allg = torch.empty((self.tp,) + tuple(y.shape), device=y.device, dtype=y.dtype)
             dist.all_gather_into_tensor(allg, y, group=self.process_group)
+            self._log("AllGather", "forward", "dchag-boundary", y.numel() * y.element_size())
             gathered = allg.squeeze(2).permute(1, 0, 2, 3)
         else:
             gathered = y
@@ -412,7 +415,21 @@ class DchagFrontEnd(torch.nn.Module):
         gathered = torch.empty(self.tp * payload.numel(), device=payload.device,
                                dtype=torch.uint8)
         dist.all_gather_into_tensor(gathered, payload, group=self.process_group)
+        self._log("AllGather", "forward", "dchag-boundary", payload.numel())
         return gathered
+
+    def _log(self, op, phase, tag, size):
+        """Record one collective in self.ledger (ledger.py) with the reference's payload
+        accounting. size: shard bytes (AllGather / ReduceScatter output chunk), buffer bytes
+        (AllToAll), or (elements, itemsize) (AllReduce)."""
+        if self.ledger is None:
+            return
+        from . import ledger as LG
+        g = self.tp
+        pay = {"AllGather": LG.allgather_payload, "ReduceScatter": LG.reduce_scatter_payload,
+               "AllToAll": LG.alltoall_payload}.get(op)
+        nbytes = pay(size, g) if pay else LG.allreduce_payload(size[0], size[1], g)
+        self.ledger.record(self.rank, op, "tp", phase, nbytes, tag)
 
     def _position_split(self, B):
         rows = B * self.seq
@@ -439,6 +456,7 @@ class DchagFrontEnd(torch.nn.Module):
         Lx = torch.empty(tp, Rl, h, device=dev, dtype=torch.float32)
         dist.all_to_all_single(Vx, V.view(tp, Rl, d), group=self.process_group)
         dist.all_to_all_single(Lx, L.view(tp, Rl, h), group=self.process_group)
+        self._log("AllToAll", "forward", "dchag-boundary", payload.numel())
         ctx_f = torch.empty(1, Rl, d, device=dev, dtype=torch.bfloat16)
         first = self._final_first(dev)
         _lib.call("dchag_combine", 1, Rl, d, h, _lib.ptr(first[0]), _lib.ptr(first[1]), tp,
@@ -450,6 +468,8 @@ class DchagFrontEnd(torch.nn.Module):
         if out is None:
             out = torch.empty(R, d, device=dev, dtype=self.out_dtype)
         dist.all_gather_into_tensor(out.view(R, d), part, group=self.process_group)
+        self._log("AllGather", "forward", "dchag-final-out",
+                  part.numel() * part.element_size())
         return out.view(B, 1, s, d)
 
     def local_payload(self, img, pk=None):
@@ -580,6 +600,7 @@ class DchagFrontEnd(torch.nn.Module):
                   d, d * kc, d, _lib.ptr(b_loc), d, 0, 0, 0, 1, _lib.ptr(part), 1, R * d, 0, d,
                   0, 0, 0, 0, _lib.stream_handle())
         dist.all_reduce(part, group=self.process_group)
+        self._log("AllReduce", "forward", "agg-final", (part.numel(), part.element_size()))
         out.copy_(part.view_as(out))
         return out.view(B, 1, s, d)
 

@@ -250,6 +250,8 @@ class DchagTrainer:
             y_all = torch.empty((fe.tp,) + tuple(y_root.shape), device=y_root.device,
                                 dtype=torch.bfloat16)
             dist.all_gather_into_tensor(y_all, y_root, group=fe.process_group)
+            fe._log("AllGather", "forward", "dchag-boundary",
+                    y_root.numel() * y_root.element_size())
         else:
             y_all = y_root.unsqueeze(0)
         return self.forward_final(y_all, saved), saved
@@ -353,6 +355,8 @@ class DchagTrainer:
         if self.fe.tp > 1:
             import torch.distributed as dist
             dist.all_reduce(grads["special.pos"], group=self.fe.process_group)
+            self.fe._log("AllReduce", "optimizer", "special.pos",
+                         (grads["special.pos"].numel(), grads["special.pos"].element_size()))
         return grads
 
     def _own_heads(self):
@@ -383,6 +387,7 @@ class DchagTrainer:
         bo = w["agg.final.bo"] if fe.rank == 0 else torch.zeros_like(w["agg.final.bo"])
         out = _gemm(ctx_f[0], w["agg.final.wo"][cols], bo, out_f32=True)
         dist.all_reduce(out, group=fe.process_group)
+        fe._log("AllReduce", "forward", "agg-final", (out.numel(), out.element_size()))
         saved.update(y_all=y_all, Vf=Vf, Lf=Lf, ctx_f=ctx_f)
         return out.view(B, 1, s, d)
 
@@ -414,12 +419,14 @@ class DchagTrainer:
         grads["agg.final.wq"] = gu["agg.final.wq"][:, cols].contiguous()
         q_grad = gu["agg.final.q"].contiguous()
         dist.all_reduce(q_grad, group=fe.process_group)                   # fanout of q
+        fe._log("AllReduce", "backward", "agg-final", (q_grad.numel(), q_grad.element_size()))
         grads["agg.final.q"] = q_grad
         U_own = query_logit_weights(w, "agg.final", h)[:, hs]
         g_part = (_mm(gV, w["agg.final.wv"][:, cols].t()) +
                   dL @ U_own.t()).contiguous()                            # [tp, R, D]
         g_y = torch.empty(R, d, device=g_out.device, dtype=torch.float32)
         dist.reduce_scatter_tensor(g_y, g_part.view(fe.tp * R, d), group=fe.process_group)
+        fe._log("ReduceScatter", "backward", "agg-final", g_y.numel() * g_y.element_size())
         return grads, g_y.view(1, R, d)
 
     def backward_final(self, saved, g_out):

@@ -47,7 +47,19 @@ def main():
                            agg_layer_kind=lk, tp=tp, rank=rank, out_dtype=torch.float32,
                            final_layer_tp_split=split)
         fe.load_weights(w)
+        from paper_2506_21411_b200.ledger import CommLedger
+        fe.ledger = CommLedger()
         out = fe(img_bf.cuda()).cpu().numpy()  # full images: the rank slices its own slab
+        # byte contract (test_strategies.py:195-208 restated for the bf16 payload): the
+        # boundary is one collective per rank in the forward (AllGather of the root payload,
+        # or its position-split all-to-all), nothing in the backward
+        R_ = 8 * (meta["image_h"] // meta["patch"]) * (meta["image_w"] // meta["patch"])
+        pay_ = R_ * (2 * meta["embed"] + 4 * meta["heads"])
+        tot_, n_ = fe.ledger.query(phase="forward", tag="dchag-boundary")
+        want_ = pay_ // tp * (tp - 1) if fe._position_split(8) and not split else pay_ * (tp - 1)
+        if n_ != 1 or tot_ != want_:
+            print(f"rank {rank}: boundary ledger {(tot_, n_)} != ({want_}, 1)", flush=True)
+            worst = max(worst, 1.0)
         if not split:
             fe.final_position_split = False
             out_ag = fe(img_bf.cuda()).cpu().numpy()
@@ -83,8 +95,18 @@ def main():
                            out_dtype=torch.float32, final_layer_tp_split=split)
         fe.load_weights(w)
         trn = DchagTrainer(fe)
+        from paper_2506_21411_b200.ledger import CommLedger
+        fe.ledger = CommLedger()
         out, saved = trn.forward_train(img.cuda())
         grads = trn.backward(saved, torch.from_numpy(probe.astype(np.float32)).cuda())
+        if fe.ledger.query(phase="backward", tag="dchag-boundary") != (0, 0) or \
+                fe.ledger.query(phase="forward", tag="dchag-boundary")[1] != 1:
+            print(f"rank {rank}: training ledger breaks the boundary contract", flush=True)
+            worst = max(worst, 1.0)
+        if rank == 0:
+            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+            fe.ledger.to_csv(os.path.join(ROOT, "gpurun_out", f"ledger_tp{tp}"
+                                          f"{'_split' if split else ''}.csv"))
         off, cnt = fe.slab
         dh = 256 // 4
         hc = 4 // tp
