@@ -109,6 +109,14 @@ int dchag_l0_dv(int g, int R, int D, int H, int nh, const void* p, const float* 
                 const void* G, const float* posV, int period, float* Gpos, void* dV,
                 void* stream);
 
+/* ViT input tokens after the front end (model.py:100-108 apply_token_mask, :111-117 meta
+ * token + concat): out[b][0] = meta_tok[b], out[b][1+s] = agg[b][s] (1 - mask[b][s]) +
+ * mask_token mask[b][s]. agg [B][S][D] and out [B][S+1][D] bf16 (or fp32 if agg_f32);
+ * mask fp32 [B][S], mask_token fp32 [D], meta_tok fp32 [B][D] (= meta @ meta_w + meta_b).
+ * D % 8 == 0. */
+int dchag_vit_tokens(const void* agg, int agg_f32, int B, int seq, int D, const float* mask,
+                     const float* mask_token, const float* meta_tok, void* out, void* stream);
+
 /* fp32 parity mode combine: as dchag_combine with fp32 child values V (row r of child j at
  * V + j*sVj + r*D) and an fp32 context (precise expf, fp32 accumulation). */
 int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,

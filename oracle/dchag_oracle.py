@@ -181,6 +181,22 @@ def dchag_frontend(images, w, *, patch, heads, tp, max_group, variant="single_qu
 # -- parameters ------------------------------------------------------------
 
 
+def apply_token_mask(agg, mask, mask_token):
+    """model.py:100-108: agg [B,1,S,D] * (1 - m) + mask_token * m, m = mask[B,S]."""
+    b, s = mask.shape
+    m = mask.reshape(b, 1, s, 1)
+    return agg * (1.0 - m) + mask_token.reshape(1, 1, 1, -1) * m
+
+
+def vit_input(agg, mask, mask_token, meta, meta_w, meta_b):
+    """model.py:100-108 + :111-117 (the trunk's first two steps): the masked aggregate
+    prefixed by the metadata token, [B, S+1, D]."""
+    b, _, s, d = agg.shape
+    masked = apply_token_mask(agg, mask, mask_token)
+    meta_tok = (meta @ meta_w + meta_b).reshape(b, 1, d)
+    return np.concatenate([meta_tok, masked.reshape(b, s, d)], axis=1)
+
+
 def frontend_param_specs(channels, image_h, image_w, patch, embed, tp, max_group,
                          variant="single_query", layer_kind="cross_attention"):
     """Names/shapes in the reference creation order (params.py:36-57, :99-115),

@@ -327,6 +327,15 @@ int dchag_l0_dv(int g, int R, int D, int H, int nh, const void* p, const float* 
                      "l0_dv");
 }
 
+int dchag_vit_tokens(const void* agg, int agg_f32, int B, int seq, int D, const float* mask,
+                     const float* mask_token, const float* meta_tok, void* out, void* stream) {
+  if (B < 1 || seq < 1 || D < 8 || D % 8 || !agg || !mask || !mask_token || !meta_tok || !out)
+    return fail(DCHAG_ERR_SHAPE, "vit_tokens: bad shape B=%d S=%d D=%d", B, seq, D);
+  return cuda_status(launch_vit_tokens(agg, agg_f32, mask, mask_token, meta_tok, out, B, seq, D,
+                                       S(stream)),
+                     "vit_tokens");
+}
+
 int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
                       int max_g, const float* V, long long sVj, const float* L, long long sLj,
                       const float* mix, float* ctx, void* stream) {

@@ -353,6 +353,62 @@ cudaError_t launch_l0_dv(int g, int R, int D, int H, int NH, const __nv_bfloat16
   return cudaGetLastError();
 }
 
+// ViT input tokens (model.py:100-117 up to the trunk): out[b][0] = meta_tok[b];
+// out[b][1 + s] = agg[b][s] * (1 - mask[b][s]) + mask_token * mask[b][s]. One thread per
+// 8 columns of an output row; rows are contiguous runs in both layouts.
+template <typename T>
+__global__ void __launch_bounds__(256) vit_tokens_kernel(const T* __restrict__ agg,
+                                                        const float* __restrict__ mask,
+                                                        const float* __restrict__ mask_token,
+                                                        const float* __restrict__ meta_tok,
+                                                        T* __restrict__ out, int B, int S, int D) {
+  const int dchunks = D >> 3;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)B * (S + 1) * dchunks) return;
+  const long long row = idx / dchunks;
+  const int d0 = (int)(idx - row * dchunks) * 8;
+  const int b = (int)(row / (S + 1)), j = (int)(row - (long long)b * (S + 1));
+  float v[8];
+  if (j == 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __ldg(meta_tok + (size_t)b * D + d0 + i);
+  } else {
+    const int s = j - 1;
+    const float m = __ldg(mask + (size_t)b * S + s);
+    const T* src = agg + ((size_t)b * S + s) * D + d0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float a;
+      if constexpr (sizeof(T) == 2) a = __bfloat162float(src[i]);
+      else a = src[i];
+      v[i] = a * (1.f - m) + __ldg(mask_token + d0 + i) * m;
+    }
+  }
+  T* dst = out + row * D + d0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if constexpr (sizeof(T) == 2) dst[i] = __float2bfloat16(v[i]);
+    else dst[i] = v[i];
+  }
+}
+
+cudaError_t launch_vit_tokens(const void* agg, int f32, const float* mask,
+                              const float* mask_token, const float* meta_tok, void* out, int B,
+                              int S, int D, cudaStream_t st) {
+  if (D % 8) return cudaErrorInvalidValue;
+  const long long n = (long long)B * (S + 1) * (D / 8);
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  if (f32)
+    vit_tokens_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(agg), mask,
+                                                    mask_token, meta_tok,
+                                                    reinterpret_cast<float*>(out), B, S, D);
+  else
+    vit_tokens_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(agg), mask, mask_token, meta_tok,
+        reinterpret_cast<__nv_bfloat16*>(out), B, S, D);
+  return cudaGetLastError();
+}
+
 // full_cross node weights (see FullCrossArgs). One CTA per (node, row), one warp per head;
 // lane j owns child j (g <= 32): it keeps k_j,h in registers and computes the row of logits
 // L_ij = q_i . k_j / sqrt(dh) against q_i broadcast from shared memory; the per-i softmax,

@@ -128,6 +128,9 @@ struct L0BwdRowsArgs {
   float* dm;                   // [g][R] (linear)
 };
 cudaError_t launch_l0_bwd_rows(const L0BwdRowsArgs& a, cudaStream_t st);
+cudaError_t launch_vit_tokens(const void* agg, int f32, const float* mask,
+                              const float* mask_token, const float* meta_tok, void* out, int B,
+                              int S, int D, cudaStream_t st);
 cudaError_t launch_l0_dv(int g, int R, int D, int H, int NH, const __nv_bfloat16* p,
                          const float* mix, const __nv_bfloat16* G, const float* posV, int S,
                          float* Gpos, __nv_bfloat16* out, cudaStream_t st);

@@ -319,6 +319,31 @@ class DchagFrontEnd(torch.nn.Module):
             res = out
         return (res, gathered) if return_payload else res
 
+    def vit_input(self, images, mask, mask_token, meta, meta_w, meta_b, out=None):
+        """Front end + the trunk's input assembly: the aggregate with masked
+        positions replaced by the mask token (model.py:100-108 apply_token_mask) and the
+        metadata token prepended (model.py:111-117) -> [B, S+1, D] in out_dtype.
+        mask [B, S] (1 = masked), mask_token [D] (`dec.mask`), meta [B, 4],
+        meta_w [4, D] / meta_b [D] (`special.meta_w/b`)."""
+        agg = self(images)
+        B, S, D = agg.shape[0], self.seq, self.model.embed
+        dev = agg.device
+        mask = torch.as_tensor(mask, device=dev, dtype=torch.float32).reshape(B, S).contiguous()
+        mtok = torch.as_tensor(mask_token, device=dev, dtype=torch.float32).reshape(D).contiguous()
+        meta = torch.as_tensor(meta, device=dev, dtype=torch.float32).reshape(B, -1)
+        meta_tok = (meta @ torch.as_tensor(meta_w, device=dev, dtype=torch.float32)
+                    + torch.as_tensor(meta_b, device=dev, dtype=torch.float32)).contiguous()
+        if out is None:
+            out = torch.empty(B, S + 1, D, device=dev, dtype=self.out_dtype)
+        elif tuple(out.shape) != (B, S + 1, D) or out.dtype != self.out_dtype or \
+                not out.is_contiguous() or out.device != dev:
+            raise ConfigError(f"out must be a contiguous {self.out_dtype} tensor of shape "
+                              f"{(B, S + 1, D)} on {dev}")
+        _lib.call("dchag_vit_tokens", _lib.ptr(agg), int(agg.dtype == torch.float32), B, S, D,
+                  _lib.ptr(mask), _lib.ptr(mtok), _lib.ptr(meta_tok), _lib.ptr(out),
+                  _lib.stream_handle())
+        return out
+
     def _forward_host(self, images, pk, out, h2d_chunks):
         """Chunked H2D -> kernels -> (D2H) pipeline for host-resident images."""
         b, cnt, himg, wimg = images.shape

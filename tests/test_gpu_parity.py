@@ -367,3 +367,39 @@ def test_fp32_module_matches_oracle(meta):
     torch.cuda.synchronize()
     err = rel_err(y.cpu().numpy(), want)
     assert err < FP32_TOL, err
+
+
+@pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
+def test_vit_input_matches_oracle(out_dtype):
+    """front end + apply_token_mask + metadata token (model.py:100-117) through
+    dchag_vit_tokens, against the oracle restatement; fp32 masks with 0/1 and fractional
+    values (the reference formula agg (1 - m) + tok m)."""
+    from paper_2506_21411_b200 import DchagFrontEnd
+    meta = CONFIGS[0]
+    specs = O.frontend_param_specs(meta["channels"], meta["image_h"], meta["image_w"],
+                                   meta["patch"], meta["embed"], 1, meta["max_group"])
+    w = O.random_params(specs, seed=5, std=0.05, bias_std=0.02)
+    w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
+    rng = np.random.default_rng(8)
+    images = _bf(rng.standard_normal((2, meta["channels"], meta["image_h"], meta["image_w"])))
+    images = images.float().numpy().astype(np.float64)
+    fe = DchagFrontEnd(meta["channels"], meta["image_h"], meta["image_w"], meta["patch"],
+                       meta["embed"], meta["heads"], max_group=meta["max_group"],
+                       out_dtype=out_dtype)
+    fe.load_weights(w)
+    S, D = fe.seq, meta["embed"]
+    mask = (rng.random((2, S)) < 0.75).astype(np.float64)
+    mask[1, :7] = 0.25
+    mtok = rng.standard_normal(D) * 0.02
+    md = rng.standard_normal((2, 4))
+    mw, mb = rng.standard_normal((4, D)) * 0.02, rng.standard_normal(D) * 0.01
+    got = fe.vit_input(_bf(images).cuda(), mask, mtok, md, mw, mb).float().cpu().numpy()
+    agg = O.dchag_frontend(images, w, patch=meta["patch"], heads=meta["heads"], tp=1,
+                           max_group=meta["max_group"])
+    want = O.vit_input(agg, mask, mtok, md, mw, mb)
+    assert got.shape == (2, S + 1, D)
+    assert rel_err(got, want) < BF16_TOL
+    # unmasked rows are the front end's output bit for bit
+    y = fe(_bf(images).cuda()).float().cpu().numpy()[:, 0]
+    keep = mask == 0
+    assert np.array_equal(got[:, 1:][keep], y[keep])

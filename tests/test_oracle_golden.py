@@ -51,3 +51,34 @@ def test_unfold_layout():
     # token s = i*wp + j, pixel k = py*P + px (tensor.py:303-323)
     i, j, py, px = 1, 2, 3, 1
     assert p[0, 1, i * 3 + j, py * 4 + px] == x[0, 1, i * 4 + py, j * 4 + px]
+
+
+def test_vit_input_restatement_matches_reference():
+    """oracle.vit_input vs the reference apply_token_mask + vit_forward's input assembly
+    (model.py:100-117), run here from /root/reference (depth-0 trunk returns its input)."""
+    import os
+    import sys
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference tree not mounted")
+    sys.path.insert(0, ref)
+    try:
+        from dchag.config import ModelConfig
+        from dchag.model import apply_token_mask, vit_forward
+        from dchag.tensor import Tensor
+    finally:
+        sys.path.remove(ref)
+    rng = np.random.default_rng(3)
+    B, S, D = 2, 16, 8
+    agg = rng.standard_normal((B, 1, S, D))
+    mask = (rng.random((B, S)) < 0.5).astype(np.float64)
+    mtok, meta = rng.standard_normal(D), rng.standard_normal((B, 4))
+    mw, mb = rng.standard_normal((4, D)), rng.standard_normal(D)
+    model = ModelConfig(channels=2, image_h=16, image_w=16, patch=4, embed=D, heads=2,
+                        depth=0, decoder_depth=0, decoder_dim=8)
+    x = apply_token_mask(Tensor(agg), mask, Tensor(mtok))
+    ref_out = vit_forward(x, Tensor(meta), {"special.meta_w": Tensor(mw),
+                                            "special.meta_b": Tensor(mb)}, model)
+    want = np.asarray(ref_out.data)
+    got = O.vit_input(agg, mask, mtok, meta, mw, mb)
+    assert np.allclose(got, want, rtol=0, atol=1e-12)
