@@ -345,11 +345,14 @@ def b200_arm(args, wl, tp, max_group):
     def reset(_):
         idx["i"] = 0
 
+    # per-kernel events follow the launch plan of one unchunked forward
+    chunks, fe.comm_chunks = fe.comm_chunks, 1
     _lib.set_launch_hook(hook)
     try:
         timed(step_inf, args.steps, per_step_hook=reset)
     finally:
         _lib.set_launch_hook(None)
+        fe.comm_chunks = chunks
     for site, a, b in events:
         site_ms[site] += a.elapsed_time(b) / args.steps
     kernels = []
@@ -369,11 +372,18 @@ def b200_arm(args, wl, tp, max_group):
     except Exception:
         pass
     if tensor_bound:
-        roof = {"bound": "tensor", "achieved": dom["tflops"], "peak": peak_sus,
-                "unit": "TFLOP/s", "frac": dom["tflops"] / peak_sus, "traffic": traffic,
+        # the sustained figure is cuBLAS back to back under the power cap; a kernel that
+        # beats it in this run is measured against the burst figure instead (never frac > 1)
+        use_burst = dom["tflops"] > peak_sus
+        peak_t = peak_burst if use_burst else peak_sus
+        roof = {"bound": "tensor", "achieved": dom["tflops"], "peak": peak_t,
+                "unit": "TFLOP/s", "frac": dom["tflops"] / peak_t, "traffic": traffic,
                 "kernel": f"{dom['kernel']}[{dom['site']}]",
                 "flops_per_launch": dom_plan[2], "launch_ms": dom["ms"],
-                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside the step)"}
+                "peak_source": (f"{peak_src} bf16_tflops (burst: the kernel ran above the "
+                                f"sustained {peak_sus})" if use_burst else
+                                f"{peak_src} bf16_tflops_sustained (kernel timed inside the "
+                                f"step)")}
     else:
         roof = {"bound": "hbm", "achieved": dom["gbs"], "peak": hbm, "unit": "GB/s",
                 "frac": dom["gbs"] / hbm, "traffic": traffic,

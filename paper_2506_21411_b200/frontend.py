@@ -21,6 +21,8 @@ from __future__ import annotations
 
 import math
 
+import os
+
 import torch
 
 from . import _lib
@@ -100,6 +102,10 @@ class DchagFrontEnd(torch.nn.Module):
         # layer's work per rank shrink by ~tp.
         self.final_position_split = bool(final_position_split)
         self.ledger = None  # optional ledger.CommLedger: every collective issued is recorded
+        # tp > 1 device forward: batch chunks whose exchange overlaps the next chunk's kernels
+        # (measured on 2 B200 at H2: 1 chunk 20.7k img/s, 2 chunks 18.9k, 4 chunks 18.3k --
+        # the exchange is short and smaller launches lose more, so off by default)
+        self.comm_chunks = int(os.environ.get("DCHAG_COMM_CHUNKS", "1"))
         if precision not in ("bf16", "fp32"):
             raise ConfigError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
         if precision == "fp32" and agg_variant != "single_query":
@@ -307,8 +313,15 @@ class DchagFrontEnd(torch.nn.Module):
             images = images.to(torch.bfloat16)
         if images.stride(3) != 1 or images.stride(2) != wimg:
             images = images.contiguous()
-        payload = self.local_payload(images, pk)
         dev_out = out if out is not None and out.is_cuda else None
+        nc = self._comm_chunks(images.shape[0])
+        if not return_payload and nc > 1:
+            res = self._forward_pipelined(images, pk, dev_out, nc)
+            if out is not None and not out.is_cuda:
+                out.copy_(res, non_blocking=True)
+                res = out
+            return res
+        payload = self.local_payload(images, pk)
         if return_payload or not self._position_split(images.shape[0]):
             gathered = self.gather(payload)
             res = self.finish(gathered, images.shape[0], out=dev_out)
@@ -456,32 +469,55 @@ class DchagFrontEnd(torch.nn.Module):
         nbytes = pay(size, g) if pay else LG.allreduce_payload(size[0], size[1], g)
         self.ledger.record(self.rank, op, "tp", phase, nbytes, tag)
 
+    def _comm_chunks(self, B):
+        """Batch chunks of the pipelined tp > 1 forward (1 = no pipelining)."""
+        n = self.comm_chunks
+        while n > 1 and (B % n or not self._position_split(B // n)):
+            n -= 1
+        return n if self.tp > 1 else 1
+
     def _position_split(self, B):
         rows = B * self.seq
         return (self.final_position_split and self.tp > 1
                 and not self.strategy.final_layer_tp_split
                 and rows % (self.tp * 128) == 0)
 
-    def exchange_finish(self, payload, B, out=None):
-        """Position-split final layer: rank j receives rows [j R/tp, (j+1) R/tp) of every
-        rank's root payload (one all-to-all of V and one of L), combines those tp streams
-        and applies the final projection on its R/tp rows, and the outputs are all-gathered
-        in rank (= row) order. Same per-row math as gather() + finish()."""
+    def exchange_start(self, payload, B, async_op=False):
+        """First half of the position-split final layer: rank j receives rows
+        [j R/tp, (j+1) R/tp) of every rank's root payload (one all-to-all of V, one of L).
+        With async_op the exchange runs on NCCL's stream while later kernels proceed."""
         import torch.distributed as dist
+        m = self.model
+        d, h = m.embed, m.heads
+        R = B * self.seq
+        tp = self.tp
+        Rl = R // tp
+        dev = payload.device
+        V, L = views(payload, R, d, h)
+        Vx = torch.empty(tp, Rl, d, device=dev, dtype=torch.bfloat16)
+        Lx = torch.empty(tp, Rl, h, device=dev, dtype=torch.float32)
+        w1 = dist.all_to_all_single(Vx, V.view(tp, Rl, d), group=self.process_group,
+                                    async_op=async_op)
+        w2 = dist.all_to_all_single(Lx, L.view(tp, Rl, h), group=self.process_group,
+                                    async_op=async_op)
+        self._log("AllToAll", "forward", "dchag-boundary", payload.numel())
+        return (B, Vx, Lx, (w1, w2) if async_op else ())
+
+    def exchange_complete(self, state, out=None, async_op=False):
+        """Second half: combine the tp streams of this rank's R/tp rows, final projection,
+        all-gather of the outputs in rank (= row) order. Returns (out, pending work)."""
+        import torch.distributed as dist
+        B, Vx, Lx, works = state
+        for wk in works:
+            wk.wait()  # the current stream waits for the exchange
         pk = self.prepare()
         m = self.model
         d, h, s = m.embed, m.heads, self.seq
         R = B * s
         tp = self.tp
         Rl = R // tp
-        dev = payload.device
+        dev = Vx.device
         st = _lib.stream_handle()
-        V, L = views(payload, R, d, h)
-        Vx = torch.empty(tp, Rl, d, device=dev, dtype=torch.bfloat16)
-        Lx = torch.empty(tp, Rl, h, device=dev, dtype=torch.float32)
-        dist.all_to_all_single(Vx, V.view(tp, Rl, d), group=self.process_group)
-        dist.all_to_all_single(Lx, L.view(tp, Rl, h), group=self.process_group)
-        self._log("AllToAll", "forward", "dchag-boundary", payload.numel())
         ctx_f = torch.empty(1, Rl, d, device=dev, dtype=torch.bfloat16)
         first = self._final_first(dev)
         _lib.call("dchag_combine", 1, Rl, d, h, _lib.ptr(first[0]), _lib.ptr(first[1]), tp,
@@ -492,10 +528,38 @@ class DchagFrontEnd(torch.nn.Module):
                   int(self.out_dtype == torch.float32), Rl * d, 0, d, 0, 0, 0, 0, st)
         if out is None:
             out = torch.empty(R, d, device=dev, dtype=self.out_dtype)
-        dist.all_gather_into_tensor(out.view(R, d), part, group=self.process_group)
+        wk = dist.all_gather_into_tensor(out.view(R, d), part, group=self.process_group,
+                                         async_op=async_op)
         self._log("AllGather", "forward", "dchag-final-out",
                   part.numel() * part.element_size())
-        return out.view(B, 1, s, d)
+        return out.view(B, 1, s, d), wk
+
+    def exchange_finish(self, payload, B, out=None):
+        """Position-split final layer: exchange_start + exchange_complete, synchronous.
+        Same per-row math as gather() + finish()."""
+        res, _ = self.exchange_complete(self.exchange_start(payload, B), out)
+        return res
+
+    def _forward_pipelined(self, images, pk, out, n):
+        """tp > 1, device images: the batch in n chunks, so the all-to-all of chunk k runs on
+        NCCL's stream while the slab kernels of chunk k+1 run (positions are independent:
+        same results as one chunk)."""
+        b = images.shape[0]
+        bounds = [(k * b) // n for k in range(n + 1)]
+        res = out if out is not None else torch.empty(b, 1, self.seq, self.model.embed,
+                                                      device=images.device, dtype=self.out_dtype)
+        states = []
+        for k in range(n):
+            pay = self.local_payload(images[bounds[k]:bounds[k + 1]], pk)
+            states.append(self.exchange_start(pay, bounds[k + 1] - bounds[k], async_op=True))
+        works = []
+        for k in range(n):
+            _, wk = self.exchange_complete(states[k], out=res[bounds[k]:bounds[k + 1]],
+                                           async_op=True)
+            works.append(wk)
+        for wk in works:
+            wk.wait()
+        return res
 
     def local_payload(self, img, pk=None):
         """Rank-local part: slab tree -> root payload [V bf16 R*D | L fp32 R*H] (bytes),

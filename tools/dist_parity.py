@@ -57,8 +57,9 @@ def main():
         pay_ = R_ * (2 * meta["embed"] + 4 * meta["heads"])
         tot_, n_ = fe.ledger.query(phase="forward", tag="dchag-boundary")
         want_ = pay_ // tp * (tp - 1) if fe._position_split(8) and not split else pay_ * (tp - 1)
-        if n_ != 1 or tot_ != want_:
-            print(f"rank {rank}: boundary ledger {(tot_, n_)} != ({want_}, 1)", flush=True)
+        nev_ = fe._comm_chunks(8) if not split else 1   # one exchange per batch chunk
+        if n_ != nev_ or tot_ != want_:
+            print(f"rank {rank}: boundary ledger {(tot_, n_)} != ({want_}, {nev_})", flush=True)
             worst = max(worst, 1.0)
         if not split:
             fe.final_position_split = False
