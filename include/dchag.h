@@ -104,7 +104,7 @@ int dchag_l0_bwd_rows(int g, int R, int D, int H, int nh, const void* V, const f
  * ([H/nh][g][R][nh] bf16), or dV[c] = mix[c] * G for linear nodes (mix != NULL). With posV
  * (fp32 [S][D], row r uses r % S) also Gpos[r][h] = sum_{d in head h} G[r][d] posV[r % S][d]
  * (fp32 [R][H]), the positional part of dp = G . V. G, dV bf16 [R][D] / [g][R][D], 16-byte
- * aligned; D/H a power of two in 8..256. */
+ * aligned; D/H a power of two in 8..256. dV == NULL computes Gpos only. */
 int dchag_l0_dv(int g, int R, int D, int H, int nh, const void* p, const float* mix,
                 const void* G, const float* posV, int period, float* Gpos, void* dV,
                 void* stream);
@@ -116,6 +116,16 @@ int dchag_l0_dv(int g, int R, int D, int H, int nh, const void* p, const float* 
  * D % 8 == 0. */
 int dchag_vit_tokens(const void* agg, int agg_f32, int B, int seq, int D, const float* mask,
                      const float* mask_token, const float* meta_tok, void* out, void* stream);
+
+/* Level-0 node backward, token-weight gradient (training; the patches^T . dtokens of
+ * tensor.py:168-188 differentiated, with the node's dV = p . G folded in so dV is never
+ * stored): T[c][k][d] = sum_r patch_c[r][k] p_c[r][h(d)] G[r][d] for the node's channels
+ * c0 .. c0+g-1 of `patches` ([B][cnt][S][PP] bf16), p as dchag_l0_dv (or mix for linear
+ * nodes), G bf16 [R][D], T fp32 [g][PP][D]. PP == 64, D % 128 == 0, S % 64 == 0,
+ * D/H in {64, 128}, nh even. */
+int dchag_l0_tgrad(const void* patches, int cnt, int c0, int g, int R, int seq, int D, int H,
+                   int nh, int PP, const void* p, const float* mix, const void* G, float* T,
+                   void* stream);
 
 /* fp32 parity mode combine: as dchag_combine with fp32 child values V (row r of child j at
  * V + j*sVj + r*D) and an fp32 context (precise expf, fp32 accumulation). */

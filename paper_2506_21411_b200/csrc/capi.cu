@@ -313,7 +313,8 @@ int dchag_l0_bwd_rows(int g, int R, int D, int H, int nh, const void* V, const f
 
 int dchag_l0_dv(int g, int R, int D, int H, int nh, const void* p, const float* mix,
                 const void* G, const float* posV, int period, float* Gpos, void* dV, void* stream) {
-  if (!mix && !p) return fail(DCHAG_ERR_SHAPE, "l0_dv: need p or mix");
+  if (!mix && !p && dV) return fail(DCHAG_ERR_SHAPE, "l0_dv: need p or mix");
+  if (!dV && !posV) return fail(DCHAG_ERR_SHAPE, "l0_dv: nothing to compute");
   const int dh = H > 0 ? D / H : 0;
   if (H < 1 || D % H || dh % 8 || dh > 256 || ((dh / 8) & (dh / 8 - 1)) ||
       ((long long)R * (D / 8)) % 32 || (!mix && (nh < 1 || H % nh)) ||
@@ -334,6 +335,23 @@ int dchag_vit_tokens(const void* agg, int agg_f32, int B, int seq, int D, const 
   return cuda_status(launch_vit_tokens(agg, agg_f32, mask, mask_token, meta_tok, out, B, seq, D,
                                        S(stream)),
                      "vit_tokens");
+}
+
+int dchag_l0_tgrad(const void* patches, int cnt, int c0, int g, int R, int seq, int D, int H,
+                   int nh, int PP, const void* p, const float* mix, const void* G, float* T,
+                   void* stream) {
+  if (!mix && !p) return fail(DCHAG_ERR_SHAPE, "l0_tgrad: need p or mix");
+  if (H < 1 || D % H || D % 128 || R % 64 || seq % 64 || R % seq || PP != 64 ||
+      (D / H != 64 && D / H != 128) || (!mix && (nh < 2 || nh % 2 || H % nh)) ||
+      (reinterpret_cast<uintptr_t>(patches) | reinterpret_cast<uintptr_t>(G)) % 16)
+    return fail(DCHAG_ERR_SHAPE, "l0_tgrad: bad shape R=%d S=%d D=%d H=%d PP=%d", R, seq, D, H,
+                PP);
+  L0TgradArgs a;
+  a.patches = reinterpret_cast<const __nv_bfloat16*>(patches);
+  a.cnt = cnt; a.c0 = c0; a.g = g; a.R = R; a.S = seq; a.D = D; a.H = H; a.NH = nh; a.PP = PP;
+  a.p = reinterpret_cast<const __nv_bfloat16*>(p); a.mix = mix;
+  a.G = reinterpret_cast<const __nv_bfloat16*>(G); a.T = T;
+  return cuda_status(launch_l0_tgrad(a, S(stream)), "l0_tgrad");
 }
 
 int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,

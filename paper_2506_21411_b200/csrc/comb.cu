@@ -6,6 +6,8 @@
 //   ctx[r, h-blk] = sum_j softmax_j(L_j[r,h]) * V_j[r, h-blk]       (layers.py:103-123)
 // or, for a linear node, ctx[r,:] = sum_j mix_j V_j[r,:]             (layers.py:141-146).
 // HBM-bound: reads g*D bf16 + g*H fp32 per row, writes D bf16.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "dchag_kernels.h"
 
@@ -328,6 +330,7 @@ __global__ void __launch_bounds__(256) l0_dv_kernel(int g, int R, int D, int H, 
     for (int off = lanes >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     if ((threadIdx.x & (lanes - 1)) == 0) Gpos[(size_t)r * H + h] = acc;
   }
+  if (!out) return;  // positional dp only
   for (int c = 0; c < g; ++c) {
     const float pc = mix ? __ldg(mix + c)
                          : __bfloat162float(p[((size_t)(hg * g + c) * R + r) * NH + hn]);
@@ -406,6 +409,186 @@ cudaError_t launch_vit_tokens(const void* agg, int f32, const float* mask,
     vit_tokens_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(agg), mask, mask_token, meta_tok,
         reinterpret_cast<__nv_bfloat16*>(out), B, S, D);
+  return cudaGetLastError();
+}
+
+// Level-0 backward token-weight gradient without dV in memory (training):
+//   T_c[k][d] = sum_r patch_c[r][k] * p_c[r][h(d)] * G[r][d]      (= patch_c^T dV_c)
+// One CTA per (channel c, 128 columns of d); 8 warps, warp = 32 k x 32 d (one head);
+// the reduction over all R rows runs through 64-row chunks staged by cp.async (double
+// buffered, 16-byte XOR swizzle for conflict-free ldmatrix). The A operand patch^T comes
+// from ldmatrix.trans and is scaled by p of the warp's head in registers; B = G by
+// ldmatrix.trans; mma.sync m16n8k16 bf16 -> fp32.
+DEV void mma16816_tg(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+DEV void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+DEV void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+DEV void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+DEV uint32_t scale_bf16x2(uint32_t v, float s0, float s1) {
+  return pack_bf16(bf16lo(v) * s0, bf16hi(v) * s1);
+}
+
+constexpr int TG_ROWS = 64;                               // rows per chunk
+constexpr int TG_G_BYTES = TG_ROWS * 128 * 2;             // G tile: 64 rows x 128 d
+constexpr int TG_P_BYTES = TG_ROWS * 64 * 2;              // patch tile: 64 rows x 64 k
+constexpr int TG_S_BYTES = TG_ROWS * 4;                   // p word (2 heads, bf16) per row
+constexpr int TG_BUF = TG_G_BYTES + TG_P_BYTES + TG_S_BYTES;
+
+__global__ void __launch_bounds__(256, 3) l0_tgrad_kernel(L0TgradArgs a) {
+  extern __shared__ __align__(128) uint8_t tg_smem[];
+  const int c = blockIdx.y;
+  const int d0 = blockIdx.x * 128;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int dh = a.D / a.H;
+  const int hA = d0 / dh;
+  const uint32_t sbase = smem_u32(tg_smem);
+  // row split: CTA z reduces chunks [z n / RS, (z+1) n / RS) and adds into T (pre-zeroed)
+  const int nall = a.R / TG_ROWS, RS = gridDim.z;
+  const int cbeg = (int)((long long)blockIdx.z * nall / RS);
+  const int nchunks = (int)((long long)(blockIdx.z + 1) * nall / RS) - cbeg;
+  auto load = [&](int i, int buf) {
+    const uint32_t sg = sbase + buf * TG_BUF, sp = sg + TG_G_BYTES;
+    uint8_t* ss = tg_smem + buf * TG_BUF;
+    const int r0 = (cbeg + i) * TG_ROWS;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {  // G: 64 rows x 16 chunks
+      const int q = threadIdx.x + t * 256, row = q >> 4, ch = q & 15;
+      cp_async16(sg + row * 256 + ((ch ^ (row & 7)) << 4),
+                 a.G + (size_t)(r0 + row) * a.D + d0 + ch * 8);
+    }
+    const int b = r0 / a.S, s0 = r0 - b * a.S;
+    const __nv_bfloat16* pbase = a.patches + (((size_t)b * a.cnt + a.c0 + c) * a.S + s0) * 64;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {  // patch: 64 rows x 8 chunks
+      const int q = threadIdx.x + t * 256, row = q >> 3, ch = q & 7;
+      cp_async16(sp + row * 128 + ((ch ^ (row & 7)) << 4), pbase + (size_t)row * 64 + ch * 8);
+    }
+    if (!a.mix && threadIdx.x < TG_ROWS) {
+      // p of the row's head pair (hA & ~1, +1): one 4-byte word of the [..][R][NH] layout
+      const int row = threadIdx.x, hg = hA / a.NH, hn = (hA - hg * a.NH) & ~1;
+      cp_async4(sg + TG_G_BYTES + TG_P_BYTES + row * 4,
+                a.p + ((size_t)(hg * a.g + c) * a.R + r0 + row) * a.NH + hn);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    (void)ss;
+  };
+  const int mbase = 32 * (warp & 1);   // k rows of this warp
+  const int nbase = 32 * (warp >> 1);  // d columns (within the CTA's 128)
+  // half of the row's p word this warp uses: its head's parity (the word holds hA & ~1, +1)
+  const int hw = (d0 + nbase) / dh;
+  const int sel = hw & 1;
+  const float mixc = a.mix ? __ldg(a.mix + c) : 0.f;
+  float acc[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.f;
+  load(0, 0);
+  for (int i = 0; i < nchunks; ++i) {
+    const int buf = i & 1;
+    if (i + 1 < nchunks) {
+      load(i + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t sg = sbase + buf * TG_BUF, sp = sg + TG_G_BYTES;
+    const uint32_t* ss = reinterpret_cast<const uint32_t*>(tg_smem + buf * TG_BUF +
+                                                           TG_G_BYTES + TG_P_BYTES);
+    auto pval = [&](int r) {
+      if (a.mix) return mixc;
+      const uint32_t w = ss[r];
+      return sel ? bf16hi(w) : bf16lo(w);
+    };
+    const int j8 = lane >> 3, i8 = lane & 7;
+#pragma unroll
+    for (int kb = 0; kb < TG_ROWS; kb += 16) {
+      // p of the 4 K indices this thread's A fragments carry
+      const float p0 = pval(kb + 2 * tig), p1 = pval(kb + 2 * tig + 1);
+      const float p8 = pval(kb + 2 * tig + 8), p9 = pval(kb + 2 * tig + 9);
+      uint32_t af[2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int r = kb + i8 + 8 * (j8 >> 1);
+        const int col = mbase + mt * 16 + 8 * (j8 & 1);
+        ldsm_x4_t(sp + r * 128 + (((col >> 3) ^ (r & 7)) << 4), af[mt]);
+        af[mt][0] = scale_bf16x2(af[mt][0], p0, p1);
+        af[mt][1] = scale_bf16x2(af[mt][1], p0, p1);
+        af[mt][2] = scale_bf16x2(af[mt][2], p8, p9);
+        af[mt][3] = scale_bf16x2(af[mt][3], p8, p9);
+      }
+#pragma unroll
+      for (int np = 0; np < 2; ++np) {
+        uint32_t bf[4];
+        const int r = kb + i8 + 8 * (j8 & 1);
+        const int col = nbase + np * 16 + 8 * (j8 >> 1);
+        ldsm_x4_t(sg + r * 256 + (((col >> 3) ^ (r & 7)) << 4), bf);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          mma16816_tg(acc[mt][2 * np], af[mt], bf[0], bf[1]);
+          mma16816_tg(acc[mt][2 * np + 1], af[mt], bf[2], bf[3]);
+        }
+      }
+    }
+    __syncthreads();  // the buffer is refilled by the next iteration's load
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int m = mbase + mt * 16 + gid;
+      const int d = d0 + nbase + nt * 8 + 2 * tig;
+      float* o = a.T + ((size_t)c * 64 + m) * a.D + d;
+      if (RS == 1) {
+        *reinterpret_cast<float2*>(o) = make_float2(acc[mt][nt][0], acc[mt][nt][1]);
+        *reinterpret_cast<float2*>(o + 8 * (size_t)a.D) =
+            make_float2(acc[mt][nt][2], acc[mt][nt][3]);
+      } else {
+        atomicAdd(o, acc[mt][nt][0]);
+        atomicAdd(o + 1, acc[mt][nt][1]);
+        atomicAdd(o + 8 * (size_t)a.D, acc[mt][nt][2]);
+        atomicAdd(o + 8 * (size_t)a.D + 1, acc[mt][nt][3]);
+      }
+    }
+}
+
+cudaError_t launch_l0_tgrad(const L0TgradArgs& a, cudaStream_t st) {
+  const int dh = a.D / a.H;
+  if (a.D % 128 || a.R % TG_ROWS || a.S % TG_ROWS || (dh != 64 && dh != 128) || a.PP != 64 ||
+      (!a.mix && a.NH % 2))
+    return cudaErrorInvalidValue;
+  const int smem = 2 * TG_BUF;
+  cudaError_t e = cudaFuncSetAttribute(l0_tgrad_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  // enough CTAs for ~3 per SM: split the row reduction (partials added atomically)
+  const int base = (a.D / 128) * a.g;
+  // measured (TR node, one B200): rs 1/2 0.225 ms, rs 4 0.194, rs 8 0.196
+  int rs = 1;
+  while (rs < 4 && base * rs < 6 * 148 && (a.R / TG_ROWS) / (rs * 2) >= 8) rs *= 2;
+  if (const char* f = getenv("DCHAG_TG_RS")) rs = atoi(f) > 0 ? atoi(f) : rs;
+  if (rs > 1) {
+    e = cudaMemsetAsync(a.T, 0, sizeof(float) * (size_t)a.g * a.PP * a.D, st);
+    if (e != cudaSuccess) return e;
+  }
+  l0_tgrad_kernel<<<dim3(a.D / 128, a.g, rs), 256, smem, st>>>(a);
   return cudaGetLastError();
 }
 

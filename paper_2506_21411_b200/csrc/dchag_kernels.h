@@ -128,6 +128,18 @@ struct L0BwdRowsArgs {
   float* dm;                   // [g][R] (linear)
 };
 cudaError_t launch_l0_bwd_rows(const L0BwdRowsArgs& a, cudaStream_t st);
+
+// Level-0 backward: T_c = patch_c^T (p_c * G) without dV in memory (comb.cu, l0_tgrad_kernel)
+struct L0TgradArgs {
+  const __nv_bfloat16* patches;  // [B][cnt][S][PP] bf16 (unfold_patches layout)
+  int cnt, c0;                   // slab channels in `patches`, first channel of the node
+  int g, R, S, D, H, NH, PP;
+  const __nv_bfloat16* p;        // node block of the normalised K_p0 output [H/NH][g][R][NH]
+  const float* mix;              // linear nodes: mix[g] (then p is unused)
+  const __nv_bfloat16* G;        // [R][D] bf16
+  float* T;                      // [g][PP][D] fp32
+};
+cudaError_t launch_l0_tgrad(const L0TgradArgs& a, cudaStream_t st);
 cudaError_t launch_vit_tokens(const void* agg, int f32, const float* mask,
                               const float* mask_token, const float* meta_tok, void* out, int B,
                               int S, int D, cudaStream_t st);

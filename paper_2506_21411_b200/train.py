@@ -25,6 +25,7 @@ dU -> (wk, q, wq) follows U[:, h] = wk[:, h-blk] (q wq)[h-blk] / sqrt(dh) (fold.
 from __future__ import annotations
 
 import math
+import os
 import weakref
 
 import torch
@@ -557,6 +558,9 @@ class DchagTrainer:
         posV_all = torch.bmm(pos_bf.unsqueeze(0).expand(n0, s, d), Wv_all,
                              out_dtype=torch.float32)                        # [n0, S, D]
         Gs_all = torch.empty(n0, s, d, device=img.device, dtype=torch.float32)
+        use_tg = (pp == 64 and d % 128 == 0 and s % 64 == 0 and d // h in (64, 128)
+                  and (not attn or pk.NH % 2 == 0)
+                  and os.environ.get("DCHAG_TRAIN_TG", "1") != "0")
         c0, p_at = 0, 0
         for gi, g in enumerate(levels[0]):
             node = f"{pre}.l0.g{gi}"
@@ -569,21 +573,30 @@ class DchagTrainer:
             else:
                 grads[f"{node}.b"] = g_y[gi].sum(0, dtype=torch.float32)
                 Gb = gyb
-            # d(Loss)/dV_c = p_c * G per head (bf16, the operand of T_c = patch_c^T dV_c); the
-            # same pass reduces the positional part of dp: Gpos[r, h] = G[r, h] . posV[s, h]
-            dV = torch.empty(g, R, d, device=img.device, dtype=torch.bfloat16)
+            # positional part of dp: Gpos[r, h] = G[r, h] . posV[s, h] (one pass over G), and
+            # T_c = patch_c^T dV_c with dV_c = p_c * G per head: straight from patches, p and
+            # G by K_tg (dV never stored) where its shape rules hold, else dV (bf16) + bmm
             Gpos = torch.empty(R, h, device=img.device, dtype=torch.float32)
             if attn:
                 pblk = pnorm[p_at:p_at + g * R * h]
                 p_at += g * R * h
-                _lib.call("dchag_l0_dv", g, R, d, h, pk.NH, _lib.ptr(pblk), 0, _lib.ptr(Gb),
-                          _lib.ptr(posV_all[gi]), s, _lib.ptr(Gpos), _lib.ptr(dV),
-                          _lib.stream_handle())
+                pptr, mptr, nh_ = _lib.ptr(pblk), 0, pk.NH
             else:
                 mixv = w[f"{node}.mix"].float().contiguous()
-                _lib.call("dchag_l0_dv", g, R, d, h, 1, 0, _lib.ptr(mixv), _lib.ptr(Gb),
+                pptr, mptr, nh_ = 0, _lib.ptr(mixv), 1
+            if use_tg:
+                _lib.call("dchag_l0_dv", g, R, d, h, nh_, pptr, mptr, _lib.ptr(Gb),
+                          _lib.ptr(posV_all[gi]), s, _lib.ptr(Gpos), 0, _lib.stream_handle())
+                T = torch.empty(g, pp, d, device=img.device, dtype=torch.float32)
+                _lib.call("dchag_l0_tgrad", _lib.ptr(patches), cnt, c0, g, R, s, d, h, nh_, pp,
+                          pptr, mptr, _lib.ptr(Gb), _lib.ptr(T), _lib.stream_handle())
+            else:
+                dV = torch.empty(g, R, d, device=img.device, dtype=torch.bfloat16)
+                _lib.call("dchag_l0_dv", g, R, d, h, nh_, pptr, mptr, _lib.ptr(Gb),
                           _lib.ptr(posV_all[gi]), s, _lib.ptr(Gpos), _lib.ptr(dV),
                           _lib.stream_handle())
+                pt_ = patches[:, c0:c0 + g].permute(1, 3, 0, 2).reshape(g, pp, R)
+                T = torch.bmm(pt_, dV, out_dtype=torch.float32)         # [g, PP, D]
             # dp_c[r, h] = G[r, h-cols] . V_c[r, h-cols] with V_c = patch_c Mt_c + Cb_c + posV:
             # the K = P^2 tcgen05 GEMM reduces each 32-column group of V_c against G in its
             # epilogue (V_c never reaches memory)
@@ -605,7 +618,6 @@ class DchagTrainer:
                 grads[f"{node}.mix"] = dp.sum((1, 2))
                 dl = None
             pt = patches[:, c0:c0 + g].permute(1, 3, 0, 2).reshape(g, pp, R)   # patch_c^T
-            T = torch.bmm(pt, dV, out_dtype=torch.float32)              # [g, PP, D]
             if attn:  # colsum_r dV_j = sum_r p_jrh G_r (per head): a small GEMM, not a dV pass
                 colV = torch.bmm(pj.permute(1, 0, 2), Gb.view(R, h, dh).permute(1, 0, 2),
                                  out_dtype=torch.float32)

@@ -125,3 +125,34 @@ def test_train_step_cuda_graph_replay(lk):
     assert torch.equal(out_g, out_e)
     for k, v in grads_e.items():
         assert rel_err(grads[k].double().cpu().numpy(), v.double().cpu().numpy()) < 1e-5, k
+
+
+@pytest.mark.parametrize("D,H,g", [(256, 4, 5), (512, 4, 3), (2048, 32, 16)])
+def test_l0_tgrad_matches_torch(D, H, g):
+    """dchag_l0_tgrad: T_c = patch_c^T (p_c * G per head) for a node's channels, against
+    the materialised dV and a float64 contraction (both p layouts: K_p0 blocks and mix)."""
+    from paper_2506_21411_b200 import _lib
+    from paper_2506_21411_b200.fold import unit_heads
+    torch.manual_seed(0)
+    B, S, PP, cnt, c0 = 2, 128, 64, g + 2, 1
+    R = B * S
+    NH = unit_heads(D, H)
+    patches = torch.randn(B, cnt, S, PP, device="cuda").to(torch.bfloat16)
+    G = torch.randn(R, D, device="cuda").to(torch.bfloat16)
+    p = torch.rand(H // NH, g, R, NH, device="cuda").to(torch.bfloat16)
+    mix = torch.rand(g, device="cuda")
+    pc = p.permute(1, 2, 0, 3).reshape(g, R, H).double()          # [g, R, H]
+    pat = patches[:, c0:c0 + g].permute(1, 0, 2, 3).reshape(g, R, PP).double()
+    Gd = G.double().view(R, H, D // H)
+    for mode in ("p", "mix"):
+        T = torch.empty(g, PP, D, device="cuda")
+        _lib.call("dchag_l0_tgrad", _lib.ptr(patches), cnt, c0, g, R, S, D, H,
+                  NH if mode == "p" else 1, PP, _lib.ptr(p) if mode == "p" else 0,
+                  _lib.ptr(mix) if mode == "mix" else 0, _lib.ptr(G), _lib.ptr(T),
+                  _lib.stream_handle())
+        w = pc if mode == "p" else mix.double().view(g, 1, 1).expand(g, R, H)
+        dV = (w.unsqueeze(-1) * Gd.unsqueeze(0)).reshape(g, R, D)
+        want = torch.einsum("grk,grd->gkd", pat, dV)
+        torch.cuda.synchronize()
+        err = ((T.double() - want).norm() / want.norm()).item()
+        assert err < 1e-2, (mode, err)
