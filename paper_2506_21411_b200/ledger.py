@@ -15,7 +15,8 @@ from dataclasses import dataclass
 DCHAG_BOUNDARY_TAG = "dchag-boundary"     # strategies.py:41
 FINAL_OUT_TAG = "dchag-final-out"         # position-split final layer: output AllGather
 FINAL_ALLSUM_TAG = "agg-final"            # head-split final layer: TpHooks.allsum
-POS_GRAD_TAG = "special.pos"              # strategies.py:251-264 (phase "optimizer")
+POS_GRAD_TAG = "shared-grad.special.pos"  # strategies.py:251-264 (phase "optimizer")
+DP_GRAD_TAG = "dp-grad."                  # + parameter name (strategies.py:352-357)
 
 
 @dataclass(frozen=True)

@@ -133,10 +133,13 @@ def _u_backward(w, prefix, dU, heads):
 class DchagTrainer:
     """Forward + backward of one rank's front end (tp ranks share the final layer)."""
 
-    def __init__(self, fe: DchagFrontEnd):
+    def __init__(self, fe: DchagFrontEnd, dp_group=None):
+        """dp_group: the data-parallel group of this rank (grid.make_groups); backward()
+        then averages every gradient over it (strategies.py:352-357)."""
         if fe.model.agg_variant != "single_query":
             raise ConfigError("training path implements agg_variant='single_query'")
         self.fe = fe
+        self.dp_group = dp_group
         self._ints = {}
 
     def _dev_ints(self, vals, dtype, dev):
@@ -353,12 +356,38 @@ class DchagTrainer:
         _BF_WEIGHTS.update(id(v) for v in self.fe.weights.values())
         grads, g_y = self.backward_final(saved, g_out)
         grads.update(self.backward_local(saved, g_y))
+        if self.dp_group is not None:
+            self._dp_average(grads)
         if self.fe.tp > 1:
             import torch.distributed as dist
             dist.all_reduce(grads["special.pos"], group=self.fe.process_group)
-            self.fe._log("AllReduce", "optimizer", "special.pos",
+            self.fe._log("AllReduce", "optimizer", "shared-grad.special.pos",
                          (grads["special.pos"].numel(), grads["special.pos"].element_size()))
         return grads
+
+    def _dp_average(self, grads):
+        """Data-parallel gradient averaging (strategies.py:352-357: every gradient
+        all-reduced over dp, x 1/dp), as ONE bucketed NCCL all-reduce of all gradients in
+        name order instead of one call per tensor; the ledger records the reference's
+        per-parameter events. special.pos is averaged here and summed over tp after."""
+        import torch.distributed as dist
+        ndp = dist.get_world_size(self.dp_group)
+        if ndp == 1:
+            return
+        names = sorted(grads)
+        flat = torch.cat([grads[k].reshape(-1).float() for k in names])
+        dist.all_reduce(flat, group=self.dp_group)
+        flat.mul_(1.0 / ndp)
+        off = 0
+        led = self.fe.ledger
+        from . import ledger as LG
+        for k in names:
+            n = grads[k].numel()
+            grads[k] = flat[off:off + n].view(grads[k].shape)
+            off += n
+            if led is not None:
+                led.record(self.fe.rank, "AllReduce", "dp", "backward",
+                           LG.allreduce_payload(n, 4, ndp), LG.DP_GRAD_TAG + k)
 
     def _own_heads(self):
         fe = self.fe

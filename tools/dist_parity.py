@@ -133,6 +133,39 @@ def main():
         print(f"rank {rank}/{tp} train step{' (head-split final)' if split else ''}: "
               f"{len(errs)} grads, worst rel_err={terr:.3e} ({max(errs, key=errs.get)})",
               flush=True)
+    # data parallel over the whole world (tp = 1, dp = N): every rank trains on
+    # its own batch, gradients averaged by one bucketed all-reduce; check against the
+    # average of the per-batch gradients computed locally without the dp group
+    from paper_2506_21411_b200.grid import make_groups
+    from paper_2506_21411_b200.ledger import CommLedger
+    _, dp_group, _, dp_i = make_groups(1, tp)
+    specs = O.frontend_param_specs(13, 64, 128, 8, 256, 1, 4)
+    w = O.random_params(specs, seed=4, std=0.05, bias_std=0.02)
+    w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
+    fe = DchagFrontEnd(13, 64, 128, 8, 256, 4, max_group=4, out_dtype=torch.float32)
+    fe.load_weights(w)
+    fe.ledger = CommLedger()
+    imgs = [torch.from_numpy(np.random.default_rng(20 + i).standard_normal((2, 13, 64, 128))
+                             .astype(np.float32)).to(torch.bfloat16).cuda() for i in range(tp)]
+    probes = [torch.from_numpy(np.random.default_rng(40 + i).standard_normal((2, 1, 128, 256))
+                               .astype(np.float32)).cuda() for i in range(tp)]
+    trd = DchagTrainer(fe, dp_group=dp_group)
+    _, sv = trd.forward_train(imgs[dp_i])
+    g_dp = trd.backward(sv, probes[dp_i])
+    tr1 = DchagTrainer(fe)
+    acc = None
+    for i in range(tp):
+        _, sv = tr1.forward_train(imgs[i])
+        gi = {k: v.double() for k, v in tr1.backward(sv, probes[i]).items()}
+        acc = gi if acc is None else {k: acc[k] + gi[k] for k in acc}
+    derr = max(O.rel_err(g_dp[k].double().cpu().numpy(), (acc[k] / tp).cpu().numpy())
+               for k in acc)
+    _, nev = fe.ledger.query(axis="dp", op="AllReduce")
+    if nev != len(acc):
+        derr = 1.0
+    worst = max(worst, derr)
+    print(f"rank {rank}/{tp} data-parallel (dp={tp}) averaged grads: worst rel_err={derr:.3e}, "
+          f"{nev} dp ledger events", flush=True)
     t = torch.tensor([worst], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
