@@ -40,6 +40,22 @@ __global__ void __launch_bounds__(256, CH >= 8 ? 1 : (CH >= 4 ? 2 : 4)) combine_
   const int rb = r / a.rows_inner, rs = r - rb * a.rows_inner;
   float* p = sp[warp];
   const long long ldv = a.ldv ? a.ldv : a.D;
+  const __nv_bfloat16* vbase =
+      a.V + (long long)first * a.sVj + (long long)rb * a.sVb + (long long)rs * ldv + col0;
+  const int nchunk = dseg / 8;  // chunks of this segment; lanes past it idle (D < 256)
+  const bool act = lane < nchunk;  // D >= 256 is a multiple of 256: all lanes active
+  // the first two children's value rows are requested before the softmax phase, so their
+  // HBM latency overlaps the logit loads
+  uint4 v0[CH], v1[CH];
+  {
+    const uint4* r0 = reinterpret_cast<const uint4*>(vbase);
+    const uint4* r1 = reinterpret_cast<const uint4*>(vbase + (g > 1 ? a.sVj : 0));
+#pragma unroll
+    for (int q = 0; q < CH; ++q) v0[q] = act ? __ldg(r0 + lane + 32 * q) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int q = 0; q < CH; ++q)
+      v1[q] = act && g > 1 ? __ldg(r1 + lane + 32 * q) : make_uint4(0, 0, 0, 0);
+  }
   if (a.W) {  // explicit per-(child, head) weights (full_cross)
     const float* wr = a.W + ((long long)n * a.R + r) * a.max_g * H;
     for (int i = lane; i < g * H; i += 32) p[i] = __ldg(wr + i);
@@ -65,13 +81,9 @@ __global__ void __launch_bounds__(256, CH >= 8 ? 1 : (CH >= 4 ? 2 : 4)) combine_
   for (int q = 0; q < CH; ++q)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[q][e] = 0.f;
-  const __nv_bfloat16* vbase =
-      a.V + (long long)first * a.sVj + (long long)rb * a.sVb + (long long)rs * ldv + col0;
-  const int nchunk = dseg / 8;  // chunks of this segment; lanes past it idle (D < 256)
   int hq[CH];  // head of each of this lane's chunks
 #pragma unroll
   for (int q = 0; q < CH; ++q) hq[q] = (col0 + (lane + 32 * q) * 8) / dh;
-  const bool act = lane < nchunk;  // D >= 256 is a multiple of 256: all lanes active
   auto accumulate = [&](const uint4 (&v)[CH], int j) {
 #pragma unroll
     for (int q = 0; q < CH; ++q) {
@@ -84,11 +96,12 @@ __global__ void __launch_bounds__(256, CH >= 8 ? 1 : (CH >= 4 ? 2 : 4)) combine_
       }
     }
   };
-  int j = 0;
+  accumulate(v0, 0);
+  if (g > 1) accumulate(v1, 1);
+  int j = 2;
   for (; j + 2 <= g; j += 2) {
     const uint4* r0 = reinterpret_cast<const uint4*>(vbase + (long long)j * a.sVj);
     const uint4* r1 = reinterpret_cast<const uint4*>(vbase + (long long)(j + 1) * a.sVj);
-    uint4 v0[CH], v1[CH];
 #pragma unroll
     for (int q = 0; q < CH; ++q) v0[q] = act ? __ldg(r0 + lane + 32 * q) : make_uint4(0, 0, 0, 0);
 #pragma unroll
@@ -98,7 +111,6 @@ __global__ void __launch_bounds__(256, CH >= 8 ? 1 : (CH >= 4 ? 2 : 4)) combine_
   }
   if (j < g) {
     const uint4* r0 = reinterpret_cast<const uint4*>(vbase + (long long)j * a.sVj);
-    uint4 v0[CH];
 #pragma unroll
     for (int q = 0; q < CH; ++q) v0[q] = act ? __ldg(r0 + lane + 32 * q) : make_uint4(0, 0, 0, 0);
     accumulate(v0, j);
