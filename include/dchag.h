@@ -89,16 +89,6 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
                   const void* Mt, int C_pad, const void* Et, int KE, const void* posV, void* ctx,
                   void* stream);
 
-/* Level-0 node backward, row stage (training; backward of layers.py:103-123 / :141-146 at
- * tree level 0 with the tokenizer folded): V [g][R][D] bf16 = x_c wv, G [R][D] fp32 =
- * dLoss/dctx, ctx [R][D] bf16, p = the node's block of the normalised dchag_l0_logits
- * output ([H/nh][g][R][nh]).  Attention: dl[j][r][h] = p (G_h . V_j,h - G_h . ctx_h),
- * dV[j][r] = p_jh G_h.  Linear (mix != NULL): dV[j][r] = mix_j G, dm[j][r] = G . V_j[r].
- * D: a multiple of 256 above 256 (of 1024 above 1024). */
-int dchag_l0_bwd_rows(int g, int R, int D, int H, int nh, const void* V, const float* G,
-                      const void* ctx, const void* p, const float* mix, float* dl, void* dV,
-                      float* dm, void* stream);
-
 /* Level-0 node backward, value gradient (training): dV[c][r][d] = p_c[r][h] * G[r][d]
  * for the node's g channels, p = the node's block of the normalised dchag_l0_logits output
  * ([H/nh][g][R][nh] bf16), or dV[c] = mix[c] * G for linear nodes (mix != NULL). With posV

@@ -30,8 +30,6 @@ SIGNATURES = {
                       c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp],
     "dchag_combine": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_vp, c_ll,
                       c_vp, c_vp, c_vp],
-    "dchag_l0_bwd_rows": [c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                          c_vp, c_vp, c_vp],
     "dchag_l0_dv": [c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp,
                     c_vp, c_vp],
     "dchag_vit_tokens": [c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp],

@@ -297,20 +297,6 @@ int dchag_combine_strided(int n_nodes, int R, int D, int H, const int* node_firs
   return cuda_status(launch_combine(a, S(stream)), "combine");
 }
 
-int dchag_l0_bwd_rows(int g, int R, int D, int H, int nh, const void* V, const float* G,
-                      const void* ctx, const void* p, const float* mix, float* dl, void* dV,
-                      float* dm, void* stream) {
-  if (!mix && (!ctx || !p || !dl)) return fail(DCHAG_ERR_SHAPE, "l0_bwd_rows: attention needs ctx, p, dl");
-  if (mix && !dm) return fail(DCHAG_ERR_SHAPE, "l0_bwd_rows: linear needs dm");
-  L0BwdRowsArgs a;
-  a.g = g; a.R = R; a.D = D; a.H = H; a.NH = nh;
-  a.V = reinterpret_cast<const __nv_bfloat16*>(V); a.G = G;
-  a.ctx = reinterpret_cast<const __nv_bfloat16*>(ctx);
-  a.p = reinterpret_cast<const __nv_bfloat16*>(p); a.mix = mix;
-  a.dl = dl; a.dV = reinterpret_cast<__nv_bfloat16*>(dV); a.dm = dm;
-  return cuda_status(launch_l0_bwd_rows(a, S(stream)), "l0_bwd_rows");
-}
-
 int dchag_l0_dv(int g, int R, int D, int H, int nh, const void* p, const float* mix,
                 const void* G, const float* posV, int period, float* Gpos, void* dV, void* stream) {
   if (!mix && !p && dV) return fail(DCHAG_ERR_SHAPE, "l0_dv: need p or mix");

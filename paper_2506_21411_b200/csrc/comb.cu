@@ -190,126 +190,6 @@ cudaError_t launch_combine_f32(const CombineF32Args& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// Level-0 node backward, row stage (training; the folded level-0 backward in train.py).
-// One warp per (row r, 1024-column segment) of the node: with G = dLoss/dctx[r] and ctx[r]
-// kept in registers, for each channel j of the node:
-//   dp_jh = G_h . V_j,h   (V_j = x_j wv, recomputed by a K = P^2 GEMM)
-//   attention: dl_jh = p_jh (dp_jh - G_h . ctx_h),  dV_j = p_jh G_h   (layers.py:103-123 bwd)
-//   linear:    dV_j = mix_j G,  dm_j[r] = G . V_j                      (layers.py:141-146 bwd)
-// Lanes own 8-column chunks (chunk c = lane + 32 i); a head's chunks are dh/8 adjacent lanes.
-// The segment's p_jh (g x heads) are gathered into shared memory up front, so the channel
-// loop carries no dependent global loads.
-template <int CPL>  // chunks per lane = ceil(segment / 256); lanes past the segment idle
-__global__ void __launch_bounds__(256) l0_bwd_rows_kernel(L0BwdRowsArgs a) {
-  __shared__ float sp[8][1024];  // per warp: p[j][head of segment], g * heads <= 1024
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nseg = (a.D + 1023) / 1024;
-  const long long item = (long long)blockIdx.x * 8 + warp;
-  const long long r = item / nseg;
-  const int seg = (int)(item - r * nseg);
-  if (r >= a.R) return;
-  const int D = a.D, H = a.H, dh = D / H, lpg = dh / 8;  // lanes per head group
-  const int col0 = seg * 1024, dseg = min(1024, D - col0);
-  const int h0 = col0 / dh, hseg = dseg / dh;
-  const bool act = lane < dseg / 8;
-  float* ps = sp[warp];
-  if (!a.mix) {
-    for (int i = lane; i < a.g * hseg; i += 32) {
-      const int j = i / hseg, h = h0 + (i - j * hseg);
-      ps[i] = __bfloat162float(a.p[(((long long)(h / a.NH) * a.g + j) * a.R + r) * a.NH + h % a.NH]);
-    }
-  }
-  float gv[CPL][8];
-  float gc[CPL];  // sum_j p_jh dp_jh of this lane's head per chunk
-#pragma unroll
-  for (int i = 0; i < CPL; ++i) {
-    const int c = act ? lane + 32 * i : 0;
-    const long long off = r * D + col0 + c * 8;
-    const float4 g0 = *reinterpret_cast<const float4*>(a.G + off);
-    const float4 g1 = *reinterpret_cast<const float4*>(a.G + off + 4);
-    gv[i][0] = g0.x; gv[i][1] = g0.y; gv[i][2] = g0.z; gv[i][3] = g0.w;
-    gv[i][4] = g1.x; gv[i][5] = g1.y; gv[i][6] = g1.z; gv[i][7] = g1.w;
-    gc[i] = 0.f;
-  }
-  __syncwarp();
-  for (int j = 0; j < a.g; ++j) {
-    const __nv_bfloat16* vr = a.V + ((long long)j * a.R + r) * D + col0;
-    __nv_bfloat16* dvr = a.dV + ((long long)j * a.R + r) * D + col0;
-    uint4 vx[CPL];
-#pragma unroll
-    for (int i = 0; i < CPL; ++i)
-      vx[i] = *reinterpret_cast<const uint4*>(vr + (act ? lane + 32 * i : 0) * 8);
-    float dmr = 0.f;
-#pragma unroll
-    for (int i = 0; i < CPL; ++i) {
-      const int c = act ? lane + 32 * i : 0;
-      const int hl = (c * 8) / dh;  // head within the segment
-      const uint32_t vw[4] = {vx[i].x, vx[i].y, vx[i].z, vx[i].w};
-      float dp = 0.f;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) dp += gv[i][2 * e] * bf16lo(vw[e]) + gv[i][2 * e + 1] * bf16hi(vw[e]);
-      if (!act) dp = 0.f;
-      float pj;
-      if (a.mix) {
-        dmr += dp;
-        pj = a.mix[j];
-      } else {
-        for (int o = 1; o < lpg; o <<= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
-        pj = ps[j * hseg + hl];
-        gc[i] += pj * dp;  // sum_j p_jh dp_jh (== G_h . ctx_h in exact arithmetic)
-        if (act && (lane % lpg) == 0) a.dl[((long long)j * a.R + r) * H + h0 + hl] = dp;
-      }
-      uint4 o;
-      o.x = pack_bf16(pj * gv[i][0], pj * gv[i][1]);
-      o.y = pack_bf16(pj * gv[i][2], pj * gv[i][3]);
-      o.z = pack_bf16(pj * gv[i][4], pj * gv[i][5]);
-      o.w = pack_bf16(pj * gv[i][6], pj * gv[i][7]);
-      if (act) *reinterpret_cast<uint4*>(dvr + c * 8) = o;
-    }
-    if (a.mix) {
-#pragma unroll
-      for (int o = 16; o; o >>= 1) dmr += __shfl_xor_sync(0xffffffffu, dmr, o);
-      if (lane == 0) atomicAdd(a.dm + (long long)j * a.R + r, dmr);  // segments of the row
-    }
-  }
-  if (a.mix) return;
-  // softmax backward with the same dp values: dl_jh = p_jh (dp_jh - sum_j' p_j'h dp_j'h), so
-  // sum_j dl_jh = 0 exactly (a one-channel node gets exactly zero logit gradient)
-  __syncwarp();
-  for (int j = 0; j < a.g; ++j) {
-#pragma unroll
-    for (int i = 0; i < CPL; ++i) {
-      const int c = act ? lane + 32 * i : 0;
-      const int hl = (c * 8) / dh;
-      if (act && (lane % lpg) == 0) {
-        float* dst = a.dl + ((long long)j * a.R + r) * H + h0 + hl;
-        *dst = ps[j * hseg + hl] * (*dst - gc[i]);
-      }
-    }
-  }
-}
-
-cudaError_t launch_l0_bwd_rows(const L0BwdRowsArgs& a, cudaStream_t st) {
-  const int dh = a.D / a.H;
-  const int segw = a.D < 1024 ? a.D : 1024;
-  if ((a.D > 256 ? a.D % 256 : a.D % 8) || (a.D > 1024 && a.D % 1024) || dh % 8 ||
-      dh / 8 > 32 || 32 % (dh / 8) || segw % dh || a.g * (segw / dh) > 1024)
-    return cudaErrorInvalidValue;
-  const long long items = (long long)a.R * ((a.D + 1023) / 1024);
-  const int grid = (int)((items + 7) / 8);
-  if (a.mix) {
-    cudaError_t e = cudaMemsetAsync(a.dm, 0, sizeof(float) * (size_t)a.g * a.R, st);
-    if (e != cudaSuccess) return e;
-  }
-  switch ((segw + 255) / 256) {
-    case 1: l0_bwd_rows_kernel<1><<<grid, 256, 0, st>>>(a); break;
-    case 2: l0_bwd_rows_kernel<2><<<grid, 256, 0, st>>>(a); break;
-    case 4: l0_bwd_rows_kernel<4><<<grid, 256, 0, st>>>(a); break;
-    default: return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
-}
-
 // Level-0 backward value gradient: dV[c][r][d] = p_c[r][h(d)] * G[r][d] (or mix[c] * G), and
 // (posV != null) the positional part of dp, Gpos[r][h] = sum_{d in h} G[r][d] posV[r % S][d].
 // One thread per (row, 8 columns): G is read once (16 B) and the node's g outputs are

@@ -115,20 +115,6 @@ struct CombineF32Args {
 };
 cudaError_t launch_combine_f32(const CombineF32Args& a, cudaStream_t st);
 
-// Level-0 node backward, row stage (see comb.cu)
-struct L0BwdRowsArgs {
-  int g, R, D, H, NH;
-  const __nv_bfloat16* V;      // [g][R][D] child values x_c wv
-  const float* G;              // [R][D] dLoss/dctx
-  const __nv_bfloat16* ctx;    // [R][D] the node's context (attention)
-  const __nv_bfloat16* p;      // node block of the K_p0 layout [H/NH][g][R][NH] (attention)
-  const float* mix;            // [g] (linear) or null
-  float* dl;                   // [g][R][H] (attention)
-  __nv_bfloat16* dV;           // [g][R][D]
-  float* dm;                   // [g][R] (linear)
-};
-cudaError_t launch_l0_bwd_rows(const L0BwdRowsArgs& a, cudaStream_t st);
-
 // Level-0 backward: T_c = patch_c^T (p_c * G) without dV in memory (comb.cu, l0_tgrad_kernel)
 struct L0TgradArgs {
   const __nv_bfloat16* patches;  // [B][cnt][S][PP] bf16 (unfold_patches layout)
