@@ -277,18 +277,20 @@ class DchagTrainer:
         return out.view(B, 1, s, d)
 
     def _level0_posV(self):
+        """pos @ Wv_n for every level-0 node (x sum(mix) for linear nodes): one batched
+        bf16 tensor-core GEMM with fp32 output (K_l0 adds it in bf16)."""
         fe = self.fe
         w = fe.weights
         pre = f"agg.slab{fe.rank}"
-        pos = w["special.pos"]
-        out = []
-        for gi in range(len(fe.tree.levels[0])):
-            node = f"{pre}.l0.g{gi}"
-            if fe.strategy.agg_layer_kind == "linear":
-                out.append(w[f"{node}.mix"].sum() * (pos @ w[f"{node}.w"]))
-            else:
-                out.append(pos @ w[f"{node}.wv"])
-        return torch.stack(out)                                          # [n0, S, D]
+        pos = _bfc(w["special.pos"])
+        n0 = len(fe.tree.levels[0])
+        lin = fe.strategy.agg_layer_kind == "linear"
+        Wv = torch.stack([_bfc(w[f"{pre}.l0.g{gi}.{'w' if lin else 'wv'}"]) for gi in range(n0)])
+        out = torch.bmm(pos.unsqueeze(0).expand(n0, -1, -1), Wv, out_dtype=torch.float32)
+        if lin:
+            mixsum = torch.stack([w[f"{pre}.l0.g{gi}.mix"].float().sum() for gi in range(n0)])
+            out.mul_(mixsum.view(n0, 1, 1))
+        return out                                                       # [n0, S, D]
 
     def _combine(self, V, L, mix, firsts, gs, R, heads=None):
         n = len(firsts)
