@@ -306,7 +306,7 @@ cudaError_t launch_vit_tokens(const void* agg, int f32, const float* mask,
 
 // Level-0 backward token-weight gradient without dV in memory (training):
 //   T_c[k][d] = sum_r patch_c[r][k] * p_c[r][h(d)] * G[r][d]      (= patch_c^T dV_c)
-// One CTA per (channel c, 128 columns of d); 8 warps, warp = 32 k x 32 d (one head);
+// One CTA per (channel c, 128 columns of d); 4 warps, warp = 32 k x 64 d (one head);
 // the reduction over all R rows runs through 64-row chunks staged by cp.async (double
 // buffered, 16-byte XOR swizzle for conflict-free ldmatrix). The A operand patch^T comes
 // from ldmatrix.trans and is scaled by p of the warp's head in registers; B = G by
@@ -338,8 +338,10 @@ constexpr int TG_G_BYTES = TG_ROWS * 128 * 2;             // G tile: 64 rows x 1
 constexpr int TG_P_BYTES = TG_ROWS * 64 * 2;              // patch tile: 64 rows x 64 k
 constexpr int TG_S_BYTES = TG_ROWS * 4;                   // p word (2 heads, bf16) per row
 constexpr int TG_BUF = TG_G_BYTES + TG_P_BYTES + TG_S_BYTES;
+constexpr int TG_THREADS = 128;                           // 4 warps: 2 k halves x 2 heads
+constexpr int TG_NW = 64;                                 // d columns per warp (one head)
 
-__global__ void __launch_bounds__(256, 3) l0_tgrad_kernel(L0TgradArgs a) {
+__global__ void __launch_bounds__(TG_THREADS, 4) l0_tgrad_kernel(L0TgradArgs a) {
   extern __shared__ __align__(128) uint8_t tg_smem[];
   const int c = blockIdx.y;
   const int d0 = blockIdx.x * 128;
@@ -357,16 +359,16 @@ __global__ void __launch_bounds__(256, 3) l0_tgrad_kernel(L0TgradArgs a) {
     uint8_t* ss = tg_smem + buf * TG_BUF;
     const int r0 = (cbeg + i) * TG_ROWS;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {  // G: 64 rows x 16 chunks
-      const int q = threadIdx.x + t * 256, row = q >> 4, ch = q & 15;
+    for (int t = 0; t < 1024 / TG_THREADS; ++t) {  // G: 64 rows x 16 chunks
+      const int q = threadIdx.x + t * TG_THREADS, row = q >> 4, ch = q & 15;
       cp_async16(sg + row * 256 + ((ch ^ (row & 7)) << 4),
                  a.G + (size_t)(r0 + row) * a.D + d0 + ch * 8);
     }
     const int b = r0 / a.S, s0 = r0 - b * a.S;
     const __nv_bfloat16* pbase = a.patches + (((size_t)b * a.cnt + a.c0 + c) * a.S + s0) * 64;
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {  // patch: 64 rows x 8 chunks
-      const int q = threadIdx.x + t * 256, row = q >> 3, ch = q & 7;
+    for (int t = 0; t < 512 / TG_THREADS; ++t) {  // patch: 64 rows x 8 chunks
+      const int q = threadIdx.x + t * TG_THREADS, row = q >> 3, ch = q & 7;
       cp_async16(sp + row * 128 + ((ch ^ (row & 7)) << 4), pbase + (size_t)row * 64 + ch * 8);
     }
     if (!a.mix && threadIdx.x < TG_ROWS) {
@@ -379,16 +381,16 @@ __global__ void __launch_bounds__(256, 3) l0_tgrad_kernel(L0TgradArgs a) {
     (void)ss;
   };
   const int mbase = 32 * (warp & 1);   // k rows of this warp
-  const int nbase = 32 * (warp >> 1);  // d columns (within the CTA's 128)
+  const int nbase = TG_NW * (warp >> 1);  // d columns (within the CTA's 128)
   // half of the row's p word this warp uses: its head's parity (the word holds hA & ~1, +1)
   const int hw = (d0 + nbase) / dh;
   const int sel = hw & 1;
   const float mixc = a.mix ? __ldg(a.mix + c) : 0.f;
-  float acc[2][4][4];
+  float acc[2][TG_NW / 8][4];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < TG_NW / 8; ++j)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.f;
   load(0, 0);
@@ -427,7 +429,7 @@ __global__ void __launch_bounds__(256, 3) l0_tgrad_kernel(L0TgradArgs a) {
         af[mt][3] = scale_bf16x2(af[mt][3], p8, p9);
       }
 #pragma unroll
-      for (int np = 0; np < 2; ++np) {
+      for (int np = 0; np < TG_NW / 16; ++np) {
         uint32_t bf[4];
         const int r = kb + i8 + 8 * (j8 & 1);
         const int col = nbase + np * 16 + 8 * (j8 >> 1);
@@ -444,7 +446,7 @@ __global__ void __launch_bounds__(256, 3) l0_tgrad_kernel(L0TgradArgs a) {
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
+    for (int nt = 0; nt < TG_NW / 8; ++nt) {
       const int m = mbase + mt * 16 + gid;
       const int d = d0 + nbase + nt * 8 + 2 * tig;
       float* o = a.T + ((size_t)c * 64 + m) * a.D + d;
@@ -472,7 +474,8 @@ cudaError_t launch_l0_tgrad(const L0TgradArgs& a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   // enough CTAs for ~3 per SM: split the row reduction (partials added atomically)
   const int base = (a.D / 128) * a.g;
-  // measured (TR node, one B200): rs 1/2 0.225 ms, rs 4 0.194, rs 8 0.196
+  // measured (TR node, one B200, 4 warps x 32 k x 64 d): rs 2 0.168 ms, rs 4 0.151, rs 8 0.157
+  // (8 warps x 32 x 32: rs 4 0.194)
   int rs = 1;
   while (rs < 4 && base * rs < 6 * 148 && (a.R / TG_ROWS) / (rs * 2) >= 8) rs *= 2;
   if (const char* f = getenv("DCHAG_TG_RS")) rs = atoi(f) > 0 ? atoi(f) : rs;
@@ -480,7 +483,7 @@ cudaError_t launch_l0_tgrad(const L0TgradArgs& a, cudaStream_t st) {
     e = cudaMemsetAsync(a.T, 0, sizeof(float) * (size_t)a.g * a.PP * a.D, st);
     if (e != cudaSuccess) return e;
   }
-  l0_tgrad_kernel<<<dim3(a.D / 128, a.g, rs), 256, smem, st>>>(a);
+  l0_tgrad_kernel<<<dim3(a.D / 128, a.g, rs), TG_THREADS, smem, st>>>(a);
   return cudaGetLastError();
 }
 
