@@ -34,6 +34,14 @@ WORKLOADS = {
     # training step (fwd+bwd), SURVEY.md section 8(d) "TR": C500 D2048 H32 (dh 64), bf16
     "train": dict(channels=500, image_h=128, image_w=128, patch=8, embed=2048, heads=32,
                   depth=3, batch=32, train=True, final_split=True),
+    # the H1 config with the other node kinds: D-CHAG-L linear nodes (the
+    # paper's best configuration) and full_cross (ModelConfig's default variant, tokens
+    # materialised)
+    "hyperspectral_linear": dict(channels=500, image_h=128, image_w=128, patch=8, embed=1024,
+                                 heads=16, depth=3, batch=32, layer_kind="linear"),
+    "hyperspectral_fullcross": dict(channels=500, image_h=128, image_w=128, patch=8,
+                                    embed=1024, heads=16, depth=3, batch=32,
+                                    variant="full_cross"),
 }
 # scaling sweep: C 64..1024 x D 1024 (16 heads) / 4096 (32 heads,
 # dh = 128), 128x128 P8, B 32, max_group 16 with the depth derived per slab
@@ -88,13 +96,15 @@ def cpu_sample(wl, tp, max_group, tokens, seed=0):
     wp = wl["image_w"] // p
     rows = max(1, tokens // wp)
     tokens = rows * wp
+    lk, var = wl.get("layer_kind", "cross_attention"), wl.get("variant", "single_query")
     specs = O.frontend_param_specs(wl["channels"], rows * p, wl["image_w"], p, wl["embed"], tp,
-                                   max_group)
+                                   max_group, variant=var, layer_kind=lk)
     w = O.random_params(specs, seed=seed)
     img = np.random.default_rng(seed).standard_normal((1, wl["channels"], rows * p,
                                                          wl["image_w"]))
     t0 = time.perf_counter()
-    O.dchag_frontend(img, w, patch=p, heads=wl["heads"], tp=tp, max_group=max_group)
+    O.dchag_frontend(img, w, patch=p, heads=wl["heads"], tp=tp, max_group=max_group,
+                     variant=var, layer_kind=lk)
     dt = time.perf_counter() - t0
     S = (wl["image_h"] // p) * wp
     return tokens / S / dt, tokens, dt
@@ -154,6 +164,8 @@ def workload_config(args, wl, tp, max_group):
             "embed": wl["embed"], "heads": wl["heads"], "depth": wl["depth"],
             "max_group": max_group, "tp": tp, "global_batch": args.batch or wl["batch"],
             "final_layer": final_layer_mode(args, wl, tp),
+            **({"layer_kind": wl["layer_kind"]} if wl.get("layer_kind") else {}),
+            **({"agg_variant": wl["variant"]} if wl.get("variant") else {}),
             "parallelism": f"dchag-tp{tp}",
             **({"launch": "eager" if args.no_graph else "cuda graph (whole step)"}
                if wl.get("train") else {}),
@@ -252,7 +264,9 @@ def b200_arm(args, wl, tp, max_group):
     # boundary gradient in backward, BASELINE.json configs[3])
     fe = DchagFrontEnd(wl["channels"], wl["image_h"], wl["image_w"], wl["patch"], wl["embed"],
                        wl["heads"], max_group=max_group, tp=tp, rank=rank,
-                       final_layer_tp_split=bool(wl.get("final_split")) and tp > 1)
+                       final_layer_tp_split=bool(wl.get("final_split")) and tp > 1,
+                       agg_variant=wl.get("variant", "single_query"),
+                       agg_layer_kind=wl.get("layer_kind", "cross_attention"))
     fe.init_weights(seed=0, all_ranks=False)
     fe.prepare()
     off, cnt = fe.slab
@@ -326,7 +340,8 @@ def b200_arm(args, wl, tp, max_group):
         step_inf = lambda: fe(images)  # noqa: E731
     else:
         step_inf = step
-    plan = fe.launch_plan(B)
+    unfolded = fe._unfolded()  # full_cross / fp32: the unfolded ops path has no launch plan
+    plan = [] if unfolded else fe.launch_plan(B)
     site_ms = {s: 0.0 for _, s, _, _ in plan}
     events = []
     idx = {"i": 0}
@@ -347,12 +362,13 @@ def b200_arm(args, wl, tp, max_group):
 
     # per-kernel events follow the launch plan of one unchunked forward
     chunks, fe.comm_chunks = fe.comm_chunks, 1
-    _lib.set_launch_hook(hook)
-    try:
-        timed(step_inf, args.steps, per_step_hook=reset)
-    finally:
-        _lib.set_launch_hook(None)
-        fe.comm_chunks = chunks
+    if plan:
+        _lib.set_launch_hook(hook)
+        try:
+            timed(step_inf, args.steps, per_step_hook=reset)
+        finally:
+            _lib.set_launch_hook(None)
+            fe.comm_chunks = chunks
     for site, a, b in events:
         site_ms[site] += a.elapsed_time(b) / args.steps
     kernels = []
@@ -362,8 +378,11 @@ def b200_arm(args, wl, tp, max_group):
         kernels.append({"site": site, "kernel": name, "ms": site_ms[site],
                         "tflops": flops / t / 1e12 if t else None,
                         "gbs": nbytes / t / 1e9 if t else None})
-    dom = max(kernels, key=lambda k: k["ms"])
-    dom_plan = next(p for p in plan if p[1] == dom["site"])
+    if not plan:
+        kernels = [{"kernel": "unfolded ops path (per-node K_gemm / K_comb / K_fc launches)",
+                    "ms": None}]
+    dom = max(kernels, key=lambda k: k["ms"] or 0)
+    dom_plan = next((p for p in plan if p[1] == dom.get("site")), None)
     tensor_bound = dom["kernel"] in ("dchag_l0_node", "dchag_gemm_bf16", "dchag_l0_logits")
     traffic = None
     try:
@@ -371,7 +390,9 @@ def b200_arm(args, wl, tp, max_group):
             traffic = json.load(f).get(f"{args.workload}:tp{tp}:{dom['site']}")
     except Exception:
         pass
-    if tensor_bound:
+    if dom_plan is None:
+        roof = None
+    elif tensor_bound:
         # the sustained figure is cuBLAS back to back under the power cap; a kernel that
         # beats it in this run is measured against the burst figure instead (never frac > 1)
         use_burst = dom["tflops"] > peak_sus
@@ -408,6 +429,11 @@ def b200_arm(args, wl, tp, max_group):
                 out = gstep.out
             if rank == 0:
                 out_host.copy_(out, non_blocking=True)
+        elif unfolded:  # device images only on the unfolded path: copy in, run, copy out
+            dev_img.copy_(host_img, non_blocking=True)
+            out = fe(dev_img)
+            if rank == 0:
+                out_host.copy_(out, non_blocking=True)
         else:
             # public API with host buffers: chunked H2D overlapped with the kernels, the
             # result rows streamed back into the pinned host tensor
@@ -421,7 +447,9 @@ def b200_arm(args, wl, tp, max_group):
 
     # ---- whole-job algorithmic work
     exec_flops = sum(p[2] for p in plan)  # this rank's folded-plan flops per step
-    if world > 1:
+    if not plan:
+        tot_exec = None
+    elif world > 1:
         t = torch.tensor([float(exec_flops - [p for p in plan if p[1] == "gemm_final"][0][2])],
                          device="cuda", dtype=torch.float64)
         dist.all_reduce(t)
@@ -458,8 +486,9 @@ def b200_arm(args, wl, tp, max_group):
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": clocks,
-            "work": {"folded_plan_tflop_per_step": tot_exec / 1e12,
-                     "folded_plan_tflops": tot_exec / (ms / args.steps / 1e3) / 1e12,
+            "work": {"folded_plan_tflop_per_step": tot_exec / 1e12 if plan else None,
+                     "folded_plan_tflops": (tot_exec / (ms / args.steps / 1e3) / 1e12
+                                            if plan else None),
                      "reference_graph_B_tflop_per_step": b_flops / 1e12,
                      "B_flops_effective_tflops": b_flops / (ms / args.steps / 1e3) / 1e12,
                      "B_flops_roofline_frac": b_flops / (ms / args.steps / 1e3) / 1e12
@@ -476,7 +505,8 @@ def b200_arm(args, wl, tp, max_group):
 
 
 def bflops_per_image(wl, slabs, max_group, train=False):
-    """SURVEY.md section 8(d) 'B' flops: collapsed single_query count, final layer once;
+    """SURVEY.md section 8(d) 'B' flops: collapsed single_query count (linear nodes
+    S (2 g D + 2 D^2); full_cross counted as single_query), final layer once;
     fwd+bwd = 3 x (nodes + final) + 2 x tokenizer."""
     from paper_2506_21411_b200.config import build_tree_spec
     S = (wl["image_h"] // wl["patch"]) * (wl["image_w"] // wl["patch"])
@@ -486,7 +516,8 @@ def bflops_per_image(wl, slabs, max_group, train=False):
         tok += 2 * c * S * pp * D
         for level in build_tree_spec(c, max_group).levels:
             for g in level:
-                nodes += S * (4 * g * D * H + 4 * D * D)
+                nodes += (S * (2 * g * D + 2 * D * D) if wl.get("layer_kind") == "linear"
+                          else S * (4 * g * D * H + 4 * D * D))
     nodes += S * (4 * len(slabs) * D * H + 4 * D * D)
     return 3 * nodes + 2 * tok if train else nodes + tok
 
