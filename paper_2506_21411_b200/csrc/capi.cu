@@ -337,6 +337,24 @@ int dchag_l0_tgrad(const void* patches, int cnt, int c0, int g, int R, int seq, 
   a.cnt = cnt; a.c0 = c0; a.g = g; a.R = R; a.S = seq; a.D = D; a.H = H; a.NH = nh; a.PP = PP;
   a.p = reinterpret_cast<const __nv_bfloat16*>(p); a.mix = mix;
   a.G = reinterpret_cast<const __nv_bfloat16*>(G); a.T = T;
+  // tcgen05 form (K_tgc: both operands MN-major straight from their global layouts) unless
+  // DCHAG_TG_TC=0 selects the mma.sync kernel
+  const char* tc = getenv("DCHAG_TG_TC");
+  if (!(tc && atoi(tc) == 0)) {
+    const int B = R / seq;
+    CUtensorMap tG, tP;
+    cuuint64_t gd[2] = {(cuuint64_t)D, (cuuint64_t)R};
+    cuuint64_t gs[1] = {(cuuint64_t)D * 2};
+    cuuint32_t gb[2] = {64u, 64u};
+    int rc = make_map(&tG, G, 2, gd, gs, gb, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    cuuint64_t pd[3] = {64u, (cuuint64_t)seq, (cuuint64_t)B * cnt};
+    cuuint64_t ps[2] = {64u * 2, (cuuint64_t)seq * 64 * 2};
+    cuuint32_t pb[3] = {64u, 64u, 1u};
+    rc = make_map(&tP, patches, 3, pd, ps, pb, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    return cuda_status(launch_l0_tgrad_tc(tG, tP, a, S(stream)), "l0_tgrad_tc");
+  }
   return cuda_status(launch_l0_tgrad(a, S(stream)), "l0_tgrad");
 }
 

@@ -126,6 +126,8 @@ struct L0TgradArgs {
   float* T;                      // [g][PP][D] fp32
 };
 cudaError_t launch_l0_tgrad(const L0TgradArgs& a, cudaStream_t st);
+cudaError_t launch_l0_tgrad_tc(const CUtensorMap& tG, const CUtensorMap& tP,
+                               const L0TgradArgs& a, cudaStream_t st);
 cudaError_t launch_vit_tokens(const void* agg, int f32, const float* mask,
                               const float* mask_token, const float* meta_tok, void* out, int B,
                               int S, int D, cudaStream_t st);

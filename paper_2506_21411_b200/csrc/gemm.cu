@@ -538,4 +538,159 @@ cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUte
   }
 }
 
+// =====================================================================  K_tgc
+// Training backward, tcgen05 form of K_tg (comb.cu):  T_c^T[d][k] = sum_r (p_c[r][h(d)] G[r][d])
+// patch_c[r][k] for one channel c and 128 columns d per CTA. Both operands are MN-major
+// (their natural global layouts): A = G tile [64 r][128 d] and B = patch tile [64 r][64 k],
+// each TMA'd as 128B-swizzled atoms (64 MN elements x 8 K rows); builder warps scale the A
+// tile in place by p (a row of one 64-column half belongs to one head, so the swizzle never
+// has to be undone); one thread issues M128 N64 K16 MMAs into a 64-column TMEM accumulator.
+constexpr int TGC_STAGES = 4;
+constexpr int TGC_A_BYTES = 2 * 64 * 64 * 2;    // two 64-column halves x 64 rows
+constexpr int TGC_B_BYTES = 64 * 64 * 2;
+constexpr int TGC_STAGE = TGC_A_BYTES + TGC_B_BYTES;
+constexpr int TGC_SMEM = TGC_STAGES * TGC_STAGE + 1024 + 256;
+
+__global__ void __launch_bounds__(192, 2)
+    l0_tgrad_tc_kernel(const __grid_constant__ CUtensorMap tmG,
+                       const __grid_constant__ CUtensorMap tmP, L0TgradArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TGC_STAGES * TGC_STAGE);
+  uint64_t* scaled = full + TGC_STAGES;
+  uint64_t* empty = scaled + TGC_STAGES;
+  uint64_t* done = empty + TGC_STAGES;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = warp_id(), lane = lane_id();
+  const int c = blockIdx.y, d0 = blockIdx.x * 128;
+  const int nst = a.R / 64;
+  const int dh = a.D / a.H;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmG);
+    tma_prefetch(&tmP);
+    for (int s = 0; s < TGC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&scaled[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tslot, 64);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int i = 0; i < nst; ++i) {
+        const int s = i % TGC_STAGES;
+        mbar_wait(&empty[s], ((i / TGC_STAGES) & 1) ^ 1);
+        uint8_t* sa = smem + s * TGC_STAGE;
+        mbar_expect_tx(&full[s], TGC_STAGE);
+        const int r0 = i * 64, b = r0 / a.S, s0 = r0 - b * a.S;
+        tma_load_2d(sa, &tmG, &full[s], d0, r0);
+        tma_load_2d(sa + TGC_A_BYTES / 2, &tmG, &full[s], d0 + 64, r0);
+        tma_load_3d(sa + TGC_A_BYTES, &tmP, &full[s], 0, s0, b * a.cnt + a.c0 + c);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_bf16_f32(128, 64) | (1u << 15) | (1u << 16);
+    for (int i = 0; i < nst; ++i) {
+      const int s = i % TGC_STAGES;
+      mbar_wait(&scaled[s], (i / TGC_STAGES) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sa = smem_u32(smem + s * TGC_STAGE), sb = sa + TGC_A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t ad = smem_desc(sa + kk * 2048, TGC_A_BYTES / 2, 1024, 2u);
+          const uint64_t bd = smem_desc(sb + kk * 2048, TGC_B_BYTES, 1024, 2u);
+          mma_ss(tmem, ad, bd, idesc, (i | kk) != 0);
+        }
+        mma_commit(&empty[s]);
+        if (i == nst - 1) mma_commit(done);
+      }
+      __syncwarp();
+    }
+  } else {
+    // builders: thread t scales row r = t % 64 of half mh = t / 64 by p[r][head(mh)]
+    const int t = threadIdx.x - 64;
+    const int row = t & 63, mh = t >> 6;
+    const int head = (d0 + mh * 64) / dh;
+    const int hA = d0 / dh;
+    const int hg = hA / (a.NH > 0 ? a.NH : 1);
+    const int hn = (hA - hg * a.NH) & ~1;
+    const int sel = head & 1;
+    const float mixc = a.mix ? __ldg(a.mix + c) : 0.f;
+    auto pval = [&](int i) -> float {
+      if (a.mix) return mixc;
+      const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(
+          a.p + ((size_t)(hg * a.g + c) * a.R + i * 64 + row) * a.NH + hn));
+      return sel ? bf16hi(w) : bf16lo(w);
+    };
+    float pn = pval(0);
+    for (int i = 0; i < nst; ++i) {
+      const int s = i % TGC_STAGES;
+      const float pc = pn;
+      if (i + 1 < nst) pn = pval(i + 1);  // next stage's p in flight during this one
+      mbar_wait(&full[s], (i / TGC_STAGES) & 1);
+      const uint32_t rowaddr = smem_u32(smem + s * TGC_STAGE) + mh * (TGC_A_BYTES / 2) +
+                               (row >> 3) * 1024 + (row & 7) * 128;
+      // rows sit 128 B apart: visit the row's 16-byte chunks in a row-rotated order so the
+      // 8 rows of a swizzle atom hit 8 different bank groups (all chunks share one p)
+      uint32_t v[8][4];
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        const uint32_t ad = rowaddr + (((ch + row) & 7) << 4);
+        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[ch][0]), "=r"(v[ch][1]), "=r"(v[ch][2]), "=r"(v[ch][3]) : "r"(ad));
+      }
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        const uint32_t ad = rowaddr + (((ch + row) & 7) << 4);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          v[ch][e] = pack_bf16(bf16lo(v[ch][e]) * pc, bf16hi(v[ch][e]) * pc);
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ad), "r"(v[ch][0]),
+                     "r"(v[ch][1]), "r"(v[ch][2]), "r"(v[ch][3])
+                     : "memory");
+      }
+      fence_async_smem();  // generic-proxy writes -> visible to the tensor core
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&scaled[s]);
+    }
+    // epilogue: lane quarter q of the accumulator = rows d0 + 32 q .. +31, 64 columns k
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int d = d0 + q * 32 + lane;
+    float* out = a.T + (size_t)c * 64 * a.D + d;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + half * 32, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) out[(size_t)(half * 32 + j) * a.D] = __uint_as_float(r[j]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 64);
+  }
+}
+
+cudaError_t launch_l0_tgrad_tc(const CUtensorMap& tG, const CUtensorMap& tP,
+                               const L0TgradArgs& a, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(l0_tgrad_tc_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, TGC_SMEM);
+  if (e != cudaSuccess) return e;
+  l0_tgrad_tc_kernel<<<dim3(a.D / 128, a.g), 192, TGC_SMEM, st>>>(tG, tP, a);
+  return cudaGetLastError();
+}
+
 }  // namespace dchag
