@@ -383,7 +383,8 @@ def b200_arm(args, wl, tp, max_group):
                     "ms": None}]
     dom = max(kernels, key=lambda k: k["ms"] or 0)
     dom_plan = next((p for p in plan if p[1] == dom.get("site")), None)
-    tensor_bound = dom["kernel"] in ("dchag_l0_node", "dchag_gemm_bf16", "dchag_l0_logits")
+    tensor_bound = dom["kernel"] in ("dchag_l0_node", "dchag_gemm_bf16", "dchag_l0_logits",
+                                     "dchag_gemm_combine")
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:

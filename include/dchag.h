@@ -54,6 +54,20 @@ int dchag_gemm_rowdot(const void* A, int G, int Mo, int Mi, int K, long long sAg
                       const float* bias, long long bias_g, const void* Gmat, long long ldG,
                       float* dot_out, void* stream);
 
+/* Tree level >= 1 fused (K_gemm COMB instance): each child's folded value projection
+ * V_c = ctx_c W_c^T + bias_c (layers.py:123 output projection folded with the parent's
+ * value projection) and the parent's softmax-weighted child sum (layers.py:114-122) in one
+ * kernel; V never reaches memory. ctx bf16 [n_children][R][D]; W bf16 rows [D][D] per child
+ * at stride sWg elements (the value rows of the folded [N][D] weights); bias fp32 at
+ * stride bias_g; Lpre fp32 [n_children][R][H] = the children's logits for the parent
+ * (a dchag_gemm_bf16 over the logit rows); parent j owns children first[j] ..
+ * first[j]+count[j]-1 (device int32). out bf16 [n_parents][R][D]. R % 256 == 0,
+ * D % 256 == 0, (D/H) % 32 == 0. The running sum is kept as fp16 pairs (fp32 math). */
+int dchag_gemm_combine(const void* ctx, int n_children, int R, int D, int H, const void* W,
+                       long long sWg, const float* bias, long long bias_g, const float* Lpre,
+                       const int* first, const int* count, int n_parents, void* out,
+                       void* stream);
+
 /* Level-0 logits + softmax over each node's channels (K_p0): replaces the
  * q@wq / x@wk / logits / softmax part of layers.py:103-121 for tree level 0 with the
  * tokenizer (model.py:51-64) folded in.  img: bf16 [B][*][Himg][W] with batch stride

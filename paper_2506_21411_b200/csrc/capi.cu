@@ -198,6 +198,52 @@ int dchag_gemm_rowdot(const void* A, int G, int Mo, int Mi, int K, long long sAg
                    1, nullptr, 0, 0, 0, 0, nullptr, 0, 0, 0, Gmat, ldG, dot_out, stream);
 }
 
+int dchag_gemm_combine(const void* ctx, int n_children, int R, int D, int H, const void* W,
+                       long long sWg, const float* bias, long long bias_g, const float* Lpre,
+                       const int* first, const int* count, int n_parents, void* out,
+                       void* stream) {
+  if (n_children < 1 || n_parents < 1 || R < 256 || R % 256 || D < 256 || D % 256 || H < 1 ||
+      D % H || (D / H) % 32 || !Lpre || !first || !count || !out)
+    return fail(DCHAG_ERR_SHAPE, "gemm_combine: bad shape R=%d D=%d H=%d", R, D, H);
+  if ((reinterpret_cast<uintptr_t>(ctx) | reinterpret_cast<uintptr_t>(W) |
+       reinterpret_cast<uintptr_t>(out) | (uintptr_t)(sWg * 2)) % 16)
+    return fail(DCHAG_ERR_SHAPE, "gemm_combine: pointers / strides must be 16-byte aligned");
+  const int bn = 256;
+  CUtensorMap tA, tW, tV;
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)R, 1, (cuuint64_t)n_children};
+    cuuint64_t str[3] = {(cuuint64_t)D * 2, (cuuint64_t)R * D * 2, (cuuint64_t)R * D * 2};
+    cuuint32_t box[4] = {64u, 128u, 1, 1};
+    int rc = make_map(&tA, ctx, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)D, (cuuint64_t)n_children};
+    cuuint64_t str[2] = {(cuuint64_t)D * 2, (cuuint64_t)sWg * 2};
+    cuuint32_t box[3] = {64u, (cuuint32_t)(bn / 2), 1};
+    int rc = make_map(&tW, W, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)R, 1, (cuuint64_t)n_parents};
+    cuuint64_t str[3] = {(cuuint64_t)D * 2, (cuuint64_t)R * D * 2, (cuuint64_t)R * D * 2};
+    cuuint32_t box[4] = {32, 32, 1, 1};
+    int rc = make_map(&tV, out, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+  }
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.G = n_parents; a.M = R; a.Mi = R; a.N = D; a.Nv = D; a.K = D; a.BN = bn;
+  a.pair = 1; a.v_tma = 1;
+  a.bias = bias; a.bias_g = bias_g;
+  a.rowbias_period = 1;
+  a.outV = out; a.sVg = (long long)R * D; a.sVmo = 0; a.sVmi = D;
+  a.cfirst = first; a.ccount = count; a.Lpre = Lpre; a.H = H; a.dh = D / H;
+  a.debug = getenv("DCHAG_GEMM_DEBUG") ? atoi(getenv("DCHAG_GEMM_DEBUG")) : 0;
+  return cuda_status(launch_gemm(tA, tW, tV, a, 64, num_sms_cached(), S(stream)),
+                     "gemm_combine");
+}
+
 int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, int Himg, int W,
                     int P, int H, int HP, int nh, int n_nodes, int gmax, const int* node_c0,
                     const int* node_g,

@@ -29,6 +29,13 @@ struct GemmArgs {
   const __nv_bfloat16* dotG;    // [M][ldG] bf16, shared by all groups
   long long ldG;
   float* dotOut;
+  // combine mode (the COMB kernel instance): G counts parents; output group j is the
+  // softmax-weighted sum over its children g = cfirst[j] .. +ccount[j]-1 (the A / W / bias
+  // groups) of the child tiles, weights softmax_c(Lpre[g][m][n / dh]) (layers.py:114-122)
+  const int* cfirst;
+  const int* ccount;
+  const float* Lpre;            // [children][M][H] fp32 logits
+  int H, dh;
 };
 
 cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUtensorMap& tV,

@@ -10,6 +10,8 @@
 //
 // Persistent grid; warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
 // warps 2..5 = epilogue (one TMEM lane quarter each).
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "dchag_kernels.h"
 
@@ -76,7 +78,7 @@ DEV void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cl, int 
       : "memory");
 }
 
-template <int BK, int STAGES, bool PAIR>
+template <int BK, int STAGES, bool PAIR, bool COMB = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                 const __grid_constant__ CUtensorMap tmV, GemmArgs args) {
@@ -106,7 +108,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // Row-dot mode walks the groups innermost over a contiguous chunk of tiles per CTA, so
   // consecutive tiles of a CTA share (mt, nt) and the epilogue keeps its dotG rows in
   // registers across the groups; otherwise tiles are strided over the CTAs, groups outermost.
-  const bool dot_mode = args.dotOut != nullptr;
+  const bool dot_mode = !COMB && args.dotOut != nullptr;
+  constexpr bool comb = COMB;
   const int chunk = (total_ct + ncl - 1) / ncl;
   const int ct_begin = dot_mode ? cid * chunk : cid;
   const int ct_end = dot_mode ? min(total_ct, ct_begin + chunk) : total_ct;
@@ -163,11 +166,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       const int w_rows = args.BN / CL;
       for (int ct = ct_begin; ct < ct_end; ct += ct_step) {
-        int g, mt, nt;
-        decode(ct, g, mt, nt);
+        int g0, mt, nt;
+        decode(ct, g0, mt, nt);
         const int m0 = mt * GEMM_BM;
         const int mo = m0 / args.Mi, mi = m0 - mo * args.Mi;
+        const int c_first = comb ? __ldg(args.cfirst + g0) : g0;
+        const int c_n = comb ? __ldg(args.ccount + g0) : 1;
+        for (int ci = 0; ci < c_n; ++ci)
         for (int ks = 0; ks < k_steps; ++ks) {
+          const int g = c_first + ci;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * SM::STAGE_BYTES;
           uint8_t* sW = sA + SM::A_BYTES;
@@ -197,6 +204,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int ct = ct_begin; ct < ct_end; ct += ct_step) {
+       int c_n = 1;
+       if (comb) {
+         int g0, mt, nt;
+         decode(ct, g0, mt, nt);
+         c_n = __ldg(args.ccount + g0);
+       }
+       for (int ci = 0; ci < c_n; ++ci) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogues drained this accumulator buffer
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * GEMM_BN_MAX;
@@ -227,6 +241,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+       }
       }
     }
   } else {
@@ -255,13 +270,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int mo = m_row / args.Mi, mi = m_row - mo * args.Mi;
       // prefetch this thread's row bias for its column groups (in flight during the wait)
       // row-dot mode: the same registers carry this row's dotG columns instead
-      const bool dot = args.dotOut != nullptr;
+      const bool dot = !COMB && args.dotOut != nullptr;
       const __nv_bfloat16* rb =
           dot ? args.dotG + (size_t)m_row * args.ldG
           : (args.rowbias && !(args.debug & 2)) ? args.rowbias + (size_t)g * args.rowbias_g +
                              (size_t)(mi % args.rowbias_period) * args.rowbias_row
                        : nullptr;
-      const bool reload = !dot || mt != prev_mt || nt != prev_nt;
+      const bool reload = !COMB && (!dot || mt != prev_mt || nt != prev_nt);
       prev_mt = mt;
       prev_nt = nt;
 #pragma unroll
@@ -288,8 +303,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
       }
+      // combine mode: softmax statistics of this row over the parent's children, per group
+      const int c_first = comb ? __ldg(args.cfirst + g) : g;
+      const int c_n = comb ? __ldg(args.ccount + g) : 1;
+      float cm[4], cs[4];
+      __half2 run[COMB ? 4 : 1][16];  // running weighted sum (fp16 pairs; fp32 math)
+      if constexpr (COMB) {
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+          const int hd = min((nt * args.BN + (hf + 2 * gi) * 32) / args.dh, args.H - 1);
+          const float* lp = args.Lpre + (size_t)m_row * args.H + hd;
+          float mx = -INFINITY;
+          for (int cc = 0; cc < c_n; ++cc)
+            mx = fmaxf(mx, __ldg(lp + (size_t)(c_first + cc) * args.M * args.H));
+          float sum = 0.f;
+          for (int cc = 0; cc < c_n; ++cc)
+            sum += __expf(__ldg(lp + (size_t)(c_first + cc) * args.M * args.H) - mx);
+          cm[gi] = mx;
+          cs[gi] = 1.f / sum;
+        }
+      }
+      for (int ci = 0; ci < c_n; ++ci) {
+      const int gb = c_first + ci;  // bias / logit group of this tile (the child in COMB)
       const float* bias =
-          (args.bias && !(args.debug & 2)) ? args.bias + (size_t)g * args.bias_g : nullptr;
+          (args.bias && !(args.debug & 2)) ? args.bias + (size_t)gb * args.bias_g : nullptr;
       // this warp's bias columns (groups hf, hf+2, hf+4, hf+6) -> shared memory with one
       // coalesced load per lane, read back as broadcasts (the per-group global loads of every
       // lane were the epilogue's largest cost)
@@ -344,13 +381,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           args.dotOut[((size_t)g * (args.N >> 5) + (n0 >> 5)) * args.M + m_row] = sdot;
           continue;
         }
+        if constexpr (COMB) {  // no row bias in combine mode
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t q[4] = {rbv[gi][j].x, rbv[gi][j].y, rbv[gi][j].z, rbv[gi][j].w};
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        } else {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            v[8 * j + 2 * e] = __uint_as_float(r[8 * j + 2 * e]) + bf16lo(q[e]);
-            v[8 * j + 2 * e + 1] = __uint_as_float(r[8 * j + 2 * e + 1]) + bf16hi(q[e]);
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t q[4] = {rbv[gi][j].x, rbv[gi][j].y, rbv[gi][j].z, rbv[gi][j].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              v[8 * j + 2 * e] = __uint_as_float(r[8 * j + 2 * e]) + bf16lo(q[e]);
+              v[8 * j + 2 * e + 1] = __uint_as_float(r[8 * j + 2 * e + 1]) + bf16hi(q[e]);
+            }
           }
         }
         if (bias) {
@@ -359,6 +401,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const float4 b4 = reinterpret_cast<const float4*>(wbias + gi * 32)[j / 4];
             v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
           }
+        }
+        if constexpr (COMB) {
+          const int hd = min(n0 / args.dh, args.H - 1);
+          const float pw =
+              __expf(__ldg(args.Lpre + ((size_t)gb * args.M + m_row) * args.H + hd) - cm[gi]) *
+              cs[gi];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float2 o = ci ? __half22float2(run[gi][j]) : make_float2(0.f, 0.f);
+            o.x = fmaf(pw, v[2 * j], o.x);
+            o.y = fmaf(pw, v[2 * j + 1], o.y);
+            if (ci + 1 < c_n) {
+              run[gi][j] = __float22half2_rn(o);
+            } else {
+              v[2 * j] = o.x;
+              v[2 * j + 1] = o.y;
+            }
+          }
+          if (ci + 1 < c_n) continue;
         }
         if (args.debug & 1) {
           if (__float_as_uint(v[0]) == 0x7fc00001u) args.outL[0] = v[1];
@@ -478,6 +539,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_arrive(&tempty[acc]);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }  // children (COMB)
     }
     if (lane == 0) bulk_wait0();  // this warp's tensor stores complete before exit
   }
@@ -495,13 +557,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-template <int BK, int STAGES, bool PAIR>
+template <int BK, int STAGES, bool PAIR, bool COMB = false>
 static cudaError_t launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tW,
                                  const CUtensorMap& tV, const GemmArgs& a, int num_sms,
                                  cudaStream_t st) {
   using SM = GemmSmem<BK, STAGES, PAIR>;
   static_assert(SM::TOTAL <= 227 * 1024, "shared memory");
-  auto kern = gemm_kernel<BK, STAGES, PAIR>;
+  auto kern = gemm_kernel<BK, STAGES, PAIR, COMB>;
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
   if (e != cudaSuccess) return e;
@@ -530,6 +592,8 @@ cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUte
                         const GemmArgs& a, int bk, int num_sms, cudaStream_t st) {
   switch (bk) {
     case 64:
+      if (a.pair && a.cfirst) return launch_gemm_t<64, 5, true, true>(tA, tW, tV, a, num_sms, st);
+      if (a.cfirst) return cudaErrorInvalidValue;
       if (a.pair) return launch_gemm_t<64, 5, true>(tA, tW, tV, a, num_sms, st);
       return launch_gemm_t<64, 3, false>(tA, tW, tV, a, num_sms, st);
     case 32: return launch_gemm_t<32, 6, false>(tA, tW, tV, a, num_sms, st);

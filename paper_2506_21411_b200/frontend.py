@@ -102,6 +102,8 @@ class DchagFrontEnd(torch.nn.Module):
         # layer's work per rank shrink by ~tp.
         self.final_position_split = bool(final_position_split)
         self.ledger = None  # optional ledger.CommLedger: every collective issued is recorded
+        # levels below the root: projection + parent combine in one K_gemm (COMB instance)
+        self.fuse_combine = os.environ.get("DCHAG_FUSE_COMBINE", "1") != "0"
         # tp > 1 device forward: batch chunks whose exchange overlaps the next chunk's kernels
         # (measured on 2 B200 at H2: 1 chunk 20.7k img/s, 2 chunks 18.9k, 4 chunks 18.3k --
         # the exchange is short and smaller launches lose more, so off by default)
@@ -431,6 +433,13 @@ class DchagFrontEnd(torch.nn.Module):
         depth = len(pk.levels)
         for li in range(depth):
             n_l, N = len(pk.levels[li]), pk.N[li]
+            if self._fused_level(pk, li, R):
+                n_next = len(pk.levels[li + 1])
+                plan.append(("dchag_gemm_bf16", f"gemm_logits_l{li}", 2 * R * n_l * d * h,
+                             n_l * R * d * 2 + n_l * R * h * 4))
+                plan.append(("dchag_gemm_combine", f"gemm_combine_l{li}", 2 * R * n_l * d * d,
+                             n_l * R * d * 2 + n_l * d * d * 2 + n_next * R * d * 2))
+                continue
             plan.append(("dchag_gemm_bf16", f"gemm_l{li}", 2 * R * n_l * d * N,
                          n_l * R * d * 2 + n_l * R * (d * 2 + (N - d) * 4) + n_l * N * d * 2))
             if li + 1 < depth:
@@ -475,6 +484,12 @@ class DchagFrontEnd(torch.nn.Module):
         while n > 1 and (B % n or not self._position_split(B // n)):
             n -= 1
         return n if self.tp > 1 else 1
+
+    def _fused_level(self, pk, li, R):
+        """Level li's projection fused with level li+1's combine (cross-attention parent)."""
+        d, h = self.model.embed, self.model.heads
+        return (self.fuse_combine and li + 1 < len(pk.levels) and pk.N[li] == d + h
+                and R % 256 == 0 and d % 256 == 0 and (d // h) % 32 == 0 and h % 16 == 0)
 
     def _position_split(self, B):
         rows = B * self.seq
@@ -609,6 +624,23 @@ class DchagFrontEnd(torch.nn.Module):
             n_l = len(pk.levels[li])
             N = pk.N[li]
             logits = N > d
+            if self._fused_level(pk, li, R):
+                # the children's logits for their parent (a thin GEMM over the logit rows of
+                # the folded weights), then projection + softmax-weighted child sum in one
+                # K_gemm (COMB): the child values never reach memory
+                n_next = len(pk.levels[li + 1])
+                Lpre = torch.empty(n_l, R, h, **f32)
+                _lib.call("dchag_gemm_bf16", _lib.ptr(ctx), n_l, 1, R, d, R * d, 0, d,
+                          _lib.ptr(pk.Wp[li][:, d:]), h, N * d, 0,
+                          _lib.ptr(pk.bp[li][:, d:]), N, 0, 0, 0, 1, 0, 0, 0, 0, 0,
+                          _lib.ptr(Lpre), R * h, 0, h, st)
+                nxt = torch.empty(n_next, R, d, **bf16)
+                _lib.call("dchag_gemm_combine", _lib.ptr(ctx), n_l, R, d, h, _lib.ptr(pk.Wp[li]),
+                          N * d, _lib.ptr(pk.bp[li]), N, _lib.ptr(Lpre),
+                          _lib.ptr(pk.comb_first[li]), _lib.ptr(pk.comb_g[li]), n_next,
+                          _lib.ptr(nxt), st)
+                ctx = nxt
+                continue
             if li == depth - 1:
                 # root: write straight into the gather payload (payload.py layout)
                 payload = torch.empty(payload_nbytes(R, d, h), device=dev, dtype=torch.uint8)

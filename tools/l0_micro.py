@@ -14,8 +14,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="hyperspectral")
 ap.add_argument("--batch", type=int, default=32)
 ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--channels", type=int, default=None, help="override (one rank's slab)")
 a = ap.parse_args()
-wl = WORKLOADS[a.workload]
+wl = dict(WORKLOADS[a.workload])
+if a.channels:
+    wl["channels"] = a.channels
 mg = max_group_for_depth([n for _, n in channel_slabs(wl["channels"], 1)], wl["depth"])
 fe = DchagFrontEnd(wl["channels"], wl["image_h"], wl["image_w"], wl["patch"], wl["embed"],
                    wl["heads"], max_group=mg)
