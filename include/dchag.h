@@ -59,14 +59,17 @@ int dchag_gemm_rowdot(const void* A, int G, int Mo, int Mi, int K, long long sAg
  * value projection) and the parent's softmax-weighted child sum (layers.py:114-122) in one
  * kernel; V never reaches memory. ctx bf16 [n_children][R][D]; W bf16 rows [D][D] per child
  * at stride sWg elements (the value rows of the folded [N][D] weights); bias fp32 at
- * stride bias_g; Lpre fp32 [n_children][R][H] = the children's logits for the parent
- * (a dchag_gemm_bf16 over the logit rows); parent j owns children first[j] ..
- * first[j]+count[j]-1 (device int32). out bf16 [n_parents][R][D]. R % 256 == 0,
- * D % 256 == 0, (D/H) % 32 == 0. The running sum is kept as fp16 pairs (fp32 math). */
+ * stride bias_g; Lpre fp32 [n_children][R][H] = the children's softmax weights (a
+ * dchag_gemm_bf16 over the logit rows, then dchag_child_softmax); parent j owns children first[j] ..
+ * first[j]+count[j]-1 (device int32). out bf16 [csplit][n_parents][R][D]: with csplit 2
+ * (every parent with >= 2 children) split s holds the sum over children
+ * [s c/2, (s+1) c/2) with the full softmax, and out[0] + out[1] is the result (more, smaller
+ * work units when parents are few). R % 256 == 0, D % 256 == 0, (D/H) % 32 == 0. The
+ * running sum is kept as fp16 pairs (fp32 math). */
 int dchag_gemm_combine(const void* ctx, int n_children, int R, int D, int H, const void* W,
                        long long sWg, const float* bias, long long bias_g, const float* Lpre,
-                       const int* first, const int* count, int n_parents, void* out,
-                       void* stream);
+                       const int* first, const int* count, int n_parents, int csplit,
+                       void* out, void* stream);
 
 /* Level-0 logits + softmax over each node's channels (K_p0): replaces the
  * q@wq / x@wk / logits / softmax part of layers.py:103-121 for tree level 0 with the
@@ -130,6 +133,12 @@ int dchag_vit_tokens(const void* agg, int agg_f32, int B, int seq, int D, const 
 int dchag_l0_tgrad(const void* patches, int cnt, int c0, int g, int R, int seq, int D, int H,
                    int nh, int PP, const void* p, const float* mix, const void* G, float* T,
                    void* stream);
+
+/* Softmax over each parent's children in place (layers.py:114-120 above level 0):
+ * L fp32 [children][R][H] logits -> p, parent j's children first[j] .. first[j]+count[j]-1
+ * (device int32). The weights dchag_gemm_combine applies. */
+int dchag_child_softmax(float* L, const int* first, const int* count, int n_parents, int R,
+                        int H, void* stream);
 
 /* fp32 parity mode combine: as dchag_combine with fp32 child values V (row r of child j at
  * V + j*sVj + r*D) and an fp32 context (precise expf, fp32 accumulation). */

@@ -25,7 +25,7 @@ SIGNATURES = {
     "dchag_gemm_rowdot": [c_vp, c_int, c_int, c_int, c_int, c_ll, c_ll, c_ll, c_vp, c_int,
                           c_ll, c_vp, c_ll, c_vp, c_ll, c_vp, c_vp],
     "dchag_gemm_combine": [c_vp, c_int, c_int, c_int, c_int, c_vp, c_ll, c_vp, c_ll, c_vp,
-                           c_vp, c_vp, c_int, c_vp, c_vp],
+                           c_vp, c_vp, c_int, c_int, c_vp, c_vp],
     "dchag_l0_logits": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                         c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "dchag_l0_node": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
@@ -37,6 +37,7 @@ SIGNATURES = {
     "dchag_vit_tokens": [c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp],
     "dchag_l0_tgrad": [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                        c_vp, c_vp, c_vp, c_vp, c_vp],
+    "dchag_child_softmax": [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_vp],
     "dchag_combine_f32": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_vp, c_ll,
                           c_vp, c_vp, c_vp],
     "dchag_fullcross_weights": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_ll,

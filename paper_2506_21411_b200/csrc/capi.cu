@@ -200,8 +200,10 @@ int dchag_gemm_rowdot(const void* A, int G, int Mo, int Mi, int K, long long sAg
 
 int dchag_gemm_combine(const void* ctx, int n_children, int R, int D, int H, const void* W,
                        long long sWg, const float* bias, long long bias_g, const float* Lpre,
-                       const int* first, const int* count, int n_parents, void* out,
-                       void* stream) {
+                       const int* first, const int* count, int n_parents, int csplit,
+                       void* out, void* stream) {
+  if (csplit != 1 && csplit != 2)
+    return fail(DCHAG_ERR_SHAPE, "gemm_combine: csplit must be 1 or 2");
   if (n_children < 1 || n_parents < 1 || R < 256 || R % 256 || D < 256 || D % 256 || H < 1 ||
       D % H || (D / H) % 32 || !Lpre || !first || !count || !out)
     return fail(DCHAG_ERR_SHAPE, "gemm_combine: bad shape R=%d D=%d H=%d", R, D, H);
@@ -225,7 +227,7 @@ int dchag_gemm_combine(const void* ctx, int n_children, int R, int D, int H, con
     if (rc) return rc;
   }
   {
-    cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)R, 1, (cuuint64_t)n_parents};
+    cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)R, 1, (cuuint64_t)n_parents * csplit};
     cuuint64_t str[3] = {(cuuint64_t)D * 2, (cuuint64_t)R * D * 2, (cuuint64_t)R * D * 2};
     cuuint32_t box[4] = {32, 32, 1, 1};
     int rc = make_map(&tV, out, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -233,7 +235,8 @@ int dchag_gemm_combine(const void* ctx, int n_children, int R, int D, int H, con
   }
   GemmArgs a;
   memset(&a, 0, sizeof(a));
-  a.G = n_parents; a.M = R; a.Mi = R; a.N = D; a.Nv = D; a.K = D; a.BN = bn;
+  a.G = n_parents * csplit; a.M = R; a.Mi = R; a.N = D; a.Nv = D; a.K = D; a.BN = bn;
+  a.nparents = n_parents; a.csplit = csplit;
   a.pair = 1; a.v_tma = 1;
   a.bias = bias; a.bias_g = bias_g;
   a.rowbias_period = 1;
@@ -402,6 +405,14 @@ int dchag_l0_tgrad(const void* patches, int cnt, int c0, int g, int R, int seq, 
     return cuda_status(launch_l0_tgrad_tc(tG, tP, a, S(stream)), "l0_tgrad_tc");
   }
   return cuda_status(launch_l0_tgrad(a, S(stream)), "l0_tgrad");
+}
+
+int dchag_child_softmax(float* L, const int* first, const int* count, int n_parents, int R,
+                        int H, void* stream) {
+  if (!L || !first || !count || n_parents < 1 || R < 1 || H < 1)
+    return fail(DCHAG_ERR_SHAPE, "child_softmax: bad arguments");
+  return cuda_status(launch_child_softmax(L, first, count, n_parents, R, H, S(stream)),
+                     "child_softmax");
 }
 
 int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,

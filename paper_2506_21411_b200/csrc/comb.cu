@@ -487,6 +487,40 @@ cudaError_t launch_l0_tgrad(const L0TgradArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Softmax over each parent's children, in place: L[c][r][h] (c = first[j] .. +count[j]-1)
+// -> p (layers.py:114-120 for a node above level 0; the operand of K_gemm's COMB epilogue).
+// One thread per (parent, row, head); the children's logits of a (row, head) are strided.
+__global__ void __launch_bounds__(256) child_softmax_kernel(float* __restrict__ L,
+                                                           const int* __restrict__ first,
+                                                           const int* __restrict__ count,
+                                                           int n_parents, int R, int H) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)n_parents * R * H) return;
+  const int j = (int)(idx / ((long long)R * H));
+  const long long rh = idx - (long long)j * R * H;
+  const int f = __ldg(first + j), g = __ldg(count + j);
+  float* base = L + (size_t)f * R * H + rh;
+  const size_t st = (size_t)R * H;
+  float m = -INFINITY;
+  for (int c = 0; c < g; ++c) m = fmaxf(m, base[c * st]);
+  float sum = 0.f;
+  for (int c = 0; c < g; ++c) {
+    const float e = __expf(base[c * st] - m);
+    base[c * st] = e;
+    sum += e;
+  }
+  const float inv = 1.f / sum;
+  for (int c = 0; c < g; ++c) base[c * st] *= inv;
+}
+
+cudaError_t launch_child_softmax(float* L, const int* first, const int* count, int n_parents,
+                                 int R, int H, cudaStream_t st) {
+  const long long n = (long long)n_parents * R * H;
+  child_softmax_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(L, first, count, n_parents,
+                                                                   R, H);
+  return cudaGetLastError();
+}
+
 // full_cross node weights (see FullCrossArgs). One CTA per (node, row), one warp per head;
 // lane j owns child j (g <= 32): it keeps k_j,h in registers and computes the row of logits
 // L_ij = q_i . k_j / sqrt(dh) against q_i broadcast from shared memory; the per-i softmax,

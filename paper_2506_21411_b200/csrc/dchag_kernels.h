@@ -36,6 +36,8 @@ struct GemmArgs {
   const int* ccount;
   const float* Lpre;            // [children][M][H] fp32 logits
   int H, dh;
+  int nparents;                 // COMB: G = nparents * csplit; group g = split s * nparents + j
+  int csplit;                   // 1, or 2: split s sums children [s c/2, (s+1) c/2) (partials)
 };
 
 cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUtensorMap& tV,
@@ -133,6 +135,8 @@ struct L0TgradArgs {
   float* T;                      // [g][PP][D] fp32
 };
 cudaError_t launch_l0_tgrad(const L0TgradArgs& a, cudaStream_t st);
+cudaError_t launch_child_softmax(float* L, const int* first, const int* count, int n_parents,
+                                 int R, int H, cudaStream_t st);
 cudaError_t launch_l0_tgrad_tc(const CUtensorMap& tG, const CUtensorMap& tP,
                                const L0TgradArgs& a, cudaStream_t st);
 cudaError_t launch_vit_tokens(const void* agg, int f32, const float* mask,

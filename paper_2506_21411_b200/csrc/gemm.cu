@@ -130,6 +130,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     mt = mc * CL + crank;
   };
 
+  // COMB: children [c_first, c_first + c_n) summed by output group g (split s of parent j)
+  auto comb_range = [&](int g, int& c_first, int& c_n) {
+    const int j = g % args.nparents, sp = g / args.nparents;
+    const int f = __ldg(args.cfirst + j), n = __ldg(args.ccount + j);
+    const int lo = sp * n / args.csplit, hi = (sp + 1) * n / args.csplit;
+    c_first = f + lo;
+    c_n = hi - lo;
+  };
+
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmW);
@@ -170,8 +179,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         decode(ct, g0, mt, nt);
         const int m0 = mt * GEMM_BM;
         const int mo = m0 / args.Mi, mi = m0 - mo * args.Mi;
-        const int c_first = comb ? __ldg(args.cfirst + g0) : g0;
-        const int c_n = comb ? __ldg(args.ccount + g0) : 1;
+        int c_first = g0, c_n = 1;
+        if (comb) comb_range(g0, c_first, c_n);
         for (int ci = 0; ci < c_n; ++ci)
         for (int ks = 0; ks < k_steps; ++ks) {
           const int g = c_first + ci;
@@ -206,9 +215,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int ct = ct_begin; ct < ct_end; ct += ct_step) {
        int c_n = 1;
        if (comb) {
-         int g0, mt, nt;
+         int g0, mt, nt, cf;
          decode(ct, g0, mt, nt);
-         c_n = __ldg(args.ccount + g0);
+         comb_range(g0, cf, c_n);
        }
        for (int ci = 0; ci < c_n; ++ci) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogues drained this accumulator buffer
@@ -304,25 +313,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       }
       // combine mode: softmax statistics of this row over the parent's children, per group
-      const int c_first = comb ? __ldg(args.cfirst + g) : g;
-      const int c_n = comb ? __ldg(args.ccount + g) : 1;
-      float cm[4], cs[4];
+      int c_first = g, c_n = 1;
+      if (comb) comb_range(g, c_first, c_n);
       __half2 run[COMB ? 4 : 1][16];  // running weighted sum (fp16 pairs; fp32 math)
-      if constexpr (COMB) {
-#pragma unroll
-        for (int gi = 0; gi < 4; ++gi) {
-          const int hd = min((nt * args.BN + (hf + 2 * gi) * 32) / args.dh, args.H - 1);
-          const float* lp = args.Lpre + (size_t)m_row * args.H + hd;
-          float mx = -INFINITY;
-          for (int cc = 0; cc < c_n; ++cc)
-            mx = fmaxf(mx, __ldg(lp + (size_t)(c_first + cc) * args.M * args.H));
-          float sum = 0.f;
-          for (int cc = 0; cc < c_n; ++cc)
-            sum += __expf(__ldg(lp + (size_t)(c_first + cc) * args.M * args.H) - mx);
-          cm[gi] = mx;
-          cs[gi] = 1.f / sum;
-        }
-      }
       for (int ci = 0; ci < c_n; ++ci) {
       const int gb = c_first + ci;  // bias / logit group of this tile (the child in COMB)
       const float* bias =
@@ -403,10 +396,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         if constexpr (COMB) {
+          // Lpre holds the softmax over the parent's children (dchag_child_softmax)
           const int hd = min(n0 / args.dh, args.H - 1);
-          const float pw =
-              __expf(__ldg(args.Lpre + ((size_t)gb * args.M + m_row) * args.H + hd) - cm[gi]) *
-              cs[gi];
+          const float pw = __ldg(args.Lpre + ((size_t)gb * args.M + m_row) * args.H + hd);
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             float2 o = ci ? __half22float2(run[gi][j]) : make_float2(0.f, 0.f);

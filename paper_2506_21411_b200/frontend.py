@@ -104,6 +104,7 @@ class DchagFrontEnd(torch.nn.Module):
         self.ledger = None  # optional ledger.CommLedger: every collective issued is recorded
         # levels below the root: projection + parent combine in one K_gemm (COMB instance)
         self.fuse_combine = os.environ.get("DCHAG_FUSE_COMBINE", "1") != "0"
+        self.combine_split = os.environ.get("DCHAG_COMBINE_SPLIT", "0") != "0"
         # tp > 1 device forward: batch chunks whose exchange overlaps the next chunk's kernels
         # (measured on 2 B200 at H2: 1 chunk 20.7k img/s, 2 chunks 18.9k, 4 chunks 18.3k --
         # the exchange is short and smaller launches lose more, so off by default)
@@ -437,6 +438,8 @@ class DchagFrontEnd(torch.nn.Module):
                 n_next = len(pk.levels[li + 1])
                 plan.append(("dchag_gemm_bf16", f"gemm_logits_l{li}", 2 * R * n_l * d * h,
                              n_l * R * d * 2 + n_l * R * h * 4))
+                plan.append(("dchag_child_softmax", f"child_softmax_l{li + 1}", 0,
+                             2 * n_l * R * h * 4))
                 plan.append(("dchag_gemm_combine", f"gemm_combine_l{li}", 2 * R * n_l * d * d,
                              n_l * R * d * 2 + n_l * d * d * 2 + n_next * R * d * 2))
                 continue
@@ -634,12 +637,20 @@ class DchagFrontEnd(torch.nn.Module):
                           _lib.ptr(pk.Wp[li][:, d:]), h, N * d, 0,
                           _lib.ptr(pk.bp[li][:, d:]), N, 0, 0, 0, 1, 0, 0, 0, 0, 0,
                           _lib.ptr(Lpre), R * h, 0, h, st)
-                nxt = torch.empty(n_next, R, d, **bf16)
+                n_next = len(pk.levels[li + 1])
+                _lib.call("dchag_child_softmax", _lib.ptr(Lpre), _lib.ptr(pk.comb_first[li]),
+                          _lib.ptr(pk.comb_g[li]), n_next, R, h, st)
+                # few parents -> few, long work units: split each parent's children in two
+                # halves (partial sums under the full softmax) when that evens out the waves
+                units = n_next * (R // 256) * (d // 256)
+                split = 2 if (units < 5 * 74 and min(pk.levels[li + 1]) >= 2
+                              and self.combine_split) else 1
+                nxt = torch.empty(split, n_next, R, d, **bf16)
                 _lib.call("dchag_gemm_combine", _lib.ptr(ctx), n_l, R, d, h, _lib.ptr(pk.Wp[li]),
                           N * d, _lib.ptr(pk.bp[li]), N, _lib.ptr(Lpre),
-                          _lib.ptr(pk.comb_first[li]), _lib.ptr(pk.comb_g[li]), n_next,
+                          _lib.ptr(pk.comb_first[li]), _lib.ptr(pk.comb_g[li]), n_next, split,
                           _lib.ptr(nxt), st)
-                ctx = nxt
+                ctx = nxt[0] if split == 1 else torch.add(nxt[0], nxt[1])
                 continue
             if li == depth - 1:
                 # root: write straight into the gather payload (payload.py layout)
