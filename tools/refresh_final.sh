@@ -10,7 +10,7 @@ timeout 600 python bench.py > $O/bench_h1.json 2> $O/bench_h1.err
 timeout 600 python bench.py --workload weather > $O/bench_weather.json 2> $O/bench_weather.err
 timeout 600 python bench.py --workload train > $O/bench_train.json 2> $O/bench_train.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none \
-    -k regex:"l0_node|gemm_kernel|l0_logits|combine_kernel" -c 200 --csv \
+    -k regex:"l0_node|gemm_kernel|l0_logits|combine_kernel|child_softmax" -c 200 --csv \
     --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
     > $O/ncu_launch.log 2>&1
 timeout 300 python tools/train_profile.py > $O/train_profile.txt 2>&1
