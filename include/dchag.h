@@ -140,6 +140,14 @@ int dchag_l0_tgrad(const void* patches, int cnt, int c0, int g, int R, int seq, 
 int dchag_child_softmax(float* L, const int* first, const int* count, int n_parents, int R,
                         int H, void* stream);
 
+/* Level-0 node backward, channel softmax (training; layers.py:114-120 through
+ * tensor.py:201-203): dp_c[r][h] = sum of dchag_gemm_rowdot's 32-column partials of head h
+ * (dpp fp32 [g][H*dh/32][R]) + Gpos[r][h] (dchag_l0_dv), then
+ * dl_c = p_c (dp_c - sum_c' p_c' dp_c'); p as dchag_l0_dv. dl fp32 and dlb bf16, both
+ * [g][H][R]. dh % 32 == 0. */
+int dchag_l0_softmax_bwd(int g, int R, int H, int nh, int dh, const float* dpp,
+                         const float* Gpos, const void* p, float* dl, void* dlb, void* stream);
+
 /* fp32 parity mode combine: as dchag_combine with fp32 child values V (row r of child j at
  * V + j*sVj + r*D) and an fp32 context (precise expf, fp32 accumulation). */
 int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,

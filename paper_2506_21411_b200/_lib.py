@@ -38,6 +38,8 @@ SIGNATURES = {
     "dchag_l0_tgrad": [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                        c_vp, c_vp, c_vp, c_vp, c_vp],
     "dchag_child_softmax": [c_vp, c_vp, c_vp, c_int, c_int, c_int, c_vp],
+    "dchag_l0_softmax_bwd": [c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
+                             c_vp],
     "dchag_combine_f32": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_vp, c_ll,
                           c_vp, c_vp, c_vp],
     "dchag_fullcross_weights": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_ll,

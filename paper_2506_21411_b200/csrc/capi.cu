@@ -415,6 +415,17 @@ int dchag_child_softmax(float* L, const int* first, const int* count, int n_pare
                      "child_softmax");
 }
 
+int dchag_l0_softmax_bwd(int g, int R, int H, int nh, int dh, const float* dpp,
+                         const float* Gpos, const void* p, float* dl, void* dlb, void* stream) {
+  if (g < 1 || R < 1 || H < 1 || dh % 32 || nh < 1 || H % nh || !dpp || !Gpos || !p || !dl ||
+      !dlb)
+    return fail(DCHAG_ERR_SHAPE, "l0_softmax_bwd: bad arguments");
+  return cuda_status(launch_l0_softmax_bwd(g, R, H, nh, dh, dpp, Gpos,
+                                           reinterpret_cast<const __nv_bfloat16*>(p), dl,
+                                           reinterpret_cast<__nv_bfloat16*>(dlb), S(stream)),
+                     "l0_softmax_bwd");
+}
+
 int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
                       int max_g, const float* V, long long sVj, const float* L, long long sLj,
                       const float* mix, float* ctx, void* stream) {

@@ -521,6 +521,46 @@ cudaError_t launch_child_softmax(float* L, const int* first, const int* count, i
   return cudaGetLastError();
 }
 
+// Level-0 backward, softmax over the node's channels (layers.py:114-120 differentiated,
+// tensor.py:201-203): dp_c[r][h] = sum of the row-dot GEMM's 32-column partials of head h
+// (dpp [g][D/32][R]) + Gpos[r][h]; dl_c = p_c (dp_c - sum_c' p_c' dp_c'). One thread per
+// (head, row), rows fastest (coalesced dpp / dl); dl written [g][H][R] fp32 and bf16.
+__global__ void __launch_bounds__(256) l0_softmax_bwd_kernel(
+    int g, int R, int H, int NH, int dh, const float* __restrict__ dpp,
+    const float* __restrict__ Gpos, const __nv_bfloat16* __restrict__ p,
+    float* __restrict__ dl, __nv_bfloat16* __restrict__ dlb) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)R * H) return;
+  const int h = (int)(idx / R), r = (int)(idx - (long long)h * R);
+  const int hg = h / NH, hn = h - hg * NH, np_ = dh / 32, D32 = H * np_;
+  const float gp = __ldg(Gpos + (size_t)r * H + h);
+  float sdp = 0.f;
+  for (int c = 0; c < g; ++c) {
+    float dp = gp;
+    for (int k = 0; k < np_; ++k) dp += __ldg(dpp + ((size_t)c * D32 + h * np_ + k) * R + r);
+    const float pc = __bfloat162float(p[((size_t)(hg * g + c) * R + r) * NH + hn]);
+    sdp = fmaf(pc, dp, sdp);
+    dl[((size_t)c * H + h) * R + r] = dp;  // dp for now; scaled below
+  }
+  for (int c = 0; c < g; ++c) {
+    const size_t o = ((size_t)c * H + h) * R + r;
+    const float pc = __bfloat162float(p[((size_t)(hg * g + c) * R + r) * NH + hn]);
+    const float v = pc * (dl[o] - sdp);
+    dl[o] = v;
+    dlb[o] = __float2bfloat16(v);
+  }
+}
+
+cudaError_t launch_l0_softmax_bwd(int g, int R, int H, int NH, int dh, const float* dpp,
+                                  const float* Gpos, const __nv_bfloat16* p, float* dl,
+                                  __nv_bfloat16* dlb, cudaStream_t st) {
+  if (dh % 32 || NH < 1 || H % NH) return cudaErrorInvalidValue;
+  const long long n = (long long)R * H;
+  l0_softmax_bwd_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, R, H, NH, dh, dpp,
+                                                                     Gpos, p, dl, dlb);
+  return cudaGetLastError();
+}
+
 // full_cross node weights (see FullCrossArgs). One CTA per (node, row), one warp per head;
 // lane j owns child j (g <= 32): it keeps k_j,h in registers and computes the row of logits
 // L_ij = q_i . k_j / sqrt(dh) against q_i broadcast from shared memory; the per-i softmax,

@@ -135,6 +135,9 @@ struct L0TgradArgs {
   float* T;                      // [g][PP][D] fp32
 };
 cudaError_t launch_l0_tgrad(const L0TgradArgs& a, cudaStream_t st);
+cudaError_t launch_l0_softmax_bwd(int g, int R, int H, int NH, int dh, const float* dpp,
+                                  const float* Gpos, const __nv_bfloat16* p, float* dl,
+                                  __nv_bfloat16* dlb, cudaStream_t st);
 cudaError_t launch_child_softmax(float* L, const int* first, const int* count, int n_parents,
                                  int R, int H, cudaStream_t st);
 cudaError_t launch_l0_tgrad_tc(const CUtensorMap& tG, const CUtensorMap& tP,

@@ -639,15 +639,18 @@ class DchagTrainer:
             _lib.call("dchag_gemm_rowdot", _lib.ptr(A), g, B, s, pp, s * pp, cnt * s * pp, pp,
                       _lib.ptr(Mt), d, d * pp, _lib.ptr(Cb), d, _lib.ptr(Gb), d, _lib.ptr(dpp),
                       _lib.stream_handle())
-            dp = dpp.view(g, h, dh // 32, R).sum(2) + Gpos.t().unsqueeze(0)   # [g, H, R]
             if attn:
                 pj = pblk.view(h // pk.NH, g, R, pk.NH).permute(1, 0, 3, 2).reshape(g, h, R)
-                pf = pj.float()
-                # softmax backward over the node's channels: dl = p (dp - sum_c p dp)
-                dl = (pf * (dp - (pf * dp).sum(0, keepdim=True))).permute(0, 2, 1).contiguous()
+                # softmax backward over the node's channels, one kernel:
+                # dp = sum of the 32-column partials + Gpos, dl = p (dp - sum_c p dp)
+                dlT = torch.empty(g, h, R, device=img.device, dtype=torch.float32)
+                dlTb = torch.empty(g, h, R, device=img.device, dtype=torch.bfloat16)
+                _lib.call("dchag_l0_softmax_bwd", g, R, h, pk.NH, dh, _lib.ptr(dpp),
+                          _lib.ptr(Gpos), _lib.ptr(pblk), _lib.ptr(dlT), _lib.ptr(dlTb),
+                          _lib.stream_handle())
             else:
+                dp = dpp.view(g, h, dh // 32, R).sum(2) + Gpos.t().unsqueeze(0)   # [g, H, R]
                 grads[f"{node}.mix"] = dp.sum((1, 2))
-                dl = None
             pt = patches[:, c0:c0 + g].permute(1, 3, 0, 2).reshape(g, pp, R)   # patch_c^T
             if attn:  # colsum_r dV_j = sum_r p_jrh G_r (per head): a small GEMM, not a dV pass
                 colV = torch.bmm(pj.permute(1, 0, 2), Gb.view(R, h, dh).permute(1, 0, 2),
@@ -660,8 +663,8 @@ class DchagTrainer:
             d_tb[c0:c0 + g] = _mm(colV, Wv.t())
             if attn:
                 U = query_logit_weights(w, node, h)
-                E = torch.bmm(pt, dl.to(torch.bfloat16), out_dtype=torch.float32)  # [g, PP, H]
-                coll = dl.sum(1)                                        # [g, H]
+                E = torch.bmm(pt, dlTb.transpose(1, 2), out_dtype=torch.float32)  # [g, PP, H]
+                coll = dlT.sum(2)                                       # [g, H]
                 dU = _mm(Wc.reshape(g * pp, d).t(), E.reshape(g * pp, h)) + _mm(tb[c0:c0 + g].t(), coll)
                 grads.update(_u_backward(w, node, dU, h))
                 d_tokw[c0:c0 + g] += _mm(E.reshape(g * pp, h), U.t()).view(g, pp, d)
