@@ -403,3 +403,46 @@ def test_vit_input_matches_oracle(out_dtype):
     y = fe(_bf(images).cuda()).float().cpu().numpy()[:, 0]
     keep = mask == 0
     assert np.array_equal(got[:, 1:][keep], y[keep])
+
+
+@pytest.mark.parametrize("D,H,groups,split", [(512, 16, [3, 1, 4], 1), (512, 16, [2, 5], 2),
+                                              (1024, 16, [16, 16], 1)])
+def test_gemm_combine_matches_torch(D, H, groups, split):
+    """dchag_gemm_combine (+ dchag_child_softmax): each child's projection and the parent's
+    softmax-weighted child sum in one kernel, against the unfused float64 computation;
+    uneven parents, a one-child parent, and the two-way child split."""
+    if split == 2 and min(groups) < 2:
+        pytest.skip("split needs >= 2 children per parent")
+    from paper_2506_21411_b200 import _lib
+    torch.manual_seed(1)
+    R, n = 256, sum(groups)
+    N = D + H
+    ctx = (torch.randn(n, R, D, device="cuda") * 0.5).to(torch.bfloat16)
+    W = (torch.randn(n, N, D, device="cuda") * D ** -0.5).to(torch.bfloat16)
+    b = torch.randn(n, N, device="cuda") * 0.1
+    first = torch.tensor([sum(groups[:j]) for j in range(len(groups))], device="cuda",
+                         dtype=torch.int32)
+    count = torch.tensor(groups, device="cuda", dtype=torch.int32)
+    st = _lib.stream_handle()
+    L = torch.empty(n, R, H, device="cuda")
+    _lib.call("dchag_gemm_bf16", _lib.ptr(ctx), n, 1, R, D, R * D, 0, D, _lib.ptr(W[:, D:]), H,
+              N * D, 0, _lib.ptr(b[:, D:]), N, 0, 0, 0, 1, 0, 0, 0, 0, 0, _lib.ptr(L), R * H, 0,
+              H, st)
+    _lib.call("dchag_child_softmax", _lib.ptr(L), _lib.ptr(first), _lib.ptr(count), len(groups),
+              R, H, st)
+    out = torch.empty(split, len(groups), R, D, device="cuda", dtype=torch.bfloat16)
+    _lib.call("dchag_gemm_combine", _lib.ptr(ctx), n, R, D, H, _lib.ptr(W), N * D, _lib.ptr(b), N,
+              _lib.ptr(L), _lib.ptr(first), _lib.ptr(count), len(groups), split, _lib.ptr(out), st)
+    torch.cuda.synchronize()
+    got = out.double().sum(0)
+    full = torch.einsum("crd,cnd->crn", ctx.double(), W.double()) + b.double()[:, None]
+    V, Lg = full[..., :D], full[..., D:]
+    want = []
+    for j, g in enumerate(groups):
+        f = sum(groups[:j])
+        p = torch.softmax(Lg[f:f + g], dim=0)                     # [g, R, H]
+        pv = p.repeat_interleave(D // H, dim=2) * V[f:f + g]
+        want.append(pv.sum(0))
+    want = torch.stack(want)
+    err = ((got - want).norm() / want.norm()).item()
+    assert err < BF16_TOL, err
