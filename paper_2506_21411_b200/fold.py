@@ -200,6 +200,10 @@ class PackedRank:
     Wf: torch.Tensor
     bf: torch.Tensor
     levels: tuple
+    # tp == 1: the root's value projection folded with the final layer (softmax over one
+    # stream is exactly 1): out = ctx_root @ (Wp_root[:, :D] @ Wf) + (bp_root[:D] @ Wf + bf)
+    Wdir: torch.Tensor = None   # [D_out][D] bf16 (n-major)
+    bdir: torch.Tensor = None   # [D] fp32
 
 
 def unit_heads(embed: int, heads: int) -> int:
@@ -262,6 +266,9 @@ def pack_rank(fr: FoldedRank, device) -> PackedRank:
     comb_first = [torch.tensor(f, **i32) for f in fr.comb_first]
     comb_g = [torch.tensor(g, **i32) for g in fr.comb_g]
     comb_mix = [None if m is None else m.to(**f32).contiguous() for m in fr.comb_mix]
+    Wr = fr.Wp[-1][0].to(**f32)[:, :d]                       # root value projection (x @ W)
+    Wdir = (Wr @ fr.Wf.to(**f32)).t().to(torch.bfloat16).contiguous()
+    bdir = (fr.bp[-1][0].to(**f32)[:d] @ fr.Wf.to(**f32) + fr.bf.to(**f32)).contiguous()
     return PackedRank(
         n0=n0, C=C, C_pad=C_pad, KE=KE, HP=HP, NH=unit_heads(d, h), attn_l0=fr.attn_l0,
         l0_c0=torch.tensor(fr.l0_c0, **i32), l0_g=torch.tensor(fr.l0_g, **i32),
@@ -269,4 +276,4 @@ def pack_rank(fr: FoldedRank, device) -> PackedRank:
         p_const=p_const, Wp=Wp, bp=bp, N=N, comb_first=comb_first, comb_g=comb_g,
         comb_mix=comb_mix,
         Wf=fr.Wf.to(**f32).t().to(torch.bfloat16).contiguous(),
-        bf=fr.bf.to(**f32).contiguous(), levels=fr.levels)
+        bf=fr.bf.to(**f32).contiguous(), levels=fr.levels, Wdir=Wdir, bdir=bdir)

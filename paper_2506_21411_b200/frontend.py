@@ -324,6 +324,17 @@ class DchagFrontEnd(torch.nn.Module):
                 out.copy_(res, non_blocking=True)
                 res = out
             return res
+        if self.tp == 1 and not return_payload:
+            # one stream: the final layer's softmax is exactly 1, so the root projection and
+            # the final projection fold into one GEMM writing the output
+            B = images.shape[0]
+            res = dev_out if dev_out is not None else torch.empty(
+                B, 1, self.seq, m.embed, device=images.device, dtype=self.out_dtype)
+            self.local_payload(images, pk, direct_out=res)
+            if out is not None and not out.is_cuda:
+                out.copy_(res, non_blocking=True)
+                res = out
+            return res
         payload = self.local_payload(images, pk)
         if return_payload or not self._position_split(images.shape[0]):
             gathered = self.gather(payload)
@@ -399,10 +410,13 @@ class DchagFrontEnd(torch.nn.Module):
         for k in range(n):
             b0, b1 = bounds[k], bounds[k + 1]
             cur.wait_event(copied[k])
-            payload = self.local_payload(dbuf[b0:b1], pk)
-            if self._position_split(b1 - b0):
-                self.exchange_finish(payload, b1 - b0, out=res[b0:b1])
+            if self.tp == 1:
+                self.local_payload(dbuf[b0:b1], pk, direct_out=res[b0:b1])
+            elif self._position_split(b1 - b0):
+                self.exchange_finish(self.local_payload(dbuf[b0:b1], pk), b1 - b0,
+                                     out=res[b0:b1])
             else:
+                payload = self.local_payload(dbuf[b0:b1], pk)
                 self.finish(self.gather(payload), b1 - b0, out=res[b0:b1])
             if out is not None and not out.is_cuda:
                 done = torch.cuda.Event()
@@ -443,6 +457,12 @@ class DchagFrontEnd(torch.nn.Module):
                 plan.append(("dchag_gemm_combine", f"gemm_combine_l{li}", 2 * R * n_l * d * d,
                              n_l * R * d * 2 + n_l * d * d * 2 + n_next * R * d * 2))
                 continue
+            if li == depth - 1 and self.tp == 1:
+                # root projection folded with the final layer (one stream)
+                ob = 4 if self.out_dtype == torch.float32 else 2
+                plan.append(("dchag_gemm_bf16", "gemm_root_final", 2 * R * d * d,
+                             R * d * 2 + d * d * 2 + R * d * ob))
+                return plan
             plan.append(("dchag_gemm_bf16", f"gemm_l{li}", 2 * R * n_l * d * N,
                          n_l * R * d * 2 + n_l * R * (d * 2 + (N - d) * 4) + n_l * N * d * 2))
             if li + 1 < depth:
@@ -579,7 +599,7 @@ class DchagFrontEnd(torch.nn.Module):
             wk.wait()
         return res
 
-    def local_payload(self, img, pk=None):
+    def local_payload(self, img, pk=None, direct_out=None):
         """Rank-local part: slab tree -> root payload [V bf16 R*D | L fp32 R*H] (bytes),
         V/L = the root stream projected into the final layer's value/logit space."""
         pk = pk or self.prepare()
@@ -652,6 +672,13 @@ class DchagFrontEnd(torch.nn.Module):
                           _lib.ptr(nxt), st)
                 ctx = nxt[0] if split == 1 else torch.add(nxt[0], nxt[1])
                 continue
+            if li == depth - 1 and direct_out is not None:
+                # tp == 1: the root projection folded with the final layer writes the output
+                _lib.call("dchag_gemm_bf16", _lib.ptr(ctx), 1, 1, R, d, R * d, 0, d,
+                          _lib.ptr(pk.Wdir), d, d * d, d, _lib.ptr(pk.bdir), d, 0, 0, 0, 1,
+                          _lib.ptr(direct_out), int(direct_out.dtype == torch.float32), R * d,
+                          0, d, 0, 0, 0, 0, st)
+                return None
             if li == depth - 1:
                 # root: write straight into the gather payload (payload.py layout)
                 payload = torch.empty(payload_nbytes(R, d, h), device=dev, dtype=torch.uint8)

@@ -446,3 +446,26 @@ def test_gemm_combine_matches_torch(D, H, groups, split):
     want = torch.stack(want)
     err = ((got - want).norm() / want.norm()).item()
     assert err < BF16_TOL, err
+
+
+@pytest.mark.parametrize("lk", ["cross_attention", "linear"])
+@pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
+def test_forward_tp1_direct_matches_oracle(lk, out_dtype):
+    """tp = 1 forward through the public call: the root projection folded with the final
+    layer (one GEMM), the fused levels above level 0, against the CPU oracle."""
+    from paper_2506_21411_b200 import DchagFrontEnd
+    C, Hh, Ww, P, D, H, mg = 37, 64, 128, 8, 1024, 16, 4
+    specs = O.frontend_param_specs(C, Hh, Ww, P, D, 1, mg, layer_kind=lk)
+    w = O.random_params(specs, seed=11, std=0.05, bias_std=0.02)
+    w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
+    rng = np.random.default_rng(12)
+    images = _bf(rng.standard_normal((4, C, Hh, Ww))).float().numpy().astype(np.float64)
+    fe = DchagFrontEnd(C, Hh, Ww, P, D, H, max_group=mg, agg_layer_kind=lk, out_dtype=out_dtype)
+    fe.load_weights(w)
+    got = fe(_bf(images).cuda()).float().cpu().numpy()
+    want = O.dchag_frontend(images, w, patch=P, heads=H, tp=1, max_group=mg, layer_kind=lk)
+    assert rel_err(got, want) < BF16_TOL
+    # the same through the payload + final-layer schedule (what tp > 1 ranks run)
+    pay = fe.local_payload(_bf(images).cuda())
+    alt = fe.finish(pay, 4).float().cpu().numpy()
+    assert rel_err(got, alt) < 1e-2
