@@ -356,7 +356,6 @@ __global__ void __launch_bounds__(TG_THREADS, 4) l0_tgrad_kernel(L0TgradArgs a) 
   const int nchunks = (int)((long long)(blockIdx.z + 1) * nall / RS) - cbeg;
   auto load = [&](int i, int buf) {
     const uint32_t sg = sbase + buf * TG_BUF, sp = sg + TG_G_BYTES;
-    uint8_t* ss = tg_smem + buf * TG_BUF;
     const int r0 = (cbeg + i) * TG_ROWS;
 #pragma unroll
     for (int t = 0; t < 1024 / TG_THREADS; ++t) {  // G: 64 rows x 16 chunks
@@ -378,7 +377,6 @@ __global__ void __launch_bounds__(TG_THREADS, 4) l0_tgrad_kernel(L0TgradArgs a) 
                 a.p + ((size_t)(hg * a.g + c) * a.R + r0 + row) * a.NH + hn);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    (void)ss;
   };
   const int mbase = 32 * (warp & 1);   // k rows of this warp
   const int nbase = TG_NW * (warp >> 1);  // d columns (within the CTA's 128)
