@@ -16,7 +16,7 @@ def unfold(images, p):
 
 
 def emulate_rank(fr, images, heads):
-    """images: [B, c_r, H, W] float64 -> (V_root [R, D], L_root [R, H])."""
+    """images: [B, c_r, H, W] float64 -> (V_root [R, D], L_root [R, H], ctx_root [R, D])."""
     d, h = fr.embed, heads
     dh = d // h
     B = images.shape[0]
@@ -50,18 +50,27 @@ def emulate_rank(fr, images, heads):
                     p = fr.comb_mix[li][first:first + g].view(g, 1, 1)
                 nxt.append((p * V[first:first + g]).sum(0))
             ctx = torch.stack(nxt)
-    return V[0], L[0]
+    return V[0], L[0], ctx[0]
 
 
-def emulate_frontend(w, images, *, slabs, trees, embed, heads, patch, variant, layer_kind):
-    """All ranks + AllGather (concat in rank order) + shared final layer."""
+def emulate_frontend(w, images, *, slabs, trees, embed, heads, patch, variant, layer_kind,
+                     fold_root_final=False):
+    """All ranks + AllGather (concat in rank order) + shared final layer.
+    fold_root_final (tp == 1 only): the plan DchagFrontEnd runs at one stream -- the final
+    softmax over one stream is 1, so out = ctx_root @ (Wp_root[:, :D] @ Wf) + (bp_root[:D]
+    @ Wf + bf), one GEMM with the weights pack_rank folds (Wdir, bdir)."""
     dh = embed // heads
     Vs, Ls, fr = [], [], None
     for r, ((off, cnt), tree) in enumerate(zip(slabs, trees)):
         fr = fold_rank(w, rank=r, slab=(off, cnt), levels=tree, embed=embed, heads=heads,
                        patch=patch, seq=(images.shape[2] // patch) * (images.shape[3] // patch),
                        variant=variant, layer_kind=layer_kind)
-        V, L = emulate_rank(fr, images[:, off:off + cnt], heads)
+        V, L, ctx_root = emulate_rank(fr, images[:, off:off + cnt], heads)
+        if fold_root_final:
+            assert len(slabs) == 1, "the root/final fold is the tp == 1 plan"
+            Wdir = fr.Wp[-1][0][:, :embed] @ fr.Wf
+            bdir = fr.bp[-1][0][:embed] @ fr.Wf + fr.bf
+            return (ctx_root @ Wdir + bdir).view(images.shape[0], 1, -1, embed)
         Vs.append(V)
         Ls.append(L)
     V, L = torch.stack(Vs), torch.stack(Ls)

@@ -51,7 +51,7 @@ def _worker(rank, world, port, meta, q):
         fr = fold_rank(tw, rank=rank, slab=(off, cnt),
                        levels=build_tree_spec(cnt, meta["g"]).levels, embed=meta["D"],
                        heads=meta["H"], patch=4, seq=16, variant="single_query", layer_kind=lk)
-        V, L = emulate_rank(fr, torch.from_numpy(images[:, off:off + cnt]), meta["H"])
+        V, L, _ = emulate_rank(fr, torch.from_numpy(images[:, off:off + cnt]), meta["H"])
         payload = pack(V, L)
         R = V.shape[0]
         assert payload.numel() == payload_nbytes(R, meta["D"], meta["H"])

@@ -11,13 +11,14 @@ from folded_emulator import emulate_frontend
 from paper_2506_21411_b200.config import build_tree_spec, channel_slabs
 
 
-def _run(meta, w, images):
+def _run(meta, w, images, fold_root_final=False):
     tw = {k: torch.from_numpy(v) for k, v in w.items()}
     slabs = channel_slabs(meta["channels"], meta["tp"])
     trees = [build_tree_spec(n, meta["max_group"]).levels for _, n in slabs]
     return emulate_frontend(tw, torch.from_numpy(images), slabs=slabs, trees=trees,
                             embed=meta["embed"], heads=meta["heads"], patch=meta["patch"],
-                            variant=meta["variant"], layer_kind=meta["layer_kind"]).numpy()
+                            variant=meta["variant"], layer_kind=meta["layer_kind"],
+                            fold_root_final=fold_root_final).numpy()
 
 
 @pytest.mark.parametrize("case", ["ref_tiny_sq_tp2", "ref_tiny_lin_tp2", "ref_tiny_sq_tp1_g3",
@@ -40,3 +41,11 @@ def test_folded_plan_uneven_slabs(tp, layer_kind):
     want = O.dchag_frontend(images, w, patch=4, heads=4, tp=tp, max_group=3,
                             layer_kind=layer_kind)
     assert rel_err(_run(meta, w, images), want) < 1e-10
+
+
+@pytest.mark.parametrize("case", ["ref_tiny_sq_tp1_g3", "T_sq_tp1"])
+def test_tp1_root_final_fold_matches_reference_golden(case):
+    # the tp == 1 plan: root value projection and final layer as one GEMM (pack_rank Wdir)
+    meta, z, w, _ = load_golden(case)
+    out = _run(meta, w, z["images"].astype(np.float64), fold_root_final=True)
+    assert rel_err(out, z["out"]) < (1e-10 if z["out"].dtype == np.float64 else 1e-6)
