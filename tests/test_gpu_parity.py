@@ -113,6 +113,9 @@ CONFIGS = [
          layer_kind="linear"),
     # D = 4096, 32 heads (sweep): combine rows split in 2048-column segments
     dict(channels=10, image_h=64, image_w=128, patch=8, embed=4096, heads=32, tp=1, max_group=4),
+    # the H8 shape in miniature: 8 uneven slabs (16 x5, 15 x3), groups of 4 and 3, depth 2
+    dict(channels=125, image_h=128, image_w=128, patch=8, embed=256, heads=4, tp=8,
+         max_group=4),
 ]
 
 
