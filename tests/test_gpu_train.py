@@ -79,7 +79,9 @@ def test_train_step_matches_reference_tape(case):
     dict(channels=12, image_h=64, image_w=128, patch=8, embed=256, heads=4, tp=3, max_group=2),
     dict(channels=9, image_h=32, image_w=64, patch=4, embed=128, heads=2, tp=1, max_group=3,
          layer_kind="linear"),
-], ids=["P8_tp3_uneven", "P4_linear"])
+    # the TR slab shape in miniature: 8 ranks, uneven slabs (4 x6, 3 x2)
+    dict(channels=30, image_h=64, image_w=128, patch=8, embed=256, heads=4, tp=8, max_group=2),
+], ids=["P8_tp3_uneven", "P4_linear", "P8_tp8_uneven"])
 def test_train_step_matches_autograd(meta):
     lk = meta.get("layer_kind", "cross_attention")
     specs = O.frontend_param_specs(meta["channels"], meta["image_h"], meta["image_w"],
