@@ -429,7 +429,7 @@ def b200_arm(args, wl, tp, max_group):
 
     def e2e_step():
         if wl.get("train"):
-            if args.no_graph:
+            if gstep is None:
                 dev_img.copy_(host_img, non_blocking=True)
                 out, saved = trainer.forward_train(dev_img)
                 trainer.backward(saved, probe)
