@@ -67,6 +67,10 @@ def parse():
                          "CUDA graph")
     ap.add_argument("--h2d-chunks", type=int, default=8,
                     help="batch chunks of the e2e host-input pipeline (copy/compute overlap)")
+    ap.add_argument("--arch-tp", type=int, default=None,
+                    help="one GPU, one process: run the tp=N architecture's N channel slabs "
+                         "back to back + one final layer (BASELINE's same-architecture "
+                         "single-GPU denominator of scaling efficiency)")
     ap.add_argument("--cpu-tokens", type=int, default=None,
                     help="tokens per CPU sample (default: 1/8 of an image)")
     return ap.parse_args()
@@ -118,6 +122,18 @@ def cpu_sample(wl, tp, max_group, tokens, seed=0):
     return tokens / S / dt, tokens, dt
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -154,6 +170,7 @@ def reference_arm(args, wl, tp, max_group):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, wl, tp, max_group),
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"1 image x {tok}/{S} tokens per step (float64 numpy "
                                    f"restatement of the reference, {blas})"
                                    + ("; forward only: the oracle has no backward, so the "
@@ -175,8 +192,6 @@ def workload_config(args, wl, tp, max_group):
             **({"layer_kind": wl["layer_kind"]} if wl.get("layer_kind") else {}),
             **({"agg_variant": wl["variant"]} if wl.get("variant") else {}),
             "parallelism": f"dchag-tp{tp}",
-            **({"launch": "eager" if (args.no_graph or tp >= 4) else "cuda graph (whole step)"}
-               if wl.get("train") else {}),
             "l2": "flushed between timed steps (256 MiB write)"}
 
 
@@ -256,6 +271,81 @@ class ClockSampler:
                 "samples": len(src), "window": "timed region" if win else "whole run"}
 
 
+class KernelTimer:
+    """Per-launch CUDA events on the launching stream around every libdchag launch
+    (_lib.set_launch_hook). A launch's site is its `work` annotation's site (train.py,
+    ops.py), else the matching entry of the inference launch plan, else the entry point."""
+
+    def __init__(self, plan=None):
+        import torch
+        self.torch = torch
+        self.plan = plan or []
+        self.events = []     # [site, name, start, stop, work]
+        self.i = 0
+
+    def hook(self, name, phase, work):
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record()
+        if phase == "pre":
+            if work and work.get("site"):
+                site = work["site"]
+            elif self.i < len(self.plan):
+                site, work = self.plan[self.i][1], {"flops": self.plan[self.i][2],
+                                                    "bytes": self.plan[self.i][3]}
+            else:
+                site = name
+            self.events.append([site, name, ev, None, work or {}])
+        else:
+            self.events[-1][3] = ev
+            self.i += 1
+
+    def new_step(self, _=None):
+        self.i = 0
+
+    def summary(self, steps):
+        """{site: {"kernel", "ms" per step, "launches" per step, "flops", "bytes"}}."""
+        out = {}
+        for site, name, a, b, work in self.events:
+            e = out.setdefault(site, {"kernel": name, "ms": 0.0, "launches": 0, "flops": 0,
+                                      "bytes": 0})
+            e["ms"] += a.elapsed_time(b) / steps
+            e["launches"] += 1 / steps
+            e["flops"] += work.get("flops", 0) / steps
+            e["bytes"] += work.get("bytes", 0) / steps
+        return out
+
+
+TENSOR_KERNELS = ("dchag_l0_node", "dchag_gemm_bf16", "dchag_l0_logits", "dchag_gemm_combine",
+                  "dchag_gemm_wgrad", "dchag_gemm_rowdot", "dchag_l0_tgrad")
+
+
+def roofline(dom, peaks, traffic):
+    """Roofline object of the dominant kernel: achieved = its algorithmic flops (or bytes) per
+    step / its measured time per step. peak = the measured burst figure (the conservative
+    denominator); frac_vs_sustained uses the back-to-back cuBLAS figure."""
+    peak_burst, peak_sus, hbm, src = peaks
+    t = dom["ms"] / 1e3
+    if not t or not (dom["flops"] or dom["bytes"]):
+        return None
+    if dom["kernel"] in TENSOR_KERNELS and dom["flops"]:
+        ach = dom["flops"] / t / 1e12
+        r = {"bound": "tensor", "achieved": ach, "peak": peak_burst, "unit": "TFLOP/s",
+             "frac": ach / peak_burst, "frac_vs_sustained": ach / peak_sus,
+             "peak_source": f"{src} bf16_tflops (burst); sustained {peak_sus}",
+             "flops_per_step": dom["flops"]}
+    else:
+        ach = dom["bytes"] / t / 1e9
+        r = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+             "peak_source": f"{src} hbm_gbs", "bytes_per_step": dom["bytes"]}
+    r.update(traffic=traffic, kernel=f"{dom['kernel']}[{dom['site']}]",
+             launch_ms=dom["ms"] / max(1.0, dom["launches"]),
+             launches_per_step=dom["launches"], ms_per_step=dom["ms"])
+    if r["frac"] > 1.0:  # never report > 1: a timing anomaly is flagged, not credited
+        r["anomaly"] = f"measured frac {r['frac']:.3f} > 1 (kernel timing anomaly)"
+        r["frac"] = 1.0
+    return r
+
+
 def b200_arm(args, wl, tp, max_group):
     import torch
     import torch.distributed as dist
@@ -268,19 +358,31 @@ def b200_arm(args, wl, tp, max_group):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B = args.batch or wl["batch"]
-    # the training config's final layer is head-split over the tp group (reduce-scatter of the
-    # boundary gradient in backward, BASELINE.json configs[3])
-    fe = DchagFrontEnd(wl["channels"], wl["image_h"], wl["image_w"], wl["patch"], wl["embed"],
-                       wl["heads"], max_group=max_group, tp=tp, rank=rank,
-                       final_layer_tp_split=bool(wl.get("final_split")) and tp > 1,
-                       agg_variant=wl.get("variant", "single_query"),
-                       agg_layer_kind=wl.get("layer_kind", "cross_attention"))
-    fe.init_weights(seed=0, all_ranks=False)
-    fe.prepare()
-    off, cnt = fe.slab
+    arch_tp = args.arch_tp if (args.arch_tp and world == 1) else None
+
+    def make_fe(tp_, rank_):
+        # the training config's final layer is head-split over the tp group (reduce-scatter
+        # of the boundary gradient in backward, BASELINE.json configs[3])
+        fe_ = DchagFrontEnd(wl["channels"], wl["image_h"], wl["image_w"], wl["patch"],
+                            wl["embed"], wl["heads"], max_group=max_group, tp=tp_, rank=rank_,
+                            final_layer_tp_split=bool(wl.get("final_split")) and tp_ > 1,
+                            agg_variant=wl.get("variant", "single_query"),
+                            agg_layer_kind=wl.get("layer_kind", "cross_attention"))
+        fe_.init_weights(seed=0, all_ranks=False)
+        fe_.prepare()
+        return fe_
+
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    images = torch.randn(B, cnt, wl["image_h"], wl["image_w"], device="cuda",
-                         generator=gen).to(torch.bfloat16)
+    if arch_tp:
+        # the tp = N architecture in one process: N slabs back to back, one final layer
+        fes = [make_fe(arch_tp, r) for r in range(arch_tp)]
+        fe = fes[0]
+        images = torch.randn(B, wl["channels"], wl["image_h"], wl["image_w"], device="cuda",
+                             generator=gen).to(torch.bfloat16)
+    else:
+        fe = make_fe(tp, rank)
+        images = torch.randn(B, fe.slab[1], wl["image_h"], wl["image_w"], device="cuda",
+                             generator=gen).to(torch.bfloat16)
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -311,23 +413,32 @@ def b200_arm(args, wl, tp, max_group):
         return float(t.item())
 
     gstep = None
+    trainer = None
     if wl.get("train"):
         from paper_2506_21411_b200.train import DchagTrainer
         trainer = DchagTrainer(fe)
         probe = torch.randn(B, 1, fe.seq, wl["embed"], device="cuda", generator=gen)
 
-        # the graphed step hangs at world >= 4 (DESIGN.md §7 known issue); run eager there
-        if args.no_graph or world >= 4:
-            def step():
-                out, saved = trainer.forward_train(images)
-                return trainer.backward(saved, probe)
+        def eager_step():
+            out, saved = trainer.forward_train(images)
+            return trainer.backward(saved, probe)
+        if args.no_graph:
+            step = eager_step
         else:
             # the whole step (forward_train + backward, collectives included) as one CUDA
             # graph over the static image / probe buffers: a replay re-runs every kernel
             gstep = trainer.capture(images, probe)
             step = gstep.replay
+    elif arch_tp:
+        slabs_img = [images[:, f.slab[0]:f.slab[0] + f.slab[1]] for f in fes]
+
+        def step():
+            pays = [f.local_payload(x) for f, x in zip(fes, slabs_img)]
+            return fe.finish(torch.cat(pays), B)
+        eager_step = step
     else:
         step = lambda: fe(images)  # noqa: E731
+        eager_step = step
     clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         step()
@@ -344,82 +455,35 @@ def b200_arm(args, wl, tp, max_group):
     ms = max_over_ranks(ms)
     value = B * args.steps / (ms / 1e3)
 
-    # ---- pass B: per-kernel CUDA events on the launching stream (inference plan)
-    if wl.get("train"):
-        step_inf = lambda: fe(images)  # noqa: E731
-    else:
-        step_inf = step
-    unfolded = fe._unfolded()  # full_cross / fp32: the unfolded ops path has no launch plan
-    plan = [] if unfolded else fe.launch_plan(B)
-    site_ms = {s: 0.0 for _, s, _, _ in plan}
-    events = []
-    idx = {"i": 0}
-
-    def hook(name, phase):
-        if phase == "pre":
-            e = torch.cuda.Event(enable_timing=True)
-            e.record()
-            events.append([plan[idx["i"]][1], e, None])
-        else:
-            e = torch.cuda.Event(enable_timing=True)
-            e.record()
-            events[-1][2] = e
-            idx["i"] += 1
-
-    def reset(_):
-        idx["i"] = 0
-
-    # per-kernel events follow the launch plan of one unchunked forward
+    # ---- pass B: per-kernel CUDA events on the launching stream, same step run eagerly
+    # (the training step's launches carry work annotations; the forward follows its plan)
+    unfolded = fe._unfolded()  # full_cross / fp32: annotated ops-path launches, no plan
+    plan = [] if (unfolded or wl.get("train") or arch_tp) else fe.launch_plan(B)
+    kt = KernelTimer(plan)
     chunks, fe.comm_chunks = fe.comm_chunks, 1
-    if plan:
-        _lib.set_launch_hook(hook)
-        try:
-            timed(step_inf, args.steps, per_step_hook=reset)
-        finally:
-            _lib.set_launch_hook(None)
-            fe.comm_chunks = chunks
-    for site, a, b in events:
-        site_ms[site] += a.elapsed_time(b) / args.steps
-    kernels = []
-    peak_burst, peak_sus, hbm, peak_src = load_peaks()
-    for name, site, flops, nbytes in plan:
-        t = site_ms[site] / 1e3
-        kernels.append({"site": site, "kernel": name, "ms": site_ms[site],
-                        "tflops": flops / t / 1e12 if t else None,
-                        "gbs": nbytes / t / 1e9 if t else None})
-    if not plan:
-        kernels = [{"kernel": "unfolded ops path (per-node K_gemm / K_comb / K_fc launches)",
-                    "ms": None}]
-    dom = max(kernels, key=lambda k: k["ms"] or 0)
-    dom_plan = next((p for p in plan if p[1] == dom.get("site")), None)
-    tensor_bound = dom["kernel"] in ("dchag_l0_node", "dchag_gemm_bf16", "dchag_l0_logits",
-                                     "dchag_gemm_combine")
+    _lib.set_launch_hook(kt.hook)
+    try:
+        step_ms = timed(eager_step, args.steps, per_step_hook=kt.new_step) / args.steps
+    finally:
+        _lib.set_launch_hook(None)
+        fe.comm_chunks = chunks
+    sites = kt.summary(args.steps)
+    kernels = [dict(site=k, **v, tflops=(v["flops"] / v["ms"] / 1e9 if v["ms"] and v["flops"]
+                                         else None),
+                    gbs=(v["bytes"] / v["ms"] / 1e6 if v["ms"] and v["bytes"] else None))
+               for k, v in sorted(sites.items(), key=lambda kv: -kv[1]["ms"])]
+    peaks = load_peaks()
     traffic = None
+    dom = kernels[0] if kernels else None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             traffic = json.load(f).get(f"{args.workload}:tp{tp}:{dom['site']}")
     except Exception:
         pass
-    if dom_plan is None:
-        roof = None
-    elif tensor_bound:
-        # the sustained figure is cuBLAS back to back under the power cap; a kernel that
-        # beats it in this run is measured against the burst figure instead (never frac > 1)
-        use_burst = dom["tflops"] > peak_sus
-        peak_t = peak_burst if use_burst else peak_sus
-        roof = {"bound": "tensor", "achieved": dom["tflops"], "peak": peak_t,
-                "unit": "TFLOP/s", "frac": dom["tflops"] / peak_t, "traffic": traffic,
-                "kernel": f"{dom['kernel']}[{dom['site']}]",
-                "flops_per_launch": dom_plan[2], "launch_ms": dom["ms"],
-                "peak_source": (f"{peak_src} bf16_tflops (burst: the kernel ran above the "
-                                f"sustained {peak_sus})" if use_burst else
-                                f"{peak_src} bf16_tflops_sustained (kernel timed inside the "
-                                f"step)")}
-    else:
-        roof = {"bound": "hbm", "achieved": dom["gbs"], "peak": hbm, "unit": "GB/s",
-                "frac": dom["gbs"] / hbm, "traffic": traffic,
-                "kernel": f"{dom['kernel']}[{dom['site']}]", "bytes_per_launch": dom_plan[3],
-                "launch_ms": dom["ms"], "peak_source": f"{peak_src} hbm_gbs"}
+    roof = roofline(dom, peaks, traffic) if dom else None
+    if roof is not None:
+        roof["share_of_step"] = dom["ms"] / step_ms if step_ms else None
+    ours_ms = sum(k["ms"] for k in kernels)
 
     # ---- pass C: end to end through the public API from pinned host memory
     host_img = images.cpu().pin_memory()
@@ -439,9 +503,14 @@ def b200_arm(args, wl, tp, max_group):
                 out = gstep.out
             if rank == 0:
                 out_host.copy_(out, non_blocking=True)
-        elif unfolded:  # device images only on the unfolded path: copy in, run, copy out
+        elif unfolded or arch_tp:  # device-image paths: copy in, run, copy out
             dev_img.copy_(host_img, non_blocking=True)
-            out = fe(dev_img)
+            if arch_tp:
+                pays = [f.local_payload(dev_img[:, f.slab[0]:f.slab[0] + f.slab[1]])
+                        for f in fes]
+                out = fe.finish(torch.cat(pays), B)
+            else:
+                out = fe(dev_img)
             if rank == 0:
                 out_host.copy_(out, non_blocking=True)
         else:
@@ -452,29 +521,29 @@ def b200_arm(args, wl, tp, max_group):
     for _ in range(2):
         e2e_step()
     e2e_ms = max_over_ranks(timed(e2e_step, args.steps))
-    h2d = images.numel() * 2
-    d2h = out_host.numel() * 2 if rank == 0 else 0
+    h2d = images.numel() * images.element_size()
+    d2h = out_host.numel() * out_host.element_size() if rank == 0 else 0
 
-    # ---- whole-job algorithmic work
-    exec_flops = sum(p[2] for p in plan)  # this rank's folded-plan flops per step
-    if not plan:
-        tot_exec = None
-    elif world > 1:
-        t = torch.tensor([float(exec_flops - [p for p in plan if p[1] == "gemm_final"][0][2])],
-                         device="cuda", dtype=torch.float64)
+    # ---- whole-job algorithmic work (executed flops of our kernels, summed over ranks;
+    # a replicated final layer counts once)
+    exec_flops = sum(k["flops"] for k in kernels)
+    if world > 1:
+        t = torch.tensor([float(exec_flops)], device="cuda", dtype=torch.float64)
         dist.all_reduce(t)
-        tot_exec = float(t.item()) + [p for p in plan if p[1] == "gemm_final"][0][2]
+        tot_exec = float(t.item())
     else:
         tot_exec = exec_flops
-    b_flops = bflops_per_image(wl, fe.slabs, max_group, train=bool(wl.get("train"))) * B
+    b_slabs = fes[0].slabs if arch_tp else fe.slabs
+    b_flops = bflops_per_image(wl, b_slabs, max_group, train=bool(wl.get("train"))) * B
 
     cpu = None  # the CPU oracle is timed on rank 0 at N = 1 only (torchrun pins 1 OMP thread)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         S = fe.seq
         tokens = args.cpu_tokens or 2 * S   # two whole images, ~10-25 s of CPU work
-        v, tok, dt = cpu_sample(wl, tp, max_group, tokens)
+        v, tok, dt = cpu_sample(wl, arch_tp or tp, max_group, tokens)
         threads, blas = blas_threads()
         cpu = {"value": v, "unit": "images/s", "cores": threads, "kind": "port",
+               "cpu_model": cpu_model(),
                "sample": f"{tok / S:g} image(s) x {S} tokens, {dt:.1f} s (float64 numpy restatement "
                          f"of the reference hot path, {blas})"
                          + ("; forward only: the oracle has no backward" if wl.get("train")
@@ -483,26 +552,36 @@ def b200_arm(args, wl, tp, max_group):
     clk.__exit__()
     if rank == 0:
         clocks = clk.summary()
+        cfg = workload_config(args, wl, arch_tp or tp, max_group)
+        if wl.get("train"):
+            cfg["launch"] = "eager" if gstep is None else "cuda graph (whole step)"
+        if arch_tp:
+            cfg["parallelism"] = f"dchag-tp{arch_tp} architecture on 1 GPU (slabs sequential)"
+            cfg["final_layer"] = "once, over the tp streams (AllGather schedule)"
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (N(0,1) bf16 images, truncated-normal(0.02) "
                                      "random-init weights)",
-            "config": workload_config(args, wl, tp, max_group),
+            "config": cfg,
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": B * args.steps / (e2e_ms / 1e3), "unit": "images/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": clocks,
-            "work": {"folded_plan_tflop_per_step": tot_exec / 1e12 if plan else None,
-                     "folded_plan_tflops": (tot_exec / (ms / args.steps / 1e3) / 1e12
-                                            if plan else None),
+            "work": {"executed_tflop_per_step": tot_exec / 1e12 if tot_exec else None,
+                     "executed_tflops": (tot_exec / (ms / args.steps / 1e3) / 1e12
+                                         if tot_exec else None),
+                     "executed_frac_of_burst": (tot_exec / (ms / args.steps / 1e3) / 1e12
+                                                / (world * peaks[0]) if tot_exec else None),
                      "reference_graph_B_tflop_per_step": b_flops / 1e12,
                      "B_flops_effective_tflops": b_flops / (ms / args.steps / 1e3) / 1e12,
                      "B_flops_roofline_frac": b_flops / (ms / args.steps / 1e3) / 1e12
-                     / (world * peak_sus)},
+                     / (world * peaks[0])},
+            "kernel_pass": {"eager_step_ms": step_ms, "our_kernels_ms": ours_ms,
+                            "other_ms": step_ms - ours_ms},
             "kernels": kernels,
         }
         print(json.dumps(line), flush=True)
@@ -539,7 +618,7 @@ def main():
     if args.impl == "reference":
         tp = args.gpus
     from paper_2506_21411_b200.config import build_tree_spec, channel_slabs, max_group_for_depth
-    slabs = [n for _, n in channel_slabs(wl["channels"], tp)]
+    slabs = [n for _, n in channel_slabs(wl["channels"], args.arch_tp or tp)]
     if wl.get("max_group"):
         max_group = wl["max_group"]
         wl = dict(wl, depth=max(build_tree_spec(n, max_group).depth for n in slabs))

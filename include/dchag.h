@@ -65,11 +65,18 @@ int dchag_gemm_rowdot(const void* A, int G, int Mo, int Mi, int K, long long sAg
  * (every parent with >= 2 children) split s holds the sum over children
  * [s c/2, (s+1) c/2) with the full softmax, and out[0] + out[1] is the result (more, smaller
  * work units when parents are few). R % 256 == 0, D % 256 == 0, (D/H) % 32 == 0. The
- * running sum is kept as fp16 pairs (fp32 math). */
+ * running sum is kept as fp16 pairs scaled by 2^-8 (fp32 math): partial child sums up to
+ * +-1.68e7 in magnitude; beyond that the kernel raises a device flag that
+ * dchag_combine_overflow reports. */
 int dchag_gemm_combine(const void* ctx, int n_children, int R, int D, int H, const void* W,
                        long long sWg, const float* bias, long long bias_g, const float* Lpre,
                        const int* first, const int* count, int n_parents, int csplit,
                        void* out, void* stream);
+
+/* Range guard of dchag_gemm_combine: *flag = 1 if any launch since the last reset saw a
+ * partial child sum beyond +-1.68e7 (its fp16 x 2^8 running-sum range), else 0; reset != 0
+ * clears it. Host-synchronous (reads a device symbol); not a kernel launch. */
+int dchag_combine_overflow(int* flag, int reset);
 
 /* Level-0 logits + softmax over each node's channels (K_p0): replaces the
  * q@wq / x@wk / logits / softmax part of layers.py:103-121 for tree level 0 with the

@@ -53,6 +53,7 @@ SIGNATURES = {
     "dchag_unfold": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp],
     "dchag_tile_weights": [c_vp, c_int, c_int, c_int, c_vp, c_vp],
     "dchag_num_sms": [],
+    "dchag_combine_overflow": [c_vp, c_int],
 }
 STRING_FNS = ("dchag_version", "dchag_last_error")
 
@@ -104,23 +105,27 @@ def check(rc: int, what: str) -> None:
 # bench bracket individual kernels with CUDA events on the launching stream)
 LAUNCH_COUNT = {"n": 0}
 _HOOK = {"fn": None}
-_NON_LAUNCH = ("dchag_num_sms",)
+_NON_LAUNCH = ("dchag_num_sms", "dchag_combine_overflow")
 
 
 def set_launch_hook(fn) -> None:
-    """fn(name, phase) with phase in {"pre", "post"} around every kernel launch."""
+    """fn(name, phase, work) with phase in {"pre", "post"} around every kernel launch; work
+    is the caller's annotation of the launch (site name, algorithmic flops and bytes) or
+    None."""
     _HOOK["fn"] = fn
 
 
-def call(name: str, *args) -> None:
+def call(name: str, *args, work: dict | None = None) -> None:
+    """Launch one C-ABI entry point; raise on a non-zero status. `work` (optional) annotates
+    the launch for measurement: {"site": str, "flops": int, "bytes": int}."""
     hook = _HOOK["fn"]
     if hook is not None:
-        hook(name, "pre")
+        hook(name, "pre", work)
     check(getattr(load(), name)(*args), name)
     if name not in _NON_LAUNCH:
         LAUNCH_COUNT["n"] += 1
     if hook is not None:
-        hook(name, "post")
+        hook(name, "post", work)
 
 
 def ptr(t) -> int:

@@ -1,24 +1,49 @@
-"""Build libdchag.so in-tree for sm_100a (no JIT cache: the .so travels with the repo)."""
+"""Build libdchag.so in-tree for sm_100a (no JIT cache: the .so travels with the repo).
+
+Each translation unit compiles to an object in parallel (build/), then one link step."""
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["capi.cu", "gemm.cu", "l0.cu", "comb.cu"]
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-diag-suppress", "177"]
+SOURCES = ["capi.cu", "gemm.cu", "l0.cu", "comb.cu", "wgrad.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                 "-diag-suppress", "177"]
+LFLAGS = ARCH + ["-shared", "-cudart", "static"]
 
 
 def build(verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     out = os.path.join(HERE, "libdchag.so")
-    srcs = [os.path.join(HERE, "csrc", s) for s in SOURCES]
-    deps = srcs + [os.path.join(HERE, "csrc", h) for h in ("common.cuh", "dchag_kernels.h")]
-    deps.append(os.path.join(os.path.dirname(HERE), "include", "dchag.h"))
-    if os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(d) for d in deps):
+    csrc = os.path.join(HERE, "csrc")
+    srcs = [os.path.join(csrc, s) for s in SOURCES if os.path.exists(os.path.join(csrc, s))]
+    headers = [os.path.join(csrc, h) for h in os.listdir(csrc) if h.endswith((".cuh", ".h"))]
+    headers.append(os.path.join(os.path.dirname(HERE), "include", "dchag.h"))
+    newest_header = max(os.path.getmtime(h) for h in headers)
+    if os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(d)
+                                   for d in srcs + headers):
         return out
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        if (os.path.exists(obj) and os.path.getmtime(obj) >= os.path.getmtime(src)
+                and os.path.getmtime(obj) >= newest_header):
+            return obj
+        cmd = [nvcc, *CFLAGS, "-c", "-o", obj + ".tmp", src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        os.replace(obj + ".tmp", obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
+        objs = list(ex.map(compile_one, srcs))
     tmp = out + ".tmp"
-    cmd = [nvcc, *FLAGS, "-o", tmp, *srcs]
+    cmd = [nvcc, *LFLAGS, "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -102,6 +102,11 @@ const char* dchag_version(void) { return "dchag-b200 0.1.0 (sm_100a)"; }
 const char* dchag_last_error(void) { return g_err.c_str(); }
 int dchag_num_sms(void) { return num_sms_cached(); }
 
+int dchag_combine_overflow(int* flag, int reset) {
+  if (!flag) return fail(DCHAG_ERR_SHAPE, "combine_overflow: null flag");
+  return cuda_status(comb_overflow_flag(flag, reset), "combine_overflow");
+}
+
 static int gemm_impl(const void* A, int G, int Mo, int Mi, int K, long long sAg, long long sAmo,
                      long long sAmi, const void* W, int N, long long sWg, int Nv,
                      const float* bias, long long bias_g, const void* rowbias,

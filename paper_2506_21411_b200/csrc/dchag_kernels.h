@@ -40,6 +40,9 @@ struct GemmArgs {
   int csplit;                   // 1, or 2: split s sums children [s c/2, (s+1) c/2) (partials)
 };
 
+// host read (and optional reset) of the COMB overflow flag (synchronous)
+cudaError_t comb_overflow_flag(int* value, int reset);
+
 cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUtensorMap& tV,
                         const GemmArgs& a, int bk, int num_sms, cudaStream_t st);
 

@@ -22,6 +22,19 @@ constexpr int GEMM_BN_MAX = 256;
 constexpr int GEMM_THREADS = 320;  // producer, MMA, 8 epilogue warps
 constexpr int GEMM_STAGE_OUT = 8 * 32 * 128;  // epilogue staging: 8 warps x 32 rows x 128 B
 constexpr int GEMM_BIAS_SMEM = 8 * 4 * 32 * 4;  // per-warp bias of its 4 column groups (fp32)
+constexpr float kCombRunMax = 65504.f * 256.f;  // range of the COMB running sum (fp16 x 2^8)
+
+// set by the COMB epilogue when a partial child sum leaves the fp16 x 2^8 range
+__device__ int g_comb_overflow = 0;
+
+cudaError_t comb_overflow_flag(int* value, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(value, g_comb_overflow, sizeof(int));
+  if (e == cudaSuccess && reset) {
+    const int zero = 0;
+    e = cudaMemcpyToSymbol(g_comb_overflow, &zero, sizeof(int));
+  }
+  return e;
+}
 
 template <int BK, int STAGES, bool PAIR = false>
 struct GemmSmem {
@@ -401,11 +414,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const float pw = __ldg(args.Lpre + ((size_t)gb * args.M + m_row) * args.H + hd);
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
+            // the running sum is stored as fp16 pairs scaled by 2^-8 (exact power-of-two
+            // scaling): range +-1.68e7 instead of fp16's 65504, absolute error <= 2^-16
+            // below 0.0156; a partial sum beyond that range raises the overflow flag
+            // (dchag_combine_overflow) instead of silently becoming inf
             float2 o = ci ? __half22float2(run[gi][j]) : make_float2(0.f, 0.f);
-            o.x = fmaf(pw, v[2 * j], o.x);
-            o.y = fmaf(pw, v[2 * j + 1], o.y);
+            o.x = fmaf(pw, v[2 * j], o.x * 256.f);
+            o.y = fmaf(pw, v[2 * j + 1], o.y * 256.f);
             if (ci + 1 < c_n) {
-              run[gi][j] = __float22half2_rn(o);
+              if (fmaxf(fabsf(o.x), fabsf(o.y)) > kCombRunMax) g_comb_overflow = 1;
+              run[gi][j] = __float22half2_rn(make_float2(o.x * (1.f / 256.f),
+                                                         o.y * (1.f / 256.f)));
             } else {
               v[2 * j] = o.x;
               v[2 * j + 1] = o.y;

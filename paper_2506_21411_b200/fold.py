@@ -204,6 +204,23 @@ class PackedRank:
     # stream is exactly 1): out = ctx_root @ (Wp_root[:, :D] @ Wf) + (bp_root[:D] @ Wf + bf)
     Wdir: torch.Tensor = None   # [D_out][D] bf16 (n-major)
     bdir: torch.Tensor = None   # [D] fp32
+    # final_layer_tp_split: this rank's column shard of Wf and its bias share (frontend)
+    head_split: tuple | None = None
+
+
+def refresh_packed(old: PackedRank, new: PackedRank) -> None:
+    """Copy a fresh fold into an existing PackedRank's device buffers in place (same
+    shapes: the tree and slab are fixed per module), so pointers captured by CUDA graphs or
+    held by callers see the new weights."""
+    import dataclasses
+    for f in dataclasses.fields(old):
+        a, b = getattr(old, f.name), getattr(new, f.name)
+        if isinstance(a, torch.Tensor):
+            a.copy_(b)
+        elif isinstance(a, list) and a and any(isinstance(x, torch.Tensor) for x in a):
+            for x, y in zip(a, b):
+                if isinstance(x, torch.Tensor):
+                    x.copy_(y)
 
 
 def unit_heads(embed: int, heads: int) -> int:

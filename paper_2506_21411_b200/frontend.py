@@ -25,10 +25,10 @@ import os
 
 import torch
 
-from . import _lib
+from . import _lib, comm
 from .config import (ConfigError, ModelConfig, StrategyConfig, TreeSpec, build_tree_spec,
                      channel_slabs, max_group_for_depth)
-from .fold import fold_rank, pack_rank
+from .fold import fold_rank, pack_rank, refresh_packed
 from .payload import payload_nbytes, views
 
 
@@ -121,6 +121,7 @@ class DchagFrontEnd(torch.nn.Module):
             else torch.device("cpu"))
         self.weights: dict[str, torch.Tensor] = {}
         self._packed = None
+        self._packed_sig = None
 
     # ------------------------------------------------------------------ config
     def _check_gpu_shape(self):
@@ -165,7 +166,10 @@ class DchagFrontEnd(torch.nn.Module):
                 raise ConfigError(f"{name}: shape {tuple(t.shape)} != {shape}")
             keep[name] = t.to(device=self.device, dtype=torch.float32)
         self.weights = keep
+        # a new weight set may differ in every derived buffer: fold from scratch (the
+        # head-split final-layer shards live on the packed rank, so they go with it)
         self._packed = None
+        self._packed_sig = None
 
     def needed_names(self):
         return [n for n, _, _ in self.param_specs()
@@ -196,22 +200,38 @@ class DchagFrontEnd(torch.nn.Module):
         self.load_weights(master)
         return master
 
+    def _weights_signature(self):
+        """Identity and in-place version of every loaded weight tensor: an optimizer step
+        (in-place update) or a reassignment changes it."""
+        return tuple((k, id(v), v._version) for k, v in self.weights.items())
+
     def prepare(self):
-        """Fold + pack the weights for the kernels (cached until weights change)."""
+        """Fold + pack the weights for the kernels. The folded buffers are rebuilt whenever
+        a loaded weight changes (reassigned, reloaded, or updated in place: the check keys on
+        each tensor's version counter). A refold of an already packed rank writes into the
+        existing device buffers, so CUDA graphs captured over them stay valid."""
         if self._unfolded():
             if not self.weights:
                 raise RuntimeError("no weights loaded")
             return None  # full_cross / fp32 run the unfolded ops path on the reference weights
-        if self._packed is None:
-            if not self.weights:
-                raise RuntimeError("no weights loaded")
+        if not self.weights:
+            raise RuntimeError("no weights loaded")
+        sig = self._weights_signature()
+        if self._packed is None or self._packed_sig != sig:
             with torch.no_grad():
                 fr = fold_rank(self.weights, rank=self.rank, slab=self.slab,
                                levels=self.tree.levels, embed=self.model.embed,
                                heads=self.model.heads, patch=self.model.patch, seq=self.seq,
                                variant=self.model.agg_variant,
                                layer_kind=self.strategy.agg_layer_kind)
-                self._packed = pack_rank(fr, self.device)
+                fresh = pack_rank(fr, self.device)
+                if self._packed is None:
+                    self._packed = fresh
+                else:
+                    refresh_packed(self._packed, fresh)
+                    if self._packed.head_split is not None:
+                        self._head_split_weights(self._packed, refresh=True)
+            self._packed_sig = sig
         return self._packed
 
     # ------------------------------------------------------------------ forward
@@ -237,10 +257,9 @@ class DchagFrontEnd(torch.nn.Module):
                                self.strategy.agg_layer_kind, "full_cross", m.heads,
                                out_dtype=torch.bfloat16)                       # [B,1,S,D]
         if self.tp > 1:
-            import torch.distributed as dist
             y = y.contiguous()
             allg = torch.empty((self.tp,) + tuple(y.shape), device=y.device, dtype=y.dtype)
-            dist.all_gather_into_tensor(allg, y, group=self.process_group)
+            comm.all_gather_into_tensor(allg, y, group=self.process_group)
             self._log("AllGather", "forward", "dchag-boundary", y.numel() * y.element_size())
             gathered = allg.squeeze(2).permute(1, 0, 2, 3)                     # [B,tp,S,D]
         else:
@@ -265,9 +284,8 @@ class DchagFrontEnd(torch.nn.Module):
         y = ops.tree_aggregate_fp32(tok, self.tree, w, f"agg.slab{self.rank}",
                                     self.strategy.agg_layer_kind, m.heads).contiguous()
         if self.tp > 1:
-            import torch.distributed as dist
             allg = torch.empty((self.tp,) + tuple(y.shape), device=y.device, dtype=y.dtype)
-            dist.all_gather_into_tensor(allg, y, group=self.process_group)
+            comm.all_gather_into_tensor(allg, y, group=self.process_group)
             self._log("AllGather", "forward", "dchag-boundary", y.numel() * y.element_size())
             gathered = allg.squeeze(2).permute(1, 0, 2, 3)
         else:
@@ -321,8 +339,7 @@ class DchagFrontEnd(torch.nn.Module):
         if not return_payload and nc > 1:
             res = self._forward_pipelined(images, pk, dev_out, nc)
             if out is not None and not out.is_cuda:
-                out.copy_(res, non_blocking=True)
-                res = out
+                res = self._to_host(res, out)
             return res
         if self.tp == 1 and not return_payload:
             # one stream: the final layer's softmax is exactly 1, so the root projection and
@@ -332,8 +349,7 @@ class DchagFrontEnd(torch.nn.Module):
                 B, 1, self.seq, m.embed, device=images.device, dtype=self.out_dtype)
             self.local_payload(images, pk, direct_out=res)
             if out is not None and not out.is_cuda:
-                out.copy_(res, non_blocking=True)
-                res = out
+                res = self._to_host(res, out)
             return res
         payload = self.local_payload(images, pk)
         if return_payload or not self._position_split(images.shape[0]):
@@ -342,9 +358,16 @@ class DchagFrontEnd(torch.nn.Module):
         else:
             res = self.exchange_finish(payload, images.shape[0], out=dev_out)
         if out is not None and not out.is_cuda:
-            out.copy_(res, non_blocking=True)
-            res = out
+            res = self._to_host(res, out)
         return (res, gathered) if return_payload else res
+
+    @staticmethod
+    def _to_host(res, out):
+        """Copy a device result into the caller's host tensor and wait for it: like the
+        reference's synchronous API, `out` is complete when forward returns."""
+        out.copy_(res, non_blocking=True)
+        torch.cuda.current_stream(res.device).synchronize()
+        return out
 
     def vit_input(self, images, mask, mask_token, meta, meta_w, meta_b, out=None):
         """Front end + the trunk's input assembly: the aggregate with masked
@@ -426,6 +449,7 @@ class DchagFrontEnd(torch.nn.Module):
                     out[b0:b1].copy_(res[b0:b1], non_blocking=True)
         if out is not None and not out.is_cuda:
             cur.wait_stream(side)
+            cur.synchronize()  # a host `out` holds the result when forward returns
             return out
         return res
 
@@ -481,10 +505,9 @@ class DchagFrontEnd(torch.nn.Module):
         """AllGather of the per-rank root payload in rank order (runtime.py:259)."""
         if self.tp == 1:
             return payload
-        import torch.distributed as dist
         gathered = torch.empty(self.tp * payload.numel(), device=payload.device,
                                dtype=torch.uint8)
-        dist.all_gather_into_tensor(gathered, payload, group=self.process_group)
+        comm.all_gather_into_tensor(gathered, payload, group=self.process_group)
         self._log("AllGather", "forward", "dchag-boundary", payload.numel())
         return gathered
 
@@ -524,7 +547,6 @@ class DchagFrontEnd(torch.nn.Module):
         """First half of the position-split final layer: rank j receives rows
         [j R/tp, (j+1) R/tp) of every rank's root payload (one all-to-all of V, one of L).
         With async_op the exchange runs on NCCL's stream while later kernels proceed."""
-        import torch.distributed as dist
         m = self.model
         d, h = m.embed, m.heads
         R = B * self.seq
@@ -534,9 +556,9 @@ class DchagFrontEnd(torch.nn.Module):
         V, L = views(payload, R, d, h)
         Vx = torch.empty(tp, Rl, d, device=dev, dtype=torch.bfloat16)
         Lx = torch.empty(tp, Rl, h, device=dev, dtype=torch.float32)
-        w1 = dist.all_to_all_single(Vx, V.view(tp, Rl, d), group=self.process_group,
+        w1 = comm.all_to_all_single(Vx, V.view(tp, Rl, d), group=self.process_group,
                                     async_op=async_op)
-        w2 = dist.all_to_all_single(Lx, L.view(tp, Rl, h), group=self.process_group,
+        w2 = comm.all_to_all_single(Lx, L.view(tp, Rl, h), group=self.process_group,
                                     async_op=async_op)
         self._log("AllToAll", "forward", "dchag-boundary", payload.numel())
         return (B, Vx, Lx, (w1, w2) if async_op else ())
@@ -544,7 +566,6 @@ class DchagFrontEnd(torch.nn.Module):
     def exchange_complete(self, state, out=None, async_op=False):
         """Second half: combine the tp streams of this rank's R/tp rows, final projection,
         all-gather of the outputs in rank (= row) order. Returns (out, pending work)."""
-        import torch.distributed as dist
         B, Vx, Lx, works = state
         for wk in works:
             wk.wait()  # the current stream waits for the exchange
@@ -566,7 +587,7 @@ class DchagFrontEnd(torch.nn.Module):
                   int(self.out_dtype == torch.float32), Rl * d, 0, d, 0, 0, 0, 0, st)
         if out is None:
             out = torch.empty(R, d, device=dev, dtype=self.out_dtype)
-        wk = dist.all_gather_into_tensor(out.view(R, d), part, group=self.process_group,
+        wk = comm.all_gather_into_tensor(out.view(R, d), part, group=self.process_group,
                                          async_op=async_op)
         self._log("AllGather", "forward", "dchag-final-out",
                   part.numel() * part.element_size())
@@ -619,7 +640,7 @@ class DchagFrontEnd(torch.nn.Module):
             for g in pk.l0_g_list:
                 poff_list.append(acc)
                 acc += g * R * h
-            poff = torch.tensor(poff_list, device=dev, dtype=torch.int64)
+            poff = self.dev_table(poff_list, torch.int64, dev)  # made once: no per-call H2D
             pbuf = torch.empty(acc, **bf16)
             # unnormalised e + 1/sum: K_l0 scales its accumulator (one exp per logit)
             pinv = torch.empty(pk.n0, R, h, **f32)
@@ -738,7 +759,6 @@ class DchagFrontEnd(torch.nn.Module):
         rank owns heads [r H/tp, (r+1) H/tp); its partial output ctx[:, own columns] @
         wo[own rows] (+ bo on rank 0) is summed over the tp group (the reference's allsum =
         ReduceScatter + AllGather, one NCCL all-reduce here)."""
-        import torch.distributed as dist
         pk = self.prepare()
         m = self.model
         d, s = m.embed, self.seq
@@ -746,29 +766,54 @@ class DchagFrontEnd(torch.nn.Module):
         dev = ctx_f.device
         kc = d // self.tp
         c0 = self.rank * kc
-        key = ("head_split_w", dev)
-        cache = self.__dict__.setdefault("_cache", {})
-        if key not in cache:
-            wf_loc = pk.Wf[:, c0:c0 + kc].contiguous()            # [D_out][D/tp] n-major
-            b_loc = pk.bf if self.rank == 0 else torch.zeros_like(pk.bf)
-            cache[key] = (wf_loc, b_loc)
-        wf_loc, b_loc = cache[key]
+        wf_loc, b_loc = self._head_split_weights(pk)
         part = torch.empty(R, d, device=dev, dtype=torch.float32)
         a = ctx_f.view(R, d)[:, c0:]                                # K = D/tp columns, row stride D
         _lib.call("dchag_gemm_bf16", _lib.ptr(a), 1, 1, R, kc, R * d, 0, d, _lib.ptr(wf_loc),
                   d, d * kc, d, _lib.ptr(b_loc), d, 0, 0, 0, 1, _lib.ptr(part), 1, R * d, 0, d,
                   0, 0, 0, 0, _lib.stream_handle())
-        dist.all_reduce(part, group=self.process_group)
+        comm.all_reduce(part, group=self.process_group)
         self._log("AllReduce", "forward", "agg-final", (part.numel(), part.element_size()))
         out.copy_(part.view_as(out))
         return out.view(B, 1, s, d)
 
+    def _head_split_weights(self, pk, refresh=False):
+        """This rank's column shard of the folded final projection and its bias share
+        (bo on rank 0 only). Kept on the packed rank, so a refold updates it in place."""
+        kc = self.model.embed // self.tp
+        c0 = self.rank * kc
+        wf_loc = pk.Wf[:, c0:c0 + kc]                              # [D_out][D/tp] n-major
+        if pk.head_split is None:
+            pk.head_split = (wf_loc.contiguous(),
+                             pk.bf.clone() if self.rank == 0 else torch.zeros_like(pk.bf))
+        elif refresh:
+            pk.head_split[0].copy_(wf_loc)
+            if self.rank == 0:
+                pk.head_split[1].copy_(pk.bf)
+        return pk.head_split
+
+    @staticmethod
+    def combine_overflowed(reset: bool = True) -> bool:
+        """Range guard of the fused level kernel (dchag_gemm_combine keeps its running child
+        sum as fp16 x 2^8, range +-1.68e7): True if any forward since the last reset produced
+        a partial sum outside that range (its output then holds inf). Synchronises the
+        device; DCHAG_FUSE_COMBINE=0 selects the unfused levels, which have no such limit."""
+        import ctypes
+        flag = ctypes.c_int(0)
+        _lib.call("dchag_combine_overflow", ctypes.byref(flag), int(reset))
+        return bool(flag.value)
+
+    def dev_table(self, vals, dtype, dev):
+        """A small host-known index table on the device, made once per content: a forward
+        (or a CUDA-graph capture) never issues a pageable H2D copy, which would synchronise
+        the stream."""
+        key = ("table", tuple(int(v) for v in vals), dtype, str(dev))
+        cache = self.__dict__.setdefault("_cache", {})
+        t = cache.get(key)
+        if t is None:
+            t = cache[key] = torch.tensor(key[1], device=dev, dtype=dtype)
+        return t
+
     def _final_first(self, dev):
-        key = ("final_first", dev)
-        cache = getattr(self, "_cache", None)
-        if cache is None:
-            cache = self._cache = {}
-        if key not in cache:
-            cache[key] = (torch.zeros(1, device=dev, dtype=torch.int32),
-                          torch.full((1,), self.tp, device=dev, dtype=torch.int32))
-        return cache[key]
+        return (self.dev_table([0], torch.int32, dev),
+                self.dev_table([self.tp], torch.int32, dev))

@@ -30,7 +30,7 @@ import weakref
 
 import torch
 
-from . import _lib
+from . import _lib, comm
 from .config import ConfigError
 from .fold import query_logit_weights
 from .frontend import DchagFrontEnd
@@ -250,10 +250,9 @@ class DchagTrainer:
         fe = self.fe
         y_root = saved["y_root"]
         if fe.tp > 1:
-            import torch.distributed as dist
             y_all = torch.empty((fe.tp,) + tuple(y_root.shape), device=y_root.device,
                                 dtype=torch.bfloat16)
-            dist.all_gather_into_tensor(y_all, y_root, group=fe.process_group)
+            comm.all_gather_into_tensor(y_all, y_root, group=fe.process_group)
             fe._log("AllGather", "forward", "dchag-boundary",
                     y_root.numel() * y_root.element_size())
         else:
@@ -361,8 +360,7 @@ class DchagTrainer:
         if self.dp_group is not None:
             self._dp_average(grads)
         if self.fe.tp > 1:
-            import torch.distributed as dist
-            dist.all_reduce(grads["special.pos"], group=self.fe.process_group)
+            comm.all_reduce(grads["special.pos"], group=self.fe.process_group)
             self.fe._log("AllReduce", "optimizer", "shared-grad.special.pos",
                          (grads["special.pos"].numel(), grads["special.pos"].element_size()))
         return grads
@@ -378,7 +376,7 @@ class DchagTrainer:
             return
         names = sorted(grads)
         flat = torch.cat([grads[k].reshape(-1).float() for k in names])
-        dist.all_reduce(flat, group=self.dp_group)
+        comm.all_reduce(flat, group=self.dp_group)
         flat.mul_(1.0 / ndp)
         off = 0
         led = self.fe.ledger
@@ -404,7 +402,6 @@ class DchagTrainer:
         streams onto its own heads only (wv / wk / wq column shards, params.py:166-177),
         combines them, and its partial ctx_own @ wo[own rows] is summed over the tp group
         (TpHooks.allsum = ReduceScatter + AllGather; one all-reduce), bo added once."""
-        import torch.distributed as dist
         fe = self.fe
         w = fe.weights
         d, h, s = fe.model.embed, fe.model.heads, fe.seq
@@ -418,7 +415,7 @@ class DchagTrainer:
         ctx_f = self._combine(Vf, Lf, None, [0], [fe.tp], R, heads=hc)
         bo = w["agg.final.bo"] if fe.rank == 0 else torch.zeros_like(w["agg.final.bo"])
         out = _gemm(ctx_f[0], w["agg.final.wo"][cols], bo, out_f32=True)
-        dist.all_reduce(out, group=fe.process_group)
+        comm.all_reduce(out, group=fe.process_group)
         fe._log("AllReduce", "forward", "agg-final", (out.numel(), out.element_size()))
         saved.update(y_all=y_all, Vf=Vf, Lf=Lf, ctx_f=ctx_f)
         return out.view(B, 1, s, d)
@@ -428,7 +425,6 @@ class DchagTrainer:
         the own heads; bo and the fanned-out q in full), and the root-stream gradient by a
         ReduceScatter of every rank's partial gathered-stream gradient along the stream axis
         (the fused TpHooks.fanout RS + AG and gather slice, strategies.py:54-67, :91-94)."""
-        import torch.distributed as dist
         fe = self.fe
         w = fe.weights
         d, h = fe.model.embed, fe.model.heads
@@ -450,14 +446,14 @@ class DchagTrainer:
         grads["agg.final.wk"] = gu["agg.final.wk"][:, cols].contiguous()
         grads["agg.final.wq"] = gu["agg.final.wq"][:, cols].contiguous()
         q_grad = gu["agg.final.q"].contiguous()
-        dist.all_reduce(q_grad, group=fe.process_group)                   # fanout of q
+        comm.all_reduce(q_grad, group=fe.process_group)                   # fanout of q
         fe._log("AllReduce", "backward", "agg-final", (q_grad.numel(), q_grad.element_size()))
         grads["agg.final.q"] = q_grad
         U_own = query_logit_weights(w, "agg.final", h)[:, hs]
         g_part = (_mm(gV, w["agg.final.wv"][:, cols].t()) +
                   dL @ U_own.t()).contiguous()                            # [tp, R, D]
         g_y = torch.empty(R, d, device=g_out.device, dtype=torch.float32)
-        dist.reduce_scatter_tensor(g_y, g_part.view(fe.tp * R, d), group=fe.process_group)
+        comm.reduce_scatter_tensor(g_y, g_part.view(fe.tp * R, d), group=fe.process_group)
         fe._log("ReduceScatter", "backward", "agg-final", g_y.numel() * g_y.element_size())
         return grads, g_y.view(1, R, d)
 

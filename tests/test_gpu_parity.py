@@ -472,3 +472,55 @@ def test_forward_tp1_direct_matches_oracle(lk, out_dtype):
     pay = fe.local_payload(_bf(images).cuda())
     alt = fe.finish(pay, 4).float().cpu().numpy()
     assert rel_err(got, alt) < 1e-2
+
+
+def test_inplace_weight_update_refolds():
+    """An in-place update of a loaded weight (an optimizer step) must reach the folded
+    kernel operands: the next forward equals a fresh module loaded with the new weights, and
+    the packed device buffers are updated in place (captured graphs keep valid pointers)."""
+    from paper_2506_21411_b200 import DchagFrontEnd
+    cfg = (20, 64, 128, 8, 256, 4)
+    fe = DchagFrontEnd(*cfg, max_group=8, out_dtype=torch.float32)
+    fe.init_weights(seed=3)
+    x = torch.randn(2, 20, 64, 128, device="cuda").to(torch.bfloat16)
+    y0 = fe(x).clone()
+    mt_ptr = fe.prepare().Mt.data_ptr()
+    with torch.no_grad():
+        for k, v in fe.weights.items():
+            if k.endswith(".wv") or k == "tok.w" or k == "agg.final.wo":
+                v.mul_(1.5)
+    y1 = fe(x)
+    assert fe.prepare().Mt.data_ptr() == mt_ptr
+    fresh = DchagFrontEnd(*cfg, max_group=8, out_dtype=torch.float32)
+    fresh.load_weights({k: v.clone() for k, v in fe.weights.items()})
+    y2 = fresh(x)
+    torch.cuda.synchronize()
+    assert not torch.equal(y0, y1)
+    assert torch.equal(y1, y2)
+
+
+@pytest.mark.parametrize("scale,overflow", [(2.0 ** 20, False), (2.0 ** 26, True)])
+def test_combine_range_guard(scale, overflow):
+    """dchag_gemm_combine keeps its running child sum as fp16 x 2^8: partial sums far beyond
+    fp16's 65504 stay exact to fp16 precision, and a sum beyond +-1.68e7 raises the overflow
+    flag (DchagFrontEnd.combine_overflowed) instead of passing silently."""
+    from paper_2506_21411_b200 import DchagFrontEnd
+    L = _lib()
+    nc, R, D, H = 4, 256, 256, 8
+    g = torch.Generator().manual_seed(9)
+    ctx = torch.randn(nc, R, D, generator=g).to(torch.bfloat16).cuda()
+    W = (torch.eye(D) * scale).expand(nc, D, D).to(torch.bfloat16).contiguous().cuda()
+    bias = torch.zeros(nc, D, device="cuda")
+    P = torch.full((nc, R, H), 0.25, device="cuda")        # softmax weights (4 children)
+    first = torch.tensor([0], dtype=torch.int32, device="cuda")
+    count = torch.tensor([nc], dtype=torch.int32, device="cuda")
+    out = torch.empty(1, 1, R, D, device="cuda", dtype=torch.bfloat16)
+    DchagFrontEnd.combine_overflowed(reset=True)
+    L.call("dchag_gemm_combine", L.ptr(ctx), nc, R, D, H, L.ptr(W), D * D, L.ptr(bias), D,
+           L.ptr(P), L.ptr(first), L.ptr(count), 1, 1, L.ptr(out), L.stream_handle())
+    torch.cuda.synchronize()
+    assert DchagFrontEnd.combine_overflowed(reset=True) == overflow
+    if not overflow:
+        want = 0.25 * scale * ctx.float().sum(0)
+        assert torch.isfinite(out).all()
+        assert rel_err(out[0, 0].float().cpu().numpy(), want.cpu().numpy()) < 5e-3

@@ -30,7 +30,7 @@ ev = []
 idx = {"i": 0}
 
 
-def hook(name, phase):
+def hook(name, phase, work=None):
     e = torch.cuda.Event(enable_timing=True)
     e.record()
     if phase == "pre":
