@@ -43,6 +43,22 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
                     int outV_f32, long long sVg, long long sVmo, long long sVmi, float* outL,
                     long long sLg, long long sLmo, long long sLmi, void* stream);
 
+/* General tcgen05 GEMM with explicit operand layouts (training backward and weight
+ * folding: the reference's matmul backward, tensor.py:168-188 differentiated by
+ * tensor.py:395-413, i.e. dW = X^T G and dX = G W^T without transposed copies):
+ *   out[g][m][n] (+)= sum_k A_g(m, k) * B_g(n, k) + bias[g][n]
+ * A: a_mn = 0 K-major, (m, k) at g*sAg + m*lda + k;
+ *    a_mn = 1 MN-major, (m, k) at g*sAg + (k / Ki)*sAko + (k % Ki)*lda + m   (Ki % 64 == 0)
+ * B: b_mn = 0 K-major, (n, k) at g*sBg + n*ldb + k;  b_mn = 1 MN-major, (n, k) at g*sBg + k*ldb + n
+ * out: fp32 (out_f32 = 1; accumulate = 1 adds the product to the existing values) or bf16,
+ * (m, n) at g*sCg + m*ldc + n. bias (fp32, optional) at g*bias_g + n.
+ * M % 128 == 0 (M % 256 == 0 with an MN-major operand), N % 16 == 0, K % 64 == 0;
+ * operands 16-byte aligned. Deterministic (fixed accumulation order, no split-K). */
+int dchag_gemm_nt(const void* A, int a_mn, long long lda, long long sAko, int Ki,
+                  long long sAg, const void* B, int b_mn, long long ldb, long long sBg, int G,
+                  int M, int N, int K, const float* bias, long long bias_g, void* out,
+                  int out_f32, int accumulate, long long ldc, long long sCg, void* stream);
+
 /* Row-dot GEMM for the level-0 backward (the `dp = G . V` term of the softmax backward,
  * layers.py:103-121 differentiated by tensor.py:395-413): the product rows
  * V[g][m][:] = A[g][m][:] W[g]^T + bias[g] are never stored; for every 32-column group

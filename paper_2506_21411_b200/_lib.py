@@ -22,6 +22,8 @@ SIGNATURES = {
     "dchag_gemm_bf16": [c_vp, c_int, c_int, c_int, c_int, c_ll, c_ll, c_ll, c_vp, c_int, c_ll,
                         c_int, c_vp, c_ll, c_vp, c_ll, c_ll, c_int, c_vp, c_int, c_ll, c_ll,
                         c_ll, c_vp, c_ll, c_ll, c_ll, c_vp],
+    "dchag_gemm_nt": [c_vp, c_int, c_ll, c_ll, c_int, c_ll, c_vp, c_int, c_ll, c_ll, c_int,
+                      c_int, c_int, c_int, c_vp, c_ll, c_vp, c_int, c_int, c_ll, c_ll, c_vp],
     "dchag_gemm_rowdot": [c_vp, c_int, c_int, c_int, c_int, c_ll, c_ll, c_ll, c_vp, c_int,
                           c_ll, c_vp, c_ll, c_vp, c_ll, c_vp, c_vp],
     "dchag_gemm_combine": [c_vp, c_int, c_int, c_int, c_int, c_vp, c_ll, c_vp, c_ll, c_vp,

@@ -28,18 +28,18 @@ def _staged(t: torch.Tensor, group) -> bool:
 def all_gather_into_tensor(out, inp, group=None, async_op=False):
     if not _staged(inp, group):
         return dist.all_gather_into_tensor(out, inp, group=group, async_op=async_op)
-    host = torch.empty(out.shape, dtype=out.dtype)
-    dist.all_gather_into_tensor(host, inp.cpu(), group=group)
-    out.copy_(host)
+    host = torch.empty(out.numel(), dtype=out.dtype)   # gloo wants [world * n] for [n]
+    dist.all_gather_into_tensor(host, inp.reshape(-1).cpu(), group=group)
+    out.copy_(host.view(out.shape))
     return _Done() if async_op else None
 
 
 def all_to_all_single(out, inp, group=None, async_op=False):
     if not _staged(inp, group):
         return dist.all_to_all_single(out, inp, group=group, async_op=async_op)
-    host = torch.empty(out.shape, dtype=out.dtype)
-    dist.all_to_all_single(host, inp.contiguous().cpu(), group=group)
-    out.copy_(host)
+    host = torch.empty(out.numel(), dtype=out.dtype)
+    dist.all_to_all_single(host, inp.reshape(-1).cpu(), group=group)
+    out.copy_(host.view(out.shape))
     return _Done() if async_op else None
 
 
@@ -54,6 +54,6 @@ def all_reduce(t, group=None):
 def reduce_scatter_tensor(out, inp, group=None):
     if not _staged(inp, group):
         return dist.reduce_scatter_tensor(out, inp, group=group)
-    host = torch.empty(out.shape, dtype=out.dtype)
-    dist.reduce_scatter_tensor(host, inp.contiguous().cpu(), group=group)
-    out.copy_(host)
+    host = torch.empty(out.numel(), dtype=out.dtype)
+    dist.reduce_scatter_tensor(host, inp.reshape(-1).cpu(), group=group)
+    out.copy_(host.view(out.shape))

@@ -194,6 +194,70 @@ int dchag_gemm_bf16(const void* A, int G, int Mo, int Mi, int K, long long sAg, 
                    sLg, sLmo, sLmi, nullptr, 0, nullptr, stream);
 }
 
+int dchag_gemm_nt(const void* A, int a_mn, long long lda, long long sAko, int Ki,
+                  long long sAg, const void* B, int b_mn, long long ldb, long long sBg, int G,
+                  int M, int N, int K, const float* bias, long long bias_g, void* out,
+                  int out_f32, int accumulate, long long ldc, long long sCg, void* stream) {
+  if (G < 1 || M < 128 || M % 128 || N < 16 || N % 16 || K < 64 || K % 64 || !A || !B ||
+      !out || (a_mn && (Ki < 64 || Ki % 64 || K % Ki)) || (accumulate && !out_f32))
+    return fail(DCHAG_ERR_SHAPE, "gemm_nt: bad shape G=%d M=%d N=%d K=%d Ki=%d", G, M, N, K, Ki);
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) % 16 ||
+      (lda * 2) % 16 || (sAko * 2) % 16 || (sAg * 2) % 16 || (ldb * 2) % 16 || (sBg * 2) % 16)
+    return fail(DCHAG_ERR_SHAPE, "gemm_nt: operand pointers / strides must be 16-byte aligned");
+  const int lay = (a_mn ? 1 : 0) | (b_mn ? 2 : 0);
+  const int ntm = M / 128;
+  const int pair = ntm % 2 == 0;
+  if (lay && !pair) return fail(DCHAG_ERR_SHAPE, "gemm_nt: MN-major operands need M %% 256 == 0");
+  // N tiles of 256 (128 when that is needed to fill the SMs, or for small N)
+  int bn = N >= 256 ? 256 : (N + 15) / 16 * 16;
+  if (b_mn) bn = N >= 256 ? 256 : 128;
+  const int sms = num_sms_cached();
+  auto units = [&](int b) { return G * (ntm / (pair ? 2 : 1)) * ((N + b - 1) / b); };
+  if (bn == 256 && units(256) < sms / (pair ? 2 : 1) && N > 128) bn = 128;
+  CUtensorMap tA, tW, tV;
+  memset(&tV, 0, sizeof(tV));
+  int rc;
+  if (a_mn) {
+    cuuint64_t dims[4] = {(cuuint64_t)M, (cuuint64_t)Ki, (cuuint64_t)(K / Ki), (cuuint64_t)G};
+    cuuint64_t str[3] = {(cuuint64_t)lda * 2, (cuuint64_t)sAko * 2, (cuuint64_t)sAg * 2};
+    cuuint32_t box[4] = {64u, 64u, 1, 1};
+    rc = make_map(&tA, A, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  } else {
+    cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)M, 1, (cuuint64_t)G};
+    cuuint64_t str[3] = {(cuuint64_t)lda * 2, (cuuint64_t)lda * M * 2, (cuuint64_t)sAg * 2};
+    cuuint32_t box[4] = {64u, 128u, 1, 1};
+    rc = make_map(&tA, A, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
+  if (rc) return rc;
+  if (b_mn) {
+    cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)K, (cuuint64_t)G};
+    cuuint64_t str[2] = {(cuuint64_t)ldb * 2, (cuuint64_t)sBg * 2};
+    cuuint32_t box[3] = {64u, 64u, 1};
+    rc = make_map(&tW, B, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  } else {
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)N, (cuuint64_t)G};
+    cuuint64_t str[2] = {(cuuint64_t)ldb * 2, (cuuint64_t)sBg * 2};
+    cuuint32_t box[3] = {64u, (cuuint32_t)(pair ? bn / 2 : bn), 1};
+    rc = make_map(&tW, B, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
+  if (rc) return rc;
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.G = G; a.M = M; a.Mi = M; a.N = N; a.Nv = N; a.K = K; a.BN = bn;
+  a.pair = pair; a.lay = lay; a.Ki = a_mn ? Ki : K; a.accum = accumulate;
+  a.bias = bias; a.bias_g = bias_g; a.rowbias_period = 1;
+  a.outV = out; a.outV_f32 = out_f32; a.sVg = sCg; a.sVmo = 0; a.sVmi = ldc;
+  if (!out_f32 && N >= 32 &&
+      ((reinterpret_cast<uintptr_t>(out) | (uintptr_t)(ldc * 2) | (uintptr_t)(sCg * 2)) % 16) == 0) {
+    cuuint64_t dims[4] = {(cuuint64_t)N, (cuuint64_t)M, 1, (cuuint64_t)G};
+    cuuint64_t str[3] = {(cuuint64_t)ldc * 2, (cuuint64_t)M * ldc * 2,
+                         (cuuint64_t)(G > 1 ? sCg : M * ldc) * 2};
+    cuuint32_t box[4] = {32, 32, 1, 1};
+    if (make_map(&tV, out, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B) == DCHAG_OK) a.v_tma = 1;
+  }
+  return cuda_status(launch_gemm(tA, tW, tV, a, 64, sms, S(stream)), "gemm_nt");
+}
+
 int dchag_gemm_rowdot(const void* A, int G, int Mo, int Mi, int K, long long sAg,
                       long long sAmo, long long sAmi, const void* W, int N, long long sWg,
                       const float* bias, long long bias_g, const void* Gmat, long long ldG,

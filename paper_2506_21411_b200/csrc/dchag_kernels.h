@@ -38,6 +38,9 @@ struct GemmArgs {
   int H, dh;
   int nparents;                 // COMB: G = nparents * csplit; group g = split s * nparents + j
   int csplit;                   // 1, or 2: split s sums children [s c/2, (s+1) c/2) (partials)
+  int lay;                      // operand layouts: bit 0 A MN-major, bit 1 W MN-major
+  int Ki;                       // MN-major A: K = Ko * Ki rows, (k / Ki) * sAko + (k % Ki) * lda
+  int accum;                    // fp32 output: out += acc instead of out = acc
 };
 
 // host read (and optional reset) of the COMB overflow flag (synchronous)

@@ -91,7 +91,12 @@ DEV void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cl, int 
       : "memory");
 }
 
-template <int BK, int STAGES, bool PAIR, bool COMB = false>
+// LAY (operand layouts, training backward / weight folding): bit 0 = A is MN-major
+// (element (m, k) at (k / Ki) * sAko + (k % Ki) * lda + m: TMA'd as two 64-row x 64-column
+// 128B-swizzled atoms per stage), bit 1 = W is MN-major ((n, k) at k * ldw + n). MN-major
+// operands need BK = 64 and the CTA-pair kernel; the MMA reads them with the transpose bits
+// of the instruction descriptor.
+template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                 const __grid_constant__ CUtensorMap tmV, GemmArgs args) {
@@ -205,8 +210,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (crank == 0)
               mbar_expect_tx(&full[stage], 2 * (SM::A_BYTES + w_rows * BK * 2));
             const uint32_t fb = rank0_addr(&full[stage]);
-            tma_load_4d_pair(sA, &tmA, fb, ks * BK, mi, mo, g);
-            tma_load_3d_pair(sW, &tmW, fb, ks * BK, nt * args.BN + crank * w_rows, g);
+            if constexpr ((LAY & 1) != 0) {
+              const int k0 = ks * BK, ko = k0 / args.Ki, ki = k0 - ko * args.Ki;
+              tma_load_4d_pair(sA, &tmA, fb, m0, ki, ko, g);
+              tma_load_4d_pair(sA + 8192, &tmA, fb, m0 + 64, ki, ko, g);
+            } else {
+              tma_load_4d_pair(sA, &tmA, fb, ks * BK, mi, mo, g);
+            }
+            if constexpr ((LAY & 2) != 0) {
+              for (int j = 0; j < w_rows / 64; ++j)
+                tma_load_3d_pair(sW + j * 8192, &tmW, fb, nt * args.BN + crank * w_rows + 64 * j,
+                                 ks * BK, g);
+            } else {
+              tma_load_3d_pair(sW, &tmW, fb, ks * BK, nt * args.BN + crank * w_rows, g);
+            }
           } else {
             mbar_expect_tx(&full[stage], SM::A_BYTES + args.BN * BK * 2);
             tma_load_4d(sA, &tmA, &full[stage], ks * BK, mi, mo, g);
@@ -219,7 +236,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (the leader of a pair)
     if (crank == 0) {
-      const uint32_t idesc = idesc_bf16_f32(GEMM_BM * CL, args.BN);
+      const uint32_t idesc = idesc_bf16_f32(GEMM_BM * CL, args.BN) |
+                             ((LAY & 1) ? (1u << 15) : 0u) | ((LAY & 2) ? (1u << 16) : 0u);
       constexpr uint32_t SBO = 8 * BK * 2;  // 8 rows x swizzle width
       int stage = 0;
       uint32_t phase = 0;
@@ -244,8 +262,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const uint32_t w_addr = a_addr + SM::A_BYTES;
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint64_t ad = smem_desc(a_addr + kk * 32, 16, SBO, swz_layout<BK>());
-              const uint64_t wd = smem_desc(w_addr + kk * 32, 16, SBO, swz_layout<BK>());
+              // MN-major: 16 K rows of 128 B per k-step, 64-element atoms 8 KB apart
+              const uint64_t ad = (LAY & 1) ? smem_desc(a_addr + kk * 2048, 8192, 1024, 2u)
+                                            : smem_desc(a_addr + kk * 32, 16, SBO, swz_layout<BK>());
+              const uint64_t wd = (LAY & 2) ? smem_desc(w_addr + kk * 2048, 8192, 1024, 2u)
+                                            : smem_desc(w_addr + kk * 32, 16, SBO, swz_layout<BK>());
               if (!(args.debug & 4)) {
                 if (PAIR) mma_ss_pair(d_tmem, ad, wd, idesc, (ks | kk) != 0);
                 else mma_ss(d_tmem, ad, wd, idesc, (ks | kk) != 0);
@@ -509,11 +530,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 const int rr = i * rows_per + lane / nk4, k = lane % nk4;
                 const int mrow = mt0 + rr;
                 const int mo2 = mrow / args.Mi, mi2 = mrow - mo2 * args.Mi;
-                const float4 o =
+                float4 o =
                     *reinterpret_cast<const float4*>(my_out + rr * 128 + ((k ^ (rr & 7)) << 4));
-                *reinterpret_cast<float4*>(reinterpret_cast<float*>(args.outV) +
-                                           (size_t)g * args.sVg + (size_t)mo2 * args.sVmo +
-                                           (size_t)mi2 * args.sVmi + n0 + k * 4) = o;
+                float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.outV) +
+                                                        (size_t)g * args.sVg + (size_t)mo2 * args.sVmo +
+                                                        (size_t)mi2 * args.sVmi + n0 + k * 4);
+                if (args.accum) {  // out += acc (one owner per element: deterministic)
+                  const float4 old = *dst;
+                  o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+                }
+                *dst = o;
               }
             }
             __syncwarp();
@@ -525,10 +551,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int n = n0 + j;
             if (n >= args.N || j >= gcols) break;
             if (n < args.Nv) {
-              if (args.outV_f32)
-                reinterpret_cast<float*>(args.outV)[(size_t)g * args.sVg + (size_t)mo * args.sVmo +
-                                                    (size_t)mi * args.sVmi + n] = v[j];
-              else
+              if (args.outV_f32) {
+                float* dst = reinterpret_cast<float*>(args.outV) + (size_t)g * args.sVg +
+                             (size_t)mo * args.sVmo + (size_t)mi * args.sVmi + n;
+                *dst = args.accum ? *dst + v[j] : v[j];
+              } else
                 reinterpret_cast<__nv_bfloat16*>(args.outV)[(size_t)g * args.sVg +
                                                             (size_t)mo * args.sVmo +
                                                             (size_t)mi * args.sVmi + n] =
@@ -568,13 +595,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-template <int BK, int STAGES, bool PAIR, bool COMB = false>
+template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0>
 static cudaError_t launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tW,
                                  const CUtensorMap& tV, const GemmArgs& a, int num_sms,
                                  cudaStream_t st) {
   using SM = GemmSmem<BK, STAGES, PAIR>;
   static_assert(SM::TOTAL <= 227 * 1024, "shared memory");
-  auto kern = gemm_kernel<BK, STAGES, PAIR, COMB>;
+  auto kern = gemm_kernel<BK, STAGES, PAIR, COMB, LAY>;
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
   if (e != cudaSuccess) return e;
@@ -603,6 +630,12 @@ cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUte
                         const GemmArgs& a, int bk, int num_sms, cudaStream_t st) {
   switch (bk) {
     case 64:
+      if (a.lay) {
+        if (!a.pair || a.cfirst) return cudaErrorInvalidValue;
+        if (a.lay == 1) return launch_gemm_t<64, 5, true, false, 1>(tA, tW, tV, a, num_sms, st);
+        if (a.lay == 2) return launch_gemm_t<64, 5, true, false, 2>(tA, tW, tV, a, num_sms, st);
+        return launch_gemm_t<64, 5, true, false, 3>(tA, tW, tV, a, num_sms, st);
+      }
       if (a.pair && a.cfirst) return launch_gemm_t<64, 5, true, true>(tA, tW, tV, a, num_sms, st);
       if (a.cfirst) return cudaErrorInvalidValue;
       if (a.pair) return launch_gemm_t<64, 5, true>(tA, tW, tV, a, num_sms, st);

@@ -163,8 +163,7 @@ def run_checks(log=print, ledger_dir=None):
         terr = max(errs.values())
         worst = max(worst, terr)
         log(f"rank {rank}/{tp} train step{' (head-split final)' if split else ''}: "
-              f"{len(errs)} grads, worst rel_err={terr:.3e} ({max(errs, key=errs.get)})",
-              flush=True)
+              f"{len(errs)} grads, worst rel_err={terr:.3e} ({max(errs, key=errs.get)})")
     # data parallel over the whole world (tp = 1, dp = N): every rank trains on
     # its own batch, gradients averaged by one bucketed all-reduce; check against the
     # average of the per-batch gradients computed locally without the dp group
