@@ -89,6 +89,65 @@ int dchag_gemm_combine(const void* ctx, int n_children, int R, int D, int H, con
                        const int* first, const int* count, int n_parents, int csplit,
                        void* out, void* stream);
 
+/* Level-0 backward in the augmented form the training step uses (dchag_l0_tgrad plus the
+ * bias and logit-weight terms): with x_c = [patch_c | 1] [tok.w[c]; tok.b[c] + chan_id[c]]
+ * (model.py:51-64), one launch per node writes the bf16 block TE (row stride te_ld):
+ *   TE[c*PP + k][d]      = sum_r patch_c[r][k] p_c[r][h(d)] G[r][d]     (d < D)
+ *   TE[ones0 + c][d]     = sum_r p_c[r][h(d)] G[r][d]
+ *   TE[c*PP + k][D + h]  = sum_r patch_c[r][k] dl_c[r][h]               (dlb given, h < H)
+ *   TE[ones0 + c][D + h] = sum_r dl_c[r][h]
+ * c = node-local channel; dlb = the node's bf16 [g][H][R] softmax-logit gradient
+ * (dchag_l0_softmax_bwd) or NULL (linear nodes). The ones column is a constant shared-memory
+ * operand atom (MMA N = 80). Other arguments as dchag_l0_tgrad; H <= 128. */
+int dchag_l0_tgrad_te(const void* patches, int cnt, int c0, int g, int R, int seq, int D,
+                      int H, int nh, int PP, const void* p, const float* mix, const void* G,
+                      const void* dlb, void* TE, long long te_ld, int ones0, void* stream);
+
+/* ---- training-step support (train.cu). Device tables are arrays of 8-byte fields. */
+
+/* fp32 -> bf16 of many tensors in one launch: jobs[i] = {src, dst, rows, cols, lds, ldd,
+ * trans, dst_f32} (int64 each; trans = 1 writes dst[c*ldd + r]; dst_f32 = 1 copies into an
+ * fp32 dst, trans must be 0); the per-step refresh of the bf16 operand copies of the fp32
+ * master weights. max_tiles = max over jobs of 32x32 tiles. */
+int dchag_cast_multi(const void* jobs, int n_jobs, int max_tiles, void* stream);
+
+/* Query fold of single_query nodes (layers.py:103-120): qp = q @ wq,
+ * U[d][h] = sum_{j in head h} wk[d][j] qp[j] / sqrt(D/H). jobs[i] = {wq, wk, q, U, ldU, qp,
+ * dU, dwk, dwq, dq} (fp32 device pointers / int64); writes U and qp. work: fp32
+ * [n_jobs][ceil(D/128)][D]. */
+int dchag_query_fold(const void* jobs, int n_jobs, int D, int H, float* work, void* stream);
+
+/* Backward of the query fold (tensor.py:395-413 through that chain): from dU (and the
+ * forward's qp) writes dwk, dwq [D][D] and dq [D]. work as dchag_query_fold, dqp fp32
+ * [n_jobs][D]. */
+int dchag_query_fold_bwd(const void* jobs, int n_jobs, int D, int H, float* work, float* dqp,
+                         void* stream);
+
+/* Periodic column sums: out[g][p][n] (+)= sum_{r = p, p+P, ... < R} X[g][r][n] (X fp32 if
+ * x_f32 else bf16, row stride ldx, group stride sxg; out fp32, group stride sog). Bias
+ * gradients (P = 1) and sums over the batch of [B*S] rows (P = S). Deterministic. work:
+ * fp32 [G][ceil(R/64)][N] when P == 1. */
+int dchag_colsum(const void* X, int x_f32, long long ldx, long long sxg, int G, int R, int N,
+                 int P, float* out, long long sog, int accumulate, float* work, void* stream);
+
+/* out[i] = sum_j X[i*ldx + j], j < N (fp32). */
+int dchag_rowsum(const float* X, long long ldx, int rows, int N, float* out, void* stream);
+
+/* Level-0 refold scatter (the training step refolds level 0 every step, fold.py's algebra):
+ * MT fp32 [n0][Dp][Kn] is the grouped GEMM product [Wv_n | U_n]^T x [tok.w rows ; tok.b +
+ * chan_id rows]^T of every level-0 node n (MT[n][d][l*PP + k] = (tok.w[c] Wv_n)[k][d] for
+ * node-local channel l of slab channel c, MT[n][d][gmax*PP + l] = ((tok.b + chan_id)[c] Wv_n)[d],
+ * rows D + h the logit weights). Writes the K_l0 operands Mt / Et (dchag_l0_node layouts),
+ * Mrow bf16 [C][D][PP] and Cb fp32 [C][D] (row-dot GEMM operand and bias), and for attention
+ * nodes WUt / bU (dchag_l0_logits layouts). With posVU (fp32 [n0][S][Dp] = pos [Wv_n | U_n])
+ * also posV0 bf16 [n0][S][D] (scaled by mixsum[n] for linear nodes) and posU fp32
+ * [n0][S][HP]. chan_node / chan_local / node_g: int32 device tables. */
+int dchag_l0_pack(const float* MT, int n0, int C, int C_pad, int D, int H, int HP, int PP,
+                  int gmax, int KE, int S, long long Dp, long long Kn, const int* chan_node,
+                  const int* chan_local, const int* node_g, void* Mt, void* Et, void* Mrow,
+                  float* Cb, void* WUt, float* bU, const float* posVU, const float* mixsum,
+                  void* posV0, float* posU, void* stream);
+
 /* Range guard of dchag_gemm_combine: *flag = 1 if any launch since the last reset saw a
  * partial child sum beyond +-1.68e7 (its fp16 x 2^8 running-sum range), else 0; reset != 0
  * clears it. Host-synchronous (reads a device symbol); not a kernel launch. */
@@ -133,11 +192,11 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
  * for the node's g channels, p = the node's block of the normalised dchag_l0_logits output
  * ([H/nh][g][R][nh] bf16), or dV[c] = mix[c] * G for linear nodes (mix != NULL). With posV
  * (fp32 [S][D], row r uses r % S) also Gpos[r][h] = sum_{d in head h} G[r][d] posV[r % S][d]
- * (fp32 [R][H]), the positional part of dp = G . V. G, dV bf16 [R][D] / [g][R][D], 16-byte
+ * (fp32 [R][H]), the positional part of dp = G . V; posV rows ldpos apart (0: D). G, dV bf16 [R][D] / [g][R][D], 16-byte
  * aligned; D/H a power of two in 8..256. dV == NULL computes Gpos only. */
 int dchag_l0_dv(int g, int R, int D, int H, int nh, const void* p, const float* mix,
-                const void* G, const float* posV, int period, float* Gpos, void* dV,
-                void* stream);
+                const void* G, const float* posV, long long ldpos, int period, float* Gpos,
+                void* dV, void* stream);
 
 /* ViT input tokens after the front end (model.py:100-108 apply_token_mask, :111-117 meta
  * token + concat): out[b][0] = meta_tok[b], out[b][1+s] = agg[b][s] (1 - mask[b][s]) +
@@ -216,6 +275,14 @@ int dchag_combine_bwd(int n_nodes, int R, int D, int H, const int* node_first, c
                       int max_g, const void* V, long long sVj, const float* L, long long sLj,
                       const float* mix, const float* G, float* dL, void* gV, float* dm,
                       void* stream);
+
+/* dchag_combine_bwd writing the K-concatenated operand of the training step's backward
+ * GEMMs: gVL child j row r at gVL + j*sGj + r*ldg holds [gV_j (D bf16) | dL_j (H bf16)]
+ * (attention) or gV_j (linear, with dm). ldg >= D + H, multiple of 8. */
+int dchag_combine_bwd_packed(int n_nodes, int R, int D, int H, const int* node_first,
+                             const int* node_g, int max_g, const void* V, long long sVj,
+                             const float* L, long long sLj, const float* mix, const float* G,
+                             void* gVL, long long sGj, long long ldg, float* dm, void* stream);
 
 /* unfold_patches (tensor.py:303-323): img [B][C][Himg][W] -> out [B][C][S][P*P] bf16. */
 int dchag_unfold(const void* img, long long img_sb, long long img_sc, int B, int C, int Himg,

@@ -34,8 +34,8 @@ SIGNATURES = {
                       c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp],
     "dchag_combine": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_vp, c_ll,
                       c_vp, c_vp, c_vp],
-    "dchag_l0_dv": [c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp,
-                    c_vp, c_vp],
+    "dchag_l0_dv": [c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_ll, c_int,
+                    c_vp, c_vp, c_vp],
     "dchag_vit_tokens": [c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp],
     "dchag_l0_tgrad": [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                        c_vp, c_vp, c_vp, c_vp, c_vp],
@@ -52,8 +52,21 @@ SIGNATURES = {
                               c_vp, c_ll, c_ll, c_int, c_vp, c_vp, c_vp],
     "dchag_combine_bwd": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_vp, c_ll,
                           c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
+    "dchag_combine_bwd_packed": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_vp,
+                                 c_ll, c_vp, c_vp, c_vp, c_ll, c_ll, c_vp, c_vp],
     "dchag_unfold": [c_vp, c_ll, c_ll, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp],
     "dchag_tile_weights": [c_vp, c_int, c_int, c_int, c_vp, c_vp],
+    "dchag_l0_tgrad_te": [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                          c_vp, c_vp, c_vp, c_vp, c_vp, c_ll, c_int, c_vp],
+    "dchag_l0_pack": [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                      c_int, c_ll, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                      c_vp, c_vp, c_vp, c_vp, c_vp],
+    "dchag_cast_multi": [c_vp, c_int, c_int, c_vp],
+    "dchag_query_fold": [c_vp, c_int, c_int, c_int, c_vp, c_vp],
+    "dchag_query_fold_bwd": [c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp],
+    "dchag_colsum": [c_vp, c_int, c_ll, c_ll, c_int, c_int, c_int, c_int, c_vp, c_ll, c_int,
+                     c_vp, c_vp],
+    "dchag_rowsum": [c_vp, c_ll, c_int, c_int, c_vp, c_vp],
     "dchag_num_sms": [],
     "dchag_combine_overflow": [c_vp, c_int],
 }

@@ -7,11 +7,11 @@ import sys
 from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["capi.cu", "gemm.cu", "l0.cu", "comb.cu", "wgrad.cu"]
+SOURCES = ["capi.cu", "gemm.cu", "l0.cu", "comb.cu", "train.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                  "-diag-suppress", "177"]
-LFLAGS = ARCH + ["-shared", "-cudart", "static"]
+LFLAGS = ARCH + ["-shared", "-cudart", "static", "-Xlinker", "--no-undefined"]
 
 
 def build(verbose: bool = False) -> str:

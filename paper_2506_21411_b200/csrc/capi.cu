@@ -102,6 +102,105 @@ const char* dchag_version(void) { return "dchag-b200 0.1.0 (sm_100a)"; }
 const char* dchag_last_error(void) { return g_err.c_str(); }
 int dchag_num_sms(void) { return num_sms_cached(); }
 
+int dchag_l0_tgrad_te(const void* patches, int cnt, int c0, int g, int R, int seq, int D,
+                      int H, int nh, int PP, const void* p, const float* mix, const void* G,
+                      const void* dlb, void* TE, long long te_ld, int ones0, void* stream) {
+  if (!mix && !p) return fail(DCHAG_ERR_SHAPE, "l0_tgrad_te: need p or mix");
+  if (H < 1 || H > 128 || D % H || D % 128 || R % 64 || seq % 64 || R % seq || PP != 64 ||
+      (D / H != 64 && D / H != 128) || (!mix && (nh < 2 || nh % 2 || H % nh)) || !TE ||
+      te_ld < D + (dlb ? H : 0) || te_ld % 8 ||
+      (reinterpret_cast<uintptr_t>(patches) | reinterpret_cast<uintptr_t>(G) |
+       reinterpret_cast<uintptr_t>(dlb)) % 16)
+    return fail(DCHAG_ERR_SHAPE, "l0_tgrad_te: bad shape R=%d S=%d D=%d H=%d PP=%d", R, seq, D,
+                H, PP);
+  L0TgradArgs a;
+  memset(&a, 0, sizeof(a));
+  a.patches = reinterpret_cast<const __nv_bfloat16*>(patches);
+  a.cnt = cnt; a.c0 = c0; a.g = g; a.R = R; a.S = seq; a.D = D; a.H = H; a.NH = nh; a.PP = PP;
+  a.p = reinterpret_cast<const __nv_bfloat16*>(p); a.mix = mix;
+  a.G = reinterpret_cast<const __nv_bfloat16*>(G);
+  a.TE = reinterpret_cast<__nv_bfloat16*>(TE); a.te_ld = te_ld; a.ones0 = ones0;
+  a.has_dl = dlb != nullptr;
+  const int B = R / seq;
+  CUtensorMap tG, tP, tDL;
+  cuuint64_t gd[2] = {(cuuint64_t)D, (cuuint64_t)R};
+  cuuint64_t gs[1] = {(cuuint64_t)D * 2};
+  cuuint32_t gb[2] = {64u, 64u};
+  int rc = make_map(&tG, G, 2, gd, gs, gb, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  cuuint64_t pd[3] = {64u, (cuuint64_t)seq, (cuuint64_t)B * cnt};
+  cuuint64_t ps[2] = {64u * 2, (cuuint64_t)seq * 64 * 2};
+  cuuint32_t pb[3] = {64u, 64u, 1u};
+  rc = make_map(&tP, patches, 3, pd, ps, pb, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  tDL = tG;
+  if (dlb) {
+    cuuint64_t dd[3] = {(cuuint64_t)R, (cuuint64_t)H, (cuuint64_t)g};
+    cuuint64_t ds[2] = {(cuuint64_t)R * 2, (cuuint64_t)R * H * 2};
+    cuuint32_t db[3] = {64u, 128u, 1u};
+    rc = make_map(&tDL, dlb, 3, dd, ds, db, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  return cuda_status(launch_l0_tgrad_te(tG, tP, tDL, a, S(stream)), "l0_tgrad_te");
+}
+
+int dchag_l0_pack(const float* MT, int n0, int C, int C_pad, int D, int H, int HP, int PP,
+                  int gmax, int KE, int seq, long long Dp, long long Kn, const int* chan_node,
+                  const int* chan_local, const int* node_g, void* Mt, void* Et, void* Mrow,
+                  float* Cb, void* WUt, float* bU, const float* posVU, const float* mixsum,
+                  void* posV0, float* posU, void* stream) {
+  if (!MT || n0 < 1 || C < 1 || C_pad < C || H < 1 || D % (2 * H) || ((D / H / 2) % 8) ||
+      PP % 8 || KE % 8 || Dp < D + (WUt ? H : 0) || Kn < (long long)gmax * PP + gmax ||
+      !chan_node || !chan_local || !node_g || !Mt || !Et || !Mrow || !Cb ||
+      (WUt && (!bU || HP < H)) || (posVU && !posV0))
+    return fail(DCHAG_ERR_SHAPE, "l0_pack: bad arguments");
+  L0PackArgs a;
+  memset(&a, 0, sizeof(a));
+  a.MT = MT; a.n0 = n0; a.C = C; a.C_pad = C_pad; a.D = D; a.H = H; a.HP = HP; a.PP = PP;
+  a.gmax = gmax; a.KE = KE; a.S = seq; a.Dp = Dp; a.Kn = Kn;
+  a.chan_node = chan_node; a.chan_local = chan_local; a.node_g = node_g;
+  a.Mt = reinterpret_cast<__nv_bfloat16*>(Mt); a.Et = reinterpret_cast<__nv_bfloat16*>(Et);
+  a.Mrow = reinterpret_cast<__nv_bfloat16*>(Mrow); a.Cb = Cb;
+  a.WUt = reinterpret_cast<__nv_bfloat16*>(WUt); a.bU = bU;
+  a.posVU = posVU; a.mixsum = mixsum; a.posV0 = reinterpret_cast<__nv_bfloat16*>(posV0);
+  a.posU = posU;
+  return cuda_status(launch_l0_pack(a, S(stream)), "l0_pack");
+}
+
+int dchag_cast_multi(const void* jobs, int n_jobs, int max_tiles, void* stream) {
+  if (n_jobs < 0 || (n_jobs && !jobs)) return fail(DCHAG_ERR_SHAPE, "cast_multi: bad table");
+  return cuda_status(launch_cast_multi(reinterpret_cast<const CastJob*>(jobs), n_jobs, max_tiles,
+                                       S(stream)), "cast_multi");
+}
+
+int dchag_query_fold(const void* jobs, int n_jobs, int D, int H, float* work, void* stream) {
+  if (n_jobs < 1 || !jobs || !work || H < 1 || D % H || (D / H) < 1)
+    return fail(DCHAG_ERR_SHAPE, "query_fold: bad arguments D=%d H=%d", D, H);
+  return cuda_status(launch_query_fold(reinterpret_cast<const QueryFoldJob*>(jobs), n_jobs, D, H,
+                                       work, S(stream)), "query_fold");
+}
+
+int dchag_query_fold_bwd(const void* jobs, int n_jobs, int D, int H, float* work, float* dqp,
+                         void* stream) {
+  if (n_jobs < 1 || !jobs || !work || !dqp || H < 1 || D % H)
+    return fail(DCHAG_ERR_SHAPE, "query_fold_bwd: bad arguments D=%d H=%d", D, H);
+  return cuda_status(launch_query_fold_bwd(reinterpret_cast<const QueryFoldJob*>(jobs), n_jobs, D,
+                                           H, work, dqp, S(stream)), "query_fold_bwd");
+}
+
+int dchag_colsum(const void* X, int x_f32, long long ldx, long long sxg, int G, int R, int N,
+                 int P, float* out, long long sog, int accumulate, float* work, void* stream) {
+  if (!X || !out || G < 1 || R < 1 || N < 1 || P < 1 || P > 65535 || (P == 1 && R > 64 && !work))
+    return fail(DCHAG_ERR_SHAPE, "colsum: bad arguments G=%d R=%d N=%d P=%d", G, R, N, P);
+  return cuda_status(launch_colsum(X, x_f32, ldx, sxg, G, R, N, P, out, sog, accumulate, work,
+                                   S(stream)), "colsum");
+}
+
+int dchag_rowsum(const float* X, long long ldx, int rows, int N, float* out, void* stream) {
+  if (!X || !out || rows < 1 || N < 1) return fail(DCHAG_ERR_SHAPE, "rowsum: bad arguments");
+  return cuda_status(launch_rowsum(X, ldx, rows, N, out, S(stream)), "rowsum");
+}
+
 int dchag_combine_overflow(int* flag, int reset) {
   if (!flag) return fail(DCHAG_ERR_SHAPE, "combine_overflow: null flag");
   return cuda_status(comb_overflow_flag(flag, reset), "combine_overflow");
@@ -416,18 +515,20 @@ int dchag_combine_strided(int n_nodes, int R, int D, int H, const int* node_firs
 }
 
 int dchag_l0_dv(int g, int R, int D, int H, int nh, const void* p, const float* mix,
-                const void* G, const float* posV, int period, float* Gpos, void* dV, void* stream) {
+                const void* G, const float* posV, long long ldpos, int period, float* Gpos,
+                void* dV, void* stream) {
   if (!mix && !p && dV) return fail(DCHAG_ERR_SHAPE, "l0_dv: need p or mix");
   if (!dV && !posV) return fail(DCHAG_ERR_SHAPE, "l0_dv: nothing to compute");
   const int dh = H > 0 ? D / H : 0;
   if (H < 1 || D % H || dh % 8 || dh > 256 || ((dh / 8) & (dh / 8 - 1)) ||
       ((long long)R * (D / 8)) % 32 || (!mix && (nh < 1 || H % nh)) ||
-      (posV && (!Gpos || period < 1 || R % period)) ||
+      (posV && (!Gpos || period < 1 || R % period || (ldpos && (ldpos < D || ldpos % 4)))) ||
       (reinterpret_cast<uintptr_t>(G) | reinterpret_cast<uintptr_t>(dV) |
        reinterpret_cast<uintptr_t>(posV)) % 16)
     return fail(DCHAG_ERR_SHAPE, "l0_dv: bad shape R=%d D=%d H=%d nh=%d", R, D, H, nh);
   return cuda_status(launch_l0_dv(g, R, D, H, nh, reinterpret_cast<const __nv_bfloat16*>(p), mix,
-                                  reinterpret_cast<const __nv_bfloat16*>(G), posV, period, Gpos,
+                                  reinterpret_cast<const __nv_bfloat16*>(G), posV, ldpos, period,
+                                  Gpos,
                                   reinterpret_cast<__nv_bfloat16*>(dV), S(stream)),
                      "l0_dv");
 }
@@ -541,12 +642,31 @@ int dchag_combine_bwd(int n_nodes, int R, int D, int H, const int* node_first, c
   if (!mix && (!L || !dL)) return fail(DCHAG_ERR_SHAPE, "combine_bwd: attention needs L and dL");
   if (mix && !dm) return fail(DCHAG_ERR_SHAPE, "combine_bwd: linear needs dm");
   CombineBwdArgs a;
+  memset(&a, 0, sizeof(a));
   a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H; a.max_g = max_g;
   a.node_first = node_first; a.node_g = node_g;
   a.V = reinterpret_cast<const __nv_bfloat16*>(V); a.sVj = sVj;
   a.L = L; a.sLj = sLj; a.mix = mix; a.G = G; a.dL = dL;
   a.gV = reinterpret_cast<__nv_bfloat16*>(gV); a.dm = dm;
   return cuda_status(launch_combine_bwd(a, S(stream)), "combine_bwd");
+}
+
+int dchag_combine_bwd_packed(int n_nodes, int R, int D, int H, const int* node_first,
+                             const int* node_g, int max_g, const void* V, long long sVj,
+                             const float* L, long long sLj, const float* mix, const float* G,
+                             void* gVL, long long sGj, long long ldg, float* dm, void* stream) {
+  if (!mix && !L) return fail(DCHAG_ERR_SHAPE, "combine_bwd_packed: attention needs L");
+  if (mix && !dm) return fail(DCHAG_ERR_SHAPE, "combine_bwd_packed: linear needs dm");
+  if (ldg < D + (mix ? 0 : H) || ldg % 8 || sGj < (long long)R * ldg)
+    return fail(DCHAG_ERR_SHAPE, "combine_bwd_packed: row stride %lld too small", ldg);
+  CombineBwdArgs a;
+  memset(&a, 0, sizeof(a));
+  a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H; a.max_g = max_g;
+  a.node_first = node_first; a.node_g = node_g;
+  a.V = reinterpret_cast<const __nv_bfloat16*>(V); a.sVj = sVj;
+  a.L = L; a.sLj = sLj; a.mix = mix; a.G = G; a.dL = nullptr;
+  a.gV = reinterpret_cast<__nv_bfloat16*>(gVL); a.dm = dm; a.sGj = sGj; a.ldg = ldg;
+  return cuda_status(launch_combine_bwd(a, S(stream)), "combine_bwd_packed");
 }
 
 int dchag_unfold(const void* img, long long img_sb, long long img_sc, int B, int C, int Himg,

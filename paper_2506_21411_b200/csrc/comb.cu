@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(256) l0_dv_kernel(int g, int R, int D, int H, 
                                                    const __nv_bfloat16* __restrict__ p,
                                                    const float* __restrict__ mix,
                                                    const __nv_bfloat16* __restrict__ G,
-                                                   const float* __restrict__ posV, int S,
+                                                   const float* __restrict__ posV,
+                                                   long long ldpos, int S,
                                                    float* __restrict__ Gpos,
                                                    __nv_bfloat16* __restrict__ out) {
   const int dchunks = D >> 3;
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(256) l0_dv_kernel(int g, int R, int D, int H, 
   const float gf[8] = {bf16lo(gv.x), bf16hi(gv.x), bf16lo(gv.y), bf16hi(gv.y),
                        bf16lo(gv.z), bf16hi(gv.z), bf16lo(gv.w), bf16hi(gv.w)};
   if (posV) {
-    const float4* pv = reinterpret_cast<const float4*>(posV + (size_t)(r % S) * D + d0);
+    const float4* pv = reinterpret_cast<const float4*>(posV + (size_t)(r % S) * ldpos + d0);
     const float4 a = __ldg(pv), b = __ldg(pv + 1);
     float acc = gf[0] * a.x + gf[1] * a.y + gf[2] * a.z + gf[3] * a.w +
                 gf[4] * b.x + gf[5] * b.y + gf[6] * b.z + gf[7] * b.w;
@@ -236,15 +237,16 @@ __global__ void __launch_bounds__(256) l0_dv_kernel(int g, int R, int D, int H, 
 }
 
 cudaError_t launch_l0_dv(int g, int R, int D, int H, int NH, const __nv_bfloat16* p,
-                         const float* mix, const __nv_bfloat16* G, const float* posV, int S,
-                         float* Gpos, __nv_bfloat16* out, cudaStream_t st) {
+                         const float* mix, const __nv_bfloat16* G, const float* posV,
+                         long long ldpos, int S, float* Gpos, __nv_bfloat16* out,
+                         cudaStream_t st) {
   const int dh = D / H;
   if (D % H || dh % 8 || dh > 256 || ((dh / 8) & (dh / 8 - 1)) || ((long long)R * (D / 8)) % 32 ||
       (!mix && (NH < 1 || H % NH)) || (posV && (!Gpos || S < 1)))
     return cudaErrorInvalidValue;
   const long long n = (long long)R * (D / 8);
-  l0_dv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, R, D, H, NH, p, mix, G, posV, S,
-                                                             Gpos, out);
+  l0_dv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, R, D, H, NH, p, mix, G, posV,
+                                                             ldpos > 0 ? ldpos : D, S, Gpos, out);
   return cudaGetLastError();
 }
 
@@ -706,7 +708,8 @@ __global__ void __launch_bounds__(128) combine_bwd_kernel(CombineBwdArgs a) {
   }
   for (int j = 0; j < g; ++j) {
     const __nv_bfloat16* vrow = a.V + (long long)(first + j) * a.sVj + (long long)r * a.D;
-    __nv_bfloat16* gvrow = a.gV + (long long)(first + j) * a.sVj + (long long)r * a.D;
+    __nv_bfloat16* gvrow = a.sGj ? a.gV + (long long)(first + j) * a.sGj + (long long)r * a.ldg
+                                 : a.gV + (long long)(first + j) * a.sVj + (long long)r * a.D;
     float dm_part = 0.f;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -744,9 +747,13 @@ __global__ void __launch_bounds__(128) combine_bwd_kernel(CombineBwdArgs a) {
   if (!a.mix && lane < H) {
     float s = 0.f;
     for (int j = 0; j < g; ++j) s += p[j * H + lane] * dp[j * H + lane];
-    for (int j = 0; j < g; ++j)
-      a.dL[(long long)(first + j) * a.sLj + (long long)r * H + lane] =
-          p[j * H + lane] * (dp[j * H + lane] - s);
+    for (int j = 0; j < g; ++j) {
+      const float v = p[j * H + lane] * (dp[j * H + lane] - s);
+      if (a.dL) a.dL[(long long)(first + j) * a.sLj + (long long)r * H + lane] = v;
+      if (a.sGj)
+        a.gV[(long long)(first + j) * a.sGj + (long long)r * a.ldg + a.D + lane] =
+            __float2bfloat16(v);
+    }
   }
 }
 

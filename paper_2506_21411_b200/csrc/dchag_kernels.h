@@ -139,6 +139,15 @@ struct L0TgradArgs {
   const float* mix;              // linear nodes: mix[g] (then p is unused)
   const __nv_bfloat16* G;        // [R][D] bf16
   float* T;                      // [g][PP][D] fp32
+  // TE mode (dchag_l0_tgrad_te): the augmented products, one bf16 block per node
+  //   TE[c*PP + k][d]      = T_c[k][d]                 (d < D)
+  //   TE[c*PP + k][D + h]  = E_c[k][h] = sum_r patch_c[r][k] dl_c[r][h]
+  //   TE[ones0 + c][d]     = sum_r p_c[r][h(d)] G[r][d]   (the bias row: colsum of dV_c)
+  //   TE[ones0 + c][D + h] = sum_r dl_c[r][h]
+  __nv_bfloat16* TE;
+  long long te_ld;               // row stride of TE (elements)
+  int ones0;                     // first bias row
+  int has_dl;                    // dl given (attention nodes): one extra CTA column for E
 };
 cudaError_t launch_l0_tgrad(const L0TgradArgs& a, cudaStream_t st);
 cudaError_t launch_l0_softmax_bwd(int g, int R, int H, int NH, int dh, const float* dpp,
@@ -148,12 +157,15 @@ cudaError_t launch_child_softmax(float* L, const int* first, const int* count, i
                                  int R, int H, cudaStream_t st);
 cudaError_t launch_l0_tgrad_tc(const CUtensorMap& tG, const CUtensorMap& tP,
                                const L0TgradArgs& a, cudaStream_t st);
+cudaError_t launch_l0_tgrad_te(const CUtensorMap& tG, const CUtensorMap& tP,
+                               const CUtensorMap& tDL, const L0TgradArgs& a, cudaStream_t st);
 cudaError_t launch_vit_tokens(const void* agg, int f32, const float* mask,
                               const float* mask_token, const float* meta_tok, void* out, int B,
                               int S, int D, cudaStream_t st);
 cudaError_t launch_l0_dv(int g, int R, int D, int H, int NH, const __nv_bfloat16* p,
-                         const float* mix, const __nv_bfloat16* G, const float* posV, int S,
-                         float* Gpos, __nv_bfloat16* out, cudaStream_t st);
+                         const float* mix, const __nv_bfloat16* G, const float* posV,
+                         long long ldpos, int S, float* Gpos, __nv_bfloat16* out,
+                         cudaStream_t st);
 
 // full_cross node weights (layers.py:125-138 folded): per (node, row), heads h:
 //   S^h = softmax_j(q_i,h . k_j,h / sqrt(dh)),  s_i = sum_h sum_j S^h_ij u_jh,
@@ -184,11 +196,67 @@ struct CombineBwdArgs {
   float* dL;                   // attention: [child][R][H]
   __nv_bfloat16* gV;           // [child][R][D]
   float* dm;                   // linear: [child][R] row dots g . V_j
+  // packed mode (the training step): gV child j row r at gV + j*sGj + r*ldg, and dL as bf16
+  // in the same row at column D + h (the K-concatenated operand [gV | dL] of the backward
+  // GEMMs); sGj = 0 keeps the V strides
+  long long sGj, ldg;
 };
 cudaError_t launch_combine_bwd(const CombineBwdArgs& a, cudaStream_t st);
 
 // images [B][C][H][W] -> patches [B][C][S][P*P] (bf16)
 cudaError_t launch_unfold(const __nv_bfloat16* img, long long img_sb, long long img_sc, int B,
                           int C, int Himg, int W, int P, __nv_bfloat16* out, cudaStream_t st);
+
+// ---- training-step support kernels (train.cu)
+struct CastJob {                 // dst (bf16) <- src (fp32): rows x cols of src
+  const float* src;
+  __nv_bfloat16* dst;
+  long long rows, cols, lds, ldd;
+  long long trans;               // 1: dst[c * ldd + r] = src[r * lds + c]
+  long long dst_f32;             // 1: dst is fp32 (a plain strided copy, e.g. stacked biases)
+};
+cudaError_t launch_cast_multi(const CastJob* jobs, int n_jobs, int max_tiles, cudaStream_t st);
+
+struct QueryFoldJob {            // one single_query node: U = fold(wq, wk, q) and its backward
+  const float* wq;
+  const float* wk;
+  const float* q;
+  float* U;                      // [D][ldU] (forward output)
+  long long ldU;
+  float* qp;                     // [D] q wq (written by the forward, read by the backward)
+  const float* dU;               // [D][ldU] (backward input)
+  float* dwk;                    // [D][D] (backward outputs)
+  float* dwq;
+  float* dq;                     // [D]
+};
+cudaError_t launch_query_fold(const QueryFoldJob* jobs, int n_jobs, int D, int H, float* part,
+                              cudaStream_t st);
+cudaError_t launch_query_fold_bwd(const QueryFoldJob* jobs, int n_jobs, int D, int H,
+                                  float* part, float* dqp, cudaStream_t st);
+cudaError_t launch_colsum(const void* X, int x_f32, long long ldx, long long sxg, int G, int R,
+                          int N, int P, float* out, long long sog, int accumulate, float* part,
+                          cudaStream_t st);
+cudaError_t launch_rowsum(const float* X, long long ldx, int rows, int N, float* out,
+                          cudaStream_t st);
+
+struct L0PackArgs {             // level-0 refold scatter (train.cu pack kernels)
+  const float* MT;              // [n0][Dp][Kn]
+  int n0, C, C_pad, D, H, HP, PP, gmax, KE, S;
+  long long Dp, Kn;
+  const int* chan_node;         // [C] node of slab channel c
+  const int* chan_local;        // [C] channel index inside its node
+  const int* node_g;            // [n0]
+  __nv_bfloat16* Mt;            // K_l0 tiled value weights
+  __nv_bfloat16* Et;            // K_l0 tiled bias blocks
+  __nv_bfloat16* Mrow;          // [C][D][PP] (row-dot GEMM operand)
+  float* Cb;                    // [C][D]
+  __nv_bfloat16* WUt;           // attention: [C][HP][PP]
+  float* bU;                    //            [C][HP]
+  const float* posVU;           // optional [n0][S][Dp] = pos [Wv | U]
+  const float* mixsum;          // linear nodes: [n0] sum of mix (posV scale), else null
+  __nv_bfloat16* posV0;         // [n0][S][D]
+  float* posU;                  // attention: [n0][S][HP]
+};
+cudaError_t launch_l0_pack(const L0PackArgs& a, cudaStream_t st);
 
 }  // namespace dchag

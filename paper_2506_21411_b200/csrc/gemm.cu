@@ -658,25 +658,39 @@ constexpr int TGC_A_BYTES = 2 * 64 * 64 * 2;    // two 64-column halves x 64 row
 constexpr int TGC_B_BYTES = 64 * 64 * 2;
 constexpr int TGC_STAGE = TGC_A_BYTES + TGC_B_BYTES;
 constexpr int TGC_SMEM = TGC_STAGES * TGC_STAGE + 1024 + 256;
+// TE mode: + one constant 64 x 64 B atom (column 0 = 1: the bias / colsum column, N = 80)
+constexpr int TGC_SMEM_TE = TGC_SMEM + TGC_B_BYTES;
 
+// TE = false: T_c (fp32) as above. TE = true (the training step's augmented form):
+//  * the B operand gets a second, constant MN atom whose first column is 1, so the MMA
+//    (N = 80) also produces the column sums sum_r A[r][m] in accumulator column 64;
+//  * CTA column x = D/128 (attention nodes) computes E_c^T = dl_c^T [patch_c | 1] with A =
+//    the node's bf16 dl [g][H][R] read K-major (rows h >= H zero-filled by TMA), unscaled;
+//  * the epilogue writes bf16 rows of the node's TE block (see L0TgradArgs).
+template <bool TE>
 __global__ void __launch_bounds__(192, 2)
     l0_tgrad_tc_kernel(const __grid_constant__ CUtensorMap tmG,
-                       const __grid_constant__ CUtensorMap tmP, L0TgradArgs a) {
+                       const __grid_constant__ CUtensorMap tmP,
+                       const __grid_constant__ CUtensorMap tmDL, L0TgradArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TGC_STAGES * TGC_STAGE);
+  uint8_t* ones = smem + TGC_STAGES * TGC_STAGE;   // TE: constant atom (1024-aligned)
+  uint64_t* full = reinterpret_cast<uint64_t*>(ones + (TE ? TGC_B_BYTES : 0));
   uint64_t* scaled = full + TGC_STAGES;
   uint64_t* empty = scaled + TGC_STAGES;
   uint64_t* done = empty + TGC_STAGES;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
   const int warp = warp_id(), lane = lane_id();
   const int c = blockIdx.y, d0 = blockIdx.x * 128;
+  const bool eblk = TE && d0 >= a.D;               // the E_c block (dl as A, K-major)
   const int nst = a.R / 64;
   const int dh = a.D / a.H;
+  constexpr uint32_t TCOLS = TE ? 128 : 64;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmG);
     tma_prefetch(&tmP);
+    if (TE) tma_prefetch(&tmDL);
     for (int s = 0; s < TGC_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&scaled[s], 4);
@@ -685,7 +699,16 @@ __global__ void __launch_bounds__(192, 2)
     mbar_init(done, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tslot, 64);
+  if (TE) {  // ones atom: element (row r, n = 0) = 1 sits in 16-byte chunk (r & 7) of row r
+    for (int i = threadIdx.x; i < TGC_B_BYTES / 16; i += blockDim.x) {
+      const int r = i >> 3, ch = i & 7;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (ch == (r & 7)) v.x = 0x3F80u;  // bf16 1.0 in the low half
+      *reinterpret_cast<uint4*>(ones + i * 16) = v;
+    }
+    fence_async_smem();
+  }
+  if (warp == 1) tmem_alloc(tslot, TCOLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -698,23 +721,30 @@ __global__ void __launch_bounds__(192, 2)
         uint8_t* sa = smem + s * TGC_STAGE;
         mbar_expect_tx(&full[s], TGC_STAGE);
         const int r0 = i * 64, b = r0 / a.S, s0 = r0 - b * a.S;
-        tma_load_2d(sa, &tmG, &full[s], d0, r0);
-        tma_load_2d(sa + TGC_A_BYTES / 2, &tmG, &full[s], d0 + 64, r0);
+        if (eblk) {
+          tma_load_3d(sa, &tmDL, &full[s], r0, 0, c);          // [128 h][64 r], K-major
+        } else {
+          tma_load_2d(sa, &tmG, &full[s], d0, r0);
+          tma_load_2d(sa + TGC_A_BYTES / 2, &tmG, &full[s], d0 + 64, r0);
+        }
         tma_load_3d(sa + TGC_A_BYTES, &tmP, &full[s], 0, s0, b * a.cnt + a.c0 + c);
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = idesc_bf16_f32(128, 64) | (1u << 15) | (1u << 16);
+    const uint32_t idesc = idesc_bf16_f32(128, TE ? 80 : 64) | (eblk ? 0u : (1u << 15)) |
+                           (1u << 16);
     for (int i = 0; i < nst; ++i) {
       const int s = i % TGC_STAGES;
       mbar_wait(&scaled[s], (i / TGC_STAGES) & 1);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t sa = smem_u32(smem + s * TGC_STAGE), sb = sa + TGC_A_BYTES;
+        const uint32_t lbo_b = TE ? smem_u32(ones) - sb : (uint32_t)TGC_B_BYTES;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t ad = smem_desc(sa + kk * 2048, TGC_A_BYTES / 2, 1024, 2u);
-          const uint64_t bd = smem_desc(sb + kk * 2048, TGC_B_BYTES, 1024, 2u);
+          const uint64_t ad = eblk ? smem_desc(sa + kk * 32, 16, 1024, 2u)
+                                   : smem_desc(sa + kk * 2048, TGC_A_BYTES / 2, 1024, 2u);
+          const uint64_t bd = smem_desc(sb + kk * 2048, lbo_b, 1024, 2u);
           mma_ss(tmem, ad, bd, idesc, (i | kk) != 0);
         }
         mma_commit(&empty[s]);
@@ -738,34 +768,37 @@ __global__ void __launch_bounds__(192, 2)
           a.p + ((size_t)(hg * a.g + c) * a.R + i * 64 + row) * a.NH + hn));
       return sel ? bf16hi(w) : bf16lo(w);
     };
-    float pn = pval(0);
+    float pn = eblk ? 0.f : pval(0);
     for (int i = 0; i < nst; ++i) {
       const int s = i % TGC_STAGES;
       const float pc = pn;
-      if (i + 1 < nst) pn = pval(i + 1);  // next stage's p in flight during this one
+      if (!eblk && i + 1 < nst) pn = pval(i + 1);  // next stage's p in flight during this one
       mbar_wait(&full[s], (i / TGC_STAGES) & 1);
-      const uint32_t rowaddr = smem_u32(smem + s * TGC_STAGE) + mh * (TGC_A_BYTES / 2) +
-                               (row >> 3) * 1024 + (row & 7) * 128;
-      // rows sit 128 B apart: visit the row's 16-byte chunks in a row-rotated order so the
-      // 8 rows of a swizzle atom hit 8 different bank groups (all chunks share one p)
-      uint32_t v[8][4];
+      if (!eblk) {
+        const uint32_t rowaddr = smem_u32(smem + s * TGC_STAGE) + mh * (TGC_A_BYTES / 2) +
+                                 (row >> 3) * 1024 + (row & 7) * 128;
+        // rows sit 128 B apart: visit the row's 16-byte chunks in a row-rotated order so the
+        // 8 rows of a swizzle atom hit 8 different bank groups (all chunks share one p)
+        uint32_t v[8][4];
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        const uint32_t ad = rowaddr + (((ch + row) & 7) << 4);
-        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v[ch][0]), "=r"(v[ch][1]), "=r"(v[ch][2]), "=r"(v[ch][3]) : "r"(ad));
+        for (int ch = 0; ch < 8; ++ch) {
+          const uint32_t ad = rowaddr + (((ch + row) & 7) << 4);
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(v[ch][0]), "=r"(v[ch][1]), "=r"(v[ch][2]), "=r"(v[ch][3])
+                       : "r"(ad));
+        }
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          const uint32_t ad = rowaddr + (((ch + row) & 7) << 4);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            v[ch][e] = pack_bf16(bf16lo(v[ch][e]) * pc, bf16hi(v[ch][e]) * pc);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ad), "r"(v[ch][0]),
+                       "r"(v[ch][1]), "r"(v[ch][2]), "r"(v[ch][3])
+                       : "memory");
+        }
+        fence_async_smem();  // generic-proxy writes -> visible to the tensor core
       }
-#pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        const uint32_t ad = rowaddr + (((ch + row) & 7) << 4);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          v[ch][e] = pack_bf16(bf16lo(v[ch][e]) * pc, bf16hi(v[ch][e]) * pc);
-        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ad), "r"(v[ch][0]),
-                     "r"(v[ch][1]), "r"(v[ch][2]), "r"(v[ch][3])
-                     : "memory");
-      }
-      fence_async_smem();  // generic-proxy writes -> visible to the tensor core
       __syncwarp();
       if (lane == 0) mbar_arrive(&scaled[s]);
     }
@@ -773,31 +806,63 @@ __global__ void __launch_bounds__(192, 2)
     mbar_wait(done, 0);
     tc_fence_after();
     const int q = warp & 3;
-    const int d = d0 + q * 32 + lane;
-    float* out = a.T + (size_t)c * 64 * a.D + d;
+    if constexpr (TE) {
+      const int m = q * 32 + lane;                          // d - d0, or h (E block)
+      const long long col = eblk ? (long long)a.D + m : (long long)d0 + m;
+      __nv_bfloat16* te = a.TE + col;
+      const bool live = !eblk || m < a.H;
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + half * 32, r);
+      for (int half = 0; half < 2; ++half) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + half * 32, r);
+        tmem_ld_wait();
+        if (live) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            te[(size_t)(c * a.PP + half * 32 + j) * a.te_ld] = __float2bfloat16(__uint_as_float(r[j]));
+        }
+      }
+      uint32_t r16[16];
+      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + 64, r16);
       tmem_ld_wait();
+      if (live) te[(size_t)(a.ones0 + c) * a.te_ld] = __float2bfloat16(__uint_as_float(r16[0]));
+    } else {
+      const int d = d0 + q * 32 + lane;
+      float* out = a.T + (size_t)c * 64 * a.D + d;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) out[(size_t)(half * 32 + j) * a.D] = __uint_as_float(r[j]);
+      for (int half = 0; half < 2; ++half) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + half * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) out[(size_t)(half * 32 + j) * a.D] = __uint_as_float(r[j]);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 64);
+    tmem_dealloc(tmem, TCOLS);
   }
 }
 
 cudaError_t launch_l0_tgrad_tc(const CUtensorMap& tG, const CUtensorMap& tP,
                                const L0TgradArgs& a, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(l0_tgrad_tc_kernel,
+  cudaError_t e = cudaFuncSetAttribute(l0_tgrad_tc_kernel<false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, TGC_SMEM);
   if (e != cudaSuccess) return e;
-  l0_tgrad_tc_kernel<<<dim3(a.D / 128, a.g), 192, TGC_SMEM, st>>>(tG, tP, a);
+  l0_tgrad_tc_kernel<false><<<dim3(a.D / 128, a.g), 192, TGC_SMEM, st>>>(tG, tP, tG, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_l0_tgrad_te(const CUtensorMap& tG, const CUtensorMap& tP,
+                               const CUtensorMap& tDL, const L0TgradArgs& a, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(l0_tgrad_tc_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, TGC_SMEM_TE);
+  if (e != cudaSuccess) return e;
+  l0_tgrad_tc_kernel<true><<<dim3(a.D / 128 + (a.has_dl ? 1 : 0), a.g), 192, TGC_SMEM_TE, st>>>(
+      tG, tP, tDL, a);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,386 @@
+// Training-step support kernels (the non-GEMM parts of the backward and of the per-step
+// weight preparation; every matrix product of the step runs on the tcgen05 GEMMs).
+//
+//   cast_multi      fp32 master weights -> bf16 operands (plain or transposed, strided /
+//                   padded destinations), every tensor of the step in one launch
+//   query_fold      U[:, h] = wk[:, h-blk] (q wq)[h-blk] / sqrt(dh)   (layers.py:103-120
+//                   with the input-independent query folded: logits = x U)
+//   query_fold_bwd  its backward: d wk, d wq, d q from dU (tensor.py:395-413 on that chain)
+//   colsum          periodic column sums: bias gradients (period 1, every row) and the
+//                   positional sums over the batch (period S), deterministic
+//   rowsum          row sums (the channel-softmax logit gradient summed over positions)
+#include "common.cuh"
+#include "dchag_kernels.h"
+
+namespace dchag {
+
+// ------------------------------------------------------------------------- cast_multi
+__global__ void __launch_bounds__(256) cast_multi_kernel(const CastJob* jobs, int n_jobs) {
+  const CastJob j = jobs[blockIdx.y];
+  const int tiles_c = (j.cols + 31) / 32;
+  const int tiles = ((j.rows + 31) / 32) * tiles_c;
+  __shared__ float tile[32][33];
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int r0 = (t / tiles_c) * 32, c0 = (t % tiles_c) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+    if (!j.trans) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = r0 + ty + 8 * k, c = c0 + tx;
+        if (r < j.rows && c < j.cols) {
+          const float v = __ldg(j.src + (size_t)r * j.lds + c);
+          if (j.dst_f32) reinterpret_cast<float*>(j.dst)[(size_t)r * j.ldd + c] = v;
+          else j.dst[(size_t)r * j.ldd + c] = __float2bfloat16(v);
+        }
+      }
+    } else {  // dst[c][r] = src[r][c] through a padded smem tile (both sides coalesced)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = r0 + ty + 8 * k, c = c0 + tx;
+        tile[ty + 8 * k][tx] = (r < j.rows && c < j.cols) ? j.src[(size_t)r * j.lds + c] : 0.f;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = c0 + ty + 8 * k, r = r0 + tx;
+        if (r < j.rows && c < j.cols)
+          j.dst[(size_t)c * j.ldd + r] = __float2bfloat16(tile[tx][ty + 8 * k]);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+cudaError_t launch_cast_multi(const CastJob* jobs, int n_jobs, int max_tiles, cudaStream_t st) {
+  if (n_jobs < 1) return cudaSuccess;
+  const int gx = max_tiles < 1024 ? max_tiles : 1024;
+  cast_multi_kernel<<<dim3(gx > 0 ? gx : 1, n_jobs), 256, 0, st>>>(jobs, n_jobs);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------- query_fold
+// phase 1: partial q wq over 128-row chunks of wq: part[node][chunk][j]
+constexpr int QF_CHUNK = 128;
+
+__global__ void qf_partial_kernel(const QueryFoldJob* jobs, int D, float* part) {
+  const QueryFoldJob jb = jobs[blockIdx.z];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i0 = blockIdx.y * QF_CHUNK;
+  if (j >= D) return;
+  float acc = 0.f;
+  for (int i = i0; i < min(D, i0 + QF_CHUNK); ++i) acc = fmaf(__ldg(jb.q + i), __ldg(jb.wq + (size_t)i * D + j), acc);
+  part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * D + j] = acc;
+}
+
+// phase 2: qp = sum of the partials (fixed order); U[d][h] = s sum_{j in h} wk[d][j] qp[j]
+__global__ void qf_final_kernel(const QueryFoldJob* jobs, int D, int H, int nchunk,
+                                const float* part) {
+  const QueryFoldJob jb = jobs[blockIdx.z];
+  extern __shared__ float qp_s[];
+  for (int j = threadIdx.x; j < D; j += blockDim.x) {
+    float a = 0.f;
+    for (int c = 0; c < nchunk; ++c) a += part[((size_t)blockIdx.z * nchunk + c) * D + j];
+    qp_s[j] = a;
+    if (blockIdx.x == 0 && jb.qp) jb.qp[j] = a;
+  }
+  __syncthreads();
+  const int dh = D / H;
+  const float s = rsqrtf((float)dh);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int d = blockIdx.x * nw + warp; d < D; d += gridDim.x * nw) {
+    const float* row = jb.wk + (size_t)d * D;
+    for (int h = 0; h < H; ++h) {
+      float a = 0.f;
+      for (int j = h * dh + lane; j < (h + 1) * dh; j += 32) a = fmaf(__ldg(row + j), qp_s[j], a);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (lane == 0) jb.U[(size_t)d * jb.ldU + h] = a * s;
+    }
+  }
+}
+
+cudaError_t launch_query_fold(const QueryFoldJob* jobs, int n_jobs, int D, int H, float* part,
+                              cudaStream_t st) {
+  const int nchunk = (D + QF_CHUNK - 1) / QF_CHUNK;
+  qf_partial_kernel<<<dim3((D + 127) / 128, nchunk, n_jobs), 128, 0, st>>>(jobs, D, part);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int smem = D * 4;
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(qf_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  qf_final_kernel<<<dim3(32, 1, n_jobs), 256, smem, st>>>(jobs, D, H, nchunk, part);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------- query_fold_bwd
+// With qp = q wq and U[d][h] = s sum_{j in h} wk[d][j] qp[j]:
+//   d wk[d][j] = s dU[d][h(j)] qp[j]
+//   d qp[j]    = s sum_d wk[d][j] dU[d][h(j)]
+//   d wq[i][j] = q[i] d qp[j],  d q[i] = sum_j wq[i][j] d qp[j]
+__global__ void qfb_partial_kernel(const QueryFoldJob* jobs, int D, int H, float* part) {
+  const QueryFoldJob jb = jobs[blockIdx.z];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int d0 = blockIdx.y * QF_CHUNK;
+  if (j >= D) return;
+  const int h = j / (D / H);
+  float acc = 0.f;
+  for (int d = d0; d < min(D, d0 + QF_CHUNK); ++d)
+    acc = fmaf(__ldg(jb.wk + (size_t)d * D + j), __ldg(jb.dU + (size_t)d * jb.ldU + h), acc);
+  part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * D + j] = acc;
+}
+
+__global__ void qfb_dqp_kernel(const QueryFoldJob* jobs, int D, int H, int nchunk,
+                               const float* part, float* dqp) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= D) return;
+  const float s = rsqrtf((float)(D / H));
+  float a = 0.f;
+  for (int c = 0; c < nchunk; ++c) a += part[((size_t)blockIdx.z * nchunk + c) * D + j];
+  dqp[(size_t)blockIdx.z * D + j] = a * s;
+}
+
+// one warp per row i: d wk row i, d wq row i, d q[i]
+__global__ void qfb_rows_kernel(const QueryFoldJob* jobs, int D, int H, const float* dqp_all) {
+  const QueryFoldJob jb = jobs[blockIdx.z];
+  const float* dqp = dqp_all + (size_t)blockIdx.z * D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int dh = D / H;
+  const float s = rsqrtf((float)dh);
+  for (int i = blockIdx.x * nw + warp; i < D; i += gridDim.x * nw) {
+    const float qi = __ldg(jb.q + i);
+    float dq = 0.f;
+    for (int j = lane; j < D; j += 32) {
+      const float g = dqp[j];
+      dq = fmaf(__ldg(jb.wq + (size_t)i * D + j), g, dq);
+      jb.dwq[(size_t)i * D + j] = qi * g;
+      jb.dwk[(size_t)i * D + j] = s * __ldg(jb.dU + (size_t)i * jb.ldU + j / dh) * __ldg(jb.qp + j);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dq += __shfl_xor_sync(0xffffffffu, dq, o);
+    if (lane == 0) jb.dq[i] = dq;
+  }
+}
+
+cudaError_t launch_query_fold_bwd(const QueryFoldJob* jobs, int n_jobs, int D, int H,
+                                  float* part, float* dqp, cudaStream_t st) {
+  const int nchunk = (D + QF_CHUNK - 1) / QF_CHUNK;
+  qfb_partial_kernel<<<dim3((D + 127) / 128, nchunk, n_jobs), 128, 0, st>>>(jobs, D, H, part);
+  qfb_dqp_kernel<<<dim3((D + 127) / 128, 1, n_jobs), 128, 0, st>>>(jobs, D, H, nchunk, part, dqp);
+  qfb_rows_kernel<<<dim3(64, 1, n_jobs), 256, 0, st>>>(jobs, D, H, dqp);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------- colsum
+// out[g][p][n] (+)= sum over rows r = p, p + P, ... < R of X[g][r][n]; X bf16 or fp32
+// (row stride ldx, group stride sxg). P == 1 takes two passes (partials over 64-row chunks,
+// then their sum in chunk order), P > 1 one (each output sums R / P rows): both
+// deterministic.
+template <typename T>
+DEV float ldf(const T* p);
+template <>
+DEV float ldf<float>(const float* p) { return __ldg(p); }
+template <>
+DEV float ldf<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+constexpr int CS_ROWS = 64;
+
+template <typename T>
+__global__ void colsum_direct_kernel(const T* X, long long ldx, long long sxg, int R, int N,
+                                     int P, float* out, long long sog, int accumulate) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = blockIdx.y, g = blockIdx.z;
+  if (n >= N) return;
+  const T* x = X + (size_t)g * sxg + n;
+  float a = 0.f;
+  for (int r = p; r < R; r += P) a += ldf(x + (size_t)r * ldx);
+  float* o = out + (size_t)g * sog + (size_t)p * N + n;
+  *o = accumulate ? *o + a : a;
+}
+
+template <typename T>
+__global__ void colsum_partial_kernel(const T* X, long long ldx, long long sxg, int R, int N,
+                                      float* part) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ch = blockIdx.y, g = blockIdx.z;
+  if (n >= N) return;
+  const T* x = X + (size_t)g * sxg + n;
+  float a = 0.f;
+  for (int r = ch * CS_ROWS; r < min(R, (ch + 1) * CS_ROWS); ++r) a += ldf(x + (size_t)r * ldx);
+  part[((size_t)g * gridDim.y + ch) * N + n] = a;
+}
+
+__global__ void colsum_final_kernel(const float* part, int nch, int N, float* out,
+                                    long long sog, int accumulate) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = blockIdx.z;
+  if (n >= N) return;
+  float a = 0.f;
+  for (int c = 0; c < nch; ++c) a += part[((size_t)g * nch + c) * N + n];
+  float* o = out + (size_t)g * sog + n;
+  *o = accumulate ? *o + a : a;
+}
+
+template <typename T>
+static cudaError_t colsum_t(const T* X, long long ldx, long long sxg, int G, int R, int N, int P,
+                            float* out, long long sog, int accumulate, float* part,
+                            cudaStream_t st) {
+  const dim3 blk(128);
+  if (P > 1 || R <= CS_ROWS) {
+    colsum_direct_kernel<T><<<dim3((N + 127) / 128, P, G), blk, 0, st>>>(X, ldx, sxg, R, N, P,
+                                                                         out, sog, accumulate);
+    return cudaGetLastError();
+  }
+  const int nch = (R + CS_ROWS - 1) / CS_ROWS;
+  colsum_partial_kernel<T><<<dim3((N + 127) / 128, nch, G), blk, 0, st>>>(X, ldx, sxg, R, N,
+                                                                          part);
+  colsum_final_kernel<<<dim3((N + 127) / 128, 1, G), blk, 0, st>>>(part, nch, N, out, sog,
+                                                                   accumulate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colsum(const void* X, int x_f32, long long ldx, long long sxg, int G, int R,
+                          int N, int P, float* out, long long sog, int accumulate, float* part,
+                          cudaStream_t st) {
+  if (x_f32)
+    return colsum_t(reinterpret_cast<const float*>(X), ldx, sxg, G, R, N, P, out, sog,
+                    accumulate, part, st);
+  return colsum_t(reinterpret_cast<const __nv_bfloat16*>(X), ldx, sxg, G, R, N, P, out, sog,
+                  accumulate, part, st);
+}
+
+// ------------------------------------------------------------------------- rowsum
+__global__ void rowsum_kernel(const float* X, long long ldx, int rows, int N, float* out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float* x = X + (size_t)warp * ldx;
+  float a = 0.f;
+  for (int j = lane; j < N; j += 32) a += x[j];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if (lane == 0) out[warp] = a;
+}
+
+cudaError_t launch_rowsum(const float* X, long long ldx, int rows, int N, float* out,
+                          cudaStream_t st) {
+  rowsum_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(X, ldx, rows, N, out);
+  return cudaGetLastError();
+}
+
+}  // namespace dchag
+
+namespace dchag {
+
+// ------------------------------------------------------------------------- level-0 pack
+// The training step refolds level 0 every step with one grouped GEMM,
+//   MT[n] = [Wv_n | U_n | 0]^T [tok.w rows of node n ; tok.b + chan_id rows ; 0]^T,
+// fp32 [n0][Dp][Kn]: MT[n][d][l*PP + k] = M_c[k][d] (c = c0_n + l), MT[n][d][gmax*PP + l] =
+// Cb_c[d], and rows D + h the logit weights (WU, bU). These kernels scatter it into the
+// operand layouts of K_p0 / K_l0 / the row-dot GEMM (fold.pack_rank's layouts).
+DEV long long tiled_off(int blk, int k, int n, int K, int N) {  // canonical K-major core mats
+  return (long long)blk * K * N + ((long long)(k >> 3) * (N >> 3) + (n >> 3)) * 64 +
+         (n & 7) * 8 + (k & 7);
+}
+
+__global__ void pack_mt_kernel(L0PackArgs a) {  // Mt [H*2][C_pad*PP][hw] tiled
+  const int hw = a.D / a.H / 2, K = a.C_pad * a.PP;
+  const long long total = (long long)a.H * 2 * K * hw;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int blk = (int)(t / ((long long)K * hw));
+    const int rem = (int)(t - (long long)blk * K * hw);
+    const int k = rem / hw, nn = rem - (rem / hw) * hw;
+    const int c = k / a.PP, kk = k - c * a.PP;
+    const int d = blk * hw + nn;  // blk = h * 2 + half
+    float v = 0.f;
+    if (c < a.C) {
+      const int n = __ldg(a.chan_node + c), l = __ldg(a.chan_local + c);
+      v = a.MT[((size_t)n * a.Dp + d) * a.Kn + l * a.PP + kk];
+    }
+    a.Mt[tiled_off(blk, k, nn, K, hw)] = __float2bfloat16(v);
+  }
+}
+
+__global__ void pack_rows_kernel(L0PackArgs a) {  // Mrow [C][D][PP] bf16, Cb [C][D] fp32
+  const long long total = (long long)a.C * a.D * (a.PP + 1);
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(t / ((long long)a.D * (a.PP + 1)));
+    const int rem = (int)(t - (long long)c * a.D * (a.PP + 1));
+    const int d = rem / (a.PP + 1), kk = rem - d * (a.PP + 1);
+    const int n = __ldg(a.chan_node + c), l = __ldg(a.chan_local + c);
+    const float* row = a.MT + ((size_t)n * a.Dp + d) * a.Kn;
+    if (kk < a.PP)
+      a.Mrow[((size_t)c * a.D + d) * a.PP + kk] = __float2bfloat16(row[l * a.PP + kk]);
+    else
+      a.Cb[(size_t)c * a.D + d] = row[a.gmax * a.PP + l];
+  }
+}
+
+__global__ void pack_et_kernel(L0PackArgs a) {  // Et [n0][H][2][KE][hw] tiled
+  const int hw = a.D / a.H / 2;
+  const long long per_node = (long long)a.H * 2 * a.KE * hw;
+  const long long total = per_node * a.n0;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)(t / per_node);
+    const long long rem0 = t - (long long)n * per_node;
+    const int hb = (int)(rem0 / ((long long)a.KE * hw));          // h * 2 + half
+    const int rem = (int)(rem0 - (long long)hb * a.KE * hw);
+    const int k = rem / hw, nn = rem - (rem / hw) * hw;
+    const int d = hb * hw + nn;
+    const float v = k < __ldg(a.node_g + n)
+                        ? a.MT[((size_t)n * a.Dp + d) * a.Kn + a.gmax * a.PP + k] : 0.f;
+    a.Et[(long long)n * per_node + tiled_off(hb, k, nn, a.KE, hw)] = __float2bfloat16(v);
+  }
+}
+
+__global__ void pack_logit_kernel(L0PackArgs a) {  // WUt [C][HP][PP] bf16, bU [C][HP] fp32
+  const long long total = (long long)a.C * a.HP * (a.PP + 1);
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(t / ((long long)a.HP * (a.PP + 1)));
+    const int rem = (int)(t - (long long)c * a.HP * (a.PP + 1));
+    const int h = rem / (a.PP + 1), kk = rem - h * (a.PP + 1);
+    const int n = __ldg(a.chan_node + c), l = __ldg(a.chan_local + c);
+    const float* row = a.MT + ((size_t)n * a.Dp + a.D + h) * a.Kn;
+    if (kk < a.PP)
+      a.WUt[((size_t)c * a.HP + h) * a.PP + kk] = __float2bfloat16(h < a.H ? row[l * a.PP + kk] : 0.f);
+    else
+      a.bU[(size_t)c * a.HP + h] = h < a.H ? row[a.gmax * a.PP + l] : 0.f;
+  }
+}
+
+// posVU fp32 [n0][S][Dp] (pos [Wv | U]) -> posV0 bf16 [n0][S][D] (x mixsum for linear
+// nodes), posU fp32 [n0][S][HP]
+__global__ void pack_pos_kernel(L0PackArgs a) {
+  const int W = a.D + a.HP;
+  const long long total = (long long)a.n0 * a.S * W;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long row = t / W;
+    const int col = (int)(t - row * W);
+    const float* src = a.posVU + row * a.Dp;
+    if (col < a.D) {
+      const int n = (int)(row / a.S);
+      const float sc = a.mixsum ? __ldg(a.mixsum + n) : 1.f;
+      a.posV0[row * a.D + col] = __float2bfloat16(src[col] * sc);
+    } else if (a.posU) {
+      const int h = col - a.D;
+      a.posU[row * a.HP + h] = h < a.H ? src[a.D + h] : 0.f;
+    }
+  }
+}
+
+cudaError_t launch_l0_pack(const L0PackArgs& a, cudaStream_t st) {
+  const int grid = 148 * 8;
+  pack_mt_kernel<<<grid, 256, 0, st>>>(a);
+  pack_rows_kernel<<<grid, 256, 0, st>>>(a);
+  pack_et_kernel<<<grid, 256, 0, st>>>(a);
+  if (a.WUt) pack_logit_kernel<<<grid, 256, 0, st>>>(a);
+  if (a.posVU) pack_pos_kernel<<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace dchag

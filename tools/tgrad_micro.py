@@ -25,7 +25,7 @@ def tg():
 
 
 def dvbmm():
-    _lib.call("dchag_l0_dv", g, R, D, H, NH, _lib.ptr(p), 0, _lib.ptr(G), _lib.ptr(posV), S,
+    _lib.call("dchag_l0_dv", g, R, D, H, NH, _lib.ptr(p), 0, _lib.ptr(G), _lib.ptr(posV), 0, S,
               _lib.ptr(Gpos), _lib.ptr(dV), st)
     torch.bmm(pt, dV, out_dtype=torch.float32)
 
