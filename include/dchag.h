@@ -136,14 +136,15 @@ int dchag_rowsum(const float* X, long long ldx, int rows, int N, float* out, voi
 /* Level-0 refold scatter (the training step refolds level 0 every step, fold.py's algebra):
  * MT fp32 [n0][Dp][Kn] is the grouped GEMM product [Wv_n | U_n]^T x [tok.w rows ; tok.b +
  * chan_id rows]^T of every level-0 node n (MT[n][d][l*PP + k] = (tok.w[c] Wv_n)[k][d] for
- * node-local channel l of slab channel c, MT[n][d][gmax*PP + l] = ((tok.b + chan_id)[c] Wv_n)[d],
+ * node-local channel l of slab channel c, MT[n][d][ones0 + l] = ((tok.b + chan_id)[c] Wv_n)[d] (ones0 >= gmax*PP),
  * rows D + h the logit weights). Writes the K_l0 operands Mt / Et (dchag_l0_node layouts),
  * Mrow bf16 [C][D][PP] and Cb fp32 [C][D] (row-dot GEMM operand and bias), and for attention
  * nodes WUt / bU (dchag_l0_logits layouts). With posVU (fp32 [n0][S][Dp] = pos [Wv_n | U_n])
  * also posV0 bf16 [n0][S][D] (scaled by mixsum[n] for linear nodes) and posU fp32
  * [n0][S][HP]. chan_node / chan_local / node_g: int32 device tables. */
 int dchag_l0_pack(const float* MT, int n0, int C, int C_pad, int D, int H, int HP, int PP,
-                  int gmax, int KE, int S, long long Dp, long long Kn, const int* chan_node,
+                  int gmax, int ones0, int KE, int S, long long Dp, long long Kn,
+                  const int* chan_node,
                   const int* chan_local, const int* node_g, void* Mt, void* Et, void* Mrow,
                   float* Cb, void* WUt, float* bU, const float* posVU, const float* mixsum,
                   void* posV0, float* posU, void* stream);

@@ -59,7 +59,7 @@ SIGNATURES = {
     "dchag_l0_tgrad_te": [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                           c_vp, c_vp, c_vp, c_vp, c_vp, c_ll, c_int, c_vp],
     "dchag_l0_pack": [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
-                      c_int, c_ll, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                      c_int, c_int, c_ll, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                       c_vp, c_vp, c_vp, c_vp, c_vp],
     "dchag_cast_multi": [c_vp, c_int, c_int, c_vp],
     "dchag_query_fold": [c_vp, c_int, c_int, c_int, c_vp, c_vp],

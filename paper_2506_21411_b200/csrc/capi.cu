@@ -145,19 +145,20 @@ int dchag_l0_tgrad_te(const void* patches, int cnt, int c0, int g, int R, int se
 }
 
 int dchag_l0_pack(const float* MT, int n0, int C, int C_pad, int D, int H, int HP, int PP,
-                  int gmax, int KE, int seq, long long Dp, long long Kn, const int* chan_node,
+                  int gmax, int ones0, int KE, int seq, long long Dp, long long Kn,
+                  const int* chan_node,
                   const int* chan_local, const int* node_g, void* Mt, void* Et, void* Mrow,
                   float* Cb, void* WUt, float* bU, const float* posVU, const float* mixsum,
                   void* posV0, float* posU, void* stream) {
   if (!MT || n0 < 1 || C < 1 || C_pad < C || H < 1 || D % (2 * H) || ((D / H / 2) % 8) ||
-      PP % 8 || KE % 8 || Dp < D + (WUt ? H : 0) || Kn < (long long)gmax * PP + gmax ||
+      PP % 8 || KE % 8 || Dp < D + (WUt ? H : 0) || ones0 < gmax * PP || Kn < ones0 + gmax ||
       !chan_node || !chan_local || !node_g || !Mt || !Et || !Mrow || !Cb ||
       (WUt && (!bU || HP < H)) || (posVU && !posV0))
     return fail(DCHAG_ERR_SHAPE, "l0_pack: bad arguments");
   L0PackArgs a;
   memset(&a, 0, sizeof(a));
   a.MT = MT; a.n0 = n0; a.C = C; a.C_pad = C_pad; a.D = D; a.H = H; a.HP = HP; a.PP = PP;
-  a.gmax = gmax; a.KE = KE; a.S = seq; a.Dp = Dp; a.Kn = Kn;
+  a.gmax = gmax; a.ones0 = ones0; a.KE = KE; a.S = seq; a.Dp = Dp; a.Kn = Kn;
   a.chan_node = chan_node; a.chan_local = chan_local; a.node_g = node_g;
   a.Mt = reinterpret_cast<__nv_bfloat16*>(Mt); a.Et = reinterpret_cast<__nv_bfloat16*>(Et);
   a.Mrow = reinterpret_cast<__nv_bfloat16*>(Mrow); a.Cb = Cb;

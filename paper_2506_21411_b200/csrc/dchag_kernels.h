@@ -242,6 +242,7 @@ cudaError_t launch_rowsum(const float* X, long long ldx, int rows, int N, float*
 struct L0PackArgs {             // level-0 refold scatter (train.cu pack kernels)
   const float* MT;              // [n0][Dp][Kn]
   int n0, C, C_pad, D, H, HP, PP, gmax, KE, S;
+  int ones0;                    // first tb row of a node block (MT column)
   long long Dp, Kn;
   const int* chan_node;         // [C] node of slab channel c
   const int* chan_local;        // [C] channel index inside its node

@@ -314,7 +314,7 @@ __global__ void pack_rows_kernel(L0PackArgs a) {  // Mrow [C][D][PP] bf16, Cb [C
     if (kk < a.PP)
       a.Mrow[((size_t)c * a.D + d) * a.PP + kk] = __float2bfloat16(row[l * a.PP + kk]);
     else
-      a.Cb[(size_t)c * a.D + d] = row[a.gmax * a.PP + l];
+      a.Cb[(size_t)c * a.D + d] = row[a.ones0 + l];
   }
 }
 
@@ -331,7 +331,7 @@ __global__ void pack_et_kernel(L0PackArgs a) {  // Et [n0][H][2][KE][hw] tiled
     const int k = rem / hw, nn = rem - (rem / hw) * hw;
     const int d = hb * hw + nn;
     const float v = k < __ldg(a.node_g + n)
-                        ? a.MT[((size_t)n * a.Dp + d) * a.Kn + a.gmax * a.PP + k] : 0.f;
+                        ? a.MT[((size_t)n * a.Dp + d) * a.Kn + a.ones0 + k] : 0.f;
     a.Et[(long long)n * per_node + tiled_off(hb, k, nn, a.KE, hw)] = __float2bfloat16(v);
   }
 }
@@ -348,7 +348,7 @@ __global__ void pack_logit_kernel(L0PackArgs a) {  // WUt [C][HP][PP] bf16, bU [
     if (kk < a.PP)
       a.WUt[((size_t)c * a.HP + h) * a.PP + kk] = __float2bfloat16(h < a.H ? row[l * a.PP + kk] : 0.f);
     else
-      a.bU[(size_t)c * a.HP + h] = h < a.H ? row[a.gmax * a.PP + l] : 0.f;
+      a.bU[(size_t)c * a.HP + h] = h < a.H ? row[a.ones0 + l] : 0.f;
   }
 }
 

@@ -5,7 +5,7 @@ each operand is read where it lies, K-major or MN-major (a transposed view such 
 `x.t()` is MN-major: no copy), with fp32 accumulation into an fp32 (optionally
 accumulating) or bf16 result. 2-D operands broadcast over the group dimension of a 3-D
 partner. Shapes outside the kernel's tiling rules (M % 128, K % 64, N % 16; MN-major
-operands M % 256 / N % 64) are zero-padded into scratch copies first -- only the small
+operands M % 256, MN-major B N % 64) are zero-padded into scratch copies first -- only the small
 test configurations need that; the benchmarked shapes run in place.
 """
 
@@ -60,7 +60,7 @@ def matmul(a, b, out=None, accumulate=False, out_dtype=torch.float32, bias=None,
     a_mn, lda = _layout(a3[0], 1)
     b_mn, ldb = _layout(b3[0].t(), 1)   # B_nt(n, k) = b[k][n]
     ok = (a_mn is not None and b_mn is not None and M % 128 == 0 and K % 64 == 0
-          and N % 16 == 0 and (not a_mn or M % 256 == 0) and (not b_mn or N % 64 == 0)
+          and N % 16 == 0 and (not (a_mn or b_mn) or M % 256 == 0) and (not b_mn or N % 64 == 0)
           and out_view.stride(-1) == 1
           and all((x * 2) % 16 == 0 for x in (lda, ldb, sAg, sBg))
           and a3.data_ptr() % 16 == 0 and b3.data_ptr() % 16 == 0)

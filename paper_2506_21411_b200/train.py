@@ -289,7 +289,7 @@ class DchagTrainer:
                work={"site": "prep:l0_fold_pos", "flops": 2 * n0 * st["S"] * D * Dp})
         attn = st["attn"]
         _lib.call("dchag_l0_pack", _ptr(st["MT"]), n0, C, st["C_pad"], D, H, st["HP"], st["PP"],
-                  st["gmax"], st["KE"], st["S"], Dp, Kn, _ptr(st["chan_node"]),
+                  st["gmax"], st["ones0"], st["KE"], st["S"], Dp, Kn, _ptr(st["chan_node"]),
                   _ptr(st["chan_local"]), _ptr(st["l0_g"]), _ptr(st["Mt"]), _ptr(st["Et"]),
                   _ptr(st["Mrow"]), _ptr(st["Cb"]), _ptr(st["WUt"]) if attn else 0,
                   _ptr(st["bU"]) if attn else 0, _ptr(st["posVU"]),
