@@ -355,6 +355,10 @@ def b200_arm(args, wl, tp, max_group):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    if world >= 4 and wl.get("train") and not args.no_graph:
+        # the graph-captured training step needs NVLS off at >= 4 ranks;
+        # must be set before the communicator is created
+        os.environ.setdefault("NCCL_NVLS_ENABLE", "0")
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B = args.batch or wl["batch"]

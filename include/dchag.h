@@ -123,12 +123,14 @@ int dchag_query_fold(const void* jobs, int n_jobs, int D, int H, float* work, vo
 int dchag_query_fold_bwd(const void* jobs, int n_jobs, int D, int H, float* work, float* dqp,
                          void* stream);
 
-/* Periodic column sums: out[g][p][n] (+)= sum_{r = p, p+P, ... < R} X[g][r][n] (X fp32 if
- * x_f32 else bf16, row stride ldx, group stride sxg; out fp32, group stride sog). Bias
- * gradients (P = 1) and sums over the batch of [B*S] rows (P = S). Deterministic. work:
- * fp32 [G][ceil(R/64)][N] when P == 1. */
+/* Periodic column sums: out[g][p][n] (+)= scale[g] * sum_{r = p, p+P, ... < R} X[g][r][n]
+ * (X fp32 if x_f32 else bf16, row stride ldx, group stride sxg; out fp32, or bf16 if
+ * out_bf16 (no accumulate), group stride sog, row stride ldo (0: N); gscale optional fp32
+ * [G]). Bias gradients (P = 1) and sums over the batch of [B*S] rows (P = S).
+ * Deterministic. work: fp32 [G][ceil(R/64)][N] when P == 1. */
 int dchag_colsum(const void* X, int x_f32, long long ldx, long long sxg, int G, int R, int N,
-                 int P, float* out, long long sog, int accumulate, float* work, void* stream);
+                 int P, void* out, long long sog, long long ldo, int out_bf16, int accumulate,
+                 const float* gscale, float* work, void* stream);
 
 /* out[i] = sum_j X[i*ldx + j], j < N (fp32). */
 int dchag_rowsum(const float* X, long long ldx, int rows, int N, float* out, void* stream);

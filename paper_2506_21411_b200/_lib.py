@@ -64,8 +64,8 @@ SIGNATURES = {
     "dchag_cast_multi": [c_vp, c_int, c_int, c_vp],
     "dchag_query_fold": [c_vp, c_int, c_int, c_int, c_vp, c_vp],
     "dchag_query_fold_bwd": [c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp],
-    "dchag_colsum": [c_vp, c_int, c_ll, c_ll, c_int, c_int, c_int, c_int, c_vp, c_ll, c_int,
-                     c_vp, c_vp],
+    "dchag_colsum": [c_vp, c_int, c_ll, c_ll, c_int, c_int, c_int, c_int, c_vp, c_ll, c_ll,
+                     c_int, c_int, c_vp, c_vp, c_vp],
     "dchag_rowsum": [c_vp, c_ll, c_int, c_int, c_vp, c_vp],
     "dchag_num_sms": [],
     "dchag_combine_overflow": [c_vp, c_int],

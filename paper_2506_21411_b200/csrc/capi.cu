@@ -190,11 +190,13 @@ int dchag_query_fold_bwd(const void* jobs, int n_jobs, int D, int H, float* work
 }
 
 int dchag_colsum(const void* X, int x_f32, long long ldx, long long sxg, int G, int R, int N,
-                 int P, float* out, long long sog, int accumulate, float* work, void* stream) {
-  if (!X || !out || G < 1 || R < 1 || N < 1 || P < 1 || P > 65535 || (P == 1 && R > 64 && !work))
+                 int P, void* out, long long sog, long long ldo, int out_bf16, int accumulate,
+                 const float* gscale, float* work, void* stream) {
+  if (!X || !out || G < 1 || R < 1 || N < 1 || P < 1 || P > 65535 ||
+      (P == 1 && R > 64 && !work) || (out_bf16 && accumulate))
     return fail(DCHAG_ERR_SHAPE, "colsum: bad arguments G=%d R=%d N=%d P=%d", G, R, N, P);
-  return cuda_status(launch_colsum(X, x_f32, ldx, sxg, G, R, N, P, out, sog, accumulate, work,
-                                   S(stream)), "colsum");
+  return cuda_status(launch_colsum(X, x_f32, ldx, sxg, G, R, N, P, out, sog, ldo, out_bf16,
+                                   accumulate, gscale, work, S(stream)), "colsum");
 }
 
 int dchag_rowsum(const float* X, long long ldx, int rows, int N, float* out, void* stream) {

@@ -767,30 +767,50 @@ cudaError_t launch_combine_bwd(const CombineBwdArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// images [B][C][H][W] (strided) -> patches [B][C][S][P*P]; one thread per patch row (py)
-__global__ void unfold_kernel(const __nv_bfloat16* img, long long sb, long long sc, int B, int C,
-                              int Himg, int W, int P, __nv_bfloat16* out) {
+// images [B][C][H][W] (strided) -> patches [B][C][S][P*P]: one CTA per (b, c, patch row):
+// the strip's P image rows are read with 16-byte coalesced loads into shared memory and its
+// wp*P*P outputs, one contiguous run, written back with 16-byte coalesced stores.
+__global__ void __launch_bounds__(256) unfold_kernel(const __nv_bfloat16* img, long long sb,
+                                                     long long sc, int B, int C, int Himg, int W,
+                                                     int P, __nv_bfloat16* out) {
+  extern __shared__ __align__(16) __nv_bfloat16 strip[];   // [P][W]
   const int hp = Himg / P, wp = W / P, S = hp * wp;
-  const long long total = (long long)B * C * S * P;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= total) return;
-  const int py = (int)(t % P);
-  long long rest = t / P;
-  const int s = (int)(rest % S);
-  rest /= S;
-  const int c = (int)(rest % C);
-  const int b = (int)(rest / C);
-  const int i = s / wp, j = s - i * wp;
-  const __nv_bfloat16* src = img + b * sb + c * sc + (long long)(i * P + py) * W + j * P;
-  __nv_bfloat16* dst = out + (((long long)b * C + c) * S + s) * P * P + py * P;
-  for (int px = 0; px < P; ++px) dst[px] = src[px];
+  const int i = blockIdx.x % hp;
+  const int bc = blockIdx.x / hp;
+  const int c = bc % C, b = bc / C;
+  const __nv_bfloat16* src = img + b * sb + c * sc + (long long)i * P * W;
+  const int n = P * W;                       // elements of the strip (multiple of 8)
+  for (int e = threadIdx.x * 8; e < n; e += blockDim.x * 8) {
+    const int py = e / W, x = e - py * W;
+    *reinterpret_cast<uint4*>(strip + e) =
+        __ldg(reinterpret_cast<const uint4*>(src + (long long)py * W + x));
+  }
+  __syncthreads();
+  __nv_bfloat16* dst = out + (((long long)b * C + c) * S + (long long)i * wp) * P * P;
+  for (int e = threadIdx.x * 8; e < n; e += blockDim.x * 8) {
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int o = e + q, j = o / (P * P), k = o - j * P * P;
+      v[q] = strip[(k / P) * W + j * P + (k % P)];
+    }
+    *reinterpret_cast<uint4*>(dst + e) = *reinterpret_cast<const uint4*>(v);
+  }
 }
 
 cudaError_t launch_unfold(const __nv_bfloat16* img, long long img_sb, long long img_sc, int B,
                           int C, int Himg, int W, int P, __nv_bfloat16* out, cudaStream_t st) {
-  const long long total = (long long)B * C * (Himg / P) * (W / P) * P;
-  const int grid = (int)((total + 255) / 256);
-  unfold_kernel<<<grid, 256, 0, st>>>(img, img_sb, img_sc, B, C, Himg, W, P, out);
+  if ((P * W) % 8 || W % 8 || (img_sb | img_sc) % 8 ||
+      (reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(out)) % 16)
+    return cudaErrorInvalidValue;
+  const int smem = P * W * 2;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(unfold_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  unfold_kernel<<<B * C * (Himg / P), 256, smem, st>>>(img, img_sb, img_sc, B, C, Himg, W, P,
+                                                        out);
   return cudaGetLastError();
 }
 

@@ -234,8 +234,8 @@ cudaError_t launch_query_fold(const QueryFoldJob* jobs, int n_jobs, int D, int H
 cudaError_t launch_query_fold_bwd(const QueryFoldJob* jobs, int n_jobs, int D, int H,
                                   float* part, float* dqp, cudaStream_t st);
 cudaError_t launch_colsum(const void* X, int x_f32, long long ldx, long long sxg, int G, int R,
-                          int N, int P, float* out, long long sog, int accumulate, float* part,
-                          cudaStream_t st);
+                          int N, int P, void* out, long long sog, long long ldo, int out_bf16,
+                          int accumulate, const float* gscale, float* part, cudaStream_t st);
 cudaError_t launch_rowsum(const float* X, long long ldx, int rows, int N, float* out,
                           cudaStream_t st);
 

@@ -20,6 +20,22 @@ __global__ void __launch_bounds__(256) cast_multi_kernel(const CastJob* jobs, in
   const int tiles_c = (j.cols + 31) / 32;
   const int tiles = ((j.rows + 31) / 32) * tiles_c;
   __shared__ float tile[32][33];
+  const bool vec = !j.trans && !j.dst_f32 && j.cols % 4 == 0 && j.lds % 4 == 0 &&
+                   j.ldd % 4 == 0 && ((reinterpret_cast<uintptr_t>(j.src) |
+                                       reinterpret_cast<uintptr_t>(j.dst)) & 15) == 0;
+  if (vec) {  // 16-byte loads, 8-byte stores, grid-stride over the job
+    const long long c4 = j.cols / 4, n = j.rows * c4;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+      const long long r = i / c4, c = (i - r * c4) * 4;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(j.src + r * j.lds + c));
+      uint2 o;
+      o.x = pack_bf16(v.x, v.y);
+      o.y = pack_bf16(v.z, v.w);
+      *reinterpret_cast<uint2*>(j.dst + r * j.ldd + c) = o;
+    }
+    return;
+  }
   for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
     const int r0 = (t / tiles_c) * 32, c0 = (t % tiles_c) * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
@@ -186,17 +202,33 @@ DEV float ldf<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*
 
 constexpr int CS_ROWS = 64;
 
+struct ColsumOut {               // where / how a column sum is written
+  void* out;
+  long long sog, ldo;            // group stride, row stride (periodic sums)
+  int bf16, accumulate;
+  const float* gscale;           // optional per-group scale
+  DEV void put(int g, int p, int n, float a) const {
+    if (gscale) a *= __ldg(gscale + g);
+    const size_t o = (size_t)g * sog + (size_t)p * ldo + n;
+    if (bf16) {
+      reinterpret_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16(a);
+    } else {
+      float* f = reinterpret_cast<float*>(out) + o;
+      *f = accumulate ? *f + a : a;
+    }
+  }
+};
+
 template <typename T>
 __global__ void colsum_direct_kernel(const T* X, long long ldx, long long sxg, int R, int N,
-                                     int P, float* out, long long sog, int accumulate) {
+                                     int P, ColsumOut o) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   const int p = blockIdx.y, g = blockIdx.z;
   if (n >= N) return;
   const T* x = X + (size_t)g * sxg + n;
   float a = 0.f;
   for (int r = p; r < R; r += P) a += ldf(x + (size_t)r * ldx);
-  float* o = out + (size_t)g * sog + (size_t)p * N + n;
-  *o = accumulate ? *o + a : a;
+  o.put(g, p, n, a);
 }
 
 template <typename T>
@@ -211,43 +243,38 @@ __global__ void colsum_partial_kernel(const T* X, long long ldx, long long sxg, 
   part[((size_t)g * gridDim.y + ch) * N + n] = a;
 }
 
-__global__ void colsum_final_kernel(const float* part, int nch, int N, float* out,
-                                    long long sog, int accumulate) {
+__global__ void colsum_final_kernel(const float* part, int nch, int N, ColsumOut o) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   const int g = blockIdx.z;
   if (n >= N) return;
   float a = 0.f;
   for (int c = 0; c < nch; ++c) a += part[((size_t)g * nch + c) * N + n];
-  float* o = out + (size_t)g * sog + n;
-  *o = accumulate ? *o + a : a;
+  o.put(g, 0, n, a);
 }
 
 template <typename T>
 static cudaError_t colsum_t(const T* X, long long ldx, long long sxg, int G, int R, int N, int P,
-                            float* out, long long sog, int accumulate, float* part,
-                            cudaStream_t st) {
+                            const ColsumOut& o, float* part, cudaStream_t st) {
   const dim3 blk(128);
   if (P > 1 || R <= CS_ROWS) {
     colsum_direct_kernel<T><<<dim3((N + 127) / 128, P, G), blk, 0, st>>>(X, ldx, sxg, R, N, P,
-                                                                         out, sog, accumulate);
+                                                                         o);
     return cudaGetLastError();
   }
   const int nch = (R + CS_ROWS - 1) / CS_ROWS;
   colsum_partial_kernel<T><<<dim3((N + 127) / 128, nch, G), blk, 0, st>>>(X, ldx, sxg, R, N,
                                                                           part);
-  colsum_final_kernel<<<dim3((N + 127) / 128, 1, G), blk, 0, st>>>(part, nch, N, out, sog,
-                                                                   accumulate);
+  colsum_final_kernel<<<dim3((N + 127) / 128, 1, G), blk, 0, st>>>(part, nch, N, o);
   return cudaGetLastError();
 }
 
 cudaError_t launch_colsum(const void* X, int x_f32, long long ldx, long long sxg, int G, int R,
-                          int N, int P, float* out, long long sog, int accumulate, float* part,
-                          cudaStream_t st) {
+                          int N, int P, void* out, long long sog, long long ldo, int out_bf16,
+                          int accumulate, const float* gscale, float* part, cudaStream_t st) {
+  ColsumOut o{out, sog, ldo > 0 ? ldo : N, out_bf16, accumulate, gscale};
   if (x_f32)
-    return colsum_t(reinterpret_cast<const float*>(X), ldx, sxg, G, R, N, P, out, sog,
-                    accumulate, part, st);
-  return colsum_t(reinterpret_cast<const __nv_bfloat16*>(X), ldx, sxg, G, R, N, P, out, sog,
-                  accumulate, part, st);
+    return colsum_t(reinterpret_cast<const float*>(X), ldx, sxg, G, R, N, P, o, part, st);
+  return colsum_t(reinterpret_cast<const __nv_bfloat16*>(X), ldx, sxg, G, R, N, P, o, part, st);
 }
 
 // ------------------------------------------------------------------------- rowsum

@@ -27,7 +27,7 @@ backward  per level, top down (grouped over the level's nodes where shapes agree
             G = g_y wo^T, the positional dp (dchag_l0_dv), dp = G . V_c by the row-dot GEMM,
             the channel-softmax backward, then ONE kernel per node gives
             TE = [patch | 1]^T [p G | dl] (dchag_l0_tgrad_te) and two grouped GEMMs finish:
-              [d Wv | d U] = [tok.w ; tb]^T TE + pos^T Gs,   d [tok.w ; tb] = TE [Wv | U]^T
+              [d Wv | d U] = [tok.w ; tb ; pos]^T [TE ; Gs],  d [tok.w ; tb ; pos] = [TE ; Gs] [Wv | U]^T
           and d wk / d wq / d q from d U (dchag_query_fold_bwd, batched over every node).
 """
 
@@ -121,7 +121,9 @@ class DchagTrainer:
         st["WvUt"] = torch.zeros(nall, D + H, D, **bf)   # [wv | U]^T (levels >= 1, final)
         st["wo16"] = torch.zeros(nall, D, D, **bf)
         st["bo32"] = torch.zeros(nall, D, **f32)         # bo (linear nodes: b)
-        st["Waug"] = torch.zeros(n0, Kn, D, **bf)        # [tok.w rows ; tb rows ; 0]
+        # [tok.w rows ; tb rows ; 0 ; pos rows]: rows Kn.. carry pos, so the level-0 weight
+        # gradient GEMMs also give pos^T Gs_n and Gs_n Wv_n^T (the positional terms)
+        st["Waug"] = torch.zeros(n0, Kn + S, D, **bf)
         st["pos16"] = torch.zeros(S, D, **bf)
         st["tb32"] = torch.zeros(C, D, **f32)
         st["U"] = torch.zeros(nall, D, H, **f32)
@@ -132,7 +134,7 @@ class DchagTrainer:
         st["dwk"] = torch.zeros(nall, D, D, **f32)
         st["dwq"] = torch.zeros(nall, D, D, **f32)
         st["dq"] = torch.zeros(nall, D, **f32)
-        st["TE"] = torch.zeros(n0, Kn, Dp, **bf)
+        st["TE"] = torch.zeros(n0, Kn + S, Dp, **bf)      # [T | E ; colV | coll ; 0 ; Gs | 0]
         # level-0 folded operands of K_p0 / K_l0 / the row-dot GEMM
         C_pad = C + 64 // PP
         KE = 16 * ((gmax + 15) // 16)
@@ -166,9 +168,9 @@ class DchagTrainer:
         st["chan_node"] = self._dev_ints(chan_node, torch.int32, dev)
         st["chan_local"] = self._dev_ints(chan_local, torch.int32, dev)
         # row indices of d tok.w / d tb inside the level-0 blocks
-        rows_w = [n * Kn + l * PP + kk for n, g in enumerate(levels[0]) for l in range(g)
+        rows_w = [n * (Kn + S) + l * PP + kk for n, g in enumerate(levels[0]) for l in range(g)
                   for kk in range(PP)]
-        rows_b = [n * Kn + ones0 + l for n, g in enumerate(levels[0]) for l in range(g)]
+        rows_b = [n * (Kn + S) + ones0 + l for n, g in enumerate(levels[0]) for l in range(g)]
         st["rows_w"] = torch.tensor(rows_w, device=dev, dtype=torch.int64)
         st["rows_b"] = torch.tensor(rows_b, device=dev, dtype=torch.int64)
         # per-level combine tables
@@ -219,6 +221,8 @@ class DchagTrainer:
             job(tokw[off + c0], st["Waug"][n], g * PP, D, D, D)
             job(st["tb32"][c0], st["Waug"][n, st["ones0"]:], g, D, D, D)
         job(w["special.pos"], st["pos16"], st["S"], D, D, D)
+        for n in range(st["n0"]):
+            job(w["special.pos"], st["Waug"][n, st["Kn"]:], st["S"], D, D, D)
         if fe.strategy.final_layer_tp_split and fe.tp > 1:
             self._head_split_buffers(job)
         tab = torch.tensor(jobs, dtype=torch.int64).to(fe.device)
@@ -283,7 +287,7 @@ class DchagTrainer:
             torch.stack([w[f"{nd.name}.mix"].float().sum() for nd in st["lvl"][0]],
                         out=st["mixsum"])
         # level-0 refold: MT_n = [Wv_n | U_n]^T Waug_n^T  and  pos [Wv_n | U_n]
-        matmul(st["WvU"][:n0].transpose(1, 2), st["Waug"].transpose(1, 2), out=st["MT"],
+        matmul(st["WvU"][:n0].transpose(1, 2), st["Waug"][:, :Kn].transpose(1, 2), out=st["MT"],
                work={"site": "prep:l0_fold", "flops": 2 * n0 * Dp * D * Kn})
         matmul(st["pos16"], st["WvU"][:n0], out=st["posVU"],
                work={"site": "prep:l0_fold_pos", "flops": 2 * n0 * st["S"] * D * Dp})
@@ -323,14 +327,15 @@ class DchagTrainer:
         return GraphedStep(graph, out, grads, _lib.LAUNCH_COUNT["n"] - n0)
 
     # ---------------------------------------------------------------- forward
-    def _proj_logits(self, A, rows, Wt, Nv, Nl, V, L, site):
-        """[V | L] = A W with the K_gemm logit split (bf16 V, fp32 L); Wt = W^T bf16."""
+    def _proj_logits(self, A, rows, Wt, Nv, Nl, V, L, site, G=1):
+        """[V | L] = A W with the K_gemm logit split (bf16 V, fp32 L); Wt = W^T bf16. G > 1:
+        G groups of `rows` rows, A / Wt / V / L with consecutive group blocks."""
         D = self._st["D"]
         N = Nv + Nl
-        _lib.call("dchag_gemm_bf16", _ptr(A), 1, 1, rows, D, rows * D, 0, D, _ptr(Wt), N, N * D,
-                  Nv, _ptr(self._st["zero_b"]), N, 0, 0, 0, 1, _ptr(V), 0, 0, 0, Nv, _ptr(L), 0,
-                  0, Nl, _lib.stream_handle(),
-                  work={"site": site, "flops": 2 * rows * D * N})
+        _lib.call("dchag_gemm_bf16", _ptr(A), G, 1, rows, D, rows * D, 0, D, _ptr(Wt), N, N * D,
+                  Nv, _ptr(self._st["zero_b"]), 0, 0, 0, 0, 1, _ptr(V), 0, rows * Nv, 0, Nv,
+                  _ptr(L), rows * Nl, 0, Nl, _lib.stream_handle(),
+                  work={"site": site, "flops": 2 * G * rows * D * N})
 
     def forward_local(self, images):
         """prep + slab tokenizer + tree of this rank up to its root stream (saved['y_root'])."""
@@ -426,7 +431,13 @@ class DchagTrainer:
         nprev = y_prev.shape[0]
         V = torch.empty(nprev, R, D, device=y_prev.device, dtype=torch.bfloat16)
         L = torch.empty(nprev, R, H, device=y_prev.device) if st["attn"] else None
-        for nd in nodes:
+        uniform = (len({nd.g for nd in nodes}) == 1 and st["attn"]
+                   and nodes[-1].first + nodes[-1].g == nprev)
+        if uniform:  # equal fan-in: the whole level in one grouped launch
+            g, k0 = nodes[0].g, nodes[0].k
+            self._proj_logits(y_prev, g * R, st["WvUt"][k0], D, H, V, L, f"fwd:vl_l{li}",
+                              G=len(nodes))
+        for nd in ([] if uniform else nodes):
             A = y_prev[nd.first:nd.first + nd.g].reshape(nd.g * R, D)
             if st["attn"]:
                 self._proj_logits(A, nd.g * R, st["WvUt"][nd.k], D, H,
@@ -508,14 +519,15 @@ class DchagTrainer:
         return out.view(B, 1, fe.seq, D)
 
     # ---------------------------------------------------------------- backward
-    def _colsum(self, X, G, R, N, out, period=1, accumulate=0):
-        """out[g] (+)= periodic column sums of X[g] (bf16 or fp32), rows X.stride(-2) apart."""
+    def _colsum(self, X, G, R, N, out, period=1, accumulate=0, ldo=0, gscale=None):
+        """out[g] (+)= periodic column sums of X[g] (bf16 or fp32), rows X.stride(-2) apart;
+        out fp32, or bf16 (rows ldo apart) for a bf16 GEMM operand."""
         sxg = X.stride(0) if X.dim() == 3 else 0
         work = torch.empty(G * (-(-R // 64)) * N, device=X.device) if period == 1 else None
         sog = out.stride(0) if out.dim() >= 2 and G > 1 else 0
         _lib.call("dchag_colsum", _ptr(X), int(X.dtype == torch.float32), X.stride(-2), sxg, G,
-                  R, N, period, _ptr(out), sog, accumulate, _lib.ptr(work),
-                  _lib.stream_handle(),
+                  R, N, period, _ptr(out), sog, ldo, int(out.dtype == torch.bfloat16),
+                  accumulate, _lib.ptr(gscale), _lib.ptr(work), _lib.stream_handle(),
                   work={"site": "bwd:colsum", "bytes": X.numel() * X.element_size()})
         return out
 
@@ -725,15 +737,30 @@ class DchagTrainer:
             dm = torch.empty(V.shape[0], R, device=V.device)
         gVL = self._combine_bwd(V, L, mix, G, st["comb"][li], R, V.shape[0], dm=dm, tag=li)
         g_prev = torch.empty(y_prev.shape, device=y_prev.device, dtype=torch.bfloat16)
-        for nd in nodes:
+        gs = {nd.g for nd in nodes}
+        if len(gs) == 1 and nodes[-1].first + nodes[-1].g == y_prev.shape[0]:
+            # equal fan-in: one grouped launch per product for the whole level
+            g = nodes[0].g
+            Y = y_prev.view(n, g * R, D)
+            gv = gVL.view(n, g * R, Dp)
+            matmul(Y.transpose(1, 2), gv, out=st["dWvU"][k0:k0 + n],
+                   work={"site": f"bwd:dwvu_l{li}", "flops": 2 * n * g * R * D * Dp})
+            matmul(gv, st["WvU"][k0:k0 + n].transpose(1, 2), out=g_prev.view(n, g * R, D),
+                   work={"site": f"bwd:gprev_l{li}", "flops": 2 * n * g * R * Dp * D})
+            groups = []
+        else:
+            groups = nodes
+        for nd in groups:
             f0, g = nd.first, nd.g
             Y = y_prev[f0:f0 + g].reshape(g * R, D)
             gv = gVL[f0:f0 + g].reshape(g * R, Dp)
             matmul(Y.t(), gv, out=st["dWvU"][nd.k],
                    work={"site": f"bwd:dwvu_l{li}", "flops": 2 * g * R * D * Dp})
-            grads[f"{nd.name}.{'wv' if attn else 'w'}"] = st["dWvU"][nd.k, :, :D]
             matmul(gv, st["WvU"][nd.k].t(), out=g_prev[f0:f0 + g].view(g * R, D),
                    work={"site": f"bwd:gprev_l{li}", "flops": 2 * g * R * Dp * D})
+        for nd in nodes:
+            f0, g = nd.first, nd.g
+            grads[f"{nd.name}.{'wv' if attn else 'w'}"] = st["dWvU"][nd.k, :, :D]
             if not attn:
                 dmix = torch.empty(g, device=V.device)
                 _lib.call("dchag_rowsum", _ptr(dm[f0:f0 + g]), R, g, R, _ptr(dmix),
@@ -773,14 +800,14 @@ class DchagTrainer:
                       _ptr(st["l0_c0"]), _ptr(st["l0_g"]), _ptr(saved["poff"]),
                       _ptr(st["WUt"]), _ptr(st["bU"]), _ptr(st["posU"]), _ptr(pnorm), 0, sh,
                       work={"site": "bwd:l0_logits", "flops": 2 * 2 * R * cnt * PP * H})
-        # positional sums over the batch: Gs_n[s] = sum_b G_n[b, s]  (x sum(mix), linear)
-        Gs = self._colsum(Gb, n0, R, D, torch.empty(n0, S, D, device=dev), period=S)
-        if not attn:
-            Gs.mul_(st["mixsum"].view(n0, 1, 1))
+        # positional sums over the batch, Gs_n[s] = sum_b G_n[b, s] (x sum(mix), linear),
+        # straight into the pos rows of the node's TE block (bf16 GEMM operand)
+        TE = st["TE"]
+        self._colsum(Gb, n0, R, D, TE[:, Kn:, :D], period=S, ldo=Dp,
+                     gscale=None if attn else st["mixsum"])
         fast = (PP == 64 and D % 128 == 0 and S % 64 == 0 and D // H in (64, 128) and H <= 128
                 and (not attn or st["NH"] % 2 == 0))
         dh = D // H
-        TE = st["TE"]
         p_at = 0
         for nd in nodes:
             g, c0, n = nd.g, st["c0s"][nd.gi], nd.gi
@@ -819,23 +846,19 @@ class DchagTrainer:
                                 "flops": 2 * g * R * 80 * (D + (128 if attn else 0))})
             else:
                 self._te_generic(patches, c0, g, R, dV, dl, dlb, TE[n])
-        # [d Wv | d U] = [tok.w ; tb]^T TE (+ pos^T Gs),  d [tok.w ; tb] = TE [Wv | U]^T
+        # [d Wv | d U] = [tok.w ; tb ; pos]^T TE   (the pos rows add pos^T Gs_n),
+        # d [tok.w ; tb ; pos_n] = TE [Wv | U]^T   (the pos rows give Gs_n Wv_n^T)
         dW = st["dWvU"][:n0]
         matmul(st["Waug"].transpose(1, 2), TE, out=dW,
-               work={"site": "bwd:l0_dwvu", "flops": 2 * n0 * Kn * D * Dp})
-        Gs16 = Gs.to(torch.bfloat16)
-        matmul(st["pos16"].t(), Gs16, out=dW[:, :, :D], accumulate=True,
-               work={"site": "bwd:l0_dwv_pos", "flops": 2 * n0 * S * D * D})
+               work={"site": "bwd:l0_dwvu", "flops": 2 * n0 * (Kn + S) * D * Dp})
         dWaug = matmul(TE, st["WvU"][:n0].transpose(1, 2),
-                       work={"site": "bwd:l0_dtok", "flops": 2 * n0 * Kn * Dp * D})
-        flat = dWaug.view(n0 * Kn, D)
+                       work={"site": "bwd:l0_dtok", "flops": 2 * n0 * (Kn + S) * Dp * D})
+        flat = dWaug.view(n0 * (Kn + S), D)
         grads["tok.w"] = flat.index_select(0, st["rows_w"]).view(cnt, PP, D)
         d_tb = flat.index_select(0, st["rows_b"])
         grads["tok.b"] = d_tb
         grads["special.channel_id"] = d_tb.clone()
-        d_pos_n = matmul(Gs16, st["WvU"][:n0, :, :D].transpose(1, 2),
-                         work={"site": "bwd:l0_dpos", "flops": 2 * n0 * S * D * D})
-        grads["special.pos"] = d_pos_n.sum(0)  # partial; backward() all-reduces it
+        grads["special.pos"] = dWaug[:, Kn:].sum(0)  # partial; backward() all-reduces it
         wname = "wv" if attn else "w"
         for nd in nodes:
             grads[f"{nd.name}.{wname}"] = dW[nd.gi, :, :D]
