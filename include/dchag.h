@@ -59,6 +59,18 @@ int dchag_gemm_nt(const void* A, int a_mn, long long lda, long long sAko, int Ki
                   int M, int N, int K, const float* bias, long long bias_g, void* out,
                   int out_f32, int accumulate, long long ldc, long long sCg, void* stream);
 
+/* The shared final layer's projection fused with the trunk's input assembly (
+ * model.py:100-108 apply_token_mask, :111-117 metadata token + concat):
+ *   out[b][1 + s][n] = (ctx[b*S + s] . W[n] + bias[n]) (1 - mask[b][s]) + mask_token[n] mask[b][s]
+ *   out[b][0][n]     = sum_k meta[b][k] meta_w[k][n] + meta_b[n]
+ * ctx bf16 [B*S][K], W bf16 [D][K] (n-major, as dchag_gemm_bf16), bias / mask / mask_token /
+ * meta fp32; out [B][S+1][D] bf16 (or fp32 if out_f32). The mask is applied in the GEMM
+ * epilogue and the rows land at their trunk positions: the aggregate is never written twice. */
+int dchag_final_vit(const void* ctx, int B, int seq, int K, const void* W, int D,
+                    const float* bias, const float* mask, const float* mask_token,
+                    const float* meta, int kmeta, const float* meta_w, const float* meta_b,
+                    void* out, int out_f32, void* stream);
+
 /* Row-dot GEMM for the level-0 backward (the `dp = G . V` term of the softmax backward,
  * layers.py:103-121 differentiated by tensor.py:395-413): the product rows
  * V[g][m][:] = A[g][m][:] W[g]^T + bias[g] are never stored; for every 32-column group

@@ -24,6 +24,8 @@ SIGNATURES = {
                         c_ll, c_vp, c_ll, c_ll, c_ll, c_vp],
     "dchag_gemm_nt": [c_vp, c_int, c_ll, c_ll, c_int, c_ll, c_vp, c_int, c_ll, c_ll, c_int,
                       c_int, c_int, c_int, c_vp, c_ll, c_vp, c_int, c_int, c_ll, c_ll, c_vp],
+    "dchag_final_vit": [c_vp, c_int, c_int, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_int,
+                        c_vp, c_vp, c_vp, c_int, c_vp],
     "dchag_gemm_rowdot": [c_vp, c_int, c_int, c_int, c_int, c_ll, c_ll, c_ll, c_vp, c_int,
                           c_ll, c_vp, c_ll, c_vp, c_ll, c_vp, c_vp],
     "dchag_gemm_combine": [c_vp, c_int, c_int, c_int, c_int, c_vp, c_ll, c_vp, c_ll, c_vp,

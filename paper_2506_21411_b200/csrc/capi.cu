@@ -215,7 +215,8 @@ static int gemm_impl(const void* A, int G, int Mo, int Mi, int K, long long sAg,
                      long long rowbias_g, long long rowbias_row, int rowbias_period, void* outV,
                      int outV_f32, long long sVg, long long sVmo, long long sVmi, float* outL,
                      long long sLg, long long sLmo, long long sLmi, const void* dotG,
-                     long long ldG, float* dotOut, void* stream) {
+                     long long ldG, float* dotOut, void* stream, const float* rmask = nullptr,
+                     const float* mtok = nullptr) {
   const bool dot = dotOut != nullptr;
   if (G < 1 || Mo < 1 || Mi < 128 || Mi % 128 || K < 16 || K % 16 || N < 16 || Nv < 0 ||
       Nv > N || Nv % 16)
@@ -275,6 +276,7 @@ static int gemm_impl(const void* A, int G, int Mo, int Mi, int K, long long sAg,
   a.rowbias_period = rowbias_period > 0 ? rowbias_period : 1;
   a.outV = outV; a.outV_f32 = outV_f32; a.sVg = sVg; a.sVmo = sVmo; a.sVmi = sVmi;
   a.outL = outL; a.sLg = sLg; a.sLmo = sLmo; a.sLmi = sLmi;
+  a.rmask = rmask; a.mtok = mtok;
   if (dot) {
     if (N % 32 || bn % 32 || ldG % 8 || !dotG || (reinterpret_cast<uintptr_t>(dotG) % 16))
       return fail(DCHAG_ERR_SHAPE, "gemm_rowdot: N, tile width and ldG must suit 32-column "
@@ -358,6 +360,24 @@ int dchag_gemm_nt(const void* A, int a_mn, long long lda, long long sAko, int Ki
     if (make_map(&tV, out, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B) == DCHAG_OK) a.v_tma = 1;
   }
   return cuda_status(launch_gemm(tA, tW, tV, a, 64, sms, S(stream)), "gemm_nt");
+}
+
+int dchag_final_vit(const void* ctx, int B, int seq, int K, const void* W, int D,
+                    const float* bias, const float* mask, const float* mask_token,
+                    const float* meta, int kmeta, const float* meta_w, const float* meta_b,
+                    void* out, int out_f32, void* stream) {
+  if (!ctx || !W || !mask || !mask_token || !out || B < 1 || seq < 128 || seq % 128 || D % 16 ||
+      kmeta < 0 || (kmeta && (!meta || !meta_w)) || !meta_b)
+    return fail(DCHAG_ERR_SHAPE, "final_vit: bad arguments B=%d S=%d D=%d", B, seq, D);
+  const size_t es = out_f32 ? 4 : 2;
+  void* rows = reinterpret_cast<uint8_t*>(out) + (size_t)D * es;  // out[b][1 + s]
+  int rc = gemm_impl(ctx, 1, B, seq, K, (long long)B * seq * K, (long long)seq * K, K, W, D,
+                     (long long)D * K, D, bias, D, nullptr, 0, 0, 1, rows, out_f32, 0,
+                     (long long)(seq + 1) * D, D, nullptr, 0, 0, 0, nullptr, 0, nullptr, stream,
+                     mask, mask_token);
+  if (rc) return rc;
+  return cuda_status(launch_vit_meta(meta, kmeta, meta_w, meta_b, out, out_f32, B, seq, D,
+                                     S(stream)), "final_vit");
 }
 
 int dchag_gemm_rowdot(const void* A, int G, int Mo, int Mi, int K, long long sAg,

@@ -250,6 +250,30 @@ cudaError_t launch_l0_dv(int g, int R, int D, int H, int NH, const __nv_bfloat16
   return cudaGetLastError();
 }
 
+// Metadata token rows of the trunk input (model.py:111-117): out[b][0][d] =
+// sum_k meta[b][k] meta_w[k][d] + meta_b[d], written next to the aggregate rows the final
+// GEMM's masked epilogue produced (dchag_final_vit).
+__global__ void vit_meta_kernel(const float* __restrict__ meta, int kmeta,
+                                const float* __restrict__ meta_w, const float* __restrict__ meta_b,
+                                void* out, int f32, int S, int D) {
+  const int b = blockIdx.y;
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= D) return;
+  float a = __ldg(meta_b + d);
+  for (int k = 0; k < kmeta; ++k) a = fmaf(__ldg(meta + (size_t)b * kmeta + k), __ldg(meta_w + (size_t)k * D + d), a);
+  const size_t o = (size_t)b * (S + 1) * D + d;
+  if (f32) reinterpret_cast<float*>(out)[o] = a;
+  else reinterpret_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16(a);
+}
+
+cudaError_t launch_vit_meta(const float* meta, int kmeta, const float* meta_w,
+                            const float* meta_b, void* out, int f32, int B, int S, int D,
+                            cudaStream_t st) {
+  vit_meta_kernel<<<dim3((D + 127) / 128, B), 128, 0, st>>>(meta, kmeta, meta_w, meta_b, out, f32,
+                                                            S, D);
+  return cudaGetLastError();
+}
+
 // ViT input tokens (model.py:100-117 up to the trunk): out[b][0] = meta_tok[b];
 // out[b][1 + s] = agg[b][s] * (1 - mask[b][s]) + mask_token * mask[b][s]. One thread per
 // 8 columns of an output row; rows are contiguous runs in both layouts.

@@ -41,6 +41,8 @@ struct GemmArgs {
   int lay;                      // operand layouts: bit 0 A MN-major, bit 1 W MN-major
   int Ki;                       // MN-major A: K = Ko * Ki rows, (k / Ki) * sAko + (k % Ki) * lda
   int accum;                    // fp32 output: out += acc instead of out = acc
+  const float* rmask;           // optional [M] row mask m: v = v (1 - m) + mtok[n] m (epilogue)
+  const float* mtok;            // [N] mask token
 };
 
 // host read (and optional reset) of the COMB overflow flag (synchronous)
@@ -159,6 +161,9 @@ cudaError_t launch_l0_tgrad_tc(const CUtensorMap& tG, const CUtensorMap& tP,
                                const L0TgradArgs& a, cudaStream_t st);
 cudaError_t launch_l0_tgrad_te(const CUtensorMap& tG, const CUtensorMap& tP,
                                const CUtensorMap& tDL, const L0TgradArgs& a, cudaStream_t st);
+cudaError_t launch_vit_meta(const float* meta, int kmeta, const float* meta_w,
+                            const float* meta_b, void* out, int f32, int B, int S, int D,
+                            cudaStream_t st);
 cudaError_t launch_vit_tokens(const void* agg, int f32, const float* mask,
                               const float* mask_token, const float* meta_tok, void* out, int B,
                               int S, int D, cudaStream_t st);

@@ -429,6 +429,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
           }
         }
+        if (!COMB && args.rmask) {
+          // trunk-input epilogue (model.py:100-108 apply_token_mask): masked rows take the
+          // mask token, v = v (1 - m) + mask_token m
+          const float mr = __ldg(args.rmask + m_row);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float mt = n0 + j < args.N ? __ldg(args.mtok + n0 + j) : 0.f;
+            v[j] = fmaf(v[j], 1.f - mr, mt * mr);
+          }
+        }
         if constexpr (COMB) {
           // Lpre holds the softmax over the parent's children (dchag_child_softmax)
           const int hd = min(n0 / args.dh, args.H - 1);

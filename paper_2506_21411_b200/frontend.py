@@ -373,26 +373,71 @@ class DchagFrontEnd(torch.nn.Module):
         """Front end + the trunk's input assembly: the aggregate with masked
         positions replaced by the mask token (model.py:100-108 apply_token_mask) and the
         metadata token prepended (model.py:111-117) -> [B, S+1, D] in out_dtype.
-        mask [B, S] (1 = masked), mask_token [D] (`dec.mask`), meta [B, 4],
-        meta_w [4, D] / meta_b [D] (`special.meta_w/b`)."""
-        agg = self(images)
-        B, S, D = agg.shape[0], self.seq, self.model.embed
-        dev = agg.device
-        mask = torch.as_tensor(mask, device=dev, dtype=torch.float32).reshape(B, S).contiguous()
-        mtok = torch.as_tensor(mask_token, device=dev, dtype=torch.float32).reshape(D).contiguous()
-        meta = torch.as_tensor(meta, device=dev, dtype=torch.float32).reshape(B, -1)
-        meta_tok = (meta @ torch.as_tensor(meta_w, device=dev, dtype=torch.float32)
-                    + torch.as_tensor(meta_b, device=dev, dtype=torch.float32)).contiguous()
+        mask [B, S] (1 = masked), mask_token [D] (`dec.mask`), meta [B, k] (k = 4 in the
+        reference), meta_w [k, D] / meta_b [D] (`special.meta_w/b`).
+
+        Device images on the folded plan (tp = 1, or the replicated final layer) fuse it into
+        the final projection: its epilogue applies the mask and writes each row at its trunk
+        position, and one small kernel writes the metadata rows (dchag_final_vit). The other
+        schedules (position- / head-split final layer, full_cross, fp32 mode) assemble it
+        from the forward's output (dchag_vit_tokens)."""
+        m = self.model
+        B, S, D = images.shape[0], self.seq, m.embed
+        dev = self.device
+        f32 = dict(device=dev, dtype=torch.float32)
+        mask = torch.as_tensor(mask).to(**f32).reshape(B, S).contiguous()
+        mtok = torch.as_tensor(mask_token).to(**f32).reshape(D).contiguous()
+        meta = torch.as_tensor(meta).to(**f32).reshape(B, -1).contiguous()
+        meta_w = torch.as_tensor(meta_w).to(**f32).reshape(meta.shape[1], D).contiguous()
+        meta_b = torch.as_tensor(meta_b).to(**f32).reshape(D).contiguous()
         if out is None:
             out = torch.empty(B, S + 1, D, device=dev, dtype=self.out_dtype)
         elif tuple(out.shape) != (B, S + 1, D) or out.dtype != self.out_dtype or \
                 not out.is_contiguous() or out.device != dev:
             raise ConfigError(f"out must be a contiguous {self.out_dtype} tensor of shape "
                               f"{(B, S + 1, D)} on {dev}")
+        vit = (mask, mtok, meta, meta_w, meta_b)
+        fused = (images.is_cuda and not self._unfolded() and self.comm_chunks == 1
+                 and not self.strategy.final_layer_tp_split
+                 and (self.tp == 1 or not self._position_split(B)))
+        if fused:
+            pk = self.prepare()
+            img = self._check_images(images)
+            if self.tp == 1:
+                self.local_payload(img, pk, direct_out=out, vit=vit)
+            else:
+                self.finish(self.gather(self.local_payload(img, pk)), B, out=out, vit=vit)
+            return out
+        agg = self(images)
+        meta_tok = (meta @ meta_w + meta_b).contiguous()
         _lib.call("dchag_vit_tokens", _lib.ptr(agg), int(agg.dtype == torch.float32), B, S, D,
                   _lib.ptr(mask), _lib.ptr(mtok), _lib.ptr(meta_tok), _lib.ptr(out),
                   _lib.stream_handle())
         return out
+
+    def _final_vit(self, ctx, W, bias, B, out, vit):
+        """Final projection with the trunk-input epilogue into out [B, S+1, D]."""
+        m = self.model
+        mask, mtok, meta, meta_w, meta_b = vit
+        _lib.call("dchag_final_vit", _lib.ptr(ctx), B, self.seq, m.embed, _lib.ptr(W), m.embed,
+                  _lib.ptr(bias), _lib.ptr(mask), _lib.ptr(mtok), _lib.ptr(meta), meta.shape[1],
+                  _lib.ptr(meta_w), _lib.ptr(meta_b), _lib.ptr(out),
+                  int(out.dtype == torch.float32), _lib.stream_handle())
+
+    def _check_images(self, images):
+        """Device images of this rank's slab as the kernels read them (bf16, row-contiguous)."""
+        m = self.model
+        off, cnt = self.slab
+        if images.shape[1] == m.channels and self.tp > 1:
+            images = images[:, off:off + cnt]
+        elif images.shape[1] != cnt:
+            raise ConfigError(f"images carry {images.shape[1]} channels; rank {self.rank} "
+                              f"expects {cnt} (its slab) or {m.channels} (all)")
+        if images.dtype != torch.bfloat16:
+            images = images.to(torch.bfloat16)
+        if images.stride(3) != 1 or images.stride(2) != m.image_w:
+            images = images.contiguous()
+        return images
 
     def _forward_host(self, images, pk, out, h2d_chunks):
         """Chunked H2D -> kernels -> (D2H) pipeline for host-resident images."""
@@ -620,7 +665,7 @@ class DchagFrontEnd(torch.nn.Module):
             wk.wait()
         return res
 
-    def local_payload(self, img, pk=None, direct_out=None):
+    def local_payload(self, img, pk=None, direct_out=None, vit=None):
         """Rank-local part: slab tree -> root payload [V bf16 R*D | L fp32 R*H] (bytes),
         V/L = the root stream projected into the final layer's value/logit space."""
         pk = pk or self.prepare()
@@ -693,6 +738,10 @@ class DchagFrontEnd(torch.nn.Module):
                           _lib.ptr(nxt), st)
                 ctx = nxt[0] if split == 1 else torch.add(nxt[0], nxt[1])
                 continue
+            if li == depth - 1 and direct_out is not None and vit is not None:
+                # ... with the trunk-input epilogue (vit_input)
+                self._final_vit(ctx, pk.Wdir, pk.bdir, B, direct_out, vit)
+                return None
             if li == depth - 1 and direct_out is not None:
                 # tp == 1: the root projection folded with the final layer writes the output
                 _lib.call("dchag_gemm_bf16", _lib.ptr(ctx), 1, 1, R, d, R * d, 0, d,
@@ -722,7 +771,7 @@ class DchagFrontEnd(torch.nn.Module):
                           _lib.ptr(ctx), st)
         return payload
 
-    def finish(self, gathered, B, out=None):
+    def finish(self, gathered, B, out=None, vit=None):
         """Shared final layer over the gathered streams -> [B, 1, S, D]."""
         pk = self.prepare()
         m = self.model
@@ -749,6 +798,9 @@ class DchagFrontEnd(torch.nn.Module):
             out = torch.empty(R, d, device=dev, dtype=self.out_dtype)
         if self.strategy.final_layer_tp_split and self.tp > 1:
             return self._finish_head_split(ctx_f, B, out)
+        if vit is not None:
+            self._final_vit(ctx_f, pk.Wf, pk.bf, B, out, vit)
+            return out
         _lib.call("dchag_gemm_bf16", _lib.ptr(ctx_f), 1, 1, R, d, R * d, 0, d, _lib.ptr(pk.Wf),
                   d, d * d, d, _lib.ptr(pk.bf), d, 0, 0, 0, 1, _lib.ptr(out),
                   int(self.out_dtype == torch.float32), R * d, 0, d, 0, 0, 0, 0, st)

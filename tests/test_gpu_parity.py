@@ -524,3 +524,35 @@ def test_combine_range_guard(scale, overflow):
         want = 0.25 * scale * ctx.float().sum(0)
         assert torch.isfinite(out).all()
         assert rel_err(out[0, 0].float().cpu().numpy(), want.cpu().numpy()) < 5e-3
+
+
+def test_vit_input_fused_final_tp2():
+    """The trunk-input epilogue on the replicated final layer (tp = 2, all ranks in one
+    process): finish(..., vit=...) writes [B, S+1, D] straight from the final projection."""
+    from paper_2506_21411_b200 import DchagFrontEnd
+    meta = dict(channels=40, image_h=64, image_w=64, patch=4, embed=256, heads=4, tp=2,
+                max_group=16)
+    specs = O.frontend_param_specs(40, 64, 64, 4, 256, 2, 16)
+    w = O.random_params(specs, seed=6, std=0.05, bias_std=0.02)
+    w = {k: v.astype(np.float32).astype(np.float64) for k, v in w.items()}
+    rng = np.random.default_rng(9)
+    images = _bf(rng.standard_normal((2, 40, 64, 64))).float().numpy().astype(np.float64)
+    img = _bf(images).cuda()
+    mods = [_frontend(meta, 2, r) for r in range(2)]
+    for m in mods:
+        m.load_weights(w)
+    pays = [m.local_payload(img[:, m.slab[0]:m.slab[0] + m.slab[1]]) for m in mods]
+    S, D = mods[0].seq, 256
+    mask = (rng.random((2, S)) < 0.5).astype(np.float32)
+    mtok = (rng.standard_normal(D) * 0.02).astype(np.float32)
+    md = rng.standard_normal((2, 4)).astype(np.float32)
+    mw = (rng.standard_normal((4, D)) * 0.02).astype(np.float32)
+    mb = (rng.standard_normal(D) * 0.01).astype(np.float32)
+    vit = tuple(torch.from_numpy(a).cuda() for a in (mask, mtok, md, mw, mb))
+    out = torch.empty(2, S + 1, D, device="cuda")
+    mods[0].finish(torch.cat(pays), 2, out=out, vit=vit)
+    torch.cuda.synchronize()
+    agg = O.dchag_frontend(images, w, patch=4, heads=4, tp=2, max_group=16)
+    want = O.vit_input(agg, mask.astype(np.float64), mtok.astype(np.float64),
+                       md.astype(np.float64), mw.astype(np.float64), mb.astype(np.float64))
+    assert rel_err(out.cpu().numpy(), want) < BF16_TOL
