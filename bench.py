@@ -42,6 +42,10 @@ WORKLOADS = {
     "hyperspectral_fullcross": dict(channels=500, image_h=128, image_w=128, patch=8,
                                     embed=1024, heads=16, depth=3, batch=32,
                                     variant="full_cross"),
+    # the fp32 parity mode (BASELINE tolerance fp32 <= 1e-4) on the H1 shape: split-bf16
+    # 3-term tcgen05 GEMMs, fp32 combines, tokens materialised in fp32
+    "hyperspectral_fp32": dict(channels=500, image_h=128, image_w=128, patch=8, embed=1024,
+                               heads=16, depth=3, batch=32, precision="fp32"),
 }
 # scaling sweep: C 64..1024 x D 1024 (16 heads) / 4096 (32 heads,
 # dh = 128), 128x128 P8, B 32, max_group 16 with the depth derived per slab
@@ -371,7 +375,8 @@ def b200_arm(args, wl, tp, max_group):
                             wl["embed"], wl["heads"], max_group=max_group, tp=tp_, rank=rank_,
                             final_layer_tp_split=bool(wl.get("final_split")) and tp_ > 1,
                             agg_variant=wl.get("variant", "single_query"),
-                            agg_layer_kind=wl.get("layer_kind", "cross_attention"))
+                            agg_layer_kind=wl.get("layer_kind", "cross_attention"),
+                            precision=wl.get("precision", "bf16"))
         fe_.init_weights(seed=0, all_ranks=False)
         fe_.prepare()
         return fe_
@@ -566,7 +571,8 @@ def b200_arm(args, wl, tp, max_group):
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic (N(0,1) bf16 images, truncated-normal(0.02) "
+            "dtype": wl.get("precision", "bf16"),
+            "data": "synthetic (N(0,1) bf16 images, truncated-normal(0.02) "
                                      "random-init weights)",
             "config": cfg,
             "roofline": roof,

@@ -306,6 +306,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t acc_phase = 0;
     int prev_mt = -1, prev_nt = -1;
     uint4 rbv[4][4];  // row bias (or, in row-dot mode, dotG) of this thread's row, 4 groups
+    float4 dot_bias_pf = make_float4(0.f, 0.f, 0.f, 0.f);  // row-dot: next tile's bias
+    bool dot_pf_valid = false;
     for (int t = ct_begin; t < ct_end; t += ct_step) {
       int g, mt, nt;
       decode(t, g, mt, nt);
@@ -345,6 +347,91 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         }
+      }
+      if (!COMB && dot) {
+        // row-dot tile: sum over each 32-column group of (acc + bias) * dotG. The tile's
+        // bias row (the channel's) was fetched during the previous tile, and the TMEM loads
+        // of group i+1 are in flight while group i is reduced.
+        float* wbias = bias_smem + (warp - 2) * 128;
+        const float* bias_t = args.bias ? args.bias + (size_t)g * args.bias_g : nullptr;
+        const int nb = nt * args.BN + (hf + 2 * (lane >> 3)) * 32 + (lane & 7) * 4;
+        auto fetch_bias = [&](const float* bp, int n) {
+          float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (!bp) return b;
+          if (b_vec && n + 4 <= args.N) return __ldg(reinterpret_cast<const float4*>(bp + n));
+          if (n < args.N) b.x = __ldg(bp + n);
+          if (n + 1 < args.N) b.y = __ldg(bp + n + 1);
+          if (n + 2 < args.N) b.z = __ldg(bp + n + 2);
+          if (n + 3 < args.N) b.w = __ldg(bp + n + 3);
+          return b;
+        };
+        if (!dot_pf_valid) dot_bias_pf = fetch_bias(bias_t, nb);
+        __syncwarp();  // the previous tile's broadcast reads are done
+        reinterpret_cast<float4*>(wbias)[lane] = dot_bias_pf;
+        __syncwarp();
+        dot_pf_valid = false;
+        if (t + ct_step < ct_end && args.bias) {
+          int g2, mt2, nt2;
+          decode(t + ct_step, g2, mt2, nt2);
+          dot_bias_pf = fetch_bias(args.bias + (size_t)g2 * args.bias_g,
+                                   nt2 * args.BN + (hf + 2 * (lane >> 3)) * 32 + (lane & 7) * 4);
+          dot_pf_valid = true;
+        }
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t t_row = lane_base + acc * GEMM_BN_MAX;
+        auto gvalid = [&](int gi) {
+          const int grp = hf + 2 * gi;
+          return grp < n_groups && nt * args.BN + grp * 32 < args.N;
+        };
+        auto reduce = [&](const uint32_t (&r)[32], int gi) {
+          const int n0 = nt * args.BN + (hf + 2 * gi) * 32;
+          float sdot = 0.f;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t q[4] = {rbv[gi][j].x, rbv[gi][j].y, rbv[gi][j].z, rbv[gi][j].w};
+            const float4 b0 = reinterpret_cast<const float4*>(wbias + gi * 32)[2 * j];
+            const float4 b1 = reinterpret_cast<const float4*>(wbias + gi * 32)[2 * j + 1];
+            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              sdot = fmaf(__uint_as_float(r[8 * j + 2 * e]) + bb[2 * e], bf16lo(q[e]), sdot);
+              sdot = fmaf(__uint_as_float(r[8 * j + 2 * e + 1]) + bb[2 * e + 1], bf16hi(q[e]),
+                          sdot);
+            }
+          }
+          args.dotOut[((size_t)g * (args.N >> 5) + (n0 >> 5)) * args.M + m_row] = sdot;
+        };
+        uint32_t ra[32], rc[32];
+        if (gvalid(0)) {
+          tmem_ld32(t_row + hf * 32, ra);
+          tmem_ld_wait();
+          if (gvalid(1)) tmem_ld32(t_row + (hf + 2) * 32, rc);
+          reduce(ra, 0);
+          tmem_ld_wait();
+          if (gvalid(1)) {
+            if (gvalid(2)) tmem_ld32(t_row + (hf + 4) * 32, ra);
+            reduce(rc, 1);
+            tmem_ld_wait();
+            if (gvalid(2)) {
+              if (gvalid(3)) tmem_ld32(t_row + (hf + 6) * 32, rc);
+              reduce(ra, 2);
+              tmem_ld_wait();
+              if (gvalid(3)) reduce(rc, 3);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR)
+            asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(rank0_addr(&tempty[acc]))
+                         : "memory");
+          else
+            mbar_arrive(&tempty[acc]);
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
       }
       // combine mode: softmax statistics of this row over the parent's children, per group
       int c_first = g, c_n = 1;

@@ -42,7 +42,8 @@ def _gemm(A, Mo, Mi, K, sAmo, sAmi, W_nk, bias, outV, sVmo, sVmi, outL=None, sLm
     _lib.call("dchag_gemm_bf16", _lib.ptr(A), 1, Mo, Mi, K, sAg, sAmo, sAmi, _lib.ptr(W_nk), N,
               N * K, Nv, _lib.ptr(bias), N, _lib.ptr(rowbias), 0, rowbias_row,
               rowbias_period, _lib.ptr(outV), int(outV_f32), 0, sVmo, sVmi, _lib.ptr(outL), 0,
-              sLmo, sLmi, _lib.stream_handle())
+              sLmo, sLmi, _lib.stream_handle(),
+              work={"site": "ops:gemm", "flops": 2 * Mo * Mi * K * N})
 
 
 def tokenize_channels(images, tok_w, tok_b, chan_id, pos, patch, out_dtype=torch.float32):
@@ -97,33 +98,72 @@ def _full_cross_tree(tokens, spec: TreeSpec, w, prefix, n_heads, out_dtype):
         U = torch.empty(n_in, R, H, device="cuda", dtype=torch.float32)
         nodes = [f"{prefix}.l{li}.g{gi}" for gi in range(len(level))]
         for node, f, g in zip(nodes, firsts, level):
-            wr = tw[f"{node}.wo"] @ tw[f"{node}.rq"] / (D ** 0.5)                    # [D]
-            Wu = (tw[f"{node}.wv"].view(D, H, dh) * wr.view(1, H, dh)).sum(-1)        # [D, H]
-            Wc = torch.cat([tw[f"{node}.wq"], tw[f"{node}.wk"], tw[f"{node}.wv"], Wu], dim=1)
-            Wnk = _bf(Wc.t())
-            zero = torch.zeros(Wnk.shape[0], device="cuda", dtype=torch.float32)
+            Wnk, _, _ = _fc_node_weights(tw, node, D, H)
+            zero = _zeros(Wnk.shape[0])
             _gemm(x[f:f + g], 1, g * R, D, 0, D, Wnk, zero, QKV[f:f + g], 0, 3 * D,
                   U[f:f + g], 0, H)
-        first_t = torch.tensor(firsts, device="cuda", dtype=torch.int32)
-        g_t = torch.tensor(list(level), device="cuda", dtype=torch.int32)
+        first_t = _dev_i32(firsts)
+        g_t = _dev_i32(level)
         gmax = max(level)
         wts = torch.empty(len(level), R, gmax, H, device="cuda", dtype=torch.float32)
         _lib.call("dchag_fullcross_weights", len(level), R, D, H, _lib.ptr(first_t),
                   _lib.ptr(g_t), gmax, _lib.ptr(QKV), R * 3 * D, 3 * D, _lib.ptr(U), R * H,
-                  _lib.ptr(wts), st)
+                  _lib.ptr(wts), st,
+                  work={"site": "ops:fullcross_weights", "bytes": n_in * R * (4 * D + 4 * H)})
         ctx = torch.empty(len(level), R, D, device="cuda", dtype=torch.bfloat16)
         _lib.call("dchag_combine_weighted", len(level), R, D, H, _lib.ptr(first_t),
                   _lib.ptr(g_t), gmax, _lib.ptr(QKV[:, :, 2 * D:]), R * 3 * D, 3 * D,
-                  _lib.ptr(wts), _lib.ptr(ctx), st)
+                  _lib.ptr(wts), _lib.ptr(ctx), st,
+                  work={"site": "ops:combine_weighted", "bytes": n_in * R * 2 * D
+                        + len(level) * R * 2 * D})
         last = li == depth - 1
         y = torch.empty(len(level), R, D, device="cuda",
                         dtype=out_dtype if last else torch.bfloat16)
         for k, node in enumerate(nodes):
-            Wo = _bf(tw[f"{node}.wo"].t())
-            _gemm(ctx[k], 1, R, D, 0, D, Wo, tw[f"{node}.bo"].contiguous(), y[k], 0, D,
-                  outV_f32=y.dtype == torch.float32)
+            _, Wo, bo = _fc_node_weights(tw, node, D, H)
+            _gemm(ctx[k], 1, R, D, 0, D, Wo, bo, y[k], 0, D, outV_f32=y.dtype == torch.float32)
         x = y
     return x.view(B, 1, S, D) if x.shape[0] == 1 else x.view(1, B, S, D).transpose(0, 1)
+
+
+# bf16 operand forms of the full_cross node weights, folded once per weight version (an
+# in-place update or a new tensor refolds; the forward never refolds unchanged weights)
+_FC_CACHE: dict = {}
+_SMALL: dict = {}
+
+
+def _fc_node_weights(tw, node, D, H):
+    """(W [q|k|v|u]^T bf16 [3D+H, D], wo^T bf16 [D, D], bo fp32) of a full_cross node:
+    u_jh = v_j,h . (wo rq)_h / sqrt(D) (the rq reduce's scores are linear in the outputs)."""
+    names = [f"{node}.{n}" for n in ("wq", "wk", "wv", "wo", "bo", "rq")]
+    key = (node, D, H) + tuple((id(tw[n]), tw[n]._version, tw[n].data_ptr()) for n in names)
+    hit = _FC_CACHE.get(node)
+    if hit is not None and hit[0] == key:
+        return hit[1]
+    dh = D // H
+    with torch.no_grad():
+        wr = tw[f"{node}.wo"] @ tw[f"{node}.rq"] / (D ** 0.5)                    # [D]
+        Wu = (tw[f"{node}.wv"].view(D, H, dh) * wr.view(1, H, dh)).sum(-1)        # [D, H]
+        Wc = torch.cat([tw[f"{node}.wq"], tw[f"{node}.wk"], tw[f"{node}.wv"], Wu], dim=1)
+        val = (_bf(Wc.t()), _bf(tw[f"{node}.wo"].t()), _f32(tw[f"{node}.bo"]))
+    _FC_CACHE[node] = (key, val)
+    return val
+
+
+def _zeros(n):
+    t = _SMALL.get(("z", n))
+    if t is None:
+        t = _SMALL[("z", n)] = torch.zeros(n, device="cuda", dtype=torch.float32)
+    return t
+
+
+def _dev_i32(vals):
+    """Device int32 table, made once per content (no per-call pageable H2D copy)."""
+    key = ("i", tuple(int(v) for v in vals))
+    t = _SMALL.get(key)
+    if t is None:
+        t = _SMALL[key] = torch.tensor(key[1], device="cuda", dtype=torch.int32)
+    return t
 
 
 def tree_aggregate(tokens, spec: TreeSpec, w, prefix, layer_kind, variant, n_heads,
@@ -182,8 +222,8 @@ def tree_aggregate(tokens, spec: TreeSpec, w, prefix, layer_kind, variant, n_hea
                       L[f:f + g] if attn else None, 0, H)
         # 2) combine children per node (+ linear bias b), then 3) node output projection
         ctx = torch.empty(len(level), R, D, device="cuda", dtype=torch.bfloat16)
-        first_t = torch.tensor(firsts, device="cuda", dtype=torch.int32)
-        g_t = torch.tensor(list(level), device="cuda", dtype=torch.int32)
+        first_t = _dev_i32(firsts)
+        g_t = _dev_i32(level)
         mix = None if attn else torch.cat([tw[f"{n}.mix"] for n in nodes]).contiguous()
         if x_layout == "bsd":
             sVj, sVb, sLj, sLb, rows_inner = S * D, n_in * S * D, S * H, n_in * S * H, S
@@ -197,11 +237,11 @@ def tree_aggregate(tokens, spec: TreeSpec, w, prefix, layer_kind, variant, n_hea
                         dtype=out_dtype if li == depth - 1 else torch.bfloat16)
         for k, node in enumerate(nodes):
             if attn:
-                Wo, bo = _bf(tw[f"{node}.wo"].t()), tw[f"{node}.bo"]
-            else:
-                Wo, bo = _bf(torch.eye(D, device="cuda")), tw[f"{node}.b"]
-            _gemm(ctx[k], 1, R, D, 0, D, Wo, bo.contiguous(), y[k], 0, D,
-                  outV_f32=y.dtype == torch.float32)
+                _gemm(ctx[k], 1, R, D, 0, D, _bf(tw[f"{node}.wo"].t()),
+                      tw[f"{node}.bo"].contiguous(), y[k], 0, D,
+                      outV_f32=y.dtype == torch.float32)
+            else:  # linear node: w was applied before the mix; only the bias remains
+                torch.add(ctx[k], tw[f"{node}.b"], out=y[k])
         x, x_layout, n_in = y, "nrd", len(level)
     return x.view(B, 1, S, D) if x.shape[0] == 1 else x.view(1, B, S, D).transpose(0, 1)
 
@@ -254,19 +294,29 @@ def _gemm3(A, W_dn, bias, N_logit=0):
 
 
 def tokenize_channels_fp32(images, tok_w, tok_b, chan_id, pos, patch):
-    """fp32 tokens [B, Cs, S, D] (model.py:51-64) with fp32-accurate GEMMs."""
+    """fp32 tokens [B, Cs, S, D] (model.py:51-64) with fp32-accurate GEMMs: one grouped
+    split-bf16 GEMM over the channels (group = channel), tok.b + chan_id in its epilogue."""
     B, C, Hh, Ww = images.shape
     P = patch
     S, PP = (Hh // P) * (Ww // P), P * P
     D = tok_w.shape[-1]
+    if (B * S) % 128 or PP % 16:
+        raise ConfigError("fp32 mode needs B*S % 128 == 0 and P*P % 16 == 0")
     x = _f32(images)
     patches = x.reshape(B, C, Hh // P, P, Ww // P, P).permute(1, 0, 2, 4, 3, 5)
     patches = patches.reshape(C, B * S, PP)                           # unfold (tensor.py:303-323)
-    out = torch.empty(B, C, S, D, device="cuda", dtype=torch.float32)
-    bias = _f32(tok_b) + _f32(chan_id)
-    for c in range(C):
-        out[:, c] = _gemm3(patches[c], tok_w[c], bias[c]).view(B, S, D)
-    return out + _f32(pos)[None, None]
+    A3 = _split3(patches)                                             # [C, R, 3 PP]
+    Wt = _f32(tok_w).transpose(1, 2)                                  # [C, D, PP]
+    hi = Wt.to(torch.bfloat16)
+    lo = (Wt - hi.float()).to(torch.bfloat16)
+    W3 = torch.cat([hi, hi, lo], dim=2).contiguous()                  # [C, D, 3 PP]
+    bias = (_f32(tok_b) + _f32(chan_id)).contiguous()                 # [C, D]
+    R, K3 = B * S, 3 * PP
+    out = torch.empty(C, R, D, device="cuda", dtype=torch.float32)
+    _lib.call("dchag_gemm_bf16", _lib.ptr(A3), C, 1, R, K3, R * K3, 0, K3, _lib.ptr(W3), D,
+              D * K3, D, _lib.ptr(bias), D, 0, 0, 0, 1, _lib.ptr(out), 1, R * D, 0, D, 0, 0, 0, 0,
+              _lib.stream_handle())
+    return out.view(C, B, S, D).permute(1, 0, 2, 3) + _f32(pos)[None, None]
 
 
 def tree_aggregate_fp32(tokens, spec: TreeSpec, w, prefix, layer_kind, n_heads):
@@ -296,8 +346,8 @@ def tree_aggregate_fp32(tokens, spec: TreeSpec, w, prefix, layer_kind, n_heads):
             else:
                 V[f:f + g] = _gemm3(x[f:f + g].reshape(g * R, D), Wc, None).view(g, R, D)
         ctx = torch.empty(len(level), R, D, device="cuda", dtype=torch.float32)
-        first_t = torch.tensor(firsts, device="cuda", dtype=torch.int32)
-        g_t = torch.tensor(list(level), device="cuda", dtype=torch.int32)
+        first_t = _dev_i32(firsts)
+        g_t = _dev_i32(level)
         mix = None if attn else torch.cat([tw[f"{n}.mix"] for n in nodes]).contiguous()
         _lib.call("dchag_combine_f32", len(level), R, D, H, _lib.ptr(first_t), _lib.ptr(g_t),
                   max(level), _lib.ptr(V), R * D, _lib.ptr(L), R * H, _lib.ptr(mix),
