@@ -256,10 +256,14 @@ int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, c
  * (wo rq)_h / sqrt(D) at u + j*sUj + r*H (fp32):  S^h = softmax_j(q_i,h . k_j,h / sqrt(dh)),
  * s_i = sum_h sum_j S^h_ij u_jh,  p2 = softmax_i(s),  w[n][r][j][h] = sum_i p2_i S^h_ij.
  * The node output is then (sum_j w_jh V_j,h) @ wo + bo (dchag_combine_weighted + GEMM).
- * max_g <= 32, H <= 32. */
+ * posq (optional, bf16 [n_nodes][seq][D]): added to every q of row r at position r % seq
+ * (level 0 with the tokenizer folded: the positional parts of k, v and u cancel in the
+ * softmaxes or are added to the context, so only the query's enters here).
+ * max_g <= 32, H <= 32, (D/H) % 16 == 0. */
 int dchag_fullcross_weights(int n_nodes, int R, int D, int H, const int* node_first,
                             const int* node_g, int max_g, const void* QK, long long sQj,
-                            long long ldq, const float* u, long long sUj, float* w, void* stream);
+                            long long ldq, const float* u, long long sUj, float* w,
+                            const void* posq, int seq, void* stream);
 
 /* ctx[n][r][h-blk] = sum_j w[n][r][j][h] V_j[r][h-blk]; V_j row r at V + j*sVj + r*ldv (bf16). */
 int dchag_combine_weighted(int n_nodes, int R, int D, int H, const int* node_first,

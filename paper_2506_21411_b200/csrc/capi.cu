@@ -632,15 +632,19 @@ int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, c
 
 int dchag_fullcross_weights(int n_nodes, int R, int D, int H, const int* node_first,
                             const int* node_g, int max_g, const void* QK, long long sQj,
-                            long long ldq, const float* u, long long sUj, float* w, void* stream) {
-  if (D % H || (D / H) % 8 || max_g < 1 || max_g > 32 || H > 32 || ldq < 2 * D || (ldq * 2) % 16 ||
+                            long long ldq, const float* u, long long sUj, float* w,
+                            const void* posq, int seq, void* stream) {
+  if (D % H || (D / H) % 16 || max_g < 1 || max_g > 32 || H > 32 || ldq < 2 * D || (ldq * 2) % 16 ||
       (sQj * 2) % 16 || reinterpret_cast<uintptr_t>(QK) % 16)
     return fail(DCHAG_ERR_SHAPE, "fullcross_weights: bad shape");
   FullCrossArgs a;
+  memset(&a, 0, sizeof(a));
   a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H; a.max_g = max_g;
   a.node_first = node_first; a.node_g = node_g;
   a.QK = reinterpret_cast<const __nv_bfloat16*>(QK); a.sQj = sQj; a.ldq = ldq;
   a.u = u; a.sUj = sUj; a.w = w;
+  a.posq = reinterpret_cast<const __nv_bfloat16*>(posq); a.S = seq > 0 ? seq : 1;
+  if (posq && (seq < 1 || R % seq)) return fail(DCHAG_ERR_SHAPE, "fullcross_weights: bad seq");
   return cuda_status(launch_fullcross_weights(a, S(stream)), "fullcross_weights");
 }
 

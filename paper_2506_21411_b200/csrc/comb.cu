@@ -585,97 +585,192 @@ cudaError_t launch_l0_softmax_bwd(int g, int R, int H, int NH, int dh, const flo
   return cudaGetLastError();
 }
 
-// full_cross node weights (see FullCrossArgs). One CTA per (node, row), one warp per head;
-// lane j owns child j (g <= 32): it keeps k_j,h in registers and computes the row of logits
-// L_ij = q_i . k_j / sqrt(dh) against q_i broadcast from shared memory; the per-i softmax,
-// the head-sum of sum_j S_ij u_jh and the softmax over i are warp / CTA reductions.
+// full_cross node weights (see FullCrossArgs; layers.py:125-138 with the rq reduce folded).
+// One CTA per (node, row), one warp per head. The row's q and k of every child (g <= 32
+// rows of D bf16 each) are staged in shared memory with 16-byte coalesced loads (row
+// stride padded by 16 B: conflict-free ldmatrix); each head's g x g logits are tensor-core
+// products (mma.sync m16n8k16: A = q_h [child i][dh], B = k_h [child j][dh]) that stay in
+// registers through the softmax over j (quad shuffles), the u-weighted sums t_i,h, the
+// head sum s_i (shared memory), p2 = softmax_i(s) and w_jh = sum_i p2_i S^h_ij
+// (shuffles over the fragment rows).
+DEV void mma_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int MI>  // MI = 1: g <= 16 children, 2: g <= 32
 __global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a) {
-  extern __shared__ float fsm[];  // q: [H][g][dh] fp32, then t: [H][32]
+  extern __shared__ __align__(16) uint8_t fsm_raw[];
+  constexpr int NJ = 2 * MI;                       // 8-wide n-tiles over the children j
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
   const long long item = blockIdx.x;
   const int n = (int)(item / a.R);
   const int r = (int)(item - (long long)n * a.R);
   const int first = __ldg(a.node_first + n), g = __ldg(a.node_g + n);
-  const int H = a.H, dh = a.D / H, h = warp;
-  const int G = a.max_g;
-  float* q = fsm;                                 // [H][G][dh]
-  float* t = fsm + (size_t)H * G * dh;            // [H][32]
-  // stage q_i,h for all children (coalesced over the head's dh columns)
-  for (int i = 0; i < g; ++i) {
-    const __nv_bfloat16* qr = a.QK + (long long)(first + i) * a.sQj + (long long)r * a.ldq + h * dh;
-    for (int e = lane; e < dh; e += 32) q[((size_t)h * G + i) * dh + e] = __bfloat162float(qr[e]);
-  }
-  __syncwarp();
-  float S[32];
-  float uj = 0.f;
-  const bool act = lane < g;
-  if (act) {
-    const __nv_bfloat16* kr =
-        a.QK + (long long)(first + lane) * a.sQj + (long long)r * a.ldq + a.D + h * dh;
-    uj = __ldg(a.u + (long long)(first + lane) * a.sUj + (long long)r * H + h);
-    const float sc = rsqrtf((float)dh);
-#pragma unroll 4
-    for (int i = 0; i < 32; ++i) S[i] = 0.f;
-    for (int e0 = 0; e0 < dh; e0 += 8) {
-      const uint4 kv = *reinterpret_cast<const uint4*>(kr + e0);
-      const uint32_t kw[4] = {kv.x, kv.y, kv.z, kv.w};
-      float kf[8];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) { kf[2 * e] = bf16lo(kw[e]); kf[2 * e + 1] = bf16hi(kw[e]); }
-      for (int i = 0; i < g; ++i) {
-        const float* qi = q + ((size_t)h * G + i) * dh + e0;
-        float acc = 0.f;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc += qi[e] * kf[e];
-        S[i] += acc;
+  const int H = a.H, D = a.D, dh = D / H, h = warp;
+  const int ld = D * 2 + 16;                       // bytes per staged row (padded)
+  const int rows = 16 * MI;
+  uint8_t* qs = fsm_raw;                           // [rows][ld] q, then k
+  uint8_t* ks = fsm_raw + rows * ld;
+  float* tsm = reinterpret_cast<float*>(fsm_raw + 2 * rows * ld);   // [H][32] t_i,h
+  float* p2s = tsm + H * 32;                                         // [32]
+  // stage q and k of the g children (zero rows beyond g), 16 B per thread per step
+  const int cpr = D / 8;                           // 16-byte chunks per row
+  for (int t = threadIdx.x; t < 2 * rows * cpr; t += blockDim.x) {
+    const int which = t / (rows * cpr), rest = t - which * rows * cpr;
+    const int j = rest / cpr, c = rest - j * cpr;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (j < g) {
+      v = __ldg(reinterpret_cast<const uint4*>(a.QK + (long long)(first + j) * a.sQj +
+                                               (long long)r * a.ldq + which * D) + c);
+      if (!which && a.posq) {  // + the positional query of this position
+        const uint4 pq = __ldg(reinterpret_cast<const uint4*>(
+            a.posq + ((long long)n * a.S + r % a.S) * D) + c);
+        v.x = pack_bf16(bf16lo(v.x) + bf16lo(pq.x), bf16hi(v.x) + bf16hi(pq.x));
+        v.y = pack_bf16(bf16lo(v.y) + bf16lo(pq.y), bf16hi(v.y) + bf16hi(pq.y));
+        v.z = pack_bf16(bf16lo(v.z) + bf16lo(pq.z), bf16hi(v.z) + bf16hi(pq.z));
+        v.w = pack_bf16(bf16lo(v.w) + bf16lo(pq.w), bf16hi(v.w) + bf16hi(pq.w));
       }
     }
-    for (int i = 0; i < g; ++i) S[i] *= sc;
+    *reinterpret_cast<uint4*>((which ? ks : qs) + j * ld + c * 16) = v;
   }
-  // softmax over j (across lanes) for every query i; t_i = sum_j S_ij u_jh
-  for (int i = 0; i < g; ++i) {
-    float m = act ? S[i] : -INFINITY;
+  __syncthreads();
+  // logits S^h = q_h k_h^T / sqrt(dh) on the tensor cores
+  float acc[MI][NJ][4];
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[mi][nj][e] = 0.f;
+  const int mat = lane >> 3, rr = lane & 7;
+  for (int k0 = 0; k0 < dh; k0 += 16) {
+    const int col = (h * dh + k0) * 2;
+    uint32_t af[MI][4];
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+      const int row = mi * 16 + rr + 8 * (mat & 1);
+      ldsm_x4(smem_u32(qs + row * ld + col + 16 * (mat >> 1)), af[mi]);
+    }
+#pragma unroll
+    for (int np = 0; np < NJ / 2; ++np) {
+      uint32_t bf[4];
+      const int row = np * 16 + rr + 8 * (mat >> 1);
+      ldsm_x4(smem_u32(ks + row * ld + col + 16 * (mat & 1)), bf);
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi) {
+        mma_16816(acc[mi][2 * np], af[mi], bf[0], bf[1]);
+        mma_16816(acc[mi][2 * np + 1], af[mi], bf[2], bf[3]);
+      }
+    }
+  }
+  // softmax over j of every row i (quad shuffles), t_i = sum_j S_ij u_jh
+  const float sc = rsqrtf((float)dh);
+  float uj[NJ][2];
+#pragma unroll
+  for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = nj * 8 + 2 * tig + e;
+      uj[nj][e] = j < g ? __ldg(a.u + (long long)(first + j) * a.sUj + (long long)r * H + h) : 0.f;
+    }
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {             // fragment rows gid (hr 0) and gid + 8
+      float m = -INFINITY;
+#pragma unroll
+      for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = nj * 8 + 2 * tig + e;
+          const float v = acc[mi][nj][2 * hr + e] * sc;
+          acc[mi][nj][2 * hr + e] = v;
+          if (j < g) m = fmaxf(m, v);
+        }
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+      float sum = 0.f;
+#pragma unroll
+      for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = nj * 8 + 2 * tig + e;
+          const float ev = j < g ? __expf(acc[mi][nj][2 * hr + e] - m) : 0.f;
+          acc[mi][nj][2 * hr + e] = ev;
+          sum += ev;
+        }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      const float inv = 1.f / sum;
+      float tu = 0.f;
+#pragma unroll
+      for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          acc[mi][nj][2 * hr + e] *= inv;
+          tu = fmaf(acc[mi][nj][2 * hr + e], uj[nj][e], tu);
+        }
+      tu += __shfl_xor_sync(0xffffffffu, tu, 1);
+      tu += __shfl_xor_sync(0xffffffffu, tu, 2);
+      if (tig == 0) tsm[h * 32 + mi * 16 + gid + 8 * hr] = tu;
+    }
+  __syncthreads();
+  // s_i = sum_h t_i,h ; p2 = softmax_i(s)  (warp 0)
+  if (warp == 0) {
+    float sv = -INFINITY;
+    if (lane < g) {
+      sv = 0.f;
+      for (int hh = 0; hh < H; ++hh) sv += tsm[hh * 32 + lane];
+    }
+    float m = sv;
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    const float e = act ? __expf(S[i] - m) : 0.f;
+    const float e = lane < g ? __expf(sv - m) : 0.f;
     float sum = e;
 #pragma unroll
     for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    S[i] = e / sum;
-    float tu = S[i] * uj;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) tu += __shfl_xor_sync(0xffffffffu, tu, o);
-    if (lane == 0) t[h * 32 + i] = tu;
+    p2s[lane] = e / sum;
   }
   __syncthreads();
-  // s_i = sum_h t[h][i] -> p2 = softmax_i(s) (every warp, lane i); w_jh = sum_i p2_i S_ij
-  float s = -INFINITY;
-  if (lane < g) {
-    s = 0.f;
-    for (int hh = 0; hh < H; ++hh) s += t[hh * 32 + lane];
-  }
-  float m = s;
+  // w_jh = sum_i p2_i S_ij : per column j, reduce over the fragment rows (gid, m-tiles)
+  float pr[MI][2];
 #pragma unroll
-  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  const float e = lane < g ? __expf(s - m) : 0.f;
-  float sum = e;
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  const float p2 = e / sum;  // lane i holds p2_i
-  float wj = 0.f;
-  for (int i = 0; i < g; ++i) wj += __shfl_sync(0xffffffffu, p2, i) * (act ? S[i] : 0.f);
-  if (act) a.w[(((long long)n * a.R + r) * a.max_g + lane) * H + h] = wj;
+    for (int hr = 0; hr < 2; ++hr) pr[mi][hr] = p2s[mi * 16 + gid + 8 * hr];  // 0 beyond g
+#pragma unroll
+  for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      float wj = 0.f;
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) wj = fmaf(pr[mi][hr], acc[mi][nj][2 * hr + e], wj);
+      wj += __shfl_xor_sync(0xffffffffu, wj, 4);
+      wj += __shfl_xor_sync(0xffffffffu, wj, 8);
+      wj += __shfl_xor_sync(0xffffffffu, wj, 16);
+      const int j = nj * 8 + 2 * tig + e;
+      if (gid == 0 && j < g) a.w[(((long long)n * a.R + r) * a.max_g + j) * H + h] = wj;
+    }
 }
 
 cudaError_t launch_fullcross_weights(const FullCrossArgs& a, cudaStream_t st) {
   const int dh = a.D / a.H;
-  if (a.max_g > 32 || a.H > 32 || dh % 8 || a.H < 1) return cudaErrorInvalidValue;
-  const size_t smem = ((size_t)a.H * a.max_g * dh + (size_t)a.H * 32) * sizeof(float);
+  if (a.max_g > 32 || a.H > 32 || dh % 16 || a.H < 1 || a.D % 8) return cudaErrorInvalidValue;
+  const int MI = a.max_g > 16 ? 2 : 1;
+  const size_t smem = (size_t)2 * 16 * MI * (a.D * 2 + 16) + ((size_t)a.H * 32 + 32) * 4;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(fullcross_weights_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = MI == 2 ? fullcross_weights_kernel<2> : fullcross_weights_kernel<1>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
   if (e != cudaSuccess) return e;
-  fullcross_weights_kernel<<<(unsigned)((long long)a.n_nodes * a.R), a.H * 32, smem, st>>>(a);
+  kern<<<(unsigned)((long long)a.n_nodes * a.R), a.H * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -184,6 +184,10 @@ struct FullCrossArgs {
   const float* u;              // child j row r: u at u + j*sUj + r*H  (V_j,h . (wo rq)_h / sqrt D)
   long long sUj;
   float* w;                    // [n][R][max_g][H]
+  // optional positional query (level 0 with the tokenizer folded): q_i += posq[n][r % S]
+  // while staging (the key/value/u positional terms cancel in the softmaxes)
+  const __nv_bfloat16* posq;   // [n][S][D] bf16 or null
+  int S;
 };
 cudaError_t launch_fullcross_weights(const FullCrossArgs& a, cudaStream_t st);
 

@@ -239,10 +239,11 @@ class DchagFrontEnd(torch.nn.Module):
         return self.model.agg_variant == "full_cross" or self.precision == "fp32"
 
     def _forward_full_cross(self, images, out=None):
-        """agg_variant='full_cross' (layers.py:125-138): the tokens are materialised
-        (ops.tokenize_channels), each rank aggregates its slab with full_cross tree nodes
-        (ops.tree_aggregate), the [B,1,S,D] root streams are all-gathered in rank order and the
-        shared final node runs over them (model.py:180-201 / strategies.py:199-218)."""
+        """agg_variant='full_cross' (layers.py:125-138): level 0 projects the patches straight
+        into each node's [q | k | v | u] space (ops.full_cross_level0_qkv: the tokenizer folded,
+        tokens never formed), the levels above run ops._full_cross_tree on the node outputs,
+        the [B,1,S,D] root streams are all-gathered in rank order and the shared final node
+        runs over them (model.py:180-201 / strategies.py:199-218)."""
         from . import ops
         w = self.weights
         m = self.model
@@ -250,12 +251,20 @@ class DchagFrontEnd(torch.nn.Module):
         sl = slice(off, off + cnt)
         if self.precision == "fp32":
             return self._forward_fp32(images, out)
-        tok = ops.tokenize_channels(images, w["tok.w"][sl], w["tok.b"][sl],
-                                    w["special.channel_id"][sl], w["special.pos"], m.patch,
-                                    out_dtype=torch.bfloat16)
-        y = ops.tree_aggregate(tok, self.tree, w, f"agg.slab{self.rank}",
-                               self.strategy.agg_layer_kind, "full_cross", m.heads,
-                               out_dtype=torch.bfloat16)                       # [B,1,S,D]
+        pre = f"agg.slab{self.rank}"
+        if self.strategy.agg_layer_kind != "linear":
+            # level 0 with the tokenizer folded into q / k / v / u (no token tensor)
+            lvl0 = ops.full_cross_level0_qkv(images, w["tok.w"][sl], w["tok.b"][sl],
+                                             w["special.channel_id"][sl], w["special.pos"],
+                                             self.tree, w, pre, m.heads, m.patch)
+            y = ops._full_cross_tree((images.shape[0], self.seq, m.embed), self.tree, w, pre,
+                                     m.heads, torch.bfloat16, level0=lvl0)     # [B,1,S,D]
+        else:
+            tok = ops.tokenize_channels(images, w["tok.w"][sl], w["tok.b"][sl],
+                                        w["special.channel_id"][sl], w["special.pos"], m.patch,
+                                        out_dtype=torch.bfloat16)
+            y = ops.tree_aggregate(tok, self.tree, w, pre, self.strategy.agg_layer_kind,
+                                   "full_cross", m.heads, out_dtype=torch.bfloat16)
         if self.tp > 1:
             y = y.contiguous()
             allg = torch.empty((self.tp,) + tuple(y.shape), device=y.device, dtype=y.dtype)

@@ -834,7 +834,7 @@ class DchagTrainer:
                 dl = torch.empty(g, H, R, device=dev)
                 dlb = torch.empty(g, H, R, device=dev, dtype=torch.bfloat16)
                 _lib.call("dchag_l0_softmax_bwd", g, R, H, st["NH"], dh, _ptr(dpp), _ptr(Gpos),
-                          _ptr(pblk), _ptr(dl), _ptr(dlb), sh,
+                          _ptr(pblk), _lib.ptr(dl), _ptr(dlb), sh,
                           work={"site": "bwd:l0_softmax", "bytes": 4 * g * R * D // 32})
             else:
                 dp = dpp.view(g, H, dh // 32, R).sum(2) + Gpos.t().unsqueeze(0)

@@ -1,0 +1,34 @@
+"""Times dchag_l0_tgrad_te (the training step's level-0 [patch | 1]^T [p G | dl] kernel) at the
+TR node shape (16 channels, R = 8192, D = 2048, H = 32)."""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+from paper_2506_21411_b200 import _lib  # noqa: E402
+
+B, S, PP, D, H, NH, g = 32, 256, 64, 2048, 32, 4, 16
+R = B * S
+patches = torch.randn(B, g, S, PP, device="cuda").to(torch.bfloat16)
+G = torch.randn(R, D, device="cuda").to(torch.bfloat16)
+p = torch.rand(H // NH, g, R, NH, device="cuda").to(torch.bfloat16)
+dlb = torch.randn(g, H, R, device="cuda").to(torch.bfloat16)
+Dp = 2304
+TE = torch.zeros(g * PP + 128, Dp, device="cuda", dtype=torch.bfloat16)
+st = _lib.stream_handle()
+
+
+def te():
+    _lib.call("dchag_l0_tgrad_te", _lib.ptr(patches), g, 0, g, R, S, D, H, NH, PP, _lib.ptr(p), 0,
+              _lib.ptr(G), _lib.ptr(dlb), _lib.ptr(TE), Dp, g * PP, st)
+
+
+for _ in range(3):
+    te()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize()
+e0.record()
+for _ in range(20):
+    te()
+e1.record()
+torch.cuda.synchronize()
+print(f"l0_tgrad_te {e0.elapsed_time(e1) / 20:.3f} ms per node")
