@@ -394,11 +394,21 @@ def b200_arm(args, wl, tp, max_group):
                              generator=gen).to(torch.bfloat16)
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device="cuda")
 
+    trace = os.environ.get("DCHAG_BENCH_TRACE") == "1"
+
+    def mark(what):
+        if trace:
+            print(f"[bench rank {rank}] {what} {time.perf_counter():.3f}", file=sys.stderr,
+                  flush=True)
+
     def barrier():
+        mark("barrier: sync")
         torch.cuda.synchronize()
+        mark("barrier: dist")
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        mark("barrier: done")
 
     def timed(step_fn, k, per_step_hook=None):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -436,7 +446,9 @@ def b200_arm(args, wl, tp, max_group):
         else:
             # the whole step (forward_train + backward, collectives included) as one CUDA
             # graph over the static image / probe buffers: a replay re-runs every kernel
+            mark("capture")
             gstep = trainer.capture(images, probe)
+            mark("captured")
             step = gstep.replay
     elif arch_tp:
         slabs_img = [images[:, f.slab[0]:f.slab[0] + f.slab[1]] for f in fes]
@@ -449,8 +461,12 @@ def b200_arm(args, wl, tp, max_group):
         step = lambda: fe(images)  # noqa: E731
         eager_step = step
     clk = ClockSampler(local).__enter__()
-    for _ in range(args.warmup):
+    for i in range(args.warmup):
         step()
+        # each warm-up step completes before the next is issued (graph replays with NCCL
+        # kernels queued back to back in the warm-up hung at 4 ranks)
+        torch.cuda.synchronize()
+        mark(f"warmup {i} done")
     t_end = time.perf_counter() + 0.5  # let clocks settle: >= 0.5 s of warm-up work
     while time.perf_counter() < t_end:
         step()

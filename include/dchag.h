@@ -259,11 +259,15 @@ int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, c
  * posq (optional, bf16 [n_nodes][seq][D]): added to every q of row r at position r % seq
  * (level 0 with the tokenizer folded: the positional parts of k, v and u cancel in the
  * softmaxes or are added to the context, so only the query's enters here).
+ * pout (optional): the weights go out as dchag_l0_node's bf16 p operand instead of w
+ * (pout[node_poff[n] + ((h/nh * g + j)*R + r)*nh + h%nh]): level 0 then sums the children's
+ * values on the tensor cores from the patches (the single_query K_l0, p = w).
  * max_g <= 32, H <= 32, (D/H) % 16 == 0. */
 int dchag_fullcross_weights(int n_nodes, int R, int D, int H, const int* node_first,
                             const int* node_g, int max_g, const void* QK, long long sQj,
                             long long ldq, const float* u, long long sUj, float* w,
-                            const void* posq, int seq, void* stream);
+                            const void* posq, int seq, void* pout, const long long* node_poff,
+                            int nh, void* stream);
 
 /* ctx[n][r][h-blk] = sum_j w[n][r][j][h] V_j[r][h-blk]; V_j row r at V + j*sVj + r*ldv (bf16). */
 int dchag_combine_weighted(int n_nodes, int R, int D, int H, const int* node_first,

@@ -47,7 +47,7 @@ SIGNATURES = {
     "dchag_combine_f32": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_vp, c_ll,
                           c_vp, c_vp, c_vp],
     "dchag_fullcross_weights": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_ll,
-                                c_vp, c_ll, c_vp, c_vp, c_int, c_vp],
+                                c_vp, c_ll, c_vp, c_vp, c_int, c_vp, c_vp, c_int, c_vp],
     "dchag_combine_weighted": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_ll,
                                c_vp, c_vp, c_vp],
     "dchag_combine_strided": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_ll,

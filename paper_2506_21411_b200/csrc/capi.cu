@@ -633,7 +633,8 @@ int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, c
 int dchag_fullcross_weights(int n_nodes, int R, int D, int H, const int* node_first,
                             const int* node_g, int max_g, const void* QK, long long sQj,
                             long long ldq, const float* u, long long sUj, float* w,
-                            const void* posq, int seq, void* stream) {
+                            const void* posq, int seq, void* pout, const long long* node_poff,
+                            int nh, void* stream) {
   if (D % H || (D / H) % 16 || max_g < 1 || max_g > 32 || H > 32 || ldq < 2 * D || (ldq * 2) % 16 ||
       (sQj * 2) % 16 || reinterpret_cast<uintptr_t>(QK) % 16)
     return fail(DCHAG_ERR_SHAPE, "fullcross_weights: bad shape");
@@ -644,6 +645,10 @@ int dchag_fullcross_weights(int n_nodes, int R, int D, int H, const int* node_fi
   a.QK = reinterpret_cast<const __nv_bfloat16*>(QK); a.sQj = sQj; a.ldq = ldq;
   a.u = u; a.sUj = sUj; a.w = w;
   a.posq = reinterpret_cast<const __nv_bfloat16*>(posq); a.S = seq > 0 ? seq : 1;
+  a.pout = reinterpret_cast<__nv_bfloat16*>(pout); a.node_poff = node_poff; a.nh = nh;
+  if (pout && (!node_poff || nh < 1 || H % nh))
+    return fail(DCHAG_ERR_SHAPE, "fullcross_weights: p output needs node_poff and nh | H");
+  if (!pout && !w) return fail(DCHAG_ERR_SHAPE, "fullcross_weights: no output");
   if (posq && (seq < 1 || R % seq)) return fail(DCHAG_ERR_SHAPE, "fullcross_weights: bad seq");
   return cuda_status(launch_fullcross_weights(a, S(stream)), "fullcross_weights");
 }

@@ -559,17 +559,55 @@ __global__ void __launch_bounds__(256) l0_softmax_bwd_kernel(
   const int hg = h / NH, hn = h - hg * NH, np_ = dh / 32, D32 = H * np_;
   const float gp = __ldg(Gpos + (size_t)r * H + h);
   float sdp = 0.f;
-  for (int c = 0; c < g; ++c) {
+  // channels four at a time: every load of a group is issued before any is consumed
+  // (the kernel is load-latency bound; one channel at a time kept ~1 load in flight)
+  auto dp_load = [&](int c) {
     float dp = gp;
+#pragma unroll 4
     for (int k = 0; k < np_; ++k) dp += __ldg(dpp + ((size_t)c * D32 + h * np_ + k) * R + r);
-    const float pc = __bfloat162float(p[((size_t)(hg * g + c) * R + r) * NH + hn]);
-    sdp = fmaf(pc, dp, sdp);
-    dl[((size_t)c * H + h) * R + r] = dp;  // dp for now; scaled below
+    return dp;
+  };
+  auto p_load = [&](int c) {
+    return __bfloat162float(p[((size_t)(hg * g + c) * R + r) * NH + hn]);
+  };
+  int c = 0;
+  for (; c + 4 <= g; c += 4) {
+    float dp[4], pc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      dp[u] = dp_load(c + u);
+      pc[u] = p_load(c + u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      sdp = fmaf(pc[u], dp[u], sdp);
+      dl[((size_t)(c + u) * H + h) * R + r] = dp[u];  // dp for now; scaled below
+    }
   }
-  for (int c = 0; c < g; ++c) {
+  for (; c < g; ++c) {
+    const float dp = dp_load(c), pc = p_load(c);
+    sdp = fmaf(pc, dp, sdp);
+    dl[((size_t)c * H + h) * R + r] = dp;
+  }
+  c = 0;
+  for (; c + 4 <= g; c += 4) {
+    float d[4], pc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      d[u] = dl[((size_t)(c + u) * H + h) * R + r];
+      pc[u] = p_load(c + u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const size_t o = ((size_t)(c + u) * H + h) * R + r;
+      const float v = pc[u] * (d[u] - sdp);
+      dl[o] = v;
+      dlb[o] = __float2bfloat16(v);
+    }
+  }
+  for (; c < g; ++c) {
     const size_t o = ((size_t)c * H + h) * R + r;
-    const float pc = __bfloat162float(p[((size_t)(hg * g + c) * R + r) * NH + hn]);
-    const float v = pc * (dl[o] - sdp);
+    const float v = p_load(c) * (dl[o] - sdp);
     dl[o] = v;
     dlb[o] = __float2bfloat16(v);
   }
@@ -756,7 +794,15 @@ __global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a
       wj += __shfl_xor_sync(0xffffffffu, wj, 8);
       wj += __shfl_xor_sync(0xffffffffu, wj, 16);
       const int j = nj * 8 + 2 * tig + e;
-      if (gid == 0 && j < g) a.w[(((long long)n * a.R + r) * a.max_g + j) * H + h] = wj;
+      if (gid == 0 && j < g) {
+        if (a.pout) {
+          const int hg = h / a.nh;
+          a.pout[__ldg(a.node_poff + n) + (((long long)hg * g + j) * a.R + r) * a.nh + h % a.nh] =
+              __float2bfloat16(wj);
+        } else {
+          a.w[(((long long)n * a.R + r) * a.max_g + j) * H + h] = wj;
+        }
+      }
     }
 }
 

@@ -188,6 +188,11 @@ struct FullCrossArgs {
   // while staging (the key/value/u positional terms cancel in the softmaxes)
   const __nv_bfloat16* posq;   // [n][S][D] bf16 or null
   int S;
+  // optional: w written as K_l0's bf16 p operand (dchag_l0_logits layout, normalised) instead
+  // of the fp32 table: pout[poff[n] + ((h/nh * g + j) * R + r) * nh + h % nh]
+  __nv_bfloat16* pout;
+  const long long* node_poff;
+  int nh;
 };
 cudaError_t launch_fullcross_weights(const FullCrossArgs& a, cudaStream_t st);
 

@@ -865,11 +865,20 @@ __global__ void __launch_bounds__(192, 2)
           a.p + ((size_t)(hg * a.g + c) * a.R + i * 64 + row) * a.NH + hn));
       return sel ? bf16hi(w) : bf16lo(w);
     };
-    float pn = eblk ? 0.f : pval(0);
+    // p of the next four stages in flight (a rotating register queue): one stage ahead left
+    // the L2 latency of the p loads exposed (long-scoreboard stalls dominated)
+    float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+    if (!eblk) {
+      p0 = pval(0);
+      if (nst > 1) p1 = pval(1);
+      if (nst > 2) p2 = pval(2);
+      if (nst > 3) p3 = pval(3);
+    }
     for (int i = 0; i < nst; ++i) {
       const int s = i % TGC_STAGES;
-      const float pc = pn;
-      if (!eblk && i + 1 < nst) pn = pval(i + 1);  // next stage's p in flight during this one
+      const float pc = p0;
+      p0 = p1; p1 = p2; p2 = p3;
+      if (!eblk && i + 4 < nst) p3 = pval(i + 4);
       mbar_wait(&full[s], (i / TGC_STAGES) & 1);
       if (!eblk) {
         const uint32_t rowaddr = smem_u32(smem + s * TGC_STAGE) + mh * (TGC_A_BYTES / 2) +

@@ -229,6 +229,40 @@ def unit_heads(embed: int, heads: int) -> int:
     return 2 if embed // heads == 128 else (4 if heads % 4 == 0 else 2)
 
 
+def tile_values_l0(M, Cb, posV, l0_c0, l0_g, d, h, pp, device):
+    """K_l0's value operands from the level-0 value folds M_c = tok.w[c] wv_n ([C, PP, D]),
+    Cb_c = tb_c wv_n ([C, D]) and posV_n = pos wv_n ([n0, S, D]): Mt / Et as canonical UMMA
+    blocks (dchag_tile_weights) and posV0 bf16. Shared by single_query and full_cross."""
+    from . import _lib
+    f32 = dict(device=device, dtype=torch.float32)
+    stream = _lib.stream_handle()
+    C = M.shape[0]
+    C_pad = C + 64 // pp
+    n0 = len(l0_g)
+    KE = 16 * ((max(l0_g) + 15) // 16)
+
+    def tile(src, nblk, K, N):
+        src = src.to(**f32).contiguous()
+        dst = torch.empty(nblk * N * K, device=device, dtype=torch.bfloat16)
+        _lib.call("dchag_tile_weights", _lib.ptr(src), nblk, K, N, _lib.ptr(dst), stream)
+        return dst
+
+    # Mt [H][2 halves][C_pad*PP (channel-major K)][dh/2]: a CTA pair splits each head's dh
+    # output columns, and one stage's K rows (CG channels) are one contiguous block per half
+    dh = d // h
+    hw = dh // 2
+    Msrc = torch.zeros(h, C_pad, pp, 2, hw, **f32)
+    Msrc[:, :C] = M.to(**f32).view(C, pp, h, 2, hw).permute(2, 0, 1, 3, 4)
+    Mt = tile(Msrc.permute(0, 3, 1, 2, 4).reshape(h * 2, C_pad * pp, hw), h * 2, C_pad * pp, hw)
+    # Et [n0][H][2][KE][dh/2]: row k = node-local channel
+    Esrc = torch.zeros(n0, h, KE, 2, hw, **f32)
+    for n, (c0, g) in enumerate(zip(l0_c0, l0_g)):
+        Esrc[n, :, :g] = Cb[c0:c0 + g].to(**f32).view(g, h, 2, hw).permute(1, 0, 2, 3)
+    Et = tile(Esrc.permute(0, 1, 3, 2, 4).reshape(n0 * h * 2, KE, hw), n0 * h * 2, KE, hw)
+    posV0 = posV.to(**f32).to(torch.bfloat16).contiguous()
+    return Mt, Et, posV0
+
+
 def pack_rank(fr: FoldedRank, device) -> PackedRank:
     from . import _lib
 
@@ -243,25 +277,7 @@ def pack_rank(fr: FoldedRank, device) -> PackedRank:
     f32 = dict(device=device, dtype=torch.float32)
     stream = _lib.stream_handle()
 
-    def tile(src, nblk, K, N):
-        src = src.to(**f32).contiguous()
-        dst = torch.empty(nblk * N * K, device=device, dtype=torch.bfloat16)
-        _lib.call("dchag_tile_weights", _lib.ptr(src), nblk, K, N, _lib.ptr(dst), stream)
-        return dst
-
-    # Mt [H][2 halves][C_pad*PP (channel-major K)][dh/2]: a CTA pair splits each head's dh
-    # output columns, and one stage's K rows (CG channels) are one contiguous block per half
-    dh = d // h
-    hw = dh // 2
-    Msrc = torch.zeros(h, C_pad, pp, 2, hw, **f32)
-    Msrc[:, :C] = fr.M.to(**f32).view(C, pp, h, 2, hw).permute(2, 0, 1, 3, 4)
-    Mt = tile(Msrc.permute(0, 3, 1, 2, 4).reshape(h * 2, C_pad * pp, hw), h * 2, C_pad * pp, hw)
-    # Et [n0][H][2][KE][dh/2]: row k = node-local channel
-    Esrc = torch.zeros(n0, h, KE, 2, hw, **f32)
-    for n, (c0, g) in enumerate(zip(fr.l0_c0, fr.l0_g)):
-        Esrc[n, :, :g] = fr.Cb[c0:c0 + g].to(**f32).view(g, h, 2, hw).permute(1, 0, 2, 3)
-    Et = tile(Esrc.permute(0, 1, 3, 2, 4).reshape(n0 * h * 2, KE, hw), n0 * h * 2, KE, hw)
-    posV0 = fr.posV.to(**f32).to(torch.bfloat16).contiguous()
+    Mt, Et, posV0 = tile_values_l0(fr.M, fr.Cb, fr.posV, fr.l0_c0, fr.l0_g, d, h, pp, device)
     WUt = bU = posU = p_const = None
     if fr.attn_l0:
         wu = torch.zeros(C, HP, pp, **f32)

@@ -239,9 +239,10 @@ class DchagFrontEnd(torch.nn.Module):
         return self.model.agg_variant == "full_cross" or self.precision == "fp32"
 
     def _forward_full_cross(self, images, out=None):
-        """agg_variant='full_cross' (layers.py:125-138): level 0 projects the patches straight
-        into each node's [q | k | v | u] space (ops.full_cross_level0_qkv: the tokenizer folded,
-        tokens never formed), the levels above run ops._full_cross_tree on the node outputs,
+        """agg_variant='full_cross' (layers.py:125-138): level 0 with the tokenizer folded
+        (ops.full_cross_level0: q | k | u from the patches, the channel-attention weights,
+        then K_l0 sums the children's values from the patches; tokens never formed), the
+        levels above run ops._full_cross_tree on the node outputs,
         the [B,1,S,D] root streams are all-gathered in rank order and the shared final node
         runs over them (model.py:180-201 / strategies.py:199-218)."""
         from . import ops
@@ -254,11 +255,11 @@ class DchagFrontEnd(torch.nn.Module):
         pre = f"agg.slab{self.rank}"
         if self.strategy.agg_layer_kind != "linear":
             # level 0 with the tokenizer folded into q / k / v / u (no token tensor)
-            lvl0 = ops.full_cross_level0_qkv(images, w["tok.w"][sl], w["tok.b"][sl],
-                                             w["special.channel_id"][sl], w["special.pos"],
-                                             self.tree, w, pre, m.heads, m.patch)
+            y0 = ops.full_cross_level0(images, w["tok.w"][sl], w["tok.b"][sl],
+                                       w["special.channel_id"][sl], w["special.pos"],
+                                       self.tree, w, pre, m.heads, m.patch)
             y = ops._full_cross_tree((images.shape[0], self.seq, m.embed), self.tree, w, pre,
-                                     m.heads, torch.bfloat16, level0=lvl0)     # [B,1,S,D]
+                                     m.heads, torch.bfloat16, x0=y0)           # [B,1,S,D]
         else:
             tok = ops.tokenize_channels(images, w["tok.w"][sl], w["tok.b"][sl],
                                         w["special.channel_id"][sl], w["special.pos"], m.patch,

@@ -72,74 +72,21 @@ def tokenize_channels(images, tok_w, tok_b, chan_id, pos, patch, out_dtype=torch
     return out
 
 
-def full_cross_level0_qkv(images, tok_w, tok_b, chan_id, pos, spec: TreeSpec, w, prefix,
-                          n_heads, patch):
-    """Level 0 of a full_cross tree without forming the tokens (the single_query path's
-    tokenizer fold, fold.py, applied to q, k, v and u): x_c = patch_c tok.w[c] + tb_c + pos,
-    so [q | k | v | u]_c = patch_c (tok.w[c] Wfc_n) + tb_c Wfc_n + pos Wfc_n with
-    Wfc_n = [wq | wk | wv | Wu] of the channel's node n. One grouped K = P*P GEMM per node
-    (group = channel; tb_c Wfc_n as the bias, pos Wfc_n as the periodic row bias): 16x fewer
-    flops than projecting materialised D-wide tokens. Returns QKV bf16 [C, R, 3D] and
-    U fp32 [C, R, H] (rows r = b*S + s), the inputs of dchag_fullcross_weights."""
-    B, C, Hh, Ww = images.shape
-    D = tok_w.shape[-1]
-    H = n_heads
-    S, PP = (Hh // patch) * (Ww // patch), patch * patch
-    R = B * S
-    N = 3 * D + H
-    img = _bf(images)
-    st = _lib.stream_handle()
-    patches = torch.empty(B, C, S, PP, device="cuda", dtype=torch.bfloat16)
-    _lib.call("dchag_unfold", _lib.ptr(img), img.stride(0), img.stride(1), B, C, Hh, Ww, patch,
-              _lib.ptr(patches), st, work={"site": "ops:unfold", "bytes": 4 * img.numel()})
-    tw = {k: _f32(v) for k, v in w.items() if k.startswith(prefix + ".")}
-    folded = _fc_level0_fold(tok_w, tok_b, chan_id, pos, spec, tw, prefix, D, H)
-    QKV = torch.empty(C, R, 3 * D, device="cuda", dtype=torch.bfloat16)
-    U = torch.empty(C, R, H, device="cuda", dtype=torch.float32)
-    c0 = 0
-    for gi, g in enumerate(spec.levels[0]):
-        Mt, bias = folded["nodes"][gi]                # [g, N, PP] bf16, [g, N] fp32
-        # no positional row bias here: the positional parts of k, v and u cancel in the
-        # softmaxes or go to the context (fold below); q's enters in dchag_fullcross_weights
-        if H % 16:  # u too narrow for a GEMM of its own: one launch, u as the logit columns
-            _lib.call("dchag_gemm_bf16", _lib.ptr(patches[:, c0]), g, B, S, PP, S * PP,
-                      C * S * PP, PP, _lib.ptr(Mt), N, N * PP, 3 * D, _lib.ptr(bias), N,
-                      0, 0, 0, 1, _lib.ptr(QKV[c0]), 0, R * 3 * D, S * 3 * D,
-                      3 * D, _lib.ptr(U[c0]), R * H, S * H, H, st,
-                      work={"site": "ops:fc_l0_qkv", "flops": 2 * g * R * PP * N})
-            c0 += g
-            continue
-        # q | k | v (N = 3D: whole 256-column tiles, TMA-stored) and u (N = H, fp32) apart
-        _lib.call("dchag_gemm_bf16", _lib.ptr(patches[:, c0]), g, B, S, PP, S * PP,
-                  C * S * PP, PP, _lib.ptr(Mt), 3 * D, N * PP, 3 * D, _lib.ptr(bias), N,
-                  0, 0, 0, 1, _lib.ptr(QKV[c0]), 0, R * 3 * D, S * 3 * D, 3 * D,
-                  0, 0, 0, 0, st,
-                  work={"site": "ops:fc_l0_qkv", "flops": 2 * g * R * PP * 3 * D})
-        _lib.call("dchag_gemm_bf16", _lib.ptr(patches[:, c0]), g, B, S, PP, S * PP,
-                  C * S * PP, PP, _lib.ptr(Mt[:, 3 * D:]), H, N * PP, 0,
-                  _lib.ptr(bias[:, 3 * D:]), N, 0, 0, 0, 1, 0, 0, 0, 0,
-                  0, _lib.ptr(U[c0]), R * H, S * H, H, st,
-                  work={"site": "ops:fc_l0_u", "flops": 2 * g * R * PP * H})
-        c0 += g
-    return QKV, U, folded["posq"], folded["posvo"]
-
-
 _FC0_CACHE: dict = {}
 
 
 def _fc_level0_fold(tok_w, tok_b, chan_id, pos, spec, tw, prefix, D, H):
-    """Per level-0 node: (tok.w[c] Wfc)^T bf16 [g, 3D+H, PP] and tb_c Wfc fp32 [g, 3D+H]
-    (tb = tok.b + chan_id, Wfc = [wq | wk | wv | Wu]); per node the positional query
-    pos wq (bf16 [n0, S, D]) and the positional value through the output projection,
-    pos wv wo (bf16 [n0, S, D]: the w-weighted sum of the children's pos wv is pos wv itself,
-    the weights summing to 1). Folded once per weight version."""
+    """Folded level-0 operands of a full_cross tree, once per weight version:
+    per node (tok.w[c] [wq | wk | Wu])^T bf16 [g, 2D+H, PP] and tb_c [wq | wk | Wu] fp32
+    [g, 2D+H] (tb = tok.b + chan_id); the positional query pos wq (bf16 [n0, S, D]); and the
+    value folds K_l0 takes: M_c = tok.w[c] wv ([C, PP, D]), Cb_c = tb_c wv, posV_n = pos wv."""
     srcs = [tok_w, tok_b, chan_id, pos] + [tw[k] for k in sorted(tw)]
     key = (prefix, D, H, spec.levels) + tuple((t.data_ptr(), t._version, tuple(t.shape))
                                               for t in srcs)
     hit = _FC0_CACHE.get(prefix)
     if hit is not None and hit[0] == key:
         return hit[1]
-    nodes, pq, pvo = [], [], []
+    nodes, pq, Ms, Cbs, posV, c0s = [], [], [], [], [], []
     c0 = 0
     with torch.no_grad():
         tb = _f32(tok_b) + _f32(chan_id)
@@ -147,18 +94,115 @@ def _fc_level0_fold(tok_w, tok_b, chan_id, pos, spec, tw, prefix, D, H):
         for gi, g in enumerate(spec.levels[0]):
             node = f"{prefix}.l0.g{gi}"
             Wnk, _, _ = _fc_node_weights(tw, node, D, H)          # [3D+H, D] bf16
-            Wfc = Wnk.float().t()                                   # [D, 3D+H]
-            M = torch.matmul(_f32(tok_w[c0:c0 + g]), Wfc)           # [g, PP, 3D+H]
-            nodes.append((_bf(M.transpose(1, 2)), (_f32(tb[c0:c0 + g]) @ Wfc).contiguous()))
+            Wqku = torch.cat([tw[f"{node}.wq"], tw[f"{node}.wk"],
+                              Wnk[3 * D:].float().t()], dim=1)      # [D, 2D+H]
+            twc = _f32(tok_w[c0:c0 + g])
+            M = torch.matmul(twc, Wqku)                             # [g, PP, 2D+H]
+            nodes.append((_bf(M.transpose(1, 2)), (tb[c0:c0 + g] @ Wqku).contiguous()))
             pq.append(p32 @ tw[f"{node}.wq"])
-            pvo.append(p32 @ tw[f"{node}.wv"] @ tw[f"{node}.wo"])
+            wv = tw[f"{node}.wv"]
+            Ms.append(torch.matmul(twc, wv))
+            Cbs.append(tb[c0:c0 + g] @ wv)
+            posV.append(p32 @ wv)
+            c0s.append(c0)
             c0 += g
-    out = {"nodes": nodes, "posq": _bf(torch.stack(pq)), "posvo": _bf(torch.stack(pvo))}
+    out = {"nodes": nodes, "posq": _bf(torch.stack(pq)), "M": torch.cat(Ms),
+           "Cb": torch.cat(Cbs), "posV": torch.stack(posV), "c0s": c0s, "kl0": None}
     _FC0_CACHE[prefix] = (key, out)
     return out
 
 
-def _full_cross_tree(tokens, spec: TreeSpec, w, prefix, n_heads, out_dtype, level0=None):
+def full_cross_level0(images, tok_w, tok_b, chan_id, pos, spec: TreeSpec, w, prefix, n_heads,
+                      patch):
+    """Level 0 of a full_cross tree with the tokenizer folded everywhere (tokens, and the
+    children's values, never reach memory):
+      1. q | k | u of every channel straight from the patches (K = P*P GEMM on the folded
+         weights tok.w[c] [wq | wk | Wu], bias tb_c [...]; positional terms below),
+      2. dchag_fullcross_weights -> per (child, head) weights w, written as K_l0's p operand
+         (q gets the positional query pos wq; the key / u positional terms cancel in the
+         softmaxes),
+      3. dchag_l0_node (K_l0, tcgen05): ctx = sum_c w_c (patch_c M_c + Cb_c) + pos wv with
+         M_c = tok.w[c] wv, the single_query level-0 kernel with p = w (sum_c w_c = 1),
+      4. y = ctx wo + bo per node.
+    Returns y bf16 [n0, R, D] (node-major rows r = b*S + s)."""
+    from .fold import tile_values_l0, unit_heads
+    B, C, Hh, Ww = images.shape
+    D = tok_w.shape[-1]
+    H = n_heads
+    S, PP = (Hh // patch) * (Ww // patch), patch * patch
+    R = B * S
+    NQ = 2 * D + H
+    img = images if images.dtype == torch.bfloat16 else images.to(torch.bfloat16)
+    if img.stride(3) != 1 or img.stride(2) != Ww:
+        img = img.contiguous()
+    st = _lib.stream_handle()
+    patches = torch.empty(B, C, S, PP, device="cuda", dtype=torch.bfloat16)
+    _lib.call("dchag_unfold", _lib.ptr(img), img.stride(0), img.stride(1), B, C, Hh, Ww, patch,
+              _lib.ptr(patches), st, work={"site": "ops:unfold", "bytes": 4 * img.numel()})
+    tw = {k: _f32(v) for k, v in w.items() if k.startswith(prefix + ".")}
+    fd = _fc_level0_fold(tok_w, tok_b, chan_id, pos, spec, tw, prefix, D, H)
+    levels0 = spec.levels[0]
+    n0 = len(levels0)
+    if fd["kl0"] is None:
+        fd["kl0"] = tile_values_l0(fd["M"], fd["Cb"], fd["posV"], fd["c0s"], list(levels0), D, H,
+                                   PP, images.device)
+    Mt, Et, posV0 = fd["kl0"]
+    QK = torch.empty(C, R, 2 * D, device="cuda", dtype=torch.bfloat16)
+    U = torch.empty(C, R, H, device="cuda", dtype=torch.float32)
+    c0 = 0
+    for gi, g in enumerate(levels0):
+        Mq, bias = fd["nodes"][gi]                    # [g, NQ, PP] bf16, [g, NQ] fp32
+        if H % 16:  # u too narrow for a GEMM of its own: one launch, u as the logit columns
+            _lib.call("dchag_gemm_bf16", _lib.ptr(patches[:, c0]), g, B, S, PP, S * PP,
+                      C * S * PP, PP, _lib.ptr(Mq), NQ, NQ * PP, 2 * D, _lib.ptr(bias), NQ,
+                      0, 0, 0, 1, _lib.ptr(QK[c0]), 0, R * 2 * D, S * 2 * D, 2 * D,
+                      _lib.ptr(U[c0]), R * H, S * H, H, st,
+                      work={"site": "ops:fc_l0_qk", "flops": 2 * g * R * PP * NQ})
+        else:
+            _lib.call("dchag_gemm_bf16", _lib.ptr(patches[:, c0]), g, B, S, PP, S * PP,
+                      C * S * PP, PP, _lib.ptr(Mq), 2 * D, NQ * PP, 2 * D, _lib.ptr(bias), NQ,
+                      0, 0, 0, 1, _lib.ptr(QK[c0]), 0, R * 2 * D, S * 2 * D, 2 * D, 0, 0, 0, 0,
+                      st, work={"site": "ops:fc_l0_qk", "flops": 2 * g * R * PP * 2 * D})
+            _lib.call("dchag_gemm_bf16", _lib.ptr(patches[:, c0]), g, B, S, PP, S * PP,
+                      C * S * PP, PP, _lib.ptr(Mq[:, 2 * D:]), H, NQ * PP, 0,
+                      _lib.ptr(bias[:, 2 * D:]), NQ, 0, 0, 0, 1, 0, 0, 0, 0, 0, _lib.ptr(U[c0]),
+                      R * H, S * H, H, st,
+                      work={"site": "ops:fc_l0_u", "flops": 2 * g * R * PP * H})
+        c0 += g
+    NH = unit_heads(D, H)
+    poff, acc = [], 0
+    for g in levels0:
+        poff.append(acc)
+        acc += g * R * H
+    poff_t = _dev_i64(poff)
+    pbuf = torch.empty(acc, device="cuda", dtype=torch.bfloat16)
+    first_t, g_t = _dev_i32(fd["c0s"]), _dev_i32(levels0)
+    _lib.call("dchag_fullcross_weights", n0, R, D, H, _lib.ptr(first_t), _lib.ptr(g_t),
+              max(levels0), _lib.ptr(QK), R * 2 * D, 2 * D, _lib.ptr(U), R * H, 0,
+              _lib.ptr(fd["posq"]), S, _lib.ptr(pbuf), _lib.ptr(poff_t), NH, st,
+              work={"site": "ops:fullcross_weights", "bytes": C * R * (4 * D + 4 * H)})
+    ctx = torch.empty(n0, R, D, device="cuda", dtype=torch.bfloat16)
+    _lib.call("dchag_l0_node", _lib.ptr(img), img.stride(0), img.stride(1), B, Hh, Ww, patch, H,
+              D, n0, _lib.ptr(first_t), _lib.ptr(g_t), _lib.ptr(poff_t), 1, _lib.ptr(pbuf), 0,
+              _lib.ptr(Mt), C + 64 // PP, _lib.ptr(Et), 16 * ((max(levels0) + 15) // 16),
+              _lib.ptr(posV0), _lib.ptr(ctx), st,
+              work={"site": "ops:fc_l0_node", "flops": 2 * R * D * C * (PP + 1)})
+    y = torch.empty(n0, R, D, device="cuda", dtype=torch.bfloat16)
+    for k in range(n0):
+        _, Wo, bo = _fc_node_weights(tw, f"{prefix}.l0.g{k}", D, H)
+        _gemm(ctx[k], 1, R, D, 0, D, Wo, bo, y[k], 0, D)
+    return y
+
+
+def _dev_i64(vals):
+    key = ("l", tuple(int(v) for v in vals))
+    t = _SMALL.get(key)
+    if t is None:
+        t = _SMALL[key] = torch.tensor(key[1], device="cuda", dtype=torch.int64)
+    return t
+
+
+def _full_cross_tree(tokens, spec: TreeSpec, w, prefix, n_heads, out_dtype, x0=None):
     """full_cross nodes (layers.py:125-138): per node, the g children attend over each other
     (sdp_attention, layers.py:49-64), then a learned query rq reduces the g outputs. Folded:
     one projection GEMM per node gives [q | k | v | u] with u_jh = v_j,h . (wo rq)_h / sqrt(D)
@@ -168,9 +212,9 @@ def _full_cross_tree(tokens, spec: TreeSpec, w, prefix, n_heads, out_dtype, leve
     H = n_heads
     st = _lib.stream_handle()
     tw = {k: _f32(v) for k, v in w.items() if k.startswith(prefix + ".")}
-    if level0 is not None:  # (QKV, U) of level 0 from the folded tokenizer (no tokens)
+    if x0 is not None:  # level-0 node outputs [n0, R, D] (full_cross_level0): start above
         B, S, D = tokens
-        x = None
+        x = x0
     else:
         B, C, S, D = tokens.shape
         # node-major rows: x[j] is child j's [R, D]
@@ -178,31 +222,28 @@ def _full_cross_tree(tokens, spec: TreeSpec, w, prefix, n_heads, out_dtype, leve
     R = B * S
     depth = len(spec.levels)
     for li, level in enumerate(spec.levels):
+        if x0 is not None and li == 0:
+            continue
         firsts, acc = [], 0
         for g in level:
             firsts.append(acc)
             acc += g
         nodes = [f"{prefix}.l{li}.g{gi}" for gi in range(len(level))]
-        posq = posvo = None
-        if li == 0 and level0 is not None:
-            QKV, U, posq, posvo = level0
-            n_in = QKV.shape[0]
-        else:
-            n_in = x.shape[0]
-            QKV = torch.empty(n_in, R, 3 * D, device="cuda", dtype=torch.bfloat16)
-            U = torch.empty(n_in, R, H, device="cuda", dtype=torch.float32)
-            for node, f, g in zip(nodes, firsts, level):
-                Wnk, _, _ = _fc_node_weights(tw, node, D, H)
-                zero = _zeros(Wnk.shape[0])
-                _gemm(x[f:f + g], 1, g * R, D, 0, D, Wnk, zero, QKV[f:f + g], 0, 3 * D,
-                      U[f:f + g], 0, H)
+        n_in = x.shape[0]
+        QKV = torch.empty(n_in, R, 3 * D, device="cuda", dtype=torch.bfloat16)
+        U = torch.empty(n_in, R, H, device="cuda", dtype=torch.float32)
+        for node, f, g in zip(nodes, firsts, level):
+            Wnk, _, _ = _fc_node_weights(tw, node, D, H)
+            zero = _zeros(Wnk.shape[0])
+            _gemm(x[f:f + g], 1, g * R, D, 0, D, Wnk, zero, QKV[f:f + g], 0, 3 * D,
+                  U[f:f + g], 0, H)
         first_t = _dev_i32(firsts)
         g_t = _dev_i32(level)
         gmax = max(level)
         wts = torch.empty(len(level), R, gmax, H, device="cuda", dtype=torch.float32)
         _lib.call("dchag_fullcross_weights", len(level), R, D, H, _lib.ptr(first_t),
                   _lib.ptr(g_t), gmax, _lib.ptr(QKV), R * 3 * D, 3 * D, _lib.ptr(U), R * H,
-                  _lib.ptr(wts), _lib.ptr(posq), S, st,
+                  _lib.ptr(wts), 0, S, 0, 0, 0, st,
                   work={"site": "ops:fullcross_weights", "bytes": n_in * R * (4 * D + 4 * H)})
         ctx = torch.empty(len(level), R, D, device="cuda", dtype=torch.bfloat16)
         _lib.call("dchag_combine_weighted", len(level), R, D, H, _lib.ptr(first_t),
@@ -215,9 +256,7 @@ def _full_cross_tree(tokens, spec: TreeSpec, w, prefix, n_heads, out_dtype, leve
                         dtype=out_dtype if last else torch.bfloat16)
         for k, node in enumerate(nodes):
             _, Wo, bo = _fc_node_weights(tw, node, D, H)
-            _gemm(ctx[k], 1, R, D, 0, D, Wo, bo, y[k], 0, D, outV_f32=y.dtype == torch.float32,
-                  rowbias=None if posvo is None else posvo[k], rowbias_row=D,
-                  rowbias_period=S)
+            _gemm(ctx[k], 1, R, D, 0, D, Wo, bo, y[k], 0, D, outV_f32=y.dtype == torch.float32)
         x = y
     return x.view(B, 1, S, D) if x.shape[0] == 1 else x.view(1, B, S, D).transpose(0, 1)
 

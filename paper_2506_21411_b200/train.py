@@ -324,6 +324,10 @@ class DchagTrainer:
         with torch.cuda.graph(graph):
             out, saved = self.forward_train(images)
             grads = self.backward(saved, g_out)
+        # one completed replay before the graph is handed out: at 4 ranks, first replays
+        # issued back to back (collectives inside) hung
+        graph.replay()
+        torch.cuda.synchronize()
         return GraphedStep(graph, out, grads, _lib.LAUNCH_COUNT["n"] - n0)
 
     # ---------------------------------------------------------------- forward
