@@ -650,31 +650,44 @@ __global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a
   const int r = (int)(item - (long long)n * a.R);
   const int first = __ldg(a.node_first + n), g = __ldg(a.node_g + n);
   const int H = a.H, D = a.D, dh = D / H, h = warp;
-  const int ld = D * 2 + 16;                       // bytes per staged row (padded)
+  // q | k of child j (contiguous in HBM, 4D bytes) land in one padded smem row by a 1-D bulk
+  // copy (no per-chunk address math or register staging); the 16-byte pad keeps the 8 rows
+  // of an ldmatrix in different banks
+  __shared__ __align__(8) uint64_t landed;
+  const int pitch = 4 * D + 16;
   const int rows = 16 * MI;
-  uint8_t* qs = fsm_raw;                           // [rows][ld] q, then k
-  uint8_t* ks = fsm_raw + rows * ld;
-  float* tsm = reinterpret_cast<float*>(fsm_raw + 2 * rows * ld);   // [H][32] t_i,h
+  uint8_t* qk = fsm_raw;                                             // [rows][pitch]
+  float* tsm = reinterpret_cast<float*>(fsm_raw + rows * pitch);     // [H][32] t_i,h
   float* p2s = tsm + H * 32;                                         // [32]
-  // stage q and k of the g children (zero rows beyond g), 16 B per thread per step
-  const int cpr = D / 8;                           // 16-byte chunks per row
-  for (int t = threadIdx.x; t < 2 * rows * cpr; t += blockDim.x) {
-    const int which = t / (rows * cpr), rest = t - which * rows * cpr;
-    const int j = rest / cpr, c = rest - j * cpr;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (j < g) {
-      v = __ldg(reinterpret_cast<const uint4*>(a.QK + (long long)(first + j) * a.sQj +
-                                               (long long)r * a.ldq + which * D) + c);
-      if (!which && a.posq) {  // + the positional query of this position
-        const uint4 pq = __ldg(reinterpret_cast<const uint4*>(
-            a.posq + ((long long)n * a.S + r % a.S) * D) + c);
-        v.x = pack_bf16(bf16lo(v.x) + bf16lo(pq.x), bf16hi(v.x) + bf16hi(pq.x));
-        v.y = pack_bf16(bf16lo(v.y) + bf16lo(pq.y), bf16hi(v.y) + bf16hi(pq.y));
-        v.z = pack_bf16(bf16lo(v.z) + bf16lo(pq.z), bf16hi(v.z) + bf16hi(pq.z));
-        v.w = pack_bf16(bf16lo(v.w) + bf16lo(pq.w), bf16hi(v.w) + bf16hi(pq.w));
-      }
+  if (threadIdx.x == 0) {
+    mbar_init(&landed, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&landed, (uint32_t)g * 4 * D);
+    for (int j = 0; j < g; ++j)
+      bulk_load(qk + j * pitch, a.QK + (long long)(first + j) * a.sQj + (long long)r * a.ldq,
+                4 * D, &landed);
+  }
+  const int cpr = D / 8;                           // 16-byte chunks of a q (or k) row
+  for (int t = threadIdx.x; t < (rows - g) * 2 * cpr; t += blockDim.x)   // rows beyond g: 0
+    *reinterpret_cast<uint4*>(qk + (g + t / (2 * cpr)) * pitch + (t % (2 * cpr)) * 16) =
+        make_uint4(0, 0, 0, 0);
+  mbar_wait(&landed, 0);
+  if (a.posq) {  // + the positional query of this position, in place
+    const __nv_bfloat16* pqr = a.posq + ((long long)n * a.S + r % a.S) * D;
+    for (int t = threadIdx.x; t < g * cpr; t += blockDim.x) {
+      const int j = t / cpr, c = t - j * cpr;
+      uint8_t* dst = qk + j * pitch + c * 16;
+      uint4 v = *reinterpret_cast<const uint4*>(dst);
+      const uint4 pq = __ldg(reinterpret_cast<const uint4*>(pqr) + c);
+      v.x = pack_bf16(bf16lo(v.x) + bf16lo(pq.x), bf16hi(v.x) + bf16hi(pq.x));
+      v.y = pack_bf16(bf16lo(v.y) + bf16lo(pq.y), bf16hi(v.y) + bf16hi(pq.y));
+      v.z = pack_bf16(bf16lo(v.z) + bf16lo(pq.z), bf16hi(v.z) + bf16hi(pq.z));
+      v.w = pack_bf16(bf16lo(v.w) + bf16lo(pq.w), bf16hi(v.w) + bf16hi(pq.w));
+      *reinterpret_cast<uint4*>(dst) = v;
     }
-    *reinterpret_cast<uint4*>((which ? ks : qs) + j * ld + c * 16) = v;
   }
   __syncthreads();
   // logits S^h = q_h k_h^T / sqrt(dh) on the tensor cores
@@ -692,13 +705,13 @@ __global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
       const int row = mi * 16 + rr + 8 * (mat & 1);
-      ldsm_x4(smem_u32(qs + row * ld + col + 16 * (mat >> 1)), af[mi]);
+      ldsm_x4(smem_u32(qk + row * pitch + col + 16 * (mat >> 1)), af[mi]);
     }
 #pragma unroll
     for (int np = 0; np < NJ / 2; ++np) {
       uint32_t bf[4];
       const int row = np * 16 + rr + 8 * (mat >> 1);
-      ldsm_x4(smem_u32(ks + row * ld + col + 16 * (mat & 1)), bf);
+      ldsm_x4(smem_u32(qk + row * pitch + 2 * D + col + 16 * (mat & 1)), bf);
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi) {
         mma_16816(acc[mi][2 * np], af[mi], bf[0], bf[1]);
@@ -810,7 +823,7 @@ cudaError_t launch_fullcross_weights(const FullCrossArgs& a, cudaStream_t st) {
   const int dh = a.D / a.H;
   if (a.max_g > 32 || a.H > 32 || dh % 16 || a.H < 1 || a.D % 8) return cudaErrorInvalidValue;
   const int MI = a.max_g > 16 ? 2 : 1;
-  const size_t smem = (size_t)2 * 16 * MI * (a.D * 2 + 16) + ((size_t)a.H * 32 + 32) * 4;
+  const size_t smem = (size_t)16 * MI * (a.D * 4 + 16) + ((size_t)a.H * 32 + 32) * 4;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   auto kern = MI == 2 ? fullcross_weights_kernel<2> : fullcross_weights_kernel<1>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -445,20 +445,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // coalesced load per lane, read back as broadcasts (the per-group global loads of every
       // lane were the epilogue's largest cost)
       float* wbias = bias_smem + (warp - 2) * 128;
+      auto bias_cols = [&](const float* bp, int n) {
+        float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (b_vec && n + 4 <= args.N) {
+          b4 = __ldg(reinterpret_cast<const float4*>(bp + n));
+        } else {
+          if (n < args.N) b4.x = __ldg(bp + n);
+          if (n + 1 < args.N) b4.y = __ldg(bp + n + 1);
+          if (n + 2 < args.N) b4.z = __ldg(bp + n + 2);
+          if (n + 3 < args.N) b4.w = __ldg(bp + n + 3);
+        }
+        return b4;
+      };
       if (bias) {
         __syncwarp();  // the previous tile's broadcast reads are done
         const int n = nt * args.BN + (hf + 2 * (lane >> 3)) * 32 + (lane & 7) * 4;
-        float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (b_vec && n + 4 <= args.N) {
-          b4 = __ldg(reinterpret_cast<const float4*>(bias + n));
-        } else {
-          if (n < args.N) b4.x = __ldg(bias + n);
-          if (n + 1 < args.N) b4.y = __ldg(bias + n + 1);
-          if (n + 2 < args.N) b4.z = __ldg(bias + n + 2);
-          if (n + 3 < args.N) b4.w = __ldg(bias + n + 3);
-        }
+        // non-COMB tiles: this tile's bias columns were fetched during the previous tile
+        const float4 b4 = (!COMB && dot_pf_valid) ? dot_bias_pf : bias_cols(bias, n);
         reinterpret_cast<float4*>(wbias)[lane] = b4;
         __syncwarp();
+      }
+      if (!COMB) {
+        dot_pf_valid = false;
+        if (bias && t + ct_step < ct_end) {  // the next tile's bias, in flight during this one
+          int g2, mt2, nt2;
+          decode(t + ct_step, g2, mt2, nt2);
+          dot_bias_pf = bias_cols(args.bias + (size_t)g2 * args.bias_g,
+                                  nt2 * args.BN + (hf + 2 * (lane >> 3)) * 32 + (lane & 7) * 4);
+          dot_pf_valid = true;
+        }
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
