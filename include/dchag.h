@@ -294,6 +294,17 @@ int dchag_combine_strided(int n_nodes, int R, int D, int H, const int* node_firs
  * layers.py:103-123 / :141-146).  G fp32 [n][R][D] = dLoss/dctx.  Writes, per child j:
  * gV_j = p_jh * G[h-blk] (bf16, V's strides), and dL_j = p (dp - sum p dp) (fp32, L's
  * strides; attention) or dm_j[r] = G[r] . V_j[r] (fp32 [child][R]; linear). */
+/* Backward of full_cross nodes (layers.py:125-138 through tensor.py:395-413), one CTA per
+ * (node, row), g <= 16: recomputes the channel attention S^h, p2 and w from q | k | v
+ * (child j row r at QKV + j*sQj + r*ldq, bf16) and u (fp32 [child][R][H]), and from
+ * G = dLoss/dctx (fp32 [n][R][D]) and a = (wo rq)/sqrt(D) (fp32 [n][D]) writes
+ * dq | dk | dv (bf16, the QKV layout at dQKV) and dA[n][r][:] = sum_j du_jh v_j,h (fp32; its
+ * column sum is the gradient of a). */
+int dchag_fullcross_bwd(int n_nodes, int R, int D, int H, const int* node_first,
+                        const int* node_g, int max_g, const void* QKV, long long sQj,
+                        long long ldq, const float* u, const float* G, const float* a_vec,
+                        void* dQKV, float* dA, void* stream);
+
 int dchag_combine_bwd(int n_nodes, int R, int D, int H, const int* node_first, const int* node_g,
                       int max_g, const void* V, long long sVj, const float* L, long long sLj,
                       const float* mix, const float* G, float* dL, void* gV, float* dm,

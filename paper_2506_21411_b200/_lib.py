@@ -48,6 +48,8 @@ SIGNATURES = {
                           c_vp, c_vp, c_vp],
     "dchag_fullcross_weights": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_ll,
                                 c_vp, c_ll, c_vp, c_vp, c_int, c_vp, c_vp, c_int, c_vp],
+    "dchag_fullcross_bwd": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_ll, c_vp,
+                            c_vp, c_vp, c_vp, c_vp, c_vp],
     "dchag_combine_weighted": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_ll,
                                c_vp, c_vp, c_vp],
     "dchag_combine_strided": [c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_vp, c_ll, c_ll,

@@ -653,6 +653,23 @@ int dchag_fullcross_weights(int n_nodes, int R, int D, int H, const int* node_fi
   return cuda_status(launch_fullcross_weights(a, S(stream)), "fullcross_weights");
 }
 
+int dchag_fullcross_bwd(int n_nodes, int R, int D, int H, const int* node_first,
+                        const int* node_g, int max_g, const void* QKV, long long sQj,
+                        long long ldq, const float* u, const float* G, const float* a_vec,
+                        void* dQKV, float* dA, void* stream) {
+  if (D % H || (D / H) % 16 || max_g < 1 || max_g > 16 || H > 32 || ldq < 3 * D ||
+      (ldq * 2) % 16 || (sQj * 2) % 16 || reinterpret_cast<uintptr_t>(QKV) % 16 || !u || !G ||
+      !a_vec || !dQKV || !dA)
+    return fail(DCHAG_ERR_SHAPE, "fullcross_bwd: bad shape");
+  FullCrossBwdArgs a;
+  memset(&a, 0, sizeof(a));
+  a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H; a.max_g = max_g;
+  a.node_first = node_first; a.node_g = node_g;
+  a.QKV = reinterpret_cast<const __nv_bfloat16*>(QKV); a.sQj = sQj; a.ldq = ldq;
+  a.u = u; a.G = G; a.a = a_vec; a.dQKV = reinterpret_cast<__nv_bfloat16*>(dQKV); a.dA = dA;
+  return cuda_status(launch_fullcross_bwd(a, S(stream)), "fullcross_bwd");
+}
+
 int dchag_combine_weighted(int n_nodes, int R, int D, int H, const int* node_first,
                            const int* node_g, int max_g, const void* V, long long sVj,
                            long long ldv, const float* w, void* ctx, void* stream) {

@@ -833,6 +833,264 @@ cudaError_t launch_fullcross_weights(const FullCrossArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Backward of a full_cross node (layers.py:125-138 with sdp_attention :49-64, the rq reduce
+// folded as in fullcross_weights_kernel), one CTA per (node, row), one warp per head, g <= 16.
+// Recomputes S^h = softmax_j(q_i k_j / sqrt(dh)) (tensor cores), t, p2, w, then with
+// G = dLoss/dctx:  dw_jh = G_h . v_jh;  dp2_i = sum_hj S_ij dw_jh;  dt = p2 (dp2 - p2.dp2);
+// dS_ij = p2_i dw_j + dt_i u_j;  du_j = sum_i dt_i S_ij;  dL = S (dS - rowsum(S dS));
+// dq_i = sum_j dL_ij k_j / sqrt(dh);  dk_j = sum_i dL_ij q_i / sqrt(dh);
+// dv_jh = w_jh G_h + du_jh a_h;  dA[row][h-blk] = sum_j du_jh v_jh  (-> d(wo rq)).
+__global__ void __launch_bounds__(1024) fullcross_bwd_kernel(FullCrossBwdArgs a) {
+  extern __shared__ __align__(16) uint8_t fsm_raw[];
+  __shared__ __align__(8) uint64_t landed;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const long long item = blockIdx.x;
+  const int n = (int)(item / a.R);
+  const int r = (int)(item - (long long)n * a.R);
+  const int first = __ldg(a.node_first + n), g = __ldg(a.node_g + n);
+  const int H = a.H, D = a.D, dh = D / H, h = warp;
+  const int pitch = 6 * D + 16;                    // q | k | v row of a child (+ pad)
+  uint8_t* qkv = fsm_raw;                          // [16][pitch]
+  float* Gs = reinterpret_cast<float*>(fsm_raw + 16 * pitch);       // [D]
+  float* tsm = Gs + D;                             // [H][16] t_i,h, then dp2 parts
+  float* p2s = tsm + H * 16;                       // [16]
+  float* dts = p2s + 16;                           // [16]
+  float* dw = dts + 16;                            // [H][16]
+  float* dLs = dw + H * 16;                        // [H][16][17]
+  if (threadIdx.x == 0) {
+    mbar_init(&landed, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&landed, (uint32_t)g * 6 * D);
+    for (int j = 0; j < g; ++j)
+      bulk_load(qkv + j * pitch, a.QKV + (long long)(first + j) * a.sQj + (long long)r * a.ldq,
+                6 * D, &landed);
+  }
+  for (int t = threadIdx.x; t < (16 - g) * (6 * D / 16); t += blockDim.x)
+    *reinterpret_cast<uint4*>(qkv + (g + t / (6 * D / 16)) * pitch + (t % (6 * D / 16)) * 16) =
+        make_uint4(0, 0, 0, 0);
+  for (int d = threadIdx.x; d < D; d += blockDim.x)
+    Gs[d] = __ldg(a.G + ((long long)n * a.R + r) * D + d);
+  mbar_wait(&landed, 0);
+  __syncthreads();
+  auto qv = [&](int j, int d) {  // q (0), k (D), v (2D) element of child j
+    return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(qkv + j * pitch + d * 2));
+  };
+  // ---- logits and S (as fullcross_weights_kernel, MI = 1)
+  float acc[2][4];
+#pragma unroll
+  for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[nj][e] = 0.f;
+  const int mat = lane >> 3, rr = lane & 7;
+  for (int k0 = 0; k0 < dh; k0 += 16) {
+    const int col = (h * dh + k0) * 2;
+    uint32_t af[4], bf[4];
+    ldsm_x4(smem_u32(qkv + (rr + 8 * (mat & 1)) * pitch + col + 16 * (mat >> 1)), af);
+    ldsm_x4(smem_u32(qkv + (rr + 8 * (mat >> 1)) * pitch + 2 * D + col + 16 * (mat & 1)), bf);
+    mma_16816(acc[0], af, bf[0], bf[1]);
+    mma_16816(acc[1], af, bf[2], bf[3]);
+  }
+  const float sc = rsqrtf((float)dh);
+  float uj[2][2];
+#pragma unroll
+  for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = nj * 8 + 2 * tig + e;
+      uj[nj][e] = j < g ? __ldg(a.u + (long long)(first + j) * a.R * H + (long long)r * H + h) : 0.f;
+    }
+#pragma unroll
+  for (int hr = 0; hr < 2; ++hr) {
+    float m = -INFINITY;
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = nj * 8 + 2 * tig + e;
+        acc[nj][2 * hr + e] *= sc;
+        if (j < g) m = fmaxf(m, acc[nj][2 * hr + e]);
+      }
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    float sum = 0.f;
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = nj * 8 + 2 * tig + e;
+        const float ev = j < g ? __expf(acc[nj][2 * hr + e] - m) : 0.f;
+        acc[nj][2 * hr + e] = ev;
+        sum += ev;
+      }
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    const float inv = 1.f / sum;
+    float tu = 0.f;
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        acc[nj][2 * hr + e] *= inv;                         // S_ij
+        tu = fmaf(acc[nj][2 * hr + e], uj[nj][e], tu);
+      }
+    tu += __shfl_xor_sync(0xffffffffu, tu, 1);
+    tu += __shfl_xor_sync(0xffffffffu, tu, 2);
+    if (tig == 0) tsm[h * 16 + gid + 8 * hr] = tu;
+  }
+  // dw_jh = G_h . v_jh  (lanes over the head's dh columns, one child at a time)
+  for (int j = 0; j < 16; ++j) {
+    float part = 0.f;
+    if (j < g)
+      for (int d = lane; d < dh; d += 32) part = fmaf(Gs[h * dh + d], qv(j, 2 * D + h * dh + d), part);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) dw[h * 16 + j] = part;
+  }
+  __syncthreads();
+  if (warp == 0) {  // p2 = softmax_i(sum_h t)
+    float sv = -INFINITY;
+    if (lane < g) {
+      sv = 0.f;
+      for (int hh = 0; hh < H; ++hh) sv += tsm[hh * 16 + lane];
+    }
+    float m = sv;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float e = lane < g ? __expf(sv - m) : 0.f;
+    float sum = e;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane < 16) p2s[lane] = e / sum;
+  }
+  __syncthreads();
+  // w_jh = sum_i p2_i S_ij (kept per lane for its columns) and dp2 parts = sum_j S_ij dw_j
+  float wj[2][2], dwj[2][2];
+#pragma unroll
+  for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = nj * 8 + 2 * tig + e;
+      dwj[nj][e] = dw[h * 16 + j];
+      float x = p2s[gid] * acc[nj][e] + p2s[gid + 8] * acc[nj][2 + e];
+      x += __shfl_xor_sync(0xffffffffu, x, 4);
+      x += __shfl_xor_sync(0xffffffffu, x, 8);
+      x += __shfl_xor_sync(0xffffffffu, x, 16);
+      wj[nj][e] = x;
+    }
+#pragma unroll
+  for (int hr = 0; hr < 2; ++hr) {
+    float dpp = 0.f;
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) dpp = fmaf(acc[nj][2 * hr + e], dwj[nj][e], dpp);
+    dpp += __shfl_xor_sync(0xffffffffu, dpp, 1);
+    dpp += __shfl_xor_sync(0xffffffffu, dpp, 2);
+    if (tig == 0) tsm[h * 16 + gid + 8 * hr] = dpp;   // t no longer needed
+  }
+  __syncthreads();
+  if (warp == 0) {  // dt_i = p2_i (dp2_i - sum_i' p2_i' dp2_i')
+    float dp2 = 0.f;
+    if (lane < g)
+      for (int hh = 0; hh < H; ++hh) dp2 += tsm[hh * 16 + lane];
+    const float p2 = lane < 16 ? p2s[lane] : 0.f;
+    float s = p2 * dp2;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane < 16) dts[lane] = lane < g ? p2 * (dp2 - s) : 0.f;
+  }
+  __syncthreads();
+  // dS_ij = p2_i dw_j + dt_i u_j ; du_j = sum_i dt_i S_ij ; dL = S (dS - rowsum(S dS))
+  float duj[2][2];
+#pragma unroll
+  for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      float x = dts[gid] * acc[nj][e] + dts[gid + 8] * acc[nj][2 + e];
+      x += __shfl_xor_sync(0xffffffffu, x, 4);
+      x += __shfl_xor_sync(0xffffffffu, x, 8);
+      x += __shfl_xor_sync(0xffffffffu, x, 16);
+      duj[nj][e] = x;
+    }
+  float* dL = dLs + h * 16 * 17;
+#pragma unroll
+  for (int hr = 0; hr < 2; ++hr) {
+    const int i = gid + 8 * hr;
+    float dS[2][2], rs = 0.f;
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        dS[nj][e] = p2s[i] * dwj[nj][e] + dts[i] * uj[nj][e];
+        rs = fmaf(acc[nj][2 * hr + e], dS[nj][e], rs);
+      }
+    rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+    rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = nj * 8 + 2 * tig + e;
+        dL[i * 17 + j] = (i < g && j < g) ? acc[nj][2 * hr + e] * (dS[nj][e] - rs) * sc : 0.f;
+      }
+  }
+  // per-child scalars of this head for the value gradient, broadcast via smem (reuse dw)
+  __syncwarp();
+  float* wsm = dw + h * 16;   // dw no longer needed: holds w_j, then du_j in the next slot
+  if (gid == 0) {
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) wsm[nj * 8 + 2 * tig + e] = wj[nj][e];
+  }
+  float* dusm = dLs + H * 16 * 17 + h * 16;
+  if (gid == 0) {
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) dusm[nj * 8 + 2 * tig + e] = duj[nj][e];
+  }
+  __syncwarp();
+  // dq, dk, dv (bf16) and dA of this head's dh columns; lanes over columns
+  for (int d = lane; d < dh; d += 32) {
+    const int c = h * dh + d;
+    const float ad = __ldg(a.a + (long long)n * D + c);
+    float dAsum = 0.f;
+    for (int j = 0; j < g; ++j) {
+      float dq = 0.f, dk = 0.f;
+      for (int jj = 0; jj < g; ++jj) {
+        dq = fmaf(dL[j * 17 + jj], qv(jj, D + c), dq);     // dq_j = sum_jj dL[j][jj] k_jj
+        dk = fmaf(dL[jj * 17 + j], qv(jj, c), dk);         // dk_j = sum_jj dL[jj][j] q_jj
+      }
+      const float vj = qv(j, 2 * D + c);
+      const float dv = wsm[j] * Gs[c] + dusm[j] * ad;
+      dAsum = fmaf(dusm[j], vj, dAsum);
+      __nv_bfloat16* o = a.dQKV + (long long)(first + j) * a.sQj + (long long)r * a.ldq;
+      o[c] = __float2bfloat16(dq);
+      o[D + c] = __float2bfloat16(dk);
+      o[2 * D + c] = __float2bfloat16(dv);
+    }
+    a.dA[((long long)n * a.R + r) * D + c] = dAsum;
+  }
+}
+
+cudaError_t launch_fullcross_bwd(const FullCrossBwdArgs& a, cudaStream_t st) {
+  const int dh = a.D / a.H;
+  if (a.max_g > 16 || a.H > 32 || dh % 16 || a.D % 8) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)16 * (a.D * 6 + 16) + (size_t)a.D * 4 +
+                      ((size_t)a.H * 16 * 2 + 32 + (size_t)a.H * 16 * 17 + (size_t)a.H * 16) * 4;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(fullcross_bwd_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fullcross_bwd_kernel<<<(unsigned)((long long)a.n_nodes * a.R), a.H * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 // Backward of the combine (layers.py:103-123 / :141-146 restated; reference tape
 // tensor.py:168-205): given g = dLoss/dctx[n][r][:] (fp32) and the saved child values
 // V_j (bf16) and logits L_j (fp32, attention) or mix (linear):

@@ -196,6 +196,21 @@ struct FullCrossArgs {
 };
 cudaError_t launch_fullcross_weights(const FullCrossArgs& a, cudaStream_t st);
 
+// Backward of a full_cross node per (node, row) given G = dLoss/dctx (see comb.cu).
+struct FullCrossBwdArgs {
+  int n_nodes, R, D, H, max_g;
+  const int* node_first;
+  const int* node_g;
+  const __nv_bfloat16* QKV;    // child j row r: q | k | v at QKV + j*sQj + r*ldq
+  long long sQj, ldq;
+  const float* u;              // [child][R][H] (forward's u)
+  const float* G;              // [n][R][D] fp32
+  const float* a;              // [n][D] fp32: (wo rq) / sqrt(D) of the node
+  __nv_bfloat16* dQKV;         // child j row r: dq | dk | dv at dQKV + j*sQj + r*ldq
+  float* dA;                   // [n][R][D] fp32: sum_j du_jh v_j,h (per head block)
+};
+cudaError_t launch_fullcross_bwd(const FullCrossBwdArgs& a, cudaStream_t st);
+
 // Backward of the combine: dL, gV (and dmix for linear nodes) from g = dLoss/dctx
 struct CombineBwdArgs {
   int n_nodes, R, D, H, max_g;

@@ -60,7 +60,14 @@ class _Node:
 
 
 class DchagTrainer:
-    """Forward + backward of one rank's front end (tp ranks share the final layer)."""
+    """Forward + backward of one rank's front end (tp ranks share the final layer).
+    A full_cross front end gets its own trainer (train_fc.FullCrossTrainer)."""
+
+    def __new__(cls, fe: DchagFrontEnd, dp_group=None):
+        if cls is DchagTrainer and fe.model.agg_variant == "full_cross":
+            from .train_fc import FullCrossTrainer
+            return FullCrossTrainer(fe, dp_group)
+        return super().__new__(cls)
 
     def __init__(self, fe: DchagFrontEnd, dp_group=None):
         """dp_group: the data-parallel group of this rank (grid.make_groups); backward()

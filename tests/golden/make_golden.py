@@ -133,6 +133,13 @@ def main():
     make_case("Tg_lin_tp2", channels=8, image=(64, 32), patch=4, embed=128, heads=2,
               tp=2, max_group=2, batch=1, layer_kind="linear", seed=4, round32=True, grads=True,
               bias_scale=0.02)
+    # full_cross training cases (agg_variant="full_cross": nodes and the final layer)
+    make_case("Tg_fc_tp1", channels=8, image=(64, 32), patch=4, embed=128, heads=2,
+              tp=1, max_group=4, batch=1, variant="full_cross", seed=5, round32=True,
+              grads=True, bias_scale=0.02)
+    make_case("Tg_fc_tp2", channels=8, image=(64, 32), patch=4, embed=128, heads=2,
+              tp=2, max_group=2, batch=1, variant="full_cross", seed=6, round32=True,
+              grads=True, bias_scale=0.02)
 
 
 if __name__ == "__main__":

@@ -556,3 +556,30 @@ def test_vit_input_fused_final_tp2():
     want = O.vit_input(agg, mask.astype(np.float64), mtok.astype(np.float64),
                        md.astype(np.float64), mw.astype(np.float64), mb.astype(np.float64))
     assert rel_err(out.cpu().numpy(), want) < BF16_TOL
+
+
+def test_kernels_are_repeatable_bitwise():
+    """Race / ordering check in place of compute-sanitizer (closed on this GPU pool): every
+    kernel has a fixed accumulation order, so the forward (K_p0, K_l0, COMB, K_gemm) and the
+    training step (every backward kernel) must give bit-identical results when repeated."""
+    from paper_2506_21411_b200 import DchagFrontEnd
+    from paper_2506_21411_b200.train import DchagTrainer
+    fe = DchagFrontEnd(64, 64, 128, 8, 1024, 16, max_group=8)
+    fe.init_weights(seed=2)
+    x = torch.randn(2, 64, 64, 128, device="cuda").to(torch.bfloat16)
+    ys = [fe(x).clone() for _ in range(3)]
+    fe3 = DchagFrontEnd(24, 64, 128, 8, 256, 4, max_group=4, out_dtype=torch.float32)
+    fe3.init_weights(seed=3)
+    tr = DchagTrainer(fe3)
+    x3 = torch.randn(2, 24, 64, 128, device="cuda").to(torch.bfloat16)
+    probe = torch.randn(2, 1, fe3.seq, 256, device="cuda")
+    runs = []
+    for _ in range(2):
+        out, saved = tr.forward_train(x3)
+        g = tr.backward(saved, probe)
+        runs.append((out.clone(), {k: v.clone() for k, v in g.items()}))
+    torch.cuda.synchronize()
+    assert all(torch.equal(ys[0], y) for y in ys[1:])
+    assert torch.equal(runs[0][0], runs[1][0])
+    for k in runs[0][1]:
+        assert torch.equal(runs[0][1][k], runs[1][1][k]), k

@@ -6,8 +6,8 @@ import pytest
 import torch_reference as TR
 from conftest import load_golden, rel_err
 
-CASES = ["ref_tiny_sq_tp2", "ref_tiny_lin_tp2", "ref_tiny_sq_tp1_g3", "Tg_sq_tp1", "Tg_sq_tp2",
-         "Tg_lin_tp2"]
+CASES = ["ref_tiny_sq_tp2", "ref_tiny_lin_tp2", "ref_tiny_fc_tp2", "ref_tiny_sq_tp1_g3",
+         "Tg_sq_tp1", "Tg_sq_tp2", "Tg_lin_tp2", "Tg_fc_tp1", "Tg_fc_tp2"]
 
 
 @pytest.mark.parametrize("case", CASES)
@@ -15,9 +15,16 @@ def test_autograd_reference_matches_reference_tape(case):
     meta, z, w, g_ref = load_golden(case)
     out, g = TR.grads(z["images"].astype(np.float64), w, z["probe"].astype(np.float64),
                       patch=meta["patch"], heads=meta["heads"], tp=meta["tp"],
-                      max_group=meta["max_group"], layer_kind=meta["layer_kind"])
+                      max_group=meta["max_group"], layer_kind=meta["layer_kind"],
+                      variant=meta.get("variant", "single_query"))
     tol = 1e-10 if z["out"].dtype == np.float64 else 1e-6
     assert rel_err(out, z["out"]) < tol
     assert set(g) == set(g_ref)
+    scale = max(np.abs(v).max() for v in g_ref.values())
     for k in g_ref:
-        assert rel_err(g[k], g_ref[k]) < tol * 10, k
+        if np.abs(g_ref[k]).max() < 1e-12 * scale:
+            # a numerically vanishing gradient (e.g. rq under a saturated reduce): compare
+            # against the largest gradient of the case instead of itself
+            assert np.abs(g[k] - g_ref[k]).max() < tol * scale, k
+        else:
+            assert rel_err(g[k], g_ref[k]) < tol * 10, k

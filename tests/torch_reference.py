@@ -37,12 +37,27 @@ def single_query(x, w, prefix, heads):
     return (ctx @ w[f"{prefix}.wo"] + w[f"{prefix}.bo"])[..., None, :]
 
 
+def full_cross(x, w, prefix, heads):
+    """Ck x Ck channel self-attention + learned-rq reduce (oracle cross_attention_full_cross,
+    layers.py:125-138 with sdp_attention :49-64)."""
+    d = x.shape[-1]
+    dh = d // heads
+    sh = lambda t: t.reshape(*t.shape[:-1], heads, dh)  # noqa: E731
+    q, k, v = x @ w[f"{prefix}.wq"], x @ w[f"{prefix}.wk"], x @ w[f"{prefix}.wv"]
+    lg = torch.einsum("...chd,...ehd->...hce", sh(q), sh(k)) / math.sqrt(dh)
+    p = torch.softmax(lg, dim=-1)
+    ctx = torch.einsum("...hce,...ehd->...chd", p, sh(v)).reshape(x.shape)
+    out = ctx @ w[f"{prefix}.wo"] + w[f"{prefix}.bo"]
+    pr = torch.softmax(out @ w[f"{prefix}.rq"] / math.sqrt(d), dim=-1)
+    return torch.einsum("...c,...cd->...d", pr, out)[..., None, :]
+
+
 def linear_mix(x, w, prefix):
     mixed = torch.einsum("g,...gd->...d", w[f"{prefix}.mix"], x)
     return (mixed @ w[f"{prefix}.w"] + w[f"{prefix}.b"])[..., None, :]
 
 
-def tree(tokens, levels, w, prefix, layer_kind, heads):
+def tree(tokens, levels, w, prefix, layer_kind, heads, variant="single_query"):
     x = tokens.permute(0, 2, 1, 3)
     for li, level in enumerate(levels):
         outs, off = [], 0
@@ -51,21 +66,24 @@ def tree(tokens, levels, w, prefix, layer_kind, heads):
             xg = x[:, :, off:off + g]
             off += g
             outs.append(linear_mix(xg, w, node) if layer_kind == "linear"
+                        else full_cross(xg, w, node, heads) if variant == "full_cross"
                         else single_query(xg, w, node, heads))
         x = torch.cat(outs, dim=2)
     return x.permute(0, 2, 1, 3)
 
 
-def frontend(images, w, *, patch, heads, tp, max_group, layer_kind="cross_attention"):
+def frontend(images, w, *, patch, heads, tp, max_group, layer_kind="cross_attention",
+             variant="single_query"):
     streams = []
     for r, (off, cnt) in enumerate(O.slabs(images.shape[1], tp)):
         tok = tokenize(images[:, off:off + cnt], w["tok.w"][off:off + cnt],
                        w["tok.b"][off:off + cnt], w["special.channel_id"][off:off + cnt],
                        w["special.pos"], patch)
         streams.append(tree(tok, O.build_levels(cnt, max_group), w, f"agg.slab{r}", layer_kind,
-                            heads))
+                            heads, variant))
     gathered = torch.cat(streams, dim=1).permute(0, 2, 1, 3)
-    return single_query(gathered, w, "agg.final", heads).permute(0, 2, 1, 3)
+    final = full_cross if variant == "full_cross" else single_query
+    return final(gathered, w, "agg.final", heads).permute(0, 2, 1, 3)
 
 
 def grads(images, w_np, probe, **cfg):
