@@ -331,7 +331,11 @@ def roofline(dom, peaks, traffic):
     t = dom["ms"] / 1e3
     if not t or not (dom["flops"] or dom["bytes"]):
         return None
-    if dom["kernel"] in TENSOR_KERNELS and dom["flops"]:
+    # the bound follows the site's arithmetic intensity when both counts are known (a K = 64
+    # GEMM writing wide rows is HBM-bound even though it runs on the tensor cores)
+    ridge = peak_burst * 1e12 / (hbm * 1e9)
+    hbm_bound = bool(dom["bytes"]) and bool(dom["flops"]) and dom["flops"] / dom["bytes"] < ridge
+    if dom["kernel"] in TENSOR_KERNELS and dom["flops"] and not hbm_bound:
         ach = dom["flops"] / t / 1e12
         r = {"bound": "tensor", "achieved": ach, "peak": peak_burst, "unit": "TFLOP/s",
              "frac": ach / peak_burst, "frac_vs_sustained": ach / peak_sus,

@@ -157,17 +157,20 @@ def full_cross_level0(images, tok_w, tok_b, chan_id, pos, spec: TreeSpec, w, pre
                       C * S * PP, PP, _lib.ptr(Mq), NQ, NQ * PP, 2 * D, _lib.ptr(bias), NQ,
                       0, 0, 0, 1, _lib.ptr(QK[c0]), 0, R * 2 * D, S * 2 * D, 2 * D,
                       _lib.ptr(U[c0]), R * H, S * H, H, st,
-                      work={"site": "ops:fc_l0_qk", "flops": 2 * g * R * PP * NQ})
+                      work={"site": "ops:fc_l0_qk", "flops": 2 * g * R * PP * NQ,
+                            "bytes": g * R * (PP * 2 + 4 * D + 4 * H)})
         else:
             _lib.call("dchag_gemm_bf16", _lib.ptr(patches[:, c0]), g, B, S, PP, S * PP,
                       C * S * PP, PP, _lib.ptr(Mq), 2 * D, NQ * PP, 2 * D, _lib.ptr(bias), NQ,
                       0, 0, 0, 1, _lib.ptr(QK[c0]), 0, R * 2 * D, S * 2 * D, 2 * D, 0, 0, 0, 0,
-                      st, work={"site": "ops:fc_l0_qk", "flops": 2 * g * R * PP * 2 * D})
+                      st, work={"site": "ops:fc_l0_qk", "flops": 2 * g * R * PP * 2 * D,
+                                "bytes": g * R * (PP + 2 * D) * 2})
             _lib.call("dchag_gemm_bf16", _lib.ptr(patches[:, c0]), g, B, S, PP, S * PP,
                       C * S * PP, PP, _lib.ptr(Mq[:, 2 * D:]), H, NQ * PP, 0,
                       _lib.ptr(bias[:, 2 * D:]), NQ, 0, 0, 0, 1, 0, 0, 0, 0, 0, _lib.ptr(U[c0]),
                       R * H, S * H, H, st,
-                      work={"site": "ops:fc_l0_u", "flops": 2 * g * R * PP * H})
+                      work={"site": "ops:fc_l0_u", "flops": 2 * g * R * PP * H,
+                            "bytes": g * R * (PP * 2 + H * 4)})
         c0 += g
     NH = unit_heads(D, H)
     poff, acc = [], 0

@@ -839,7 +839,8 @@ class DchagTrainer:
             _lib.call("dchag_gemm_rowdot", _ptr(patches[:, c0:c0 + g]), g, B, S, PP, S * PP,
                       cnt * S * PP, PP, _ptr(st["Mrow"][c0]), D, D * PP, _ptr(st["Cb"][c0]), D,
                       _ptr(Gn), D, _ptr(dpp), sh,
-                      work={"site": "bwd:l0_rowdot", "flops": 2 * g * R * D * PP})
+                      work={"site": "bwd:l0_rowdot", "flops": 2 * g * R * D * PP,
+                            "bytes": R * D * 2 + g * R * PP * 2 + g * D // 32 * R * 4})
             dl = dlb = None
             if attn:
                 dl = torch.empty(g, H, R, device=dev)
