@@ -16,9 +16,9 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_r
 for n in 2 4 8; do timeout 600 python bench.py --arch-tp $n --no-cpu-baseline > $OUT/bench_arch$n.json 2> $OUT/bench_arch$n.err; done
 timeout 900 python tools/costmodel_validate.py > $OUT/costmodel_validate.json 2> $OUT/costmodel_validate.err
 NCU=/usr/local/cuda/bin/ncu
-timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_h1.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -k regex:"l0_|gemm_kernel|combine|child_softmax|unfold|vit_" -c 200 --csv --log-file $OUT/launches_h1.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:l0_node_kernel -c 1 -o $OUT/l0_node python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $OUT/ncu_l0.log 2>&1
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:gemm_kernel -s 2 -c 1 -o $OUT/gemm python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $OUT/ncu_gemm.log 2>&1
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:gemm_kernel -s 1 -c 1 -o $OUT/gemm python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $OUT/ncu_gemm.log 2>&1
 timeout 900 $NCU --set full --clock-control none -k regex:gemm_kernel -c 3 -o $OUT/train_gemm python bench.py --workload train --steps 1 --warmup 1 --no-graph --no-cpu-baseline > $OUT/ncu_train.log 2>&1
 for tool in memcheck racecheck synccheck; do
   timeout 1200 /usr/local/cuda/bin/compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_t.py > $OUT/sanitize_$tool.log 2>&1; echo "exit $?" >> $OUT/sanitize_$tool.log
