@@ -374,10 +374,12 @@ def b200_arm(args, wl, tp, max_group):
 
     def make_fe(tp_, rank_):
         # the training config's final layer is head-split over the tp group (reduce-scatter
-        # of the boundary gradient in backward, BASELINE.json configs[3])
+        # of the boundary gradient in backward, BASELINE.json configs[3]); the in-process
+        # architecture mode keeps the replicated final layer (no collectives in one process)
         fe_ = DchagFrontEnd(wl["channels"], wl["image_h"], wl["image_w"], wl["patch"],
                             wl["embed"], wl["heads"], max_group=max_group, tp=tp_, rank=rank_,
-                            final_layer_tp_split=bool(wl.get("final_split")) and tp_ > 1,
+                            final_layer_tp_split=(bool(wl.get("final_split")) and tp_ > 1
+                                                  and not arch_tp),
                             agg_variant=wl.get("variant", "single_query"),
                             agg_layer_kind=wl.get("layer_kind", "cross_attention"),
                             precision=wl.get("precision", "bf16"))
@@ -437,7 +439,25 @@ def b200_arm(args, wl, tp, max_group):
 
     gstep = None
     trainer = None
-    if wl.get("train"):
+    if wl.get("train") and arch_tp:
+        # the tp = N training architecture in one process: every rank's slab forward, the
+        # root streams stacked in rank order (the AllGather), each rank's replicated final
+        # layer and backward, as tests/test_gpu_train.py runs it
+        from paper_2506_21411_b200.train import DchagTrainer
+        trainers = [DchagTrainer(f) for f in fes]
+        probe = torch.randn(B, 1, fe.seq, wl["embed"], device="cuda", generator=gen)
+        slabs_img = [images[:, f.slab[0]:f.slab[0] + f.slab[1]] for f in fes]
+
+        def step():
+            saves = [t.forward_local(x) for t, x in zip(trainers, slabs_img)]
+            y_all = torch.stack([sv["y_root"] for sv in saves])
+            outs = [t.forward_final(y_all, sv) for t, sv in zip(trainers, saves)]
+            for t, sv in zip(trainers, saves):
+                _, g_y = t.backward_final(sv, probe)
+                t.backward_local(sv, g_y)
+            return outs[0]
+        eager_step = step
+    elif wl.get("train"):
         from paper_2506_21411_b200.train import DchagTrainer
         trainer = DchagTrainer(fe)
         probe = torch.randn(B, 1, fe.seq, wl["embed"], device="cuda", generator=gen)
@@ -521,7 +541,12 @@ def b200_arm(args, wl, tp, max_group):
     dev_img = torch.empty_like(images)
 
     def e2e_step():
-        if wl.get("train"):
+        if wl.get("train") and arch_tp:
+            images.copy_(host_img, non_blocking=True)
+            out = step()
+            if rank == 0:
+                out_host.copy_(out, non_blocking=True)
+        elif wl.get("train"):
             if gstep is None:
                 dev_img.copy_(host_img, non_blocking=True)
                 out, saved = trainer.forward_train(dev_img)
