@@ -260,16 +260,27 @@ static int gemm_impl(const void* A, int G, int Mo, int Mi, int K, long long sAg,
   // value columns by TMA tensor store (bf16 output, 16-byte aligned strides, 32-row boxes)
   CUtensorMap tV;
   memset(&tV, 0, sizeof(tV));
+  a.debug = getenv("DCHAG_GEMM_DEBUG") ? atoi(getenv("DCHAG_GEMM_DEBUG")) : 0;
+  // the lean epilogue: plain bf16 tiles, all full and 64-column aligned (DCHAG_GEMM_LEAN=0
+  // selects the general epilogue, for A/B probes)
+  const char* lean_env = getenv("DCHAG_GEMM_LEAN");
+  const bool lean = pair && !dot && !rowbias && !rmask && outV && !outV_f32 && Nv == N &&
+                    bn % 64 == 0 && N % bn == 0 && Mi % 32 == 0 && a.debug == 0 &&
+                    (!bias || (bias_g % 4 == 0 && reinterpret_cast<uintptr_t>(bias) % 16 == 0)) &&
+                    !(lean_env && atoi(lean_env) == 0);
   if (outV && !outV_f32 && Nv >= 32 && Mi % 32 == 0 &&
       ((reinterpret_cast<uintptr_t>(outV) | (uintptr_t)(sVmi * 2) | (uintptr_t)(sVmo * 2) |
         (uintptr_t)(sVg * 2)) % 16) == 0 && !getenv("DCHAG_GEMM_NO_TMA_STORE")) {
     cuuint64_t dims[4] = {(cuuint64_t)Nv, (cuuint64_t)Mi, (cuuint64_t)Mo, (cuuint64_t)G};
     cuuint64_t str[3] = {(cuuint64_t)sVmi * 2, (cuuint64_t)(Mo > 1 ? sVmo : Mi * sVmi) * 2,
                          (cuuint64_t)(G > 1 ? sVg : Mo * (Mo > 1 ? sVmo : Mi * sVmi)) * 2};
-    cuuint32_t box[4] = {32, 32, 1, 1};
-    if (make_map(&tV, outV, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B) == DCHAG_OK) a.v_tma = 1;
+    cuuint32_t box[4] = {lean ? 64u : 32u, 32, 1, 1};
+    if (make_map(&tV, outV, 4, dims, str, box,
+                 lean ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B) == DCHAG_OK) {
+      a.v_tma = 1;
+      a.lean = lean;
+    }
   }
-  a.debug = getenv("DCHAG_GEMM_DEBUG") ? atoi(getenv("DCHAG_GEMM_DEBUG")) : 0;
   a.bias = bias; a.bias_g = bias_g;
   a.rowbias = reinterpret_cast<const __nv_bfloat16*>(rowbias);
   a.rowbias_g = rowbias_g; a.rowbias_row = rowbias_row;
@@ -351,13 +362,21 @@ int dchag_gemm_nt(const void* A, int a_mn, long long lda, long long sAko, int Ki
   a.pair = pair; a.lay = lay; a.Ki = a_mn ? Ki : K; a.accum = accumulate;
   a.bias = bias; a.bias_g = bias_g; a.rowbias_period = 1;
   a.outV = out; a.outV_f32 = out_f32; a.sVg = sCg; a.sVmo = 0; a.sVmi = ldc;
+  const char* lean_env = getenv("DCHAG_GEMM_LEAN");
+  const bool lean = pair && !lay && !out_f32 && bn % 64 == 0 && N % bn == 0 &&
+                    (!bias || (bias_g % 4 == 0 && reinterpret_cast<uintptr_t>(bias) % 16 == 0)) &&
+                    !getenv("DCHAG_GEMM_DEBUG") && !(lean_env && atoi(lean_env) == 0);
   if (!out_f32 && N >= 32 &&
       ((reinterpret_cast<uintptr_t>(out) | (uintptr_t)(ldc * 2) | (uintptr_t)(sCg * 2)) % 16) == 0) {
     cuuint64_t dims[4] = {(cuuint64_t)N, (cuuint64_t)M, 1, (cuuint64_t)G};
     cuuint64_t str[3] = {(cuuint64_t)ldc * 2, (cuuint64_t)M * ldc * 2,
                          (cuuint64_t)(G > 1 ? sCg : M * ldc) * 2};
-    cuuint32_t box[4] = {32, 32, 1, 1};
-    if (make_map(&tV, out, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B) == DCHAG_OK) a.v_tma = 1;
+    cuuint32_t box[4] = {lean ? 64u : 32u, 32, 1, 1};
+    if (make_map(&tV, out, 4, dims, str, box,
+                 lean ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B) == DCHAG_OK) {
+      a.v_tma = 1;
+      a.lean = lean;
+    }
   }
   return cuda_status(launch_gemm(tA, tW, tV, a, 64, sms, S(stream)), "gemm_nt");
 }

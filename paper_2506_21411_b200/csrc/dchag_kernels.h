@@ -39,6 +39,8 @@ struct GemmArgs {
   int nparents;                 // COMB: G = nparents * csplit; group g = split s * nparents + j
   int csplit;                   // 1, or 2: split s sums children [s c/2, (s+1) c/2) (partials)
   int lay;                      // operand layouts: bit 0 A MN-major, bit 1 W MN-major
+  int lean;                     // 1: lean bf16 epilogue (tV box 64 columns x 32 rows, 128B
+                                //    swizzle; see gemm_kernel)
   int Ki;                       // MN-major A: K = Ko * Ki rows, (k / Ki) * sAko + (k % Ki) * lda
   int accum;                    // fp32 output: out += acc instead of out = acc
   const float* rmask;           // optional [M] row mask m: v = v (1 - m) + mtok[n] m (epilogue)

@@ -10,6 +10,7 @@
 //
 // Persistent grid; warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
 // warps 2..5 = epilogue (one TMEM lane quarter each).
+#include <type_traits>
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -36,14 +37,17 @@ cudaError_t comb_overflow_flag(int* value, int reset) {
   return e;
 }
 
-template <int BK, int STAGES, bool PAIR = false>
+template <int BK, int STAGES, bool PAIR = false, int OUT = GEMM_STAGE_OUT>
 struct GemmSmem {
   static constexpr int A_BYTES = GEMM_BM * BK * 2;
   static constexpr int W_BYTES = (PAIR ? GEMM_BN_MAX / 2 : GEMM_BN_MAX) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + W_BYTES;
+  static constexpr int OUT_BYTES = OUT;  // epilogue staging
   static constexpr int TOTAL =
-      STAGES * STAGE_BYTES + GEMM_STAGE_OUT + GEMM_BIAS_SMEM + 1024 /*align*/ + 256 /*barriers*/;
+      STAGES * STAGE_BYTES + OUT + GEMM_BIAS_SMEM + 1024 /*align*/ + 256 /*barriers*/;
 };
+// LEAN epilogue staging: 8 warps x two 4 KB buffers (32 rows x 128 B, 128B swizzle)
+constexpr int GEMM_LEAN_OUT = 8 * 2 * 4096;
 
 template <int BK>
 DEV uint32_t swz_layout() {
@@ -96,18 +100,31 @@ DEV void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cl, int 
 // 128B-swizzled atoms per stage), bit 1 = W is MN-major ((n, k) at k * ldw + n). MN-major
 // operands need BK = 64 and the CTA-pair kernel; the MMA reads them with the transpose bits
 // of the instruction descriptor.
-template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0>
+// DCHAG_GEMM_DEBUG bit 16: per-tile event timestamps (globaltimer ns) into outL, as
+// [event][cta][64 tiles] int64 (timing probe only; tools/gemm_epi_probe.py)
+#define GEMM_TRACE(ev, i)                                                                     \
+  do {                                                                                        \
+    if ((args.debug & 16) && (i) < 64) {                                                      \
+      long long t_;                                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                  \
+      reinterpret_cast<long long*>(args.outL)[((ev) * gridDim.x + blockIdx.x) * 64 + (i)] = t_; \
+    }                                                                                         \
+  } while (0)
+
+// LEAN: the plain bf16 epilogue (bias, no row bias / mask / row-dot / combine, every tile
+// full and a multiple of 64 columns wide) -- see the epilogue below.
+template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0, bool LEAN = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                 const __grid_constant__ CUtensorMap tmV, GemmArgs args) {
-  using SM = GemmSmem<BK, STAGES, PAIR>;
+  using SM = GemmSmem<BK, STAGES, PAIR, LEAN ? GEMM_LEAN_OUT : GEMM_STAGE_OUT>;
   constexpr int CL = PAIR ? 2 : 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* stage_out = smem + STAGES * SM::STAGE_BYTES;
-  float* bias_smem = reinterpret_cast<float*>(stage_out + GEMM_STAGE_OUT);
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + GEMM_STAGE_OUT + GEMM_BIAS_SMEM);
+  float* bias_smem = reinterpret_cast<float*>(stage_out + SM::OUT_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + SM::OUT_BYTES + GEMM_BIAS_SMEM);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -203,6 +220,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int ks = 0; ks < k_steps; ++ks) {
           const int g = c_first + ci;
           mbar_wait(&empty[stage], phase ^ 1);
+          GEMM_TRACE(0, (ct - ct_begin) / ct_step);
           uint8_t* sA = smem + stage * SM::STAGE_BYTES;
           uint8_t* sW = sA + SM::A_BYTES;
           if (PAIR) {
@@ -253,10 +271,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
        for (int ci = 0; ci < c_n; ++ci) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogues drained this accumulator buffer
         tc_fence_after();
+        if (lane == 0) GEMM_TRACE(1, (ct - ct_begin) / ct_step);
         const uint32_t d_tmem = tmem_base + acc * GEMM_BN_MAX;
         for (int ks = 0; ks < k_steps; ++ks) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (lane == 0) GEMM_TRACE(2, (ct - ct_begin) / ct_step);
           if (elect_one()) {
             const uint32_t a_addr = smem_u32(smem + stage * SM::STAGE_BYTES);
             const uint32_t w_addr = a_addr + SM::A_BYTES;
@@ -287,6 +307,93 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
        }
       }
     }
+  } else if constexpr (LEAN) {
+    // ------------------------------------------------ lean epilogue (warps 2..9)
+    // Warp (quarter q, half hf) drains rows [32q, 32q + 32) x columns [128 hf, 128 hf + 128)
+    // of its CTA's tile, 64 columns at a time: two TMEM loads in flight together, bias add,
+    // bf16 pack, one 128B-swizzled 4 KB staging buffer (two per warp), one TMA store of
+    // 32 rows x 128 B. The accumulator buffer goes back to the MMA warp as soon as the last
+    // TMEM load of the tile has landed. (The general epilogue below spends ~350 instructions
+    // and a dozen dependent branches per 32 columns; this path ~70.)
+    const int quarter = warp & 3;
+    const int hf = (warp - 2) >> 2;
+    const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t my_stage = smem_u32(stage_out) + (uint32_t)(warp - 2) * 8192u;
+    const uint32_t my_bias = smem_u32(bias_smem) + (uint32_t)(warp - 2) * 512u;
+    const int cols = args.BN - hf * 128;  // this warp's columns: 128, 64 or <= 0
+    const int npairs = cols >= 128 ? 2 : (cols >= 64 ? 1 : 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int vbuf = 0;
+    for (int t = ct_begin; t < ct_end; t += ct_step) {
+      int g, mt, nt;
+      decode(t, g, mt, nt);
+      const int c0 = nt * args.BN + hf * 128;
+      float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (args.bias && 4 * lane < cols)
+        b4 = __ldg(reinterpret_cast<const float4*>(args.bias + (size_t)g * args.bias_g + c0) + lane);
+      __syncwarp();  // the previous tile's bias reads are done
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(my_bias + 16u * lane),
+                   "f"(b4.x), "f"(b4.y), "f"(b4.z), "f"(b4.w)
+                   : "memory");
+      __syncwarp();
+      const int r0 = mt * GEMM_BM + quarter * 32;
+      const int mo0 = r0 / args.Mi, mi0 = r0 - mo0 * args.Mi;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_col = lane_base + acc * GEMM_BN_MAX + hf * 128;
+      auto release = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR)
+            asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(rank0_addr(&tempty[acc]))
+                         : "memory");
+          else
+            mbar_arrive(&tempty[acc]);
+        }
+      };
+      if (npairs == 0) release();
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        if (p >= npairs) break;
+        uint32_t ra[32], rb[32];
+        tmem_ld32(t_col + p * 64, ra);
+        tmem_ld32(t_col + p * 64 + 32, rb);
+        tmem_ld_wait(ra);
+        reg_fence32(rb);
+        if (p == npairs - 1) release();
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float4 b;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                       : "r"(my_bias + (uint32_t)(p * 64 + 4 * j) * 4u));
+          const uint32_t* r = j < 8 ? ra + 4 * j : rb + 4 * (j - 8);
+          pk[2 * j] = pack_bf16(__uint_as_float(r[0]) + b.x, __uint_as_float(r[1]) + b.y);
+          pk[2 * j + 1] = pack_bf16(__uint_as_float(r[2]) + b.z, __uint_as_float(r[3]) + b.w);
+        }
+        const uint32_t buf = my_stage + (uint32_t)vbuf * 4096u;
+        if (lane == 0) bulk_wait_read1();  // this buffer's previous store has read it
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                           buf + 128u * lane + ((uint32_t)(k ^ (lane & 7)) << 4)),
+                       "r"(pk[4 * k]), "r"(pk[4 * k + 1]), "r"(pk[4 * k + 2]), "r"(pk[4 * k + 3])
+                       : "memory");
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(&tmV, buf, c0 + p * 64, mi0, mo0, g);
+          bulk_commit();
+        }
+        vbuf ^= 1;
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) bulk_wait0();  // this warp's tensor stores complete before exit
   } else {
     // ------------------------------------------------ epilogue (warps 2..9)
     // Two warps per TMEM lane quarter; warp half hf drains the 32-column groups
@@ -304,51 +411,70 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const bool b_vec = (args.bias_g & 3) == 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    // two instantiations of the tile loop: row-dot tiles and the rest (each carries only its
+    // own registers: the row-dot dotG rows would otherwise stay live through the value path)
+    auto tile_loop = [&](auto dot_tag) {
+    constexpr bool DOT = !COMB && decltype(dot_tag)::value;
     int prev_mt = -1, prev_nt = -1;
-    uint4 rbv[4][4];  // row bias (or, in row-dot mode, dotG) of this thread's row, 4 groups
-    float4 dot_bias_pf = make_float4(0.f, 0.f, 0.f, 0.f);  // row-dot: next tile's bias
+    uint4 rbv[DOT ? 4 : 1][4];  // row-dot mode: this thread's dotG row, 4 column groups
+    float4 dot_bias_pf = make_float4(0.f, 0.f, 0.f, 0.f);  // the next tile's bias columns
     bool dot_pf_valid = false;
     for (int t = ct_begin; t < ct_end; t += ct_step) {
       int g, mt, nt;
+      if (warp == 2 && lane == 0) GEMM_TRACE(17, (t - ct_begin) / ct_step);
       decode(t, g, mt, nt);
       const int m_row = mt * GEMM_BM + row_in_tile;
       const int mo = m_row / args.Mi, mi = m_row - mo * args.Mi;
       // prefetch this thread's row bias for its column groups (in flight during the wait)
       // row-dot mode: the same registers carry this row's dotG columns instead
-      const bool dot = !COMB && args.dotOut != nullptr;
+      constexpr bool dot = DOT;
       const __nv_bfloat16* rb =
           dot ? args.dotG + (size_t)m_row * args.ldG
           : (args.rowbias && !(args.debug & 2)) ? args.rowbias + (size_t)g * args.rowbias_g +
                              (size_t)(mi % args.rowbias_period) * args.rowbias_row
                        : nullptr;
-      const bool reload = !COMB && (!dot || mt != prev_mt || nt != prev_nt);
+      // row-dot mode keeps its dotG rows in registers across the groups of one (mt, nt); the
+      // plain row bias is loaded per column group inside the (rolled) group loop below
+      const bool reload = dot && (mt != prev_mt || nt != prev_nt);
       prev_mt = mt;
       prev_nt = nt;
+      if constexpr (DOT) {
 #pragma unroll
-      for (int gi = 0; gi < 4; ++gi) {
-        if (!reload) break;
-        const int n0 = nt * args.BN + (hf + 2 * gi) * 32;
+        for (int gi = 0; gi < 4; ++gi) {
+          if (!reload) break;
+          const int n0 = nt * args.BN + (hf + 2 * gi) * 32;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          rbv[gi][j] = make_uint4(0, 0, 0, 0);
-          const int n = n0 + 8 * j;
-          if (rb && hf + 2 * gi < n_groups && n < args.N) {
-            if ((dot || rb_vec) && n + 8 <= args.N) {
-              rbv[gi][j] = __ldg(reinterpret_cast<const uint4*>(rb + n));
-            } else {
-              uint32_t w[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float lo = n + 2 * e < args.N ? __bfloat162float(rb[n + 2 * e]) : 0.f;
-                const float hi = n + 2 * e + 1 < args.N ? __bfloat162float(rb[n + 2 * e + 1]) : 0.f;
-                w[e] = pack_bf16(lo, hi);
-              }
-              rbv[gi][j] = make_uint4(w[0], w[1], w[2], w[3]);
+          for (int j = 0; j < 4; ++j) {
+            rbv[gi][j] = make_uint4(0, 0, 0, 0);
+            const int n = n0 + 8 * j;
+            if (rb && hf + 2 * gi < n_groups && n < args.N) {
+              rbv[gi][j] = __ldg(reinterpret_cast<const uint4*>(rb + n));  // N % 32 == 0
             }
           }
         }
       }
-      if (!COMB && dot) {
+      // row bias of one 32-column group (bf16, 8 per uint4), zeros past N / without row bias
+      auto load_rowbias = [&](int n0, uint4 (&q)[4]) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          q[j] = make_uint4(0, 0, 0, 0);
+          const int n = n0 + 8 * j;
+          if (!rb || n >= args.N) continue;
+          if (rb_vec && n + 8 <= args.N) {
+            q[j] = __ldg(reinterpret_cast<const uint4*>(rb + n));
+          } else {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float lo = n + 2 * e < args.N ? __bfloat162float(rb[n + 2 * e]) : 0.f;
+              const float hi = n + 2 * e + 1 < args.N ? __bfloat162float(rb[n + 2 * e + 1]) : 0.f;
+              w[e] = pack_bf16(lo, hi);
+            }
+            q[j] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      };
+      if constexpr (DOT) {
         // row-dot tile: sum over each 32-column group of (acc + bias) * dotG. The tile's
         // bias row (the channel's) was fetched during the previous tile, and the TMEM loads
         // of group i+1 are in flight while group i is reduced.
@@ -431,8 +557,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_arrive(&tempty[acc]);
         }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        continue;
-      }
+      } else {
       // combine mode: softmax statistics of this row over the parent's children, per group
       int c_first = g, c_n = 1;
       if (comb) comb_range(g, c_first, c_n);
@@ -475,48 +600,57 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           dot_pf_valid = true;
         }
       }
+      if (warp == 2 && lane == 0) GEMM_TRACE(18, (t - ct_begin) / ct_step);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (warp == 2 && lane == 0) GEMM_TRACE(3, (t - ct_begin) / ct_step);
       const uint32_t t_row = lane_base + acc * GEMM_BN_MAX;
-#pragma unroll
-      for (int gi = 0; gi < ((args.debug & 8) ? 0 : 4); ++gi) {
+      // a rolled loop over the warp's column groups (COMB keeps its running sums in registers
+      // and unrolls): the kernel's instruction footprint, and with it the per-tile
+      // instruction-fetch stalls, stays small
+      // The TMEM load of group gi + 1 is in flight while group gi is processed, and the
+      // accumulator buffer is handed back to the MMA warp as soon as the last load landed.
+      auto gvalid = [&](int gi) {
         const int grp = hf + 2 * gi;
-        if (grp >= n_groups) break;
-        const int n0 = nt * args.BN + grp * 32;
-        if (n0 >= args.N) break;
-        uint32_t r[32];
-        tmem_ld32(t_row + grp * 32, r);
-        tmem_ld_wait();
-        float v[32];
-        if (dot) {
-          // sum over the group's 32 columns of (acc + bias) * dotG (fp32)
-          float sdot = 0.f;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t q[4] = {rbv[gi][j].x, rbv[gi][j].y, rbv[gi][j].z, rbv[gi][j].w};
-            float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;
-            if (bias) {
-              b0 = reinterpret_cast<const float4*>(wbias + gi * 32)[2 * j];
-              b1 = reinterpret_cast<const float4*>(wbias + gi * 32)[2 * j + 1];
-            }
-            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              sdot = fmaf(__uint_as_float(r[8 * j + 2 * e]) + bb[2 * e], bf16lo(q[e]), sdot);
-              sdot = fmaf(__uint_as_float(r[8 * j + 2 * e + 1]) + bb[2 * e + 1], bf16hi(q[e]),
-                          sdot);
-            }
-          }
-          args.dotOut[((size_t)g * (args.N >> 5) + (n0 >> 5)) * args.M + m_row] = sdot;
-          continue;
+        return gi < 4 && !(args.debug & 8) && grp < n_groups && nt * args.BN + grp * 32 < args.N;
+      };
+      bool released = false;
+      auto release = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (warp == 2 && lane == 0) GEMM_TRACE(4, (t - ct_begin) / ct_step);
+        if (lane == 0) {
+          if (PAIR)  // the leader's MMA warp waits for both CTAs' drains
+            asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(rank0_addr(&tempty[acc]))
+                         : "memory");
+          else
+            mbar_arrive(&tempty[acc]);
         }
+        released = true;
+      };
+      uint32_t rn[32];
+      if (gvalid(0)) tmem_ld32(t_row + hf * 32, rn);
+#pragma unroll(COMB ? 4 : 1)
+      for (int gi = 0; gi < 4; ++gi) {
+        if (!gvalid(gi)) break;
+        const int grp = hf + 2 * gi;
+        const int n0 = nt * args.BN + grp * 32;
+        uint4 rq[4];
+        if constexpr (!COMB) load_rowbias(n0, rq);
+        tmem_ld_wait(rn);
+        uint32_t r[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = rn[j];
+        if (gvalid(gi + 1)) tmem_ld32(t_row + (grp + 2) * 32, rn);
+        else release();
+        float v[32];
         if constexpr (COMB) {  // no row bias in combine mode
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         } else {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const uint32_t q[4] = {rbv[gi][j].x, rbv[gi][j].y, rbv[gi][j].z, rbv[gi][j].w};
+            const uint32_t q[4] = {rq[j].x, rq[j].y, rq[j].z, rq[j].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               v[8 * j + 2 * e] = __uint_as_float(r[8 * j + 2 * e]) + bf16lo(q[e]);
@@ -679,18 +813,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (PAIR)  // the leader's MMA warp waits for both CTAs' drains
-          asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(rank0_addr(&tempty[acc]))
-                       : "memory");
-        else
-          mbar_arrive(&tempty[acc]);
-      }
+      if (!released) release();
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }  // children (COMB)
+      }  // value / combine tiles
     }
+    };
+    if (!COMB && dot_mode) tile_loop(std::true_type{});
+    else tile_loop(std::false_type{});
     if (lane == 0) bulk_wait0();  // this warp's tensor stores complete before exit
   }
 
@@ -707,13 +837,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0>
+template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0, bool LEAN = false>
 static cudaError_t launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tW,
                                  const CUtensorMap& tV, const GemmArgs& a, int num_sms,
                                  cudaStream_t st) {
-  using SM = GemmSmem<BK, STAGES, PAIR>;
+  using SM = GemmSmem<BK, STAGES, PAIR, LEAN ? GEMM_LEAN_OUT : GEMM_STAGE_OUT>;
   static_assert(SM::TOTAL <= 227 * 1024, "shared memory");
-  auto kern = gemm_kernel<BK, STAGES, PAIR, COMB, LAY>;
+  auto kern = gemm_kernel<BK, STAGES, PAIR, COMB, LAY, LEAN>;
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
   if (e != cudaSuccess) return e;
@@ -750,6 +880,8 @@ cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUte
       }
       if (a.pair && a.cfirst) return launch_gemm_t<64, 5, true, true>(tA, tW, tV, a, num_sms, st);
       if (a.cfirst) return cudaErrorInvalidValue;
+      if (a.pair && a.lean)
+        return launch_gemm_t<64, 4, true, false, 0, true>(tA, tW, tV, a, num_sms, st);
       if (a.pair) return launch_gemm_t<64, 5, true>(tA, tW, tV, a, num_sms, st);
       return launch_gemm_t<64, 3, false>(tA, tW, tV, a, num_sms, st);
     case 32: return launch_gemm_t<32, 6, false>(tA, tW, tV, a, num_sms, st);
