@@ -241,7 +241,7 @@ int dchag_child_softmax(float* L, const int* first, const int* count, int n_pare
  * tensor.py:201-203): dp_c[r][h] = sum of dchag_gemm_rowdot's 32-column partials of head h
  * (dpp fp32 [g][H*dh/32][R]) + Gpos[r][h] (dchag_l0_dv), then
  * dl_c = p_c (dp_c - sum_c' p_c' dp_c'); p as dchag_l0_dv. dl fp32 and dlb bf16, both
- * [g][H][R]. dh % 32 == 0. */
+ * [g][H][R]. dh % 32 == 0. dl may be NULL when g <= 16 and dh == 64 (only the bf16 copy is written). */
 int dchag_l0_softmax_bwd(int g, int R, int H, int nh, int dh, const float* dpp,
                          const float* Gpos, const void* p, float* dl, void* dlb, void* stream);
 

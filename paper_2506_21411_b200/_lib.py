@@ -13,7 +13,8 @@ import os
 from .config import ConfigError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdchag.so")
+# DCHAG_LIB: an alternative build of the same ABI (A/B timing probes only)
+LIB_PATH = os.environ.get("DCHAG_LIB") or os.path.join(_HERE, "libdchag.so")
 
 c_int, c_ll, c_vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p
 

@@ -294,6 +294,12 @@ static int gemm_impl(const void* A, int G, int Mo, int Mi, int K, long long sAg,
                                    "groups of 16-byte aligned rows (N=%d ldG=%lld)", N, ldG);
     a.v_tma = 0; a.rowbias = nullptr; a.outV = nullptr; a.outL = nullptr; a.Nv = N;
     a.dotG = reinterpret_cast<const __nv_bfloat16*>(dotG); a.ldG = ldG; a.dotOut = dotOut;
+    // lean row-dot drain: full tiles, 64-column aligned (DCHAG_GEMM_LEAN=0: general drain)
+    if ((a.debug & 16) && getenv("DCHAG_GEMM_TRACE_BUF"))  // timing probe: trace buffer
+      a.outL = reinterpret_cast<float*>(strtoull(getenv("DCHAG_GEMM_TRACE_BUF"), nullptr, 0));
+    a.lean = (pair && bn % 64 == 0 && N % bn == 0 && (a.debug & ~20) == 0 &&
+              (!bias || (bias_g % 4 == 0 && reinterpret_cast<uintptr_t>(bias) % 16 == 0)) &&
+              !(lean_env && atoi(lean_env) == 0)) ? 2 : 0;
   }
   return cuda_status(launch_gemm(tA, tW, tV, a, bk, num_sms_cached(), S(stream)), "gemm");
 }
@@ -629,8 +635,8 @@ int dchag_child_softmax(float* L, const int* first, const int* count, int n_pare
 
 int dchag_l0_softmax_bwd(int g, int R, int H, int nh, int dh, const float* dpp,
                          const float* Gpos, const void* p, float* dl, void* dlb, void* stream) {
-  if (g < 1 || R < 1 || H < 1 || dh % 32 || nh < 1 || H % nh || !dpp || !Gpos || !p || !dl ||
-      !dlb)
+  if (g < 1 || R < 1 || H < 1 || dh % 32 || nh < 1 || H % nh || !dpp || !Gpos || !p ||
+      (!dl && (g > 16 || dh != 64)) || !dlb)
     return fail(DCHAG_ERR_SHAPE, "l0_softmax_bwd: bad arguments");
   return cuda_status(launch_l0_softmax_bwd(g, R, H, nh, dh, dpp, Gpos,
                                            reinterpret_cast<const __nv_bfloat16*>(p), dl,

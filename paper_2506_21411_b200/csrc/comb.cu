@@ -613,10 +613,56 @@ __global__ void __launch_bounds__(256) l0_softmax_bwd_kernel(
   }
 }
 
+// Register-resident variant for g <= 16 channels and dh = 64: one thread per (head, row)
+// as above, every dp_c / p_c of the thread in registers -- all loads issued before any is
+// consumed, no dl round trip through memory; dl fp32 is optional (the tcgen05 TE path reads
+// only the bf16 copy).
+template <int GM, int NP>
+__global__ void __launch_bounds__(256) l0_softmax_bwd_reg_kernel(
+    int g, int R, int H, int NH, const float* __restrict__ dpp,
+    const float* __restrict__ Gpos, const __nv_bfloat16* __restrict__ p,
+    float* __restrict__ dl, __nv_bfloat16* __restrict__ dlb) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)R * H) return;
+  const int h = (int)(idx / R), r = (int)(idx - (long long)h * R);
+  const int hg = h / NH, hn = h - hg * NH, D32 = H * NP;
+  const float gp = __ldg(Gpos + (size_t)r * H + h);
+  float dp[GM], pv[GM];
+#pragma unroll
+  for (int c = 0; c < GM; ++c) {
+    dp[c] = gp;
+    pv[c] = 0.f;
+    if (c < g) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) dp[c] += __ldg(dpp + ((size_t)c * D32 + h * NP + k) * R + r);
+      pv[c] = __bfloat162float(p[((size_t)(hg * g + c) * R + r) * NH + hn]);
+    }
+  }
+  float sdp = 0.f;
+#pragma unroll
+  for (int c = 0; c < GM; ++c) sdp = fmaf(pv[c], dp[c], sdp);
+#pragma unroll
+  for (int c = 0; c < GM; ++c) {
+    if (c < g) {
+      const size_t o = ((size_t)c * H + h) * R + r;
+      const float v = pv[c] * (dp[c] - sdp);
+      if (dl) dl[o] = v;
+      dlb[o] = __float2bfloat16(v);
+    }
+  }
+}
+
 cudaError_t launch_l0_softmax_bwd(int g, int R, int H, int NH, int dh, const float* dpp,
                                   const float* Gpos, const __nv_bfloat16* p, float* dl,
                                   __nv_bfloat16* dlb, cudaStream_t st) {
   if (dh % 32 || NH < 1 || H % NH) return cudaErrorInvalidValue;
+  if (g <= 16 && dh == 64) {
+    const long long n = (long long)R * H;
+    l0_softmax_bwd_reg_kernel<16, 2><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        g, R, H, NH, dpp, Gpos, p, dl, dlb);
+    return cudaGetLastError();
+  }
+  if (!dl) return cudaErrorInvalidValue;  // the general kernel keeps dp in dl
   const long long n = (long long)R * H;
   l0_softmax_bwd_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, R, H, NH, dh, dpp,
                                                                      Gpos, p, dl, dlb);
@@ -1234,11 +1280,54 @@ __global__ void __launch_bounds__(256) unfold_kernel(const __nv_bfloat16* img, l
   }
 }
 
+// P = 8 / 16: a CTA takes ns consecutive strips of one image (one contiguous input run and
+// one contiguous output run), and every 16-byte output chunk -- eight consecutive pixels of
+// one patch row -- is a single 16-byte shared-memory read (shift / mask index math).
+template <int P>
+__global__ void __launch_bounds__(256) unfold_wide_kernel(const __nv_bfloat16* img,
+                                                          long long sb, long long sc, int C,
+                                                          int Himg, int W, int ns,
+                                                          __nv_bfloat16* out) {
+  extern __shared__ __align__(16) __nv_bfloat16 strip[];   // [ns * P][W]
+  const int hp = Himg / P, wp = W / P, S = hp * wp, nblk = hp / ns;
+  const int i0 = (blockIdx.x % nblk) * ns;
+  const int bc = blockIdx.x / nblk;
+  const int c = bc % C, b = bc / C;
+  const __nv_bfloat16* src = img + b * sb + c * sc + (long long)i0 * P * W;
+  const int n = ns * P * W;
+  for (int e = threadIdx.x * 8; e < n; e += blockDim.x * 8)
+    *reinterpret_cast<uint4*>(strip + e) = __ldg(reinterpret_cast<const uint4*>(src + e));
+  __syncthreads();
+  __nv_bfloat16* dst = out + (((long long)b * C + c) * S + (long long)i0 * wp) * P * P;
+  const int PW = P * W;
+  for (int e = threadIdx.x * 8; e < n; e += blockDim.x * 8) {
+    const int si = e / PW, o = e - si * PW;      // strip, offset in the strip's output run
+    const int j = o / (P * P), k = o % (P * P);  // patch, pixel (k % 8 == 0)
+    const int py = k / P, px = k % P;
+    *reinterpret_cast<uint4*>(dst + e) =
+        *reinterpret_cast<const uint4*>(strip + si * PW + py * W + j * P + px);
+  }
+}
+
 cudaError_t launch_unfold(const __nv_bfloat16* img, long long img_sb, long long img_sc, int B,
                           int C, int Himg, int W, int P, __nv_bfloat16* out, cudaStream_t st) {
   if ((P * W) % 8 || W % 8 || (img_sb | img_sc) % 8 ||
       (reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(out)) % 16)
     return cudaErrorInvalidValue;
+  if ((P == 8 || P == 16) && P * W * 2 <= 32 * 1024) {
+    // strips per CTA: the largest divisor of Himg / P within 32 KB of shared memory
+    const int hp = Himg / P;
+    int ns = 1;
+    for (int d = 1; d <= hp; ++d)
+      if (hp % d == 0 && d * P * W * 2 <= 32 * 1024) ns = d;
+    const int smem = ns * P * W * 2;
+    const unsigned grid = (unsigned)((long long)B * C * (hp / ns));
+    if (P == 8)
+      unfold_wide_kernel<8><<<grid, 256, smem, st>>>(img, img_sb, img_sc, C, Himg, W, ns, out);
+    else
+      unfold_wide_kernel<16><<<grid, 256, smem, st>>>(img, img_sb, img_sc, C, Himg, W, ns, out);
+    return cudaGetLastError();
+  }
   const int smem = P * W * 2;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(unfold_kernel,

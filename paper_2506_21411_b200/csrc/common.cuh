@@ -48,6 +48,17 @@ DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
+#ifdef DCHAG_MBAR_HINT
+  // suspend-time hint (ns): the waiting warp sleeps until the phase completes or the hint
+  // expires instead of re-polling
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "n"(DCHAG_MBAR_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
@@ -55,6 +66,7 @@ DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "=r"(ok)
       : "r"(addr), "r"(parity)
       : "memory");
+#endif
   return ok != 0;
 }
 // Blocking wait.  A wait that exceeds ~20 s (a pipeline bug) traps instead of hanging

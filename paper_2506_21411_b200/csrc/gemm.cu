@@ -111,13 +111,14 @@ DEV void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cl, int 
     }                                                                                         \
   } while (0)
 
-// LEAN: the plain bf16 epilogue (bias, no row bias / mask / row-dot / combine, every tile
-// full and a multiple of 64 columns wide) -- see the epilogue below.
-template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0, bool LEAN = false>
+// LEAN 1: the plain bf16 epilogue (bias, no row bias / mask / row-dot / combine, every tile
+// full and a multiple of 64 columns wide); LEAN 2: the same drain for row-dot tiles (see
+// the epilogue below).
+template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0, int LEAN = 0>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                 const __grid_constant__ CUtensorMap tmV, GemmArgs args) {
-  using SM = GemmSmem<BK, STAGES, PAIR, LEAN ? GEMM_LEAN_OUT : GEMM_STAGE_OUT>;
+  using SM = GemmSmem<BK, STAGES, PAIR, LEAN == 1 ? GEMM_LEAN_OUT : GEMM_STAGE_OUT>;
   constexpr int CL = PAIR ? 2 : 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -307,14 +308,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
        }
       }
     }
-  } else if constexpr (LEAN) {
+  } else if constexpr (LEAN != 0) {
     // ------------------------------------------------ lean epilogue (warps 2..9)
     // Warp (quarter q, half hf) drains rows [32q, 32q + 32) x columns [128 hf, 128 hf + 128)
     // of its CTA's tile, 64 columns at a time: two TMEM loads in flight together, bias add,
-    // bf16 pack, one 128B-swizzled 4 KB staging buffer (two per warp), one TMA store of
-    // 32 rows x 128 B. The accumulator buffer goes back to the MMA warp as soon as the last
-    // TMEM load of the tile has landed. (The general epilogue below spends ~350 instructions
-    // and a dozen dependent branches per 32 columns; this path ~70.)
+    // then either (LEAN 1) bf16 pack, one 128B-swizzled 4 KB staging buffer (two per warp)
+    // and one TMA store of 32 rows x 128 B, or (LEAN 2, row-dot) the two 32-column dot
+    // products with this row's dotG columns (held in registers while consecutive tiles share
+    // (mt, nt)), four independent partial sums each. The accumulator buffer goes back to
+    // the MMA warp as soon as the last TMEM load of the tile has landed. (The general
+    // epilogue below spends ~350 instructions and a dozen dependent branches per 32
+    // columns; this path ~70.)
     const int quarter = warp & 3;
     const int hf = (warp - 2) >> 2;
     const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
@@ -325,13 +329,39 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int vbuf = 0;
+    int prev_mt = -1, prev_nt = -1;
+    uint4 dg[LEAN == 2 ? 16 : 1];  // row-dot: this row's 128 dotG columns (bf16)
+    // the bias columns of a tile are fetched one tile ahead (a dependent global load per
+    // tile would otherwise stall the drain for the load's latency)
+    auto fetch_bias = [&](int t2) {
+      float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t2 < ct_end && args.bias && 4 * lane < cols) {
+        int g2, mt2, nt2;
+        decode(t2, g2, mt2, nt2);
+        b = __ldg(reinterpret_cast<const float4*>(args.bias + (size_t)g2 * args.bias_g +
+                                                  nt2 * args.BN + hf * 128) + lane);
+      }
+      return b;
+    };
+    float4 b_next = fetch_bias(ct_begin);
     for (int t = ct_begin; t < ct_end; t += ct_step) {
       int g, mt, nt;
       decode(t, g, mt, nt);
       const int c0 = nt * args.BN + hf * 128;
-      float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (args.bias && 4 * lane < cols)
-        b4 = __ldg(reinterpret_cast<const float4*>(args.bias + (size_t)g * args.bias_g + c0) + lane);
+      if constexpr (LEAN == 2) {
+        if (mt != prev_mt || nt != prev_nt) {
+          const uint4* src = reinterpret_cast<const uint4*>(
+              args.dotG + (size_t)(mt * GEMM_BM + quarter * 32 + lane) * args.ldG + c0);
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            dg[j] = 8 * j < cols ? __ldg(src + j) : make_uint4(0, 0, 0, 0);
+          prev_mt = mt;
+          prev_nt = nt;
+        }
+      }
+      if (warp == 2 && lane == 0) GEMM_TRACE(17, (t - ct_begin) / ct_step);
+      const float4 b4 = b_next;
+      b_next = fetch_bias(t + ct_step);
       __syncwarp();  // the previous tile's bias reads are done
       asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(my_bias + 16u * lane),
                    "f"(b4.x), "f"(b4.y), "f"(b4.z), "f"(b4.w)
@@ -339,12 +369,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       __syncwarp();
       const int r0 = mt * GEMM_BM + quarter * 32;
       const int mo0 = r0 / args.Mi, mi0 = r0 - mo0 * args.Mi;
+      if (warp == 2 && lane == 0) GEMM_TRACE(18, (t - ct_begin) / ct_step);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (warp == 2 && lane == 0) GEMM_TRACE(3, (t - ct_begin) / ct_step);
       const uint32_t t_col = lane_base + acc * GEMM_BN_MAX + hf * 128;
       auto release = [&]() {
         tc_fence_before();
         __syncwarp();
+        if (warp == 2 && lane == 0) GEMM_TRACE(4, (t - ct_begin) / ct_step);
         if (lane == 0) {
           if (PAIR)
             asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(rank0_addr(&tempty[acc]))
@@ -363,6 +396,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tmem_ld_wait(ra);
         reg_fence32(rb);
         if (p == npairs - 1) release();
+        if constexpr (LEAN == 2) {
+          const int m_row = mt * GEMM_BM + quarter * 32 + lane;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t* r = h ? rb : ra;
+            float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // 4 columns per step
+              float4 b;
+              asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                           : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                           : "r"(my_bias + (uint32_t)(p * 64 + h * 32 + 4 * j) * 4u));
+              const uint4 q = dg[8 * p + 4 * h + (j >> 1)];
+              const uint32_t q0 = (j & 1) ? q.z : q.x, q1 = (j & 1) ? q.w : q.y;
+              float& a = s4[j & 3];
+              a = fmaf(__uint_as_float(r[4 * j]) + b.x, bf16lo(q0), a);
+              a = fmaf(__uint_as_float(r[4 * j + 1]) + b.y, bf16hi(q0), a);
+              a = fmaf(__uint_as_float(r[4 * j + 2]) + b.z, bf16lo(q1), a);
+              a = fmaf(__uint_as_float(r[4 * j + 3]) + b.w, bf16hi(q1), a);
+            }
+            args.dotOut[((size_t)g * (args.N >> 5) + (c0 >> 5) + 2 * p + h) * args.M + m_row] =
+                (s4[0] + s4[1]) + (s4[2] + s4[3]);
+          }
+        } else {
         uint32_t pk[32];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -390,6 +447,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           bulk_commit();
         }
         vbuf ^= 1;
+        }  // store tiles
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -837,11 +895,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0, bool LEAN = false>
+template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0, int LEAN = 0>
 static cudaError_t launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tW,
                                  const CUtensorMap& tV, const GemmArgs& a, int num_sms,
                                  cudaStream_t st) {
-  using SM = GemmSmem<BK, STAGES, PAIR, LEAN ? GEMM_LEAN_OUT : GEMM_STAGE_OUT>;
+  using SM = GemmSmem<BK, STAGES, PAIR, LEAN == 1 ? GEMM_LEAN_OUT : GEMM_STAGE_OUT>;
   static_assert(SM::TOTAL <= 227 * 1024, "shared memory");
   auto kern = gemm_kernel<BK, STAGES, PAIR, COMB, LAY, LEAN>;
   cudaError_t e =
@@ -880,8 +938,10 @@ cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUte
       }
       if (a.pair && a.cfirst) return launch_gemm_t<64, 5, true, true>(tA, tW, tV, a, num_sms, st);
       if (a.cfirst) return cudaErrorInvalidValue;
-      if (a.pair && a.lean)
-        return launch_gemm_t<64, 4, true, false, 0, true>(tA, tW, tV, a, num_sms, st);
+      if (a.pair && a.lean == 1)
+        return launch_gemm_t<64, 4, true, false, 0, 1>(tA, tW, tV, a, num_sms, st);
+      if (a.pair && a.lean == 2)
+        return launch_gemm_t<64, 5, true, false, 0, 2>(tA, tW, tV, a, num_sms, st);
       if (a.pair) return launch_gemm_t<64, 5, true>(tA, tW, tV, a, num_sms, st);
       return launch_gemm_t<64, 3, false>(tA, tW, tV, a, num_sms, st);
     case 32: return launch_gemm_t<32, 6, false>(tA, tW, tV, a, num_sms, st);

@@ -310,26 +310,12 @@ DEV long long tiled_off(int blk, int k, int n, int K, int N) {  // canonical K-m
          (n & 7) * 8 + (k & 7);
 }
 
-__global__ void pack_mt_kernel(L0PackArgs a) {  // Mt [H*2][C_pad*PP][hw] tiled
+// One pass over the slab's fold rows, k fastest so every MT row segment is read coalesced,
+// written to both layouts that hold M_c: K_l0's tiled Mt [H*2][C_pad*PP][hw] (8-element
+// runs) and the row-dot operand Mrow [C][D][PP], plus Cb [C][D]. Mt's padding channels
+// [C, C_pad) are zero from allocation and never written.
+__global__ void pack_rows_kernel(L0PackArgs a) {
   const int hw = a.D / a.H / 2, K = a.C_pad * a.PP;
-  const long long total = (long long)a.H * 2 * K * hw;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int blk = (int)(t / ((long long)K * hw));
-    const int rem = (int)(t - (long long)blk * K * hw);
-    const int k = rem / hw, nn = rem - (rem / hw) * hw;
-    const int c = k / a.PP, kk = k - c * a.PP;
-    const int d = blk * hw + nn;  // blk = h * 2 + half
-    float v = 0.f;
-    if (c < a.C) {
-      const int n = __ldg(a.chan_node + c), l = __ldg(a.chan_local + c);
-      v = a.MT[((size_t)n * a.Dp + d) * a.Kn + l * a.PP + kk];
-    }
-    a.Mt[tiled_off(blk, k, nn, K, hw)] = __float2bfloat16(v);
-  }
-}
-
-__global__ void pack_rows_kernel(L0PackArgs a) {  // Mrow [C][D][PP] bf16, Cb [C][D] fp32
   const long long total = (long long)a.C * a.D * (a.PP + 1);
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
@@ -338,10 +324,14 @@ __global__ void pack_rows_kernel(L0PackArgs a) {  // Mrow [C][D][PP] bf16, Cb [C
     const int d = rem / (a.PP + 1), kk = rem - d * (a.PP + 1);
     const int n = __ldg(a.chan_node + c), l = __ldg(a.chan_local + c);
     const float* row = a.MT + ((size_t)n * a.Dp + d) * a.Kn;
-    if (kk < a.PP)
-      a.Mrow[((size_t)c * a.D + d) * a.PP + kk] = __float2bfloat16(row[l * a.PP + kk]);
-    else
+    if (kk < a.PP) {
+      const __nv_bfloat16 v = __float2bfloat16(row[l * a.PP + kk]);
+      a.Mrow[((size_t)c * a.D + d) * a.PP + kk] = v;
+      const int blk = d / hw, nn = d - blk * hw;
+      a.Mt[tiled_off(blk, c * a.PP + kk, nn, K, hw)] = v;
+    } else {
       a.Cb[(size_t)c * a.D + d] = row[a.ones0 + l];
+    }
   }
 }
 
@@ -402,7 +392,6 @@ __global__ void pack_pos_kernel(L0PackArgs a) {
 
 cudaError_t launch_l0_pack(const L0PackArgs& a, cudaStream_t st) {
   const int grid = 148 * 8;
-  pack_mt_kernel<<<grid, 256, 0, st>>>(a);
   pack_rows_kernel<<<grid, 256, 0, st>>>(a);
   pack_et_kernel<<<grid, 256, 0, st>>>(a);
   if (a.WUt) pack_logit_kernel<<<grid, 256, 0, st>>>(a);

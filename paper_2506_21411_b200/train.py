@@ -843,7 +843,9 @@ class DchagTrainer:
                             "bytes": R * D * 2 + g * R * PP * 2 + g * D // 32 * R * 4})
             dl = dlb = None
             if attn:
-                dl = torch.empty(g, H, R, device=dev)
+                # the tcgen05 TE kernel reads only the bf16 copy (fp32 dl: the generic path)
+                if not fast or g > 16 or dh != 64:
+                    dl = torch.empty(g, H, R, device=dev)
                 dlb = torch.empty(g, H, R, device=dev, dtype=torch.bfloat16)
                 _lib.call("dchag_l0_softmax_bwd", g, R, H, st["NH"], dh, _ptr(dpp), _ptr(Gpos),
                           _ptr(pblk), _lib.ptr(dl), _ptr(dlb), sh,
