@@ -703,7 +703,8 @@ __global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a
   const int pitch = 4 * D + 16;
   const int rows = 16 * MI;
   uint8_t* qk = fsm_raw;                                             // [rows][pitch]
-  float* tsm = reinterpret_cast<float*>(fsm_raw + rows * pitch);     // [H][32] t_i,h
+  uint8_t* pqs = fsm_raw + rows * pitch;                             // positional query row
+  float* tsm = reinterpret_cast<float*>(pqs + pitch);                // [H][32] t_i,h
   float* p2s = tsm + H * 32;                                         // [32]
   if (threadIdx.x == 0) {
     mbar_init(&landed, 1);
@@ -711,30 +712,28 @@ __global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    mbar_expect_tx(&landed, (uint32_t)g * 4 * D);
+    mbar_expect_tx(&landed, (uint32_t)g * 4 * D + (a.posq ? 2 * D : 0));
     for (int j = 0; j < g; ++j)
       bulk_load(qk + j * pitch, a.QK + (long long)(first + j) * a.sQj + (long long)r * a.ldq,
                 4 * D, &landed);
+    if (a.posq)
+      bulk_load(pqs, a.posq + ((long long)n * a.S + r % a.S) * D, 2 * D, &landed);
   }
+  // this lane's u values (independent of the copies: in flight during them)
+  const float sc = rsqrtf((float)dh);
+  float uj[2 * MI][2];
+#pragma unroll
+  for (int nj = 0; nj < 2 * MI; ++nj)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = nj * 8 + 2 * tig + e;
+      uj[nj][e] = j < g ? __ldg(a.u + (long long)(first + j) * a.sUj + (long long)r * H + h) : 0.f;
+    }
   const int cpr = D / 8;                           // 16-byte chunks of a q (or k) row
   for (int t = threadIdx.x; t < (rows - g) * 2 * cpr; t += blockDim.x)   // rows beyond g: 0
     *reinterpret_cast<uint4*>(qk + (g + t / (2 * cpr)) * pitch + (t % (2 * cpr)) * 16) =
         make_uint4(0, 0, 0, 0);
   mbar_wait(&landed, 0);
-  if (a.posq) {  // + the positional query of this position, in place
-    const __nv_bfloat16* pqr = a.posq + ((long long)n * a.S + r % a.S) * D;
-    for (int t = threadIdx.x; t < g * cpr; t += blockDim.x) {
-      const int j = t / cpr, c = t - j * cpr;
-      uint8_t* dst = qk + j * pitch + c * 16;
-      uint4 v = *reinterpret_cast<const uint4*>(dst);
-      const uint4 pq = __ldg(reinterpret_cast<const uint4*>(pqr) + c);
-      v.x = pack_bf16(bf16lo(v.x) + bf16lo(pq.x), bf16hi(v.x) + bf16hi(pq.x));
-      v.y = pack_bf16(bf16lo(v.y) + bf16lo(pq.y), bf16hi(v.y) + bf16hi(pq.y));
-      v.z = pack_bf16(bf16lo(v.z) + bf16lo(pq.z), bf16hi(v.z) + bf16hi(pq.z));
-      v.w = pack_bf16(bf16lo(v.w) + bf16lo(pq.w), bf16hi(v.w) + bf16hi(pq.w));
-      *reinterpret_cast<uint4*>(dst) = v;
-    }
-  }
   __syncthreads();
   // logits S^h = q_h k_h^T / sqrt(dh) on the tensor cores
   float acc[MI][NJ][4];
@@ -754,6 +753,11 @@ __global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a
       ldsm_x4(smem_u32(qk + row * pitch + col + 16 * (mat >> 1)), af[mi]);
     }
 #pragma unroll
+    // the positional query (q_i + pos q) . k_j = q_i . k_j + posq . k_j: one more product
+    // with the posq row broadcast to all 16 fragment rows (no in-place add over g rows)
+    uint32_t pf[4];
+    if (a.posq) ldsm_x4(smem_u32(pqs + col + 16 * (mat >> 1)), pf);
+#pragma unroll
     for (int np = 0; np < NJ / 2; ++np) {
       uint32_t bf[4];
       const int row = np * 16 + rr + 8 * (mat >> 1);
@@ -762,19 +766,14 @@ __global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a
       for (int mi = 0; mi < MI; ++mi) {
         mma_16816(acc[mi][2 * np], af[mi], bf[0], bf[1]);
         mma_16816(acc[mi][2 * np + 1], af[mi], bf[2], bf[3]);
+        if (a.posq) {
+          mma_16816(acc[mi][2 * np], pf, bf[0], bf[1]);
+          mma_16816(acc[mi][2 * np + 1], pf, bf[2], bf[3]);
+        }
       }
     }
   }
   // softmax over j of every row i (quad shuffles), t_i = sum_j S_ij u_jh
-  const float sc = rsqrtf((float)dh);
-  float uj[NJ][2];
-#pragma unroll
-  for (int nj = 0; nj < NJ; ++nj)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int j = nj * 8 + 2 * tig + e;
-      uj[nj][e] = j < g ? __ldg(a.u + (long long)(first + j) * a.sUj + (long long)r * H + h) : 0.f;
-    }
 #pragma unroll
   for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
@@ -869,7 +868,7 @@ cudaError_t launch_fullcross_weights(const FullCrossArgs& a, cudaStream_t st) {
   const int dh = a.D / a.H;
   if (a.max_g > 32 || a.H > 32 || dh % 16 || a.H < 1 || a.D % 8) return cudaErrorInvalidValue;
   const int MI = a.max_g > 16 ? 2 : 1;
-  const size_t smem = (size_t)16 * MI * (a.D * 4 + 16) + ((size_t)a.H * 32 + 32) * 4;
+  const size_t smem = (size_t)(16 * MI + 1) * (a.D * 4 + 16) + ((size_t)a.H * 32 + 32) * 4;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   auto kern = MI == 2 ? fullcross_weights_kernel<2> : fullcross_weights_kernel<1>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
