@@ -268,6 +268,13 @@ static int gemm_impl(const void* A, int G, int Mo, int Mi, int K, long long sAg,
                     bn % 64 == 0 && N % bn == 0 && Mi % 32 == 0 && a.debug == 0 &&
                     (!bias || (bias_g % 4 == 0 && reinterpret_cast<uintptr_t>(bias) % 16 == 0)) &&
                     !(lean_env && atoi(lean_env) == 0);
+  // narrow fp32 logit-only GEMMs (the full_cross u columns): lean drain, direct row stores
+  if (pair && !dot && !rowbias && !rmask && Nv == 0 && outL && N <= 256 && N % 16 == 0 &&
+      bn == N && a.debug == 0 && !(lean_env && atoi(lean_env) == 0) &&
+      ((reinterpret_cast<uintptr_t>(outL) | (uintptr_t)(sLmi * 4) | (uintptr_t)(sLmo * 4) |
+        (uintptr_t)(sLg * 4)) % 16) == 0 &&
+      (!bias || (bias_g % 4 == 0 && reinterpret_cast<uintptr_t>(bias) % 16 == 0)))
+    a.lean = 3;
   if (outV && !outV_f32 && Nv >= 32 && Mi % 32 == 0 &&
       ((reinterpret_cast<uintptr_t>(outV) | (uintptr_t)(sVmi * 2) | (uintptr_t)(sVmo * 2) |
         (uintptr_t)(sVg * 2)) % 16) == 0 && !getenv("DCHAG_GEMM_NO_TMA_STORE")) {

@@ -112,8 +112,8 @@ DEV void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cl, int 
   } while (0)
 
 // LEAN 1: the plain bf16 epilogue (bias, no row bias / mask / row-dot / combine, every tile
-// full and a multiple of 64 columns wide); LEAN 2: the same drain for row-dot tiles (see
-// the epilogue below).
+// full and a multiple of 64 columns wide); LEAN 2: the same drain for row-dot tiles; LEAN 3:
+// narrow fp32 logit-only tiles (see the epilogue below).
 template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0, int LEAN = 0>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
@@ -386,6 +386,39 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_arrive(&tempty[acc]);
         }
       };
+      if constexpr (LEAN == 3) {
+        // narrow fp32 tiles (the logit columns alone, N <= 256): each thread writes its row's
+        // columns straight from registers, 16-byte stores (rows are contiguous: coalesced)
+        const int nq = cols > 0 ? (min(cols, 128) + 31) / 32 : 0;
+        const int m_row = mt * GEMM_BM + quarter * 32 + lane;
+        const int mo = m_row / args.Mi, mi = m_row - mo * args.Mi;
+        float* dst = args.outL + (size_t)g * args.sLg + (size_t)mo * args.sLmo +
+                     (size_t)mi * args.sLmi + c0;
+        if (nq == 0) release();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (q >= nq) break;
+          uint32_t ra[32];
+          tmem_ld32(t_col + q * 32, ra);
+          tmem_ld_wait(ra);
+          if (q == nq - 1) release();
+          const int nvalid = min(32, cols - q * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (4 * j >= nvalid) break;
+            float4 b;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                         : "r"(my_bias + (uint32_t)(q * 32 + 4 * j) * 4u));
+            reinterpret_cast<float4*>(dst + q * 32)[j] =
+                make_float4(__uint_as_float(ra[4 * j]) + b.x, __uint_as_float(ra[4 * j + 1]) + b.y,
+                            __uint_as_float(ra[4 * j + 2]) + b.z,
+                            __uint_as_float(ra[4 * j + 3]) + b.w);
+          }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
       if (npairs == 0) release();
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
@@ -942,6 +975,8 @@ cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUte
         return launch_gemm_t<64, 4, true, false, 0, 1>(tA, tW, tV, a, num_sms, st);
       if (a.pair && a.lean == 2)
         return launch_gemm_t<64, 5, true, false, 0, 2>(tA, tW, tV, a, num_sms, st);
+      if (a.pair && a.lean == 3)
+        return launch_gemm_t<64, 5, true, false, 0, 3>(tA, tW, tV, a, num_sms, st);
       if (a.pair) return launch_gemm_t<64, 5, true>(tA, tW, tV, a, num_sms, st);
       return launch_gemm_t<64, 3, false>(tA, tW, tV, a, num_sms, st);
     case 32: return launch_gemm_t<32, 6, false>(tA, tW, tV, a, num_sms, st);
