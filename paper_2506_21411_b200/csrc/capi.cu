@@ -449,11 +449,18 @@ int dchag_gemm_combine(const void* ctx, int n_children, int R, int D, int H, con
     int rc = make_map(&tW, W, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
   }
+  // lean combine drain (heads of >= 64 columns, 64-column aligned; DCHAG_GEMM_LEAN=0 or a
+  // timing probe selects the general epilogue)
+  const char* lean_env = getenv("DCHAG_GEMM_LEAN");
+  const int dbg = getenv("DCHAG_GEMM_DEBUG") ? atoi(getenv("DCHAG_GEMM_DEBUG")) : 0;
+  const bool lean = (D / H) % 64 == 0 && dbg == 0 && !(lean_env && atoi(lean_env) == 0) &&
+                    (!bias || (bias_g % 4 == 0 && reinterpret_cast<uintptr_t>(bias) % 16 == 0));
   {
     cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)R, 1, (cuuint64_t)n_parents * csplit};
     cuuint64_t str[3] = {(cuuint64_t)D * 2, (cuuint64_t)R * D * 2, (cuuint64_t)R * D * 2};
-    cuuint32_t box[4] = {32, 32, 1, 1};
-    int rc = make_map(&tV, out, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B);
+    cuuint32_t box[4] = {lean ? 64u : 32u, 32, 1, 1};
+    int rc = make_map(&tV, out, 4, dims, str, box,
+                      lean ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
   GemmArgs a;
@@ -465,7 +472,8 @@ int dchag_gemm_combine(const void* ctx, int n_children, int R, int D, int H, con
   a.rowbias_period = 1;
   a.outV = out; a.sVg = (long long)R * D; a.sVmo = 0; a.sVmi = D;
   a.cfirst = first; a.ccount = count; a.Lpre = Lpre; a.H = H; a.dh = D / H;
-  a.debug = getenv("DCHAG_GEMM_DEBUG") ? atoi(getenv("DCHAG_GEMM_DEBUG")) : 0;
+  a.debug = dbg;
+  a.lean = lean ? 4 : 0;
   return cuda_status(launch_gemm(tA, tW, tV, a, 64, num_sms_cached(), S(stream)),
                      "gemm_combine");
 }

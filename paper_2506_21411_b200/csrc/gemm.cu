@@ -118,7 +118,7 @@ template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0, int LEA
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                 const __grid_constant__ CUtensorMap tmV, GemmArgs args) {
-  using SM = GemmSmem<BK, STAGES, PAIR, LEAN == 1 ? GEMM_LEAN_OUT : GEMM_STAGE_OUT>;
+  using SM = GemmSmem<BK, STAGES, PAIR, (LEAN == 1 || LEAN == 4) ? GEMM_LEAN_OUT : GEMM_STAGE_OUT>;
   constexpr int CL = PAIR ? 2 : 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -308,6 +308,134 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
        }
       }
     }
+  } else if constexpr (COMB && LEAN == 4) {
+    // ------------------------------------------------ lean combine epilogue (warps 2..9)
+    // As the lean epilogue (warp = rows [32q, 32q + 32) x columns [128 hf, 128 hf + 128)),
+    // with the softmax-weighted sum over the parent's children kept in registers as fp16
+    // pairs scaled by 2^-8 (range +-1.68e7, as the general combine epilogue): per child and
+    // column pair one FFMA pair ((acc + bias) / 256 with the bias pre-scaled in shared
+    // memory), one pack and one HFMA2 (run += p_child,head * v / 256); the last child is
+    // added in fp32 and leaves as bf16 through the 128B-swizzled staging + TMA store. A
+    // partial sum beyond the fp16 range raises the overflow flag (dchag_combine_overflow).
+    const int quarter = warp & 3;
+    const int hf = (warp - 2) >> 2;
+    const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t my_stage = smem_u32(stage_out) + (uint32_t)(warp - 2) * 8192u;
+    const uint32_t my_bias = smem_u32(bias_smem) + (uint32_t)(warp - 2) * 512u;
+    const int cols = args.BN - hf * 128;  // 128, 64 or <= 0 (BN % 64 == 0)
+    const int npairs = cols >= 128 ? 2 : (cols >= 64 ? 1 : 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int vbuf = 0;
+    for (int t = ct_begin; t < ct_end; t += ct_step) {
+      int g, mt, nt;
+      decode(t, g, mt, nt);
+      int c_first, c_n;
+      comb_range(g, c_first, c_n);
+      const int c0 = nt * args.BN + hf * 128;
+      const int m_row = mt * GEMM_BM + quarter * 32 + lane;
+      const int r0 = mt * GEMM_BM + quarter * 32;
+      const int mo0 = r0 / args.Mi, mi0 = r0 - mo0 * args.Mi;
+      const int hd0 = min(c0 / args.dh, args.H - 1), hd1 = min((c0 + 64) / args.dh, args.H - 1);
+      __half2 run[2][32];
+      __half2 mx = __float2half2_rn(0.f);
+      for (int ci = 0; ci < c_n; ++ci) {
+        const int gb = c_first + ci;
+        const bool last = ci + 1 == c_n;
+        float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (args.bias && 4 * lane < cols)
+          b4 = __ldg(reinterpret_cast<const float4*>(args.bias + (size_t)gb * args.bias_g + c0) +
+                     lane);
+        const float* lp = args.Lpre + ((size_t)gb * args.M + m_row) * args.H;
+        const float pw0 = __ldg(lp + hd0), pw1 = __ldg(lp + hd1);
+        __syncwarp();  // the previous child's bias reads are done
+        constexpr float kS = 1.f / 256.f;
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(my_bias + 16u * lane),
+                     "f"(b4.x * kS), "f"(b4.y * kS), "f"(b4.z * kS), "f"(b4.w * kS)
+                     : "memory");
+        __syncwarp();
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t t_col = lane_base + acc * GEMM_BN_MAX + hf * 128;
+        auto release = [&]() {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(rank0_addr(&tempty[acc]))
+                         : "memory");
+        };
+        if (npairs == 0) release();
+        uint32_t rn[32];
+        if (npairs > 0) tmem_ld32(t_col, rn);
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          if (p >= npairs) break;
+          const float pw = p ? pw1 : pw0;
+          const __half2 pw2 = __float2half2_rn(pw);
+          const uint32_t buf = my_stage + (uint32_t)vbuf * 4096u;
+          if (last) {
+            if (lane == 0) bulk_wait_read1();  // this staging buffer's previous store is read
+            __syncwarp();
+          }
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {  // 32-column halves; the next half's load in flight
+            tmem_ld_wait(rn);
+            uint32_t r[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) r[e] = rn[e];
+            if (hh == 0 || p + 1 < npairs) tmem_ld32(t_col + p * 64 + hh * 32 + 32, rn);
+            else release();
+            uint32_t pk[16];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // 4 columns per step
+              float4 b;
+              asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                           : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                           : "r"(my_bias + (uint32_t)(p * 64 + hh * 32 + 4 * j) * 4u));
+              const float f0 = fmaf(__uint_as_float(r[4 * j]), kS, b.x);
+              const float f1 = fmaf(__uint_as_float(r[4 * j + 1]), kS, b.y);
+              const float f2 = fmaf(__uint_as_float(r[4 * j + 2]), kS, b.z);
+              const float f3 = fmaf(__uint_as_float(r[4 * j + 3]), kS, b.w);
+              __half2& u01 = run[p][16 * hh + 2 * j];
+              __half2& u23 = run[p][16 * hh + 2 * j + 1];
+              if (!last) {
+                const __half2 h01 = __floats2half2_rn(f0, f1), h23 = __floats2half2_rn(f2, f3);
+                u01 = ci ? __hfma2(pw2, h01, u01) : __hmul2(pw2, h01);
+                u23 = ci ? __hfma2(pw2, h23, u23) : __hmul2(pw2, h23);
+                mx = __hmax2(mx, __hmax2(__habs2(u01), __habs2(u23)));
+              } else {  // last child in fp32: out = 256 (pw f / 256 + run)
+                const float2 q01 = ci ? __half22float2(u01) : make_float2(0.f, 0.f);
+                const float2 q23 = ci ? __half22float2(u23) : make_float2(0.f, 0.f);
+                pk[2 * j] = pack_bf16(256.f * fmaf(pw, f0, q01.x), 256.f * fmaf(pw, f1, q01.y));
+                pk[2 * j + 1] = pack_bf16(256.f * fmaf(pw, f2, q23.x), 256.f * fmaf(pw, f3, q23.y));
+              }
+            }
+            if (last) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                 buf + 128u * lane + ((uint32_t)((4 * hh + k) ^ (lane & 7)) << 4)),
+                             "r"(pk[4 * k]), "r"(pk[4 * k + 1]), "r"(pk[4 * k + 2]),
+                             "r"(pk[4 * k + 3])
+                             : "memory");
+            }
+          }
+          if (last) {
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_4d(&tmV, buf, c0 + p * 64, mi0, mo0, g);
+              bulk_commit();
+            }
+            vbuf ^= 1;
+          }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+      // the fp16 partial sums stayed finite (an inf / NaN compares false: flagged too)
+      if (!(fmaxf(__low2float(mx), __high2float(mx)) <= 65504.f)) g_comb_overflow = 1;
+    }
+    if (lane == 0) bulk_wait0();
   } else if constexpr (LEAN != 0) {
     // ------------------------------------------------ lean epilogue (warps 2..9)
     // Warp (quarter q, half hf) drains rows [32q, 32q + 32) x columns [128 hf, 128 hf + 128)
@@ -932,7 +1060,7 @@ template <int BK, int STAGES, bool PAIR, bool COMB = false, int LAY = 0, int LEA
 static cudaError_t launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tW,
                                  const CUtensorMap& tV, const GemmArgs& a, int num_sms,
                                  cudaStream_t st) {
-  using SM = GemmSmem<BK, STAGES, PAIR, LEAN == 1 ? GEMM_LEAN_OUT : GEMM_STAGE_OUT>;
+  using SM = GemmSmem<BK, STAGES, PAIR, (LEAN == 1 || LEAN == 4) ? GEMM_LEAN_OUT : GEMM_STAGE_OUT>;
   static_assert(SM::TOTAL <= 227 * 1024, "shared memory");
   auto kern = gemm_kernel<BK, STAGES, PAIR, COMB, LAY, LEAN>;
   cudaError_t e =
@@ -969,6 +1097,8 @@ cudaError_t launch_gemm(const CUtensorMap& tA, const CUtensorMap& tW, const CUte
         if (a.lay == 2) return launch_gemm_t<64, 5, true, false, 2>(tA, tW, tV, a, num_sms, st);
         return launch_gemm_t<64, 5, true, false, 3>(tA, tW, tV, a, num_sms, st);
       }
+      if (a.pair && a.cfirst && a.lean == 4)
+        return launch_gemm_t<64, 4, true, true, 0, 4>(tA, tW, tV, a, num_sms, st);
       if (a.pair && a.cfirst) return launch_gemm_t<64, 5, true, true>(tA, tW, tV, a, num_sms, st);
       if (a.cfirst) return cudaErrorInvalidValue;
       if (a.pair && a.lean == 1)
