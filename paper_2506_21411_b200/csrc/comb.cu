@@ -711,12 +711,13 @@ __global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a
     fence_barrier_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(&landed, (uint32_t)g * 4 * D + (a.posq ? 2 * D : 0));
-    for (int j = 0; j < g; ++j)
-      bulk_load(qk + j * pitch, a.QK + (long long)(first + j) * a.sQj + (long long)r * a.ldq,
+  if (warp == 0) {  // lane j issues child j's copy (lane g the posq row): parallel issue
+    if (lane == 0) mbar_expect_tx(&landed, (uint32_t)g * 4 * D + (a.posq ? 2 * D : 0));
+    __syncwarp();
+    if (lane < g)
+      bulk_load(qk + lane * pitch, a.QK + (long long)(first + lane) * a.sQj + (long long)r * a.ldq,
                 4 * D, &landed);
-    if (a.posq)
+    else if (lane == g && a.posq)
       bulk_load(pqs, a.posq + ((long long)n * a.S + r % a.S) * D, 2 * D, &landed);
   }
   // this lane's u values (independent of the copies: in flight during them)
@@ -729,10 +730,6 @@ __global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a
       const int j = nj * 8 + 2 * tig + e;
       uj[nj][e] = j < g ? __ldg(a.u + (long long)(first + j) * a.sUj + (long long)r * H + h) : 0.f;
     }
-  const int cpr = D / 8;                           // 16-byte chunks of a q (or k) row
-  for (int t = threadIdx.x; t < (rows - g) * 2 * cpr; t += blockDim.x)   // rows beyond g: 0
-    *reinterpret_cast<uint4*>(qk + (g + t / (2 * cpr)) * pitch + (t % (2 * cpr)) * 16) =
-        make_uint4(0, 0, 0, 0);
   mbar_wait(&landed, 0);
   __syncthreads();
   // logits S^h = q_h k_h^T / sqrt(dh) on the tensor cores
@@ -749,10 +746,11 @@ __global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a
     uint32_t af[MI][4];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
-      const int row = mi * 16 + rr + 8 * (mat & 1);
+      // children beyond g read child 0's row (finite; their logits rows / columns are masked)
+      int row = mi * 16 + rr + 8 * (mat & 1);
+      row = row < g ? row : 0;
       ldsm_x4(smem_u32(qk + row * pitch + col + 16 * (mat >> 1)), af[mi]);
     }
-#pragma unroll
     // the positional query (q_i + pos q) . k_j = q_i . k_j + posq . k_j: one more product
     // with the posq row broadcast to all 16 fragment rows (no in-place add over g rows)
     uint32_t pf[4];
@@ -760,7 +758,8 @@ __global__ void __launch_bounds__(1024) fullcross_weights_kernel(FullCrossArgs a
 #pragma unroll
     for (int np = 0; np < NJ / 2; ++np) {
       uint32_t bf[4];
-      const int row = np * 16 + rr + 8 * (mat >> 1);
+      int row = np * 16 + rr + 8 * (mat >> 1);
+      row = row < g ? row : 0;
       ldsm_x4(smem_u32(qk + row * pitch + 2 * D + col + 16 * (mat & 1)), bf);
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi) {

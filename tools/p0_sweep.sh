@@ -1,5 +1,13 @@
-mkdir -p gpurun_out/p0
-for rb in 16 32 64 128; do for nb in 1 2; do
-  DCHAG_P0_RB=$rb DCHAG_P0_NBUF=$nb timeout 300 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/p0/rb${rb}_nb${nb}.json 2> gpurun_out/p0/rb${rb}_nb${nb}.err
-done; done
-timeout 300 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/p0/default.json 2> gpurun_out/p0/default.err
+#!/bin/bash
+# K_p0 (dchag_l0_logits) launch-shape sweep on the H1 step (DCHAG_P0_* experiment overrides)
+run() {
+  env "$@" timeout 300 python bench.py --no-cpu-baseline --steps 10 --warmup 3 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read().strip().splitlines()[-1])
+ks={k['site']:k['ms'] for k in d['kernels']}
+print('$*', 'step', round(d['ms_per_step'],3), 'l0_logits', round(ks.get('l0_logits',0),3))"
+}
+run X=0
+for rb in 16 32 64 128; do for nb in 1 2; do for ps in 1 2 3 4; do
+  run DCHAG_P0_RB=$rb DCHAG_P0_NBUF=$nb DCHAG_P0_PERSM=$ps
+done; done; done
