@@ -236,46 +236,6 @@ __global__ void __launch_bounds__(256) l0_dv_kernel(int g, int R, int D, int H, 
   }
 }
 
-// Gpos alone (the training step's tcgen05 path): one thread per (row, 32 columns), its four
-// G chunks and eight posV chunks all requested before any is consumed (one 16-byte chunk per
-// thread left ~3 loads in flight per thread: 1.4 TB/s), heads of dh >= 32 columns reduced
-// over dh / 32 lanes.
-__global__ void __launch_bounds__(256) l0_gpos_kernel(int R, int D, int H,
-                                                      const __nv_bfloat16* __restrict__ G,
-                                                      const float* __restrict__ posV,
-                                                      long long ldpos, int S,
-                                                      float* __restrict__ Gpos) {
-  const int c32 = D >> 5;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)R * c32) return;  // R * D/32 is a multiple of 32: whole warps
-  const int r = (int)(idx / c32);
-  const int d0 = (int)(idx - (long long)r * c32) * 32;
-  const uint4* gp = reinterpret_cast<const uint4*>(G + (size_t)r * D + d0);
-  const float4* pv = reinterpret_cast<const float4*>(posV + (size_t)(r % S) * ldpos + d0);
-  uint4 gv[4];
-  float4 pf[8];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) gv[k] = __ldg(gp + k);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) pf[k] = __ldg(pv + k);
-  float acc = 0.f;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float4 a = pf[2 * k], b = pf[2 * k + 1];
-    acc = fmaf(bf16lo(gv[k].x), a.x, acc);
-    acc = fmaf(bf16hi(gv[k].x), a.y, acc);
-    acc = fmaf(bf16lo(gv[k].y), a.z, acc);
-    acc = fmaf(bf16hi(gv[k].y), a.w, acc);
-    acc = fmaf(bf16lo(gv[k].z), b.x, acc);
-    acc = fmaf(bf16hi(gv[k].z), b.y, acc);
-    acc = fmaf(bf16lo(gv[k].w), b.z, acc);
-    acc = fmaf(bf16hi(gv[k].w), b.w, acc);
-  }
-  const int dh = D / H, lanes = dh >> 5;  // 1..8, a power of two
-  for (int off = lanes >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if ((threadIdx.x & (lanes - 1)) == 0) Gpos[(size_t)r * H + d0 / dh] = acc;
-}
-
 cudaError_t launch_l0_dv(int g, int R, int D, int H, int NH, const __nv_bfloat16* p,
                          const float* mix, const __nv_bfloat16* G, const float* posV,
                          long long ldpos, int S, float* Gpos, __nv_bfloat16* out,
@@ -284,16 +244,9 @@ cudaError_t launch_l0_dv(int g, int R, int D, int H, int NH, const __nv_bfloat16
   if (D % H || dh % 8 || dh > 256 || ((dh / 8) & (dh / 8 - 1)) || ((long long)R * (D / 8)) % 32 ||
       (!mix && (NH < 1 || H % NH)) || (posV && (!Gpos || S < 1)))
     return cudaErrorInvalidValue;
-  const long long ld = ldpos > 0 ? ldpos : D;
-  if (!out && posV && dh % 32 == 0 && dh <= 256 && ((long long)R * (D / 32)) % 32 == 0 &&
-      ld % 4 == 0 && (reinterpret_cast<uintptr_t>(posV) | reinterpret_cast<uintptr_t>(G)) % 16 == 0) {
-    const long long n = (long long)R * (D / 32);
-    l0_gpos_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(R, D, H, G, posV, ld, S, Gpos);
-    return cudaGetLastError();
-  }
   const long long n = (long long)R * (D / 8);
   l0_dv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, R, D, H, NH, p, mix, G, posV,
-                                                             ld, S, Gpos, out);
+                                                             ldpos > 0 ? ldpos : D, S, Gpos, out);
   return cudaGetLastError();
 }
 

@@ -1137,7 +1137,7 @@ constexpr int TGC_SMEM_TE = TGC_SMEM + TGC_B_BYTES;
 //    the node's bf16 dl [g][H][R] read K-major (rows h >= H zero-filled by TMA), unscaled;
 //  * the epilogue writes bf16 rows of the node's TE block (see L0TgradArgs).
 template <bool TE>
-__global__ void __launch_bounds__(TE ? 320 : 192, 2)
+__global__ void __launch_bounds__(192, 2)
     l0_tgrad_tc_kernel(const __grid_constant__ CUtensorMap tmG,
                        const __grid_constant__ CUtensorMap tmP,
                        const __grid_constant__ CUtensorMap tmDL, L0TgradArgs a) {
@@ -1150,7 +1150,6 @@ __global__ void __launch_bounds__(TE ? 320 : 192, 2)
   uint64_t* empty = scaled + TGC_STAGES;
   uint64_t* done = empty + TGC_STAGES;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
-  constexpr int TGC_BUILDERS = TE ? 8 : 4;  // builder warps (2 + builders = the CTA)
   const int warp = warp_id(), lane = lane_id();
   const int c = blockIdx.y, d0 = blockIdx.x * 128;
   const bool eblk = TE && d0 >= a.D;               // the E_c block (dl as A, K-major)
@@ -1163,7 +1162,7 @@ __global__ void __launch_bounds__(TE ? 320 : 192, 2)
     if (TE) tma_prefetch(&tmDL);
     for (int s = 0; s < TGC_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&scaled[s], TGC_BUILDERS);
+      mbar_init(&scaled[s], 4);
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
@@ -1223,13 +1222,9 @@ __global__ void __launch_bounds__(TE ? 320 : 192, 2)
       __syncwarp();
     }
   } else {
-    // builders: thread t scales row r = t % 64 of half mh by p[r][head(mh)]; with 8 builder
-    // warps (TE) each thread takes half of the row's 8 chunks (chunk group cg)
+    // builders: thread t scales row r = t % 64 of half mh = t / 64 by p[r][head(mh)]
     const int t = threadIdx.x - 64;
-    const int row = t & 63;
-    const int mh = TGC_BUILDERS == 8 ? (t >> 7) : (t >> 6);
-    const int cg = TGC_BUILDERS == 8 ? ((t >> 6) & 1) : 0;
-    constexpr int NCH = TGC_BUILDERS == 8 ? 4 : 8;  // 16-byte chunks per thread
+    const int row = t & 63, mh = t >> 6;
     const int head = (d0 + mh * 64) / dh;
     const int hA = d0 / dh;
     const int hg = hA / (a.NH > 0 ? a.NH : 1);
@@ -1262,17 +1257,17 @@ __global__ void __launch_bounds__(TE ? 320 : 192, 2)
                                  (row >> 3) * 1024 + (row & 7) * 128;
         // rows sit 128 B apart: visit the row's 16-byte chunks in a row-rotated order so the
         // 8 rows of a swizzle atom hit 8 different bank groups (all chunks share one p)
-        uint32_t v[NCH][4];
+        uint32_t v[8][4];
 #pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-          const uint32_t ad = rowaddr + (((ch + cg * NCH + row) & 7) << 4);
+        for (int ch = 0; ch < 8; ++ch) {
+          const uint32_t ad = rowaddr + (((ch + row) & 7) << 4);
           asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
                        : "=r"(v[ch][0]), "=r"(v[ch][1]), "=r"(v[ch][2]), "=r"(v[ch][3])
                        : "r"(ad));
         }
 #pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-          const uint32_t ad = rowaddr + (((ch + cg * NCH + row) & 7) << 4);
+        for (int ch = 0; ch < 8; ++ch) {
+          const uint32_t ad = rowaddr + (((ch + row) & 7) << 4);
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             v[ch][e] = pack_bf16(bf16lo(v[ch][e]) * pc, bf16hi(v[ch][e]) * pc);
@@ -1294,10 +1289,8 @@ __global__ void __launch_bounds__(TE ? 320 : 192, 2)
       const long long col = eblk ? (long long)a.D + m : (long long)d0 + m;
       __nv_bfloat16* te = a.TE + col;
       const bool live = !eblk || m < a.H;
-      const int wset = (warp - 2) >> 2;                     // which 32-column half to drain
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
-        if (half != wset) continue;
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + half * 32, r);
         tmem_ld_wait();
@@ -1307,12 +1300,10 @@ __global__ void __launch_bounds__(TE ? 320 : 192, 2)
             te[(size_t)(c * a.PP + half * 32 + j) * a.te_ld] = __float2bfloat16(__uint_as_float(r[j]));
         }
       }
-      if (wset == 0) {
-        uint32_t r16[16];
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + 64, r16);
-        tmem_ld_wait();
-        if (live) te[(size_t)(a.ones0 + c) * a.te_ld] = __float2bfloat16(__uint_as_float(r16[0]));
-      }
+      uint32_t r16[16];
+      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + 64, r16);
+      tmem_ld_wait();
+      if (live) te[(size_t)(a.ones0 + c) * a.te_ld] = __float2bfloat16(__uint_as_float(r16[0]));
     } else {
       const int d = d0 + q * 32 + lane;
       float* out = a.T + (size_t)c * 64 * a.D + d;
@@ -1348,7 +1339,7 @@ cudaError_t launch_l0_tgrad_te(const CUtensorMap& tG, const CUtensorMap& tP,
   cudaError_t e = cudaFuncSetAttribute(l0_tgrad_tc_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, TGC_SMEM_TE);
   if (e != cudaSuccess) return e;
-  l0_tgrad_tc_kernel<true><<<dim3(a.D / 128 + (a.has_dl ? 1 : 0), a.g), 320, TGC_SMEM_TE, st>>>(
+  l0_tgrad_tc_kernel<true><<<dim3(a.D / 128 + (a.has_dl ? 1 : 0), a.g), 192, TGC_SMEM_TE, st>>>(
       tG, tP, tDL, a);
   return cudaGetLastError();
 }
