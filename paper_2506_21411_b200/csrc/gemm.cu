@@ -1231,27 +1231,34 @@ __global__ void __launch_bounds__(192, 2)
     const int hn = (hA - hg * a.NH) & ~1;
     const int sel = head & 1;
     const float mixc = a.mix ? __ldg(a.mix + c) : 0.f;
-    auto pval = [&](int i) -> float {
-      if (a.mix) return mixc;
-      const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(
+    // the raw p word (two heads' bf16) of stage i; converted only where it is consumed, so
+    // the loads of the queue below really stay in flight (a conversion right after the load
+    // made every load stall for its full latency)
+    auto pword = [&](int i) -> uint32_t {
+      if (a.mix) return 0u;
+      return __ldg(reinterpret_cast<const uint32_t*>(
           a.p + ((size_t)(hg * a.g + c) * a.R + i * 64 + row) * a.NH + hn));
+    };
+    auto pconv = [&](uint32_t w) -> float {
+      if (a.mix) return mixc;
       return sel ? bf16hi(w) : bf16lo(w);
     };
-    // p of the next four stages in flight (a rotating register queue): one stage ahead left
-    // the L2 latency of the p loads exposed (long-scoreboard stalls dominated)
-    float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
-    if (!eblk) {
-      p0 = pval(0);
-      if (nst > 1) p1 = pval(1);
-      if (nst > 2) p2 = pval(2);
-      if (nst > 3) p3 = pval(3);
-    }
-    for (int i = 0; i < nst; ++i) {
-      const int s = i % TGC_STAGES;
-      const float pc = p0;
-      p0 = p1; p1 = p2; p2 = p3;
-      if (!eblk && i + 4 < nst) p3 = pval(i + 4);
+    // p of the next four stages in flight: one register per ring slot, the stage loop
+    // unrolled by the ring depth so no register copy (which would wait for the load) moves
+    // the queue along
+    static_assert(TGC_STAGES == 4, "the p queue is unrolled by the ring depth");
+    uint32_t pq[TGC_STAGES];
+#pragma unroll
+    for (int j = 0; j < TGC_STAGES; ++j) pq[j] = (!eblk && j < nst) ? pword(j) : 0u;
+    for (int i0 = 0; i0 < nst; i0 += TGC_STAGES)
+#pragma unroll
+    for (int s = 0; s < TGC_STAGES; ++s) {
+      const int i = i0 + s;
+      if (i >= nst) break;
+      const uint32_t pw = pq[s];
+      if (!eblk && i + TGC_STAGES < nst) pq[s] = pword(i + TGC_STAGES);
       mbar_wait(&full[s], (i / TGC_STAGES) & 1);
+      const float pc = pconv(pw);
       if (!eblk) {
         const uint32_t rowaddr = smem_u32(smem + s * TGC_STAGE) + mh * (TGC_A_BYTES / 2) +
                                  (row >> 3) * 1024 + (row & 7) * 128;
