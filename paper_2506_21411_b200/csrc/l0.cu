@@ -374,11 +374,19 @@ cudaError_t launch_l0_logits(const L0LogitArgs& a, int num_sms, cudaStream_t st)
     if (rb <= 32 && smem_for(rb, 1) <= 113 * 1024) break;
   }
   if (RB == 0) return cudaErrorInvalidValue;
+  // many heads (large weight block): when two CTAs per SM only fit 16-row single-buffered
+  // items, one CTA per SM with 32-row double-buffered items is faster (TR, H = 32: 0.68 ->
+  // 0.36 ms per launch, tools/p0_sweep_train.sh)
+  bool one_cta = false;
+  if (RB < 32 && a.wp <= 32 && 32 % a.wp == 0 && R % 32 == 0 && smem_for(32, 2) <= 227 * 1024) {
+    RB = 32;
+    one_cta = true;
+  }
   if (const char* f = getenv("DCHAG_P0_RB")) {  // experiment override
     const int rb = atoi(f);
     if (rb >= 16 && rb % a.wp == 0 && R % rb == 0) RB = rb;
   }
-  if (smem_for(RB, 2) <= 113 * 1024) nbuf = 2;
+  if (smem_for(RB, 2) <= (one_cta ? 227 : 113) * 1024) nbuf = 2;
   if (const char* f = getenv("DCHAG_P0_NBUF")) nbuf = atoi(f) == 2 ? 2 : 1;
   const long long smem = smem_for(RB, nbuf);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
