@@ -204,10 +204,12 @@ __global__ void __launch_bounds__(256) l0_dv_kernel(int g, int R, int D, int H, 
                                                    float* __restrict__ Gpos,
                                                    __nv_bfloat16* __restrict__ out) {
   const int dchunks = D >> 3;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)R * dchunks) return;  // R * D/8 is a multiple of 32: whole warps
-  const int r = (int)(idx / dchunks);
-  const int d0 = (int)(idx - (long long)r * dchunks) * 8;
+  // 32-bit index math (R * D / 8 < 2^31, checked at launch): a 64-bit division per thread
+  // was a visible share of this memory-bound kernel
+  const unsigned idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (unsigned)R * (unsigned)dchunks) return;  // a multiple of 32: whole warps
+  const int r = (int)(idx / (unsigned)dchunks);
+  const int d0 = (int)(idx - (unsigned)r * dchunks) * 8;
   const uint4 gv = __ldg(reinterpret_cast<const uint4*>(G + (size_t)r * D + d0));
   const int dh = D / H;
   const int h = d0 / dh;
@@ -245,6 +247,7 @@ cudaError_t launch_l0_dv(int g, int R, int D, int H, int NH, const __nv_bfloat16
       (!mix && (NH < 1 || H % NH)) || (posV && (!Gpos || S < 1)))
     return cudaErrorInvalidValue;
   const long long n = (long long)R * (D / 8);
+  if (n >= (1ll << 31)) return cudaErrorInvalidValue;
   l0_dv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, R, D, H, NH, p, mix, G, posV,
                                                              ldpos > 0 ? ldpos : D, S, Gpos, out);
   return cudaGetLastError();
@@ -622,9 +625,9 @@ __global__ void __launch_bounds__(256) l0_softmax_bwd_reg_kernel(
     int g, int R, int H, int NH, const float* __restrict__ dpp,
     const float* __restrict__ Gpos, const __nv_bfloat16* __restrict__ p,
     float* __restrict__ dl, __nv_bfloat16* __restrict__ dlb) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)R * H) return;
-  const int h = (int)(idx / R), r = (int)(idx - (long long)h * R);
+  const unsigned idx = blockIdx.x * blockDim.x + threadIdx.x;  // R * H < 2^31 (launch)
+  if (idx >= (unsigned)R * (unsigned)H) return;
+  const int h = (int)(idx / (unsigned)R), r = (int)(idx - (unsigned)h * R);
   const int hg = h / NH, hn = h - hg * NH, D32 = H * NP;
   const float gp = __ldg(Gpos + (size_t)r * H + h);
   float dp[GM], pv[GM];
@@ -656,7 +659,7 @@ cudaError_t launch_l0_softmax_bwd(int g, int R, int H, int NH, int dh, const flo
                                   const float* Gpos, const __nv_bfloat16* p, float* dl,
                                   __nv_bfloat16* dlb, cudaStream_t st) {
   if (dh % 32 || NH < 1 || H % NH) return cudaErrorInvalidValue;
-  if (g <= 16 && dh == 64) {
+  if (g <= 16 && dh == 64 && (long long)R * H < (1ll << 31)) {
     const long long n = (long long)R * H;
     l0_softmax_bwd_reg_kernel<16, 2><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
         g, R, H, NH, dpp, Gpos, p, dl, dlb);

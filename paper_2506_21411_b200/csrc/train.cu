@@ -23,16 +23,21 @@ __global__ void __launch_bounds__(256) cast_multi_kernel(const CastJob* jobs, in
   const bool vec = !j.trans && !j.dst_f32 && j.cols % 4 == 0 && j.lds % 4 == 0 &&
                    j.ldd % 4 == 0 && ((reinterpret_cast<uintptr_t>(j.src) |
                                        reinterpret_cast<uintptr_t>(j.dst)) & 15) == 0;
-  if (vec) {  // 16-byte loads, 8-byte stores, grid-stride over the job
-    const long long c4 = j.cols / 4, n = j.rows * c4;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-      const long long r = i / c4, c = (i - r * c4) * 4;
-      const float4 v = __ldg(reinterpret_cast<const float4*>(j.src + r * j.lds + c));
-      uint2 o;
-      o.x = pack_bf16(v.x, v.y);
-      o.y = pack_bf16(v.z, v.w);
-      *reinterpret_cast<uint2*>(j.dst + r * j.ldd + c) = o;
+  if (vec) {  // 16-byte loads, 8-byte stores; one warp per row (no per-element division)
+    const int c4 = (int)(j.cols / 4);
+    const int lane = threadIdx.x & 31;
+    const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long r = w0; r < j.rows; r += nw) {
+      const float4* src = reinterpret_cast<const float4*>(j.src + r * j.lds);
+      uint2* dst = reinterpret_cast<uint2*>(j.dst + r * j.ldd);
+      for (int c = lane; c < c4; c += 32) {
+        const float4 v = __ldg(src + c);
+        uint2 o;
+        o.x = pack_bf16(v.x, v.y);
+        o.y = pack_bf16(v.z, v.w);
+        dst[c] = o;
+      }
     }
     return;
   }
@@ -315,23 +320,25 @@ DEV long long tiled_off(int blk, int k, int n, int K, int N) {  // canonical K-m
 // runs) and the row-dot operand Mrow [C][D][PP], plus Cb [C][D]. Mt's padding channels
 // [C, C_pad) are zero from allocation and never written.
 __global__ void pack_rows_kernel(L0PackArgs a) {
+  // one warp per fold row (channel c, column d): lanes sweep its PP contiguous values (no
+  // per-element 64-bit index division), lane 0 also moves the Cb term
   const int hw = a.D / a.H / 2, K = a.C_pad * a.PP;
-  const long long total = (long long)a.C * a.D * (a.PP + 1);
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(t / ((long long)a.D * (a.PP + 1)));
-    const int rem = (int)(t - (long long)c * a.D * (a.PP + 1));
-    const int d = rem / (a.PP + 1), kk = rem - d * (a.PP + 1);
+  const int lane = threadIdx.x & 31;
+  const long long rows = (long long)a.C * a.D;
+  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long w = w0; w < rows; w += nw) {
+    const int c = (int)(w / a.D), d = (int)(w - (long long)c * a.D);
     const int n = __ldg(a.chan_node + c), l = __ldg(a.chan_local + c);
     const float* row = a.MT + ((size_t)n * a.Dp + d) * a.Kn;
-    if (kk < a.PP) {
+    const int blk = d / hw, nn = d - blk * hw;
+    __nv_bfloat16* mrow = a.Mrow + ((size_t)c * a.D + d) * a.PP;
+    for (int kk = lane; kk < a.PP; kk += 32) {
       const __nv_bfloat16 v = __float2bfloat16(row[l * a.PP + kk]);
-      a.Mrow[((size_t)c * a.D + d) * a.PP + kk] = v;
-      const int blk = d / hw, nn = d - blk * hw;
+      mrow[kk] = v;
       a.Mt[tiled_off(blk, c * a.PP + kk, nn, K, hw)] = v;
-    } else {
-      a.Cb[(size_t)c * a.D + d] = row[a.ones0 + l];
     }
+    if (lane == 0) a.Cb[(size_t)c * a.D + d] = row[a.ones0 + l];
   }
 }
 
@@ -372,20 +379,23 @@ __global__ void pack_logit_kernel(L0PackArgs a) {  // WUt [C][HP][PP] bf16, bU [
 // posVU fp32 [n0][S][Dp] (pos [Wv | U]) -> posV0 bf16 [n0][S][D] (x mixsum for linear
 // nodes), posU fp32 [n0][S][HP]
 __global__ void pack_pos_kernel(L0PackArgs a) {
+  // one warp per positional row (node n, position s), lanes sweep its columns
   const int W = a.D + a.HP;
-  const long long total = (long long)a.n0 * a.S * W;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long row = t / W;
-    const int col = (int)(t - row * W);
+  const int lane = threadIdx.x & 31;
+  const long long rows = (long long)a.n0 * a.S;
+  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long row = w0; row < rows; row += nw) {
     const float* src = a.posVU + row * a.Dp;
-    if (col < a.D) {
-      const int n = (int)(row / a.S);
-      const float sc = a.mixsum ? __ldg(a.mixsum + n) : 1.f;
-      a.posV0[row * a.D + col] = __float2bfloat16(src[col] * sc);
-    } else if (a.posU) {
-      const int h = col - a.D;
-      a.posU[row * a.HP + h] = h < a.H ? src[a.D + h] : 0.f;
+    const int n = (int)(row / a.S);
+    const float sc = a.mixsum ? __ldg(a.mixsum + n) : 1.f;
+    for (int col = lane; col < W; col += 32) {
+      if (col < a.D) {
+        a.posV0[row * a.D + col] = __float2bfloat16(src[col] * sc);
+      } else if (a.posU) {
+        const int h = col - a.D;
+        a.posU[row * a.HP + h] = h < a.H ? src[a.D + h] : 0.f;
+      }
     }
   }
 }
