@@ -1189,8 +1189,22 @@ __global__ void __launch_bounds__(128) combine_bwd_kernel(CombineBwdArgs a) {
       gr[q][4] = g1.x; gr[q][5] = g1.y; gr[q][6] = g1.z; gr[q][7] = g1.w;
     }
   }
-  for (int j = 0; j < g; ++j) {
+  // child j + 1's value row is requested while child j is reduced (software pipeline)
+  auto load_v = [&](int j, uint4 (&v)[8]) {
     const __nv_bfloat16* vrow = a.V + (long long)(first + j) * a.sVj + (long long)r * a.D;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int ch = lane + 32 * q;
+      v[q] = (q < per_lane && ch < nchunk) ? __ldg(reinterpret_cast<const uint4*>(vrow) + ch)
+                                           : make_uint4(0, 0, 0, 0);
+    }
+  };
+  uint4 vcur[8], vnext[8];
+  if (g > 0) load_v(0, vnext);
+  for (int j = 0; j < g; ++j) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) vcur[q] = vnext[q];
+    if (j + 1 < g) load_v(j + 1, vnext);
     __nv_bfloat16* gvrow = a.sGj ? a.gV + (long long)(first + j) * a.sGj + (long long)r * a.ldg
                                  : a.gV + (long long)(first + j) * a.sVj + (long long)r * a.D;
     float dm_part = 0.f;
@@ -1200,7 +1214,7 @@ __global__ void __launch_bounds__(128) combine_bwd_kernel(CombineBwdArgs a) {
       const int ch = lane + 32 * q;
       const bool ok = q < per_lane && ch < nchunk;
       if (ok) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(vrow) + ch);
+        const uint4 v = vcur[q];
         const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e)

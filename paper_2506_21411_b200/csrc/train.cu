@@ -257,10 +257,100 @@ __global__ void colsum_final_kernel(const float* part, int nch, int N, ColsumOut
   o.put(g, 0, n, a);
 }
 
+// vectorised forms: a thread sums VW adjacent columns (one 16-byte load per row), rows
+// unrolled by 8 so eight loads are in flight per thread
+template <typename T>
+struct ColVec;
+template <>
+struct ColVec<float> {
+  static constexpr int VW = 4;
+  static DEV void load(const float* p, float (&v)[4]) {
+    const float4 f = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  }
+};
+template <>
+struct ColVec<__nv_bfloat16> {
+  static constexpr int VW = 8;
+  static DEV void load(const __nv_bfloat16* p, float (&v)[8]) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { v[2 * e] = bf16lo(w[e]); v[2 * e + 1] = bf16hi(w[e]); }
+  }
+};
+
+// rows r0, r0 + step, ... < r1 of VW columns starting at x (8 rows per round in flight)
+template <typename T>
+DEV void colsum_rows(const T* x, long long ldx, int r0, int r1, int step,
+                     float (&a)[ColVec<T>::VW]) {
+  constexpr int VW = ColVec<T>::VW;
+#pragma unroll
+  for (int e = 0; e < VW; ++e) a[e] = 0.f;
+  int r = r0;
+  for (; r + 7 * step < r1; r += 8 * step) {
+    float v[8][VW];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) ColVec<T>::load(x + (size_t)(r + u * step) * ldx, v[u]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int e = 0; e < VW; ++e) a[e] += v[u][e];
+  }
+  for (; r < r1; r += step) {
+    float v[VW];
+    ColVec<T>::load(x + (size_t)r * ldx, v);
+#pragma unroll
+    for (int e = 0; e < VW; ++e) a[e] += v[e];
+  }
+}
+
+template <typename T>
+__global__ void colsum_direct_vec_kernel(const T* X, long long ldx, long long sxg, int R, int N,
+                                         int P, ColsumOut o) {
+  constexpr int VW = ColVec<T>::VW;
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) * VW;
+  const int p = blockIdx.y, g = blockIdx.z;
+  if (n >= N) return;
+  float a[VW];
+  colsum_rows<T>(X + (size_t)g * sxg + n, ldx, p, R, P, a);
+#pragma unroll
+  for (int e = 0; e < VW; ++e) o.put(g, p, n + e, a[e]);
+}
+
+template <typename T>
+__global__ void colsum_partial_vec_kernel(const T* X, long long ldx, long long sxg, int R, int N,
+                                          float* part) {
+  constexpr int VW = ColVec<T>::VW;
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) * VW;
+  const int ch = blockIdx.y, g = blockIdx.z;
+  if (n >= N) return;
+  float a[VW];
+  colsum_rows<T>(X + (size_t)g * sxg + n, ldx, ch * CS_ROWS, min(R, (ch + 1) * CS_ROWS), 1, a);
+#pragma unroll
+  for (int e = 0; e < VW; ++e) part[((size_t)g * gridDim.y + ch) * N + n + e] = a[e];
+}
+
 template <typename T>
 static cudaError_t colsum_t(const T* X, long long ldx, long long sxg, int G, int R, int N, int P,
                             const ColsumOut& o, float* part, cudaStream_t st) {
   const dim3 blk(128);
+  constexpr int VW = ColVec<T>::VW;
+  const bool vec = N % VW == 0 && ldx % VW == 0 && sxg % VW == 0 &&
+                   reinterpret_cast<uintptr_t>(X) % 16 == 0;
+  if (vec) {
+    const int nthr = N / VW;
+    if (P > 1 || R <= CS_ROWS) {
+      colsum_direct_vec_kernel<T><<<dim3((nthr + 127) / 128, P, G), blk, 0, st>>>(
+          X, ldx, sxg, R, N, P, o);
+      return cudaGetLastError();
+    }
+    const int nch = (R + CS_ROWS - 1) / CS_ROWS;
+    colsum_partial_vec_kernel<T><<<dim3((nthr + 127) / 128, nch, G), blk, 0, st>>>(
+        X, ldx, sxg, R, N, part);
+    colsum_final_kernel<<<dim3((N + 127) / 128, 1, G), blk, 0, st>>>(part, nch, N, o);
+    return cudaGetLastError();
+  }
   if (P > 1 || R <= CS_ROWS) {
     colsum_direct_kernel<T><<<dim3((N + 127) / 128, P, G), blk, 0, st>>>(X, ldx, sxg, R, N, P,
                                                                          o);
