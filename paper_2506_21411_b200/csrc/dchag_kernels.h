@@ -8,6 +8,28 @@
 
 namespace dchag {
 
+// n / d for 0 <= n < 2^31 by a multiply-high with a host-computed magic number
+// (Granlund-Montgomery: m = ceil(2^(31+l) / d), l = ceil(log2 d)): two instructions instead
+// of a ~30-instruction integer division in the per-tile index math of the GEMM kernels
+struct FastDiv {
+  unsigned int m, s, d;
+#ifdef __CUDACC__
+  __host__ __device__ __forceinline__ int div(int n) const {
+    return (int)(((unsigned long long)(unsigned int)n * m) >> s);
+  }
+#endif
+};
+inline FastDiv make_fastdiv(unsigned int d) {
+  unsigned int l = 0;
+  while ((1ull << l) < d) ++l;
+  const unsigned long long num = 1ull << (31 + l);
+  FastDiv f;
+  f.m = (unsigned int)((num + d - 1) / d);
+  f.s = 31 + l;
+  f.d = d;
+  return f;
+}
+
 struct GemmArgs {
   int G, M, Mi, N, Nv, K, BN;   // M = Mo * Mi rows per group
   int debug;                    // timing probes (DCHAG_GEMM_DEBUG)
@@ -39,6 +61,7 @@ struct GemmArgs {
   int nparents;                 // COMB: G = nparents * csplit; group g = split s * nparents + j
   int csplit;                   // 1, or 2: split s sums children [s c/2, (s+1) c/2) (partials)
   int lay;                      // operand layouts: bit 0 A MN-major, bit 1 W MN-major
+  FastDiv fd_G, fd_cpg, fd_ctn, fd_Mi;  // set by launch_gemm: G, tiles per group, N tiles, Mi
   int lean;                     // 1: lean bf16 epilogue (tV box 64 columns x 32 rows, 128B
                                 //    swizzle; see gemm_kernel)
   int Ki;                       // MN-major A: K = Ko * Ki rows, (k / Ki) * sAko + (k % Ki) * lda

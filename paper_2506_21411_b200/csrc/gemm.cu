@@ -153,14 +153,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   auto decode = [&](int ct, int& g, int& mt, int& nt) {
     int mc;
     if (dot_mode) {
-      g = ct % args.G;
-      const int rest = ct / args.G;
-      mc = rest / ctiles_n;
+      const int rest = args.fd_G.div(ct);
+      g = ct - rest * args.G;
+      mc = args.fd_ctn.div(rest);
       nt = rest - mc * ctiles_n;
     } else {
-      g = ct / ctiles_per_g;
+      g = args.fd_cpg.div(ct);
       const int rem = ct - g * ctiles_per_g;
-      mc = rem / ctiles_n;
+      mc = args.fd_ctn.div(rem);
       nt = rem - mc * ctiles_n;
     }
     mt = mc * CL + crank;
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         int g0, mt, nt;
         decode(ct, g0, mt, nt);
         const int m0 = mt * GEMM_BM;
-        const int mo = m0 / args.Mi, mi = m0 - mo * args.Mi;
+        const int mo = args.fd_Mi.div(m0), mi = m0 - mo * args.Mi;
         int c_first = g0, c_n = 1;
         if (comb) comb_range(g0, c_first, c_n);
         for (int ci = 0; ci < c_n; ++ci)
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int c0 = nt * args.BN + hf * 128;
       const int m_row = mt * GEMM_BM + quarter * 32 + lane;
       const int r0 = mt * GEMM_BM + quarter * 32;
-      const int mo0 = r0 / args.Mi, mi0 = r0 - mo0 * args.Mi;
+      const int mo0 = args.fd_Mi.div(r0), mi0 = r0 - mo0 * args.Mi;
       const int hd0 = min(c0 / args.dh, args.H - 1), hd1 = min((c0 + 64) / args.dh, args.H - 1);
       __half2 run[2][32];
       __half2 mx = __float2half2_rn(0.f);
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                    : "memory");
       __syncwarp();
       const int r0 = mt * GEMM_BM + quarter * 32;
-      const int mo0 = r0 / args.Mi, mi0 = r0 - mo0 * args.Mi;
+      const int mo0 = args.fd_Mi.div(r0), mi0 = r0 - mo0 * args.Mi;
       if (warp == 2 && lane == 0) GEMM_TRACE(18, (t - ct_begin) / ct_step);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // columns straight from registers, 16-byte stores (rows are contiguous: coalesced)
         const int nq = cols > 0 ? (min(cols, 128) + 31) / 32 : 0;
         const int m_row = mt * GEMM_BM + quarter * 32 + lane;
-        const int mo = m_row / args.Mi, mi = m_row - mo * args.Mi;
+        const int mo = args.fd_Mi.div(m_row), mi = m_row - mo * args.Mi;
         float* dst = args.outL + (size_t)g * args.sLg + (size_t)mo * args.sLmo +
                      (size_t)mi * args.sLmi + c0;
         if (nq == 0) release();
@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (warp == 2 && lane == 0) GEMM_TRACE(17, (t - ct_begin) / ct_step);
       decode(t, g, mt, nt);
       const int m_row = mt * GEMM_BM + row_in_tile;
-      const int mo = m_row / args.Mi, mi = m_row - mo * args.Mi;
+      const int mo = args.fd_Mi.div(m_row), mi = m_row - mo * args.Mi;
       // prefetch this thread's row bias for its column groups (in flight during the wait)
       // row-dot mode: the same registers carry this row's dotG columns instead
       constexpr bool dot = DOT;
@@ -945,7 +945,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             __syncwarp();
             if (lane == 0) {
               const int r0 = mt * GEMM_BM + quarter * 32;
-              const int mo0 = r0 / args.Mi, mi0 = r0 - mo0 * args.Mi;
+              const int mo0 = args.fd_Mi.div(r0), mi0 = r0 - mo0 * args.Mi;
               tma_store_4d(&tmV, smem_u32(buf), n0, mi0, mo0, g);
               bulk_commit();
             }
@@ -970,7 +970,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               if (i < nk) {
                 const int rr = i * rows_per + lane / nk, k = lane % nk;
                 const int mrow = mt0 + rr;
-                const int mo2 = mrow / args.Mi, mi2 = mrow - mo2 * args.Mi;
+                const int mo2 = args.fd_Mi.div(mrow), mi2 = mrow - mo2 * args.Mi;
                 const uint4 o =
                     *reinterpret_cast<const uint4*>(my_out + rr * 64 + ((k ^ (rr & 3)) << 4));
                 *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.outV) +
@@ -994,7 +994,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               if (i < nk4) {
                 const int rr = i * rows_per + lane / nk4, k = lane % nk4;
                 const int mrow = mt0 + rr;
-                const int mo2 = mrow / args.Mi, mi2 = mrow - mo2 * args.Mi;
+                const int mo2 = args.fd_Mi.div(mrow), mi2 = mrow - mo2 * args.Mi;
                 float4 o =
                     *reinterpret_cast<const float4*>(my_out + rr * 128 + ((k ^ (rr & 7)) << 4));
                 float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.outV) +
@@ -1063,6 +1063,16 @@ static cudaError_t launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tW,
   using SM = GemmSmem<BK, STAGES, PAIR, (LEAN == 1 || LEAN == 4) ? GEMM_LEAN_OUT : GEMM_STAGE_OUT>;
   static_assert(SM::TOTAL <= 227 * 1024, "shared memory");
   auto kern = gemm_kernel<BK, STAGES, PAIR, COMB, LAY, LEAN>;
+  GemmArgs af = a;
+  {
+    constexpr int CLh = PAIR ? 2 : 1;
+    const int ctn = (a.N + a.BN - 1) / a.BN;
+    const int cpg = (a.M / GEMM_BM / CLh) * ctn;
+    af.fd_G = make_fastdiv((unsigned)a.G);
+    af.fd_cpg = make_fastdiv((unsigned)(cpg > 0 ? cpg : 1));
+    af.fd_ctn = make_fastdiv((unsigned)(ctn > 0 ? ctn : 1));
+    af.fd_Mi = make_fastdiv((unsigned)a.Mi);
+  }
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
   if (e != cudaSuccess) return e;
@@ -1082,7 +1092,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tW,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, tA, tW, tV, a);
+  e = cudaLaunchKernelEx(&cfg, kern, tA, tW, tV, af);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
