@@ -8,6 +8,7 @@ model.py:51-64 tokenizer, layers.py:103-123 nodes over the channel axis, model.p
 so the crop changes nothing but the oracle's cost.
 
   H1  C500 128x128 P8 D1024 H16, max_group 16: groups of 16, 32 level-0 nodes, depth 3
+      (also with D-CHAG-L linear nodes and with full_cross nodes)
   W   C128 128x256 P4 D1024 H16, max_group 64: KE = 64, S = 2048
   H8  C500 over 8 slabs (63 x4, 62 x4), max_group 4, all ranks in one process
   TR  fwd+bwd at D2048 H32 on a 24-channel slab with the TR tree (groups of 4, depth 3)
@@ -41,7 +42,8 @@ def _frontends(cfg, tp, out_dtype=torch.float32):
     return [DchagFrontEnd(cfg["channels"], cfg["image_h"], cfg["image_w"], cfg["patch"],
                           cfg["embed"], cfg["heads"], max_group=cfg["max_group"], tp=tp, rank=r,
                           out_dtype=out_dtype,
-                          agg_layer_kind=cfg.get("layer_kind", "cross_attention"))
+                          agg_layer_kind=cfg.get("layer_kind", "cross_attention"),
+                          agg_variant=cfg.get("variant", "single_query"))
             for r in range(tp)]
 
 
@@ -67,7 +69,8 @@ def _oracle_rows(cfg, master, img, tp, rows):
     x = img[:, :, :rows * P].float().cpu().numpy().astype(np.float64)
     return O.dchag_frontend(x, w, patch=P, heads=cfg["heads"], tp=tp,
                             max_group=cfg["max_group"],
-                            layer_kind=cfg.get("layer_kind", "cross_attention"))
+                            layer_kind=cfg.get("layer_kind", "cross_attention"),
+                            variant=cfg.get("variant", "single_query"))
 
 
 SHAPES = {
@@ -75,6 +78,8 @@ SHAPES = {
                 max_group=16), 1, 2, 2),
     "H1_linear": (dict(channels=500, image_h=128, image_w=128, patch=8, embed=1024, heads=16,
                        max_group=16, layer_kind="linear"), 1, 2, 2),
+    "H1_fullcross": (dict(channels=500, image_h=128, image_w=128, patch=8, embed=1024,
+                          heads=16, max_group=16, variant="full_cross"), 1, 2, 2),
     "W": (dict(channels=128, image_h=128, image_w=256, patch=4, embed=1024, heads=16,
                max_group=64), 1, 2, 1),
     "H2": (dict(channels=500, image_h=128, image_w=128, patch=8, embed=1024, heads=16,
