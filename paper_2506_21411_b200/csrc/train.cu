@@ -83,14 +83,36 @@ cudaError_t launch_cast_multi(const CastJob* jobs, int n_jobs, int max_tiles, cu
 // phase 1: partial q wq over 128-row chunks of wq: part[node][chunk][j]
 constexpr int QF_CHUNK = 128;
 
+// a thread takes 4 adjacent columns (16-byte loads), rows 8 at a time in flight; the sum
+// order over i is unchanged (sequential per column)
 __global__ void qf_partial_kernel(const QueryFoldJob* jobs, int D, float* part) {
   const QueryFoldJob jb = jobs[blockIdx.z];
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i0 = blockIdx.y * QF_CHUNK;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int i0 = blockIdx.y * QF_CHUNK, i1 = min(D, i0 + QF_CHUNK);
   if (j >= D) return;
-  float acc = 0.f;
-  for (int i = i0; i < min(D, i0 + QF_CHUNK); ++i) acc = fmaf(__ldg(jb.q + i), __ldg(jb.wq + (size_t)i * D + j), acc);
-  part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * D + j] = acc;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int i = i0;
+  for (; i + 8 <= i1; i += 8) {
+    float4 w[8];
+    float qv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      w[u] = __ldg(reinterpret_cast<const float4*>(jb.wq + (size_t)(i + u) * D + j));
+      qv[u] = __ldg(jb.q + i + u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc.x = fmaf(qv[u], w[u].x, acc.x); acc.y = fmaf(qv[u], w[u].y, acc.y);
+      acc.z = fmaf(qv[u], w[u].z, acc.z); acc.w = fmaf(qv[u], w[u].w, acc.w);
+    }
+  }
+  for (; i < i1; ++i) {
+    const float4 w = __ldg(reinterpret_cast<const float4*>(jb.wq + (size_t)i * D + j));
+    const float qv = __ldg(jb.q + i);
+    acc.x = fmaf(qv, w.x, acc.x); acc.y = fmaf(qv, w.y, acc.y);
+    acc.z = fmaf(qv, w.z, acc.z); acc.w = fmaf(qv, w.w, acc.w);
+  }
+  *reinterpret_cast<float4*>(part + ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * D + j) = acc;
 }
 
 // phase 2: qp = sum of the partials (fixed order); U[d][h] = s sum_{j in h} wk[d][j] qp[j]
@@ -123,7 +145,8 @@ __global__ void qf_final_kernel(const QueryFoldJob* jobs, int D, int H, int nchu
 cudaError_t launch_query_fold(const QueryFoldJob* jobs, int n_jobs, int D, int H, float* part,
                               cudaStream_t st) {
   const int nchunk = (D + QF_CHUNK - 1) / QF_CHUNK;
-  qf_partial_kernel<<<dim3((D + 127) / 128, nchunk, n_jobs), 128, 0, st>>>(jobs, D, part);
+  if (D % 4) return cudaErrorInvalidValue;
+  qf_partial_kernel<<<dim3((D / 4 + 127) / 128, nchunk, n_jobs), 128, 0, st>>>(jobs, D, part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int smem = D * 4;
@@ -142,14 +165,33 @@ cudaError_t launch_query_fold(const QueryFoldJob* jobs, int n_jobs, int D, int H
 //   d wq[i][j] = q[i] d qp[j],  d q[i] = sum_j wq[i][j] d qp[j]
 __global__ void qfb_partial_kernel(const QueryFoldJob* jobs, int D, int H, float* part) {
   const QueryFoldJob jb = jobs[blockIdx.z];
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int d0 = blockIdx.y * QF_CHUNK;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4;   // 4 columns of one head
+  const int d0 = blockIdx.y * QF_CHUNK, d1 = min(D, d0 + QF_CHUNK);
   if (j >= D) return;
   const int h = j / (D / H);
-  float acc = 0.f;
-  for (int d = d0; d < min(D, d0 + QF_CHUNK); ++d)
-    acc = fmaf(__ldg(jb.wk + (size_t)d * D + j), __ldg(jb.dU + (size_t)d * jb.ldU + h), acc);
-  part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * D + j] = acc;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int d = d0;
+  for (; d + 8 <= d1; d += 8) {
+    float4 w[8];
+    float g[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      w[u] = __ldg(reinterpret_cast<const float4*>(jb.wk + (size_t)(d + u) * D + j));
+      g[u] = __ldg(jb.dU + (size_t)(d + u) * jb.ldU + h);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc.x = fmaf(w[u].x, g[u], acc.x); acc.y = fmaf(w[u].y, g[u], acc.y);
+      acc.z = fmaf(w[u].z, g[u], acc.z); acc.w = fmaf(w[u].w, g[u], acc.w);
+    }
+  }
+  for (; d < d1; ++d) {
+    const float4 w = __ldg(reinterpret_cast<const float4*>(jb.wk + (size_t)d * D + j));
+    const float g = __ldg(jb.dU + (size_t)d * jb.ldU + h);
+    acc.x = fmaf(w.x, g, acc.x); acc.y = fmaf(w.y, g, acc.y);
+    acc.z = fmaf(w.z, g, acc.z); acc.w = fmaf(w.w, g, acc.w);
+  }
+  *reinterpret_cast<float4*>(part + ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * D + j) = acc;
 }
 
 __global__ void qfb_dqp_kernel(const QueryFoldJob* jobs, int D, int H, int nchunk,
@@ -169,14 +211,31 @@ __global__ void qfb_rows_kernel(const QueryFoldJob* jobs, int D, int H, const fl
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int dh = D / H;
   const float s = rsqrtf((float)dh);
+  const bool vec = D % 128 == 0 && dh % 4 == 0;
   for (int i = blockIdx.x * nw + warp; i < D; i += gridDim.x * nw) {
     const float qi = __ldg(jb.q + i);
     float dq = 0.f;
-    for (int j = lane; j < D; j += 32) {
-      const float g = dqp[j];
-      dq = fmaf(__ldg(jb.wq + (size_t)i * D + j), g, dq);
-      jb.dwq[(size_t)i * D + j] = qi * g;
-      jb.dwk[(size_t)i * D + j] = s * __ldg(jb.dU + (size_t)i * jb.ldU + j / dh) * __ldg(jb.qp + j);
+    if (vec) {  // 4 adjacent columns (one head) per lane and step: 16-byte loads / stores
+      const float4* wq4 = reinterpret_cast<const float4*>(jb.wq + (size_t)i * D);
+      const float4* g4 = reinterpret_cast<const float4*>(dqp);
+      const float4* qp4 = reinterpret_cast<const float4*>(jb.qp);
+      float4* dwq4 = reinterpret_cast<float4*>(jb.dwq + (size_t)i * D);
+      float4* dwk4 = reinterpret_cast<float4*>(jb.dwk + (size_t)i * D);
+      for (int c = lane; c < D / 4; c += 32) {
+        const float4 g = g4[c], w = __ldg(wq4 + c), qp = __ldg(qp4 + c);
+        const float du = s * __ldg(jb.dU + (size_t)i * jb.ldU + (4 * c) / dh);
+        dq = fmaf(w.x, g.x, dq); dq = fmaf(w.y, g.y, dq);
+        dq = fmaf(w.z, g.z, dq); dq = fmaf(w.w, g.w, dq);
+        dwq4[c] = make_float4(qi * g.x, qi * g.y, qi * g.z, qi * g.w);
+        dwk4[c] = make_float4(du * qp.x, du * qp.y, du * qp.z, du * qp.w);
+      }
+    } else {
+      for (int j = lane; j < D; j += 32) {
+        const float g = dqp[j];
+        dq = fmaf(__ldg(jb.wq + (size_t)i * D + j), g, dq);
+        jb.dwq[(size_t)i * D + j] = qi * g;
+        jb.dwk[(size_t)i * D + j] = s * __ldg(jb.dU + (size_t)i * jb.ldU + j / dh) * __ldg(jb.qp + j);
+      }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) dq += __shfl_xor_sync(0xffffffffu, dq, o);
@@ -187,7 +246,8 @@ __global__ void qfb_rows_kernel(const QueryFoldJob* jobs, int D, int H, const fl
 cudaError_t launch_query_fold_bwd(const QueryFoldJob* jobs, int n_jobs, int D, int H,
                                   float* part, float* dqp, cudaStream_t st) {
   const int nchunk = (D + QF_CHUNK - 1) / QF_CHUNK;
-  qfb_partial_kernel<<<dim3((D + 127) / 128, nchunk, n_jobs), 128, 0, st>>>(jobs, D, H, part);
+  if (D % 4 || (D / H) % 4) return cudaErrorInvalidValue;
+  qfb_partial_kernel<<<dim3((D / 4 + 127) / 128, nchunk, n_jobs), 128, 0, st>>>(jobs, D, H, part);
   qfb_dqp_kernel<<<dim3((D + 127) / 128, 1, n_jobs), 128, 0, st>>>(jobs, D, H, nchunk, part, dqp);
   qfb_rows_kernel<<<dim3(64, 1, n_jobs), 256, 0, st>>>(jobs, D, H, dqp);
   return cudaGetLastError();
