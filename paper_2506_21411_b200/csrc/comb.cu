@@ -1148,11 +1148,16 @@ cudaError_t launch_fullcross_bwd(const FullCrossBwdArgs& a, cudaStream_t st) {
 //   dmix_j(r) = g[r] . V_j[r]                        -> dm  [child][R]      (linear)
 // One warp per (node, row); lanes own 8-column chunks, head dot products reduced with
 // shuffles inside the dh/8 lanes of a head.
+// SPLIT = 2 (attention nodes): a row's D columns are shared by two warps (half the heads
+// each), so a warp holds half the G row and half the value-row prefetch -- twice the warps
+// per SM, twice the bytes in flight
+template <int SPLIT>
 __global__ void __launch_bounds__(128) combine_bwd_kernel(CombineBwdArgs a) {
   __shared__ float sp[4][COMB_PTAB];
   __shared__ float sd[4][COMB_PTAB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long item = (long long)blockIdx.x * 4 + warp;
+  const long long item = ((long long)blockIdx.x * 4 + warp) / SPLIT;
+  const int part_id = (int)(((long long)blockIdx.x * 4 + warp) % SPLIT);
   const int n = (int)(item / a.R);
   const int r = (int)(item - (long long)n * a.R);
   if (n >= a.n_nodes) return;
@@ -1176,43 +1181,47 @@ __global__ void __launch_bounds__(128) combine_bwd_kernel(CombineBwdArgs a) {
     for (int j = 0; j < g; ++j) p[j * H + lane] *= inv;
   }
   __syncwarp();
-  const int nchunk = a.D / 8;
+  constexpr int QN = 8 / SPLIT;                 // 16-byte chunks per lane (D <= 2048)
+  const int nchunk = a.D / 8 / SPLIT;           // this warp's chunks: [cbase, cbase + nchunk)
+  const int cbase = part_id * nchunk;
   const int per_lane = (nchunk + 31) / 32;
-  float gr[8][8];
+  float gr[QN][8];
   const float* grow = a.G + ((long long)n * a.R + r) * a.D;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < QN; ++q) {
     if (q < per_lane && lane + 32 * q < nchunk) {
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow) + 2 * (lane + 32 * q));
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow) + 2 * (lane + 32 * q) + 1);
+      const int ch = cbase + lane + 32 * q;
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow) + 2 * ch);
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow) + 2 * ch + 1);
       gr[q][0] = g0.x; gr[q][1] = g0.y; gr[q][2] = g0.z; gr[q][3] = g0.w;
       gr[q][4] = g1.x; gr[q][5] = g1.y; gr[q][6] = g1.z; gr[q][7] = g1.w;
     }
   }
   // child j + 1's value row is requested while child j is reduced (software pipeline)
-  auto load_v = [&](int j, uint4 (&v)[8]) {
+  auto load_v = [&](int j, uint4 (&v)[QN]) {
     const __nv_bfloat16* vrow = a.V + (long long)(first + j) * a.sVj + (long long)r * a.D;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < QN; ++q) {
       const int ch = lane + 32 * q;
-      v[q] = (q < per_lane && ch < nchunk) ? __ldg(reinterpret_cast<const uint4*>(vrow) + ch)
-                                           : make_uint4(0, 0, 0, 0);
+      v[q] = (q < per_lane && ch < nchunk)
+                 ? __ldg(reinterpret_cast<const uint4*>(vrow) + cbase + ch)
+                 : make_uint4(0, 0, 0, 0);
     }
   };
-  uint4 vcur[8], vnext[8];
+  uint4 vcur[QN], vnext[QN];
   if (g > 0) load_v(0, vnext);
   for (int j = 0; j < g; ++j) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) vcur[q] = vnext[q];
+    for (int q = 0; q < QN; ++q) vcur[q] = vnext[q];
     if (j + 1 < g) load_v(j + 1, vnext);
     __nv_bfloat16* gvrow = a.sGj ? a.gV + (long long)(first + j) * a.sGj + (long long)r * a.ldg
                                  : a.gV + (long long)(first + j) * a.sVj + (long long)r * a.D;
     float dm_part = 0.f;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < QN; ++q) {
       float part = 0.f;
-      const int ch = lane + 32 * q;
-      const bool ok = q < per_lane && ch < nchunk;
+      const int ch = cbase + lane + 32 * q;
+      const bool ok = q < per_lane && lane + 32 * q < nchunk;
       if (ok) {
         const uint4 v = vcur[q];
         const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
@@ -1241,14 +1250,15 @@ __global__ void __launch_bounds__(128) combine_bwd_kernel(CombineBwdArgs a) {
     }
   }
   __syncwarp();
-  if (!a.mix && lane < H) {
+  const int hd = part_id * (H / SPLIT) + lane;  // this warp's heads
+  if (!a.mix && lane < H / SPLIT) {
     float s = 0.f;
-    for (int j = 0; j < g; ++j) s += p[j * H + lane] * dp[j * H + lane];
+    for (int j = 0; j < g; ++j) s += p[j * H + hd] * dp[j * H + hd];
     for (int j = 0; j < g; ++j) {
-      const float v = p[j * H + lane] * (dp[j * H + lane] - s);
-      if (a.dL) a.dL[(long long)(first + j) * a.sLj + (long long)r * H + lane] = v;
+      const float v = p[j * H + hd] * (dp[j * H + hd] - s);
+      if (a.dL) a.dL[(long long)(first + j) * a.sLj + (long long)r * H + hd] = v;
       if (a.sGj)
-        a.gV[(long long)(first + j) * a.sGj + (long long)r * a.ldg + a.D + lane] =
+        a.gV[(long long)(first + j) * a.sGj + (long long)r * a.ldg + a.D + hd] =
             __float2bfloat16(v);
     }
   }
@@ -1260,7 +1270,12 @@ cudaError_t launch_combine_bwd(const CombineBwdArgs& a, cudaStream_t st) {
       a.max_g * (a.mix ? 1 : a.H) > COMB_PTAB)
     return cudaErrorInvalidValue;
   const long long items = (long long)a.n_nodes * a.R;
-  combine_bwd_kernel<<<(int)((items + 3) / 4), 128, 0, st>>>(a);
+  // two warps per row for attention nodes whose head split keeps whole heads per warp
+  if (!a.mix && a.H % 2 == 0 && (a.D / 16) % dh == 0 && a.D >= 512) {
+    combine_bwd_kernel<2><<<(int)((2 * items + 3) / 4), 128, 0, st>>>(a);
+  } else {
+    combine_bwd_kernel<1><<<(int)((items + 3) / 4), 128, 0, st>>>(a);
+  }
   return cudaGetLastError();
 }
 
