@@ -238,6 +238,41 @@ __global__ void __launch_bounds__(256) l0_dv_kernel(int g, int R, int D, int H, 
   }
 }
 
+// Gpos alone (the training step's tcgen05 path), organised by position: a CTA takes one
+// position s and a range of images b, so each thread reads its 8 posV columns once and
+// reuses them for every image (posV rows were re-read from L2 once per image: 2x the bytes
+// of G). The G chunks of BU images are requested before any is reduced.
+constexpr int GPOS_BG = 8;   // images per CTA
+__global__ void __launch_bounds__(256) l0_gpos_s_kernel(int R, int D, int H, int S,
+                                                        const __nv_bfloat16* __restrict__ G,
+                                                        const float* __restrict__ posV,
+                                                        long long ldpos,
+                                                        float* __restrict__ Gpos) {
+  const int s = blockIdx.x, b0 = blockIdx.y * GPOS_BG;
+  const int nb = min(GPOS_BG, R / S - b0);
+  const int dh = D / H, lanes = dh >> 3;  // lanes per head (1..32, a power of two)
+  for (int c = threadIdx.x; c < D / 8; c += blockDim.x) {  // D / 8 % 32 == 0: whole warps
+    const int d0 = c * 8;
+    const float4* pv = reinterpret_cast<const float4*>(posV + (size_t)s * ldpos + d0);
+    const float4 pa = __ldg(pv), pb = __ldg(pv + 1);
+    uint4 gv[GPOS_BG];
+#pragma unroll
+    for (int u = 0; u < GPOS_BG; ++u)
+      gv[u] = u < nb ? __ldg(reinterpret_cast<const uint4*>(G + ((size_t)(b0 + u) * S + s) * D + d0))
+                     : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < GPOS_BG; ++u) {
+      float acc = bf16lo(gv[u].x) * pa.x + bf16hi(gv[u].x) * pa.y + bf16lo(gv[u].y) * pa.z +
+                  bf16hi(gv[u].y) * pa.w + bf16lo(gv[u].z) * pb.x + bf16hi(gv[u].z) * pb.y +
+                  bf16lo(gv[u].w) * pb.z + bf16hi(gv[u].w) * pb.w;
+      for (int off = lanes >> 1; off > 0; off >>= 1)
+        acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (u < nb && (threadIdx.x & (lanes - 1)) == 0)
+        Gpos[((size_t)(b0 + u) * S + s) * H + d0 / dh] = acc;
+    }
+  }
+}
+
 cudaError_t launch_l0_dv(int g, int R, int D, int H, int NH, const __nv_bfloat16* p,
                          const float* mix, const __nv_bfloat16* G, const float* posV,
                          long long ldpos, int S, float* Gpos, __nv_bfloat16* out,
@@ -246,6 +281,12 @@ cudaError_t launch_l0_dv(int g, int R, int D, int H, int NH, const __nv_bfloat16
   if (D % H || dh % 8 || dh > 256 || ((dh / 8) & (dh / 8 - 1)) || ((long long)R * (D / 8)) % 32 ||
       (!mix && (NH < 1 || H % NH)) || (posV && (!Gpos || S < 1)))
     return cudaErrorInvalidValue;
+  if (!out && posV && R % S == 0 && (D / 8) % 32 == 0 && dh % 8 == 0 && dh / 8 <= 32 &&
+      ((ldpos > 0 ? ldpos : D) % 4) == 0) {
+    const dim3 grid(S, (R / S + GPOS_BG - 1) / GPOS_BG);
+    l0_gpos_s_kernel<<<grid, 256, 0, st>>>(R, D, H, S, G, posV, ldpos > 0 ? ldpos : D, Gpos);
+    return cudaGetLastError();
+  }
   const long long n = (long long)R * (D / 8);
   if (n >= (1ll << 31)) return cudaErrorInvalidValue;
   l0_dv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, R, D, H, NH, p, mix, G, posV,
