@@ -320,7 +320,8 @@ class KernelTimer:
 
 
 TENSOR_KERNELS = ("dchag_l0_node", "dchag_gemm_bf16", "dchag_l0_logits", "dchag_gemm_combine",
-                  "dchag_gemm_wgrad", "dchag_gemm_rowdot", "dchag_l0_tgrad", "dchag_l0_tgrad_te",
+                  "dchag_gemm_wgrad", "dchag_gemm_rowdot", "dchag_gemm_rowdot_heads", "dchag_l0_tgrad",
+                  "dchag_l0_tgrad_te",
                   "dchag_gemm_nt", "dchag_fullcross_weights")
 
 

@@ -82,6 +82,15 @@ int dchag_gemm_rowdot(const void* A, int G, int Mo, int Mi, int K, long long sAg
                       const float* bias, long long bias_g, const void* Gmat, long long ldG,
                       float* dot_out, void* stream);
 
+/* As dchag_gemm_rowdot with `group` (32 or 64) columns per dot: group = 64 gives one sum per
+ * 64-column block, dot_out [G][N/64][M] (a head of 64 columns: the per-head dp partial the
+ * softmax backward reads with dh = 32, i.e. one partial per head). 64-column groups need the
+ * lean row-dot drain (CTA pairs, N % 64 == 0). */
+int dchag_gemm_rowdot_heads(const void* A, int G, int Mo, int Mi, int K, long long sAg,
+                            long long sAmo, long long sAmi, const void* W, int N, long long sWg,
+                            const float* bias, long long bias_g, const void* Gmat, long long ldG,
+                            int group, float* dot_out, void* stream);
+
 /* Tree level >= 1 fused (K_gemm COMB instance): each child's folded value projection
  * V_c = ctx_c W_c^T + bias_c (layers.py:123 output projection folded with the parent's
  * value projection) and the parent's softmax-weighted child sum (layers.py:114-122) in one
@@ -241,7 +250,9 @@ int dchag_child_softmax(float* L, const int* first, const int* count, int n_pare
  * tensor.py:201-203): dp_c[r][h] = sum of dchag_gemm_rowdot's 32-column partials of head h
  * (dpp fp32 [g][H*dh/32][R]) + Gpos[r][h] (dchag_l0_dv), then
  * dl_c = p_c (dp_c - sum_c' p_c' dp_c'); p as dchag_l0_dv. dl fp32 and dlb bf16, both
- * [g][H][R]. dh % 32 == 0. dl may be NULL when g <= 16 and dh == 64 (only the bf16 copy is written). */
+ * [g][H][R]. dh % 32 == 0: dpp holds dh / 32 partials per head (pass dh = 32 for one partial
+ * per head, dchag_gemm_rowdot_heads with group 64). dl may be NULL when g <= 16 and dh is 32
+ * or 64 (only the bf16 copy is written). */
 int dchag_l0_softmax_bwd(int g, int R, int H, int nh, int dh, const float* dpp,
                          const float* Gpos, const void* p, float* dl, void* dlb, void* stream);
 

@@ -216,7 +216,7 @@ static int gemm_impl(const void* A, int G, int Mo, int Mi, int K, long long sAg,
                      int outV_f32, long long sVg, long long sVmo, long long sVmi, float* outL,
                      long long sLg, long long sLmo, long long sLmi, const void* dotG,
                      long long ldG, float* dotOut, void* stream, const float* rmask = nullptr,
-                     const float* mtok = nullptr) {
+                     const float* mtok = nullptr, int dot_group = 32) {
   const bool dot = dotOut != nullptr;
   if (G < 1 || Mo < 1 || Mi < 128 || Mi % 128 || K < 16 || K % 16 || N < 16 || Nv < 0 ||
       Nv > N || Nv % 16)
@@ -307,6 +307,10 @@ static int gemm_impl(const void* A, int G, int Mo, int Mi, int K, long long sAg,
     a.lean = (pair && bn % 64 == 0 && N % bn == 0 && (a.debug & ~20) == 0 &&
               (!bias || (bias_g % 4 == 0 && reinterpret_cast<uintptr_t>(bias) % 16 == 0)) &&
               !(lean_env && atoi(lean_env) == 0)) ? 2 : 0;
+    a.dot64 = dot_group == 64;
+    if (a.dot64 && (a.lean != 2 || N % 64))
+      return fail(DCHAG_ERR_SHAPE, "gemm_rowdot_heads: 64-column groups need the lean row-dot "
+                                   "drain (CTA pairs, 64-column tiles; N=%d)", N);
   }
   return cuda_status(launch_gemm(tA, tW, tV, a, bk, num_sms_cached(), S(stream)), "gemm");
 }
@@ -419,6 +423,18 @@ int dchag_gemm_rowdot(const void* A, int G, int Mo, int Mi, int K, long long sAg
   if (!dot_out) return fail(DCHAG_ERR_SHAPE, "gemm_rowdot: dot_out is null");
   return gemm_impl(A, G, Mo, Mi, K, sAg, sAmo, sAmi, W, N, sWg, N, bias, bias_g, nullptr, 0, 0,
                    1, nullptr, 0, 0, 0, 0, nullptr, 0, 0, 0, Gmat, ldG, dot_out, stream);
+}
+
+int dchag_gemm_rowdot_heads(const void* A, int G, int Mo, int Mi, int K, long long sAg,
+                            long long sAmo, long long sAmi, const void* W, int N, long long sWg,
+                            const float* bias, long long bias_g, const void* Gmat, long long ldG,
+                            int group, float* dot_out, void* stream) {
+  if (!dot_out) return fail(DCHAG_ERR_SHAPE, "gemm_rowdot_heads: dot_out is null");
+  if (group != 32 && group != 64)
+    return fail(DCHAG_ERR_SHAPE, "gemm_rowdot_heads: group must be 32 or 64 (got %d)", group);
+  return gemm_impl(A, G, Mo, Mi, K, sAg, sAmo, sAmi, W, N, sWg, N, bias, bias_g, nullptr, 0, 0,
+                   1, nullptr, 0, 0, 0, 0, nullptr, 0, 0, 0, Gmat, ldG, dot_out, stream, nullptr,
+                   nullptr, group);
 }
 
 int dchag_gemm_combine(const void* ctx, int n_children, int R, int D, int H, const void* W,
@@ -651,7 +667,7 @@ int dchag_child_softmax(float* L, const int* first, const int* count, int n_pare
 int dchag_l0_softmax_bwd(int g, int R, int H, int nh, int dh, const float* dpp,
                          const float* Gpos, const void* p, float* dl, void* dlb, void* stream) {
   if (g < 1 || R < 1 || H < 1 || dh % 32 || nh < 1 || H % nh || !dpp || !Gpos || !p ||
-      (!dl && (g > 16 || dh != 64)) || !dlb)
+      (!dl && (g > 16 || (dh != 64 && dh != 32))) || !dlb)
     return fail(DCHAG_ERR_SHAPE, "l0_softmax_bwd: bad arguments");
   return cuda_status(launch_l0_softmax_bwd(g, R, H, nh, dh, dpp, Gpos,
                                            reinterpret_cast<const __nv_bfloat16*>(p), dl,

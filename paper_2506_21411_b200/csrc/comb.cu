@@ -700,10 +700,14 @@ cudaError_t launch_l0_softmax_bwd(int g, int R, int H, int NH, int dh, const flo
                                   const float* Gpos, const __nv_bfloat16* p, float* dl,
                                   __nv_bfloat16* dlb, cudaStream_t st) {
   if (dh % 32 || NH < 1 || H % NH) return cudaErrorInvalidValue;
-  if (g <= 16 && dh == 64 && (long long)R * H < (1ll << 31)) {
+  if (g <= 16 && (dh == 64 || dh == 32) && (long long)R * H < (1ll << 31)) {
     const long long n = (long long)R * H;
-    l0_softmax_bwd_reg_kernel<16, 2><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        g, R, H, NH, dpp, Gpos, p, dl, dlb);
+    if (dh == 64)
+      l0_softmax_bwd_reg_kernel<16, 2><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+          g, R, H, NH, dpp, Gpos, p, dl, dlb);
+    else  // one partial per head (dchag_gemm_rowdot_heads with 64-column groups)
+      l0_softmax_bwd_reg_kernel<16, 1><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+          g, R, H, NH, dpp, Gpos, p, dl, dlb);
     return cudaGetLastError();
   }
   if (!dl) return cudaErrorInvalidValue;  // the general kernel keeps dp in dl

@@ -62,6 +62,7 @@ struct GemmArgs {
   int csplit;                   // 1, or 2: split s sums children [s c/2, (s+1) c/2) (partials)
   int lay;                      // operand layouts: bit 0 A MN-major, bit 1 W MN-major
   FastDiv fd_G, fd_cpg, fd_ctn, fd_Mi;  // set by launch_gemm: G, tiles per group, N tiles, Mi
+  int dot64;                    // row-dot: one sum per 64 columns (dot_out [G][N/64][M])
   int lean;                     // 1: lean bf16 epilogue (tV box 64 columns x 32 rows, 128B
                                 //    swizzle; see gemm_kernel)
   int Ki;                       // MN-major A: K = Ko * Ki rows, (k / Ki) * sAko + (k % Ki) * lda

@@ -559,6 +559,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (p == npairs - 1) release();
         if constexpr (LEAN == 2) {
           const int m_row = mt * GEMM_BM + quarter * 32 + lane;
+          float hsum = 0.f;  // dot64: the pair's two 32-column sums
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint32_t* r = h ? rb : ra;
@@ -577,9 +578,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               a = fmaf(__uint_as_float(r[4 * j + 2]) + b.z, bf16lo(q1), a);
               a = fmaf(__uint_as_float(r[4 * j + 3]) + b.w, bf16hi(q1), a);
             }
-            args.dotOut[((size_t)g * (args.N >> 5) + (c0 >> 5) + 2 * p + h) * args.M + m_row] =
-                (s4[0] + s4[1]) + (s4[2] + s4[3]);
+            const float sh = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+            if (args.dot64)
+              hsum += sh;
+            else
+              args.dotOut[((size_t)g * (args.N >> 5) + (c0 >> 5) + 2 * p + h) * args.M + m_row] = sh;
           }
+          if (args.dot64)
+            args.dotOut[((size_t)g * (args.N >> 6) + (c0 >> 6) + p) * args.M + m_row] = hsum;
         } else {
         uint32_t pk[32];
 #pragma unroll

@@ -835,23 +835,28 @@ class DchagTrainer:
             _lib.call("dchag_l0_dv", g, R, D, H, nh_, pptr, mptr, _ptr(Gn), _ptr(st["posVU"][n]),
                       Dp, S, _ptr(Gpos), _lib.ptr(dV), sh,
                       work={"site": "bwd:l0_dv", "bytes": 2 * R * D * (1 + (0 if fast else g))})
-            dpp = torch.empty(g, D // 32, R, device=dev)
-            _lib.call("dchag_gemm_rowdot", _ptr(patches[:, c0:c0 + g]), g, B, S, PP, S * PP,
-                      cnt * S * PP, PP, _ptr(st["Mrow"][c0]), D, D * PP, _ptr(st["Cb"][c0]), D,
-                      _ptr(Gn), D, _ptr(dpp), sh,
+            # heads of 64 columns summed inside the row-dot drain (one dp partial per head:
+            # half the partials written and read back) where the lean drain takes the shape
+            heads = (attn and fast and dh == 64 and g <= 16 and D % 256 == 0
+                     and (R // 128) % 2 == 0 and os.environ.get("DCHAG_GEMM_LEAN", "1") != "0")
+            grp = 64 if heads else 32
+            dpp = torch.empty(g, D // grp, R, device=dev)
+            _lib.call("dchag_gemm_rowdot_heads", _ptr(patches[:, c0:c0 + g]), g, B, S, PP,
+                      S * PP, cnt * S * PP, PP, _ptr(st["Mrow"][c0]), D, D * PP,
+                      _ptr(st["Cb"][c0]), D, _ptr(Gn), D, grp, _ptr(dpp), sh,
                       work={"site": "bwd:l0_rowdot", "flops": 2 * g * R * D * PP,
-                            "bytes": R * D * 2 + g * R * PP * 2 + g * D // 32 * R * 4})
+                            "bytes": R * D * 2 + g * R * PP * 2 + g * D // grp * R * 4})
             dl = dlb = None
             if attn:
                 # the tcgen05 TE kernel reads only the bf16 copy (fp32 dl: the generic path)
                 if not fast or g > 16 or dh != 64:
                     dl = torch.empty(g, H, R, device=dev)
                 dlb = torch.empty(g, H, R, device=dev, dtype=torch.bfloat16)
-                _lib.call("dchag_l0_softmax_bwd", g, R, H, st["NH"], dh, _ptr(dpp), _ptr(Gpos),
-                          _ptr(pblk), _lib.ptr(dl), _ptr(dlb), sh,
-                          work={"site": "bwd:l0_softmax", "bytes": 4 * g * R * D // 32})
+                _lib.call("dchag_l0_softmax_bwd", g, R, H, st["NH"], 32 if heads else dh,
+                          _ptr(dpp), _ptr(Gpos), _ptr(pblk), _lib.ptr(dl), _ptr(dlb), sh,
+                          work={"site": "bwd:l0_softmax", "bytes": 4 * g * R * D // grp})
             else:
-                dp = dpp.view(g, H, dh // 32, R).sum(2) + Gpos.t().unsqueeze(0)
+                dp = dpp.view(g, H, dh // grp, R).sum(2) + Gpos.t().unsqueeze(0)
                 grads[f"{nd.name}.mix"] = dp.sum((1, 2))
             if fast:
                 _lib.call("dchag_l0_tgrad_te", _ptr(patches), cnt, c0, g, R, S, D, H, nh_, PP,
