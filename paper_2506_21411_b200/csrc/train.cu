@@ -470,25 +470,50 @@ DEV long long tiled_off(int blk, int k, int n, int K, int N) {  // canonical K-m
 // runs) and the row-dot operand Mrow [C][D][PP], plus Cb [C][D]. Mt's padding channels
 // [C, C_pad) are zero from allocation and never written.
 __global__ void pack_rows_kernel(L0PackArgs a) {
-  // one warp per fold row (channel c, column d): lanes sweep its PP contiguous values (no
-  // per-element 64-bit index division), lane 0 also moves the Cb term
+  // one warp per group of four fold rows (channel c, columns d .. d+3): lanes sweep the PP
+  // contiguous values of every row, all four rows' loads issued before any store (no
+  // per-element 64-bit index division); lane 0 also moves the Cb terms
+  constexpr int RW = 4;
   const int hw = a.D / a.H / 2, K = a.C_pad * a.PP;
   const int lane = threadIdx.x & 31;
   const long long rows = (long long)a.C * a.D;
   const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long w = w0; w < rows; w += nw) {
-    const int c = (int)(w / a.D), d = (int)(w - (long long)c * a.D);
-    const int n = __ldg(a.chan_node + c), l = __ldg(a.chan_local + c);
-    const float* row = a.MT + ((size_t)n * a.Dp + d) * a.Kn;
-    const int blk = d / hw, nn = d - blk * hw;
-    __nv_bfloat16* mrow = a.Mrow + ((size_t)c * a.D + d) * a.PP;
-    for (int kk = lane; kk < a.PP; kk += 32) {
-      const __nv_bfloat16 v = __float2bfloat16(row[l * a.PP + kk]);
-      mrow[kk] = v;
-      a.Mt[tiled_off(blk, c * a.PP + kk, nn, K, hw)] = v;
+  for (long long w4 = w0 * RW; w4 < rows; w4 += nw * RW) {
+    float v[RW][2];
+    const float* rowp[RW];
+    int cs[RW], ds[RW], ls[RW];
+#pragma unroll
+    for (int u = 0; u < RW; ++u) {
+      const long long w = w4 + u;
+      cs[u] = -1;
+      if (w >= rows) continue;
+      const int c = (int)(w / a.D), d = (int)(w - (long long)c * a.D);
+      const int n = __ldg(a.chan_node + c), l = __ldg(a.chan_local + c);
+      cs[u] = c; ds[u] = d; ls[u] = l;
+      rowp[u] = a.MT + ((size_t)n * a.Dp + d) * a.Kn;
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2) {
+        const int kk = lane + 32 * k2;
+        v[u][k2] = kk < a.PP ? rowp[u][l * a.PP + kk] : 0.f;
+      }
     }
-    if (lane == 0) a.Cb[(size_t)c * a.D + d] = row[a.ones0 + l];
+#pragma unroll
+    for (int u = 0; u < RW; ++u) {
+      if (cs[u] < 0) continue;
+      const int c = cs[u], d = ds[u];
+      const int blk = d / hw, nn = d - blk * hw;
+      __nv_bfloat16* mrow = a.Mrow + ((size_t)c * a.D + d) * a.PP;
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2) {
+        const int kk = lane + 32 * k2;
+        if (kk >= a.PP) continue;
+        const __nv_bfloat16 b = __float2bfloat16(v[u][k2]);
+        mrow[kk] = b;
+        a.Mt[tiled_off(blk, c * a.PP + kk, nn, K, hw)] = b;
+      }
+      if (lane == 0) a.Cb[(size_t)c * a.D + d] = rowp[u][a.ones0 + ls[u]];
+    }
   }
 }
 
@@ -551,6 +576,7 @@ __global__ void pack_pos_kernel(L0PackArgs a) {
 }
 
 cudaError_t launch_l0_pack(const L0PackArgs& a, cudaStream_t st) {
+  if (a.PP > 64) return cudaErrorInvalidValue;  // pack_rows: two 32-lane sweeps per row
   const int grid = 148 * 8;
   pack_rows_kernel<<<grid, 256, 0, st>>>(a);
   pack_et_kernel<<<grid, 256, 0, st>>>(a);
