@@ -115,6 +115,7 @@ int dchag_l0_tgrad_te(const void* patches, int cnt, int c0, int g, int R, int se
                 H, PP);
   L0TgradArgs a;
   memset(&a, 0, sizeof(a));
+  a.debug = getenv("DCHAG_TE_DEBUG") ? atoi(getenv("DCHAG_TE_DEBUG")) : 0;
   a.patches = reinterpret_cast<const __nv_bfloat16*>(patches);
   a.cnt = cnt; a.c0 = c0; a.g = g; a.R = R; a.S = seq; a.D = D; a.H = H; a.NH = nh; a.PP = PP;
   a.p = reinterpret_cast<const __nv_bfloat16*>(p); a.mix = mix;

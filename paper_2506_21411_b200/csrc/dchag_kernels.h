@@ -176,6 +176,7 @@ struct L0TgradArgs {
   long long te_ld;               // row stride of TE (elements)
   int ones0;                     // first bias row
   int has_dl;                    // dl given (attention nodes): one extra CTA column for E
+  int debug;                     // timing probes (DCHAG_TE_DEBUG): 1 no scaling, 2 no MMA
 };
 cudaError_t launch_l0_tgrad(const L0TgradArgs& a, cudaStream_t st);
 cudaError_t launch_l0_softmax_bwd(int g, int R, int H, int NH, int dh, const float* dpp,

@@ -1230,7 +1230,7 @@ __global__ void __launch_bounds__(192, 2)
           const uint64_t ad = eblk ? smem_desc(sa + kk * 32, 16, 1024, 2u)
                                    : smem_desc(sa + kk * 2048, TGC_A_BYTES / 2, 1024, 2u);
           const uint64_t bd = smem_desc(sb + kk * 2048, lbo_b, 1024, 2u);
-          mma_ss(tmem, ad, bd, idesc, (i | kk) != 0);
+          if (!(a.debug & 2)) mma_ss(tmem, ad, bd, idesc, (i | kk) != 0);
         }
         mma_commit(&empty[s]);
         if (i == nst - 1) mma_commit(done);
@@ -1275,7 +1275,7 @@ __global__ void __launch_bounds__(192, 2)
       if (!eblk && i + TGC_STAGES < nst) pq[s] = pword(i + TGC_STAGES);
       mbar_wait(&full[s], (i / TGC_STAGES) & 1);
       const float pc = pconv(pw);
-      if (!eblk) {
+      if (!eblk && !(a.debug & 1)) {
         const uint32_t rowaddr = smem_u32(smem + s * TGC_STAGE) + mh * (TGC_A_BYTES / 2) +
                                  (row >> 3) * 1024 + (row & 7) * 128;
         // rows sit 128 B apart: visit the row's 16-byte chunks in a row-rotated order so the
