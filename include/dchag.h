@@ -196,6 +196,14 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
                     const long long* node_poff, const void* WUt, const float* bU,
                     const float* posU, void* p, float* pinv, void* stream);
 
+/* The normalised level-0 softmax from dchag_l0_logits' pinv form (training backward):
+ * p[i] = e[i] * pinv[(n*R + r)*H + h] over each node's block (layout as dchag_l0_logits'
+ * p: poff[n] + ((hg*g + c)*R + r)*nh + h%nh). node_poff (int64) / node_g (int32) are device
+ * arrays of n_nodes; gmax >= all node_g. (R*H) % 8 == 0; e and p 16-byte aligned. */
+int dchag_l0_p_normalize(const void* e, const float* pinv, void* p, const long long* node_poff,
+                         const int* node_g, int n_nodes, int gmax, int R, int H, int nh,
+                         void* stream);
+
 /* Level-0 node context (K_l0, tcgen05 with A in TMEM):
  *   ctx[n][r][h*64:(h+1)*64] = sum_c p[r,c,h] * (patch_c[r] @ M_c[:, h-block])
  *                             + sum_c p[r,c,h] * E_n[c, h-block]

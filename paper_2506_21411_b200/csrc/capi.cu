@@ -205,6 +205,18 @@ int dchag_rowsum(const float* X, long long ldx, int rows, int N, float* out, voi
   return cuda_status(launch_rowsum(X, ldx, rows, N, out, S(stream)), "rowsum");
 }
 
+int dchag_l0_p_normalize(const void* e, const float* pinv, void* p, const long long* node_poff,
+                         const int* node_g, int n_nodes, int gmax, int R, int H, int nh,
+                         void* stream) {
+  if (!e || !pinv || !p || !node_poff || !node_g || n_nodes < 1 || gmax < 1 || R < 1 ||
+      H < 1 || nh < 1 || H % nh || (R * H) % 8)
+    return fail(DCHAG_ERR_SHAPE, "l0_p_normalize: bad arguments");
+  return cuda_status(launch_l0_p_normalize(reinterpret_cast<const __nv_bfloat16*>(e), pinv,
+                                           reinterpret_cast<__nv_bfloat16*>(p), node_poff,
+                                           node_g, n_nodes, gmax, R, H, nh, S(stream)),
+                     "l0_p_normalize");
+}
+
 int dchag_combine_overflow(int* flag, int reset) {
   if (!flag) return fail(DCHAG_ERR_SHAPE, "combine_overflow: null flag");
   return cuda_status(comb_overflow_flag(flag, reset), "combine_overflow");

@@ -575,6 +575,60 @@ __global__ void pack_pos_kernel(L0PackArgs a) {
   }
 }
 
+// ------------------------------------------------------------------------- p normalise
+// p[poff[n] + ((hg*g + c)*R + r)*NH + hn] = e[same] * pinv[(n*R + r)*H + hg*NH + hn]: the
+// training backward's normalised level-0 softmax from the forward's K_p0 output (e and 1/sum
+// e), instead of a second K_p0 pass over the images. One thread per 8 elements (16 bytes).
+__global__ void l0_p_normalize_kernel(const __nv_bfloat16* __restrict__ e,
+                                      const float* __restrict__ pinv,
+                                      __nv_bfloat16* __restrict__ p,
+                                      const long long* __restrict__ node_poff,
+                                      const int* __restrict__ node_g, int R, int H, int NH) {
+  const int n = blockIdx.y;
+  const int g = __ldg(node_g + n);
+  const long long base = __ldg(node_poff + n);
+  const int nel = g * R * H;          // the node's elements (< 2^31, a multiple of 8)
+  const int rows8 = 8 / NH;           // rows covered by one 8-element chunk
+  const float* pin = pinv + (long long)n * R * H;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) * 8; i < nel;
+       i += gridDim.x * blockDim.x * 8) {
+    const int t0 = i / NH;            // (hg*g + c)*R + r0
+    const int r0 = t0 % R, hg = t0 / R / g;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(e + base + i));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    float sc[8];
+    if (NH == 4) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(pin + (r0 + u) * H + hg * 4));
+        sc[4 * u] = q.x; sc[4 * u + 1] = q.y; sc[4 * u + 2] = q.z; sc[4 * u + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sc[k] = __ldg(pin + (r0 + k / NH) * H + hg * NH + k % NH);
+    }
+    (void)rows8;
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      o[k] = pack_bf16(bf16lo(w[k]) * sc[2 * k], bf16hi(w[k]) * sc[2 * k + 1]);
+    *reinterpret_cast<uint4*>(p + base + i) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+cudaError_t launch_l0_p_normalize(const __nv_bfloat16* e, const float* pinv, __nv_bfloat16* p,
+                                  const long long* node_poff, const int* node_g, int n_nodes,
+                                  int gmax, int R, int H, int NH, cudaStream_t st) {
+  if ((R * H) % 8 || NH < 1 || H % NH || 8 % NH || R % (8 / NH) ||
+      (long long)gmax * R * H >= (1ll << 31) || (NH == 4 && H % 4))
+    return cudaErrorInvalidValue;
+  const long long per = (long long)gmax * R * H / 8;
+  const int bx = (int)((per + 255) / 256 < 2048 ? (per + 255) / 256 : 2048);
+  l0_p_normalize_kernel<<<dim3(bx, n_nodes), 256, 0, st>>>(e, pinv, p, node_poff, node_g, R, H,
+                                                           NH);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_l0_pack(const L0PackArgs& a, cudaStream_t st) {
   if (a.PP > 64) return cudaErrorInvalidValue;  // pack_rows: two 32-lane sweeps per row
   const int grid = 148 * 8;

@@ -385,6 +385,7 @@ class DchagTrainer:
                             "flops": 2 * 2 * R * cnt * st["PP"] * H})
             prow = 1
             saved["poff"] = poff_t
+            saved["p_e"], saved["pinv"] = pbuf, pinv  # the backward normalises these
         else:
             poff_t = self._dev_ints([c * H for c in st["c0s"]], torch.int64, dev)
             pbuf, prow, pinv = st["p_const"], 0, None
@@ -803,14 +804,13 @@ class DchagTrainer:
         _lib.call("dchag_unfold", _ptr(img), img.stride(0), img.stride(1), B, cnt, m.image_h,
                   m.image_w, m.patch, _ptr(patches), sh,
                   work={"site": "bwd:unfold", "bytes": 4 * img.numel()})
-        if attn:  # normalised level-0 softmax (K_p0 without pinv)
+        if attn:  # normalised level-0 softmax: the forward's e x 1/sum e (no second K_p0)
             gl = st["levels"][0]
             pnorm = torch.empty(sum(gl) * R * H, device=dev, dtype=torch.bfloat16)
-            _lib.call("dchag_l0_logits", _ptr(img), img.stride(0), img.stride(1), B,
-                      m.image_h, m.image_w, m.patch, H, st["HP"], st["NH"], n0, max(gl),
-                      _ptr(st["l0_c0"]), _ptr(st["l0_g"]), _ptr(saved["poff"]),
-                      _ptr(st["WUt"]), _ptr(st["bU"]), _ptr(st["posU"]), _ptr(pnorm), 0, sh,
-                      work={"site": "bwd:l0_logits", "flops": 2 * 2 * R * cnt * PP * H})
+            _lib.call("dchag_l0_p_normalize", _ptr(saved["p_e"]), _ptr(saved["pinv"]),
+                      _ptr(pnorm), _ptr(saved["poff"]), _ptr(st["l0_g"]), n0, max(gl), R, H,
+                      st["NH"], sh,
+                      work={"site": "bwd:p_normalize", "bytes": sum(gl) * R * H * 4 + n0 * R * H * 4})
         # positional sums over the batch, Gs_n[s] = sum_b G_n[b, s] (x sum(mix), linear),
         # straight into the pos rows of the node's TE block (bf16 GEMM operand)
         TE = st["TE"]
