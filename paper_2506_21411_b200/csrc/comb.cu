@@ -696,10 +696,65 @@ __global__ void __launch_bounds__(256) l0_softmax_bwd_reg_kernel(
   }
 }
 
+// One dp partial per head, NH = 4: one thread per (head group, row) takes the group's four
+// heads, so each channel's p is one 8-byte load (the per-head form read 2 bytes of every
+// 8: a quarter of each sector) and Gpos one float4.
+template <int GM>
+__global__ void __launch_bounds__(256) l0_softmax_bwd_hg4_kernel(
+    int g, int R, int H, const float* __restrict__ dpp, const float* __restrict__ Gpos,
+    const __nv_bfloat16* __restrict__ p, float* __restrict__ dl,
+    __nv_bfloat16* __restrict__ dlb) {
+  const unsigned idx = blockIdx.x * blockDim.x + threadIdx.x;  // R * H / 4 < 2^31 (launch)
+  const int HG = H / 4;
+  if (idx >= (unsigned)R * (unsigned)HG) return;
+  const int hg = (int)(idx / (unsigned)R), r = (int)(idx - (unsigned)hg * R);
+  const float4 gp = __ldg(reinterpret_cast<const float4*>(Gpos + (size_t)r * H + hg * 4));
+  float dp[GM][4];
+  uint2 pw[GM];
+#pragma unroll
+  for (int c = 0; c < GM; ++c) {
+    dp[c][0] = gp.x; dp[c][1] = gp.y; dp[c][2] = gp.z; dp[c][3] = gp.w;
+    pw[c] = make_uint2(0u, 0u);
+    if (c < g) {
+#pragma unroll
+      for (int hn = 0; hn < 4; ++hn)
+        dp[c][hn] += __ldg(dpp + ((size_t)c * H + hg * 4 + hn) * R + r);
+      pw[c] = __ldg(reinterpret_cast<const uint2*>(p + ((size_t)(hg * g + c) * R + r) * 4));
+    }
+  }
+#pragma unroll
+  for (int hn = 0; hn < 4; ++hn) {
+    float sdp = 0.f;
+#pragma unroll
+    for (int c = 0; c < GM; ++c) {
+      const uint32_t w = (hn < 2) ? pw[c].x : pw[c].y;
+      sdp = fmaf((hn & 1) ? bf16hi(w) : bf16lo(w), dp[c][hn], sdp);
+    }
+#pragma unroll
+    for (int c = 0; c < GM; ++c) {
+      if (c < g) {
+        const uint32_t w = (hn < 2) ? pw[c].x : pw[c].y;
+        const float pc = (hn & 1) ? bf16hi(w) : bf16lo(w);
+        const size_t o = ((size_t)c * H + hg * 4 + hn) * R + r;
+        const float v = pc * (dp[c][hn] - sdp);
+        if (dl) dl[o] = v;
+        dlb[o] = __float2bfloat16(v);
+      }
+    }
+  }
+}
+
 cudaError_t launch_l0_softmax_bwd(int g, int R, int H, int NH, int dh, const float* dpp,
                                   const float* Gpos, const __nv_bfloat16* p, float* dl,
                                   __nv_bfloat16* dlb, cudaStream_t st) {
   if (dh % 32 || NH < 1 || H % NH) return cudaErrorInvalidValue;
+  if (g <= 16 && dh == 32 && NH == 4 && H % 4 == 0 && (long long)R * H < (1ll << 31) &&
+      reinterpret_cast<uintptr_t>(p) % 8 == 0) {
+    const long long n = (long long)R * (H / 4);
+    l0_softmax_bwd_hg4_kernel<16><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        g, R, H, dpp, Gpos, p, dl, dlb);
+    return cudaGetLastError();
+  }
   if (g <= 16 && (dh == 64 || dh == 32) && (long long)R * H < (1ll << 31)) {
     const long long n = (long long)R * H;
     if (dh == 64)
