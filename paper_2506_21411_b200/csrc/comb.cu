@@ -240,9 +240,9 @@ __global__ void __launch_bounds__(256) l0_dv_kernel(int g, int R, int D, int H, 
 
 // Gpos alone (the training step's tcgen05 path), organised by position: a CTA takes one
 // position s and a range of images b, so each thread reads its 8 posV columns once and
-// reuses them for every image (posV rows were re-read from L2 once per image: 2x the bytes
+// reuses them for four images (posV rows were re-read from L2 once per image: 2x the bytes
 // of G). The G chunks of BU images are requested before any is reduced.
-constexpr int GPOS_BG = 8;   // images per CTA
+constexpr int GPOS_BG = 4;   // images per CTA
 __global__ void __launch_bounds__(256) l0_gpos_s_kernel(int R, int D, int H, int S,
                                                         const __nv_bfloat16* __restrict__ G,
                                                         const float* __restrict__ posV,
