@@ -484,8 +484,39 @@ def b200_arm(args, wl, tp, max_group):
             return fe.finish(torch.cat(pays), B)
         eager_step = step
     else:
-        step = lambda: fe(images)  # noqa: E731
-        eager_step = step
+        eager_step = lambda: fe(images)  # noqa: E731
+        step = eager_step
+        if not args.no_graph and world == 1 and not fe._unfolded():
+            # the inference forward as one CUDA graph (serving): a replay re-runs every
+            # kernel of the step; the eager launches before capture build every cached
+            # device table, so the captured region holds kernels only
+            for _ in range(2):
+                eager_step()
+            torch.cuda.synchronize()
+            n_cap = _lib.LAUNCH_COUNT["n"]
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            fgraph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(fgraph, stream=side):
+                    eager_step()
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            f_launches = _lib.LAUNCH_COUNT["n"] - n_cap
+
+            def graph_step():
+                fgraph.replay()
+                _lib.LAUNCH_COUNT["n"] += f_launches
+            graph_step()
+            torch.cuda.synchronize()
+            # keep the graph only where it is faster (launch-bound steps: the CPU launch cost
+            # of ~10-20 kernels exceeds a small step's GPU time; ms-scale steps tie)
+            t_eager = timed(eager_step, 5)
+            t_graph = timed(graph_step, 5)
+            if t_graph < t_eager:
+                step, gstep = graph_step, fgraph
+            else:
+                fgraph.reset()
     clk = ClockSampler(local).__enter__()
     for i in range(args.warmup):
         step()
@@ -609,8 +640,7 @@ def b200_arm(args, wl, tp, max_group):
     if rank == 0:
         clocks = clk.summary()
         cfg = workload_config(args, wl, arch_tp or tp, max_group)
-        if wl.get("train"):
-            cfg["launch"] = "eager" if gstep is None else "cuda graph (whole step)"
+        cfg["launch"] = "eager" if gstep is None else "cuda graph (whole step)"
         if arch_tp:
             cfg["parallelism"] = f"dchag-tp{arch_tp} architecture on 1 GPU (slabs sequential)"
             cfg["final_layer"] = "once, over the tp streams (AllGather schedule)"
@@ -644,7 +674,8 @@ def b200_arm(args, wl, tp, max_group):
         print(json.dumps(line), flush=True)
     if gstep is not None:
         torch.cuda.synchronize()
-        gstep.graph.reset()  # release the captured NCCL work before the group goes away
+        # release the captured work (NCCL included) before the group goes away
+        (gstep.graph if hasattr(gstep, "graph") else gstep).reset()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
