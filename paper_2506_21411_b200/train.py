@@ -838,7 +838,8 @@ class DchagTrainer:
             # heads of 64 columns summed inside the row-dot drain (one dp partial per head:
             # half the partials written and read back) where the lean drain takes the shape
             heads = (attn and fast and dh == 64 and g <= 16 and D % 256 == 0
-                     and (R // 128) % 2 == 0 and os.environ.get("DCHAG_GEMM_LEAN", "1") != "0")
+                     and (R // 128) % 2 == 0 and os.environ.get("DCHAG_GEMM_LEAN", "1") != "0"
+                     and int(os.environ.get("DCHAG_GEMM_DEBUG", "0") or 0) & ~20 == 0)
             grp = 64 if heads else 32
             dpp = torch.empty(g, D // grp, R, device=dev)
             _lib.call("dchag_gemm_rowdot_heads", _ptr(patches[:, c0:c0 + g]), g, B, S, PP,
