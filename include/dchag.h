@@ -196,6 +196,13 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
                     const long long* node_poff, const void* WUt, const float* bU,
                     const float* posU, void* p, float* pinv, void* stream);
 
+/* fp32 parity mode operand split: x fp32 [rows][K] (row stride ldx) -> out bf16 [rows][3K]
+ * (row stride ldo) = [hi | lo | hi], hi = bf16(x), lo = bf16(x - hi); with the weights as
+ * [hi | hi | lo] one bf16 GEMM over 3K gives x W to ~2^-16 relative. K % 4 == 0, x 16-byte
+ * and out 8-byte aligned. */
+int dchag_split3_bf16(const float* x, long long rows, int K, long long ldx, void* out,
+                      long long ldo, void* stream);
+
 /* The normalised level-0 softmax from dchag_l0_logits' pinv form (training backward):
  * p[i] = e[i] * pinv[(n*R + r)*H + h] over each node's block (layout as dchag_l0_logits'
  * p: poff[n] + ((hg*g + c)*R + r)*nh + h%nh). node_poff (int64) / node_g (int32) are device

@@ -29,6 +29,7 @@ SIGNATURES = {
                         c_vp, c_vp, c_vp, c_int, c_vp],
     "dchag_gemm_rowdot": [c_vp, c_int, c_int, c_int, c_int, c_ll, c_ll, c_ll, c_vp, c_int,
                           c_ll, c_vp, c_ll, c_vp, c_ll, c_vp, c_vp],
+    "dchag_split3_bf16": [c_vp, c_ll, c_int, c_ll, c_vp, c_ll, c_vp],
     "dchag_l0_p_normalize": [c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_int,
                              c_vp],
     "dchag_gemm_rowdot_heads": [c_vp, c_int, c_int, c_int, c_int, c_ll, c_ll, c_ll, c_vp, c_int,

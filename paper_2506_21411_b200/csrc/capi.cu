@@ -205,6 +205,15 @@ int dchag_rowsum(const float* X, long long ldx, int rows, int N, float* out, voi
   return cuda_status(launch_rowsum(X, ldx, rows, N, out, S(stream)), "rowsum");
 }
 
+int dchag_split3_bf16(const float* x, long long rows, int K, long long ldx, void* out,
+                      long long ldo, void* stream) {
+  if (!x || !out || rows < 1 || K < 4 || K % 4 || ldx < K || ldo < 3LL * K)
+    return fail(DCHAG_ERR_SHAPE, "split3_bf16: bad arguments rows=%lld K=%d", rows, K);
+  return cuda_status(launch_split3(x, rows, K, ldx, reinterpret_cast<__nv_bfloat16*>(out), ldo,
+                                   S(stream)),
+                     "split3_bf16");
+}
+
 int dchag_l0_p_normalize(const void* e, const float* pinv, void* p, const long long* node_poff,
                          const int* node_g, int n_nodes, int gmax, int R, int H, int nh,
                          void* stream) {
@@ -516,6 +525,7 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
       H % nh)
     return fail(DCHAG_ERR_SHAPE, "l0_logits: bad shape");
   L0LogitArgs a;
+  memset(&a, 0, sizeof(a));
   a.img = reinterpret_cast<const __nv_bfloat16*>(img);
   a.img_sb = img_sb; a.img_sc = img_sc;
   a.B = B; a.S = (Himg / P) * (W / P); a.W = W; a.P = P; a.wp = W / P; a.H = H; a.HP = HP;
@@ -540,6 +550,7 @@ int dchag_l0_node(const void* img, long long img_sb, long long img_sc, int B, in
                   void* stream) {
   if (Himg % P || W % P) return fail(DCHAG_ERR_SHAPE, "l0_node: image not divisible by patch");
   L0NodeArgs a;
+  memset(&a, 0, sizeof(a));
   a.img = reinterpret_cast<const __nv_bfloat16*>(img);
   a.img_sb = img_sb; a.img_sc = img_sc;
   a.B = B; a.S = (Himg / P) * (W / P); a.W = W; a.P = P; a.wp = W / P; a.H = H; a.D = D;
@@ -644,6 +655,8 @@ int dchag_l0_tgrad(const void* patches, int cnt, int c0, int g, int R, int seq, 
     return fail(DCHAG_ERR_SHAPE, "l0_tgrad: bad shape R=%d S=%d D=%d H=%d PP=%d", R, seq, D, H,
                 PP);
   L0TgradArgs a;
+  memset(&a, 0, sizeof(a));  // every field defined (timing-probe bits included)
+  a.debug = getenv("DCHAG_TE_DEBUG") ? atoi(getenv("DCHAG_TE_DEBUG")) : 0;
   a.patches = reinterpret_cast<const __nv_bfloat16*>(patches);
   a.cnt = cnt; a.c0 = c0; a.g = g; a.R = R; a.S = seq; a.D = D; a.H = H; a.NH = nh; a.PP = PP;
   a.p = reinterpret_cast<const __nv_bfloat16*>(p); a.mix = mix;
@@ -693,6 +706,7 @@ int dchag_combine_f32(int n_nodes, int R, int D, int H, const int* node_first, c
                       const float* mix, float* ctx, void* stream) {
   if (!mix && !L) return fail(DCHAG_ERR_SHAPE, "combine_f32: need logits or mix");
   CombineF32Args a;
+  memset(&a, 0, sizeof(a));
   a.n_nodes = n_nodes; a.R = R; a.D = D; a.H = H; a.max_g = max_g;
   a.node_first = node_first; a.node_g = node_g;
   a.V = V; a.sVj = sVj; a.L = L; a.sLj = sLj; a.mix = mix; a.ctx = ctx;

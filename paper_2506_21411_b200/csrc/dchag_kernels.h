@@ -315,6 +315,8 @@ struct L0PackArgs {             // level-0 refold scatter (train.cu pack kernels
   float* posU;                  // attention: [n0][S][HP]
 };
 cudaError_t launch_l0_pack(const L0PackArgs& a, cudaStream_t st);
+cudaError_t launch_split3(const float* x, long long rows, int K, long long ldx,
+                          __nv_bfloat16* out, long long ldo, cudaStream_t st);
 cudaError_t launch_l0_p_normalize(const __nv_bfloat16* e, const float* pinv, __nv_bfloat16* p,
                                   const long long* node_poff, const int* node_g, int n_nodes,
                                   int gmax, int R, int H, int NH, cudaStream_t st);

@@ -575,6 +575,46 @@ __global__ void pack_pos_kernel(L0PackArgs a) {
   }
 }
 
+// ------------------------------------------------------------------------- split3
+// fp32 x [rows][K] (row stride ldx) -> bf16 out [rows][3K] (row stride ldo) = [hi | lo | hi]
+// with hi = bf16(x), lo = bf16(x - hi): the A operand of the fp32 parity mode's split-bf16
+// 3-term GEMM, in one pass (the torch form read x twice and wrote four intermediates).
+__global__ void split3_kernel(const float* __restrict__ x, long long rows, int K, long long ldx,
+                              __nv_bfloat16* __restrict__ out, long long ldo) {
+  const int k4 = K / 4;
+  const long long n = rows * k4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / k4;
+    const int c = (int)(i - r * k4) * 4;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(x + r * ldx + c));
+    const float f[4] = {v.x, v.y, v.z, v.w};
+    uint32_t hi[2], lo[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const __nv_bfloat16 h0 = __float2bfloat16(f[2 * e]), h1 = __float2bfloat16(f[2 * e + 1]);
+      const float r0 = f[2 * e] - __bfloat162float(h0), r1 = f[2 * e + 1] - __bfloat162float(h1);
+      hi[e] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+      lo[e] = pack_bf16(r0, r1);
+    }
+    __nv_bfloat16* o = out + r * ldo + c;
+    *reinterpret_cast<uint2*>(o) = make_uint2(hi[0], hi[1]);
+    *reinterpret_cast<uint2*>(o + K) = make_uint2(lo[0], lo[1]);
+    *reinterpret_cast<uint2*>(o + 2 * K) = make_uint2(hi[0], hi[1]);
+  }
+}
+
+cudaError_t launch_split3(const float* x, long long rows, int K, long long ldx,
+                          __nv_bfloat16* out, long long ldo, cudaStream_t st) {
+  if (K % 4 || ldx % 4 || ldo % 4 || (reinterpret_cast<uintptr_t>(x) % 16) ||
+      (reinterpret_cast<uintptr_t>(out) % 8))
+    return cudaErrorInvalidValue;
+  const long long n = rows * (K / 4);
+  const int blocks = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  split3_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(x, rows, K, ldx, out, ldo);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------- p normalise
 // p[poff[n] + ((hg*g + c)*R + r)*NH + hn] = e[same] * pinv[(n*R + r)*H + hg*NH + hn]: the
 // training backward's normalised level-0 softmax from the forward's K_p0 output (e and 1/sum

@@ -290,9 +290,11 @@ class DchagFrontEnd(torch.nn.Module):
         off, cnt = self.slab
         sl = slice(off, off + cnt)
         tok = ops.tokenize_channels_fp32(images.float(), w["tok.w"][sl], w["tok.b"][sl],
-                                         w["special.channel_id"][sl], w["special.pos"], m.patch)
+                                         w["special.channel_id"][sl], w["special.pos"], m.patch,
+                                         node_major=True)
         y = ops.tree_aggregate_fp32(tok, self.tree, w, f"agg.slab{self.rank}",
-                                    self.strategy.agg_layer_kind, m.heads).contiguous()
+                                    self.strategy.agg_layer_kind, m.heads,
+                                    B=images.shape[0]).contiguous()
         if self.tp > 1:
             allg = torch.empty((self.tp,) + tuple(y.shape), device=y.device, dtype=y.dtype)
             comm.all_gather_into_tensor(allg, y, group=self.process_group)

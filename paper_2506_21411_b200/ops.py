@@ -404,27 +404,36 @@ def flat_aggregate(tokens, w, prefix, variant, n_heads, hooks=None, tag="aggrega
 # long = A W - A_lo W_lo (relative error ~2^-16, fp32 accumulation); combines run in fp32.
 
 def _split3(x):
-    """fp32 [..., K] -> bf16 [..., 3K] = [hi | lo | hi]."""
-    hi = x.to(torch.bfloat16)
-    lo = (x - hi.float()).to(torch.bfloat16)
-    return torch.cat([hi, lo, hi], dim=-1).contiguous()
+    """fp32 [..., K] -> bf16 [..., 3K] = [hi | lo | hi] (dchag_split3_bf16: one pass)."""
+    x = _f32(x)
+    K = x.shape[-1]
+    x2 = x.reshape(-1, K)
+    if x2.stride(-1) != 1 or x2.data_ptr() % 16 or x2.stride(0) % 4:
+        x2 = x2.contiguous()
+    out = torch.empty(x2.shape[0], 3 * K, device=x.device, dtype=torch.bfloat16)
+    _lib.call("dchag_split3_bf16", _lib.ptr(x2), x2.shape[0], K, x2.stride(0), _lib.ptr(out),
+              3 * K, _lib.stream_handle(),
+              work={"site": "ops:split3", "bytes": x2.numel() * 10})
+    return out.view(*x.shape[:-1], 3 * K)
 
 
-def _gemm3(A, W_dn, bias, N_logit=0):
+def _gemm3(A, W_dn, bias, N_logit=0, out=None, out_L=None):
     """fp32 A [M, K] @ W_dn [K, N] + bias, fp32-accurate; returns fp32 [M, N - N_logit]
-    (and the last N_logit columns separately)."""
+    (and the last N_logit columns separately), written into `out` / `out_L` when given
+    (row-contiguous [M, N - N_logit] / [M, N_logit])."""
     M, K = A.shape
     N = W_dn.shape[1]
     if M % 128 or K % 16:
         raise ConfigError("fp32 mode needs rows % 128 == 0 and K % 16 == 0")
-    A3 = _split3(_f32(A))
+    A3 = _split3(A)
     Wt = _f32(W_dn).t()
     hi = Wt.to(torch.bfloat16)
     lo = (Wt - hi.float()).to(torch.bfloat16)
     W3 = torch.cat([hi, hi, lo], dim=1).contiguous()                 # [N, 3K]
     Nv = N - N_logit
-    V = torch.empty(M, Nv, device="cuda", dtype=torch.float32)
-    L = torch.empty(M, max(N_logit, 1), device="cuda", dtype=torch.float32)
+    V = out if out is not None else torch.empty(M, Nv, device="cuda", dtype=torch.float32)
+    L = out_L if out_L is not None else torch.empty(M, max(N_logit, 1), device="cuda",
+                                                    dtype=torch.float32)
     b = _f32(bias) if bias is not None else torch.zeros(N, device="cuda")
     _lib.call("dchag_gemm_bf16", _lib.ptr(A3), 1, 1, M, 3 * K, M * 3 * K, M * 3 * K, 3 * K,
               _lib.ptr(W3), N, N * 3 * K, Nv, _lib.ptr(b), N, 0, 0, N, 1, _lib.ptr(V), 1, 0, 0,
@@ -432,9 +441,10 @@ def _gemm3(A, W_dn, bias, N_logit=0):
     return (V, L) if N_logit else V
 
 
-def tokenize_channels_fp32(images, tok_w, tok_b, chan_id, pos, patch):
+def tokenize_channels_fp32(images, tok_w, tok_b, chan_id, pos, patch, node_major=False):
     """fp32 tokens [B, Cs, S, D] (model.py:51-64) with fp32-accurate GEMMs: one grouped
-    split-bf16 GEMM over the channels (group = channel), tok.b + chan_id in its epilogue."""
+    split-bf16 GEMM over the channels (group = channel), tok.b + chan_id in its epilogue.
+    node_major=True returns them as [Cs, B*S, D] (the tree's layout: no transposed copy)."""
     B, C, Hh, Ww = images.shape
     P = patch
     S, PP = (Hh // P) * (Ww // P), P * P
@@ -455,17 +465,26 @@ def tokenize_channels_fp32(images, tok_w, tok_b, chan_id, pos, patch):
     _lib.call("dchag_gemm_bf16", _lib.ptr(A3), C, 1, R, K3, R * K3, 0, K3, _lib.ptr(W3), D,
               D * K3, D, _lib.ptr(bias), D, 0, 0, 0, 1, _lib.ptr(out), 1, R * D, 0, D, 0, 0, 0, 0,
               _lib.stream_handle())
+    if node_major:
+        out.view(C, B, S, D).add_(_f32(pos)[None, None])
+        return out
     return out.view(C, B, S, D).permute(1, 0, 2, 3) + _f32(pos)[None, None]
 
 
-def tree_aggregate_fp32(tokens, spec: TreeSpec, w, prefix, layer_kind, n_heads):
-    """fp32 [B, C, S, D] -> [B, 1, S, D] (model.py:76-97), single_query / linear nodes."""
-    B, C, S, D = tokens.shape
+def tree_aggregate_fp32(tokens, spec: TreeSpec, w, prefix, layer_kind, n_heads, B=None):
+    """fp32 [B, C, S, D] -> [B, 1, S, D] (model.py:76-97), single_query / linear nodes.
+    A 3-D node-major [C, B*S, D] input (tokenize_channels_fp32(node_major=True)) needs B."""
+    if tokens.dim() == 3:
+        C, R, D = tokens.shape
+        S = R // B
+        x = _f32(tokens)
+    else:
+        B, C, S, D = tokens.shape
+        R = B * S
+        x = _f32(tokens).permute(1, 0, 2, 3).reshape(C, R, D).contiguous()
     H = n_heads
-    R = B * S
     st = _lib.stream_handle()
     tw = {k: _f32(v) for k, v in w.items() if k.startswith(prefix + ".")}
-    x = _f32(tokens).permute(1, 0, 2, 3).reshape(C, R, D).contiguous()
     attn = layer_kind != "linear"
     for li, level in enumerate(spec.levels):
         n_in = x.shape[0]
@@ -479,11 +498,10 @@ def tree_aggregate_fp32(tokens, spec: TreeSpec, w, prefix, layer_kind, n_heads):
         for node, f, g in zip(nodes, firsts, level):
             Wc, _ = consumer_weight(tw, node, layer_kind, H)
             if attn:
-                v, lg = _gemm3(x[f:f + g].reshape(g * R, D), Wc, None, N_logit=H)
-                V[f:f + g] = v.view(g, R, D)
-                L[f:f + g] = lg.view(g, R, H)
+                _gemm3(x[f:f + g].reshape(g * R, D), Wc, None, N_logit=H,
+                       out=V[f:f + g].view(g * R, D), out_L=L[f:f + g].view(g * R, H))
             else:
-                V[f:f + g] = _gemm3(x[f:f + g].reshape(g * R, D), Wc, None).view(g, R, D)
+                _gemm3(x[f:f + g].reshape(g * R, D), Wc, None, out=V[f:f + g].view(g * R, D))
         ctx = torch.empty(len(level), R, D, device="cuda", dtype=torch.float32)
         first_t = _dev_i32(firsts)
         g_t = _dev_i32(level)
@@ -494,7 +512,7 @@ def tree_aggregate_fp32(tokens, spec: TreeSpec, w, prefix, layer_kind, n_heads):
         y = torch.empty(len(level), R, D, device="cuda", dtype=torch.float32)
         for k, node in enumerate(nodes):
             if attn:
-                y[k] = _gemm3(ctx[k], tw[f"{node}.wo"], tw[f"{node}.bo"])
+                _gemm3(ctx[k], tw[f"{node}.wo"], tw[f"{node}.bo"], out=y[k])
             else:
                 y[k] = ctx[k] + tw[f"{node}.b"]
         x = y
