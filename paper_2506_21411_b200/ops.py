@@ -417,6 +417,28 @@ def _split3(x):
     return out.view(*x.shape[:-1], 3 * K)
 
 
+_W3_CACHE: dict = {}
+
+
+def _split_w3(W_dn):
+    """bf16 [N, 3K] = [hi | hi | lo] of an fp32 weight [K, N], made once per weight version
+    (keyed on storage, version counter and shape, like the full_cross fold cache)."""
+    # the entry holds the source tensor itself: a hit needs the same live object at the same
+    # version (a freed temporary's recycled storage can never match)
+    key = (W_dn.data_ptr(), tuple(W_dn.shape), tuple(W_dn.stride()))
+    hit = _W3_CACHE.get(key)
+    if hit is not None and hit[0] is W_dn and hit[1] == W_dn._version:
+        return hit[2]
+    Wt = _f32(W_dn).t()
+    hi = Wt.to(torch.bfloat16)
+    lo = (Wt - hi.float()).to(torch.bfloat16)
+    W3 = torch.cat([hi, hi, lo], dim=1).contiguous()
+    if len(_W3_CACHE) > 256:
+        _W3_CACHE.clear()
+    _W3_CACHE[key] = (W_dn, W_dn._version, W3)
+    return W3
+
+
 def _gemm3(A, W_dn, bias, N_logit=0, out=None, out_L=None):
     """fp32 A [M, K] @ W_dn [K, N] + bias, fp32-accurate; returns fp32 [M, N - N_logit]
     (and the last N_logit columns separately), written into `out` / `out_L` when given
@@ -426,10 +448,7 @@ def _gemm3(A, W_dn, bias, N_logit=0, out=None, out_L=None):
     if M % 128 or K % 16:
         raise ConfigError("fp32 mode needs rows % 128 == 0 and K % 16 == 0")
     A3 = _split3(A)
-    Wt = _f32(W_dn).t()
-    hi = Wt.to(torch.bfloat16)
-    lo = (Wt - hi.float()).to(torch.bfloat16)
-    W3 = torch.cat([hi, hi, lo], dim=1).contiguous()                 # [N, 3K]
+    W3 = _split_w3(W_dn)                                             # [N, 3K]
     Nv = N - N_logit
     V = out if out is not None else torch.empty(M, Nv, device="cuda", dtype=torch.float32)
     L = out_L if out_L is not None else torch.empty(M, max(N_logit, 1), device="cuda",
