@@ -126,3 +126,42 @@ def test_lean_rowdot(group):
         torch.cuda.synchronize()
         assert torch.allclose(lean, pairs, rtol=1e-6, atol=1e-3)
     assert rel_err(lean.double().cpu().numpy(), want.cpu().numpy()) < 1e-4
+
+
+def test_split3_matches_torch():
+    """dchag_split3_bf16: [hi | lo | hi] with hi = bf16(x), lo = bf16(x - hi), strided rows."""
+    L = _lib()
+    g = torch.Generator().manual_seed(3)
+    x = torch.randn(300, 200, generator=g).cuda()[:, :192]            # row stride 200
+    out = torch.empty(300, 3 * 192, device="cuda", dtype=torch.bfloat16)
+    L.call("dchag_split3_bf16", L.ptr(x), 300, 192, x.stride(0), L.ptr(out), 3 * 192,
+           L.stream_handle())
+    torch.cuda.synchronize()
+    hi = x.to(torch.bfloat16)
+    lo = (x - hi.float()).to(torch.bfloat16)
+    assert torch.equal(out, torch.cat([hi, lo, hi], dim=1))
+
+
+def test_p_normalize_matches_torch():
+    """dchag_l0_p_normalize: p = e * pinv over the K_p0 node blocks [hg][g][R][NH]."""
+    L = _lib()
+    R, H, NH = 256, 8, 4
+    gs = [3, 5]
+    g = torch.Generator().manual_seed(4)
+    e = [torch.rand(H // NH, c, R, NH, generator=g) for c in gs]
+    pinv = torch.rand(len(gs), R, H, generator=g)
+    flat = torch.cat([t.reshape(-1) for t in e]).to(torch.bfloat16).cuda()
+    poff = torch.tensor([0, gs[0] * R * H], dtype=torch.int64, device="cuda")
+    node_g = torch.tensor(gs, dtype=torch.int32, device="cuda")
+    pin = pinv.cuda()
+    out = torch.empty_like(flat)
+    L.call("dchag_l0_p_normalize", L.ptr(flat), L.ptr(pin), L.ptr(out), L.ptr(poff),
+           L.ptr(node_g), len(gs), max(gs), R, H, NH, L.stream_handle())
+    torch.cuda.synchronize()
+    at = 0
+    for n, c in enumerate(gs):
+        blk = flat[at:at + c * R * H].float().view(H // NH, c, R, NH)
+        sc = pin[n].view(R, H // NH, NH).permute(1, 0, 2).unsqueeze(1)     # [hg, 1, R, NH]
+        want = (blk * sc).to(torch.bfloat16)
+        assert torch.equal(out[at:at + c * R * H].view(H // NH, c, R, NH), want)
+        at += c * R * H
