@@ -583,3 +583,31 @@ def test_kernels_are_repeatable_bitwise():
     assert torch.equal(runs[0][0], runs[1][0])
     for k in runs[0][1]:
         assert torch.equal(runs[0][1][k], runs[1][1][k]), k
+
+
+def test_forward_cuda_graph_replay():
+    """The single-GPU forward captured as one CUDA graph (bench.py's launch mode for
+    launch-bound steps) replays bit-identically to the eager forward, and re-reads its static
+    input buffer on every replay."""
+    from paper_2506_21411_b200 import DchagFrontEnd
+    fe = DchagFrontEnd(16, 64, 64, 4, 128, 2, max_group=4)
+    fe.init_weights(seed=5, all_ranks=False)
+    gen = torch.Generator(device="cuda").manual_seed(2)
+    img = torch.randn(2, 16, 64, 64, device="cuda", generator=gen).to(torch.bfloat16)
+    for _ in range(2):
+        fe(img)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(graph, stream=side):
+            out_g = fe(img)
+    torch.cuda.current_stream().wait_stream(side)
+    img2 = torch.randn(2, 16, 64, 64, device="cuda", generator=gen).to(torch.bfloat16)
+    img.copy_(img2)
+    graph.replay()
+    torch.cuda.synchronize()
+    want = fe(img2)
+    torch.cuda.synchronize()
+    assert torch.equal(out_g, want)
