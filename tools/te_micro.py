@@ -22,13 +22,27 @@ def te():
               _lib.ptr(G), _lib.ptr(dlb), _lib.ptr(TE), Dp, g * PP, st)
 
 
-for _ in range(3):
-    te()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-torch.cuda.synchronize()
-e0.record()
-for _ in range(20):
-    te()
-e1.record()
-torch.cuda.synchronize()
-print(f"l0_tgrad_te {e0.elapsed_time(e1) / 20:.3f} ms per node")
+def timed():
+    for _ in range(3):
+        te()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(20):
+        te()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 20
+
+
+print(f"l0_tgrad_te {timed():.3f} ms per node")
+if len(sys.argv) > 1:  # DCHAG_TE_DEBUG probes: 1 no scaling, 2 no MMA
+    ref = None
+    for dbg in sys.argv[1:]:
+        os.environ["DCHAG_TE_DEBUG"] = dbg
+        ms = timed()
+        out = TE.float().clone()
+        err = "" if ref is None else f"  max |diff| vs first {(out - ref).abs().max().item():.3g}"
+        ref = out if ref is None else ref
+        print(f"debug={dbg}: {ms:.3f} ms{err}")
+    os.environ["DCHAG_TE_DEBUG"] = "0"
