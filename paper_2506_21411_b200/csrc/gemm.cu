@@ -1348,6 +1348,233 @@ __global__ void __launch_bounds__(192, 2)
   }
 }
 
+// K_te with two channels per CTA. K_te's floor is the L2 -> SM fan-out: the one-channel
+// form moves each G tile into shared memory once per channel. Here a stage holds one G tile
+// and both channels' patch tiles; the builders scale G into two A operands, p_c0 G into a
+// small ring of copies (A0, two slots) and p_c1 G in place. G then crosses the fabric once per
+// channel pair, and a unit of work moves 16 KB instead of 24. The E columns (A = dl_c,
+// unscaled) take one channel per CTA: two CTA columns past the D / 128 G columns.
+// Ring depth: 4, 5 and 6 stages ran alike (87-88 us per TR node; load-only 76 us at every
+// depth), one copy slot instead of two cost 20 us (the builders then wait for the MMAs).
+constexpr int TE2_STAGES = 4;
+constexpr int TE2_A0 = 2;                                 // copy slots for channel c0
+constexpr int TE2_STAGE = TGC_A_BYTES + 2 * TGC_B_BYTES;  // G | B0 | B1 = 32 KB
+constexpr int TE2_SMEM = TE2_STAGES * TE2_STAGE + TE2_A0 * TGC_A_BYTES + TGC_B_BYTES + 1024 + 256;
+constexpr int TE2_BUILDERS = 8;
+
+__global__ void __launch_bounds__(64 + 32 * TE2_BUILDERS, 1)
+    l0_tgrad_te2_kernel(const __grid_constant__ CUtensorMap tmG,
+                        const __grid_constant__ CUtensorMap tmP,
+                        const __grid_constant__ CUtensorMap tmDL, L0TgradArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* a0 = smem + TE2_STAGES * TE2_STAGE;     // [TE2_A0] scaled copies for channel c0
+  uint8_t* ones = a0 + TE2_A0 * TGC_A_BYTES;       // constant atom (column 0 = 1)
+  uint64_t* full = reinterpret_cast<uint64_t*>(ones + TGC_B_BYTES);
+  uint64_t* scaled = full + TE2_STAGES;
+  uint64_t* empty = scaled + TE2_STAGES;
+  uint64_t* done = empty + TE2_STAGES;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = warp_id(), lane = lane_id();
+  const int c0 = blockIdx.y * 2, d0 = blockIdx.x * 128;
+  const bool eblk = d0 >= a.D;
+  const int ech = eblk ? (int)blockIdx.x - a.D / 128 : 0;  // E column: its channel c0 + ech
+  const int nst = a.R / 64;
+  const int nit = nst;
+  const int dh = a.D / a.H;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmG);
+    tma_prefetch(&tmP);
+    tma_prefetch(&tmDL);
+    for (int s = 0; s < TE2_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&scaled[s], TE2_BUILDERS);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  for (int i = threadIdx.x; i < TGC_B_BYTES / 16; i += blockDim.x) {
+    const int r = i >> 3, ch = i & 7;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (ch == (r & 7)) v.x = 0x3F80u;
+    *reinterpret_cast<uint4*>(ones + i * 16) = v;
+  }
+  fence_async_smem();
+  if (warp == 1) tmem_alloc(tslot, 256);           // two accumulators, columns 0 and 128
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int i = 0; i < nit; ++i) {
+        const int s = i % TE2_STAGES;
+        mbar_wait(&empty[s], ((i / TE2_STAGES) & 1) ^ 1);
+        uint8_t* sa = smem + s * TE2_STAGE;
+        if (eblk) {
+          const int r0 = i * 64, b = r0 / a.S, s0 = r0 - b * a.S;
+          mbar_expect_tx(&full[s], TGC_A_BYTES + TGC_B_BYTES);
+          tma_load_3d(sa, &tmDL, &full[s], r0, 0, c0 + ech);     // [128 h][64 r], K-major
+          tma_load_3d(sa + TGC_A_BYTES, &tmP, &full[s], 0, s0, b * a.cnt + a.c0 + c0 + ech);
+        } else {
+          const int r0 = i * 64, b = r0 / a.S, s0 = r0 - b * a.S;
+          mbar_expect_tx(&full[s], TE2_STAGE);
+          tma_load_2d(sa, &tmG, &full[s], d0, r0);
+          tma_load_2d(sa + TGC_A_BYTES / 2, &tmG, &full[s], d0 + 64, r0);
+          tma_load_3d(sa + TGC_A_BYTES, &tmP, &full[s], 0, s0, b * a.cnt + a.c0 + c0);
+          tma_load_3d(sa + TGC_A_BYTES + TGC_B_BYTES, &tmP, &full[s], 0, s0,
+                      b * a.cnt + a.c0 + c0 + 1);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_bf16_f32(128, 80) | (eblk ? 0u : (1u << 15)) | (1u << 16);
+    for (int i = 0; i < nit; ++i) {
+      const int s = i % TE2_STAGES;
+      mbar_wait(&scaled[s], (i / TE2_STAGES) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sg = smem_u32(smem + s * TE2_STAGE);
+        if (eblk) {
+          const uint32_t sb = sg + TGC_A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            if (!(a.debug & 2))
+              mma_ss(tmem + ech * 128, smem_desc(sg + kk * 32, 16, 1024, 2u),
+                     smem_desc(sb + kk * 2048, smem_u32(ones) - sb, 1024, 2u), idesc,
+                     (i | kk) != 0);
+        } else {
+#pragma unroll
+          for (int ch = 0; ch < 2; ++ch) {
+            const uint32_t sa = ch ? sg : smem_u32(a0 + (i % TE2_A0) * TGC_A_BYTES);
+            const uint32_t sb = sg + TGC_A_BYTES + ch * TGC_B_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              if (!(a.debug & 2))
+                mma_ss(tmem + ch * 128, smem_desc(sa + kk * 2048, TGC_A_BYTES / 2, 1024, 2u),
+                       smem_desc(sb + kk * 2048, smem_u32(ones) - sb, 1024, 2u), idesc,
+                       (i | kk) != 0);
+          }
+        }
+        mma_commit(&empty[s]);
+        if (i == nit - 1) mma_commit(done);
+      }
+      __syncwarp();
+    }
+  } else {
+    // builders: thread t scales chunks [4 cq, 4 cq + 4) of row r = t % 64 of half mh
+    const int t = threadIdx.x - 64;
+    const int row = t & 63, mh = (t >> 6) & 1, cq = t >> 7;
+    const int head = (d0 + mh * 64) / dh;
+    const int hA = d0 / dh;
+    const int hg = hA / (a.NH > 0 ? a.NH : 1);
+    const int hn = (hA - hg * a.NH) & ~1;
+    const int sel = head & 1;
+    const float mix0 = (a.mix && !eblk) ? __ldg(a.mix + c0) : 0.f;
+    const float mix1 = (a.mix && !eblk) ? __ldg(a.mix + c0 + 1) : 0.f;
+    auto pword = [&](int ch, int i) -> uint32_t {
+      if (a.mix) return 0u;
+      return __ldg(reinterpret_cast<const uint32_t*>(
+          a.p + ((size_t)(hg * a.g + c0 + ch) * a.R + i * 64 + row) * a.NH + hn));
+    };
+    auto pconv = [&](uint32_t w, float mixc) -> float {
+      if (a.mix) return mixc;
+      return sel ? bf16hi(w) : bf16lo(w);
+    };
+    // p of the next four stages in flight (raw words, one register per queue slot; the loop
+    // is unrolled by the queue depth so no register copy waits for a load)
+    constexpr int PQ = 4;
+    uint32_t pq0[PQ], pq1[PQ];
+#pragma unroll
+    for (int j = 0; j < PQ; ++j) {
+      pq0[j] = (!eblk && j < nst) ? pword(0, j) : 0u;
+      pq1[j] = (!eblk && j < nst) ? pword(1, j) : 0u;
+    }
+    for (int i0 = 0; i0 < nit; i0 += PQ)
+#pragma unroll
+    for (int j = 0; j < PQ; ++j) {
+      const int i = i0 + j;
+      if (i >= nit) break;
+      const int s = i % TE2_STAGES;
+      const uint32_t w0 = pq0[j], w1 = pq1[j];
+      if (!eblk && i + PQ < nst) {
+        pq0[j] = pword(0, i + PQ);
+        pq1[j] = pword(1, i + PQ);
+      }
+      mbar_wait(&full[s], (i / TE2_STAGES) & 1);
+      if (!eblk && !(a.debug & 1)) {
+        // the copy slot i % TE2_A0 is free once the MMAs of stage i - TE2_A0 have completed
+        if (i >= TE2_A0)
+          mbar_wait(&empty[(i - TE2_A0) % TE2_STAGES], ((i - TE2_A0) / TE2_STAGES) & 1);
+        const float p0 = pconv(w0, mix0), p1 = pconv(w1, mix1);
+        const uint32_t off = mh * (TGC_A_BYTES / 2) + (row >> 3) * 1024 + (row & 7) * 128;
+        const uint32_t rg = smem_u32(smem + s * TE2_STAGE) + off;
+        const uint32_t rc = smem_u32(a0 + (i % TE2_A0) * TGC_A_BYTES) + off;
+        uint32_t v[4][4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t ad = rg + (((4 * cq + k + row) & 7) << 4);
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(v[k][0]), "=r"(v[k][1]), "=r"(v[k][2]), "=r"(v[k][3])
+                       : "r"(ad));
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t o = ((4 * cq + k + row) & 7) << 4;
+          uint32_t x0[4], x1[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float lo = bf16lo(v[k][e]), hi = bf16hi(v[k][e]);
+            x0[e] = pack_bf16(lo * p0, hi * p0);
+            x1[e] = pack_bf16(lo * p1, hi * p1);
+          }
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rc + o), "r"(x0[0]),
+                       "r"(x0[1]), "r"(x0[2]), "r"(x0[3])
+                       : "memory");
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rg + o), "r"(x1[0]),
+                       "r"(x1[1]), "r"(x1[2]), "r"(x1[3])
+                       : "memory");
+        }
+        fence_async_smem();  // generic-proxy writes -> visible to the tensor core
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&scaled[s]);
+    }
+    // epilogue: warps 2..5 drain channel c0's accumulator, warps 6..9 channel c0 + 1's
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int q = warp & 3, ch = (warp - 2) >> 2, c = c0 + ch;
+    const uint32_t tacc = tmem + ch * 128 + ((uint32_t)(q * 32) << 16);
+    const int m = q * 32 + lane;
+    const long long col = eblk ? (long long)a.D + m : (long long)d0 + m;
+    __nv_bfloat16* te = a.TE + col;
+    const bool live = !eblk || (m < a.H && ch == ech);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t r[32];
+      tmem_ld32(tacc + half * 32, r);
+      tmem_ld_wait();
+      if (live) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          te[(size_t)(c * a.PP + half * 32 + j) * a.te_ld] = __float2bfloat16(__uint_as_float(r[j]));
+      }
+    }
+    uint32_t r16[16];
+    tmem_ld16(tacc + 64, r16);
+    tmem_ld_wait();
+    if (live) te[(size_t)(a.ones0 + c) * a.te_ld] = __float2bfloat16(__uint_as_float(r16[0]));
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
 cudaError_t launch_l0_tgrad_tc(const CUtensorMap& tG, const CUtensorMap& tP,
                                const L0TgradArgs& a, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(l0_tgrad_tc_kernel<false>,
@@ -1359,6 +1586,16 @@ cudaError_t launch_l0_tgrad_tc(const CUtensorMap& tG, const CUtensorMap& tP,
 
 cudaError_t launch_l0_tgrad_te(const CUtensorMap& tG, const CUtensorMap& tP,
                                const CUtensorMap& tDL, const L0TgradArgs& a, cudaStream_t st) {
+  // two channels per CTA when the node's channel count is even (DCHAG_TE_CH=1: one)
+  const char* ch1 = getenv("DCHAG_TE_CH");
+  if (a.g % 2 == 0 && !(ch1 && atoi(ch1) == 1)) {
+    cudaError_t e = cudaFuncSetAttribute(l0_tgrad_te2_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, TE2_SMEM);
+    if (e != cudaSuccess) return e;
+    l0_tgrad_te2_kernel<<<dim3(a.D / 128 + (a.has_dl ? 2 : 0), a.g / 2), 64 + 32 * TE2_BUILDERS,
+                          TE2_SMEM, st>>>(tG, tP, tDL, a);
+    return cudaGetLastError();
+  }
   cudaError_t e = cudaFuncSetAttribute(l0_tgrad_tc_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, TGC_SMEM_TE);
   if (e != cudaSuccess) return e;

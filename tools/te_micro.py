@@ -46,3 +46,16 @@ if len(sys.argv) > 1:  # DCHAG_TE_DEBUG probes: 1 no scaling, 2 no MMA
         ref = out if ref is None else ref
         print(f"debug={dbg}: {ms:.3f} ms{err}")
     os.environ["DCHAG_TE_DEBUG"] = "0"
+
+# one- vs two-channel CTAs (DCHAG_TE_CH=1 selects the one-channel kernel): equal bits, times
+if os.environ.get("TE_AB"):
+    outs = {}
+    for ch in ("1", "2"):
+        os.environ["DCHAG_TE_CH"] = ch
+        TE.zero_()
+        ms = timed()
+        outs[ch] = TE.clone()
+        print(f"channels per CTA {ch}: {ms:.4f} ms")
+    os.environ.pop("DCHAG_TE_CH")
+    print("bit-equal:", torch.equal(outs["1"], outs["2"]),
+          "max |diff|", (outs["1"].float() - outs["2"].float()).abs().max().item())
