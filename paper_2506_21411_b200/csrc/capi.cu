@@ -526,6 +526,9 @@ int dchag_l0_logits(const void* img, long long img_sb, long long img_sc, int B, 
     return fail(DCHAG_ERR_SHAPE, "l0_logits: bad shape");
   L0LogitArgs a;
   memset(&a, 0, sizeof(a));
+  if (const char* tr = getenv("DCHAG_P0_TRACE_PTR"))
+    a.trace = reinterpret_cast<long long*>(strtoull(tr, nullptr, 0));
+  if (const char* is = getenv("DCHAG_P0_ISSUE")) a.issue_serial = atoi(is) == 1;
   a.img = reinterpret_cast<const __nv_bfloat16*>(img);
   a.img_sb = img_sb; a.img_sc = img_sc;
   a.B = B; a.S = (Himg / P) * (W / P); a.W = W; a.P = P; a.wp = W / P; a.H = H; a.HP = HP;

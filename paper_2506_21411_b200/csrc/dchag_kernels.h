@@ -95,6 +95,8 @@ struct L0LogitArgs {
   __nv_bfloat16* p;           // p[poff[n] + ((hg*g + c)*R + r)*NH + h%NH], hg = h/NH,
                               // NH = 4 if H % 4 == 0 else 2 (head group of one K_l0 CTA);
                               // a 128-row tile's slice of (hg, c) is one contiguous 1 KB run
+  long long* trace;           // timing probe (DCHAG_P0_TRACE_PTR): CTAs 0..3, 64 items
+  int issue_serial;           // A/B probe (DCHAG_P0_ISSUE=1): one thread issues every copy
 };
 cudaError_t launch_l0_logits(const L0LogitArgs& a, int num_sms, cudaStream_t st);
 

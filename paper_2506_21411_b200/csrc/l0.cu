@@ -22,6 +22,16 @@
 namespace dchag {
 
 // =====================================================================  K_p0
+DEV long long globaltimer_ns() {  // comparable across the two SMs of a pair (clock64 is not)
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define P0_TRACE(ev, k)                                                                     \
+  do {                                                                                      \
+    if (a.trace && blockIdx.x < 4 && threadIdx.x == 0 && (k) < 64)                          \
+      a.trace[(blockIdx.x * 8 + (ev)) * 64 + (k)] = globaltimer_ns();                      \
+  } while (0)
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4],
                                                uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -41,7 +51,8 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
 // in shared memory. Pass 1: max over the node's channels (merged across channel phases
 // through shared memory); pass 2: e = 2^(t - max), sums; pass 3 (no pinv): p = e / sum.
 template <int NT, int P, int MT>  // NT = HP / 8 head tiles, MT = RB / 16 row tiles
-__global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items_per_cta, int nbuf) {
+__global__ void __launch_bounds__(256, NT <= 2 ? 2 : 1)  // two CTAs per SM need <= 128 registers
+    l0_logits_kernel(L0LogitArgs a, int items_per_cta, int nbuf) {
   constexpr int RB = MT * 16, CS = 8 / MT;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t landed[2];
@@ -66,24 +77,49 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
   float* stat = reinterpret_cast<float*>(smem_raw + (sU - smem_u32(smem_raw)) +
                                          (size_t)a.gmax * a.HP * 4);  // [CS][MT][NT][4][32]
   const int lwp = __ffs(a.wp) - 1;   // W / P divides 128: a power of two
-  auto issue = [&](int it, int buf) {  // thread 0: bulk copies of item it into buffer buf
+  // warp 0: bulk copies of item it into buffer buf, one channel per lane (one thread issuing
+  // all g copies took ~70 ns per copy, ~1.1 us per 16-channel item, on the critical path)
+  // (c0, g: the item's node, loaded by the caller ahead of time -- a dependent load here
+  // held the issuing warp for its latency)
+  auto issue = [&](int it, int buf, int c0, int g) {
     const int n = it / bpn, r0 = (it - n * bpn) * RB;
-    const int c0 = __ldg(a.node_c0 + n), g = __ldg(a.node_g + n);
     const int b = r0 / a.S, s0 = r0 - b * a.S;
     const __nv_bfloat16* src0 = a.img + b * a.img_sb + (long long)(s0 >> lwp) * P * a.W;
-    mbar_expect_tx(&landed[buf], chunk * g);
-    for (int c = 0; c < g; ++c)
+    const int ln = threadIdx.x & 31;
+    if (ln == 0) mbar_expect_tx(&landed[buf], chunk * g);
+    __syncwarp();
+    const int nl = a.issue_serial ? 1 : 32;
+    if (ln < nl)
+    for (int c = ln; c < g; c += nl)
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
           ::"r"(sbase + buf * ibuf + c * chunk), "l"(src0 + (long long)(c0 + c) * a.img_sc),
           "r"(chunk), "r"(smem_u32(&landed[buf]))
           : "memory");
   };
+  // all 8 warps: lane 0 of warp w issues the copies of channels w, w + 8, ... (a warp that
+  // issues all of them is held up ~1 us and the item's barriers wait for it)
+  auto issue_all = [&](int it, int buf, int c0, int g) {
+    const int n = it / bpn, r0 = (it - n * bpn) * RB;
+    const int b = r0 / a.S, s0 = r0 - b * a.S;
+    const __nv_bfloat16* src0 = a.img + b * a.img_sb + (long long)(s0 >> lwp) * P * a.W;
+    if (threadIdx.x == 0) mbar_expect_tx(&landed[buf], chunk * g);
+    if ((threadIdx.x & 31) == 0)
+      for (int c = threadIdx.x >> 5; c < g; c += 8)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(sbase + buf * ibuf + c * chunk), "l"(src0 + (long long)(c0 + c) * a.img_sc),
+            "r"(chunk), "r"(smem_u32(&landed[buf]))
+            : "memory");
+  };
   if (threadIdx.x == 0) {
     mbar_init(&landed[0], 1);
     mbar_init(&landed[1], 1);
     fence_barrier_init();
-    issue(it0, 0);
+  }
+  if (threadIdx.x < 32) {
+    __syncwarp();
+    issue(it0, 0, __ldg(a.node_c0 + it0 / bpn), __ldg(a.node_g + it0 / bpn));
   }
   auto wswz = [&](int row, int ch) -> uint32_t {  // byte offset of chunk ch of weight row
     const int f = CPR >= 8 ? (row & 7) : ((row / (8 / CPR)) & (CPR - 1));
@@ -130,8 +166,13 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
     const int n = it / bpn, r0 = (it - n * bpn) * RB;
     const int c0 = __ldg(a.node_c0 + n), g = __ldg(a.node_g + n);
     const long long poff = __ldg(a.node_poff + n);
+    // the next item's node (usually this one): its copies are issued mid-item
+    const int nn = (it + 1) / bpn;
+    const int c0n = nn == n ? c0 : __ldg(a.node_c0 + min(nn, a.n_nodes - 1));
+    const int gn = nn == n ? g : __ldg(a.node_g + min(nn, a.n_nodes - 1));
     // item k-1 is finished by every warp (end-of-item barrier): its buffer takes item k+1
-    if (nbuf == 2 && threadIdx.x == 0 && it + 1 < it1) issue(it + 1, buf ^ 1);
+    P0_TRACE(0, k);
+    if (nbuf == 2 && threadIdx.x < 32 && it + 1 < it1) issue(it + 1, buf ^ 1, c0n, gn);
     if (n != cur_node) {  // stage this node's logit weights and bias rows
       const uint4* src = reinterpret_cast<const uint4*>(a.WUt + (long long)c0 * a.HP * PP);
       const int nchunks = g * a.HP * CPR;
@@ -158,6 +199,7 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
     }
     mbar_wait(&landed[buf], ph[buf]);
     ph[buf] ^= 1;
+    P0_TRACE(1, k);
     const uint32_t ibase = sbase + buf * ibuf;
     auto logits = [&](int c, float (&L)[NT][4]) {
       const uint32_t ab = ibase + c * chunk;
@@ -234,7 +276,12 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
       for (int e = 0; e < 4; ++e) stat[sidx(cph, nt, e)] = mx[nt][e];
     __syncthreads();
     const bool early = keep && nbuf == 1 && it + 1 < it1;
-    if (early && threadIdx.x == 0) issue(it + 1, 0);  // every warp is done with the image
+    P0_TRACE(2, k);
+    if (early) {  // every warp is done with the image
+      if (a.issue_serial) { if (threadIdx.x < 32) issue(it + 1, 0, c0n, gn); }
+      else issue_all(it + 1, 0, c0n, gn);
+    }
+    P0_TRACE(5, k);
     float nmx[NT][4];  // -max * log2(e)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
@@ -246,6 +293,7 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
         nmx[nt][e] = -m * LOG2E;
       }
     __syncthreads();  // stat reused for the sums
+    P0_TRACE(6, k);
     // p / e store offsets (elements, relative to the node's p block) for channel 0
     int poff_e[NT][2];
 #pragma unroll
@@ -295,6 +343,7 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) stat[sidx(cph, nt, e)] = sm_[nt][e];
+    P0_TRACE(7, k);
     __syncthreads();
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
@@ -348,8 +397,10 @@ __global__ void __launch_bounds__(256) l0_logits_kernel(L0LogitArgs a, int items
         }
       }
     }
+    P0_TRACE(3, k);
     __syncthreads();  // item done: its image buffer and the stat area may be reused
-    if (nbuf == 1 && !early && threadIdx.x == 0 && it + 1 < it1) issue(it + 1, 0);
+    P0_TRACE(4, k);
+    if (nbuf == 1 && !early && threadIdx.x < 32 && it + 1 < it1) issue(it + 1, 0, c0n, gn);
   }
 }
 
@@ -405,6 +456,9 @@ cudaError_t launch_l0_logits(const L0LogitArgs& a, int num_sms, cudaStream_t st)
   if (e != cudaSuccess) return e;
   const int total = a.n_nodes * (R / RB);
   int per_sm = (int)((227 * 1024) / smem);  // co-resident CTAs (smem-limited), at most 4
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k) == cudaSuccess && fa.numRegs > 0)
+    per_sm = min(per_sm, 65536 / (fa.numRegs * 256));  // and register-limited
   if (per_sm > 4) per_sm = 4;
   if (per_sm < 1) per_sm = 1;
   if (const char* f = getenv("DCHAG_P0_PERSM")) per_sm = atoi(f) > 0 ? atoi(f) : per_sm;
@@ -432,11 +486,6 @@ constexpr uint32_t L0_SLOT_COLS = 4 * 32;          // A slot: 64 bf16 K per head
       a.trace[((ev) + 8 * blockIdx.x) * 256 + (idx)] = globaltimer_ns();                    \
   } while (0)
 
-DEV long long globaltimer_ns() {  // comparable across the two SMs of a pair (clock64 is not)
-  long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 DEV void tmem_alloc_pair(uint32_t* slot, uint32_t cols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
