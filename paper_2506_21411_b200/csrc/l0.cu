@@ -27,15 +27,11 @@ DEV long long globaltimer_ns() {  // comparable across the two SMs of a pair (cl
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#ifdef DCHAG_P0_TRACE  // per-item timeline probe (tools/p0_trace.py; build_variant.sh -DDCHAG_P0_TRACE)
 #define P0_TRACE(ev, k)                                                                     \
   do {                                                                                      \
     if (a.trace && blockIdx.x < 4 && threadIdx.x == 0 && (k) < 64)                          \
       a.trace[(blockIdx.x * 8 + (ev)) * 64 + (k)] = globaltimer_ns();                      \
   } while (0)
-#else
-#define P0_TRACE(ev, k) do { } while (0)
-#endif
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4],
                                                uint32_t b0, uint32_t b1) {
   asm volatile(

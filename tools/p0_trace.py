@@ -1,7 +1,5 @@
 """Per-item timeline of K_p0 (l0_logits_kernel) for CTAs 0..3 on the H1 forward (globaltimer,
-DCHAG_P0_TRACE_PTR; a library built with -DDCHAG_P0_TRACE, e.g.
-  bash tools/build_variant.sh paper_2506_21411_b200/libdchag_p0trace.so -DDCHAG_P0_TRACE
-  DCHAG_LIB=paper_2506_21411_b200/libdchag_p0trace.so python tools/p0_trace.py): 0 item top, 1 image landed, 2 max pass done (next item's copies issued
+DCHAG_P0_TRACE_PTR): 0 item top, 1 image landed, 2 max pass done (next item's copies issued
 when single-buffered), 3 thread 0 done with the exp pass, 4 item end (after the barrier); 5 copies issued, 6 past the max-stat barrier, 7 exp pass done."""
 import os
 import statistics
