@@ -569,6 +569,29 @@ __global__ void __launch_bounds__(256) child_softmax_kernel(float* __restrict__ 
   const int f = __ldg(first + j), g = __ldg(count + j);
   float* base = L + (size_t)f * R * H + rh;
   const size_t st = (size_t)R * H;
+  if (g <= 16) {
+    // up to 16 children: every logit loaded once, all loads in flight together, one store
+    // each (the loop below reads each value three times)
+    float v[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) v[c] = c < g ? base[c * st] : -INFINITY;
+    float m = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) m = fmaxf(m, v[c]);
+    float sum = 0.f;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      if (c < g) {
+        v[c] = __expf(v[c] - m);
+        sum += v[c];
+      }
+    }
+    const float inv = 1.f / sum;
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c < g) base[c * st] = v[c] * inv;
+    return;
+  }
   float m = -INFINITY;
   for (int c = 0; c < g; ++c) m = fmaxf(m, base[c * st]);
   float sum = 0.f;
